@@ -1,0 +1,315 @@
+#!/usr/bin/env python
+"""Benchmark of the Flash PD-SSM fwd+bwd scan on B200 (BASELINE.json metric:
+"PD-SSM fwd+bwd scan tokens/s at L=2048, d=1024; HBM GB/s vs peak; 1/2/4/8 GPU").
+
+A step = pdssm_scan_fwd (h_t + chunk_state) followed by pdssm_scan_bwd (db, dD, g)
+over one batch of the headline workload (config 2: B=16, L=2048, H=8, N=128,
+K=32, complex fp32, per-step D), inputs resident in HBM (>= 1.3 GB per step, larger
+than the 126 MB L2, so no flush is needed).  Multi-GPU: one process per GPU,
+batch x head sharding with no data-path collective -- every rank runs its own
+full batch (weak scaling); value = all ranks' tokens / max-over-ranks time.
+
+--impl reference times the float64 CPU oracle (oracle/, the only reference this
+paper-only tier has) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PD-SSM fwd+bwd scan tokens/s at L=2048,d=1024; HBM GB/s vs peak; 1/2/4/8 GPU"
+UNIT = "tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
+    ap.add_argument("--complex", type=int, default=2, choices=[1, 2])
+    ap.add_argument("--heads", type=int, default=8)
+    ap.add_argument("--state", type=int, default=128)
+    ap.add_argument("--tau", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--seed", type=int, default=2000)
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def algo_bytes_per_seq_step(N, c, p):
+    """fwd reads D, b, k*, writes h -> 3cNp + 1;
+    bwd reads dh, D, h_{t-1}, k*, writes db, dD, g -> 5cNp + 5."""
+    return 3 * c * N * p + 1, 5 * c * N * p + 5
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, idx):
+        self.idx = idx
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{idx}.csv")
+
+    def start(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_oracle_sample(L, N, K, c, seed, seqs=1):
+    """Oracle (O5 + O8, float64 NumPy) on `seqs` (b,h) sequences of the workload."""
+    import oracle as O
+    import synth
+    inp = synth.scan_inputs(1, seqs, L, N, K, c, seed=seed, dh=True)
+    Pm = O.gather_P(inp["dict_idx"], inp["kstar"])
+    Dz, bz, ez = (O.planes_to_complex(inp[k]) for k in ("diag", "bias", "dh"))
+    t0 = time.perf_counter()
+    h = O.scan_forward(Pm, Dz, bz)
+    O.scan_backward(Pm, Dz, h, ez)
+    return time.perf_counter() - t0
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    B, L, H, N, K, c = 16, 2048, a.heads, a.state, 32, a.complex
+    Lh = 512                                    # bounded sample: one (b,h) sequence, 512 steps
+    cpu_oracle_sample(64, N, K, c, a.seed)     # warm numpy
+    for _ in range(a.warmup):
+        pass
+    times = [cpu_oracle_sample(Lh, N, K, c, a.seed + i) for i in range(a.steps)]
+    t = float(np.sum(times))
+    tokens = a.steps * Lh / H                   # one head of Lh tokens = Lh/H token-equivalents
+    v = tokens / t
+    cores = 1
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": 1e3 * t / a.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "config2 fig1-shape scan fwd+bwd (oracle sample)", "batch": B, "seq_len": L,
+                       "heads": H, "state": N, "dict": K, "complex": c == 2},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"1 (b,h) sequence x {Lh} steps per step, N={N}, complex={c == 2}"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_2605_19150_b200 as P
+    import synth
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    B, L, H, N, K, c = 16, 2048, a.heads, a.state, 32, a.complex
+    bf16 = a.dtype == "bf16"
+    p = 2 if bf16 else 4
+    adt = torch.bfloat16 if bf16 else torch.float32
+    # global inputs are generated per rank-shard (batch x head sharding: rank r owns batch block r)
+    inp = synth.scan_inputs(B, H, L, N, K, c, seed=a.seed + 17 * rank, dh=True, bf16=bf16)
+    host = {k: torch.from_numpy(v) for k, v in inp.items()}
+    d = {k: v.to(dev) for k, v in host.items()}
+    d["dict_idx"] = d["dict_idx"].to(torch.int16)
+    for k in ("diag", "bias", "dh"):
+        d[k] = d[k].to(adt)
+    # outputs / workspaces preallocated once (calls are allocation-free)
+    f = P.scan_fwd(d["kstar"], d["dict_idx"], d["diag"], d["bias"], tau=a.tau)
+    dims = f["dims"]
+    fo = {"h": f["h"], "chunk_state": f["chunk_state"],
+          "ws": torch.empty(P.workspace_bytes(dims, P.OP_FWD), dtype=torch.uint8, device=dev)}
+    bo = {"ws": torch.empty(P.workspace_bytes(dims, P.OP_BWD), dtype=torch.uint8, device=dev),
+          "dbias": torch.empty_like(f["h"]), "ddiag": torch.empty_like(f["h"]),
+          "gsel": torch.empty((B, H, L), dtype=torch.float32, device=dev)}
+    stream = torch.cuda.current_stream()
+
+    def step_fwd():
+        return P.scan_fwd(d["kstar"], d["dict_idx"], d["diag"], d["bias"], tau=a.tau, out=fo)
+
+    def step_bwd(fr):
+        return P.scan_bwd(d["kstar"], d["dict_idx"], d["diag"], fr["h"], fr["chunk_state"], dims, dh=d["dh"],
+                          want_dh0=False, out=bo)
+
+    for _ in range(max(a.warmup, 3)):
+        step_bwd(step_fwd())
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, per-call CUDA events on the launching stream
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(a.steps)]
+    clk = Clocks(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk.start()
+    time.sleep(0.3)
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for i in range(a.steps):
+        ev[i][0].record(stream)
+        fr = step_fwd()
+        ev[i][1].record(stream)
+        step_bwd(fr)
+        ev[i][2].record(stream)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    if world > 1:
+        dist.barrier()
+    elapsed = t_start.elapsed_time(t_end) / 1e3
+    fwd_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
+    bwd_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
+    if world > 1:
+        tt = torch.tensor([elapsed], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        elapsed = float(tt.item())
+    tokens_per_rank = B * L
+    value = world * tokens_per_rank * a.steps / elapsed
+
+    fb, bb = algo_bytes_per_seq_step(N, c, p)
+    S = B * H
+    fwd_bytes = fb * S * L
+    bwd_bytes = bb * S * L
+    peak, peak_kind = peaks()
+    dominant = "scan_bwd" if bwd_ms >= fwd_ms else "scan_fwd"
+    dom_bytes, dom_ms = (bwd_bytes, bwd_ms) if dominant == "scan_bwd" else (fwd_bytes, fwd_ms)
+    achieved = dom_bytes / (dom_ms / 1e3) / 1e9
+    step_gbs = (fwd_bytes + bwd_bytes) / (elapsed / a.steps) / 1e9
+
+    # ---- end-to-end through the public API with pinned host buffers
+    e2e = None
+    if not a.no_e2e:
+        pin = {k: host[k].pin_memory() for k in ("kstar", "diag", "bias", "dh")}
+        if bf16:
+            pin = {k: (v.to(adt).pin_memory() if k in ("diag", "bias", "dh") else v) for k, v in pin.items()}
+        g_host = torch.empty((B, H, L), dtype=torch.float32).pin_memory()
+        h2d = sum(v.numel() * v.element_size() for v in pin.values())
+        d2h = g_host.numel() * 4
+        e_steps = max(3, min(a.steps, 10))
+
+        def e2e_step():
+            for k, v in pin.items():
+                d[k].copy_(v, non_blocking=True)
+            fr = step_fwd()
+            step_bwd(fr)
+            g_host.copy_(bo["gsel"], non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(e_steps):
+            e2e_step()
+        s1.record(stream)
+        torch.cuda.synchronize()
+        et = s0.elapsed_time(s1) / 1e3
+        if world > 1:
+            tt = torch.tensor([et], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            et = float(tt.item())
+        e2e = {"value": world * tokens_per_rank * e_steps / et, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h)}
+
+    # ---- CPU oracle baseline on a bounded sample (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        Lh = 512
+        cpu_oracle_sample(64, N, K, c, a.seed)
+        reps = 3
+        t = sum(cpu_oracle_sample(Lh, N, K, c, a.seed + i) for i in range(reps))
+        cpu = {"value": reps * Lh / H / t, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{reps} x one (b,h) sequence of {Lh} steps (N={N}, complex={c == 2}), fwd O5 + bwd O8, "
+                         "float64 NumPy, single thread; tokens = steps/H"}
+
+    launches_per_step = 7   # fwd: plan, A, B, C ; bwd: A', B', C'
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+                "ms_per_step": 1e3 * elapsed / a.steps, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": a.dtype, "data": "synthetic",
+                "config": {"workload": "config2: paper Fig.1 shape, fwd+bwd scan", "batch_per_gpu": B, "seq_len": L,
+                           "heads": H, "state": N, "d": H * N, "dict": K, "complex": c == 2, "diag": "per_step",
+                           "tau": int(f["tau"]), "parallelism": f"dp{world} (batch x head shards, no collective)",
+                           "l2": "inputs larger than L2 (>=1.3 GB per step), no flush"},
+                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                             "frac": achieved / peak, "traffic": None, "kernel": dominant,
+                             "peak_kind": peak_kind},
+                "step_hbm": {"achieved_gbs": step_gbs, "frac": step_gbs / peak, "fwd_ms": fwd_ms, "bwd_ms": bwd_ms,
+                             "algo_bytes_fwd": fwd_bytes, "algo_bytes_bwd": bwd_bytes},
+                "clocks": clocks, "e2e": e2e, "gpu_launches": launches_per_step * a.steps, "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,252 @@
+/*
+ * pdssm.h -- C ABI of the B200 (sm_100a) Flash PD-SSM hot path.
+ *
+ * Paper: "Flash PD-SSM" (arXiv 2605.19150), cited as PAPER.md:<line>.
+ *
+ * The library computes, per batch element b and head h, the input-dependent
+ * structured-sparse recurrence (Eq. 1, with A_t = P_t D_t,
+ * PAPER.md:926):
+ *
+ *     h_t = P_t D_t h_{t-1} + b_t,        y_t = Re(C_h h_t)
+ *
+ * where P_t = dict_idx[h][k*_t] is hard-selected (Eqs. 5-8)
+ * and A_t acts as a COLUMN-ONE-HOT scatter:  A_t[P_t[j], j] = D_t[j], i.e.
+ * (A_t v)[i] = sum_{j : P_t[j] = i} D_t[j] v[j]   (the
+ * gather form of PAPER.md:938 is the transpose -- DESIGN.md reading R1).
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - All tensor pointers are caller-owned DEVICE memory unless stated; the
+ *    library never allocates, never synchronises the host (except
+ *    pdssm_check_device), and enqueues all work on the given stream, so every
+ *    call is CUDA-graph capturable.  stream = NULL is the legacy default stream.
+ *  - Indices are 0-based.  Every argmax breaks ties toward the smallest index
+ *    and treats NaN as -inf (readings R6-R8).
+ *  - Complex tensors are split re/im planes: a "[c][N]" block holds c = 1 (real)
+ *    or c = 2 (re plane, then im plane) rows of N values.
+ *  - Floating tensors marked "act" are in dims->dtype (PDSSM_F32 = float32,
+ *    PDSSM_BF16 = bfloat16 bits); all accumulation is fp32.  Tensors marked
+ *    f32 are always float32.
+ *  - Validation is synchronous and happens before any CUDA call; a violation
+ *    returns the status code and records a message (pdssm_last_error) without
+ *    touching the device.
+ *  - Kernels never trap.  Out-of-range k* / dict_idx values are a caller
+ *    precondition: they are clamped into range (memory safety) and, when
+ *    PDSSM_CHECK_FINITE is set, reported (with NaN/Inf inputs) through a device
+ *    error word read by pdssm_check_device.
+ *  - Outputs are fully overwritten.  Inputs are read-only.
+ *  - Integer outputs (dict_idx, k*, P, maps) are bit-exact and run-to-run
+ *    identical; float outputs are run-to-run bitwise identical (the scatter
+ *    sums colliding sources in ascending source order; no float atomics).
+ *  - Pointer alignment: every tensor pointer must be aligned to its element
+ *    size; 16-byte alignment enables the vectorised/bulk-copy paths
+ *    (otherwise PDSSM_ERR_ALIGN).
+ */
+#ifndef PDSSM_H
+#define PDSSM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* pdssm_stream_t; /* == cudaStream_t */
+
+typedef enum {
+    PDSSM_OK = 0,
+    PDSSM_ERR_NULL = 1,        /* a required pointer is NULL                        */
+    PDSSM_ERR_SHAPE = 2,       /* a dimension is out of the supported range         */
+    PDSSM_ERR_RANGE = 3,       /* device reported an out-of-range index (CHECK_FINITE) */
+    PDSSM_ERR_ALIGN = 4,       /* a pointer is misaligned                           */
+    PDSSM_ERR_DTYPE = 5,       /* unknown dtype / diag mode / flag combination      */
+    PDSSM_ERR_WORKSPACE = 6,   /* workspace or chunk_state too small / NULL         */
+    PDSSM_ERR_NONFINITE = 7,   /* device reported NaN/Inf input (CHECK_FINITE)      */
+    PDSSM_ERR_CUDA = 8,        /* a CUDA runtime call failed (message in last_error) */
+    PDSSM_ERR_UNSUPPORTED = 9  /* valid request this build does not implement       */
+} pdssm_status;
+
+typedef enum { PDSSM_F32 = 0, PDSSM_BF16 = 1 } pdssm_dtype;
+
+/* Origin of the transition diagonal D_t (reading R3):
+ *  PER_STEP: D_t given per step, diag = act [B][H][L][c][N]
+ *  PER_DICT: D_t = D_k[h][k*_t], diag = f32 [H][K][c][N] ("dictionary {P_k, D_k}") */
+typedef enum { PDSSM_DIAG_PER_STEP = 0, PDSSM_DIAG_PER_DICT = 1 } pdssm_diag_mode;
+
+enum {
+    PDSSM_CHECK_FINITE = 1u,   /* scan inputs for NaN/Inf and out-of-range indices   */
+    PDSSM_DETERMINISTIC = 2u,  /* accepted; the library is always deterministic      */
+    PDSSM_EXPORT_MAPS = 8u     /* pdssm_scan_fwd also writes maps_opt                 */
+};
+
+enum { PDSSM_OP_SELECT = 0, PDSSM_OP_FWD = 1, PDSSM_OP_BWD = 2, PDSSM_OP_SEGMENT = 3 };
+
+/* Problem statement (north_star: x, selector S, dictionary {P_k, D_k}, B, C,
+ * L, N, K, batch, heads).  Plain C struct; all fields are read-only inputs. */
+typedef struct {
+    int64_t batch;       /* B >= 1                                                  */
+    int64_t heads;       /* H >= 1                                                  */
+    int64_t len;         /* L >= 1 (time steps)                                     */
+    int64_t state;       /* N, 1 <= N <= 1024 (index maps stored as uint16)         */
+    int64_t dict;        /* K, 1 <= K <= 256 (k* stored as uint8)     */
+    int64_t d_in;        /* selector input width (pdssm_select only)                */
+    int64_t p_out;       /* readout rows P per head (0 = no readout)                */
+    int32_t chunk;       /* tau >= 1, or 0 = library default (pdssm_default_chunk)  */
+    int32_t is_complex;  /* c: 1 = real, 2 = complex (split re/im planes)           */
+    int32_t dtype;       /* pdssm_dtype of the "act" tensors                        */
+    int32_t diag_mode;   /* pdssm_diag_mode                                         */
+    uint32_t flags;      /* PDSSM_CHECK_FINITE | PDSSM_EXPORT_MAPS | ...            */
+    uint32_t reserved;   /* must be 0                                               */
+} pdssm_dims;
+
+/* ---------------------------------------------------------------------------
+ * Sizes
+ * ------------------------------------------------------------------------- */
+/* tau actually used for these dims (dims->chunk, or the tuned default). */
+int32_t pdssm_default_chunk(const pdssm_dims* dims);
+
+/* Bytes of device workspace `op` (PDSSM_OP_*) needs; 0 on invalid dims.
+ * Workspace contents are scratch: nothing is kept between calls. */
+size_t pdssm_workspace_bytes(const pdssm_dims* dims, int op);
+
+/* Bytes of the chunk_state buffer written by pdssm_scan_fwd and read by
+ * pdssm_scan_bwd.  Layout (sections 256-byte aligned, S = B*H, C = ceil(L/tau)):
+ *   section 0: pi_bar  uint16 [S][C][N]     chunk aggregate index maps   (Alg. 1 A_c)
+ *   section 1: d_bar   f32    [S][C][c][N]  chunk aggregate diagonals    (Alg. 1 A_c)
+ *   section 2: beta_bar f32   [S][C][c][N]  chunk local-replay biases    (Alg. 1 B_c)
+ *   section 3: carry   f32    [S][C][c][N]  state entering chunk c, carry_0 = h0
+ *                                           (Alg. 1 Carry_c)
+ * pdssm_chunk_state_offsets writes the 4 byte offsets. */
+size_t pdssm_chunk_state_bytes(const pdssm_dims* dims);
+pdssm_status pdssm_chunk_state_offsets(const pdssm_dims* dims, size_t offsets[4]);
+
+/* ---------------------------------------------------------------------------
+ * a1: dictionary sparsification (Eq. 5; App. E.2.1)
+ *   M        f32    [H][K][N][N]   dense dictionary, M[h][k][i][j] (row i, column j)
+ *   dict_idx uint16 [H][K][N]      out: dict_idx[h][k][j] = argmax_i M[h][k][i][j]
+ * "only done once, e.g. at the beginning of the optimization step".
+ * ------------------------------------------------------------------------- */
+pdssm_status pdssm_sparsify(const float* M, uint16_t* dict_idx, const pdssm_dims* dims,
+                            pdssm_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * a2-a4: selection (Eqs. 6-8; App. E.2.1)
+ *   x        act    [B][L][d_in]  tokens
+ *   S        act    [H][K][d_in]  selector weights
+ *   dict_idx uint16 [H][K][N]     sparse dictionary (needed only if P_opt)
+ *   kstar    uint8  [B][H][L]     out: k* = argmax_k sum_d S[h][k][d] x[b][t][d]
+ *   P_opt    uint16 [B][H][L][N]  out (optional): P_t = dict_idx[h][k*]
+ *   logits_opt f32  [B][H][L][K]  out (optional): the selector logits
+ * Logits are accumulated in fp32 from the act-dtype products.
+ * ------------------------------------------------------------------------- */
+pdssm_status pdssm_select(const void* x, const void* S, const uint16_t* dict_idx,
+                          uint8_t* kstar, uint16_t* P_opt, float* logits_opt,
+                          const pdssm_dims* dims, void* ws, size_t ws_bytes,
+                          pdssm_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * a6-a8: forward chunked scan (Alg. 1; Kernels A/B/C
+ * PAPER.md:1020-1095) + fused readout (Eq. 1 y_t = Re(C x_t))
+ *   kstar      uint8  [B][H][L]
+ *   dict_idx   uint16 [H][K][N]
+ *   diag       PER_STEP: act [B][H][L][c][N];  PER_DICT: f32 [H][K][c][N]
+ *   bias       act    [B][H][L][c][N]   b_t (= B x_t, computed by the caller)
+ *   h0_opt     f32    [B][H][c][N]      initial state (NULL = 0; reading R5)
+ *   C_opt      f32    [H][c][P][N]      readout (needed iff y_opt)
+ *   h_out_opt  act    [B][H][L][c][N]   out: h_t
+ *   y_opt      act    [B][L][H][P]      out: y_t = Re(C_h h_t)
+ *   chunk_state                          out: see pdssm_chunk_state_bytes (required)
+ *   maps_opt   uint16 [B][H][C+1][N]     out (PDSSM_EXPORT_MAPS): exclusive prefix
+ *              maps Pi before chunk c (maps[0] = identity) and the final map Pi_{L-1}
+ * At least one of h_out_opt / y_opt must be given.
+ * ------------------------------------------------------------------------- */
+pdssm_status pdssm_scan_fwd(const uint8_t* kstar, const uint16_t* dict_idx, const void* diag,
+                            const void* bias, const float* h0_opt, const float* C_opt,
+                            void* h_out_opt, void* y_opt, void* chunk_state, uint16_t* maps_opt,
+                            const pdssm_dims* dims, void* ws, size_t ws_bytes,
+                            pdssm_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * a9: backward (reverse, transposed) scan (App. C; Prop. 2
+ * PAPER.md:210-223).  Real-linear split gradients packed re + i*im (reading R13):
+ *   lambda_{L-1} = e_{L-1} + lam_in,  lambda_{t-1} = e_{t-1} + A_t^T lambda_t,
+ *   (A_t^T mu)[j] = conj(D_t[j]) mu[P_t[j]]           (a pure gather)
+ *   dbias_t = lambda_t
+ *   ddiag_t[j] = conj(h_{t-1}[j]) lambda_t[P_t[j]]       (h_{-1} = h0)
+ *   gsel_t = sum_j Re(conj(lambda_t[P_t[j]]) D_t[j] h_{t-1}[j])   (dl/dP_t . P_t, reading R14)
+ *   dh0 = A_0^T lambda_0
+ * with the direct gradient e_t = dh_t + conj(C_h)^T dy_t.
+ *   kstar, dict_idx, diag, h0_opt : the SAME tensors given to pdssm_scan_fwd
+ *   h_saved    act [B][H][L][c][N]  the forward states h_t (required)
+ *   chunk_state                      the forward's chunk_state (reused Abar_c)
+ *   dh_opt     act [B][H][L][c][N]  direct state gradient (NULL = 0)
+ *   dy_opt     act [B][L][H][P] with C_opt f32 [H][c][P][N] (NULL = 0)
+ *   lam_in_opt f32 [B][H][c][N]     adjoint entering h_{L-1} from a later
+ *                                    sequence segment (NULL = 0; sequence parallel)
+ *   dbias      act [B][H][L][c][N]  out
+ *   ddiag      PER_STEP act [B][H][L][c][N]; PER_DICT f32 [H][K][c][N] (summed over b,t) out
+ *   gsel       f32 [B][H][L]        out (optional)
+ *   dh0_opt    f32 [B][H][c][N]     out (optional)
+ * ------------------------------------------------------------------------- */
+pdssm_status pdssm_scan_bwd(const uint8_t* kstar, const uint16_t* dict_idx, const void* diag,
+                            const void* h_saved, const float* h0_opt, const void* chunk_state,
+                            const void* dh_opt, const void* dy_opt, const float* C_opt,
+                            const float* lam_in_opt, void* dbias, void* ddiag, float* gsel,
+                            float* dh0_opt, const pdssm_dims* dims, void* ws, size_t ws_bytes,
+                            pdssm_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * Sequence parallelism (the chunk algebra lifted to per-rank segments; the
+ * associativity of PAPER.md:927-932).  A summary of a segment is, per (b,h):
+ *   pi uint16[N] (padded to an even count), d f32[c][N], beta f32[c][N]
+ * stored contiguously as pdssm_summary_bytes(dims) bytes per (b,h) in the
+ * order [B][H] { pi, d, beta }.
+ * ------------------------------------------------------------------------- */
+size_t pdssm_summary_bytes(const pdssm_dims* dims);
+
+/* forward summary (pi, d, beta) of the segment described by dims (len = the
+ * segment length): its Phase-A aggregate from identity / zero state. */
+pdssm_status pdssm_segment_summary(const uint8_t* kstar, const uint16_t* dict_idx,
+                                   const void* diag, const void* bias, void* summary_out,
+                                   const pdssm_dims* dims, void* ws, size_t ws_bytes,
+                                   pdssm_stream_t stream);
+
+/* Compose the first `rank` of G gathered summaries ([G][B][H] blocks, rank
+ * order) onto h0: carry_out = S_{rank-1} o ... o S_0 (h0) (f32 [B][H][c][N]);
+ * map_out_opt uint16 [B][H][N] = composed index map.  Deterministic order. */
+pdssm_status pdssm_compose_carry(const void* summaries, int32_t rank, int32_t G,
+                                 const float* h0_opt, float* carry_out, uint16_t* map_out_opt,
+                                 const pdssm_dims* dims, pdssm_stream_t stream);
+
+/* Backward summary of a segment: beta'_seg = A_{s}^T lambda_loc_{s} (the adjoint
+ * the segment sends to the state before it, from zero incoming adjoint),
+ * f32 [B][H][c][N].  Needs the segment's forward chunk_state. */
+pdssm_status pdssm_segment_summary_bwd(const uint8_t* kstar, const uint16_t* dict_idx,
+                                       const void* diag, const void* chunk_state,
+                                       const void* dh_opt, const void* dy_opt, const float* C_opt,
+                                       float* beta_out, const pdssm_dims* dims, void* ws,
+                                       size_t ws_bytes, pdssm_stream_t stream);
+
+/* Adjoint entering segment `rank` from the segments after it:
+ * mu = sum over g > rank of (Abar_{rank+1}^T ... Abar_{g-1}^T) beta'_g, where
+ * fwd_summaries are the gathered FORWARD summaries (their (pi, d) = Abar_g)
+ * and beta_bwd the gathered backward summaries f32 [G][B][H][c][N]. */
+pdssm_status pdssm_compose_lambda(const void* fwd_summaries, const float* beta_bwd, int32_t rank,
+                                  int32_t G, float* lam_out, const pdssm_dims* dims,
+                                  pdssm_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * Diagnostics
+ * ------------------------------------------------------------------------- */
+const char* pdssm_status_string(pdssm_status s);
+const char* pdssm_last_error(void);           /* thread-local message of the last failure */
+const char* pdssm_version(void);
+/* Synchronises `stream`, reads and clears the device error word set under
+ * PDSSM_CHECK_FINITE: PDSSM_ERR_RANGE / PDSSM_ERR_NONFINITE / PDSSM_OK. */
+pdssm_status pdssm_check_device(pdssm_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PDSSM_H */

@@ -1,0 +1,229 @@
+// Backward (reverse, transposed) chunked scan.  The paper gives no backward
+// kernel (only App. C PAPER.md:818-823 and Prop. 2); this is
+// the transposed Algorithm 1:
+//   lambda_{t-1} = e_{t-1} + A_t^T lambda_t,  (A_t^T mu)[j] = conj(D_t[j]) mu[P_t[j]]
+// which is a pure gather -- no collisions.  Chunk summaries:
+//   Phase A': beta'_c = A_{s_c}^T lambda_loc_{s_c}   (reverse local scan, zero incoming)
+//   Phase B': mu_{C-1} = lam_in, mu_{c-1} = beta'_c + Abar_c^T mu_c  (forward (pi_bar, d_bar) reused)
+//   Phase C': replay lambda from e_{e_c} + mu_c, emit db, dD, g.
+#pragma once
+#include "k_scan_fwd.cuh"
+
+namespace pdssm {
+
+template <typename TE, int NC>
+__device__ __forceinline__ cpx load_e(const TE* e, size_t off, int N, int j) {
+    if (e == nullptr) return cpx{0.f, 0.f};
+    return load_plane<TE, NC>(e, off, N, j);
+}
+
+// Phase A': reverse local scan of chunk c from zero incoming adjoint.
+template <typename T, typename TE, int NC, bool PERDICT>
+__global__ void k_bwd_phaseA(const uint8_t* __restrict__ kstar, const uint16_t* __restrict__ dict_idx,
+                             const T* __restrict__ diag, const float* __restrict__ diag_dict,
+                             const TE* __restrict__ e, float* __restrict__ betap, int H, int L, int N, int K,
+                             int tau, int C_ch) {
+    extern __shared__ float smem[];
+    float* lsh = smem;  // [2][NC][N]
+    const int item = blockIdx.x;
+    const int s = item / C_ch, c = item % C_ch, h = s % H;
+    const int t0 = c * tau, t1 = min(t0 + tau, L);
+    const int j = threadIdx.x;
+    const bool act = j < N;
+    cpx lam{0.f, 0.f};
+    if (act) lam = load_e<TE, NC>(e, ((size_t)s * L + (t1 - 1)) * NC * N, N, j);
+    for (int t = t1 - 1; t >= t0; --t) {
+        const int buf = (t1 - 1 - t) & 1;
+        float* l_b = lsh + buf * NC * N;
+        if (act) {
+            l_b[j] = lam.re;
+            if (NC == 2) l_b[N + j] = lam.im;
+        }
+        __syncthreads();
+        if (act) {
+            const int k = load_k(kstar, (size_t)s * L + t, K, 0);
+            const size_t off = ((size_t)s * L + t) * NC * N;
+            const int pj = clamp_idx(__ldg(dict_idx + (size_t)(h * K + k) * N + j), N, 0);
+            cpx lamP{l_b[pj], NC == 2 ? l_b[N + pj] : 0.f};
+            cpx Dj = load_diag<T, NC, PERDICT>(diag, diag_dict, off, h, k, K, N, j);
+            cpx back = cmulc(Dj, lamP);
+            if (t > t0) {
+                lam = cadd(load_e<TE, NC>(e, off - (size_t)NC * N, N, j), back);
+            } else {
+                const size_t ci = (size_t)s * C_ch + c;
+                betap[ci * NC * N + j] = back.re;
+                if (NC == 2) betap[ci * NC * N + N + j] = back.im;
+            }
+        }
+    }
+}
+
+// Phase B': reverse carry chain per sequence; also dh0 = beta'_0 + Abar_0^T mu_0.
+template <int NC>
+__global__ void k_bwd_phaseB(ChunkStateView cs, const float* __restrict__ betap, const float* __restrict__ lam_in,
+                             float* __restrict__ mu_out, float* __restrict__ dh0, int N, int C_ch) {
+    extern __shared__ float smem[];
+    float* msh = smem;  // [NC][N]
+    const int s = blockIdx.x;
+    const int j = threadIdx.x;
+    const bool act = j < N;
+    cpx mu{0.f, 0.f};
+    if (act && lam_in) {
+        mu.re = lam_in[(size_t)s * NC * N + j];
+        if (NC == 2) mu.im = lam_in[(size_t)s * NC * N + N + j];
+    }
+    for (int c = C_ch - 1; c >= 0; --c) {
+        const size_t ci = (size_t)s * C_ch + c;
+        if (act) {
+            mu_out[ci * NC * N + j] = mu.re;
+            if (NC == 2) mu_out[ci * NC * N + N + j] = mu.im;
+            msh[j] = mu.re;
+            if (NC == 2) msh[N + j] = mu.im;
+        }
+        __syncthreads();
+        if (act) {
+            const int pj = cs.pi[ci * N + j];
+            cpx db{cs.d[ci * NC * N + j], NC == 2 ? cs.d[ci * NC * N + N + j] : 0.f};
+            cpx bp{betap[ci * NC * N + j], NC == 2 ? betap[ci * NC * N + N + j] : 0.f};
+            cpx mP{msh[pj], NC == 2 ? msh[N + pj] : 0.f};
+            mu = cadd(bp, cmulc(db, mP));
+        }
+        __syncthreads();
+    }
+    if (act && dh0) {
+        dh0[(size_t)s * NC * N + j] = mu.re;
+        if (NC == 2) dh0[(size_t)s * NC * N + N + j] = mu.im;
+    }
+}
+
+// Phase C': replay lambda from e_{e_c} + mu_c and emit the gradients.
+//   db_t = lambda_t, dD_t[j] = conj(h_{t-1}[j]) lambda_t[P_t[j]],
+//   g_t = sum_j Re(conj(lambda_t[P_t[j]]) D_t[j] h_{t-1}[j])   (warp shuffles +
+//   per-warp partials summed in warp order: deterministic)
+template <typename T, typename TE, int NC, bool PERDICT>
+__global__ void k_bwd_phaseC(const uint8_t* __restrict__ kstar, const uint16_t* __restrict__ dict_idx,
+                             const T* __restrict__ diag, const float* __restrict__ diag_dict,
+                             const T* __restrict__ hsaved, const float* __restrict__ h0,
+                             const TE* __restrict__ e, const float* __restrict__ mu_in, T* __restrict__ dbias,
+                             T* __restrict__ ddiag, float* __restrict__ ddiag_f32, float* __restrict__ gsel,
+                             int H, int L, int N, int K, int tau, int C_ch) {
+    extern __shared__ float smem[];
+    const int nw = blockDim.x / 32;
+    float* lsh = smem;                   // [2][NC][N]
+    float* gpart = smem + 2 * NC * N;    // ring [64][nw] of per-warp partials of g
+    const int item = blockIdx.x;
+    const int s = item / C_ch, c = item % C_ch, h = s % H;
+    const int t0 = c * tau, t1 = min(t0 + tau, L);
+    const int j = threadIdx.x;
+    const int lane = j & 31, w = j >> 5;
+    const bool act = j < N;
+    const size_t ci = (size_t)s * C_ch + c;
+    cpx lam{0.f, 0.f};
+    if (act) {
+        lam = load_e<TE, NC>(e, ((size_t)s * L + (t1 - 1)) * NC * N, N, j);
+        lam.re += mu_in[ci * NC * N + j];
+        if (NC == 2) lam.im += mu_in[ci * NC * N + N + j];
+    }
+    for (int t = t1 - 1; t >= t0; --t) {
+        const int buf = (t1 - 1 - t) & 1;
+        float* l_b = lsh + buf * NC * N;
+        const size_t off = ((size_t)s * L + t) * NC * N;
+        if (act) {
+            l_b[j] = lam.re;
+            if (NC == 2) l_b[N + j] = lam.im;
+            stact(dbias + off + j, lam.re);
+            if (NC == 2) stact(dbias + off + N + j, lam.im);
+        }
+        __syncthreads();
+        const int q = t1 - 1 - t;            // reverse step count within the chunk
+        if (gsel && q > 0 && (q & 31) == 0 && j < 32) {
+            // flush steps [q-32, q): their partials were written before this barrier
+            const int qq = q - 32 + j;
+            float acc = 0.f;
+            for (int ww = 0; ww < nw; ++ww) acc += gpart[(qq & 63) * nw + ww];
+            gsel[(size_t)s * L + (t1 - 1 - qq)] = acc;
+        }
+        float gval = 0.f;
+        if (act) {
+            const int k = load_k(kstar, (size_t)s * L + t, K, 0);
+            const int pj = clamp_idx(__ldg(dict_idx + (size_t)(h * K + k) * N + j), N, 0);
+            cpx lamP{l_b[pj], NC == 2 ? l_b[N + pj] : 0.f};
+            cpx Dj = load_diag<T, NC, PERDICT>(diag, diag_dict, off, h, k, K, N, j);
+            cpx hp{0.f, 0.f};
+            if (t > 0) {
+                hp = load_plane<T, NC>(hsaved, off - (size_t)NC * N, N, j);
+            } else if (h0) {
+                hp.re = h0[(size_t)s * NC * N + j];
+                if (NC == 2) hp.im = h0[(size_t)s * NC * N + N + j];
+            }
+            cpx dD = cmulc(hp, lamP);
+            if (PERDICT) {
+                ddiag_f32[off + j] = dD.re;
+                if (NC == 2) ddiag_f32[off + N + j] = dD.im;
+            } else {
+                stact(ddiag + off + j, dD.re);
+                if (NC == 2) stact(ddiag + off + N + j, dD.im);
+            }
+            cpx prod = cmul(Dj, hp);
+            gval = lamP.re * prod.re + lamP.im * prod.im;
+            if (t > t0) lam = cadd(load_e<TE, NC>(e, off - (size_t)NC * N, N, j), cmulc(Dj, lamP));
+        }
+        for (int o = 16; o > 0; o >>= 1) gval += __shfl_xor_sync(0xffffffffu, gval, o);
+        if (lane == 0) gpart[(q & 63) * nw + w] = gval;
+    }
+    __syncthreads();
+    if (gsel) {
+        const int nsteps = t1 - t0;
+        const int qlast = ((nsteps - 1) / 32) * 32;
+        for (int qq = qlast + j; qq < nsteps; qq += blockDim.x) {
+            float acc = 0.f;
+            for (int ww = 0; ww < nw; ++ww) acc += gpart[(qq & 63) * nw + ww];
+            gsel[(size_t)s * L + (t1 - 1 - qq)] = acc;
+        }
+    }
+}
+
+// e_t = dh_t + conj(C_h)^T dy_t  (readout adjoint, reading R13) into f32 scratch.
+template <typename T, int NC>
+__global__ void k_bwd_prepare_e(const T* __restrict__ dh, const T* __restrict__ dy, const float* __restrict__ Cw,
+                                float* __restrict__ e, int H, int L, int N, int P) {
+    extern __shared__ float smem[];
+    const int t = blockIdx.x % L;
+    const int s = blockIdx.x / L;
+    const int h = s % H, b = s / H;
+    for (int p = threadIdx.x; p < P; p += blockDim.x) smem[p] = dy ? ldact(dy + (((size_t)b * L + t) * H + h) * P + p) : 0.f;
+    __syncthreads();
+    const size_t off = ((size_t)s * L + t) * NC * N;
+    for (int q = threadIdx.x; q < NC * N; q += blockDim.x) {
+        const int pl = q / N, j = q % N;
+        float acc = dh ? ldact(dh + off + q) : 0.f;
+        if (dy) {
+            const float* cp = Cw + ((size_t)(h * NC + pl) * P) * N + j;
+            float sgn = pl == 0 ? 1.f : -1.f;   // conj(C): re part +, im part -
+            for (int p = 0; p < P; ++p) acc += sgn * __ldg(cp + (size_t)p * N) * smem[p];
+        }
+        e[off + q] = acc;
+    }
+}
+
+// PER_DICT: ddiag[h][k][pl][j] = sum over (b, t) with k*[b,h,t] = k of dD (fixed order).
+template <int NC>
+__global__ void k_bwd_reduce_dict(const uint8_t* __restrict__ kstar, const float* __restrict__ dD,
+                                  float* __restrict__ ddiag, int B, int H, int L, int N, int K) {
+    const int e = blockIdx.x;   // h*K + k
+    const int h = e / K, k = e % K;
+    for (int q = threadIdx.x; q < NC * N; q += blockDim.x) {
+        float acc = 0.f;
+        for (int b = 0; b < B; ++b) {
+            const size_t s = (size_t)b * H + h;
+            for (int t = 0; t < L; ++t) {
+                int kk = __ldg(kstar + s * L + t);
+                if (kk >= K) kk = K - 1;
+                if (kk == k) acc += dD[(s * L + t) * NC * N + q];
+            }
+        }
+        ddiag[(size_t)e * NC * N + q] = acc;
+    }
+}
+
+}  // namespace pdssm

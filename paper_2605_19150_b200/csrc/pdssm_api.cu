@@ -1,0 +1,590 @@
+// C ABI of libpdssm.so (declarations and contracts: include/pdssm.h).
+// Validation is synchronous and happens before any CUDA call; every kernel is
+// enqueued on the caller's stream; nothing is allocated.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <type_traits>
+#include <utility>
+
+#include "pdssm_common.cuh"
+#include "k_scan_fwd.cuh"
+#include "k_scan_bwd.cuh"
+#include "k_select.cuh"
+#include "k_sp.cuh"
+#include "k_scan_fused.cuh"
+
+
+using namespace pdssm;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+pdssm_status fail(pdssm_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return s;
+}
+
+struct Geo {
+    int64_t B, H, L, N, K, S, d_in, P;
+    int tau, C, nc, dtype, diag_mode;
+    uint32_t flags;
+    size_t act;   // bytes per act element
+};
+
+constexpr uint32_t kKnownFlags = PDSSM_CHECK_FINITE | PDSSM_DETERMINISTIC | PDSSM_EXPORT_MAPS;
+
+int default_tau(const pdssm_dims* d) {
+    (void)d;
+    return 64;
+}
+
+pdssm_status geo_of(const pdssm_dims* d, Geo* g) {
+    if (!d) return fail(PDSSM_ERR_NULL, "dims is NULL");
+    if (d->batch < 1 || d->heads < 1 || d->len < 1)
+        return fail(PDSSM_ERR_SHAPE, "batch, heads, len must be >= 1 (got %lld, %lld, %lld)", (long long)d->batch,
+                    (long long)d->heads, (long long)d->len);
+    if (d->state < 1 || d->state > 1024) return fail(PDSSM_ERR_SHAPE, "state N must be in [1, 1024] (got %lld)", (long long)d->state);
+    if (d->dict < 1 || d->dict > 256) return fail(PDSSM_ERR_SHAPE, "dict K must be in [1, 256] (got %lld)", (long long)d->dict);
+    if (d->is_complex != 1 && d->is_complex != 2) return fail(PDSSM_ERR_SHAPE, "is_complex must be 1 or 2");
+    if (d->dtype != PDSSM_F32 && d->dtype != PDSSM_BF16) return fail(PDSSM_ERR_DTYPE, "unknown dtype %d", d->dtype);
+    if (d->diag_mode != PDSSM_DIAG_PER_STEP && d->diag_mode != PDSSM_DIAG_PER_DICT)
+        return fail(PDSSM_ERR_DTYPE, "unknown diag_mode %d", d->diag_mode);
+    if (d->flags & ~kKnownFlags) return fail(PDSSM_ERR_DTYPE, "unknown flag bits 0x%x", d->flags & ~kKnownFlags);
+    if (d->reserved != 0) return fail(PDSSM_ERR_DTYPE, "reserved must be 0");
+    if (d->chunk < 0) return fail(PDSSM_ERR_SHAPE, "chunk must be >= 0");
+    if (d->p_out < 0 || d->d_in < 0) return fail(PDSSM_ERR_SHAPE, "p_out, d_in must be >= 0");
+    g->B = d->batch; g->H = d->heads; g->L = d->len; g->N = d->state; g->K = d->dict;
+    g->S = g->B * g->H; g->d_in = d->d_in; g->P = d->p_out;
+    g->tau = d->chunk ? d->chunk : default_tau(d);
+    if (g->tau > g->L) g->tau = (int)g->L;
+    g->C = (int)ceil_div(g->L, g->tau);
+    if ((int64_t)g->S * g->C > (int64_t)1 << 31) return fail(PDSSM_ERR_SHAPE, "too many (sequence, chunk) items");
+    g->nc = d->is_complex; g->dtype = d->dtype; g->diag_mode = d->diag_mode; g->flags = d->flags;
+    g->act = d->dtype == PDSSM_BF16 ? 2 : 4;
+    return PDSSM_OK;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct Bump {
+    char* base;
+    size_t off = 0;
+    explicit Bump(void* p) : base(static_cast<char*>(p)) {}
+    template <typename T> T* take(size_t bytes) {
+        T* r = reinterpret_cast<T*>(base ? base + off : nullptr);
+        off += align256(bytes);
+        return r;
+    }
+};
+
+size_t plan_bytes(const Geo& g) {
+    return align256((size_t)g.H * g.K * (g.N + 1) * 2) + align256((size_t)g.H * g.K * g.N * 2);
+}
+size_t cs_pi_bytes(const Geo& g) { return align256((size_t)g.S * g.C * g.N * 2); }
+size_t cs_f_bytes(const Geo& g) { return align256((size_t)g.S * g.C * g.nc * g.N * 4); }
+size_t chunk_state_bytes_g(const Geo& g) { return cs_pi_bytes(g) + 3 * cs_f_bytes(g); }
+size_t seq_f_bytes(const Geo& g) { return align256((size_t)g.S * g.L * g.nc * g.N * 4); }
+size_t seq_act_bytes(const Geo& g) { return align256((size_t)g.S * g.L * g.nc * g.N * g.act); }
+int npad8(int64_t N) { return (int)((N + 7) & ~7); }
+size_t summary_block_bytes(const Geo& g) { return (size_t)npad8(g.N) * 2 + (size_t)2 * g.nc * g.N * 4; }
+
+ChunkStateView cs_view(const Geo& g, void* p) {
+    char* b = static_cast<char*>(p);
+    ChunkStateView v;
+    v.pi = reinterpret_cast<uint16_t*>(b);
+    v.d = reinterpret_cast<float*>(b + cs_pi_bytes(g));
+    v.beta = reinterpret_cast<float*>(b + cs_pi_bytes(g) + cs_f_bytes(g));
+    v.carry = reinterpret_cast<float*>(b + cs_pi_bytes(g) + 2 * cs_f_bytes(g));
+    return v;
+}
+
+size_t ws_bytes_g(const Geo& g, int op) {
+    switch (op) {
+        case PDSSM_OP_SELECT:
+            return align256((size_t)g.S * g.L * g.K * 4);
+        case PDSSM_OP_FWD:
+            return plan_bytes(g) + (g.P > 0 ? seq_act_bytes(g) : 0) + fused_ws_bytes(g.S, g.C);
+        case PDSSM_OP_BWD:
+            return 2 * cs_f_bytes(g) + (g.P > 0 ? seq_f_bytes(g) : 0) +
+                   (g.diag_mode == PDSSM_DIAG_PER_DICT ? seq_f_bytes(g) : 0);
+        case PDSSM_OP_SEGMENT: {
+            size_t fwd = plan_bytes(g) + chunk_state_bytes_g(g);
+            size_t bwd = 2 * cs_f_bytes(g) + (g.P > 0 ? seq_f_bytes(g) : 0);
+            return fwd > bwd ? fwd : bwd;
+        }
+        default:
+            return 0;
+    }
+}
+
+bool misaligned(const void* p, size_t a) { return p && (reinterpret_cast<uintptr_t>(p) % a) != 0; }
+
+pdssm_status cuda_check(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(PDSSM_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    return PDSSM_OK;
+}
+
+int threads_for(int64_t N) { return (int)((N + 31) / 32 * 32); }
+
+template <typename F>
+pdssm_status with_nc(int nc, F&& f) {
+    if (nc == 1) return f(std::integral_constant<int, 1>{});
+    return f(std::integral_constant<int, 2>{});
+}
+
+template <typename F>
+pdssm_status with_act(int dtype, F&& f) {
+    if (dtype == PDSSM_BF16) return f(__nv_bfloat16{});
+    return f(float{});
+}
+
+template <typename F>
+pdssm_status with_pd(int mode, F&& f) {
+    if (mode == PDSSM_DIAG_PER_DICT) return f(std::true_type{});
+    return f(std::false_type{});
+}
+
+pdssm_status set_smem(const void* fn, size_t bytes) {
+    if (bytes > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        if (e != cudaSuccess) return fail(PDSSM_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    }
+    return PDSSM_OK;
+}
+
+// ------------------------------------------------------------------ plan
+pdssm_status launch_plan(const Geo& g, const uint16_t* dict_idx, uint16_t* pstart, uint16_t* psrc,
+                         cudaStream_t st) {
+    int thr = threads_for(g.N);
+    if (thr > 1024) thr = 1024;
+    k_build_plan<<<(unsigned)(g.H * g.K), thr, (size_t)g.N * 2, st>>>(dict_idx, pstart, psrc, (int)g.N, g.flags);
+    return cuda_check("build_plan");
+}
+
+// ------------------------------------------------------------------ forward phases
+pdssm_status fwd_three_phase(const Geo& g, const uint8_t* kstar, const uint16_t* dict_idx, const uint16_t* pstart,
+                             const uint16_t* psrc, const void* diag, const void* bias, const float* h0,
+                             ChunkStateView cs, uint16_t* maps, void* hout, bool phaseC, cudaStream_t st) {
+    const int thr = threads_for(g.N);
+    const unsigned items = (unsigned)(g.S * g.C);
+    return with_act(g.dtype, [&](auto tv) {
+        using T = decltype(tv);
+        return with_nc(g.nc, [&](auto ncv) {
+            constexpr int NC = decltype(ncv)::value;
+            return with_pd(g.diag_mode, [&](auto pdv) {
+                constexpr bool PD = decltype(pdv)::value;
+                const T* dg = PD ? nullptr : static_cast<const T*>(diag);
+                const float* dd = PD ? static_cast<const float*>(diag) : nullptr;
+                size_t smA = (size_t)4 * NC * g.N * 4;
+                k_fwd_phaseA<T, NC, PD><<<items, thr, smA, st>>>(kstar, dict_idx, pstart, psrc, dg, dd,
+                                                                 static_cast<const T*>(bias), cs, (int)g.H, (int)g.L,
+                                                                 (int)g.N, (int)g.K, g.tau, g.C, g.flags);
+                pdssm_status r = cuda_check("fwd_phaseA");
+                if (r) return r;
+                size_t smB = (size_t)NC * g.N * 4 + (size_t)g.N * 2 + 16;
+                k_fwd_phaseB<NC><<<(unsigned)g.S, thr, smB, st>>>(cs, h0, maps, nullptr, (int)g.N, g.C);
+                r = cuda_check("fwd_phaseB");
+                if (r || !phaseC) return r;
+                size_t smC = (size_t)2 * NC * g.N * 4;
+                k_fwd_phaseC<T, NC, PD><<<items, thr, smC, st>>>(kstar, pstart, psrc, dg, dd,
+                                                                 static_cast<const T*>(bias), cs,
+                                                                 static_cast<T*>(hout), (int)g.H, (int)g.L,
+                                                                 (int)g.N, (int)g.K, g.tau, g.C, g.flags);
+                return cuda_check("fwd_phaseC");
+            });
+        });
+    });
+}
+
+}  // namespace
+
+// ====================================================================== ABI
+extern "C" {
+
+int32_t pdssm_default_chunk(const pdssm_dims* dims) {
+    Geo g;
+    if (geo_of(dims, &g)) return 0;
+    return g.tau;
+}
+
+size_t pdssm_workspace_bytes(const pdssm_dims* dims, int op) {
+    Geo g;
+    if (geo_of(dims, &g)) return 0;
+    return ws_bytes_g(g, op);
+}
+
+size_t pdssm_chunk_state_bytes(const pdssm_dims* dims) {
+    Geo g;
+    if (geo_of(dims, &g)) return 0;
+    return chunk_state_bytes_g(g);
+}
+
+pdssm_status pdssm_chunk_state_offsets(const pdssm_dims* dims, size_t offsets[4]) {
+    Geo g;
+    pdssm_status r = geo_of(dims, &g);
+    if (r) return r;
+    if (!offsets) return fail(PDSSM_ERR_NULL, "offsets is NULL");
+    offsets[0] = 0;
+    offsets[1] = cs_pi_bytes(g);
+    offsets[2] = cs_pi_bytes(g) + cs_f_bytes(g);
+    offsets[3] = cs_pi_bytes(g) + 2 * cs_f_bytes(g);
+    return PDSSM_OK;
+}
+
+size_t pdssm_summary_bytes(const pdssm_dims* dims) {
+    Geo g;
+    if (geo_of(dims, &g)) return 0;
+    return summary_block_bytes(g);
+}
+
+const char* pdssm_status_string(pdssm_status s) {
+    switch (s) {
+        case PDSSM_OK: return "PDSSM_OK";
+        case PDSSM_ERR_NULL: return "PDSSM_ERR_NULL";
+        case PDSSM_ERR_SHAPE: return "PDSSM_ERR_SHAPE";
+        case PDSSM_ERR_RANGE: return "PDSSM_ERR_RANGE";
+        case PDSSM_ERR_ALIGN: return "PDSSM_ERR_ALIGN";
+        case PDSSM_ERR_DTYPE: return "PDSSM_ERR_DTYPE";
+        case PDSSM_ERR_WORKSPACE: return "PDSSM_ERR_WORKSPACE";
+        case PDSSM_ERR_NONFINITE: return "PDSSM_ERR_NONFINITE";
+        case PDSSM_ERR_CUDA: return "PDSSM_ERR_CUDA";
+        case PDSSM_ERR_UNSUPPORTED: return "PDSSM_ERR_UNSUPPORTED";
+    }
+    return "PDSSM_UNKNOWN";
+}
+
+const char* pdssm_last_error(void) { return g_last_error.c_str(); }
+
+const char* pdssm_version(void) { return "pdssm-b200 0.1 (sm_100a)"; }
+
+pdssm_status pdssm_check_device(pdssm_stream_t stream) {
+    cudaError_t e = cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return fail(PDSSM_ERR_CUDA, "cudaStreamSynchronize: %s", cudaGetErrorString(e));
+    uint32_t w = 0;
+    e = cudaMemcpyFromSymbol(&w, g_err_word, sizeof(w));
+    if (e != cudaSuccess) return fail(PDSSM_ERR_CUDA, "read error word: %s", cudaGetErrorString(e));
+    uint32_t z = 0;
+    e = cudaMemcpyToSymbol(g_err_word, &z, sizeof(z));
+    if (e != cudaSuccess) return fail(PDSSM_ERR_CUDA, "clear error word: %s", cudaGetErrorString(e));
+    if (w & ERRBIT_NONFINITE) return fail(PDSSM_ERR_NONFINITE, "device reported NaN/Inf input");
+    if (w & ERRBIT_RANGE) return fail(PDSSM_ERR_RANGE, "device reported an out-of-range index");
+    return PDSSM_OK;
+}
+
+pdssm_status pdssm_sparsify(const float* M, uint16_t* dict_idx, const pdssm_dims* dims, pdssm_stream_t stream) {
+    Geo g;
+    pdssm_status r = geo_of(dims, &g);
+    if (r) return r;
+    if (!M || !dict_idx) return fail(PDSSM_ERR_NULL, "sparsify: M and dict_idx are required");
+    if (misaligned(M, 4) || misaligned(dict_idx, 2)) return fail(PDSSM_ERR_ALIGN, "sparsify: misaligned pointer");
+    int thr = threads_for(g.N);
+    if (thr > 1024) thr = 1024;
+    k_sparsify<<<(unsigned)(g.H * g.K), thr, 0, reinterpret_cast<cudaStream_t>(stream)>>>(M, dict_idx, (int)g.N,
+                                                                                          g.flags);
+    return cuda_check("sparsify");
+}
+
+pdssm_status pdssm_select(const void* x, const void* S, const uint16_t* dict_idx, uint8_t* kstar, uint16_t* P_opt,
+                          float* logits_opt, const pdssm_dims* dims, void* ws, size_t ws_bytes,
+                          pdssm_stream_t stream) {
+    Geo g;
+    pdssm_status r = geo_of(dims, &g);
+    if (r) return r;
+    if (g.d_in < 1) return fail(PDSSM_ERR_SHAPE, "select: d_in must be >= 1");
+    if (!x || !S || !kstar) return fail(PDSSM_ERR_NULL, "select: x, S, kstar are required");
+    if (P_opt && !dict_idx) return fail(PDSSM_ERR_NULL, "select: P_opt needs dict_idx");
+    if (misaligned(x, g.act) || misaligned(S, g.act) || misaligned(dict_idx, 2) || misaligned(P_opt, 2) ||
+        misaligned(logits_opt, 4))
+        return fail(PDSSM_ERR_ALIGN, "select: misaligned pointer");
+    float* logits = logits_opt;
+    if (!logits) {
+        if (!ws || ws_bytes < ws_bytes_g(g, PDSSM_OP_SELECT))
+            return fail(PDSSM_ERR_WORKSPACE, "select: workspace too small (need %zu)", ws_bytes_g(g, PDSSM_OP_SELECT));
+        logits = static_cast<float*>(ws);
+    }
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t M = g.B * g.L, NN = g.H * g.K;
+    dim3 grid((unsigned)ceil_div(M, 64), (unsigned)ceil_div(NN, 64));
+    r = with_act(g.dtype, [&](auto tv) {
+        using T = decltype(tv);
+        k_select_logits_simt<T><<<grid, 256, 0, st>>>(static_cast<const T*>(x), static_cast<const T*>(S), logits,
+                                                      (int)g.B, (int)g.L, (int)g.H, (int)g.K, (int)g.d_in, g.flags);
+        return cuda_check("select_logits");
+    });
+    if (r) return r;
+    const int64_t rows = g.S * g.L;
+    k_select_argmax<<<(unsigned)ceil_div(rows, 8), dim3(32, 8), 0, st>>>(logits, dict_idx, kstar, P_opt, rows,
+                                                                       (int)g.H, (int)g.L, (int)g.N, (int)g.K);
+    return cuda_check("select_argmax");
+}
+
+static pdssm_status common_scan_checks(const Geo& g, const void* kstar, const void* dict_idx, const void* diag) {
+    if (!kstar || !dict_idx || !diag) return fail(PDSSM_ERR_NULL, "kstar, dict_idx and diag are required");
+    if (misaligned(dict_idx, 2)) return fail(PDSSM_ERR_ALIGN, "dict_idx misaligned");
+    if (misaligned(diag, g.diag_mode == PDSSM_DIAG_PER_DICT ? 4 : g.act)) return fail(PDSSM_ERR_ALIGN, "diag misaligned");
+    return PDSSM_OK;
+}
+
+pdssm_status pdssm_scan_fwd(const uint8_t* kstar, const uint16_t* dict_idx, const void* diag, const void* bias,
+                            const float* h0_opt, const float* C_opt, void* h_out_opt, void* y_opt, void* chunk_state,
+                            uint16_t* maps_opt, const pdssm_dims* dims, void* ws, size_t ws_bytes,
+                            pdssm_stream_t stream) {
+    Geo g;
+    pdssm_status r = geo_of(dims, &g);
+    if (r) return r;
+    if ((r = common_scan_checks(g, kstar, dict_idx, diag))) return r;
+    if (!bias) return fail(PDSSM_ERR_NULL, "scan_fwd: bias is required");
+    if (!chunk_state) return fail(PDSSM_ERR_WORKSPACE, "scan_fwd: chunk_state is required");
+    if (!h_out_opt && !y_opt) return fail(PDSSM_ERR_NULL, "scan_fwd: need h_out_opt and/or y_opt");
+    if (y_opt && (!C_opt || g.P < 1)) return fail(PDSSM_ERR_NULL, "scan_fwd: y_opt needs C_opt and p_out >= 1");
+    if ((g.flags & PDSSM_EXPORT_MAPS) && !maps_opt) return fail(PDSSM_ERR_NULL, "scan_fwd: EXPORT_MAPS needs maps_opt");
+    if (misaligned(bias, g.act) || misaligned(h_out_opt, g.act) || misaligned(y_opt, g.act) || misaligned(h0_opt, 4) ||
+        misaligned(C_opt, 4) || misaligned(chunk_state, 16) || misaligned(maps_opt, 2))
+        return fail(PDSSM_ERR_ALIGN, "scan_fwd: misaligned pointer");
+    const size_t need = ws_bytes_g(g, PDSSM_OP_FWD);
+    if (!ws || ws_bytes < need) return fail(PDSSM_ERR_WORKSPACE, "scan_fwd: workspace too small (need %zu)", need);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    Bump bump(ws);
+    uint16_t* pstart = bump.take<uint16_t>((size_t)g.H * g.K * (g.N + 1) * 2);
+    uint16_t* psrc = bump.take<uint16_t>((size_t)g.H * g.K * g.N * 2);
+    void* hscratch = g.P > 0 ? bump.take<char>(seq_act_bytes(g)) : nullptr;
+    void* fused_ws = bump.take<char>(fused_ws_bytes(g.S, g.C));
+    void* hout = h_out_opt ? h_out_opt : hscratch;
+    ChunkStateView cs = cs_view(g, chunk_state);
+    if ((r = launch_plan(g, dict_idx, pstart, psrc, st))) return r;
+    uint16_t* maps = (g.flags & PDSSM_EXPORT_MAPS) ? maps_opt : nullptr;
+    bool done = false;
+    if ((r = fwd_fused_try(g.S, g.H, g.L, g.N, g.K, g.tau, g.C, g.nc, g.dtype, g.diag_mode, g.flags, kstar, dict_idx,
+                           pstart, psrc, diag, bias, h0_opt, cs, maps, hout, fused_ws, st, &done)))
+        return fail(r, "scan_fwd (fused): %s", cudaGetErrorString(cudaGetLastError()));
+    if (!done) {
+        if ((r = fwd_three_phase(g, kstar, dict_idx, pstart, psrc, diag, bias, h0_opt, cs, maps, hout, true, st)))
+            return r;
+    }
+    if (y_opt) {
+        r = with_act(g.dtype, [&](auto tv) {
+            using T = decltype(tv);
+            return with_nc(g.nc, [&](auto ncv) {
+                constexpr int NC = decltype(ncv)::value;
+                k_readout<T, NC><<<(unsigned)(g.S * g.L), 128, (size_t)NC * g.N * 4, st>>>(
+                    static_cast<const T*>(hout), C_opt, static_cast<T*>(y_opt), (int)g.H, (int)g.L, (int)g.N, (int)g.P);
+                return cuda_check("readout");
+            });
+        });
+    }
+    return r;
+}
+
+pdssm_status pdssm_scan_bwd(const uint8_t* kstar, const uint16_t* dict_idx, const void* diag, const void* h_saved,
+                            const float* h0_opt, const void* chunk_state, const void* dh_opt, const void* dy_opt,
+                            const float* C_opt, const float* lam_in_opt, void* dbias, void* ddiag, float* gsel,
+                            float* dh0_opt, const pdssm_dims* dims, void* ws, size_t ws_bytes,
+                            pdssm_stream_t stream) {
+    Geo g;
+    pdssm_status r = geo_of(dims, &g);
+    if (r) return r;
+    if ((r = common_scan_checks(g, kstar, dict_idx, diag))) return r;
+    if (!h_saved) return fail(PDSSM_ERR_NULL, "scan_bwd: h_saved is required");
+    if (!chunk_state) return fail(PDSSM_ERR_WORKSPACE, "scan_bwd: chunk_state is required");
+    if (!dbias || !ddiag) return fail(PDSSM_ERR_NULL, "scan_bwd: dbias and ddiag are required");
+    if (dy_opt && (!C_opt || g.P < 1)) return fail(PDSSM_ERR_NULL, "scan_bwd: dy_opt needs C_opt and p_out >= 1");
+    if (misaligned(h_saved, g.act) || misaligned(dh_opt, g.act) || misaligned(dy_opt, g.act) || misaligned(dbias, g.act) ||
+        misaligned(ddiag, g.diag_mode == PDSSM_DIAG_PER_DICT ? 4 : g.act) || misaligned(gsel, 4) ||
+        misaligned(dh0_opt, 4) || misaligned(h0_opt, 4) || misaligned(lam_in_opt, 4) || misaligned(C_opt, 4) ||
+        misaligned(chunk_state, 16))
+        return fail(PDSSM_ERR_ALIGN, "scan_bwd: misaligned pointer");
+    const size_t need = ws_bytes_g(g, PDSSM_OP_BWD);
+    if (!ws || ws_bytes < need) return fail(PDSSM_ERR_WORKSPACE, "scan_bwd: workspace too small (need %zu)", need);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    Bump bump(ws);
+    float* betap = bump.take<float>(cs_f_bytes(g));
+    float* mu = bump.take<float>(cs_f_bytes(g));
+    float* ebuf = g.P > 0 ? bump.take<float>(seq_f_bytes(g)) : nullptr;
+    float* dDbuf = g.diag_mode == PDSSM_DIAG_PER_DICT ? bump.take<float>(seq_f_bytes(g)) : nullptr;
+    ChunkStateView cs = cs_view(g, const_cast<void*>(chunk_state));
+    const int thr = threads_for(g.N);
+    const unsigned items = (unsigned)(g.S * g.C);
+    return with_act(g.dtype, [&](auto tv) {
+        using T = decltype(tv);
+        return with_nc(g.nc, [&](auto ncv) {
+            constexpr int NC = decltype(ncv)::value;
+            return with_pd(g.diag_mode, [&](auto pdv) -> pdssm_status {
+                constexpr bool PD = decltype(pdv)::value;
+                const T* dg = PD ? nullptr : static_cast<const T*>(diag);
+                const float* dd = PD ? static_cast<const float*>(diag) : nullptr;
+                auto run = [&](auto ev) -> pdssm_status {
+                    using TE = decltype(ev);
+                    const TE* e = nullptr;
+                    if (std::is_same<TE, float>::value && dy_opt) e = reinterpret_cast<const TE*>(ebuf);
+                    else if (dh_opt) e = reinterpret_cast<const TE*>(dh_opt);
+                    size_t smA = (size_t)2 * NC * g.N * 4;
+                    k_bwd_phaseA<T, TE, NC, PD><<<items, thr, smA, st>>>(kstar, dict_idx, dg, dd, e, betap, (int)g.H,
+                                                                         (int)g.L, (int)g.N, (int)g.K, g.tau, g.C);
+                    pdssm_status rr = cuda_check("bwd_phaseA");
+                    if (rr) return rr;
+                    k_bwd_phaseB<NC><<<(unsigned)g.S, thr, (size_t)NC * g.N * 4, st>>>(cs, betap, lam_in_opt, mu,
+                                                                                         dh0_opt, (int)g.N, g.C);
+                    if ((rr = cuda_check("bwd_phaseB"))) return rr;
+                    const int nw = thr / 32;
+                    size_t smC = (size_t)2 * NC * g.N * 4 + (size_t)64 * nw * 4;
+                    if ((rr = set_smem((const void*)k_bwd_phaseC<T, TE, NC, PD>, smC))) return rr;
+                    k_bwd_phaseC<T, TE, NC, PD><<<items, thr, smC, st>>>(
+                        kstar, dict_idx, dg, dd, static_cast<const T*>(h_saved), h0_opt, e, mu, static_cast<T*>(dbias),
+                        PD ? nullptr : static_cast<T*>(ddiag), dDbuf, gsel, (int)g.H, (int)g.L, (int)g.N, (int)g.K,
+                        g.tau, g.C);
+                    if ((rr = cuda_check("bwd_phaseC"))) return rr;
+                    if (PD) {
+                        k_bwd_reduce_dict<NC><<<(unsigned)(g.H * g.K), 256, 0, st>>>(
+                            kstar, dDbuf, static_cast<float*>(ddiag), (int)g.B, (int)g.H, (int)g.L, (int)g.N, (int)g.K);
+                        if ((rr = cuda_check("bwd_reduce_dict"))) return rr;
+                    }
+                    return PDSSM_OK;
+                };
+                if (dy_opt) {
+                    k_bwd_prepare_e<T, NC><<<(unsigned)(g.S * g.L), 128, (size_t)g.P * 4, st>>>(
+                        static_cast<const T*>(dh_opt), static_cast<const T*>(dy_opt), C_opt, ebuf, (int)g.H, (int)g.L,
+                        (int)g.N, (int)g.P);
+                    pdssm_status rr = cuda_check("bwd_prepare_e");
+                    if (rr) return rr;
+                    return run(float{});
+                }
+                return run(T{});
+            });
+        });
+    });
+}
+
+pdssm_status pdssm_segment_summary(const uint8_t* kstar, const uint16_t* dict_idx, const void* diag,
+                                   const void* bias, void* summary_out, const pdssm_dims* dims, void* ws,
+                                   size_t ws_bytes, pdssm_stream_t stream) {
+    Geo g;
+    pdssm_status r = geo_of(dims, &g);
+    if (r) return r;
+    if ((r = common_scan_checks(g, kstar, dict_idx, diag))) return r;
+    if (!bias || !summary_out) return fail(PDSSM_ERR_NULL, "segment_summary: bias and summary_out are required");
+    if (misaligned(bias, g.act) || misaligned(summary_out, 16)) return fail(PDSSM_ERR_ALIGN, "segment_summary: misaligned");
+    const size_t need = ws_bytes_g(g, PDSSM_OP_SEGMENT);
+    if (!ws || ws_bytes < need) return fail(PDSSM_ERR_WORKSPACE, "segment_summary: workspace too small (need %zu)", need);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    Bump bump(ws);
+    uint16_t* pstart = bump.take<uint16_t>((size_t)g.H * g.K * (g.N + 1) * 2);
+    uint16_t* psrc = bump.take<uint16_t>((size_t)g.H * g.K * g.N * 2);
+    void* csmem = bump.take<char>(chunk_state_bytes_g(g));
+    ChunkStateView cs = cs_view(g, csmem);
+    if ((r = launch_plan(g, dict_idx, pstart, psrc, st))) return r;
+    if ((r = fwd_three_phase(g, kstar, dict_idx, pstart, psrc, diag, bias, nullptr, cs, nullptr, nullptr, false, st)))
+        return r;
+    SummaryView sv{static_cast<char*>(summary_out), summary_block_bytes(g), npad8(g.N)};
+    return with_nc(g.nc, [&](auto ncv) {
+        constexpr int NC = decltype(ncv)::value;
+        k_fold_aggregates<NC><<<(unsigned)g.S, threads_for(g.N), (size_t)NC * g.N * 4 + g.N * 2 + 16, st>>>(
+            cs, sv, (int)g.N, g.C);
+        return cuda_check("fold_aggregates");
+    });
+}
+
+pdssm_status pdssm_compose_carry(const void* summaries, int32_t rank, int32_t G, const float* h0_opt, float* carry_out,
+                                 uint16_t* map_out_opt, const pdssm_dims* dims, pdssm_stream_t stream) {
+    Geo g;
+    pdssm_status r = geo_of(dims, &g);
+    if (r) return r;
+    if (!summaries || !carry_out) return fail(PDSSM_ERR_NULL, "compose_carry: summaries and carry_out are required");
+    if (G < 1 || rank < 0 || rank >= G) return fail(PDSSM_ERR_SHAPE, "compose_carry: need 0 <= rank < G");
+    if (misaligned(summaries, 16) || misaligned(carry_out, 4) || misaligned(h0_opt, 4) || misaligned(map_out_opt, 2))
+        return fail(PDSSM_ERR_ALIGN, "compose_carry: misaligned");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    SummaryView sv{static_cast<char*>(const_cast<void*>(summaries)), summary_block_bytes(g), npad8(g.N)};
+    return with_nc(g.nc, [&](auto ncv) {
+        constexpr int NC = decltype(ncv)::value;
+        k_compose_carry<NC><<<(unsigned)g.S, threads_for(g.N), (size_t)NC * g.N * 4 + g.N * 2 + 16, st>>>(
+            sv, rank, (int)g.S, h0_opt, carry_out, map_out_opt, (int)g.N);
+        return cuda_check("compose_carry");
+    });
+}
+
+pdssm_status pdssm_segment_summary_bwd(const uint8_t* kstar, const uint16_t* dict_idx, const void* diag,
+                                       const void* chunk_state, const void* dh_opt, const void* dy_opt,
+                                       const float* C_opt, float* beta_out, const pdssm_dims* dims, void* ws,
+                                       size_t ws_bytes, pdssm_stream_t stream) {
+    Geo g;
+    pdssm_status r = geo_of(dims, &g);
+    if (r) return r;
+    if ((r = common_scan_checks(g, kstar, dict_idx, diag))) return r;
+    if (!chunk_state || !beta_out) return fail(PDSSM_ERR_NULL, "segment_summary_bwd: chunk_state and beta_out required");
+    if (dy_opt && (!C_opt || g.P < 1)) return fail(PDSSM_ERR_NULL, "segment_summary_bwd: dy_opt needs C_opt");
+    if (misaligned(dh_opt, g.act) || misaligned(dy_opt, g.act) || misaligned(beta_out, 4) || misaligned(chunk_state, 16))
+        return fail(PDSSM_ERR_ALIGN, "segment_summary_bwd: misaligned");
+    const size_t need = ws_bytes_g(g, PDSSM_OP_SEGMENT);
+    if (!ws || ws_bytes < need) return fail(PDSSM_ERR_WORKSPACE, "segment_summary_bwd: workspace too small (need %zu)", need);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    Bump bump(ws);
+    float* betap = bump.take<float>(cs_f_bytes(g));
+    float* mu = bump.take<float>(cs_f_bytes(g));
+    float* ebuf = g.P > 0 ? bump.take<float>(seq_f_bytes(g)) : nullptr;
+    ChunkStateView cs = cs_view(g, const_cast<void*>(chunk_state));
+    const int thr = threads_for(g.N);
+    const unsigned items = (unsigned)(g.S * g.C);
+    return with_act(g.dtype, [&](auto tv) {
+        using T = decltype(tv);
+        return with_nc(g.nc, [&](auto ncv) {
+            constexpr int NC = decltype(ncv)::value;
+            return with_pd(g.diag_mode, [&](auto pdv) -> pdssm_status {
+                constexpr bool PD = decltype(pdv)::value;
+                const T* dg = PD ? nullptr : static_cast<const T*>(diag);
+                const float* dd = PD ? static_cast<const float*>(diag) : nullptr;
+                auto run = [&](auto ev) -> pdssm_status {
+                    using TE = decltype(ev);
+                    const TE* e = nullptr;
+                    if (std::is_same<TE, float>::value && dy_opt) e = reinterpret_cast<const TE*>(ebuf);
+                    else if (dh_opt) e = reinterpret_cast<const TE*>(dh_opt);
+                    k_bwd_phaseA<T, TE, NC, PD><<<items, thr, (size_t)2 * NC * g.N * 4, st>>>(
+                        kstar, dict_idx, dg, dd, e, betap, (int)g.H, (int)g.L, (int)g.N, (int)g.K, g.tau, g.C);
+                    pdssm_status rr = cuda_check("bwd_phaseA");
+                    if (rr) return rr;
+                    k_bwd_phaseB<NC><<<(unsigned)g.S, thr, (size_t)NC * g.N * 4, st>>>(cs, betap, nullptr, mu,
+                                                                                         beta_out, (int)g.N, g.C);
+                    return cuda_check("bwd_phaseB");
+                };
+                if (dy_opt) {
+                    k_bwd_prepare_e<T, NC><<<(unsigned)(g.S * g.L), 128, (size_t)g.P * 4, st>>>(
+                        static_cast<const T*>(dh_opt), static_cast<const T*>(dy_opt), C_opt, ebuf, (int)g.H, (int)g.L,
+                        (int)g.N, (int)g.P);
+                    pdssm_status rr = cuda_check("bwd_prepare_e");
+                    if (rr) return rr;
+                    return run(float{});
+                }
+                return run(T{});
+            });
+        });
+    });
+}
+
+pdssm_status pdssm_compose_lambda(const void* fwd_summaries, const float* beta_bwd, int32_t rank, int32_t G,
+                                  float* lam_out, const pdssm_dims* dims, pdssm_stream_t stream) {
+    Geo g;
+    pdssm_status r = geo_of(dims, &g);
+    if (r) return r;
+    if (!fwd_summaries || !beta_bwd || !lam_out) return fail(PDSSM_ERR_NULL, "compose_lambda: null argument");
+    if (G < 1 || rank < 0 || rank >= G) return fail(PDSSM_ERR_SHAPE, "compose_lambda: need 0 <= rank < G");
+    if (misaligned(fwd_summaries, 16) || misaligned(beta_bwd, 4) || misaligned(lam_out, 4))
+        return fail(PDSSM_ERR_ALIGN, "compose_lambda: misaligned");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    SummaryView sv{static_cast<char*>(const_cast<void*>(fwd_summaries)), summary_block_bytes(g), npad8(g.N)};
+    return with_nc(g.nc, [&](auto ncv) {
+        constexpr int NC = decltype(ncv)::value;
+        k_compose_lambda<NC><<<(unsigned)g.S, threads_for(g.N), (size_t)NC * g.N * 4, st>>>(sv, beta_bwd, rank, G,
+                                                                                           (int)g.S, lam_out, (int)g.N);
+        return cuda_check("compose_lambda");
+    });
+}
+
+}  // extern "C"

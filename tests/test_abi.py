@@ -1,0 +1,90 @@
+"""CPU-only checks of the C-ABI library: it loads, exports every symbol the
+header declares, and validates arguments synchronously (before any CUDA call,
+so no GPU is needed)."""
+import ctypes
+
+import pytest
+
+import paper_2605_19150_b200 as P
+
+
+def dims(**kw):
+    base = dict(B=2, H=3, L=100, N=16, K=4, c=2, dtype=P.F32, tau=0)
+    base.update(kw)
+    return P.make_dims(**base)
+
+
+def test_all_header_symbols_exported():
+    syms = P.header_symbols()
+    assert len(syms) >= 15
+    for s in syms:
+        assert hasattr(P.lib, s), s
+    assert P.lib.pdssm_version().startswith(b"pdssm")
+
+
+def test_status_strings():
+    for code, name in P.STATUS.items():
+        assert P.lib.pdssm_status_string(code).decode() == name
+
+
+def test_sizes_and_default_chunk():
+    d = dims(tau=7)
+    assert P.default_chunk(d) == 7
+    d = dims(tau=1000)          # tau > L is clamped to L
+    assert P.default_chunk(d) == 100
+    d = dims()
+    tau = P.default_chunk(d)
+    assert tau >= 1
+    Cch = -(-100 // tau)
+    assert P.lib.pdssm_chunk_state_bytes(ctypes.byref(d)) >= 6 * Cch * 16 * 2 + 3 * 6 * Cch * 2 * 16 * 4
+    offs = (ctypes.c_size_t * 4)()
+    assert P.lib.pdssm_chunk_state_offsets(ctypes.byref(d), offs) == 0
+    assert offs[0] == 0 and offs[1] < offs[2] < offs[3]
+    assert all(o % 256 == 0 for o in offs)
+    for op in (P.OP_FWD, P.OP_BWD, P.OP_SEGMENT):
+        assert P.workspace_bytes(d, op) > 0
+    assert P.lib.pdssm_summary_bytes(ctypes.byref(d)) == 16 * 2 + 2 * 2 * 16 * 4
+
+
+@pytest.mark.parametrize("bad,code", [
+    (dict(B=0), 2), (dict(N=0), 2), (dict(N=1025), 2), (dict(K=257), 2), (dict(c=3), 2),
+    (dict(dtype=7), 5), (dict(tau=-1), 2),
+])
+def test_invalid_dims_rejected(bad, code):
+    d = dims(**bad)
+    assert P.workspace_bytes(d, P.OP_FWD) == 0
+    st = P.lib.pdssm_scan_fwd(None, None, None, None, None, None, None, None, None, None,
+                              ctypes.byref(d), None, 0, None)
+    assert st == code
+    assert len(P.lib.pdssm_last_error()) > 0
+
+
+def test_null_and_workspace_and_alignment_checks():
+    d = dims()
+    p = ctypes.c_void_p(0x10000)     # never dereferenced: validation fails first
+    # missing required pointers
+    assert P.lib.pdssm_scan_fwd(None, p, p, p, None, None, p, None, p, None, ctypes.byref(d), p, 1 << 30, None) == 1
+    # no outputs requested
+    assert P.lib.pdssm_scan_fwd(p, p, p, p, None, None, None, None, p, None, ctypes.byref(d), p, 1 << 30, None) == 1
+    # workspace too small
+    assert P.lib.pdssm_scan_fwd(p, p, p, p, None, None, p, None, p, None, ctypes.byref(d), p, 1, None) == 6
+    # misaligned bias
+    q = ctypes.c_void_p(0x10001)
+    assert P.lib.pdssm_scan_fwd(p, p, p, q, None, None, p, None, p, None, ctypes.byref(d), p, 1 << 30, None) == 4
+    # readout without C
+    assert P.lib.pdssm_scan_fwd(p, p, p, p, None, None, None, p, p, None, ctypes.byref(d), p, 1 << 30, None) == 1
+    # backward requires h_saved
+    assert P.lib.pdssm_scan_bwd(p, p, p, None, None, p, None, None, None, None, p, p, None, None,
+                                ctypes.byref(d), p, 1 << 30, None) == 1
+    # select requires d_in >= 1
+    assert P.lib.pdssm_select(p, p, None, p, None, None, ctypes.byref(d), p, 1 << 30, None) == 2
+    ds = dims(d_in=8)
+    assert P.lib.pdssm_select(p, p, None, p, p, None, ctypes.byref(ds), p, 1 << 30, None) == 1   # P needs dict
+    # compose: rank out of range
+    assert P.lib.pdssm_compose_carry(p, 4, 4, None, p, None, ctypes.byref(d), None) == 2
+    assert P.lib.pdssm_compose_lambda(p, p, -1, 4, p, ctypes.byref(d), None) == 2
+    assert P.lib.pdssm_sparsify(None, p, ctypes.byref(d), None) == 1
+
+
+def test_dims_struct_layout():
+    assert ctypes.sizeof(P.Dims) == 80

@@ -1,0 +1,236 @@
+"""GPU parity of the scan path (a4-a9) through the C ABI against the float64
+oracle.  Bars (BASELINE.json north_star): index maps and
+integer outputs bit-exact; floats within max|gpu - oracle| / max|oracle|
+<= 1e-4 (fp32) / 2e-2 (bf16) per tensor."""
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = {"f32": 1e-4, "bf16": 2e-2}
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2605_19150_b200 as mod
+    return mod
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.complex128 if np.iscomplexobj(a) or np.iscomplexobj(b) else np.float64)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30)) if np.size(b) else 0.0
+
+
+def to_dev(inp, bf16):
+    out = {}
+    for k, v in inp.items():
+        t = torch.from_numpy(np.ascontiguousarray(v)).cuda()
+        if k == "dict_idx":
+            t = t.to(torch.int16)
+        elif k in ("diag_step", "bias", "dh", "diag") and bf16 and v.dtype == np.float32:
+            t = t.to(torch.bfloat16)
+        out[k] = t
+    return out
+
+
+def cpx(t):
+    return O.planes_to_complex(t.float().cpu().numpy())
+
+
+def run_case(P, B, H, L, N, K, c, tau, bf16=False, per_dict=False, h0=True, seed=0, sticky=0.0):
+    inp = synth.scan_inputs(B, H, L, N, K, c, seed=seed, h0=h0, dh=True, per_dict=per_dict, bf16=bf16, sticky=sticky)
+    d = to_dev(inp, bf16)
+    if per_dict:
+        d["diag"] = torch.from_numpy(inp["diag"]).cuda()        # PER_DICT diag stays f32
+    f = P.scan_fwd(d["kstar"], d["dict_idx"], d["diag"], d["bias"], h0=d.get("h0"), tau=tau, per_dict=per_dict,
+                   export_maps=True)
+    db, dD, g, dh0 = P.scan_bwd(d["kstar"], d["dict_idx"], d["diag"], f["h"], f["chunk_state"], f["dims"],
+                                dh=d["dh"], h0=d.get("h0"))
+    torch.cuda.synchronize()
+    Pm = O.gather_P(inp["dict_idx"], inp["kstar"])
+    Dz = O.planes_to_complex(inp["diag"])
+    if per_dict:
+        Dz = O.gather_D_per_dict(Dz, inp["kstar"])
+    bz = O.planes_to_complex(inp["bias"])
+    h0z = O.planes_to_complex(inp["h0"]) if h0 else None
+    ch = O.scan_chunked(Pm, Dz, bz, f["tau"], h0z)
+    e = O.planes_to_complex(inp["dh"])
+    db_r, dD_r, g_r, dh0_r = O.scan_backward(Pm, Dz, ch["h"], e, h0z)
+    return inp, f, (db, dD, g, dh0), ch, (db_r, dD_r, g_r, dh0_r), Pm, Dz
+
+
+CASES = [
+    # B, H, L, N, K, c, tau
+    (1, 1, 64, 8, 4, 2, 16),      # config 1 (tiny)
+    (1, 1, 64, 8, 4, 1, 7),
+    (2, 3, 65, 5, 3, 2, 64),
+    (1, 2, 257, 32, 8, 2, 128),   # ragged last chunk
+    (2, 1, 63, 64, 16, 1, 1),
+    (1, 1, 1, 16, 4, 2, 0),       # L = 1
+    (1, 2, 100, 120, 48, 2, 32),
+    (2, 2, 300, 128, 32, 2, 0),   # headline N, default tau
+    (1, 1, 50, 2, 2, 1, 1000),    # tau >= L
+    (1, 1, 40, 1, 1, 2, 8),       # N = 1, K = 1
+    (1, 1, 33, 200, 5, 1, 16),    # N not a multiple of 32
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[str(c) for c in CASES])
+@pytest.mark.parametrize("bf16", [False, True], ids=["f32", "bf16"])
+def test_scan_fwd_bwd_parity(P, case, bf16):
+    B, H, L, N, K, c, tau = case
+    inp, f, got, ch, ref, Pm, Dz = run_case(P, B, H, L, N, K, c, tau, bf16=bf16, seed=hash(case) % 1000)
+    tol = TOL["bf16" if bf16 else "f32"]
+    assert rel(cpx(f["h"]), ch["h"]) <= tol
+    # integer maps: bit-exact
+    assert np.array_equal(f["maps"].cpu().numpy().astype(np.int64), ch["maps"])
+    pi, d_bar, beta_bar, carry = P.chunk_state_views(f["chunk_state"], f["dims"])
+    assert np.array_equal(pi.cpu().numpy().astype(np.int64), ch["pi_bar"])
+    assert rel(O.planes_to_complex(d_bar.cpu().numpy()), ch["d_bar"]) <= 1e-4
+    assert rel(O.planes_to_complex(beta_bar.cpu().numpy()), ch["beta_bar"]) <= 1e-4
+    assert rel(O.planes_to_complex(carry.cpu().numpy()), ch["carries"]) <= 1e-4
+    db, dD, g, dh0 = got
+    db_r, dD_r, g_r, dh0_r = ref
+    # the backward consumes the GPU's own (rounded) h; compare against the oracle's
+    assert rel(cpx(db), db_r) <= tol
+    assert rel(cpx(dD), dD_r) <= (tol if not bf16 else 3e-2)
+    assert rel(g.cpu().numpy(), g_r) <= (tol if not bf16 else 3e-2)
+    assert rel(O.planes_to_complex(dh0.cpu().numpy()), dh0_r) <= tol
+
+
+def test_scan_per_dict_and_no_h0(P):
+    inp, f, got, ch, ref, Pm, Dz = run_case(P, 2, 2, 90, 16, 5, 2, 16, per_dict=True, h0=False, seed=7)
+    assert rel(cpx(f["h"]), ch["h"]) <= 1e-4
+    db, dD, g, dh0 = got
+    db_r, dD_r, g_r, dh0_r = ref
+    assert rel(cpx(db), db_r) <= 1e-4
+    # PER_DICT ddiag = sum over steps selecting k of dD_t
+    kst = inp["kstar"]
+    H, K = 2, 5
+    want = np.zeros((H, K, 16), np.complex128)
+    for h in range(H):
+        for k in range(K):
+            sel = kst[:, h, :] == k
+            want[h, k] = dD_r[:, h][sel].sum(axis=0)
+    assert rel(O.planes_to_complex(dD.cpu().numpy()), want) <= 1e-4
+    assert rel(g.cpu().numpy(), g_r) <= 1e-4
+
+
+def test_determinism_bitwise(P):
+    args = (2, 2, 200, 64, 16, 2, 32)
+    _, f1, g1, *_ = run_case(P, *args, seed=3)
+    _, f2, g2, *_ = run_case(P, *args, seed=3)
+    assert torch.equal(f1["h"], f2["h"]) and torch.equal(f1["chunk_state"], f2["chunk_state"])
+    for a, b in zip(g1, g2):
+        assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("tau", [1, 7, 64, 128])
+def test_tau_invariance_of_final_outputs(P, tau):
+    _, f, got, ch, ref, *_ = run_case(P, 1, 2, 257, 32, 8, 2, tau, seed=11)
+    _, f0, got0, *_ = run_case(P, 1, 2, 257, 32, 8, 2, 257, seed=11)
+    assert torch.equal(f["maps"][:, :, -1], f0["maps"][:, :, -1])
+    assert rel(cpx(f["h"]), cpx(f0["h"])) <= 1e-4
+    assert rel(cpx(got[0]), cpx(got0[0])) <= 1e-4
+
+
+def test_fsa_emulation_exact(P):
+    """Prop. 1 (App. D): states exactly one-hot, on the GPU."""
+    from oracle import fsa
+    import itertools
+    for make in (fsa.parity, fsa.cyclic_z5, fsa.cycle_nav, fsa.even_pairs, fsa.mod_arith):
+        A = make()
+        dict_idx, dg, h0, C = A.compile()
+        L = 6 if A.K <= 5 else 4
+        words = np.array(list(itertools.product(range(A.K), repeat=L)), dtype=np.uint8)
+        Bn = len(words)
+        kst = torch.from_numpy(words[:, None, :].copy()).cuda()
+        di = torch.from_numpy(dict_idx.astype(np.int16)).cuda()
+        diag = torch.ones((1, A.K, 1, A.N), dtype=torch.float32, device="cuda")
+        bias = torch.zeros((Bn, 1, L, 1, A.N), dtype=torch.float32, device="cuda")
+        h0t = torch.from_numpy(np.tile(h0, (Bn, 1, 1, 1)).astype(np.float32)).cuda()
+        for tau in (1, 2, 3, L):
+            f = P.scan_fwd(kst, di, diag, bias, h0=h0t, tau=tau, per_dict=True, export_maps=True)
+            h = f["h"].cpu().numpy()[:, 0, :, 0, :]
+            runs = np.array([A.run(list(w)) for w in words])
+            onehot = np.zeros((Bn, L, A.N), np.float32)
+            np.put_along_axis(onehot, runs[:, :, None], 1.0, axis=2)
+            assert np.array_equal(h, onehot), (A.name, tau)
+            final_map = f["maps"].cpu().numpy()[:, 0, -1].astype(np.int64)
+            for b in range(0, Bn, max(1, Bn // 50)):
+                q = A.q_init
+                assert final_map[b, q] == runs[b, -1]
+
+
+def test_s5_word_problem_exact(P):
+    """config 5 structure at reduced L: exact permuted arange states and exact maps."""
+    dict_idx, perms5, blocks = synth.s5_dictionary(64, 16, seed=5000)
+    B, H, L = 2, 2, 4096
+    k = synth.kstar(B, H, L, 16, seed=5001)
+    di = torch.from_numpy(np.tile(dict_idx[None], (H, 1, 1)).astype(np.int16)).cuda()
+    kst = torch.from_numpy(k).cuda()
+    diag = torch.ones((H, 16, 1, 64), dtype=torch.float32, device="cuda")
+    bias = torch.zeros((B, H, L, 1, 64), dtype=torch.float32, device="cuda")
+    h0 = torch.arange(64, dtype=torch.float32, device="cuda").view(1, 1, 1, 64).repeat(B, H, 1, 1).contiguous()
+    f = P.scan_fwd(kst, di, diag, bias, h0=h0, tau=64, per_dict=True, export_maps=True)
+    Pm = O.gather_P(np.tile(dict_idx[None], (H, 1, 1)), k)
+    Pi, _ = O.prefix_maps(Pm, np.ones(Pm.shape))
+    maps = f["maps"].cpu().numpy().astype(np.int64)
+    for c in range(1, maps.shape[2] - 1):
+        assert np.array_equal(maps[:, :, c], Pi[:, :, c * 64 - 1])
+    assert np.array_equal(maps[:, :, -1], Pi[:, :, -1])
+    hlast = f["h"].cpu().numpy()[:, :, -1, 0]
+    expect = np.zeros((B, H, 64))
+    np.put_along_axis(expect, Pi[:, :, -1], np.arange(64.0)[None, None].repeat(B, 0).repeat(H, 1), axis=2)
+    assert np.array_equal(hlast, expect)
+
+
+def test_readout_fused_and_dy_backward(P):
+    B, H, L, N, K, c, Pp = 2, 2, 70, 16, 4, 2, 8
+    inp = synth.scan_inputs(B, H, L, N, K, c, seed=21, h0=True)
+    Cw = synth.readout_C(H, Pp, N, c, seed=21)
+    d = to_dev(inp, False)
+    Ct = torch.from_numpy(Cw).cuda()
+    f = P.scan_fwd(d["kstar"], d["dict_idx"], d["diag"], d["bias"], h0=d["h0"], C=Ct, tau=16, want_y=True)
+    rng = np.random.default_rng(0)
+    dy = rng.standard_normal((B, L, H, Pp)).astype(np.float32)
+    db, dD, g, dh0 = P.scan_bwd(d["kstar"], d["dict_idx"], d["diag"], f["h"], f["chunk_state"], f["dims"],
+                                dy=torch.from_numpy(dy).cuda(), C=Ct, h0=d["h0"])
+    torch.cuda.synchronize()
+    Pm = O.gather_P(inp["dict_idx"], inp["kstar"])
+    Dz, bz, h0z = (O.planes_to_complex(inp[k]) for k in ("diag", "bias", "h0"))
+    h = O.scan_forward(Pm, Dz, bz, h0z)
+    Cz = O.planes_to_complex(np.moveaxis(Cw, 1, -2))          # [H][P][N] complex
+    y = O.readout(h, Cz)
+    assert rel(f["y"].cpu().numpy(), y) <= 1e-4
+    e = O.readout_adjoint(dy, Cz)
+    db_r, dD_r, g_r, dh0_r = O.scan_backward(Pm, Dz, h, e, h0z)
+    assert rel(cpx(db), db_r) <= 1e-4
+    assert rel(cpx(dD), dD_r) <= 1e-4
+    assert rel(g.cpu().numpy(), g_r) <= 1e-4
+
+
+def test_check_finite_reports(P):
+    B, H, L, N, K, c = 1, 1, 20, 8, 4, 1
+    inp = synth.scan_inputs(B, H, L, N, K, c, seed=2)
+    d = to_dev(inp, False)
+    P.check_device()
+    bias = d["bias"].clone()
+    bias[0, 0, 5, 0, 3] = float("nan")
+    P.scan_fwd(d["kstar"], d["dict_idx"], d["diag"], bias, tau=8, check_finite=True)
+    with pytest.raises(P.PdssmError) as ei:
+        P.check_device()
+    assert ei.value.status == 7
+    k = d["kstar"].clone()
+    k[0, 0, 3] = 200
+    P.scan_fwd(k, d["dict_idx"], d["diag"], d["bias"], tau=8, check_finite=True)
+    with pytest.raises(P.PdssmError) as ei:
+        P.check_device()
+    assert ei.value.status == 3
+    P.check_device()      # cleared

@@ -70,8 +70,9 @@ def test_select_integer_exact_and_ties():
 
 
 def test_argmax_nan_rule():
-    v = np.array([[np.nan, 1.0, 1.0], [np.nan, np.nan, np.nan], [-np.inf, -np.inf, 0.0]])
-    assert list(O.argmax_smallest(v)) == [1, 0, 2]
+    v = np.array([[np.nan, 1.0, 1.0], [np.nan, np.nan, np.nan], [-np.inf, -np.inf, 0.0],
+                  [-np.inf, -np.inf, -np.inf], [np.nan, -np.inf, 2.0]])
+    assert list(O.argmax_smallest(v)) == [1, 0, 2, 0, 2]
 
 
 def test_gather_P_definition():
