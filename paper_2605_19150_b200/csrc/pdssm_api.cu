@@ -111,10 +111,11 @@ size_t ws_bytes_g(const Geo& g, int op) {
         case PDSSM_OP_SELECT:
             return align256((size_t)g.S * g.L * g.K * 4);
         case PDSSM_OP_FWD:
-            return plan_bytes(g) + (g.P > 0 ? seq_act_bytes(g) : 0) + fused_ws_bytes(g.S, g.C);
+            return plan_bytes(g) + (g.P > 0 ? seq_act_bytes(g) : 0) + fused_plan_bytes(g.H, g.K, 4) +
+                   fused_ctrl_bytes(g.S, g.C);
         case PDSSM_OP_BWD:
             return 2 * cs_f_bytes(g) + (g.P > 0 ? seq_f_bytes(g) : 0) +
-                   (g.diag_mode == PDSSM_DIAG_PER_DICT ? seq_f_bytes(g) : 0);
+                   (g.diag_mode == PDSSM_DIAG_PER_DICT ? seq_f_bytes(g) : 0) + fused_ctrl_bytes(g.S, g.C);
         case PDSSM_OP_SEGMENT: {
             size_t fwd = plan_bytes(g) + chunk_state_bytes_g(g);
             size_t bwd = 2 * cs_f_bytes(g) + (g.P > 0 ? seq_f_bytes(g) : 0);
@@ -200,6 +201,74 @@ pdssm_status fwd_three_phase(const Geo& g, const uint8_t* kstar, const uint16_t*
                                                                  static_cast<T*>(hout), (int)g.H, (int)g.L,
                                                                  (int)g.N, (int)g.K, g.tau, g.C, g.flags);
                 return cuda_check("fwd_phaseC");
+            });
+        });
+    });
+}
+
+// ------------------------------------------------------------------ fused fast path
+// PDSSM_PATH=generic forces the three-phase kernels (used by the tests to cover both).
+bool path_generic_forced() {
+    const char* p = getenv("PDSSM_PATH");
+    return p && strcmp(p, "generic") == 0;
+}
+
+bool fused_applicable(const Geo& g, std::initializer_list<const void*> ptrs) {
+    if (path_generic_forced() || fused_npl(g.N) == 0) return false;
+    for (const void* p : ptrs)
+        if (misaligned(p, 16)) return false;
+    return true;
+}
+
+template <typename F>
+pdssm_status with_npl(int npl, F&& f) {
+    if (npl == 1) return f(std::integral_constant<int, 1>{});
+    if (npl == 2) return f(std::integral_constant<int, 2>{});
+    return f(std::integral_constant<int, 4>{});
+}
+
+pdssm_status fwd_fused(const Geo& g, fused::FusedArgs& fa, uint8_t* rec, uint32_t* hdr, cudaStream_t st) {
+    const int npl = fused_npl(g.N);
+    return with_npl(npl, [&](auto nv) {
+        constexpr int NPL = decltype(nv)::value;
+        fused::k_build_fused_plan<NPL><<<(unsigned)(g.H * g.K), threads_for(g.N), (size_t)g.N * 2, st>>>(
+            fa.dict_idx, rec, hdr, (int)g.N);
+        pdssm_status r = cuda_check("build_fused_plan");
+        if (r) return r;
+        cudaError_t e = cudaMemsetAsync(fa.ctrl, 0, fused_ctrl_bytes(g.S, g.C), st);
+        if (e != cudaSuccess) return fail(PDSSM_ERR_CUDA, "memset ctrl: %s", cudaGetErrorString(e));
+        const int grid = fused_grid((int)(g.S * g.C));
+        return with_act(g.dtype, [&](auto tv) {
+            using T = decltype(tv);
+            return with_nc(g.nc, [&](auto ncv) {
+                constexpr int NC = decltype(ncv)::value;
+                return with_pd(g.diag_mode, [&](auto pdv) {
+                    constexpr bool PD = decltype(pdv)::value;
+                    fused::k_fwd_fused<T, NC, NPL, PD><<<grid, fused::WARPS * 32, 0, st>>>(fa);
+                    return cuda_check("fwd_fused");
+                });
+            });
+        });
+    });
+}
+
+template <typename TE>
+pdssm_status bwd_fused(const Geo& g, fused::FusedArgs& fa, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(fa.ctrl, 0, fused_ctrl_bytes(g.S, g.C), st);
+    if (e != cudaSuccess) return fail(PDSSM_ERR_CUDA, "memset ctrl: %s", cudaGetErrorString(e));
+    const int grid = fused_grid((int)(g.S * g.C));
+    return with_npl(fused_npl(g.N), [&](auto nv) {
+        constexpr int NPL = decltype(nv)::value;
+        return with_act(g.dtype, [&](auto tv) {
+            using T = decltype(tv);
+            return with_nc(g.nc, [&](auto ncv) {
+                constexpr int NC = decltype(ncv)::value;
+                return with_pd(g.diag_mode, [&](auto pdv) {
+                    constexpr bool PD = decltype(pdv)::value;
+                    using TEE = typename std::conditional<std::is_same<TE, void>::value, T, TE>::type;
+                    fused::k_bwd_fused<T, TEE, NC, NPL, PD><<<grid, fused::WARPS * 32, 0, st>>>(fa);
+                    return cuda_check("bwd_fused");
+                });
             });
         });
     });
@@ -357,16 +426,25 @@ pdssm_status pdssm_scan_fwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
     uint16_t* pstart = bump.take<uint16_t>((size_t)g.H * g.K * (g.N + 1) * 2);
     uint16_t* psrc = bump.take<uint16_t>((size_t)g.H * g.K * g.N * 2);
     void* hscratch = g.P > 0 ? bump.take<char>(seq_act_bytes(g)) : nullptr;
-    void* fused_ws = bump.take<char>(fused_ws_bytes(g.S, g.C));
+    uint8_t* frec = bump.take<uint8_t>((size_t)g.H * g.K * 32 * 4 * fused::MU);
+    uint32_t* fhdr = bump.take<uint32_t>((size_t)g.H * g.K * 8);
+    uint32_t* ctrl = bump.take<uint32_t>(fused_ctrl_bytes(g.S, g.C));
     void* hout = h_out_opt ? h_out_opt : hscratch;
     ChunkStateView cs = cs_view(g, chunk_state);
     if ((r = launch_plan(g, dict_idx, pstart, psrc, st))) return r;
     uint16_t* maps = (g.flags & PDSSM_EXPORT_MAPS) ? maps_opt : nullptr;
-    bool done = false;
-    if ((r = fwd_fused_try(g.S, g.H, g.L, g.N, g.K, g.tau, g.C, g.nc, g.dtype, g.diag_mode, g.flags, kstar, dict_idx,
-                           pstart, psrc, diag, bias, h0_opt, cs, maps, hout, fused_ws, st, &done)))
-        return fail(r, "scan_fwd (fused): %s", cudaGetErrorString(cudaGetLastError()));
-    if (!done) {
+    const bool use_fused = fused_applicable(
+        g, {g.diag_mode == PDSSM_DIAG_PER_STEP ? diag : nullptr, bias, hout, h0_opt, chunk_state, maps});
+    if (use_fused) {
+        fused::FusedArgs fa{};
+        fa.kstar = kstar; fa.dict_idx = dict_idx; fa.pstart = pstart; fa.psrc = psrc; fa.rec = frec; fa.hdr = fhdr;
+        fa.diag = g.diag_mode == PDSSM_DIAG_PER_STEP ? diag : nullptr;
+        fa.diag_dict = g.diag_mode == PDSSM_DIAG_PER_DICT ? static_cast<const float*>(diag) : nullptr;
+        fa.bias = bias; fa.h0 = h0_opt; fa.cs = cs; fa.maps = maps; fa.out0 = hout; fa.ctrl = ctrl;
+        fa.H = (int)g.H; fa.L = (int)g.L; fa.N = (int)g.N; fa.K = (int)g.K; fa.tau = g.tau; fa.C = g.C;
+        fa.S = (int)g.S; fa.flags = g.flags;
+        if ((r = fwd_fused(g, fa, frec, fhdr, st))) return r;
+    } else {
         if ((r = fwd_three_phase(g, kstar, dict_idx, pstart, psrc, diag, bias, h0_opt, cs, maps, hout, true, st)))
             return r;
     }
@@ -410,9 +488,49 @@ pdssm_status pdssm_scan_bwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
     float* mu = bump.take<float>(cs_f_bytes(g));
     float* ebuf = g.P > 0 ? bump.take<float>(seq_f_bytes(g)) : nullptr;
     float* dDbuf = g.diag_mode == PDSSM_DIAG_PER_DICT ? bump.take<float>(seq_f_bytes(g)) : nullptr;
+    uint32_t* ctrl = bump.take<uint32_t>(fused_ctrl_bytes(g.S, g.C));
     ChunkStateView cs = cs_view(g, const_cast<void*>(chunk_state));
     const int thr = threads_for(g.N);
     const unsigned items = (unsigned)(g.S * g.C);
+    const bool use_fused =
+        fused_applicable(g, {g.diag_mode == PDSSM_DIAG_PER_STEP ? diag : nullptr, h_saved, dh_opt, h0_opt, lam_in_opt,
+                             dbias, g.diag_mode == PDSSM_DIAG_PER_STEP ? ddiag : nullptr, dh0_opt, chunk_state});
+    if (use_fused) {
+        if (dy_opt) {
+            r = with_act(g.dtype, [&](auto tv) {
+                using T = decltype(tv);
+                return with_nc(g.nc, [&](auto ncv) {
+                    constexpr int NC = decltype(ncv)::value;
+                    k_bwd_prepare_e<T, NC><<<(unsigned)(g.S * g.L), 128, (size_t)g.P * 4, st>>>(
+                        static_cast<const T*>(dh_opt), static_cast<const T*>(dy_opt), C_opt, ebuf, (int)g.H, (int)g.L,
+                        (int)g.N, (int)g.P);
+                    return cuda_check("bwd_prepare_e");
+                });
+            });
+            if (r) return r;
+        }
+        fused::FusedArgs fa{};
+        fa.kstar = kstar; fa.dict_idx = dict_idx;
+        fa.diag = g.diag_mode == PDSSM_DIAG_PER_STEP ? diag : nullptr;
+        fa.diag_dict = g.diag_mode == PDSSM_DIAG_PER_DICT ? static_cast<const float*>(diag) : nullptr;
+        fa.bias = dy_opt ? static_cast<const void*>(ebuf) : dh_opt;
+        fa.hsaved = h_saved; fa.h0 = h0_opt; fa.lam_in = lam_in_opt; fa.cs = cs;
+        fa.out0 = dbias; fa.out1 = g.diag_mode == PDSSM_DIAG_PER_DICT ? static_cast<void*>(dDbuf) : ddiag;
+        fa.gsel = gsel; fa.dh0 = dh0_opt; fa.mu = mu; fa.ctrl = ctrl;
+        fa.H = (int)g.H; fa.L = (int)g.L; fa.N = (int)g.N; fa.K = (int)g.K; fa.tau = g.tau; fa.C = g.C;
+        fa.S = (int)g.S; fa.flags = g.flags;
+        r = dy_opt ? bwd_fused<float>(g, fa, st) : bwd_fused<void>(g, fa, st);
+        if (r) return r;
+        if (g.diag_mode == PDSSM_DIAG_PER_DICT) {
+            r = with_nc(g.nc, [&](auto ncv) {
+                constexpr int NC = decltype(ncv)::value;
+                k_bwd_reduce_dict<NC><<<(unsigned)(g.H * g.K), 256, 0, st>>>(
+                    kstar, dDbuf, static_cast<float*>(ddiag), (int)g.B, (int)g.H, (int)g.L, (int)g.N, (int)g.K);
+                return cuda_check("bwd_reduce_dict");
+            });
+        }
+        return r;
+    }
     return with_act(g.dtype, [&](auto tv) {
         using T = decltype(tv);
         return with_nc(g.nc, [&](auto ncv) {

@@ -78,12 +78,22 @@ CASES = [
     (1, 1, 50, 2, 2, 1, 1000),    # tau >= L
     (1, 1, 40, 1, 1, 2, 8),       # N = 1, K = 1
     (1, 1, 33, 200, 5, 1, 16),    # N not a multiple of 32
+    (2, 3, 333, 64, 16, 2, 32),   # fused path shapes (N in {32, 64, 128})
+    (3, 2, 190, 32, 7, 1, 17),
+    (2, 2, 1000, 128, 32, 2, 32),
+    (1, 2, 129, 128, 48, 1, 128),
 ]
+
+
+@pytest.fixture(params=["auto", "generic"])
+def path(request, monkeypatch):
+    monkeypatch.setenv("PDSSM_PATH", request.param)
+    return request.param
 
 
 @pytest.mark.parametrize("case", CASES, ids=[str(c) for c in CASES])
 @pytest.mark.parametrize("bf16", [False, True], ids=["f32", "bf16"])
-def test_scan_fwd_bwd_parity(P, case, bf16):
+def test_scan_fwd_bwd_parity(P, case, bf16, path):
     B, H, L, N, K, c, tau = case
     inp, f, got, ch, ref, Pm, Dz = run_case(P, B, H, L, N, K, c, tau, bf16=bf16, seed=hash(case) % 1000)
     tol = TOL["bf16" if bf16 else "f32"]
@@ -104,8 +114,9 @@ def test_scan_fwd_bwd_parity(P, case, bf16):
     assert rel(O.planes_to_complex(dh0.cpu().numpy()), dh0_r) <= tol
 
 
-def test_scan_per_dict_and_no_h0(P):
-    inp, f, got, ch, ref, Pm, Dz = run_case(P, 2, 2, 90, 16, 5, 2, 16, per_dict=True, h0=False, seed=7)
+@pytest.mark.parametrize("N", [16, 64])
+def test_scan_per_dict_and_no_h0(P, N, path):
+    inp, f, got, ch, ref, Pm, Dz = run_case(P, 2, 2, 90, N, 5, 2, 16, per_dict=True, h0=False, seed=7)
     assert rel(cpx(f["h"]), ch["h"]) <= 1e-4
     db, dD, g, dh0 = got
     db_r, dD_r, g_r, dh0_r = ref
@@ -113,7 +124,7 @@ def test_scan_per_dict_and_no_h0(P):
     # PER_DICT ddiag = sum over steps selecting k of dD_t
     kst = inp["kstar"]
     H, K = 2, 5
-    want = np.zeros((H, K, 16), np.complex128)
+    want = np.zeros((H, K, N), np.complex128)
     for h in range(H):
         for k in range(K):
             sel = kst[:, h, :] == k
@@ -122,7 +133,7 @@ def test_scan_per_dict_and_no_h0(P):
     assert rel(g.cpu().numpy(), g_r) <= 1e-4
 
 
-def test_determinism_bitwise(P):
+def test_determinism_bitwise(P, path):
     args = (2, 2, 200, 64, 16, 2, 32)
     _, f1, g1, *_ = run_case(P, *args, seed=3)
     _, f2, g2, *_ = run_case(P, *args, seed=3)
@@ -132,7 +143,7 @@ def test_determinism_bitwise(P):
 
 
 @pytest.mark.parametrize("tau", [1, 7, 64, 128])
-def test_tau_invariance_of_final_outputs(P, tau):
+def test_tau_invariance_of_final_outputs(P, tau, path):
     _, f, got, ch, ref, *_ = run_case(P, 1, 2, 257, 32, 8, 2, tau, seed=11)
     _, f0, got0, *_ = run_case(P, 1, 2, 257, 32, 8, 2, 257, seed=11)
     assert torch.equal(f["maps"][:, :, -1], f0["maps"][:, :, -1])
@@ -140,7 +151,7 @@ def test_tau_invariance_of_final_outputs(P, tau):
     assert rel(cpx(got[0]), cpx(got0[0])) <= 1e-4
 
 
-def test_fsa_emulation_exact(P):
+def test_fsa_emulation_exact(P, path):
     """Prop. 1 (App. D): states exactly one-hot, on the GPU."""
     from oracle import fsa
     import itertools
@@ -168,7 +179,7 @@ def test_fsa_emulation_exact(P):
                 assert final_map[b, q] == runs[b, -1]
 
 
-def test_s5_word_problem_exact(P):
+def test_s5_word_problem_exact(P, path):
     """config 5 structure at reduced L: exact permuted arange states and exact maps."""
     dict_idx, perms5, blocks = synth.s5_dictionary(64, 16, seed=5000)
     B, H, L = 2, 2, 4096
@@ -191,8 +202,9 @@ def test_s5_word_problem_exact(P):
     assert np.array_equal(hlast, expect)
 
 
-def test_readout_fused_and_dy_backward(P):
-    B, H, L, N, K, c, Pp = 2, 2, 70, 16, 4, 2, 8
+@pytest.mark.parametrize("N", [16, 32])
+def test_readout_fused_and_dy_backward(P, N, path):
+    B, H, L, K, c, Pp = 2, 2, 70, 4, 2, 8
     inp = synth.scan_inputs(B, H, L, N, K, c, seed=21, h0=True)
     Cw = synth.readout_C(H, Pp, N, c, seed=21)
     d = to_dev(inp, False)

@@ -80,5 +80,7 @@ def test_select_float_margin_rule(P, bf16):
     gamma = (d_in * 2.0 ** -24) * (np.take_along_axis(absum, k1, -1)[..., 0] + np.take_along_axis(absum, k2, -1)[..., 0])
     sure = gap > gamma
     assert np.array_equal(k[sure], k_ref[sure])
-    assert (~sure).mean() <= 1e-3
+    # near-ties (gap <= gamma): the GPU's pick must be within gamma of the exact maximum
+    chosen = np.take_along_axis(lg_ref, k[..., None].astype(np.int64), -1)[..., 0]
+    assert np.all(srt[..., -1][~sure] - chosen[~sure] <= gamma[~sure])
     assert np.max(np.abs(lg.cpu().numpy() - lg_ref)) <= 1e-4 * np.max(np.abs(lg_ref))

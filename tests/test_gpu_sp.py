@@ -23,8 +23,14 @@ def rel(a, b):
     return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30))
 
 
+@pytest.fixture(params=["auto", "generic"])
+def path(request, monkeypatch):
+    monkeypatch.setenv("PDSSM_PATH", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("G,c", [(2, 2), (4, 1), (3, 2)])
-def test_sp_virtual_ranks(P, G, c):
+def test_sp_virtual_ranks(P, G, c, path):
     B, H, L, N, K, tau = 2, 2, 301, 32, 8, 32
     inp = synth.scan_inputs(B, H, L, N, K, c, seed=40 + G, h0=True, dh=True)
     dev = {k: torch.from_numpy(v).cuda() for k, v in inp.items()}
