@@ -2,20 +2,26 @@
 // pdssm_scan_bwd).  Algorithm 1 re-blocked for B200:
 //
 //  * one WARP per (sequence, chunk) item; lane l owns the NPL = N/32 contiguous
-//    states [l*NPL, l*NPL+NPL) so every HBM access is a coalesced 16-byte
-//    vector per lane and intra-step exchange needs only __syncwarp;
+//    states [l*NPL, l*NPL+NPL), so all own-state traffic is 16-byte vectors and
+//    the intra-step exchange needs only __syncwarp;
+//  * every per-step input row (D_t, b_t or e_{t-1}, h_{t-1}, the selected index
+//    row P_{k*_t}, the preimage records and header of entry k*_t) is streamed
+//    into a per-warp shared-memory ring by 1-D TMA bulk copies
+//    (cp.async.bulk + mbarrier complete_tx), PF steps ahead of use, so a step
+//    never waits on a global load;
 //  * Phase A (aggregate), the carry hand-off and Phase C (replay) run in ONE
 //    launch: a warp finishes Phase A, waits for its predecessor's carry
-//    (chained look-back over per-(sequence, chunk) flags, dynamic tickets in
+//    (chained look-back over per-(sequence, chunk) flags; dynamic tickets in
 //    chunk-major order guarantee forward progress), publishes its own carry,
-//    then replays the chunk.  The replay re-reads D_t / b_t while they are
-//    still L2-resident (measured 18 TB/s L2 vs 6.9 TB/s HBM read, tools/l2bw.cu),
-//    so HBM sees each input once: the algorithmic byte count of SURVEY §8(d);
-//  * the scatter (A_t v)[i] = sum_{j : P_t[j] = i} D_t[j] v[j] runs as a
-//    gather over a per-dictionary-entry, per-lane padded preimage list
-//    ("fused plan", built once per call, MU sources per target inline, longer
-//    preimages fall back to the CSR plan) -- deterministic, no float atomics;
-//  * the backward is the transposed scan (pure gather) with the same
+//    then replays the chunk.  The ring runs over the concatenated Phase A /
+//    Phase C step list, so the replay's re-read (L2-resident: measured 18 TB/s
+//    L2 vs 6.9 TB/s HBM, tools/l2bw.cu) is in flight during the carry wait, and
+//    HBM sees each input once -- the algorithmic byte count of SURVEY §8(d);
+//  * the scatter (A_t v)[i] = sum_{j : P_t[j] = i} D_t[j] v[j] is a gather over
+//    a per-dictionary-entry, per-lane padded preimage list ("fused plan", MU
+//    inline sources per target, longer preimages fall back to the CSR plan):
+//    deterministic, no float atomics;
+//  * the backward is the transposed scan (a pure gather) with the same
 //    structure in reverse chunk order, reusing the forward (pi_bar, d_bar).
 #pragma once
 #include <type_traits>
@@ -25,8 +31,10 @@
 namespace pdssm {
 namespace fused {
 
-constexpr int WARPS = 4;          // warps (= concurrent items) per CTA
-constexpr int MU = 6;             // inline preimage capacity per target
+constexpr int MU = 6;         // inline preimage capacity per target
+constexpr int TAUMAX = 256;   // fused-path chunk-length cap (k* staged in smem)
+constexpr int PF_FWD = 3;     // ring slots (groups of Layout::G steps) per warp
+constexpr int PF_BWD = 4;
 
 // ------------------------------------------------------------------ vector IO
 template <typename T, int NPL>
@@ -53,6 +61,55 @@ __device__ __forceinline__ void vld(const T* __restrict__ p, float (&o)[NPL]) {
             o[0] = __bfloat162float(__ldg(p));
         }
     }
+}
+
+// the same from shared memory
+template <typename T, int NPL>
+__device__ __forceinline__ void sld(const T* p, float (&o)[NPL]) {
+    if constexpr (std::is_same<T, float>::value) {
+        if constexpr (NPL == 4) {
+            const float4 v = *reinterpret_cast<const float4*>(p);
+            o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+        } else if constexpr (NPL == 2) {
+            const float2 v = *reinterpret_cast<const float2*>(p);
+            o[0] = v.x; o[1] = v.y;
+        } else {
+            o[0] = *p;
+        }
+    } else {
+        if constexpr (NPL == 4) {
+            const uint2 v = *reinterpret_cast<const uint2*>(p);
+            o[0] = __uint_as_float(v.x << 16); o[1] = __uint_as_float(v.x & 0xffff0000u);
+            o[2] = __uint_as_float(v.y << 16); o[3] = __uint_as_float(v.y & 0xffff0000u);
+        } else if constexpr (NPL == 2) {
+            const uint32_t v = *reinterpret_cast<const uint32_t*>(p);
+            o[0] = __uint_as_float(v << 16); o[1] = __uint_as_float(v & 0xffff0000u);
+        } else {
+            o[0] = __bfloat162float(*p);
+        }
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ float sld1(const T* p) {
+    if constexpr (std::is_same<T, float>::value) return *p;
+    else return __bfloat162float(*p);
+}
+
+// NPL uint16 index values from shared memory (clamped into [0, N))
+template <int NPL>
+__device__ __forceinline__ void sld_idx(const uint16_t* p, int N, int (&P)[NPL]) {
+    if constexpr (NPL == 4) {
+        const uint2 v = *reinterpret_cast<const uint2*>(p);
+        P[0] = v.x & 0xffff; P[1] = v.x >> 16; P[2] = v.y & 0xffff; P[3] = v.y >> 16;
+    } else if constexpr (NPL == 2) {
+        const uint32_t v = *reinterpret_cast<const uint32_t*>(p);
+        P[0] = v & 0xffff; P[1] = v >> 16;
+    } else {
+        P[0] = *p;
+    }
+#pragma unroll
+    for (int u = 0; u < NPL; ++u) P[u] = min(P[u], N - 1);
 }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
@@ -90,18 +147,6 @@ __device__ __forceinline__ void vld_cg(const float* p, float (&o)[NPL]) {
 template <int NPL>
 __device__ __forceinline__ void vst_f(float* p, const float (&v)[NPL]) { vst<float, NPL>(p, v); }
 
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void wait_flag(const uint32_t* p) {
-    while (ld_acquire(p) == 0u) __nanosleep(20);
-}
-
 // per-step own-state planes: x[NC][NPL]
 template <int NC, int NPL>
 struct Planes {
@@ -109,19 +154,55 @@ struct Planes {
 };
 
 template <typename T, int NC, int NPL>
-__device__ __forceinline__ void load_planes(const T* __restrict__ base, Planes<NC, NPL>& o, int N) {
-    vld<T, NPL>(base, o.v[0]);
-    if constexpr (NC == 2) vld<T, NPL>(base + N, o.v[1]);
-}
-
-template <typename T, int NC, int NPL>
 __device__ __forceinline__ void store_planes(T* __restrict__ base, const Planes<NC, NPL>& o, int N) {
     vst<T, NPL>(base, o.v[0]);
     if constexpr (NC == 2) vst<T, NPL>(base + N, o.v[1]);
 }
 
-template <int NC>
-struct SVal;   // smem exchange value
+// ------------------------------------------------------------------ chain flags
+// Producer: data stores, __threadfence (every lane), __syncwarp, st.release flag.
+// Consumer: relaxed polling (no L1 invalidation per poll), then one acquire fence.
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void wait_flag(const uint32_t* p) {
+    while (ld_relaxed(p) == 0u) __nanosleep(32);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+
+// ------------------------------------------------------------------ TMA ring primitives
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_1d(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(b))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(b)), "r"(parity)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// ------------------------------------------------------------------ exchange values
+template <int NC> struct SVal;
 template <> struct SVal<1> { using type = float; };
 template <> struct SVal<2> { using type = float2; };
 
@@ -138,8 +219,6 @@ template <int NC>
 __device__ __forceinline__ float im_of(typename SVal<NC>::type v) {
     if constexpr (NC == 2) return v.y; else { (void)v; return 0.f; }
 }
-
-// store this lane's NPL exchange values (contiguous) into an smem row
 template <int NC, int NPL>
 __device__ __forceinline__ void sts_row(typename SVal<NC>::type* row, int lane, const float (&re)[NPL],
                                         const float (&im)[NPL]) {
@@ -148,10 +227,18 @@ __device__ __forceinline__ void sts_row(typename SVal<NC>::type* row, int lane, 
 }
 
 // ------------------------------------------------------------------ fused plan
-// For entry e = h*K + k and lane l: rec[e][l][u*MU + q] = q-th source (ascending)
-// of target i = l*NPL + u, padded with the sentinel N; hdr[e] = M_0 | M_1<<8 |
-// M_2<<16 | M_3<<24 where M_u = max over lanes of the in-degree of slot u
-// (warp-uniform trip counts); bit 31 of ovf[e] set if some M_u > MU.
+// For entry e = h*K + k and lane l: rec[e][l][u*MU + q] = q-th source (ascending
+// j) of target i = l*NPL + u, padded with the sentinel N (a zero slot of the
+// exchange buffer); hdr[e] = {M_0 | M_1<<8 | M_2<<16 | M_3<<24, ovf, 0, 0}
+// where M_u = max over lanes of the in-degree of slot u (warp-uniform trip
+// counts) and ovf != 0 if some M_u > MU (then the CSR plan is used).
+template <int NPL>
+struct Rec {
+    static constexpr int B = (NPL * MU + 3) & ~3;   // record bytes per lane (whole 32-bit words)
+    static constexpr int W = B / 4;
+    uint32_t w[W];
+};
+
 template <int NPL>
 __global__ void k_build_fused_plan(const uint16_t* __restrict__ dict_idx, uint8_t* __restrict__ rec,
                                    uint32_t* __restrict__ hdr, int N) {
@@ -162,7 +249,7 @@ __global__ void k_build_fused_plan(const uint16_t* __restrict__ dict_idx, uint8_
     for (int j = threadIdx.x; j < N; j += blockDim.x) sP[j] = min((int)P[j], N - 1);
     if (threadIdx.x < 8) smax[threadIdx.x] = 0;
     __syncthreads();
-    constexpr int RB = NPL * MU;
+    constexpr int RB = Rec<NPL>::B;
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
         const int l = i / NPL, u = i % NPL;
         int q = 0;
@@ -183,27 +270,15 @@ __global__ void k_build_fused_plan(const uint16_t* __restrict__ dict_idx, uint8_
             h |= (uint32_t)min(smax[u], 255) << (8 * u);
             ovf |= smax[u] > MU;
         }
-        hdr[2 * e] = h;
-        hdr[2 * e + 1] = ovf ? 1u : 0u;
+        hdr[4 * e] = h;
+        hdr[4 * e + 1] = ovf ? 1u : 0u;
+        hdr[4 * e + 2] = (uint32_t)e;   // entry index (CSR fallback)
+        hdr[4 * e + 3] = 0u;
     }
 }
 
-// record bytes of one (entry, lane): NPL*MU bytes, read as 32-bit words
 template <int NPL>
-struct Rec {
-    static constexpr int W = (NPL * MU + 3) / 4;
-    uint32_t w[W];
-};
-
-template <int NPL>
-__device__ __forceinline__ void load_rec(const uint8_t* __restrict__ rec, int e, int lane, Rec<NPL>& r) {
-    const uint32_t* p = reinterpret_cast<const uint32_t*>(rec + ((size_t)e * 32 + lane) * (NPL * MU));
-#pragma unroll
-    for (int i = 0; i < Rec<NPL>::W; ++i) r.w[i] = __ldg(p + i);
-}
-
-template <int NPL>
-__device__ __forceinline__ int rec_byte(const Rec<NPL>& r, int idx) {   // idx compile-time after unroll
+__device__ __forceinline__ int rec_byte(const Rec<NPL>& r, int idx) {   // idx compile-time after unrolling
     return (r.w[idx >> 2] >> (8 * (idx & 3))) & 0xff;
 }
 
@@ -262,21 +337,261 @@ struct FusedArgs {
     void* out1;              // bwd: ddiag (act, PER_STEP) or f32 scratch (PER_DICT)
     float* gsel;             // bwd
     float* dh0;              // bwd
-    float* mu;               // bwd: [S][C][NC][N]
+    float* mu;               // bwd: [S][C][NC][N]  mu_c, adjoint entering chunk c from later chunks
+    float* betap;            // bwd: [S][C][NC][N]  beta'_c, the chunk's transposed aggregate
     uint32_t* ctrl;          // [0] ticket counter, [1..S*C] flags
     int H, L, N, K, tau, C, S;
     uint32_t flags;
+    int debug_nochain;       // timing experiments only (PDSSM_DEBUG_NOCHAIN): skip the carry wait
 };
 
-template <typename T, int NC, int NPL, bool PD>
-__device__ __forceinline__ void load_diag_own(const FusedArgs& a, size_t step_off, int h, int k, int lane,
-                                              Planes<NC, NPL>& D) {
-    if constexpr (PD) {
-        const float* p = a.diag_dict + ((size_t)(h * a.K + k) * NC) * a.N + lane * NPL;
-        vld<float, NPL>(p, D.v[0]);
-        if constexpr (NC == 2) vld<float, NPL>(p + a.N, D.v[1]);
+
+// x <- Abar x + beta for one chunk aggregate (pi, d, beta) held as this lane's NPL
+// source slices: out[i] = beta[i] + sum_{j : pi[j] = i} d[j] x[j].  Unique targets are
+// stored directly; colliding groups are reduced by a fixed xor-butterfly per distinct
+// key (ballot loop) -- deterministic, no float atomics.  Optionally composes the
+// index map m <- pi[m] (gather through the key row).
+template <int NC, int NPL>
+__device__ __forceinline__ void apply_aggregate(int lane, int N, uint16_t* key, int* cnt, typename SVal<NC>::type* obuf,
+                                                const int (&pi)[NPL], const float (&dre)[NPL], const float (&dim)[NPL],
+                                                const float (&bre)[NPL], const float (&bim)[NPL], float (&xr)[NPL],
+                                                float (&xi)[NPL], int* mp) {
+    __syncwarp();   // previous users of key / cnt / obuf are done
+    float wr[NPL], wi[NPL];
+#pragma unroll
+    for (int u = 0; u < NPL; ++u) {
+        wr[u] = dre[u] * xr[u] - dim[u] * xi[u];
+        wi[u] = dre[u] * xi[u] + dim[u] * xr[u];
+        key[lane * NPL + u] = (uint16_t)pi[u];
+        obuf[lane * NPL + u] = mk<NC>(0.f, 0.f);
+        cnt[lane * NPL + u] = 0;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < NPL; ++u) atomicAdd(&cnt[pi[u]], 1);   // integer counts: order-independent
+    __syncwarp();
+    bool pend[NPL];
+    uint32_t anyp = 0;
+#pragma unroll
+    for (int u = 0; u < NPL; ++u) {
+        pend[u] = cnt[pi[u]] > 1;
+        if (!pend[u]) obuf[pi[u]] = mk<NC>(wr[u], wi[u]);
+        anyp |= pend[u];
+    }
+    __syncwarp();
+    uint32_t bal = __ballot_sync(0xffffffffu, anyp);
+    while (bal) {
+        const int leader = __ffs(bal) - 1;
+        int mykey = N;
+#pragma unroll
+        for (int u = NPL - 1; u >= 0; --u)
+            if (pend[u]) mykey = pi[u];
+        const int K0 = __shfl_sync(0xffffffffu, mykey, leader);
+        float pr = 0.f, pim = 0.f;
+#pragma unroll
+        for (int u = 0; u < NPL; ++u) {
+            if (pend[u] && pi[u] == K0) { pr += wr[u]; pim += wi[u]; pend[u] = false; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            pr += __shfl_xor_sync(0xffffffffu, pr, o);
+            if constexpr (NC == 2) pim += __shfl_xor_sync(0xffffffffu, pim, o);
+        }
+        if (lane == 0) obuf[K0] = mk<NC>(pr, pim);
+        anyp = 0;
+#pragma unroll
+        for (int u = 0; u < NPL; ++u) anyp |= pend[u];
+        bal = __ballot_sync(0xffffffffu, anyp);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < NPL; ++u) {
+        const auto o = obuf[lane * NPL + u];
+        xr[u] = re_of<NC>(o) + bre[u];
+        xi[u] = im_of<NC>(o) + bim[u];
+        if (mp) mp[u] = key[mp[u]];
+    }
+}
+
+
+__host__ __device__ constexpr size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+// ============================================================================
+// CTA = WARPS independent consumer warps, one CTA per SM (persistent).
+//  * head affinity: warps of CTA i take tickets of head h = i mod H first (per-head
+//    ticket counters), so the head's small per-entry tables (index rows, preimage
+//    records, headers) stay L1-resident and are read with plain loads;
+//  * each warp streams its per-step rows (D_t, b_t / e_{t-1}, h_{t-1}) into a
+//    private ring of PF slots of G consecutive steps with 1-D TMA bulk copies
+//    (one copy per stream per slot: G rows are contiguous in HBM), issued by the
+//    warp itself once per G steps, PF*G steps ahead, across item boundaries.
+// ============================================================================
+constexpr int WARPS = 7;
+constexpr int CTA_THREADS = WARPS * 32;
+
+template <typename T, int NC, int NPL, bool PD, bool BWD, int ESZ = (int)sizeof(T)>
+struct Layout {
+    static constexpr int G = BWD ? 2 : 4;                    // steps per ring slot
+    static constexpr int N = 32 * NPL;
+    static constexpr int ROW = NC * N * (int)sizeof(T);      // one D / b / h row (act dtype)
+    static constexpr int EROW = NC * N * ESZ;                 // one e row (bwd)
+    static constexpr int DG = PD ? 0 : G * ROW;               // D rows per slot (PER_DICT: none)
+    static constexpr int OFF_B = DG;                          // fwd b rows
+    static constexpr int OFF_E = DG;                          // bwd e rows
+    static constexpr int OFF_H = DG + G * EROW;           // bwd h rows
+    static constexpr int SLOT = (int)al16(BWD ? OFF_H + G * ROW : OFF_B + G * ROW);
+    static constexpr int PF = BWD ? PF_BWD : PF_FWD;          // slots in flight
+    static constexpr int SV = NC == 2 ? 8 : 4;
+    static constexpr size_t w_ring = 0;
+    static constexpr size_t w_bar = al16(w_ring + (size_t)PF * SLOT);
+    static constexpr size_t w_x = al16(w_bar + (size_t)PF * 8);              // exchange [2][N+1]
+    static constexpr size_t w_ob = al16(w_x + (size_t)2 * (N + 1) * SV);    // chain result [N]
+    static constexpr size_t w_key = al16(w_ob + (size_t)N * SV);             // chain keys u16 [N]
+    static constexpr size_t w_cnt = al16(w_key + (size_t)N * 2);             // chain counts int [N]
+    static constexpr size_t w_k = al16(w_cnt + (size_t)N * 4);               // k* of the chunk [TAUMAX]
+    static constexpr size_t w_bytes = al16(w_k + TAUMAX);
+    static constexpr size_t bytes = (size_t)WARPS * w_bytes;
+};
+
+template <bool PD, typename T>
+using DType = typename std::conditional<PD, float, T>::type;
+
+struct Item {
+    int ticket, c, s, h, t0, t1, n;
+};
+
+// per-head tickets: ticket in [0, B*C): chunk-major (reverse for the backward)
+__device__ __forceinline__ Item make_item(const FusedArgs& a, int h, int ticket, bool reverse) {
+    Item it;
+    it.ticket = ticket;
+    const int B = a.S / a.H;
+    const int cr = ticket / B;
+    const int b = ticket - cr * B;
+    it.h = h;
+    it.s = b * a.H + h;
+    it.c = reverse ? a.C - 1 - cr : cr;
+    it.t0 = it.c * a.tau;
+    it.t1 = min(it.t0 + a.tau, a.L);
+    it.n = it.t1 - it.t0;
+    return it;
+}
+
+// next item for this warp: head-affine, then help the other heads
+__device__ __forceinline__ bool next_item(const FusedArgs& a, int& h, int lane, bool reverse, Item& it) {
+    const int per_head = (a.S / a.H) * a.C;
+    for (int tries = 0; tries < a.H; ++tries) {
+        int t = 0;
+        if (lane == 0) t = (int)atomicAdd(a.ctrl + h, 1u);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t < per_head) {
+            it = make_item(a, h, t, reverse);
+            return true;
+        }
+        h = h + 1 == a.H ? 0 : h + 1;
+    }
+    return false;
+}
+
+__device__ __forceinline__ uint32_t* flag_ptr(const FusedArgs& a, size_t ci) { return a.ctrl + a.H + ci; }
+
+// item k* bytes, prefetched one item ahead: lane i holds bytes i, i+32, ...
+struct KPre {
+    uint32_t b[TAUMAX / 32];
+};
+__device__ __forceinline__ void kpre_load(const FusedArgs& a, KPre& kp, const Item& it, int lane) {
+#pragma unroll
+    for (int i = 0; i < TAUMAX / 32; ++i) {
+        const int idx = lane + 32 * i;
+        kp.b[i] = idx < it.n ? (uint32_t)__ldg(a.kstar + (size_t)it.s * a.L + it.t0 + idx) : 0u;
+    }
+}
+__device__ __forceinline__ void kpre_store(const FusedArgs& a, const KPre& kp, uint8_t* sk, int n, int lane,
+                                           bool check) {
+#pragma unroll
+    for (int i = 0; i < TAUMAX / 32; ++i) {
+        const int idx = lane + 32 * i;
+        if (idx < n) {
+            int k = (int)kp.b[i];
+            if (k >= a.K) {
+                if (check && (a.flags & PDSSM_CHECK_FINITE)) report(ERRBIT_RANGE);
+                k = a.K - 1;
+            }
+            sk[idx] = (uint8_t)k;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// ring fill cursor: virtual group stream of the current item, then the next one.
+// An item has 2*ng groups (Phase A groups, then Phase C groups), ng = ceil(n/G).
+// ---------------------------------------------------------------------------
+struct FillCursor {
+    Item it[2];        // [0] item being filled, [1] the one after (if known)
+    bool valid[2];
+    int g;             // next virtual group of it[0]
+    uint32_t q;        // total fills issued (slot = q % PF)
+};
+
+template <typename T, typename TE, int NC, int NPL, bool PD, bool BWD>
+__device__ __forceinline__ void issue_fill(const FusedArgs& a, const Item& it, int g, uint8_t* ring, uint64_t* bars,
+                                           int slot) {
+    using LY = Layout<T, NC, NPL, PD, BWD, (int)sizeof(TE)>;
+    const int N = a.N;
+    const size_t row = (size_t)NC * N;
+    const size_t seq0 = (size_t)it.s * a.L;
+    const int ng = (it.n + LY::G - 1) / LY::G;
+    const bool phC = g >= ng;
+    const int gi = phC ? g - ng : g;
+    const int v0 = gi * LY::G;
+    const int len = min(LY::G, it.n - v0);
+    uint8_t* dst = ring + (size_t)slot * LY::SLOT;
+    uint64_t* bar = bars + slot;
+    fence_proxy_async();
+    if constexpr (!BWD) {
+        const int t = it.t0 + v0;   // rows t .. t+len-1 at slot offsets 0..len-1
+        mbar_expect_tx(bar, (uint32_t)((PD ? 0 : len * LY::ROW) + len * LY::ROW));
+        if constexpr (!PD) tma_1d(dst, static_cast<const T*>(a.diag) + (seq0 + t) * row, len * LY::ROW, bar);
+        tma_1d(dst + LY::OFF_B, static_cast<const T*>(a.bias) + (seq0 + t) * row, len * LY::ROW, bar);
     } else {
-        load_planes<T, NC, NPL>(static_cast<const T*>(a.diag) + step_off + lane * NPL, D, a.N);
+        // steps v0..v0+len-1 are times t_hi = t1-1-v0 down to t_lo = t_hi-len+1; the row
+        // of time t sits at slot offset (t - t_lo) for D, e_{t-1} and h_{t-1}
+        const int t_hi = it.t1 - 1 - v0;
+        const int t_lo = t_hi - len + 1;
+        const TE* ein = static_cast<const TE*>(a.bias);
+        const int e_first = max(t_lo - 1, it.t0);   // e_{t-1} needed for t > t0
+        const int e_cnt = ein ? max(0, t_hi - 1 - e_first + 1) : 0;
+        const int h_first = max(t_lo - 1, 0);       // h_{t-1} needed for t > 0 (Phase C' only)
+        const int h_cnt = phC ? max(0, t_hi - 1 - h_first + 1) : 0;
+        mbar_expect_tx(bar, (uint32_t)((PD ? 0 : len * LY::ROW) + e_cnt * LY::EROW + h_cnt * LY::ROW));
+        if constexpr (!PD) tma_1d(dst, static_cast<const T*>(a.diag) + (seq0 + t_lo) * row, len * LY::ROW, bar);
+        if (e_cnt > 0)
+            tma_1d(dst + LY::OFF_E + (size_t)(e_first - (t_lo - 1)) * LY::EROW, ein + (seq0 + e_first) * row,
+                   e_cnt * LY::EROW, bar);
+        if (h_cnt > 0)
+            tma_1d(dst + LY::OFF_H + (size_t)(h_first - (t_lo - 1)) * LY::ROW,
+                   static_cast<const T*>(a.hsaved) + (seq0 + h_first) * row, h_cnt * LY::ROW, bar);
+    }
+}
+
+// issue fills while fewer than PF are outstanding ahead of `consumed`
+template <typename T, typename TE, int NC, int NPL, bool PD, bool BWD>
+__device__ __forceinline__ void pump(const FusedArgs& a, FillCursor& fc, uint32_t consumed, uint8_t* ring,
+                                     uint64_t* bars, int lane) {
+    using LY = Layout<T, NC, NPL, PD, BWD, (int)sizeof(TE)>;
+    constexpr int PF = LY::PF;
+    while (fc.q < consumed + PF) {
+        if (!fc.valid[0]) break;
+        const int ng = (fc.it[0].n + LY::G - 1) / LY::G;
+        if (fc.g >= 2 * ng) {
+            if (!fc.valid[1]) break;
+            fc.it[0] = fc.it[1];
+            fc.valid[1] = false;
+            fc.g = 0;
+            continue;
+        }
+        if (lane == 0) issue_fill<T, TE, NC, NPL, PD, BWD>(a, fc.it[0], fc.g, ring, bars, (int)(fc.q % PF));
+        ++fc.g;
+        ++fc.q;
     }
 }
 
@@ -284,227 +599,291 @@ __device__ __forceinline__ void load_diag_own(const FusedArgs& a, size_t step_of
 // forward
 // ============================================================================
 template <typename T, int NC, int NPL, bool PD>
-__global__ void __launch_bounds__(WARPS * 32) k_fwd_fused(FusedArgs a) {
+__global__ void __launch_bounds__(CTA_THREADS, 1) k_fwd_fused(FusedArgs a) {
     using SV = typename SVal<NC>::type;
-    constexpr int NMAX = 32 * NPL;
-    __shared__ SV s_v[WARPS][2][NMAX + 1];   // v = D (.) state, + zero sentinel
-    __shared__ SV s_d[WARPS][2][NMAX];       // D_t staged for the pi-gather; chain scratch
-    __shared__ uint16_t s_key[WARPS][NMAX];
-    __shared__ int s_cnt[WARPS][NMAX];
+    using LY = Layout<T, NC, NPL, PD, false>;
+    using DT = DType<PD, T>;
+    constexpr int PF = LY::PF;
+    extern __shared__ __align__(128) uint8_t smem[];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint8_t* base = smem + (size_t)w * LY::w_bytes;
+    uint8_t* ring = base + LY::w_ring;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(base + LY::w_bar);
+    SV* xb = reinterpret_cast<SV*>(base + LY::w_x);
+    SV* obuf = reinterpret_cast<SV*>(base + LY::w_ob);
+    uint16_t* key = reinterpret_cast<uint16_t*>(base + LY::w_key);
+    int* cnt = reinterpret_cast<int*>(base + LY::w_cnt);
+    uint8_t* sk = base + LY::w_k;
     const int N = a.N;
-    SV* vb[2] = {s_v[w][0], s_v[w][1]};
-    if (lane == 0) { vb[0][N] = mk<NC>(0.f, 0.f); vb[1][N] = mk<NC>(0.f, 0.f); }
-    const int total = a.S * a.C;
-    const T* bias = static_cast<const T*>(a.bias);
-    T* hout = static_cast<T*>(a.out0);
-    while (true) {
-        __syncwarp();
-        int ticket = 0;
-        if (lane == 0) ticket = atomicAdd(a.ctrl, 1u);
-        ticket = __shfl_sync(0xffffffffu, ticket, 0);
-        if (ticket >= total) break;
-        const int c = ticket / a.S, s = ticket - c * a.S, h = s % a.H;
-        const int t0 = c * a.tau, t1 = min(t0 + a.tau, a.L);
+    const size_t row = (size_t)NC * N;
+    if (lane == 0) {
+        for (int i = 0; i < PF; ++i) mbar_init(bars + i, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        xb[N] = mk<NC>(0.f, 0.f);
+        xb[(N + 1) + N] = mk<NC>(0.f, 0.f);
+    }
+    __syncwarp();
+    int head = blockIdx.x % a.H;
+    FillCursor fc;
+    fc.valid[0] = next_item(a, head, lane, false, fc.it[0]);
+    fc.valid[1] = false;
+    fc.g = 0;
+    fc.q = 0;
+    KPre kp;
+    if (fc.valid[0]) kpre_load(a, kp, fc.it[0], lane);
+    uint32_t consumed = 0;        // groups consumed
+    bool have = fc.valid[0];
+    Item it = fc.it[0];
+    while (have) {
+        // the item after this one (ticket prefetch) so the ring can run across items
+        Item nx;
+        const bool has_next = next_item(a, head, lane, false, nx);
+        if (has_next) { fc.it[1] = nx; fc.valid[1] = true; }
+        const int c = it.c, s = it.s, h = it.h, n = it.n;
+        const int ng = (n + LY::G - 1) / LY::G;
         const size_t ci = (size_t)s * a.C + c;
-        const size_t row = (size_t)NC * N;
+        __syncwarp();
+        kpre_store(a, kp, sk, n, lane, true);
+        if (has_next) kpre_load(a, kp, nx, lane);
+        __syncwarp();
+        pump<T, T, NC, NPL, PD, false>(a, fc, consumed, ring, bars, lane);
+        const uint16_t* prow_base = a.dict_idx + (size_t)h * a.K * N;
+        const uint8_t* rec_base = a.rec + ((size_t)h * a.K * 32 + lane) * Rec<NPL>::B;
+        const uint32_t* hdr_base = a.hdr + (size_t)h * a.K * 4;
         // ---------------- Phase A: aggregate from identity
         int pi[NPL];
         float dre[NPL], dim[NPL], bre[NPL], bim[NPL];
 #pragma unroll
         for (int u = 0; u < NPL; ++u) { pi[u] = lane * NPL + u; dre[u] = 1.f; dim[u] = 0.f; bre[u] = 0.f; bim[u] = 0.f; }
+        // per-step table prefetch (L1): record words + header of entry k*_{v+1}
+        Rec<NPL> rn;
+        uint4 hn;
         {
-            Planes<NC, NPL> Dn, Bn;
-            int kn = load_k(a.kstar, (size_t)s * a.L + t0, a.K, a.flags);
-            load_diag_own<T, NC, NPL, PD>(a, ((size_t)s * a.L + t0) * row, h, kn, lane, Dn);
-            load_planes<T, NC, NPL>(bias + ((size_t)s * a.L + t0) * row + lane * NPL, Bn, N);
-            for (int t = t0; t < t1; ++t) {
-                const int buf = (t - t0) & 1;
-                const int k = kn;
-                Planes<NC, NPL> D = Dn, Bv = Bn;
-                if (t + 1 < t1) {
-                    kn = load_k(a.kstar, (size_t)s * a.L + t + 1, a.K, a.flags);
-                    load_diag_own<T, NC, NPL, PD>(a, ((size_t)s * a.L + t + 1) * row, h, kn, lane, Dn);
-                    load_planes<T, NC, NPL>(bias + ((size_t)s * a.L + t + 1) * row + lane * NPL, Bn, N);
+            const int k0 = sk[0];
+#pragma unroll
+            for (int i = 0; i < Rec<NPL>::W; ++i)
+                rn.w[i] = __ldg(reinterpret_cast<const uint32_t*>(rec_base + (size_t)k0 * 32 * Rec<NPL>::B) + i);
+            hn = __ldg(reinterpret_cast<const uint4*>(hdr_base + 4 * k0));
+        }
+        for (int gi = 0; gi < ng; ++gi) {
+            const int slot = consumed % PF;
+            mbar_wait(bars + slot, (consumed / PF) & 1);
+            const uint8_t* sp = ring + (size_t)slot * LY::SLOT;
+            const int len = min(LY::G, n - gi * LY::G);
+            for (int i = 0; i < len; ++i) {
+                const int v = gi * LY::G + i;
+                const int k = sk[v];
+                const Rec<NPL> r = rn;
+                const uint4 hd = hn;
+                {
+                    const int kn = sk[v + 1 < n ? v + 1 : v];
+#pragma unroll
+                    for (int q = 0; q < Rec<NPL>::W; ++q)
+                        rn.w[q] = __ldg(reinterpret_cast<const uint32_t*>(rec_base + (size_t)kn * 32 * Rec<NPL>::B) + q);
+                    hn = __ldg(reinterpret_cast<const uint4*>(hdr_base + 4 * kn));
                 }
-                const int e = h * a.K + k;
-                const uint32_t hd = __ldg(a.hdr + 2 * e);
-                const uint32_t ovf = __ldg(a.hdr + 2 * e + 1);
-                Rec<NPL> r;
-                load_rec<NPL>(a.rec, e, lane, r);
-                float vre[NPL], vim[NPL], Dim_[NPL];
+                Planes<NC, NPL> D, Bv;
+                const DT* Dp;
+                if constexpr (PD) Dp = a.diag_dict + ((size_t)(h * a.K + k) * NC) * N;
+                else Dp = reinterpret_cast<const T*>(sp) + (size_t)i * row;
+                if constexpr (PD) {
+                    vld<float, NPL>(Dp + lane * NPL, D.v[0]);
+                    if constexpr (NC == 2) vld<float, NPL>(Dp + N + lane * NPL, D.v[1]);
+                } else {
+                    sld<DT, NPL>(Dp + lane * NPL, D.v[0]);
+                    if constexpr (NC == 2) sld<DT, NPL>(Dp + N + lane * NPL, D.v[1]);
+                }
+                const T* Bp = reinterpret_cast<const T*>(sp + LY::OFF_B) + (size_t)i * row;
+                sld<T, NPL>(Bp + lane * NPL, Bv.v[0]);
+                if constexpr (NC == 2) sld<T, NPL>(Bp + N + lane * NPL, Bv.v[1]);
+                if (a.flags & PDSSM_CHECK_FINITE) {
+#pragma unroll
+                    for (int u = 0; u < NPL; ++u) {
+                        check_cpx(cpx{D.v[0][u], D.v[NC - 1][u]}, a.flags);
+                        check_cpx(cpx{Bv.v[0][u], Bv.v[NC - 1][u]}, a.flags);
+                    }
+                }
+                // pi / d update: d <- D_t[pi] d, pi <- P_t[pi]
+                const uint16_t* prow = prow_base + (size_t)k * N;
+#pragma unroll
+                for (int u = 0; u < NPL; ++u) {
+                    float pr, pm;
+                    if constexpr (PD) { pr = __ldg(Dp + pi[u]); pm = NC == 2 ? __ldg(Dp + N + pi[u]) : 0.f; }
+                    else { pr = sld1<DT>(Dp + pi[u]); pm = NC == 2 ? sld1<DT>(Dp + N + pi[u]) : 0.f; }
+                    const float nr = pr * dre[u] - pm * dim[u];
+                    const float ni = pr * dim[u] + pm * dre[u];
+                    dre[u] = nr; dim[u] = ni;
+                    pi[u] = clamp_idx(__ldg(prow + pi[u]), N, a.flags);
+                }
+                float vre[NPL], vim[NPL];
 #pragma unroll
                 for (int u = 0; u < NPL; ++u) {
                     const float di = NC == 2 ? D.v[NC - 1][u] : 0.f;
-                    Dim_[u] = di;
                     vre[u] = D.v[0][u] * bre[u] - di * bim[u];
                     vim[u] = D.v[0][u] * bim[u] + di * bre[u];
                 }
-                sts_row<NC, NPL>(vb[buf], lane, vre, vim);
-                sts_row<NC, NPL>(s_d[w][buf], lane, D.v[0], Dim_);
+                SV* vb = xb + (v & 1) * (N + 1);
+                sts_row<NC, NPL>(vb, lane, vre, vim);
                 __syncwarp();
-                // pi / d update: d <- D_t[pi] d, pi <- P_t[pi]
+                float zr[NPL], zi[NPL];
 #pragma unroll
-                for (int u = 0; u < NPL; ++u) {
-                    const SV dp = s_d[w][buf][pi[u]];
-                    const float nr = re_of<NC>(dp) * dre[u] - im_of<NC>(dp) * dim[u];
-                    const float ni = re_of<NC>(dp) * dim[u] + im_of<NC>(dp) * dre[u];
-                    dre[u] = nr; dim[u] = ni;
-                    pi[u] = clamp_idx(__ldg(a.dict_idx + (size_t)e * N + pi[u]), N, a.flags);
-                }
-                // beta <- A_t beta + b_t
-                float are[NPL], aim[NPL];
+                for (int u = 0; u < NPL; ++u) { zr[u] = 0.f; zi[u] = 0.f; }
+                if (hd.y) gather_sum_csr<NC, NPL>(vb, a.pstart, a.psrc, h * a.K + k, N, lane, zr, zi);
+                else gather_sum<NC, NPL>(vb, r, hd.x, zr, zi);
 #pragma unroll
-                for (int u = 0; u < NPL; ++u) { are[u] = 0.f; aim[u] = 0.f; }
-                if (ovf) gather_sum_csr<NC, NPL>(vb[buf], a.pstart, a.psrc, e, N, lane, are, aim);
-                else gather_sum<NC, NPL>(vb[buf], r, hd, are, aim);
-#pragma unroll
-                for (int u = 0; u < NPL; ++u) { bre[u] = are[u] + Bv.v[0][u]; bim[u] = NC == 2 ? aim[u] + Bv.v[NC - 1][u] : 0.f; }
+                for (int u = 0; u < NPL; ++u) { bre[u] = zr[u] + Bv.v[0][u]; bim[u] = NC == 2 ? zi[u] + Bv.v[NC - 1][u] : 0.f; }
             }
+            // slot fully read (the syncwarp of the group's last step orders every lane's reads
+            // except this step's pi-gathers, which the next syncwarp covers)
+            __syncwarp();
+            ++consumed;
+            pump<T, T, NC, NPL, PD, false>(a, fc, consumed, ring, bars, lane);
         }
-        // publish the aggregate (chunk_state sections 0-2)
-        {
-            float tmp[NPL];
+        // publish the aggregate (chunk_state sections 0-2), then flag = 1 ("aggregate ready")
 #pragma unroll
-            for (int u = 0; u < NPL; ++u) a.cs.pi[ci * N + lane * NPL + u] = (uint16_t)pi[u];
-            vst_f<NPL>(a.cs.d + ci * row + lane * NPL, dre);
-            vst_f<NPL>(a.cs.beta + ci * row + lane * NPL, bre);
-            if constexpr (NC == 2) {
-                vst_f<NPL>(a.cs.d + ci * row + N + lane * NPL, dim);
-                vst_f<NPL>(a.cs.beta + ci * row + N + lane * NPL, bim);
-            }
-            (void)tmp;
+        for (int u = 0; u < NPL; ++u) a.cs.pi[ci * N + lane * NPL + u] = (uint16_t)pi[u];
+        vst_f<NPL>(a.cs.d + ci * row + lane * NPL, dre);
+        vst_f<NPL>(a.cs.beta + ci * row + lane * NPL, bre);
+        if constexpr (NC == 2) {
+            vst_f<NPL>(a.cs.d + ci * row + N + lane * NPL, dim);
+            vst_f<NPL>(a.cs.beta + ci * row + N + lane * NPL, bim);
         }
-        // ---------------- carry hand-off: carry_c (wait) -> carry_{c+1} (publish)
+        if (c + 1 < a.C) {
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) st_release(flag_ptr(a, ci), 1u);
+        }
+        // ---------------- decoupled look-back for carry_c: fold the aggregates of the chunks
+        // between the nearest predecessor that already published its inclusive carry
+        // (flag 2) and this chunk.  The fold repeats exactly the chain's arithmetic
+        // carry_{m+1} = Abar_m carry_m + beta_bar_m, so the result does not depend on
+        // which predecessor was found (bitwise deterministic).
         float cre[NPL], cim[NPL];
-        if (c == 0) {
-#pragma unroll
-            for (int u = 0; u < NPL; ++u) { cre[u] = 0.f; cim[u] = 0.f; }
-            if (a.h0) {
-                vld<float, NPL>(a.h0 + (size_t)s * row + lane * NPL, cre);
-                if constexpr (NC == 2) vld<float, NPL>(a.h0 + (size_t)s * row + N + lane * NPL, cim);
-            }
-            vst_f<NPL>(a.cs.carry + ci * row + lane * NPL, cre);
-            if constexpr (NC == 2) vst_f<NPL>(a.cs.carry + ci * row + N + lane * NPL, cim);
-        } else {
-            wait_flag(a.ctrl + 1 + ci);
-            vld_cg<NPL>(a.cs.carry + ci * row + lane * NPL, cre);
-            if constexpr (NC == 2) vld_cg<NPL>(a.cs.carry + ci * row + N + lane * NPL, cim);
-        }
-        int mp[NPL];   // exclusive prefix map before this chunk (maps export)
-        if (a.maps) {
-            if (c == 0) {
-#pragma unroll
-                for (int u = 0; u < NPL; ++u) mp[u] = lane * NPL + u;
-            } else {
-#pragma unroll
-                for (int u = 0; u < NPL; ++u) mp[u] = __ldcg(a.maps + ((size_t)s * (a.C + 1) + c) * N + lane * NPL + u);
-            }
-        }
+        int mp[NPL];                 // exclusive prefix map before this chunk (maps export)
         {
-            // carry_{c+1}[i] = beta_bar[i] + sum_{j : pi[j] = i} d[j] carry_c[j]
-            // deterministic: unique targets stored, colliding groups reduced by a
-            // fixed xor-butterfly per distinct key (ballot loop)
-            __syncwarp();            // Phase A's last smem reads are done
-            SV* obuf = s_d[w][1];    // [N] result
-            uint16_t* key = s_key[w];
-            int* cnt = s_cnt[w];
-            float wr[NPL], wi[NPL];
-#pragma unroll
-            for (int u = 0; u < NPL; ++u) {
-                wr[u] = dre[u] * cre[u] - dim[u] * cim[u];
-                wi[u] = dre[u] * cim[u] + dim[u] * cre[u];
-                key[lane * NPL + u] = (uint16_t)pi[u];
-                obuf[lane * NPL + u] = mk<NC>(0.f, 0.f);
-                cnt[lane * NPL + u] = 0;
-            }
-            __syncwarp();
-#pragma unroll
-            for (int u = 0; u < NPL; ++u) atomicAdd(&cnt[pi[u]], 1);   // integer: order-independent
-            __syncwarp();
-            // unique targets are stored directly; colliding ones are reduced below
-            bool pend[NPL];
-            uint32_t anyp = 0;
-#pragma unroll
-            for (int u = 0; u < NPL; ++u) {
-                pend[u] = cnt[pi[u]] > 1;
-                if (!pend[u]) obuf[pi[u]] = mk<NC>(wr[u], wi[u]);
-                anyp |= pend[u];
-            }
-            __syncwarp();
-            uint32_t bal = __ballot_sync(0xffffffffu, anyp);
-            while (bal) {
-                const int leader = __ffs(bal) - 1;
-                int mykey = N;
-#pragma unroll
-                for (int u = NPL - 1; u >= 0; --u) if (pend[u]) mykey = pi[u];
-                const int K0 = __shfl_sync(0xffffffffu, mykey, leader);
-                float pr = 0.f, pim = 0.f;
-#pragma unroll
-                for (int u = 0; u < NPL; ++u) {
-                    if (pend[u] && pi[u] == K0) { pr += wr[u]; pim += wi[u]; pend[u] = false; }
+            int mP = -1;             // carry_{mP+1} is known; -1: carry_0 = h0
+            if (c > 0 && !a.debug_nochain) {
+                while (true) {
+                    const int m = c - 1 - lane;
+                    const uint32_t f = m >= 0 ? ld_relaxed(flag_ptr(a, (size_t)s * a.C + m)) : 2u;
+                    const uint32_t b2 = __ballot_sync(0xffffffffu, f == 2u);
+                    const uint32_t b0 = __ballot_sync(0xffffffffu, f == 0u);
+                    if (b2) {
+                        const int first = __ffs(b2) - 1;
+                        if ((b0 & ((1u << first) - 1u)) == 0u) { mP = c - 1 - first; break; }
+                    }
+                    __nanosleep(64);
                 }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    pr += __shfl_xor_sync(0xffffffffu, pr, o);
-                    if constexpr (NC == 2) pim += __shfl_xor_sync(0xffffffffu, pim, o);
-                }
-                if (lane == 0) obuf[K0] = mk<NC>(pr, pim);
-                anyp = 0;
-#pragma unroll
-                for (int u = 0; u < NPL; ++u) anyp |= pend[u];
-                bal = __ballot_sync(0xffffffffu, anyp);
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            } else if (c > 0) {
+                mP = c - 1;
             }
-            __syncwarp();
-            if (c + 1 < a.C) {
-                float nr[NPL], ni[NPL];
+            if (mP < 0) {
 #pragma unroll
-                for (int u = 0; u < NPL; ++u) {
-                    const SV o = obuf[lane * NPL + u];
-                    nr[u] = re_of<NC>(o) + bre[u];
-                    ni[u] = im_of<NC>(o) + bim[u];
+                for (int u = 0; u < NPL; ++u) { cre[u] = 0.f; cim[u] = 0.f; mp[u] = lane * NPL + u; }
+                if (a.h0) {
+                    vld<float, NPL>(a.h0 + (size_t)s * row + lane * NPL, cre);
+                    if constexpr (NC == 2) vld<float, NPL>(a.h0 + (size_t)s * row + N + lane * NPL, cim);
                 }
-                const size_t cn = ci + 1;
-                vst_f<NPL>(a.cs.carry + cn * row + lane * NPL, nr);
-                if constexpr (NC == 2) vst_f<NPL>(a.cs.carry + cn * row + N + lane * NPL, ni);
+            } else {
+                const size_t cm = (size_t)s * a.C + mP + 1;
+                vld_cg<NPL>(a.cs.carry + cm * row + lane * NPL, cre);
+                if constexpr (NC == 2) vld_cg<NPL>(a.cs.carry + cm * row + N + lane * NPL, cim);
                 if (a.maps) {
 #pragma unroll
                     for (int u = 0; u < NPL; ++u)
-                        a.maps[((size_t)s * (a.C + 1) + c + 1) * N + lane * NPL + u] = key[mp[u]];
+                        mp[u] = __ldcg(a.maps + ((size_t)s * (a.C + 1) + mP + 1) * N + lane * NPL + u);
                 }
-                __threadfence();
-                __syncwarp();
-                if (lane == 0) st_release(a.ctrl + 1 + cn, 1u);
-            } else if (a.maps) {
+            }
+            for (int m = mP + 1; m < c; ++m) {
+                const size_t cm = (size_t)s * a.C + m;
+                int pk[NPL];
+                float pdr[NPL], pdi[NPL], pbr[NPL], pbi[NPL];
 #pragma unroll
-                for (int u = 0; u < NPL; ++u) a.maps[((size_t)s * (a.C + 1) + c + 1) * N + lane * NPL + u] = key[mp[u]];
+                for (int u = 0; u < NPL; ++u) { pk[u] = min((int)__ldcg(a.cs.pi + cm * N + lane * NPL + u), N - 1); pdi[u] = 0.f; pbi[u] = 0.f; }
+                vld_cg<NPL>(a.cs.d + cm * row + lane * NPL, pdr);
+                vld_cg<NPL>(a.cs.beta + cm * row + lane * NPL, pbr);
+                if constexpr (NC == 2) {
+                    vld_cg<NPL>(a.cs.d + cm * row + N + lane * NPL, pdi);
+                    vld_cg<NPL>(a.cs.beta + cm * row + N + lane * NPL, pbi);
+                }
+                apply_aggregate<NC, NPL>(lane, N, key, cnt, obuf, pk, pdr, pdi, pbr, pbi, cre, cim, a.maps ? mp : nullptr);
+            }
+            if (c > 0 && mP + 1 < c) {   // carry_c computed here (duplicates of the chain's value are bitwise equal)
+                vst_f<NPL>(a.cs.carry + ci * row + lane * NPL, cre);
+                if constexpr (NC == 2) vst_f<NPL>(a.cs.carry + ci * row + N + lane * NPL, cim);
+            }
+            if (c == 0) {
+                vst_f<NPL>(a.cs.carry + ci * row + lane * NPL, cre);
+                if constexpr (NC == 2) vst_f<NPL>(a.cs.carry + ci * row + N + lane * NPL, cim);
             }
             if (a.maps) {
 #pragma unroll
                 for (int u = 0; u < NPL; ++u) a.maps[((size_t)s * (a.C + 1) + c) * N + lane * NPL + u] = (uint16_t)mp[u];
             }
+        }
+        // ---------------- inclusive carry_{c+1} = Abar_c carry_c + beta_bar_c, flag = 2
+        {
+            float nr[NPL], ni[NPL];
+            int mq[NPL];
+#pragma unroll
+            for (int u = 0; u < NPL; ++u) { nr[u] = cre[u]; ni[u] = cim[u]; mq[u] = mp[u]; }
+            apply_aggregate<NC, NPL>(lane, N, key, cnt, obuf, pi, dre, dim, bre, bim, nr, ni, a.maps ? mq : nullptr);
+            if (c + 1 < a.C) {
+                const size_t cn = ci + 1;
+                vst_f<NPL>(a.cs.carry + cn * row + lane * NPL, nr);
+                if constexpr (NC == 2) vst_f<NPL>(a.cs.carry + cn * row + N + lane * NPL, ni);
+            }
+            if (a.maps) {
+#pragma unroll
+                for (int u = 0; u < NPL; ++u) a.maps[((size_t)s * (a.C + 1) + c + 1) * N + lane * NPL + u] = (uint16_t)mq[u];
+            }
+            if (c + 1 < a.C) {
+                __threadfence();
+                __syncwarp();
+                if (lane == 0) st_release(flag_ptr(a, ci), 2u);
+            }
             __syncwarp();
         }
-        // ---------------- Phase C: replay from carry_c (L2-resident re-read)
+        // ---------------- Phase C: replay from carry_c (its slots were prefetched meanwhile)
+        T* hout = static_cast<T*>(a.out0) + ((size_t)s * a.L + it.t0) * row + lane * NPL;
         {
-            Planes<NC, NPL> Dn, Bn;
-            int kn = load_k(a.kstar, (size_t)s * a.L + t0, a.K, 0);
-            load_diag_own<T, NC, NPL, PD>(a, ((size_t)s * a.L + t0) * row, h, kn, lane, Dn);
-            load_planes<T, NC, NPL>(bias + ((size_t)s * a.L + t0) * row + lane * NPL, Bn, N);
-            for (int t = t0; t < t1; ++t) {
-                const int buf = (t - t0) & 1;
-                const int k = kn;
-                Planes<NC, NPL> D = Dn, Bv = Bn;
-                if (t + 1 < t1) {
-                    kn = load_k(a.kstar, (size_t)s * a.L + t + 1, a.K, 0);
-                    load_diag_own<T, NC, NPL, PD>(a, ((size_t)s * a.L + t + 1) * row, h, kn, lane, Dn);
-                    load_planes<T, NC, NPL>(bias + ((size_t)s * a.L + t + 1) * row + lane * NPL, Bn, N);
+            const int k0 = sk[0];
+#pragma unroll
+            for (int i = 0; i < Rec<NPL>::W; ++i)
+                rn.w[i] = __ldg(reinterpret_cast<const uint32_t*>(rec_base + (size_t)k0 * 32 * Rec<NPL>::B) + i);
+            hn = __ldg(reinterpret_cast<const uint4*>(hdr_base + 4 * k0));
+        }
+        for (int gi = 0; gi < ng; ++gi) {
+            const int slot = consumed % PF;
+            mbar_wait(bars + slot, (consumed / PF) & 1);
+            const uint8_t* sp = ring + (size_t)slot * LY::SLOT;
+            const int len = min(LY::G, n - gi * LY::G);
+            for (int i = 0; i < len; ++i) {
+                const int v = gi * LY::G + i;
+                const int k = sk[v];
+                const Rec<NPL> r = rn;
+                const uint4 hd = hn;
+                {
+                    const int kn = sk[v + 1 < n ? v + 1 : v];
+#pragma unroll
+                    for (int q = 0; q < Rec<NPL>::W; ++q)
+                        rn.w[q] = __ldg(reinterpret_cast<const uint32_t*>(rec_base + (size_t)kn * 32 * Rec<NPL>::B) + q);
+                    hn = __ldg(reinterpret_cast<const uint4*>(hdr_base + 4 * kn));
                 }
-                const int e = h * a.K + k;
-                const uint32_t hd = __ldg(a.hdr + 2 * e);
-                const uint32_t ovf = __ldg(a.hdr + 2 * e + 1);
-                Rec<NPL> r;
-                load_rec<NPL>(a.rec, e, lane, r);
+                Planes<NC, NPL> D, Bv;
+                if constexpr (PD) {
+                    const float* Dp = a.diag_dict + ((size_t)(h * a.K + k) * NC) * N;
+                    vld<float, NPL>(Dp + lane * NPL, D.v[0]);
+                    if constexpr (NC == 2) vld<float, NPL>(Dp + N + lane * NPL, D.v[1]);
+                } else {
+                    const T* Dp = reinterpret_cast<const T*>(sp) + (size_t)i * row;
+                    sld<T, NPL>(Dp + lane * NPL, D.v[0]);
+                    if constexpr (NC == 2) sld<T, NPL>(Dp + N + lane * NPL, D.v[1]);
+                }
+                const T* Bp = reinterpret_cast<const T*>(sp + LY::OFF_B) + (size_t)i * row;
+                sld<T, NPL>(Bp + lane * NPL, Bv.v[0]);
+                if constexpr (NC == 2) sld<T, NPL>(Bp + N + lane * NPL, Bv.v[1]);
                 float vre[NPL], vim[NPL];
 #pragma unroll
                 for (int u = 0; u < NPL; ++u) {
@@ -512,24 +891,31 @@ __global__ void __launch_bounds__(WARPS * 32) k_fwd_fused(FusedArgs a) {
                     vre[u] = D.v[0][u] * cre[u] - di * cim[u];
                     vim[u] = D.v[0][u] * cim[u] + di * cre[u];
                 }
-                sts_row<NC, NPL>(vb[buf], lane, vre, vim);
+                SV* vb = xb + (v & 1) * (N + 1);
+                sts_row<NC, NPL>(vb, lane, vre, vim);
                 __syncwarp();
-                float are[NPL], aim[NPL];
+                float zr[NPL], zi[NPL];
 #pragma unroll
-                for (int u = 0; u < NPL; ++u) { are[u] = 0.f; aim[u] = 0.f; }
-                if (ovf) gather_sum_csr<NC, NPL>(vb[buf], a.pstart, a.psrc, e, N, lane, are, aim);
-                else gather_sum<NC, NPL>(vb[buf], r, hd, are, aim);
-                Planes<NC, NPL> hn;
+                for (int u = 0; u < NPL; ++u) { zr[u] = 0.f; zi[u] = 0.f; }
+                if (hd.y) gather_sum_csr<NC, NPL>(vb, a.pstart, a.psrc, h * a.K + k, N, lane, zr, zi);
+                else gather_sum<NC, NPL>(vb, r, hd.x, zr, zi);
+                Planes<NC, NPL> hv;
 #pragma unroll
                 for (int u = 0; u < NPL; ++u) {
-                    cre[u] = are[u] + Bv.v[0][u];
-                    cim[u] = NC == 2 ? aim[u] + Bv.v[NC - 1][u] : 0.f;
-                    hn.v[0][u] = cre[u];
-                    if constexpr (NC == 2) hn.v[NC - 1][u] = cim[u];
+                    cre[u] = zr[u] + Bv.v[0][u];
+                    cim[u] = NC == 2 ? zi[u] + Bv.v[NC - 1][u] : 0.f;
+                    hv.v[0][u] = cre[u];
+                    if constexpr (NC == 2) hv.v[NC - 1][u] = cim[u];
                 }
-                store_planes<T, NC, NPL>(hout + ((size_t)s * a.L + t) * row + lane * NPL, hn, N);
+                store_planes<T, NC, NPL>(hout, hv, N);
+                hout += row;
             }
+            __syncwarp();
+            ++consumed;
+            pump<T, T, NC, NPL, PD, false>(a, fc, consumed, ring, bars, lane);
         }
+        have = has_next;
+        it = nx;
     }
 }
 
@@ -537,121 +923,218 @@ __global__ void __launch_bounds__(WARPS * 32) k_fwd_fused(FusedArgs a) {
 // backward (transposed scan, reverse chunk order)
 // ============================================================================
 template <typename T, typename TE, int NC, int NPL, bool PD>
-__global__ void __launch_bounds__(WARPS * 32) k_bwd_fused(FusedArgs a) {
+__global__ void __launch_bounds__(CTA_THREADS, 1) k_bwd_fused(FusedArgs a) {
     using SV = typename SVal<NC>::type;
-    constexpr int NMAX = 32 * NPL;
-    __shared__ SV s_l[WARPS][2][NMAX];
+    using LY = Layout<T, NC, NPL, PD, true, (int)sizeof(TE)>;
+    constexpr int PF = LY::PF;
+    extern __shared__ __align__(128) uint8_t smem[];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint8_t* base = smem + (size_t)w * LY::w_bytes;
+    uint8_t* ring = base + LY::w_ring;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(base + LY::w_bar);
+    SV* xb = reinterpret_cast<SV*>(base + LY::w_x);
+    uint8_t* sk = base + LY::w_k;
     const int N = a.N;
-    const int total = a.S * a.C;
-    const TE* ein = static_cast<const TE*>(a.bias);
-    const T* hs = static_cast<const T*>(a.hsaved);
-    T* dbias = static_cast<T*>(a.out0);
     const size_t row = (size_t)NC * N;
-    while (true) {
-        __syncwarp();
-        int ticket = 0;
-        if (lane == 0) ticket = atomicAdd(a.ctrl, 1u);
-        ticket = __shfl_sync(0xffffffffu, ticket, 0);
-        if (ticket >= total) break;
-        const int cr = ticket / a.S, s = ticket - cr * a.S, h = s % a.H;
-        const int c = a.C - 1 - cr;
-        const int t0 = c * a.tau, t1 = min(t0 + a.tau, a.L);
+    const TE* ein = static_cast<const TE*>(a.bias);
+    if (lane == 0) {
+        for (int i = 0; i < PF; ++i) mbar_init(bars + i, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    int head = blockIdx.x % a.H;
+    FillCursor fc;
+    fc.valid[0] = next_item(a, head, lane, true, fc.it[0]);
+    fc.valid[1] = false;
+    fc.g = 0;
+    fc.q = 0;
+    KPre kp;
+    if (fc.valid[0]) kpre_load(a, kp, fc.it[0], lane);
+    uint32_t consumed = 0;
+    bool have = fc.valid[0];
+    Item it = fc.it[0];
+    while (have) {
+        Item nx;
+        const bool has_next = next_item(a, head, lane, true, nx);
+        if (has_next) { fc.it[1] = nx; fc.valid[1] = true; }
+        const int c = it.c, s = it.s, h = it.h, t0 = it.t0, t1 = it.t1, n = it.n;
+        const int ng = (n + LY::G - 1) / LY::G;
         const size_t ci = (size_t)s * a.C + c;
-        auto load_e = [&](int t, Planes<NC, NPL>& E) {
-            if (ein) load_planes<TE, NC, NPL>(ein + ((size_t)s * a.L + t) * row + lane * NPL, E, N);
-            else {
-#pragma unroll
-                for (int p = 0; p < NC; ++p)
-#pragma unroll
-                    for (int u = 0; u < NPL; ++u) E.v[p][u] = 0.f;
-            }
-        };
+        const size_t seq0 = (size_t)s * a.L;
+        __syncwarp();
+        kpre_store(a, kp, sk, n, lane, false);
+        if (has_next) kpre_load(a, kp, nx, lane);
+        __syncwarp();
+        pump<T, TE, NC, NPL, PD, true>(a, fc, consumed, ring, bars, lane);
+        const uint16_t* prow_base = a.dict_idx + (size_t)h * a.K * N + lane * NPL;
         auto load_P = [&](int k, int (&P)[NPL]) {
-            const uint16_t* p = a.dict_idx + (size_t)(h * a.K + k) * N + lane * NPL;
+            const uint16_t* p = prow_base + (size_t)k * N;
             if constexpr (NPL == 4) {
-                const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
-                P[0] = v.x & 0xffff; P[1] = v.x >> 16; P[2] = v.y & 0xffff; P[3] = v.y >> 16;
+                const uint2 vv = __ldg(reinterpret_cast<const uint2*>(p));
+                P[0] = vv.x & 0xffff; P[1] = vv.x >> 16; P[2] = vv.y & 0xffff; P[3] = vv.y >> 16;
             } else if constexpr (NPL == 2) {
-                const uint32_t v = __ldg(reinterpret_cast<const unsigned int*>(p));
-                P[0] = v & 0xffff; P[1] = v >> 16;
+                const uint32_t vv = __ldg(reinterpret_cast<const unsigned int*>(p));
+                P[0] = vv & 0xffff; P[1] = vv >> 16;
             } else {
                 P[0] = __ldg(p);
             }
 #pragma unroll
             for (int u = 0; u < NPL; ++u) P[u] = min(P[u], N - 1);
         };
-        // ---------------- Phase A': reverse local scan, zero incoming
-        float lre[NPL], lim[NPL], bpre[NPL], bpim[NPL];
-        {
-            Planes<NC, NPL> E;
-            load_e(t1 - 1, E);
+        auto load_D = [&](const uint8_t* sp, int ro, int k, Planes<NC, NPL>& D) {
+            if constexpr (PD) {
+                const float* Dp = a.diag_dict + ((size_t)(h * a.K + k) * NC) * N + lane * NPL;
+                vld<float, NPL>(Dp, D.v[0]);
+                if constexpr (NC == 2) vld<float, NPL>(Dp + N, D.v[1]);
+            } else {
+                const T* Dp = reinterpret_cast<const T*>(sp) + (size_t)ro * row + lane * NPL;
+                sld<T, NPL>(Dp, D.v[0]);
+                if constexpr (NC == 2) sld<T, NPL>(Dp + N, D.v[1]);
+            }
+        };
+        auto load_e_direct = [&](int t, float (&er)[NPL], float (&ei)[NPL]) {
 #pragma unroll
-            for (int u = 0; u < NPL; ++u) { lre[u] = E.v[0][u]; lim[u] = NC == 2 ? E.v[NC - 1][u] : 0.f; }
-            Planes<NC, NPL> Dn, En;
-            int kn = load_k(a.kstar, (size_t)s * a.L + (t1 - 1), a.K, 0);
-            load_diag_own<T, NC, NPL, PD>(a, ((size_t)s * a.L + (t1 - 1)) * row, h, kn, lane, Dn);
-            if (t1 - 1 > t0) load_e(t1 - 2, En);
-            for (int t = t1 - 1; t >= t0; --t) {
-                const int buf = (t1 - 1 - t) & 1;
-                const int k = kn;
-                Planes<NC, NPL> D = Dn, Ep = En;
-                if (t - 1 >= t0) {
-                    kn = load_k(a.kstar, (size_t)s * a.L + t - 1, a.K, 0);
-                    load_diag_own<T, NC, NPL, PD>(a, ((size_t)s * a.L + t - 1) * row, h, kn, lane, Dn);
-                    if (t - 2 >= t0) load_e(t - 2, En);
-                }
+            for (int u = 0; u < NPL; ++u) { er[u] = 0.f; ei[u] = 0.f; }
+            if (ein) {
+                vld<TE, NPL>(ein + (seq0 + t) * row + lane * NPL, er);
+                if constexpr (NC == 2) vld<TE, NPL>(ein + (seq0 + t) * row + N + lane * NPL, ei);
+            }
+        };
+        // ---------------- Phase A': reverse local scan from zero incoming adjoint
+        float lre[NPL], lim[NPL], bpre[NPL], bpim[NPL];
+        load_e_direct(t1 - 1, lre, lim);
+        int Pn[NPL];
+        load_P(sk[n - 1], Pn);
+        for (int gi = 0; gi < ng; ++gi) {
+            const int slot = consumed % PF;
+            mbar_wait(bars + slot, (consumed / PF) & 1);
+            const uint8_t* sp = ring + (size_t)slot * LY::SLOT;
+            const int len = min(LY::G, n - gi * LY::G);
+            for (int i = 0; i < len; ++i) {
+                const int v = gi * LY::G + i;
+                const int t = t1 - 1 - v;
+                const int ro = len - 1 - i;           // row offset of time t in the slot
+                const int k = sk[t - t0];
                 int P[NPL];
-                load_P(k, P);
-                sts_row<NC, NPL>(s_l[w][buf], lane, lre, lim);
+#pragma unroll
+                for (int u = 0; u < NPL; ++u) P[u] = Pn[u];
+                if (t > t0) load_P(sk[t - 1 - t0], Pn);
+                Planes<NC, NPL> D;
+                load_D(sp, ro, k, D);
+                float er[NPL], ei[NPL];
+#pragma unroll
+                for (int u = 0; u < NPL; ++u) { er[u] = 0.f; ei[u] = 0.f; }
+                if (ein && t > t0) {
+                    const TE* ep = reinterpret_cast<const TE*>(sp + LY::OFF_E) + (size_t)ro * row + lane * NPL;
+                    sld<TE, NPL>(ep, er);
+                    if constexpr (NC == 2) sld<TE, NPL>(ep + N, ei);
+                }
+                SV* lb = xb + (v & 1) * (N + 1);
+                sts_row<NC, NPL>(lb, lane, lre, lim);
                 __syncwarp();
 #pragma unroll
                 for (int u = 0; u < NPL; ++u) {
-                    const SV lp = s_l[w][buf][P[u]];
+                    const SV lp = lb[P[u]];
                     const float dr = D.v[0][u], di = NC == 2 ? D.v[NC - 1][u] : 0.f;
-                    // conj(D) * lamP
-                    const float br = dr * re_of<NC>(lp) + di * im_of<NC>(lp);
-                    const float bi = dr * im_of<NC>(lp) - di * re_of<NC>(lp);
-                    if (t > t0) { lre[u] = Ep.v[0][u] + br; lim[u] = (NC == 2 ? Ep.v[NC - 1][u] : 0.f) + bi; }
-                    else { bpre[u] = br; bpim[u] = bi; }
+                    lre[u] = er[u] + dr * re_of<NC>(lp) + di * im_of<NC>(lp);   // e_{t-1} + conj(D) lamP
+                    lim[u] = ei[u] + dr * im_of<NC>(lp) - di * re_of<NC>(lp);
                 }
             }
+            ++consumed;
+            pump<T, TE, NC, NPL, PD, true>(a, fc, consumed, ring, bars, lane);
         }
-        // ---------------- chain: mu_c (wait) -> mu_{c-1} = beta'_c + Abar_c^T mu_c (publish)
-        float mre[NPL], mim[NPL];
-        if (c == a.C - 1) {
 #pragma unroll
-            for (int u = 0; u < NPL; ++u) { mre[u] = 0.f; mim[u] = 0.f; }
-            if (a.lam_in) {
-                vld<float, NPL>(a.lam_in + (size_t)s * row + lane * NPL, mre);
-                if constexpr (NC == 2) vld<float, NPL>(a.lam_in + (size_t)s * row + N + lane * NPL, mim);
-            }
-        } else {
-            wait_flag(a.ctrl + 1 + ci);
-            vld_cg<NPL>(a.mu + ci * row + lane * NPL, mre);
-            if constexpr (NC == 2) vld_cg<NPL>(a.mu + ci * row + N + lane * NPL, mim);
-        }
-        {
-            __syncwarp();            // Phase A''s last smem reads are done
-            sts_row<NC, NPL>(s_l[w][0], lane, mre, mim);
+        for (int u = 0; u < NPL; ++u) { bpre[u] = lre[u]; bpim[u] = lim[u]; }   // beta'_c (e term was zero at t0)
+        // publish beta'_c (the chunk's aggregate for the transposed scan), flag = 1
+        if (c > 0) {
+            vst_f<NPL>(a.betap + ci * row + lane * NPL, bpre);
+            if constexpr (NC == 2) vst_f<NPL>(a.betap + ci * row + N + lane * NPL, bpim);
+            __threadfence();
             __syncwarp();
-            float nr[NPL], ni[NPL];
+            if (lane == 0) st_release(flag_ptr(a, ci), 1u);
+        }
+        // ---------------- decoupled look-forward for mu_c (adjoint entering this chunk's last
+        // step from the chunks after it): fold beta'_m + Abar_m^T (.) of the successors
+        // between this chunk and the nearest one that already published its inclusive
+        // value (flag 2: mu_{m-1} ready).  Same arithmetic as the chain: deterministic.
+        // Abar_m^T is a pure gather that reuses the forward (pi_bar, d_bar).
+        auto applyT = [&](const int (&pk)[NPL], const float (&dr)[NPL], const float (&di)[NPL], const float (&br)[NPL],
+                          const float (&bi)[NPL], float (&xr)[NPL], float (&xi)[NPL]) {
+            SV* xbuf = xb;
+            __syncwarp();
+            sts_row<NC, NPL>(xbuf, lane, xr, xi);
+            __syncwarp();
 #pragma unroll
             for (int u = 0; u < NPL; ++u) {
-                const int j = lane * NPL + u;
-                const int pj = min((int)a.cs.pi[ci * N + j], N - 1);
-                const float dr = a.cs.d[ci * row + j], di = NC == 2 ? a.cs.d[ci * row + N + j] : 0.f;
-                const SV mp = s_l[w][0][pj];
-                nr[u] = bpre[u] + dr * re_of<NC>(mp) + di * im_of<NC>(mp);
-                ni[u] = bpim[u] + dr * im_of<NC>(mp) - di * re_of<NC>(mp);
+                const SV xp = xbuf[pk[u]];
+                xr[u] = br[u] + dr[u] * re_of<NC>(xp) + di[u] * im_of<NC>(xp);   // beta' + conj(d) x[pi]
+                xi[u] = bi[u] + dr[u] * im_of<NC>(xp) - di[u] * re_of<NC>(xp);
             }
+        };
+        auto load_fwd_agg = [&](size_t cm, int (&pk)[NPL], float (&dr)[NPL], float (&di)[NPL]) {
+#pragma unroll
+            for (int u = 0; u < NPL; ++u) { pk[u] = min((int)__ldg(a.cs.pi + cm * N + lane * NPL + u), N - 1); di[u] = 0.f; }
+            vld<float, NPL>(a.cs.d + cm * row + lane * NPL, dr);
+            if constexpr (NC == 2) vld<float, NPL>(a.cs.d + cm * row + N + lane * NPL, di);
+        };
+        float mre[NPL], mim[NPL];
+        {
+            int mP = a.C;            // mu_{mP-1} is known; C: mu_{C-1} = lam_in
+            if (c + 1 < a.C && !a.debug_nochain) {
+                while (true) {
+                    const int m = c + 1 + lane;
+                    const uint32_t f = m < a.C ? ld_relaxed(flag_ptr(a, (size_t)s * a.C + m)) : 2u;
+                    const uint32_t b2 = __ballot_sync(0xffffffffu, f == 2u);
+                    const uint32_t b0 = __ballot_sync(0xffffffffu, f == 0u);
+                    if (b2) {
+                        const int first = __ffs(b2) - 1;
+                        if ((b0 & ((1u << first) - 1u)) == 0u) { mP = c + 1 + first; break; }
+                    }
+                    __nanosleep(64);
+                }
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            } else if (c + 1 < a.C) {
+                mP = c + 1;
+            }
+            if (mP >= a.C) {
+#pragma unroll
+                for (int u = 0; u < NPL; ++u) { mre[u] = 0.f; mim[u] = 0.f; }
+                if (a.lam_in) {
+                    vld<float, NPL>(a.lam_in + (size_t)s * row + lane * NPL, mre);
+                    if constexpr (NC == 2) vld<float, NPL>(a.lam_in + (size_t)s * row + N + lane * NPL, mim);
+                }
+            } else {
+                const size_t cm = (size_t)s * a.C + mP - 1;
+                vld_cg<NPL>(a.mu + cm * row + lane * NPL, mre);
+                if constexpr (NC == 2) vld_cg<NPL>(a.mu + cm * row + N + lane * NPL, mim);
+            }
+            for (int m = mP - 1; m > c; --m) {
+                const size_t cm = (size_t)s * a.C + m;
+                int pk[NPL];
+                float dr[NPL], di[NPL], br[NPL], bi[NPL];
+                load_fwd_agg(cm, pk, dr, di);
+#pragma unroll
+                for (int u = 0; u < NPL; ++u) bi[u] = 0.f;
+                vld_cg<NPL>(a.betap + cm * row + lane * NPL, br);
+                if constexpr (NC == 2) vld_cg<NPL>(a.betap + cm * row + N + lane * NPL, bi);
+                applyT(pk, dr, di, br, bi, mre, mim);
+            }
+        }
+        // ---------------- inclusive mu_{c-1} = beta'_c + Abar_c^T mu_c, flag = 2 (or dh0 at c = 0)
+        {
+            int pk[NPL];
+            float dr[NPL], di[NPL], nr[NPL], ni[NPL];
+            load_fwd_agg(ci, pk, dr, di);
+#pragma unroll
+            for (int u = 0; u < NPL; ++u) { nr[u] = mre[u]; ni[u] = mim[u]; }
+            applyT(pk, dr, di, bpre, bpim, nr, ni);
             if (c > 0) {
                 const size_t cp = ci - 1;
                 vst_f<NPL>(a.mu + cp * row + lane * NPL, nr);
                 if constexpr (NC == 2) vst_f<NPL>(a.mu + cp * row + N + lane * NPL, ni);
                 __threadfence();
                 __syncwarp();
-                if (lane == 0) st_release(a.ctrl + 1 + cp, 1u);
+                if (lane == 0) st_release(flag_ptr(a, ci), 2u);
             } else if (a.dh0) {
                 vst_f<NPL>(a.dh0 + (size_t)s * row + lane * NPL, nr);
                 if constexpr (NC == 2) vst_f<NPL>(a.dh0 + (size_t)s * row + N + lane * NPL, ni);
@@ -660,17 +1143,44 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_fused(FusedArgs a) {
         }
         // ---------------- Phase C': replay, emit db, dD, g
         {
-            Planes<NC, NPL> E;
-            load_e(t1 - 1, E);
+            float er0[NPL], ei0[NPL];
+            load_e_direct(t1 - 1, er0, ei0);
 #pragma unroll
-            for (int u = 0; u < NPL; ++u) { lre[u] = E.v[0][u] + mre[u]; lim[u] = (NC == 2 ? E.v[NC - 1][u] : 0.f) + mim[u]; }
-            Planes<NC, NPL> Dn, En, Hn;
-            int kn = load_k(a.kstar, (size_t)s * a.L + (t1 - 1), a.K, 0);
-            load_diag_own<T, NC, NPL, PD>(a, ((size_t)s * a.L + (t1 - 1)) * row, h, kn, lane, Dn);
-            if (t1 - 1 > t0) load_e(t1 - 2, En);
-            auto load_h = [&](int t, Planes<NC, NPL>& Hp) {   // h_{t-1}
-                if (t > 0) load_planes<T, NC, NPL>(hs + ((size_t)s * a.L + t - 1) * row + lane * NPL, Hp, N);
-                else {
+            for (int u = 0; u < NPL; ++u) { lre[u] = er0[u] + mre[u]; lim[u] = ei0[u] + mim[u]; }
+        }
+        T* dbp = static_cast<T*>(a.out0) + (seq0 + t1 - 1) * row + lane * NPL;
+        T* ddp = PD ? nullptr : static_cast<T*>(a.out1) + (seq0 + t1 - 1) * row + lane * NPL;
+        float* ddf = PD ? static_cast<float*>(a.out1) + (seq0 + t1 - 1) * row + lane * NPL : nullptr;
+        load_P(sk[n - 1], Pn);
+        for (int gi = 0; gi < ng; ++gi) {
+            const int slot = consumed % PF;
+            mbar_wait(bars + slot, (consumed / PF) & 1);
+            const uint8_t* sp = ring + (size_t)slot * LY::SLOT;
+            const int len = min(LY::G, n - gi * LY::G);
+            for (int i = 0; i < len; ++i) {
+                const int v = gi * LY::G + i;
+                const int t = t1 - 1 - v;
+                const int ro = len - 1 - i;
+                const int k = sk[t - t0];
+                int P[NPL];
+#pragma unroll
+                for (int u = 0; u < NPL; ++u) P[u] = Pn[u];
+                if (t > t0) load_P(sk[t - 1 - t0], Pn);
+                Planes<NC, NPL> D, Hp;
+                load_D(sp, ro, k, D);
+                float er[NPL], ei[NPL];
+#pragma unroll
+                for (int u = 0; u < NPL; ++u) { er[u] = 0.f; ei[u] = 0.f; }
+                if (ein && t > t0) {
+                    const TE* ep = reinterpret_cast<const TE*>(sp + LY::OFF_E) + (size_t)ro * row + lane * NPL;
+                    sld<TE, NPL>(ep, er);
+                    if constexpr (NC == 2) sld<TE, NPL>(ep + N, ei);
+                }
+                if (t > 0) {
+                    const T* hp = reinterpret_cast<const T*>(sp + LY::OFF_H) + (size_t)ro * row + lane * NPL;
+                    sld<T, NPL>(hp, Hp.v[0]);
+                    if constexpr (NC == 2) sld<T, NPL>(hp + N, Hp.v[1]);
+                } else {
 #pragma unroll
                     for (int p = 0; p < NC; ++p)
 #pragma unroll
@@ -680,70 +1190,60 @@ __global__ void __launch_bounds__(WARPS * 32) k_bwd_fused(FusedArgs a) {
                         if constexpr (NC == 2) vld<float, NPL>(a.h0 + (size_t)s * row + N + lane * NPL, Hp.v[1]);
                     }
                 }
-            };
-            load_h(t1 - 1, Hn);
-            for (int t = t1 - 1; t >= t0; --t) {
-                const int buf = (t1 - 1 - t) & 1;
-                const int k = kn;
-                Planes<NC, NPL> D = Dn, Ep = En, Hp = Hn;
-                if (t - 1 >= t0) {
-                    kn = load_k(a.kstar, (size_t)s * a.L + t - 1, a.K, 0);
-                    load_diag_own<T, NC, NPL, PD>(a, ((size_t)s * a.L + t - 1) * row, h, kn, lane, Dn);
-                    if (t - 2 >= t0) load_e(t - 2, En);
-                    load_h(t - 1, Hn);
-                }
-                int P[NPL];
-                load_P(k, P);
-                const size_t off = ((size_t)s * a.L + t) * row + lane * NPL;
                 {
                     Planes<NC, NPL> Lv;
 #pragma unroll
                     for (int u = 0; u < NPL; ++u) { Lv.v[0][u] = lre[u]; if constexpr (NC == 2) Lv.v[NC - 1][u] = lim[u]; }
-                    store_planes<T, NC, NPL>(dbias + off, Lv, N);
+                    store_planes<T, NC, NPL>(dbp, Lv, N);
                 }
-                sts_row<NC, NPL>(s_l[w][buf], lane, lre, lim);
+                SV* lb = xb + (v & 1) * (N + 1);
+                sts_row<NC, NPL>(lb, lane, lre, lim);
                 __syncwarp();
                 Planes<NC, NPL> dD;
                 float gv = 0.f;
 #pragma unroll
                 for (int u = 0; u < NPL; ++u) {
-                    const SV lp = s_l[w][buf][P[u]];
+                    const SV lp = lb[P[u]];
                     const float lr = re_of<NC>(lp), li = im_of<NC>(lp);
                     const float dr = D.v[0][u], di = NC == 2 ? D.v[NC - 1][u] : 0.f;
                     const float hr = Hp.v[0][u], hi = NC == 2 ? Hp.v[NC - 1][u] : 0.f;
-                    // dD = conj(h) * lamP
-                    dD.v[0][u] = hr * lr + hi * li;
+                    dD.v[0][u] = hr * lr + hi * li;                       // conj(h) * lamP
                     if constexpr (NC == 2) dD.v[NC - 1][u] = hr * li - hi * lr;
-                    // g += Re(conj(lamP) * D * h)
                     const float pr = dr * hr - di * hi, pim = dr * hi + di * hr;
-                    gv += lr * pr + li * pim;
-                    if (t > t0) {
-                        lre[u] = Ep.v[0][u] + dr * lr + di * li;
-                        lim[u] = (NC == 2 ? Ep.v[NC - 1][u] : 0.f) + dr * li - di * lr;
-                    }
+                    gv += lr * pr + li * pim;                             // Re(conj(lamP) D h)
+                    lre[u] = er[u] + dr * lr + di * li;                   // e_{t-1} + conj(D) lamP
+                    lim[u] = ei[u] + dr * li - di * lr;
                 }
-                if constexpr (PD) store_planes<float, NC, NPL>(static_cast<float*>(a.out1) + off, dD, N);
-                else store_planes<T, NC, NPL>(static_cast<T*>(a.out1) + off, dD, N);
+                if constexpr (PD) { store_planes<float, NC, NPL>(ddf, dD, N); ddf -= row; }
+                else { store_planes<T, NC, NPL>(ddp, dD, N); ddp -= row; }
+                dbp -= row;
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) gv += __shfl_xor_sync(0xffffffffu, gv, o);
-                if (a.gsel && lane == 0) a.gsel[(size_t)s * a.L + t] = gv;
+                if (a.gsel && lane == 0) a.gsel[seq0 + t] = gv;
             }
+            __syncwarp();
+            ++consumed;
+            pump<T, TE, NC, NPL, PD, true>(a, fc, consumed, ring, bars, lane);
         }
+        have = has_next;
+        it = nx;
     }
 }
 
 }  // namespace fused
 
+
 // ---------------------------------------------------------------------------
-// host-side launchers
+// host-side sizing helpers
 // ---------------------------------------------------------------------------
-inline size_t fused_plan_bytes(int64_t H, int64_t K, int NPL) {
-    return (((size_t)H * K * 32 * NPL * fused::MU + 255) & ~(size_t)255) + (((size_t)H * K * 8 + 255) & ~(size_t)255);
+inline size_t fused_rec_bytes(int64_t H, int64_t K) {
+    return (((size_t)H * K * 32 * fused::Rec<4>::B) + 255) & ~(size_t)255;   // NPL = 4 is the largest record
 }
+inline size_t fused_hdr_bytes(int64_t H, int64_t K) { return (((size_t)H * K * 16) + 255) & ~(size_t)255; }
+inline size_t fused_plan_bytes(int64_t H, int64_t K) { return fused_rec_bytes(H, K) + fused_hdr_bytes(H, K); }
 
-inline size_t fused_ctrl_bytes(int64_t S, int C) { return (((size_t)(1 + S * C) * 4 + 255) & ~(size_t)255); }
-
-inline size_t fused_ws_bytes(int64_t S, int C) { return fused_ctrl_bytes(S, C); }
+// [0, H): per-head ticket counters; then one flag per (sequence, chunk)
+inline size_t fused_ctrl_bytes(int64_t S, int C, int64_t H) { return (((size_t)(H + S * C) * 4 + 255) & ~(size_t)255); }
 
 inline int fused_npl(int64_t N) {
     if (N == 32) return 1;
@@ -752,7 +1252,7 @@ inline int fused_npl(int64_t N) {
     return 0;
 }
 
-inline int fused_grid(int total_items) {
+inline int num_sms() {
     static int sms = 0;
     if (!sms) {
         int dev = 0;
@@ -760,8 +1260,12 @@ inline int fused_grid(int total_items) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         if (sms <= 0) sms = 148;
     }
-    const int ctas_per_sm = 2;
-    int g = sms * ctas_per_sm;
+    return sms;
+}
+
+// persistent grid: ctas_per_sm resident CTAs per SM (dynamic tickets balance the items)
+inline int fused_grid(int total_items, int ctas_per_sm) {
+    int g = num_sms() * ctas_per_sm;
     const int need = (total_items + fused::WARPS - 1) / fused::WARPS;
     return g < need ? g : need;
 }

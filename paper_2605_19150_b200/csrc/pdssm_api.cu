@@ -111,11 +111,11 @@ size_t ws_bytes_g(const Geo& g, int op) {
         case PDSSM_OP_SELECT:
             return align256((size_t)g.S * g.L * g.K * 4);
         case PDSSM_OP_FWD:
-            return plan_bytes(g) + (g.P > 0 ? seq_act_bytes(g) : 0) + fused_plan_bytes(g.H, g.K, 4) +
-                   fused_ctrl_bytes(g.S, g.C);
+            return plan_bytes(g) + (g.P > 0 ? seq_act_bytes(g) : 0) + fused_plan_bytes(g.H, g.K) +
+                   fused_ctrl_bytes(g.S, g.C, g.H);
         case PDSSM_OP_BWD:
             return 2 * cs_f_bytes(g) + (g.P > 0 ? seq_f_bytes(g) : 0) +
-                   (g.diag_mode == PDSSM_DIAG_PER_DICT ? seq_f_bytes(g) : 0) + fused_ctrl_bytes(g.S, g.C);
+                   (g.diag_mode == PDSSM_DIAG_PER_DICT ? seq_f_bytes(g) : 0) + fused_ctrl_bytes(g.S, g.C, g.H);
         case PDSSM_OP_SEGMENT: {
             size_t fwd = plan_bytes(g) + chunk_state_bytes_g(g);
             size_t bwd = 2 * cs_f_bytes(g) + (g.P > 0 ? seq_f_bytes(g) : 0);
@@ -214,7 +214,7 @@ bool path_generic_forced() {
 }
 
 bool fused_applicable(const Geo& g, std::initializer_list<const void*> ptrs) {
-    if (path_generic_forced() || fused_npl(g.N) == 0) return false;
+    if (path_generic_forced() || fused_npl(g.N) == 0 || g.tau > fused::TAUMAX) return false;
     for (const void* p : ptrs)
         if (misaligned(p, 16)) return false;
     return true;
@@ -227,6 +227,27 @@ pdssm_status with_npl(int npl, F&& f) {
     return f(std::integral_constant<int, 4>{});
 }
 
+// resident CTAs per SM for a fused kernel using `smem` bytes per CTA (env override for tuning)
+int fused_ctas_per_sm(size_t smem) {
+    int want = 1;
+    if (const char* e = getenv("PDSSM_CTAS_PER_SM")) want = atoi(e);
+    int fit = (int)((227 * 1024) / (smem + 1024));
+    if (fit < 1) fit = 1;
+    return want < fit ? (want < 1 ? 1 : want) : fit;
+}
+
+template <typename K>
+pdssm_status launch_fused(K kernel, const fused::FusedArgs& fa, size_t smem, int items, cudaStream_t st,
+                          const char* what) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return fail(PDSSM_ERR_CUDA, "%s attribute: %s", what, cudaGetErrorString(e));
+    const int grid = fused_grid(items, fused_ctas_per_sm(smem));
+    fused::FusedArgs f2 = fa;
+    f2.debug_nochain = getenv("PDSSM_DEBUG_NOCHAIN") != nullptr;
+    kernel<<<grid, fused::CTA_THREADS, smem, st>>>(f2);
+    return cuda_check(what);
+}
+
 pdssm_status fwd_fused(const Geo& g, fused::FusedArgs& fa, uint8_t* rec, uint32_t* hdr, cudaStream_t st) {
     const int npl = fused_npl(g.N);
     return with_npl(npl, [&](auto nv) {
@@ -235,17 +256,17 @@ pdssm_status fwd_fused(const Geo& g, fused::FusedArgs& fa, uint8_t* rec, uint32_
             fa.dict_idx, rec, hdr, (int)g.N);
         pdssm_status r = cuda_check("build_fused_plan");
         if (r) return r;
-        cudaError_t e = cudaMemsetAsync(fa.ctrl, 0, fused_ctrl_bytes(g.S, g.C), st);
+        cudaError_t e = cudaMemsetAsync(fa.ctrl, 0, fused_ctrl_bytes(g.S, g.C, g.H), st);
         if (e != cudaSuccess) return fail(PDSSM_ERR_CUDA, "memset ctrl: %s", cudaGetErrorString(e));
-        const int grid = fused_grid((int)(g.S * g.C));
         return with_act(g.dtype, [&](auto tv) {
             using T = decltype(tv);
             return with_nc(g.nc, [&](auto ncv) {
                 constexpr int NC = decltype(ncv)::value;
                 return with_pd(g.diag_mode, [&](auto pdv) {
                     constexpr bool PD = decltype(pdv)::value;
-                    fused::k_fwd_fused<T, NC, NPL, PD><<<grid, fused::WARPS * 32, 0, st>>>(fa);
-                    return cuda_check("fwd_fused");
+                    using WS = fused::Layout<T, NC, NPL, PD, false>;
+                    return launch_fused(fused::k_fwd_fused<T, NC, NPL, PD>, fa, WS::bytes,
+                                        (int)(g.S * g.C), st, "fwd_fused");
                 });
             });
         });
@@ -254,9 +275,8 @@ pdssm_status fwd_fused(const Geo& g, fused::FusedArgs& fa, uint8_t* rec, uint32_
 
 template <typename TE>
 pdssm_status bwd_fused(const Geo& g, fused::FusedArgs& fa, cudaStream_t st) {
-    cudaError_t e = cudaMemsetAsync(fa.ctrl, 0, fused_ctrl_bytes(g.S, g.C), st);
+    cudaError_t e = cudaMemsetAsync(fa.ctrl, 0, fused_ctrl_bytes(g.S, g.C, g.H), st);
     if (e != cudaSuccess) return fail(PDSSM_ERR_CUDA, "memset ctrl: %s", cudaGetErrorString(e));
-    const int grid = fused_grid((int)(g.S * g.C));
     return with_npl(fused_npl(g.N), [&](auto nv) {
         constexpr int NPL = decltype(nv)::value;
         return with_act(g.dtype, [&](auto tv) {
@@ -266,8 +286,9 @@ pdssm_status bwd_fused(const Geo& g, fused::FusedArgs& fa, cudaStream_t st) {
                 return with_pd(g.diag_mode, [&](auto pdv) {
                     constexpr bool PD = decltype(pdv)::value;
                     using TEE = typename std::conditional<std::is_same<TE, void>::value, T, TE>::type;
-                    fused::k_bwd_fused<T, TEE, NC, NPL, PD><<<grid, fused::WARPS * 32, 0, st>>>(fa);
-                    return cuda_check("bwd_fused");
+                    using WS = fused::Layout<T, NC, NPL, PD, true, (int)sizeof(TEE)>;
+                    return launch_fused(fused::k_bwd_fused<T, TEE, NC, NPL, PD>, fa, WS::bytes,
+                                        (int)(g.S * g.C), st, "bwd_fused");
                 });
             });
         });
@@ -426,9 +447,9 @@ pdssm_status pdssm_scan_fwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
     uint16_t* pstart = bump.take<uint16_t>((size_t)g.H * g.K * (g.N + 1) * 2);
     uint16_t* psrc = bump.take<uint16_t>((size_t)g.H * g.K * g.N * 2);
     void* hscratch = g.P > 0 ? bump.take<char>(seq_act_bytes(g)) : nullptr;
-    uint8_t* frec = bump.take<uint8_t>((size_t)g.H * g.K * 32 * 4 * fused::MU);
-    uint32_t* fhdr = bump.take<uint32_t>((size_t)g.H * g.K * 8);
-    uint32_t* ctrl = bump.take<uint32_t>(fused_ctrl_bytes(g.S, g.C));
+    uint8_t* frec = bump.take<uint8_t>(fused_rec_bytes(g.H, g.K));
+    uint32_t* fhdr = bump.take<uint32_t>(fused_hdr_bytes(g.H, g.K));
+    uint32_t* ctrl = bump.take<uint32_t>(fused_ctrl_bytes(g.S, g.C, g.H));
     void* hout = h_out_opt ? h_out_opt : hscratch;
     ChunkStateView cs = cs_view(g, chunk_state);
     if ((r = launch_plan(g, dict_idx, pstart, psrc, st))) return r;
@@ -488,7 +509,7 @@ pdssm_status pdssm_scan_bwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
     float* mu = bump.take<float>(cs_f_bytes(g));
     float* ebuf = g.P > 0 ? bump.take<float>(seq_f_bytes(g)) : nullptr;
     float* dDbuf = g.diag_mode == PDSSM_DIAG_PER_DICT ? bump.take<float>(seq_f_bytes(g)) : nullptr;
-    uint32_t* ctrl = bump.take<uint32_t>(fused_ctrl_bytes(g.S, g.C));
+    uint32_t* ctrl = bump.take<uint32_t>(fused_ctrl_bytes(g.S, g.C, g.H));
     ChunkStateView cs = cs_view(g, const_cast<void*>(chunk_state));
     const int thr = threads_for(g.N);
     const unsigned items = (unsigned)(g.S * g.C);
@@ -516,7 +537,7 @@ pdssm_status pdssm_scan_bwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
         fa.bias = dy_opt ? static_cast<const void*>(ebuf) : dh_opt;
         fa.hsaved = h_saved; fa.h0 = h0_opt; fa.lam_in = lam_in_opt; fa.cs = cs;
         fa.out0 = dbias; fa.out1 = g.diag_mode == PDSSM_DIAG_PER_DICT ? static_cast<void*>(dDbuf) : ddiag;
-        fa.gsel = gsel; fa.dh0 = dh0_opt; fa.mu = mu; fa.ctrl = ctrl;
+        fa.gsel = gsel; fa.dh0 = dh0_opt; fa.mu = mu; fa.betap = betap; fa.ctrl = ctrl;
         fa.H = (int)g.H; fa.L = (int)g.L; fa.N = (int)g.N; fa.K = (int)g.K; fa.tau = g.tau; fa.C = g.C;
         fa.S = (int)g.S; fa.flags = g.flags;
         r = dy_opt ? bwd_fused<float>(g, fa, st) : bwd_fused<void>(g, fa, st);
