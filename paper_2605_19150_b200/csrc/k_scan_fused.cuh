@@ -449,7 +449,8 @@ struct Layout {
     static constexpr size_t w_key = al16(w_ob + (size_t)N * SV);             // chain keys u16 [N]
     static constexpr size_t w_cnt = al16(w_key + (size_t)N * 2);             // chain counts int [N]
     static constexpr size_t w_k = al16(w_cnt + (size_t)N * 4);               // k* of the chunk [TAUMAX]
-    static constexpr size_t w_bytes = al16(w_k + TAUMAX);
+    static constexpr size_t w_g = al16(w_k + TAUMAX);                        // bwd g partials [32][33]
+    static constexpr size_t w_bytes = al16(w_g + (BWD ? 32 * 33 * 4 : 0));
     static constexpr size_t bytes = (size_t)WARPS * w_bytes;
 };
 
@@ -934,6 +935,7 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) k_bwd_fused(FusedArgs a) {
     uint64_t* bars = reinterpret_cast<uint64_t*>(base + LY::w_bar);
     SV* xb = reinterpret_cast<SV*>(base + LY::w_x);
     uint8_t* sk = base + LY::w_k;
+    float* gbuf = reinterpret_cast<float*>(base + LY::w_g);   // [32][33] per-lane g partials
     const int N = a.N;
     const size_t row = (size_t)NC * N;
     const TE* ein = static_cast<const TE*>(a.bias);
@@ -967,17 +969,17 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) k_bwd_fused(FusedArgs a) {
         __syncwarp();
         pump<T, TE, NC, NPL, PD, true>(a, fc, consumed, ring, bars, lane);
         const uint16_t* prow_base = a.dict_idx + (size_t)h * a.K * N + lane * NPL;
-        auto load_P = [&](int k, int (&P)[NPL]) {
+        // index row slice of entry k: raw words loaded one step ahead, decoded at use
+        auto load_P = [&](int k) -> uint2 {
             const uint16_t* p = prow_base + (size_t)k * N;
-            if constexpr (NPL == 4) {
-                const uint2 vv = __ldg(reinterpret_cast<const uint2*>(p));
-                P[0] = vv.x & 0xffff; P[1] = vv.x >> 16; P[2] = vv.y & 0xffff; P[3] = vv.y >> 16;
-            } else if constexpr (NPL == 2) {
-                const uint32_t vv = __ldg(reinterpret_cast<const unsigned int*>(p));
-                P[0] = vv & 0xffff; P[1] = vv >> 16;
-            } else {
-                P[0] = __ldg(p);
-            }
+            if constexpr (NPL == 4) return __ldg(reinterpret_cast<const uint2*>(p));
+            else if constexpr (NPL == 2) return make_uint2(__ldg(reinterpret_cast<const unsigned int*>(p)), 0u);
+            else return make_uint2((uint32_t)__ldg(p), 0u);
+        };
+        auto decode_P = [&](uint2 vv, int (&P)[NPL]) {
+            if constexpr (NPL == 4) { P[0] = vv.x & 0xffff; P[1] = vv.x >> 16; P[2] = vv.y & 0xffff; P[3] = vv.y >> 16; }
+            else if constexpr (NPL == 2) { P[0] = vv.x & 0xffff; P[1] = vv.x >> 16; }
+            else { P[0] = vv.x; }
 #pragma unroll
             for (int u = 0; u < NPL; ++u) P[u] = min(P[u], N - 1);
         };
@@ -1003,8 +1005,7 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) k_bwd_fused(FusedArgs a) {
         // ---------------- Phase A': reverse local scan from zero incoming adjoint
         float lre[NPL], lim[NPL], bpre[NPL], bpim[NPL];
         load_e_direct(t1 - 1, lre, lim);
-        int Pn[NPL];
-        load_P(sk[n - 1], Pn);
+        uint2 Pn = load_P(sk[n - 1]);
         for (int gi = 0; gi < ng; ++gi) {
             const int slot = consumed % PF;
             mbar_wait(bars + slot, (consumed / PF) & 1);
@@ -1016,9 +1017,8 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) k_bwd_fused(FusedArgs a) {
                 const int ro = len - 1 - i;           // row offset of time t in the slot
                 const int k = sk[t - t0];
                 int P[NPL];
-#pragma unroll
-                for (int u = 0; u < NPL; ++u) P[u] = Pn[u];
-                if (t > t0) load_P(sk[t - 1 - t0], Pn);
+                decode_P(Pn, P);
+                if (t > t0) Pn = load_P(sk[t - 1 - t0]);
                 Planes<NC, NPL> D;
                 load_D(sp, ro, k, D);
                 float er[NPL], ei[NPL];
@@ -1151,7 +1151,7 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) k_bwd_fused(FusedArgs a) {
         T* dbp = static_cast<T*>(a.out0) + (seq0 + t1 - 1) * row + lane * NPL;
         T* ddp = PD ? nullptr : static_cast<T*>(a.out1) + (seq0 + t1 - 1) * row + lane * NPL;
         float* ddf = PD ? static_cast<float*>(a.out1) + (seq0 + t1 - 1) * row + lane * NPL : nullptr;
-        load_P(sk[n - 1], Pn);
+        Pn = load_P(sk[n - 1]);
         for (int gi = 0; gi < ng; ++gi) {
             const int slot = consumed % PF;
             mbar_wait(bars + slot, (consumed / PF) & 1);
@@ -1163,9 +1163,8 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) k_bwd_fused(FusedArgs a) {
                 const int ro = len - 1 - i;
                 const int k = sk[t - t0];
                 int P[NPL];
-#pragma unroll
-                for (int u = 0; u < NPL; ++u) P[u] = Pn[u];
-                if (t > t0) load_P(sk[t - 1 - t0], Pn);
+                decode_P(Pn, P);
+                if (t > t0) Pn = load_P(sk[t - 1 - t0]);
                 Planes<NC, NPL> D, Hp;
                 load_D(sp, ro, k, D);
                 float er[NPL], ei[NPL];
@@ -1217,9 +1216,18 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) k_bwd_fused(FusedArgs a) {
                 if constexpr (PD) { store_planes<float, NC, NPL>(ddf, dD, N); ddf -= row; }
                 else { store_planes<T, NC, NPL>(ddp, dD, N); ddp -= row; }
                 dbp -= row;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) gv += __shfl_xor_sync(0xffffffffu, gv, o);
-                if (a.gsel && lane == 0) a.gsel[seq0 + t] = gv;
+                // g_t = sum over lanes of gv: park the partial, reduce 32 steps at a time
+                gbuf[(v & 31) * 33 + lane] = gv;
+                if ((v & 31) == 31 || v == n - 1) {
+                    __syncwarp();
+                    if (a.gsel && lane <= (v & 31)) {
+                        float acc = 0.f;
+#pragma unroll 8
+                        for (int q = 0; q < 32; ++q) acc += gbuf[lane * 33 + q];
+                        a.gsel[seq0 + (t1 - 1 - (v - (v & 31) + lane))] = acc;
+                    }
+                    __syncwarp();
+                }
             }
             __syncwarp();
             ++consumed;
