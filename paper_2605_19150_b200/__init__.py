@@ -24,6 +24,8 @@ __all__ = [
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libpdssm.so")
+if os.environ.get("PDSSM_LIB_VARIANT"):   # tuning experiments: variants/<name>.so built by tools/build_variant.sh
+    LIB_PATH = os.path.join(_HERE, "variants", os.environ["PDSSM_LIB_VARIANT"] + ".so")
 
 F32, BF16 = 0, 1
 PER_STEP, PER_DICT = 0, 1

@@ -33,8 +33,14 @@ namespace fused {
 
 constexpr int MU = 6;         // inline preimage capacity per target
 constexpr int TAUMAX = 256;   // fused-path chunk-length cap (k* staged in smem)
-constexpr int PF_FWD = 3;     // ring slots (groups of Layout::G steps) per warp
-constexpr int PF_BWD = 4;
+#ifndef PDSSM_PF_FWD
+#define PDSSM_PF_FWD 3
+#endif
+#ifndef PDSSM_PF_BWD
+#define PDSSM_PF_BWD 2
+#endif
+constexpr int PF_FWD = PDSSM_PF_FWD;     // ring slots (groups of Layout::G steps) per warp
+constexpr int PF_BWD = PDSSM_PF_BWD;
 
 // ------------------------------------------------------------------ vector IO
 template <typename T, int NPL>
@@ -159,6 +165,36 @@ __device__ __forceinline__ void store_planes(T* __restrict__ base, const Planes<
     if constexpr (NC == 2) vst<T, NPL>(base + N, o.v[1]);
 }
 
+// streamed output stores with an L2 evict_first policy (never re-read in this launch)
+template <typename T, int NPL>
+__device__ __forceinline__ void vst_stream(T* p, const float (&v)[NPL], uint64_t pol) {
+    if constexpr (std::is_same<T, float>::value && NPL == 4) {
+        asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v[0]), "f"(v[1]),
+                     "f"(v[2]), "f"(v[3]), "l"(pol)
+                     : "memory");
+    } else if constexpr (std::is_same<T, float>::value && NPL == 2) {
+        asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(p), "f"(v[0]), "f"(v[1]), "l"(pol)
+                     : "memory");
+    } else if constexpr (std::is_same<T, float>::value) {
+        asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v[0]), "l"(pol) : "memory");
+    } else if constexpr (NPL == 4) {
+        asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;" ::"l"(p), "r"(pack_bf16x2(v[0], v[1])),
+                     "r"(pack_bf16x2(v[2], v[3])), "l"(pol)
+                     : "memory");
+    } else if constexpr (NPL == 2) {
+        asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(pack_bf16x2(v[0], v[1])), "l"(pol)
+                     : "memory");
+    } else {
+        vst<T, NPL>(p, v);
+    }
+}
+template <typename T, int NC, int NPL>
+__device__ __forceinline__ void store_planes_stream(T* __restrict__ base, const Planes<NC, NPL>& o, int N,
+                                                    uint64_t pol) {
+    vst_stream<T, NPL>(base, o.v[0], pol);
+    if constexpr (NC == 2) vst_stream<T, NPL>(base + N, o.v[1], pol);
+}
+
 // ------------------------------------------------------------------ chain flags
 // Producer: data stores, __threadfence (every lane), __syncwarp, st.release flag.
 // Consumer: relaxed polling (no L1 invalidation per poll), then one acquire fence.
@@ -187,6 +223,26 @@ __device__ __forceinline__ void tma_1d(void* dst, const void* src, uint32_t byte
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(b))
+        : "memory");
+}
+// L2 eviction-priority policies (createpolicy) and the cache-hinted bulk copy:
+// Phase-A rows are kept (evict_last) for the replay's re-read, replay rows and all
+// streamed outputs are evict_first, so the replay working set stays L2-resident.
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void tma_1d_hint(void* dst, const void* src, uint32_t bytes, uint64_t* b, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(b)), "l"(pol)
         : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
@@ -227,76 +283,116 @@ __device__ __forceinline__ void sts_row(typename SVal<NC>::type* row, int lane, 
 }
 
 // ------------------------------------------------------------------ fused plan
-// For entry e = h*K + k and lane l: rec[e][l][u*MU + q] = q-th source (ascending
-// j) of target i = l*NPL + u, padded with the sentinel N (a zero slot of the
-// exchange buffer); hdr[e] = {M_0 | M_1<<8 | M_2<<16 | M_3<<24, ovf, 0, 0}
-// where M_u = max over lanes of the in-degree of slot u (warp-uniform trip
-// counts) and ovf != 0 if some M_u > MU (then the CSR plan is used).
+// The gather that realises the scatter (A_t v)[i] = sum_{j : P_t[j] = i} v[j] is
+// balanced per dictionary entry: targets are ranked by in-degree (descending,
+// ties by index) and rank r is computed by lane r % 32 in slot u = r / 32, so the
+// warp-uniform trip count of slot u, M_u = max in-degree inside the slot, is
+// small (random maps, N = 128: sum_u M_u = 7.0 on average vs 14.1 for the
+// natural i -> (i / NPL, i % NPL) assignment).  The computing lane writes the
+// target's sum to the exchange buffer; the owner of state i reads it back.
+// Record of (entry e, lane l), 32 bytes: byte u (< NPL) = target of slot u, then
+// per slot u its sources (ascending j) at REC_SOFF[u], at most REC_SCAP[u] of them,
+// padded with the sentinel N (a zero slot of the exchange buffer).
+// hdr[e] = {M_0 | M_1<<8 | M_2<<16 | M_3<<24, ovf, e, 0}; ovf != 0 if some slot
+// exceeds its capacity (then the CSR plan is used for that step).
+// Fixed per-slot capacities (unconditional, branch-free gathers; the zero sentinel pads):
+// slot 0 holds the highest in-degrees (<= 6), slot 1 <= 2, slots 2-3 <= 1 -- the
+// in-degree profile of random maps; entries that do not fit take the CSR path.
+// Record entries are uint16 BYTE offsets into the exchange buffer (index * element
+// size), so a gather is one extract + one add + one LDS.
+__host__ __device__ constexpr int rec_scap(int u) { return u == 0 ? 6 : u == 1 ? 2 : 1; }
+__host__ __device__ constexpr int rec_soff(int u) { return u == 0 ? 4 : u == 1 ? 10 : u == 2 ? 12 : 13; }   // in u16 units
+
 template <int NPL>
 struct Rec {
-    static constexpr int B = (NPL * MU + 3) & ~3;   // record bytes per lane (whole 32-bit words)
+    static constexpr int B = 32;   // record bytes per lane: 4 target + 10 source u16 offsets (+2 pad)
     static constexpr int W = B / 4;
     uint32_t w[W];
 };
 
 template <int NPL>
 __global__ void k_build_fused_plan(const uint16_t* __restrict__ dict_idx, uint8_t* __restrict__ rec,
-                                   uint32_t* __restrict__ hdr, int N) {
-    extern __shared__ uint16_t sP[];
+                                   uint32_t* __restrict__ hdr, uint16_t* __restrict__ pclamp, int N, int sv,
+                                   uint32_t flags) {
+    extern __shared__ uint16_t sP[];   // [N] clamped row, then [N] in-degrees
     __shared__ int smax[8];
+    __shared__ int sovf;
+    uint16_t* sdeg = sP + N;
     const int e = blockIdx.x;
     const uint16_t* P = dict_idx + (size_t)e * N;
-    for (int j = threadIdx.x; j < N; j += blockDim.x) sP[j] = min((int)P[j], N - 1);
+    for (int j = threadIdx.x; j < N; j += blockDim.x) {
+        int p = P[j];
+        if (p >= N) {
+            if (flags & PDSSM_CHECK_FINITE) report(ERRBIT_RANGE);
+            p = N - 1;
+        }
+        sP[j] = (uint16_t)p;
+        pclamp[(size_t)e * N + j] = (uint16_t)p;   // clamped index rows used by the fused kernels
+    }
     if (threadIdx.x < 8) smax[threadIdx.x] = 0;
+    if (threadIdx.x == 0) sovf = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        int d = 0;
+        for (int j = 0; j < N; ++j) d += sP[j] == i;
+        sdeg[i] = (uint16_t)d;
+    }
     __syncthreads();
     constexpr int RB = Rec<NPL>::B;
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
-        const int l = i / NPL, u = i % NPL;
+        const int di = sdeg[i];
+        int rank = 0;
+        for (int i2 = 0; i2 < N; ++i2) {
+            const int d2 = sdeg[i2];
+            rank += (d2 > di) || (d2 == di && i2 < i);
+        }
+        const int l = rank % 32, u = rank / 32;
+        uint16_t* r = reinterpret_cast<uint16_t*>(rec + ((size_t)e * 32 + l) * RB);
+        r[u] = (uint16_t)(i * sv);
         int q = 0;
         for (int j = 0; j < N; ++j) {
             if (sP[j] == i) {
-                if (q < MU) rec[((size_t)e * 32 + l) * RB + u * MU + q] = (uint8_t)j;
+                if (q < rec_scap(u)) r[rec_soff(u) + q] = (uint16_t)(j * sv);
                 ++q;
             }
         }
-        for (int qq = q; qq < MU; ++qq) rec[((size_t)e * 32 + l) * RB + u * MU + qq] = (uint8_t)N;
+        for (int qq = q; qq < rec_scap(u); ++qq) r[rec_soff(u) + qq] = (uint16_t)(N * sv);
         atomicMax(&smax[u], q);
+        if (q > rec_scap(u)) sovf = 1;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         uint32_t h = 0;
-        bool ovf = false;
-        for (int u = 0; u < NPL; ++u) {
-            h |= (uint32_t)min(smax[u], 255) << (8 * u);
-            ovf |= smax[u] > MU;
-        }
+        for (int u = 0; u < NPL; ++u) h |= (uint32_t)min(smax[u], rec_scap(u)) << (8 * u);   // informative
         hdr[4 * e] = h;
-        hdr[4 * e + 1] = ovf ? 1u : 0u;
+        hdr[4 * e + 1] = sovf ? 1u : 0u;
         hdr[4 * e + 2] = (uint32_t)e;   // entry index (CSR fallback)
         hdr[4 * e + 3] = 0u;
     }
 }
 
 template <int NPL>
-__device__ __forceinline__ int rec_byte(const Rec<NPL>& r, int idx) {   // idx compile-time after unrolling
-    return (r.w[idx >> 2] >> (8 * (idx & 3))) & 0xff;
+__device__ __forceinline__ uint32_t rec_off(const Rec<NPL>& r, int idx) {   // u16 entry idx (compile-time)
+    return (idx & 1) ? (r.w[idx >> 1] >> 16) : (r.w[idx >> 1] & 0xffffu);
 }
 
-// acc[u] += sum_{q < M_u} vbuf[src_q] for the lane's NPL targets
+// Balanced, branch-free gather: sum over the slot's (padded) source list, written
+// to s[target_u].  Padding reads the zero slot v[N] (a broadcast, no conflict).
 template <int NC, int NPL>
-__device__ __forceinline__ void gather_sum(const typename SVal<NC>::type* vbuf, const Rec<NPL>& r, uint32_t hdr,
-                                           float (&are)[NPL], float (&aim)[NPL]) {
+__device__ __forceinline__ void gather_sorted(const typename SVal<NC>::type* vbuf, typename SVal<NC>::type* sbuf,
+                                              const Rec<NPL>& r) {
 #pragma unroll
     for (int u = 0; u < NPL; ++u) {
-        const int M = (hdr >> (8 * u)) & 0xff;
+        float ar = 0.f, ai = 0.f;
+        using SVT = typename SVal<NC>::type;
+        const char* vb = reinterpret_cast<const char*>(vbuf);
 #pragma unroll
-        for (int q = 0; q < MU; ++q) {
-            if (q < M) {
-                const auto v = vbuf[rec_byte<NPL>(r, u * MU + q)];
-                are[u] += re_of<NC>(v);
-                if constexpr (NC == 2) aim[u] += im_of<NC>(v);
-            }
+        for (int q = 0; q < rec_scap(u); ++q) {
+            const SVT v = *reinterpret_cast<const SVT*>(vb + rec_off<NPL>(r, rec_soff(u) + q));
+            ar += re_of<NC>(v);
+            if constexpr (NC == 2) ai += im_of<NC>(v);
         }
+        *reinterpret_cast<SVT*>(reinterpret_cast<char*>(sbuf) + rec_off<NPL>(r, u)) = mk<NC>(ar, ai);
     }
 }
 
@@ -325,6 +421,7 @@ struct FusedArgs {
     const uint16_t* psrc;
     const uint8_t* rec;
     const uint32_t* hdr;
+    const uint16_t* pclamp;  // fwd: clamped copy of dict_idx (fused plan)
     const void* diag;        // PER_STEP act tensor
     const float* diag_dict;  // PER_DICT f32 [H][K][NC][N]
     const void* bias;        // fwd: b_t ; bwd: e (direct gradient)
@@ -343,6 +440,7 @@ struct FusedArgs {
     int H, L, N, K, tau, C, S;
     uint32_t flags;
     int debug_nochain;       // timing experiments only (PDSSM_DEBUG_NOCHAIN): skip the carry wait
+    int smem_tables;         // 1: the CTA's home-head tables live in shared memory
 };
 
 
@@ -426,12 +524,26 @@ __host__ __device__ constexpr size_t al16(size_t x) { return (x + 15) & ~(size_t
 //    (one copy per stream per slot: G rows are contiguous in HBM), issued by the
 //    warp itself once per G steps, PF*G steps ahead, across item boundaries.
 // ============================================================================
-constexpr int WARPS = 7;
-constexpr int CTA_THREADS = WARPS * 32;
+#ifndef PDSSM_WARPS_FWD
+#define PDSSM_WARPS_FWD 11
+#endif
+#ifndef PDSSM_WARPS_BWD
+#define PDSSM_WARPS_BWD 11
+#endif
+#ifndef PDSSM_G_FWD
+#define PDSSM_G_FWD 2
+#endif
+#ifndef PDSSM_G_BWD
+#define PDSSM_G_BWD 2
+#endif
+constexpr int WARPS_FWD = PDSSM_WARPS_FWD;   // consumer warps (= items in flight) per CTA, one CTA per SM
+constexpr int WARPS_BWD = PDSSM_WARPS_BWD;
 
 template <typename T, int NC, int NPL, bool PD, bool BWD, int ESZ = (int)sizeof(T)>
 struct Layout {
-    static constexpr int G = BWD ? 2 : 4;                    // steps per ring slot
+    static constexpr int WARPS = BWD ? WARPS_BWD : WARPS_FWD;
+    static constexpr int THREADS = WARPS * 32;
+    static constexpr int G = BWD ? PDSSM_G_BWD : PDSSM_G_FWD;  // steps per ring slot
     static constexpr int N = 32 * NPL;
     static constexpr int ROW = NC * N * (int)sizeof(T);      // one D / b / h row (act dtype)
     static constexpr int EROW = NC * N * ESZ;                 // one e row (bwd)
@@ -445,14 +557,45 @@ struct Layout {
     static constexpr size_t w_ring = 0;
     static constexpr size_t w_bar = al16(w_ring + (size_t)PF * SLOT);
     static constexpr size_t w_x = al16(w_bar + (size_t)PF * 8);              // exchange [2][N+1]
-    static constexpr size_t w_ob = al16(w_x + (size_t)2 * (N + 1) * SV);    // chain result [N]
-    static constexpr size_t w_key = al16(w_ob + (size_t)N * SV);             // chain keys u16 [N]
-    static constexpr size_t w_cnt = al16(w_key + (size_t)N * 2);             // chain counts int [N]
-    static constexpr size_t w_k = al16(w_cnt + (size_t)N * 4);               // k* of the chunk [TAUMAX]
+    static constexpr size_t w_ob = al16(w_x + (size_t)2 * (N + 1) * SV);    // fwd chain result [N]
+    static constexpr size_t w_key = al16(w_ob + (BWD ? 0 : (size_t)N * SV)); // fwd chain keys u16 [N]
+    static constexpr size_t w_cnt = al16(w_key + (BWD ? 0 : (size_t)N * 2)); // fwd chain counts int [N]
+    static constexpr size_t w_k = al16(w_cnt + (BWD ? 0 : (size_t)N * 4));   // k* of the chunk [TAUMAX]
     static constexpr size_t w_g = al16(w_k + TAUMAX);                        // bwd g partials [32][33]
     static constexpr size_t w_bytes = al16(w_g + (BWD ? 32 * 33 * 4 : 0));
     static constexpr size_t bytes = (size_t)WARPS * w_bytes;
+    // CTA-shared tables of the home head (after the warps' blocks), K entries:
+    //   P rows u16 [K][N] (clamped), fwd: records [K][32][Rec::B] and headers [K][4] u32,
+    //   PER_DICT: diagonal rows f32 [K][NC][N]
+    static constexpr size_t t_P = 0;
+    __host__ __device__ static constexpr size_t t_rec(int K) { return al16(t_P + (size_t)K * N * 2); }
+    __host__ __device__ static constexpr size_t t_hdr(int K) { return al16(t_rec(K) + (BWD ? 0 : (size_t)K * 32 * Rec<NPL>::B)); }
+    __host__ __device__ static constexpr size_t t_dk(int K) { return al16(t_hdr(K) + (BWD ? 0 : (size_t)K * 16)); }
+    __host__ __device__ static constexpr size_t t_bytes(int K) { return al16(t_dk(K) + (PD ? (size_t)K * NC * N * 4 : 0)); }
 };
+
+// CTA-cooperative copy of the home head's tables into shared memory
+template <typename LY, bool BWD, bool PD, int NC, int NPL>
+__device__ __forceinline__ void load_tables(const FusedArgs& a, uint8_t* tb, int h) {
+    const int K = a.K, N = a.N;
+    uint16_t* sP = reinterpret_cast<uint16_t*>(tb + LY::t_P);
+    const uint16_t* gP = a.dict_idx + (size_t)h * K * N;
+    for (int i = threadIdx.x; i < K * N; i += blockDim.x) sP[i] = (uint16_t)min((int)__ldg(gP + i), N - 1);
+    if constexpr (!BWD) {
+        const uint4* gr = reinterpret_cast<const uint4*>(a.rec + (size_t)h * K * 32 * Rec<NPL>::B);
+        uint4* sr = reinterpret_cast<uint4*>(tb + LY::t_rec(K));
+        const int nr = K * 32 * Rec<NPL>::B / 16;
+        for (int i = threadIdx.x; i < nr; i += blockDim.x) sr[i] = __ldg(gr + i);
+        const uint4* gh = reinterpret_cast<const uint4*>(a.hdr + (size_t)h * K * 4);
+        uint4* sh = reinterpret_cast<uint4*>(tb + LY::t_hdr(K));
+        for (int i = threadIdx.x; i < K; i += blockDim.x) sh[i] = __ldg(gh + i);
+    }
+    if constexpr (PD) {
+        const float* gd = a.diag_dict + (size_t)h * K * NC * N;
+        float* sd = reinterpret_cast<float*>(tb + LY::t_dk(K));
+        for (int i = threadIdx.x; i < K * NC * N; i += blockDim.x) sd[i] = __ldg(gd + i);
+    }
+}
 
 template <bool PD, typename T>
 using DType = typename std::conditional<PD, float, T>::type;
@@ -477,18 +620,15 @@ __device__ __forceinline__ Item make_item(const FusedArgs& a, int h, int ticket,
     return it;
 }
 
-// next item for this warp: head-affine, then help the other heads
-__device__ __forceinline__ bool next_item(const FusedArgs& a, int& h, int lane, bool reverse, Item& it) {
+// next item of head h for this warp (per-head ticket counter)
+__device__ __forceinline__ bool next_item(const FusedArgs& a, int h, int lane, bool reverse, Item& it) {
     const int per_head = (a.S / a.H) * a.C;
-    for (int tries = 0; tries < a.H; ++tries) {
-        int t = 0;
-        if (lane == 0) t = (int)atomicAdd(a.ctrl + h, 1u);
-        t = __shfl_sync(0xffffffffu, t, 0);
-        if (t < per_head) {
-            it = make_item(a, h, t, reverse);
-            return true;
-        }
-        h = h + 1 == a.H ? 0 : h + 1;
+    int t = 0;
+    if (lane == 0) t = (int)atomicAdd(a.ctrl + h, 1u);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (t < per_head) {
+        it = make_item(a, h, t, reverse);
+        return true;
     }
     return false;
 }
@@ -535,7 +675,7 @@ struct FillCursor {
 
 template <typename T, typename TE, int NC, int NPL, bool PD, bool BWD>
 __device__ __forceinline__ void issue_fill(const FusedArgs& a, const Item& it, int g, uint8_t* ring, uint64_t* bars,
-                                           int slot) {
+                                           int slot, uint64_t pol_last, uint64_t pol_first) {
     using LY = Layout<T, NC, NPL, PD, BWD, (int)sizeof(TE)>;
     const int N = a.N;
     const size_t row = (size_t)NC * N;
@@ -547,12 +687,14 @@ __device__ __forceinline__ void issue_fill(const FusedArgs& a, const Item& it, i
     const int len = min(LY::G, it.n - v0);
     uint8_t* dst = ring + (size_t)slot * LY::SLOT;
     uint64_t* bar = bars + slot;
-    fence_proxy_async();
+    // WAR on the slot: its previous contents were consumed (generic-proxy reads whose
+    // values were used) before this lane reached here, in program order after __syncwarp
+    const uint64_t pol = phC ? pol_first : pol_last;
     if constexpr (!BWD) {
         const int t = it.t0 + v0;   // rows t .. t+len-1 at slot offsets 0..len-1
         mbar_expect_tx(bar, (uint32_t)((PD ? 0 : len * LY::ROW) + len * LY::ROW));
-        if constexpr (!PD) tma_1d(dst, static_cast<const T*>(a.diag) + (seq0 + t) * row, len * LY::ROW, bar);
-        tma_1d(dst + LY::OFF_B, static_cast<const T*>(a.bias) + (seq0 + t) * row, len * LY::ROW, bar);
+        if constexpr (!PD) tma_1d_hint(dst, static_cast<const T*>(a.diag) + (seq0 + t) * row, len * LY::ROW, bar, pol);
+        tma_1d_hint(dst + LY::OFF_B, static_cast<const T*>(a.bias) + (seq0 + t) * row, len * LY::ROW, bar, pol);
     } else {
         // steps v0..v0+len-1 are times t_hi = t1-1-v0 down to t_lo = t_hi-len+1; the row
         // of time t sits at slot offset (t - t_lo) for D, e_{t-1} and h_{t-1}
@@ -564,20 +706,20 @@ __device__ __forceinline__ void issue_fill(const FusedArgs& a, const Item& it, i
         const int h_first = max(t_lo - 1, 0);       // h_{t-1} needed for t > 0 (Phase C' only)
         const int h_cnt = phC ? max(0, t_hi - 1 - h_first + 1) : 0;
         mbar_expect_tx(bar, (uint32_t)((PD ? 0 : len * LY::ROW) + e_cnt * LY::EROW + h_cnt * LY::ROW));
-        if constexpr (!PD) tma_1d(dst, static_cast<const T*>(a.diag) + (seq0 + t_lo) * row, len * LY::ROW, bar);
+        if constexpr (!PD) tma_1d_hint(dst, static_cast<const T*>(a.diag) + (seq0 + t_lo) * row, len * LY::ROW, bar, pol);
         if (e_cnt > 0)
-            tma_1d(dst + LY::OFF_E + (size_t)(e_first - (t_lo - 1)) * LY::EROW, ein + (seq0 + e_first) * row,
-                   e_cnt * LY::EROW, bar);
+            tma_1d_hint(dst + LY::OFF_E + (size_t)(e_first - (t_lo - 1)) * LY::EROW, ein + (seq0 + e_first) * row,
+                        e_cnt * LY::EROW, bar, pol);
         if (h_cnt > 0)
-            tma_1d(dst + LY::OFF_H + (size_t)(h_first - (t_lo - 1)) * LY::ROW,
-                   static_cast<const T*>(a.hsaved) + (seq0 + h_first) * row, h_cnt * LY::ROW, bar);
+            tma_1d_hint(dst + LY::OFF_H + (size_t)(h_first - (t_lo - 1)) * LY::ROW,
+                        static_cast<const T*>(a.hsaved) + (seq0 + h_first) * row, h_cnt * LY::ROW, bar, pol_first);
     }
 }
 
 // issue fills while fewer than PF are outstanding ahead of `consumed`
 template <typename T, typename TE, int NC, int NPL, bool PD, bool BWD>
 __device__ __forceinline__ void pump(const FusedArgs& a, FillCursor& fc, uint32_t consumed, uint8_t* ring,
-                                     uint64_t* bars, int lane) {
+                                     uint64_t* bars, int lane, uint64_t pol_last, uint64_t pol_first) {
     using LY = Layout<T, NC, NPL, PD, BWD, (int)sizeof(TE)>;
     constexpr int PF = LY::PF;
     while (fc.q < consumed + PF) {
@@ -590,7 +732,8 @@ __device__ __forceinline__ void pump(const FusedArgs& a, FillCursor& fc, uint32_
             fc.g = 0;
             continue;
         }
-        if (lane == 0) issue_fill<T, TE, NC, NPL, PD, BWD>(a, fc.it[0], fc.g, ring, bars, (int)(fc.q % PF));
+        if (lane == 0 && !(a.debug_nochain & 2))
+            issue_fill<T, TE, NC, NPL, PD, BWD>(a, fc.it[0], fc.g, ring, bars, (int)(fc.q % PF), pol_last, pol_first);
         ++fc.g;
         ++fc.q;
     }
@@ -600,7 +743,7 @@ __device__ __forceinline__ void pump(const FusedArgs& a, FillCursor& fc, uint32_
 // forward
 // ============================================================================
 template <typename T, int NC, int NPL, bool PD>
-__global__ void __launch_bounds__(CTA_THREADS, 1) k_fwd_fused(FusedArgs a) {
+__global__ void __launch_bounds__(Layout<T, NC, NPL, PD, false>::THREADS, 1) k_fwd_fused(FusedArgs a) {
     using SV = typename SVal<NC>::type;
     using LY = Layout<T, NC, NPL, PD, false>;
     using DT = DType<PD, T>;
@@ -624,15 +767,47 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) k_fwd_fused(FusedArgs a) {
         xb[(N + 1) + N] = mk<NC>(0.f, 0.f);
     }
     __syncwarp();
-    int head = blockIdx.x % a.H;
+    // one scatter step: z = A_t-scatter of v (own slices in, own target sums out).
+    // v -> vbuf, sync, balanced gather -> sbuf[target], sync, own sums <- sbuf.
+    SV* vbuf = xb;
+    SV* sbuf = xb + (N + 1);
+    auto scatter_step = [&](const float (&vr)[NPL], const float (&vi)[NPL], const Rec<NPL>& r, const uint4& hd, int e,
+                            float (&zr)[NPL], float (&zi)[NPL]) {
+        sts_row<NC, NPL>(vbuf, lane, vr, vi);
+        __syncwarp();
+        if (hd.y) {
+            float cr[NPL], ci[NPL];
+#pragma unroll
+            for (int u = 0; u < NPL; ++u) { cr[u] = 0.f; ci[u] = 0.f; }
+            gather_sum_csr<NC, NPL>(vbuf, a.pstart, a.psrc, e, N, lane, cr, ci);
+            sts_row<NC, NPL>(sbuf, lane, cr, ci);
+        } else {
+            gather_sorted<NC, NPL>(vbuf, sbuf, r);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < NPL; ++u) {
+            const SV z = sbuf[lane * NPL + u];
+            zr[u] = re_of<NC>(z);
+            zi[u] = im_of<NC>(z);
+        }
+    };
+    const uint64_t pol_out = policy_evict_first();
+    const uint64_t pol_last = policy_evict_last();
+    uint8_t* tbl = smem + LY::bytes;
     FillCursor fc;
+    fc.q = 0;
+    uint32_t consumed = 0;        // groups consumed
+    // heads of this CTA: blockIdx % H when grid = (SMs / H) * H >= H, else blockIdx, + grid, ...
+    for (int head = blockIdx.x % a.H; head < a.H; head += gridDim.x) {
+    __syncthreads();
+    load_tables<LY, false, PD, NC, NPL>(a, tbl, head);
+    __syncthreads();
     fc.valid[0] = next_item(a, head, lane, false, fc.it[0]);
     fc.valid[1] = false;
     fc.g = 0;
-    fc.q = 0;
     KPre kp;
     if (fc.valid[0]) kpre_load(a, kp, fc.it[0], lane);
-    uint32_t consumed = 0;        // groups consumed
     bool have = fc.valid[0];
     Item it = fc.it[0];
     while (have) {
@@ -647,10 +822,12 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) k_fwd_fused(FusedArgs a) {
         kpre_store(a, kp, sk, n, lane, true);
         if (has_next) kpre_load(a, kp, nx, lane);
         __syncwarp();
-        pump<T, T, NC, NPL, PD, false>(a, fc, consumed, ring, bars, lane);
-        const uint16_t* prow_base = a.dict_idx + (size_t)h * a.K * N;
-        const uint8_t* rec_base = a.rec + ((size_t)h * a.K * 32 + lane) * Rec<NPL>::B;
-        const uint32_t* hdr_base = a.hdr + (size_t)h * a.K * 4;
+        pump<T, T, NC, NPL, PD, false>(a, fc, consumed, ring, bars, lane, pol_last, pol_out);
+        // per-entry tables of this head, in shared memory
+        const uint16_t* prow_base = reinterpret_cast<const uint16_t*>(tbl + LY::t_P);
+        const uint8_t* rec_base = tbl + LY::t_rec(a.K) + lane * Rec<NPL>::B;
+        const uint32_t* hdr_base = reinterpret_cast<const uint32_t*>(tbl + LY::t_hdr(a.K));
+        const float* dk_base = reinterpret_cast<const float*>(tbl + LY::t_dk(a.K));
         // ---------------- Phase A: aggregate from identity
         int pi[NPL];
         float dre[NPL], dim[NPL], bre[NPL], bim[NPL];
@@ -663,12 +840,12 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) k_fwd_fused(FusedArgs a) {
             const int k0 = sk[0];
 #pragma unroll
             for (int i = 0; i < Rec<NPL>::W; ++i)
-                rn.w[i] = __ldg(reinterpret_cast<const uint32_t*>(rec_base + (size_t)k0 * 32 * Rec<NPL>::B) + i);
-            hn = __ldg(reinterpret_cast<const uint4*>(hdr_base + 4 * k0));
+                rn.w[i] = reinterpret_cast<const uint32_t*>(rec_base + (size_t)k0 * 32 * Rec<NPL>::B)[i];
+            hn = *reinterpret_cast<const uint4*>(hdr_base + 4 * k0);
         }
         for (int gi = 0; gi < ng; ++gi) {
             const int slot = consumed % PF;
-            mbar_wait(bars + slot, (consumed / PF) & 1);
+            if (!(a.debug_nochain & 2)) mbar_wait(bars + slot, (consumed / PF) & 1);
             const uint8_t* sp = ring + (size_t)slot * LY::SLOT;
             const int len = min(LY::G, n - gi * LY::G);
             for (int i = 0; i < len; ++i) {
@@ -680,20 +857,15 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) k_fwd_fused(FusedArgs a) {
                     const int kn = sk[v + 1 < n ? v + 1 : v];
 #pragma unroll
                     for (int q = 0; q < Rec<NPL>::W; ++q)
-                        rn.w[q] = __ldg(reinterpret_cast<const uint32_t*>(rec_base + (size_t)kn * 32 * Rec<NPL>::B) + q);
-                    hn = __ldg(reinterpret_cast<const uint4*>(hdr_base + 4 * kn));
+                        rn.w[q] = reinterpret_cast<const uint32_t*>(rec_base + (size_t)kn * 32 * Rec<NPL>::B)[q];
+                    hn = *reinterpret_cast<const uint4*>(hdr_base + 4 * kn);
                 }
                 Planes<NC, NPL> D, Bv;
                 const DT* Dp;
-                if constexpr (PD) Dp = a.diag_dict + ((size_t)(h * a.K + k) * NC) * N;
+                if constexpr (PD) Dp = dk_base + (size_t)k * NC * N;
                 else Dp = reinterpret_cast<const T*>(sp) + (size_t)i * row;
-                if constexpr (PD) {
-                    vld<float, NPL>(Dp + lane * NPL, D.v[0]);
-                    if constexpr (NC == 2) vld<float, NPL>(Dp + N + lane * NPL, D.v[1]);
-                } else {
-                    sld<DT, NPL>(Dp + lane * NPL, D.v[0]);
-                    if constexpr (NC == 2) sld<DT, NPL>(Dp + N + lane * NPL, D.v[1]);
-                }
+                sld<DT, NPL>(Dp + lane * NPL, D.v[0]);
+                if constexpr (NC == 2) sld<DT, NPL>(Dp + N + lane * NPL, D.v[1]);
                 const T* Bp = reinterpret_cast<const T*>(sp + LY::OFF_B) + (size_t)i * row;
                 sld<T, NPL>(Bp + lane * NPL, Bv.v[0]);
                 if constexpr (NC == 2) sld<T, NPL>(Bp + N + lane * NPL, Bv.v[1]);
@@ -709,12 +881,12 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) k_fwd_fused(FusedArgs a) {
 #pragma unroll
                 for (int u = 0; u < NPL; ++u) {
                     float pr, pm;
-                    if constexpr (PD) { pr = __ldg(Dp + pi[u]); pm = NC == 2 ? __ldg(Dp + N + pi[u]) : 0.f; }
-                    else { pr = sld1<DT>(Dp + pi[u]); pm = NC == 2 ? sld1<DT>(Dp + N + pi[u]) : 0.f; }
+                    pr = sld1<DT>(Dp + pi[u]);
+                    pm = NC == 2 ? sld1<DT>(Dp + N + pi[u]) : 0.f;
                     const float nr = pr * dre[u] - pm * dim[u];
                     const float ni = pr * dim[u] + pm * dre[u];
                     dre[u] = nr; dim[u] = ni;
-                    pi[u] = clamp_idx(__ldg(prow + pi[u]), N, a.flags);
+                    pi[u] = prow[pi[u]];   // rows are pre-clamped (plan build / table load)
                 }
                 float vre[NPL], vim[NPL];
 #pragma unroll
@@ -723,14 +895,8 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) k_fwd_fused(FusedArgs a) {
                     vre[u] = D.v[0][u] * bre[u] - di * bim[u];
                     vim[u] = D.v[0][u] * bim[u] + di * bre[u];
                 }
-                SV* vb = xb + (v & 1) * (N + 1);
-                sts_row<NC, NPL>(vb, lane, vre, vim);
-                __syncwarp();
                 float zr[NPL], zi[NPL];
-#pragma unroll
-                for (int u = 0; u < NPL; ++u) { zr[u] = 0.f; zi[u] = 0.f; }
-                if (hd.y) gather_sum_csr<NC, NPL>(vb, a.pstart, a.psrc, h * a.K + k, N, lane, zr, zi);
-                else gather_sum<NC, NPL>(vb, r, hd.x, zr, zi);
+                scatter_step(vre, vim, r, hd, h * a.K + k, zr, zi);
 #pragma unroll
                 for (int u = 0; u < NPL; ++u) { bre[u] = zr[u] + Bv.v[0][u]; bim[u] = NC == 2 ? zi[u] + Bv.v[NC - 1][u] : 0.f; }
             }
@@ -738,7 +904,7 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) k_fwd_fused(FusedArgs a) {
             // except this step's pi-gathers, which the next syncwarp covers)
             __syncwarp();
             ++consumed;
-            pump<T, T, NC, NPL, PD, false>(a, fc, consumed, ring, bars, lane);
+            pump<T, T, NC, NPL, PD, false>(a, fc, consumed, ring, bars, lane, pol_last, pol_out);
         }
         // publish the aggregate (chunk_state sections 0-2), then flag = 1 ("aggregate ready")
 #pragma unroll
@@ -763,7 +929,7 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) k_fwd_fused(FusedArgs a) {
         int mp[NPL];                 // exclusive prefix map before this chunk (maps export)
         {
             int mP = -1;             // carry_{mP+1} is known; -1: carry_0 = h0
-            if (c > 0 && !a.debug_nochain) {
+            if (c > 0 && !(a.debug_nochain & 1)) {
                 while (true) {
                     const int m = c - 1 - lane;
                     const uint32_t f = m >= 0 ? ld_relaxed(flag_ptr(a, (size_t)s * a.C + m)) : 2u;
@@ -852,12 +1018,12 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) k_fwd_fused(FusedArgs a) {
             const int k0 = sk[0];
 #pragma unroll
             for (int i = 0; i < Rec<NPL>::W; ++i)
-                rn.w[i] = __ldg(reinterpret_cast<const uint32_t*>(rec_base + (size_t)k0 * 32 * Rec<NPL>::B) + i);
-            hn = __ldg(reinterpret_cast<const uint4*>(hdr_base + 4 * k0));
+                rn.w[i] = reinterpret_cast<const uint32_t*>(rec_base + (size_t)k0 * 32 * Rec<NPL>::B)[i];
+            hn = *reinterpret_cast<const uint4*>(hdr_base + 4 * k0);
         }
         for (int gi = 0; gi < ng; ++gi) {
             const int slot = consumed % PF;
-            mbar_wait(bars + slot, (consumed / PF) & 1);
+            if (!(a.debug_nochain & 2)) mbar_wait(bars + slot, (consumed / PF) & 1);
             const uint8_t* sp = ring + (size_t)slot * LY::SLOT;
             const int len = min(LY::G, n - gi * LY::G);
             for (int i = 0; i < len; ++i) {
@@ -869,14 +1035,14 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) k_fwd_fused(FusedArgs a) {
                     const int kn = sk[v + 1 < n ? v + 1 : v];
 #pragma unroll
                     for (int q = 0; q < Rec<NPL>::W; ++q)
-                        rn.w[q] = __ldg(reinterpret_cast<const uint32_t*>(rec_base + (size_t)kn * 32 * Rec<NPL>::B) + q);
-                    hn = __ldg(reinterpret_cast<const uint4*>(hdr_base + 4 * kn));
+                        rn.w[q] = reinterpret_cast<const uint32_t*>(rec_base + (size_t)kn * 32 * Rec<NPL>::B)[q];
+                    hn = *reinterpret_cast<const uint4*>(hdr_base + 4 * kn);
                 }
                 Planes<NC, NPL> D, Bv;
                 if constexpr (PD) {
-                    const float* Dp = a.diag_dict + ((size_t)(h * a.K + k) * NC) * N;
-                    vld<float, NPL>(Dp + lane * NPL, D.v[0]);
-                    if constexpr (NC == 2) vld<float, NPL>(Dp + N + lane * NPL, D.v[1]);
+                    const float* Dp = dk_base + (size_t)k * NC * N;
+                    sld<float, NPL>(Dp + lane * NPL, D.v[0]);
+                    if constexpr (NC == 2) sld<float, NPL>(Dp + N + lane * NPL, D.v[1]);
                 } else {
                     const T* Dp = reinterpret_cast<const T*>(sp) + (size_t)i * row;
                     sld<T, NPL>(Dp + lane * NPL, D.v[0]);
@@ -892,14 +1058,8 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) k_fwd_fused(FusedArgs a) {
                     vre[u] = D.v[0][u] * cre[u] - di * cim[u];
                     vim[u] = D.v[0][u] * cim[u] + di * cre[u];
                 }
-                SV* vb = xb + (v & 1) * (N + 1);
-                sts_row<NC, NPL>(vb, lane, vre, vim);
-                __syncwarp();
                 float zr[NPL], zi[NPL];
-#pragma unroll
-                for (int u = 0; u < NPL; ++u) { zr[u] = 0.f; zi[u] = 0.f; }
-                if (hd.y) gather_sum_csr<NC, NPL>(vb, a.pstart, a.psrc, h * a.K + k, N, lane, zr, zi);
-                else gather_sum<NC, NPL>(vb, r, hd.x, zr, zi);
+                scatter_step(vre, vim, r, hd, h * a.K + k, zr, zi);
                 Planes<NC, NPL> hv;
 #pragma unroll
                 for (int u = 0; u < NPL; ++u) {
@@ -908,23 +1068,24 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) k_fwd_fused(FusedArgs a) {
                     hv.v[0][u] = cre[u];
                     if constexpr (NC == 2) hv.v[NC - 1][u] = cim[u];
                 }
-                store_planes<T, NC, NPL>(hout, hv, N);
+                store_planes_stream<T, NC, NPL>(hout, hv, N, pol_out);
                 hout += row;
             }
             __syncwarp();
             ++consumed;
-            pump<T, T, NC, NPL, PD, false>(a, fc, consumed, ring, bars, lane);
+            pump<T, T, NC, NPL, PD, false>(a, fc, consumed, ring, bars, lane, pol_last, pol_out);
         }
         have = has_next;
         it = nx;
     }
+    }   // head loop
 }
 
 // ============================================================================
 // backward (transposed scan, reverse chunk order)
 // ============================================================================
 template <typename T, typename TE, int NC, int NPL, bool PD>
-__global__ void __launch_bounds__(CTA_THREADS, 1) k_bwd_fused(FusedArgs a) {
+__global__ void __launch_bounds__(Layout<T, NC, NPL, PD, true, (int)sizeof(TE)>::THREADS, 1) k_bwd_fused(FusedArgs a) {
     using SV = typename SVal<NC>::type;
     using LY = Layout<T, NC, NPL, PD, true, (int)sizeof(TE)>;
     constexpr int PF = LY::PF;
@@ -944,15 +1105,21 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) k_bwd_fused(FusedArgs a) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
-    int head = blockIdx.x % a.H;
+    const uint64_t pol_out = policy_evict_first();
+    const uint64_t pol_last = policy_evict_last();
+    uint8_t* tbl = smem + LY::bytes;
     FillCursor fc;
+    fc.q = 0;
+    uint32_t consumed = 0;
+    for (int head = blockIdx.x % a.H; head < a.H; head += gridDim.x) {
+    __syncthreads();
+    load_tables<LY, true, PD, NC, NPL>(a, tbl, head);
+    __syncthreads();
     fc.valid[0] = next_item(a, head, lane, true, fc.it[0]);
     fc.valid[1] = false;
     fc.g = 0;
-    fc.q = 0;
     KPre kp;
     if (fc.valid[0]) kpre_load(a, kp, fc.it[0], lane);
-    uint32_t consumed = 0;
     bool have = fc.valid[0];
     Item it = fc.it[0];
     while (have) {
@@ -967,14 +1134,15 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) k_bwd_fused(FusedArgs a) {
         kpre_store(a, kp, sk, n, lane, false);
         if (has_next) kpre_load(a, kp, nx, lane);
         __syncwarp();
-        pump<T, TE, NC, NPL, PD, true>(a, fc, consumed, ring, bars, lane);
-        const uint16_t* prow_base = a.dict_idx + (size_t)h * a.K * N + lane * NPL;
+        pump<T, TE, NC, NPL, PD, true>(a, fc, consumed, ring, bars, lane, pol_last, pol_out);
+        const uint16_t* prow_base = reinterpret_cast<const uint16_t*>(tbl + LY::t_P) + lane * NPL;
+        const float* dk_base = reinterpret_cast<const float*>(tbl + LY::t_dk(a.K));
         // index row slice of entry k: raw words loaded one step ahead, decoded at use
         auto load_P = [&](int k) -> uint2 {
             const uint16_t* p = prow_base + (size_t)k * N;
-            if constexpr (NPL == 4) return __ldg(reinterpret_cast<const uint2*>(p));
-            else if constexpr (NPL == 2) return make_uint2(__ldg(reinterpret_cast<const unsigned int*>(p)), 0u);
-            else return make_uint2((uint32_t)__ldg(p), 0u);
+            if constexpr (NPL == 4) return *reinterpret_cast<const uint2*>(p);
+            else if constexpr (NPL == 2) return make_uint2(*reinterpret_cast<const unsigned int*>(p), 0u);
+            else return make_uint2((uint32_t)*p, 0u);
         };
         auto decode_P = [&](uint2 vv, int (&P)[NPL]) {
             if constexpr (NPL == 4) { P[0] = vv.x & 0xffff; P[1] = vv.x >> 16; P[2] = vv.y & 0xffff; P[3] = vv.y >> 16; }
@@ -985,9 +1153,9 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) k_bwd_fused(FusedArgs a) {
         };
         auto load_D = [&](const uint8_t* sp, int ro, int k, Planes<NC, NPL>& D) {
             if constexpr (PD) {
-                const float* Dp = a.diag_dict + ((size_t)(h * a.K + k) * NC) * N + lane * NPL;
-                vld<float, NPL>(Dp, D.v[0]);
-                if constexpr (NC == 2) vld<float, NPL>(Dp + N, D.v[1]);
+                const float* Dp = dk_base + (size_t)k * NC * N + lane * NPL;
+                sld<float, NPL>(Dp, D.v[0]);
+                if constexpr (NC == 2) sld<float, NPL>(Dp + N, D.v[1]);
             } else {
                 const T* Dp = reinterpret_cast<const T*>(sp) + (size_t)ro * row + lane * NPL;
                 sld<T, NPL>(Dp, D.v[0]);
@@ -1008,7 +1176,7 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) k_bwd_fused(FusedArgs a) {
         uint2 Pn = load_P(sk[n - 1]);
         for (int gi = 0; gi < ng; ++gi) {
             const int slot = consumed % PF;
-            mbar_wait(bars + slot, (consumed / PF) & 1);
+            if (!(a.debug_nochain & 2)) mbar_wait(bars + slot, (consumed / PF) & 1);
             const uint8_t* sp = ring + (size_t)slot * LY::SLOT;
             const int len = min(LY::G, n - gi * LY::G);
             for (int i = 0; i < len; ++i) {
@@ -1041,7 +1209,7 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) k_bwd_fused(FusedArgs a) {
                 }
             }
             ++consumed;
-            pump<T, TE, NC, NPL, PD, true>(a, fc, consumed, ring, bars, lane);
+            pump<T, TE, NC, NPL, PD, true>(a, fc, consumed, ring, bars, lane, pol_last, pol_out);
         }
 #pragma unroll
         for (int u = 0; u < NPL; ++u) { bpre[u] = lre[u]; bpim[u] = lim[u]; }   // beta'_c (e term was zero at t0)
@@ -1080,7 +1248,7 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) k_bwd_fused(FusedArgs a) {
         float mre[NPL], mim[NPL];
         {
             int mP = a.C;            // mu_{mP-1} is known; C: mu_{C-1} = lam_in
-            if (c + 1 < a.C && !a.debug_nochain) {
+            if (c + 1 < a.C && !(a.debug_nochain & 1)) {
                 while (true) {
                     const int m = c + 1 + lane;
                     const uint32_t f = m < a.C ? ld_relaxed(flag_ptr(a, (size_t)s * a.C + m)) : 2u;
@@ -1154,7 +1322,7 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) k_bwd_fused(FusedArgs a) {
         Pn = load_P(sk[n - 1]);
         for (int gi = 0; gi < ng; ++gi) {
             const int slot = consumed % PF;
-            mbar_wait(bars + slot, (consumed / PF) & 1);
+            if (!(a.debug_nochain & 2)) mbar_wait(bars + slot, (consumed / PF) & 1);
             const uint8_t* sp = ring + (size_t)slot * LY::SLOT;
             const int len = min(LY::G, n - gi * LY::G);
             for (int i = 0; i < len; ++i) {
@@ -1193,7 +1361,7 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) k_bwd_fused(FusedArgs a) {
                     Planes<NC, NPL> Lv;
 #pragma unroll
                     for (int u = 0; u < NPL; ++u) { Lv.v[0][u] = lre[u]; if constexpr (NC == 2) Lv.v[NC - 1][u] = lim[u]; }
-                    store_planes<T, NC, NPL>(dbp, Lv, N);
+                    store_planes_stream<T, NC, NPL>(dbp, Lv, N, pol_out);
                 }
                 SV* lb = xb + (v & 1) * (N + 1);
                 sts_row<NC, NPL>(lb, lane, lre, lim);
@@ -1213,8 +1381,8 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) k_bwd_fused(FusedArgs a) {
                     lre[u] = er[u] + dr * lr + di * li;                   // e_{t-1} + conj(D) lamP
                     lim[u] = ei[u] + dr * li - di * lr;
                 }
-                if constexpr (PD) { store_planes<float, NC, NPL>(ddf, dD, N); ddf -= row; }
-                else { store_planes<T, NC, NPL>(ddp, dD, N); ddp -= row; }
+                if constexpr (PD) { store_planes_stream<float, NC, NPL>(ddf, dD, N, pol_out); ddf -= row; }
+                else { store_planes_stream<T, NC, NPL>(ddp, dD, N, pol_out); ddp -= row; }
                 dbp -= row;
                 // g_t = sum over lanes of gv: park the partial, reduce 32 steps at a time
                 gbuf[(v & 31) * 33 + lane] = gv;
@@ -1231,11 +1399,12 @@ __global__ void __launch_bounds__(CTA_THREADS, 1) k_bwd_fused(FusedArgs a) {
             }
             __syncwarp();
             ++consumed;
-            pump<T, TE, NC, NPL, PD, true>(a, fc, consumed, ring, bars, lane);
+            pump<T, TE, NC, NPL, PD, true>(a, fc, consumed, ring, bars, lane, pol_last, pol_out);
         }
         have = has_next;
         it = nx;
     }
+    }   // head loop
 }
 
 }  // namespace fused
@@ -1248,7 +1417,8 @@ inline size_t fused_rec_bytes(int64_t H, int64_t K) {
     return (((size_t)H * K * 32 * fused::Rec<4>::B) + 255) & ~(size_t)255;   // NPL = 4 is the largest record
 }
 inline size_t fused_hdr_bytes(int64_t H, int64_t K) { return (((size_t)H * K * 16) + 255) & ~(size_t)255; }
-inline size_t fused_plan_bytes(int64_t H, int64_t K) { return fused_rec_bytes(H, K) + fused_hdr_bytes(H, K); }
+inline size_t fused_pclamp_bytes(int64_t H, int64_t K, int64_t N) { return (((size_t)H * K * N * 2) + 255) & ~(size_t)255; }
+inline size_t fused_plan_bytes(int64_t H, int64_t K, int64_t N) { return fused_rec_bytes(H, K) + fused_hdr_bytes(H, K) + fused_pclamp_bytes(H, K, N); }
 
 // [0, H): per-head ticket counters; then one flag per (sequence, chunk)
 inline size_t fused_ctrl_bytes(int64_t S, int C, int64_t H) { return (((size_t)(H + S * C) * 4 + 255) & ~(size_t)255); }
@@ -1271,11 +1441,12 @@ inline int num_sms() {
     return sms;
 }
 
-// persistent grid: ctas_per_sm resident CTAs per SM (dynamic tickets balance the items)
-inline int fused_grid(int total_items, int ctas_per_sm) {
-    int g = num_sms() * ctas_per_sm;
-    const int need = (total_items + fused::WARPS - 1) / fused::WARPS;
-    return g < need ? g : need;
+// persistent grid, one CTA per SM: the same number of CTAs for every head (CTA i serves
+// head i mod H) when H <= #SMs, else #SMs CTAs that walk the heads i, i + grid, ...
+inline int fused_grid(int64_t H) {
+    const int sms = num_sms();
+    if (H > sms) return sms;
+    return (int)((sms / H) * H);
 }
 
 }  // namespace pdssm

@@ -111,7 +111,7 @@ size_t ws_bytes_g(const Geo& g, int op) {
         case PDSSM_OP_SELECT:
             return align256((size_t)g.S * g.L * g.K * 4);
         case PDSSM_OP_FWD:
-            return plan_bytes(g) + (g.P > 0 ? seq_act_bytes(g) : 0) + fused_plan_bytes(g.H, g.K) +
+            return plan_bytes(g) + (g.P > 0 ? seq_act_bytes(g) : 0) + fused_plan_bytes(g.H, g.K, g.N) +
                    fused_ctrl_bytes(g.S, g.C, g.H);
         case PDSSM_OP_BWD:
             return 2 * cs_f_bytes(g) + (g.P > 0 ? seq_f_bytes(g) : 0) +
@@ -212,12 +212,10 @@ bool path_generic_forced() {
     const char* p = getenv("PDSSM_PATH");
     return p && strcmp(p, "generic") == 0;
 }
-
-bool fused_applicable(const Geo& g, std::initializer_list<const void*> ptrs) {
-    if (path_generic_forced() || fused_npl(g.N) == 0 || g.tau > fused::TAUMAX) return false;
-    for (const void* p : ptrs)
-        if (misaligned(p, 16)) return false;
-    return true;
+// PDSSM_PATH=fused makes the fused path mandatory (tests): a shape it cannot take is an error
+bool path_fused_forced() {
+    const char* p = getenv("PDSSM_PATH");
+    return p && strcmp(p, "fused") == 0;
 }
 
 template <typename F>
@@ -227,24 +225,54 @@ pdssm_status with_npl(int npl, F&& f) {
     return f(std::integral_constant<int, 4>{});
 }
 
-// resident CTAs per SM for a fused kernel using `smem` bytes per CTA (env override for tuning)
-int fused_ctas_per_sm(size_t smem) {
-    int want = 1;
-    if (const char* e = getenv("PDSSM_CTAS_PER_SM")) want = atoi(e);
-    int fit = (int)((227 * 1024) / (smem + 1024));
-    if (fit < 1) fit = 1;
-    return want < fit ? (want < 1 ? 1 : want) : fit;
+// shared memory (warp blocks + the head's tables) of the fused kernels for these dims
+template <bool BWD>
+size_t fused_smem(const Geo& g, int esz) {
+    size_t r = 0;
+    with_npl(fused_npl(g.N), [&](auto nv) {
+        constexpr int NPL = decltype(nv)::value;
+        return with_act(g.dtype, [&](auto tv) {
+            using T = decltype(tv);
+            return with_nc(g.nc, [&](auto ncv) {
+                constexpr int NC = decltype(ncv)::value;
+                return with_pd(g.diag_mode, [&](auto pdv) {
+                    constexpr bool PD = decltype(pdv)::value;
+                    if (esz == 4) {
+                        using LY = fused::Layout<T, NC, NPL, PD, BWD, 4>;
+                        r = LY::bytes + LY::t_bytes((int)g.K);
+                    } else {
+                        using LY = fused::Layout<T, NC, NPL, PD, BWD, (int)sizeof(T)>;
+                        r = LY::bytes + LY::t_bytes((int)g.K);
+                    }
+                    return PDSSM_OK;
+                });
+            });
+        });
+    });
+    return r;
 }
 
+bool fused_applicable(const Geo& g, std::initializer_list<const void*> ptrs) {
+    if (path_generic_forced() || fused_npl(g.N) == 0 || g.tau > fused::TAUMAX) return false;
+    for (const void* p : ptrs)
+        if (misaligned(p, 16)) return false;
+    const size_t lim = 227 * 1024;
+    if (fused_smem<false>(g, (int)g.act) > lim || fused_smem<true>(g, 4) > lim || fused_smem<true>(g, (int)g.act) > lim)
+        return false;
+    return true;
+}
+
+
 template <typename K>
-pdssm_status launch_fused(K kernel, const fused::FusedArgs& fa, size_t smem, int items, cudaStream_t st,
-                          const char* what) {
+pdssm_status launch_fused(K kernel, const fused::FusedArgs& fa_in, size_t smem, int threads, const Geo& g,
+                          cudaStream_t st, const char* what) {
+    fused::FusedArgs fa = fa_in;
+    fa.smem_tables = 1;
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return fail(PDSSM_ERR_CUDA, "%s attribute: %s", what, cudaGetErrorString(e));
-    const int grid = fused_grid(items, fused_ctas_per_sm(smem));
-    fused::FusedArgs f2 = fa;
-    f2.debug_nochain = getenv("PDSSM_DEBUG_NOCHAIN") != nullptr;
-    kernel<<<grid, fused::CTA_THREADS, smem, st>>>(f2);
+    // timing experiments only: bit 0 skips the carry wait, bit 1 skips the TMA ring (results invalid)
+    fa.debug_nochain = getenv("PDSSM_DEBUG_NOCHAIN") ? atoi(getenv("PDSSM_DEBUG_NOCHAIN")) : 0;
+    kernel<<<fused_grid(g.H), threads, smem, st>>>(fa);
     return cuda_check(what);
 }
 
@@ -252,8 +280,8 @@ pdssm_status fwd_fused(const Geo& g, fused::FusedArgs& fa, uint8_t* rec, uint32_
     const int npl = fused_npl(g.N);
     return with_npl(npl, [&](auto nv) {
         constexpr int NPL = decltype(nv)::value;
-        fused::k_build_fused_plan<NPL><<<(unsigned)(g.H * g.K), threads_for(g.N), (size_t)g.N * 2, st>>>(
-            fa.dict_idx, rec, hdr, (int)g.N);
+        fused::k_build_fused_plan<NPL><<<(unsigned)(g.H * g.K), threads_for(g.N), (size_t)g.N * 4, st>>>(
+            fa.dict_idx, rec, hdr, const_cast<uint16_t*>(fa.pclamp), (int)g.N, g.nc == 2 ? 8 : 4, g.flags);
         pdssm_status r = cuda_check("build_fused_plan");
         if (r) return r;
         cudaError_t e = cudaMemsetAsync(fa.ctrl, 0, fused_ctrl_bytes(g.S, g.C, g.H), st);
@@ -265,8 +293,8 @@ pdssm_status fwd_fused(const Geo& g, fused::FusedArgs& fa, uint8_t* rec, uint32_
                 return with_pd(g.diag_mode, [&](auto pdv) {
                     constexpr bool PD = decltype(pdv)::value;
                     using WS = fused::Layout<T, NC, NPL, PD, false>;
-                    return launch_fused(fused::k_fwd_fused<T, NC, NPL, PD>, fa, WS::bytes,
-                                        (int)(g.S * g.C), st, "fwd_fused");
+                    return launch_fused(fused::k_fwd_fused<T, NC, NPL, PD>, fa, WS::bytes + WS::t_bytes((int)g.K),
+                                        WS::THREADS, g, st, "fwd_fused");
                 });
             });
         });
@@ -287,8 +315,8 @@ pdssm_status bwd_fused(const Geo& g, fused::FusedArgs& fa, cudaStream_t st) {
                     constexpr bool PD = decltype(pdv)::value;
                     using TEE = typename std::conditional<std::is_same<TE, void>::value, T, TE>::type;
                     using WS = fused::Layout<T, NC, NPL, PD, true, (int)sizeof(TEE)>;
-                    return launch_fused(fused::k_bwd_fused<T, TEE, NC, NPL, PD>, fa, WS::bytes,
-                                        (int)(g.S * g.C), st, "bwd_fused");
+                    return launch_fused(fused::k_bwd_fused<T, TEE, NC, NPL, PD>, fa, WS::bytes + WS::t_bytes((int)g.K),
+                                        WS::THREADS, g, st, "bwd_fused");
                 });
             });
         });
@@ -449,6 +477,7 @@ pdssm_status pdssm_scan_fwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
     void* hscratch = g.P > 0 ? bump.take<char>(seq_act_bytes(g)) : nullptr;
     uint8_t* frec = bump.take<uint8_t>(fused_rec_bytes(g.H, g.K));
     uint32_t* fhdr = bump.take<uint32_t>(fused_hdr_bytes(g.H, g.K));
+    uint16_t* fpcl = bump.take<uint16_t>(fused_pclamp_bytes(g.H, g.K, g.N));
     uint32_t* ctrl = bump.take<uint32_t>(fused_ctrl_bytes(g.S, g.C, g.H));
     void* hout = h_out_opt ? h_out_opt : hscratch;
     ChunkStateView cs = cs_view(g, chunk_state);
@@ -459,12 +488,15 @@ pdssm_status pdssm_scan_fwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
     if (use_fused) {
         fused::FusedArgs fa{};
         fa.kstar = kstar; fa.dict_idx = dict_idx; fa.pstart = pstart; fa.psrc = psrc; fa.rec = frec; fa.hdr = fhdr;
+        fa.pclamp = fpcl;
         fa.diag = g.diag_mode == PDSSM_DIAG_PER_STEP ? diag : nullptr;
         fa.diag_dict = g.diag_mode == PDSSM_DIAG_PER_DICT ? static_cast<const float*>(diag) : nullptr;
         fa.bias = bias; fa.h0 = h0_opt; fa.cs = cs; fa.maps = maps; fa.out0 = hout; fa.ctrl = ctrl;
         fa.H = (int)g.H; fa.L = (int)g.L; fa.N = (int)g.N; fa.K = (int)g.K; fa.tau = g.tau; fa.C = g.C;
         fa.S = (int)g.S; fa.flags = g.flags;
         if ((r = fwd_fused(g, fa, frec, fhdr, st))) return r;
+    } else if (path_fused_forced()) {
+        return fail(PDSSM_ERR_UNSUPPORTED, "scan_fwd: PDSSM_PATH=fused but the fused path does not apply to these dims");
     } else {
         if ((r = fwd_three_phase(g, kstar, dict_idx, pstart, psrc, diag, bias, h0_opt, cs, maps, hout, true, st)))
             return r;
@@ -516,6 +548,8 @@ pdssm_status pdssm_scan_bwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
     const bool use_fused =
         fused_applicable(g, {g.diag_mode == PDSSM_DIAG_PER_STEP ? diag : nullptr, h_saved, dh_opt, h0_opt, lam_in_opt,
                              dbias, g.diag_mode == PDSSM_DIAG_PER_STEP ? ddiag : nullptr, dh0_opt, chunk_state});
+    if (!use_fused && path_fused_forced())
+        return fail(PDSSM_ERR_UNSUPPORTED, "scan_bwd: PDSSM_PATH=fused but the fused path does not apply to these dims");
     if (use_fused) {
         if (dy_opt) {
             r = with_act(g.dtype, [&](auto tv) {

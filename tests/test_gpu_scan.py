@@ -85,16 +85,26 @@ CASES = [
 ]
 
 
+FUSED_N = (32, 64, 128)
+
+
 @pytest.fixture(params=["auto", "generic"])
 def path(request, monkeypatch):
     monkeypatch.setenv("PDSSM_PATH", request.param)
     return request.param
 
 
+def use_path(monkeypatch, path, N, tau):
+    """'auto' on a fused-eligible shape is upgraded to 'fused' so the test proves the fast path ran."""
+    if path == "auto" and N in FUSED_N and tau <= 256:
+        monkeypatch.setenv("PDSSM_PATH", "fused")
+
+
 @pytest.mark.parametrize("case", CASES, ids=[str(c) for c in CASES])
 @pytest.mark.parametrize("bf16", [False, True], ids=["f32", "bf16"])
-def test_scan_fwd_bwd_parity(P, case, bf16, path):
+def test_scan_fwd_bwd_parity(P, case, bf16, path, monkeypatch):
     B, H, L, N, K, c, tau = case
+    use_path(monkeypatch, path, N, tau if tau else 64)
     inp, f, got, ch, ref, Pm, Dz = run_case(P, B, H, L, N, K, c, tau, bf16=bf16, seed=hash(case) % 1000)
     tol = TOL["bf16" if bf16 else "f32"]
     assert rel(cpx(f["h"]), ch["h"]) <= tol
@@ -115,7 +125,8 @@ def test_scan_fwd_bwd_parity(P, case, bf16, path):
 
 
 @pytest.mark.parametrize("N", [16, 64])
-def test_scan_per_dict_and_no_h0(P, N, path):
+def test_scan_per_dict_and_no_h0(P, N, path, monkeypatch):
+    use_path(monkeypatch, path, N, 16)
     inp, f, got, ch, ref, Pm, Dz = run_case(P, 2, 2, 90, N, 5, 2, 16, per_dict=True, h0=False, seed=7)
     assert rel(cpx(f["h"]), ch["h"]) <= 1e-4
     db, dD, g, dh0 = got
@@ -133,7 +144,8 @@ def test_scan_per_dict_and_no_h0(P, N, path):
     assert rel(g.cpu().numpy(), g_r) <= 1e-4
 
 
-def test_determinism_bitwise(P, path):
+def test_determinism_bitwise(P, path, monkeypatch):
+    use_path(monkeypatch, path, 64, 32)
     args = (2, 2, 200, 64, 16, 2, 32)
     _, f1, g1, *_ = run_case(P, *args, seed=3)
     _, f2, g2, *_ = run_case(P, *args, seed=3)
@@ -143,7 +155,8 @@ def test_determinism_bitwise(P, path):
 
 
 @pytest.mark.parametrize("tau", [1, 7, 64, 128])
-def test_tau_invariance_of_final_outputs(P, tau, path):
+def test_tau_invariance_of_final_outputs(P, tau, path, monkeypatch):
+    use_path(monkeypatch, path, 32, 257)
     _, f, got, ch, ref, *_ = run_case(P, 1, 2, 257, 32, 8, 2, tau, seed=11)
     _, f0, got0, *_ = run_case(P, 1, 2, 257, 32, 8, 2, 257, seed=11)
     assert torch.equal(f["maps"][:, :, -1], f0["maps"][:, :, -1])
@@ -179,7 +192,8 @@ def test_fsa_emulation_exact(P, path):
                 assert final_map[b, q] == runs[b, -1]
 
 
-def test_s5_word_problem_exact(P, path):
+def test_s5_word_problem_exact(P, path, monkeypatch):
+    use_path(monkeypatch, path, 64, 64)
     """config 5 structure at reduced L: exact permuted arange states and exact maps."""
     dict_idx, perms5, blocks = synth.s5_dictionary(64, 16, seed=5000)
     B, H, L = 2, 2, 4096
@@ -203,7 +217,8 @@ def test_s5_word_problem_exact(P, path):
 
 
 @pytest.mark.parametrize("N", [16, 32])
-def test_readout_fused_and_dy_backward(P, N, path):
+def test_readout_fused_and_dy_backward(P, N, path, monkeypatch):
+    use_path(monkeypatch, path, N, 16)
     B, H, L, K, c, Pp = 2, 2, 70, 4, 2, 8
     inp = synth.scan_inputs(B, H, L, N, K, c, seed=21, h0=True)
     Cw = synth.readout_C(H, Pp, N, c, seed=21)
