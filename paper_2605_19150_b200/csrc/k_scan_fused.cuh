@@ -275,11 +275,18 @@ template <int NC>
 __device__ __forceinline__ float im_of(typename SVal<NC>::type v) {
     if constexpr (NC == 2) return v.y; else { (void)v; return 0.f; }
 }
+// Exchange-buffer position of state i (N = 32 * NPL): lane l owns states l*NPL + u in
+// registers, and slot u of every lane forms one contiguous 32-element row, so the
+// owners' stores and read-backs are conflict-free (one wavefront per 128 B).  The
+// zero sentinel sits at position N.
+template <int NPL>
+__host__ __device__ constexpr int xpos(int i) { return NPL == 1 ? i : (i % NPL) * 32 + i / NPL; }
+
 template <int NC, int NPL>
 __device__ __forceinline__ void sts_row(typename SVal<NC>::type* row, int lane, const float (&re)[NPL],
                                         const float (&im)[NPL]) {
 #pragma unroll
-    for (int u = 0; u < NPL; ++u) row[lane * NPL + u] = mk<NC>(re[u], im[u]);
+    for (int u = 0; u < NPL; ++u) row[u * 32 + lane] = mk<NC>(re[u], im[u]);
 }
 
 // ------------------------------------------------------------------ fused plan
@@ -309,6 +316,19 @@ struct Rec {
     static constexpr int W = B / 4;
     uint32_t w[W];
 };
+
+// Records of one entry are stored as two 512-byte halves [2][32 lanes][16 B] so that a
+// warp reads its records with two conflict-free 16-byte loads; u16 field idx of lane l:
+__device__ __forceinline__ uint16_t& rec_u16(uint8_t* entry, int l, int idx) {
+    return reinterpret_cast<uint16_t*>(entry + (idx >> 3) * 512 + l * 16)[idx & 7];
+}
+template <int NPL>
+__device__ __forceinline__ void rec_load(const uint8_t* entry, int lane, Rec<NPL>& r) {
+    const uint4 lo = *reinterpret_cast<const uint4*>(entry + lane * 16);
+    const uint4 hi = *reinterpret_cast<const uint4*>(entry + 512 + lane * 16);
+    r.w[0] = lo.x; r.w[1] = lo.y; r.w[2] = lo.z; r.w[3] = lo.w;
+    r.w[4] = hi.x; r.w[5] = hi.y; r.w[6] = hi.z; r.w[7] = hi.w;
+}
 
 template <int NPL>
 __global__ void k_build_fused_plan(const uint16_t* __restrict__ dict_idx, uint8_t* __restrict__ rec,
@@ -347,16 +367,16 @@ __global__ void k_build_fused_plan(const uint16_t* __restrict__ dict_idx, uint8_
             rank += (d2 > di) || (d2 == di && i2 < i);
         }
         const int l = rank % 32, u = rank / 32;
-        uint16_t* r = reinterpret_cast<uint16_t*>(rec + ((size_t)e * 32 + l) * RB);
-        r[u] = (uint16_t)(i * sv);
+        uint8_t* re = rec + (size_t)e * 32 * RB;
+        rec_u16(re, l, u) = (uint16_t)(xpos<NPL>(i) * sv);
         int q = 0;
         for (int j = 0; j < N; ++j) {
             if (sP[j] == i) {
-                if (q < rec_scap(u)) r[rec_soff(u) + q] = (uint16_t)(j * sv);
+                if (q < rec_scap(u)) rec_u16(re, l, rec_soff(u) + q) = (uint16_t)(xpos<NPL>(j) * sv);
                 ++q;
             }
         }
-        for (int qq = q; qq < rec_scap(u); ++qq) r[rec_soff(u) + qq] = (uint16_t)(N * sv);
+        for (int qq = q; qq < rec_scap(u); ++qq) rec_u16(re, l, rec_soff(u) + qq) = (uint16_t)(N * sv);
         atomicMax(&smax[u], q);
         if (q > rec_scap(u)) sovf = 1;
     }
@@ -407,7 +427,7 @@ __device__ __forceinline__ void gather_sum_csr(const typename SVal<NC>::type* vb
         const int st = __ldg(pstart + (size_t)e * (N + 1) + i);
         const int en = __ldg(pstart + (size_t)e * (N + 1) + i + 1);
         for (int q = st; q < en; ++q) {
-            const auto v = vbuf[__ldg(psrc + (size_t)e * N + q)];
+            const auto v = vbuf[xpos<NPL>(__ldg(psrc + (size_t)e * N + q))];
             are[u] += re_of<NC>(v);
             if constexpr (NC == 2) aim[u] += im_of<NC>(v);
         }
@@ -580,7 +600,11 @@ __device__ __forceinline__ void load_tables(const FusedArgs& a, uint8_t* tb, int
     const int K = a.K, N = a.N;
     uint16_t* sP = reinterpret_cast<uint16_t*>(tb + LY::t_P);
     const uint16_t* gP = a.dict_idx + (size_t)h * K * N;
-    for (int i = threadIdx.x; i < K * N; i += blockDim.x) sP[i] = (uint16_t)min((int)__ldg(gP + i), N - 1);
+    // fwd: natural state indices (the pi composition indexes D rows); bwd: exchange positions
+    for (int i = threadIdx.x; i < K * N; i += blockDim.x) {
+        const int p = min((int)__ldg(gP + i), N - 1);
+        sP[i] = (uint16_t)(BWD ? xpos<NPL>(p) : p);
+    }
     if constexpr (!BWD) {
         const uint4* gr = reinterpret_cast<const uint4*>(a.rec + (size_t)h * K * 32 * Rec<NPL>::B);
         uint4* sr = reinterpret_cast<uint4*>(tb + LY::t_rec(K));
@@ -787,7 +811,7 @@ __global__ void __launch_bounds__(Layout<T, NC, NPL, PD, false>::THREADS, 1) k_f
         __syncwarp();
 #pragma unroll
         for (int u = 0; u < NPL; ++u) {
-            const SV z = sbuf[lane * NPL + u];
+            const SV z = sbuf[u * 32 + lane];
             zr[u] = re_of<NC>(z);
             zi[u] = im_of<NC>(z);
         }
@@ -825,7 +849,7 @@ __global__ void __launch_bounds__(Layout<T, NC, NPL, PD, false>::THREADS, 1) k_f
         pump<T, T, NC, NPL, PD, false>(a, fc, consumed, ring, bars, lane, pol_last, pol_out);
         // per-entry tables of this head, in shared memory
         const uint16_t* prow_base = reinterpret_cast<const uint16_t*>(tbl + LY::t_P);
-        const uint8_t* rec_base = tbl + LY::t_rec(a.K) + lane * Rec<NPL>::B;
+        const uint8_t* rec_base = tbl + LY::t_rec(a.K);
         const uint32_t* hdr_base = reinterpret_cast<const uint32_t*>(tbl + LY::t_hdr(a.K));
         const float* dk_base = reinterpret_cast<const float*>(tbl + LY::t_dk(a.K));
         // ---------------- Phase A: aggregate from identity
@@ -838,9 +862,7 @@ __global__ void __launch_bounds__(Layout<T, NC, NPL, PD, false>::THREADS, 1) k_f
         uint4 hn;
         {
             const int k0 = sk[0];
-#pragma unroll
-            for (int i = 0; i < Rec<NPL>::W; ++i)
-                rn.w[i] = reinterpret_cast<const uint32_t*>(rec_base + (size_t)k0 * 32 * Rec<NPL>::B)[i];
+            rec_load<NPL>(rec_base + (size_t)k0 * 32 * Rec<NPL>::B, lane, rn);
             hn = *reinterpret_cast<const uint4*>(hdr_base + 4 * k0);
         }
         for (int gi = 0; gi < ng; ++gi) {
@@ -855,9 +877,7 @@ __global__ void __launch_bounds__(Layout<T, NC, NPL, PD, false>::THREADS, 1) k_f
                 const uint4 hd = hn;
                 {
                     const int kn = sk[v + 1 < n ? v + 1 : v];
-#pragma unroll
-                    for (int q = 0; q < Rec<NPL>::W; ++q)
-                        rn.w[q] = reinterpret_cast<const uint32_t*>(rec_base + (size_t)kn * 32 * Rec<NPL>::B)[q];
+                    rec_load<NPL>(rec_base + (size_t)kn * 32 * Rec<NPL>::B, lane, rn);
                     hn = *reinterpret_cast<const uint4*>(hdr_base + 4 * kn);
                 }
                 Planes<NC, NPL> D, Bv;
@@ -1016,9 +1036,7 @@ __global__ void __launch_bounds__(Layout<T, NC, NPL, PD, false>::THREADS, 1) k_f
         T* hout = static_cast<T*>(a.out0) + ((size_t)s * a.L + it.t0) * row + lane * NPL;
         {
             const int k0 = sk[0];
-#pragma unroll
-            for (int i = 0; i < Rec<NPL>::W; ++i)
-                rn.w[i] = reinterpret_cast<const uint32_t*>(rec_base + (size_t)k0 * 32 * Rec<NPL>::B)[i];
+            rec_load<NPL>(rec_base + (size_t)k0 * 32 * Rec<NPL>::B, lane, rn);
             hn = *reinterpret_cast<const uint4*>(hdr_base + 4 * k0);
         }
         for (int gi = 0; gi < ng; ++gi) {
@@ -1033,9 +1051,7 @@ __global__ void __launch_bounds__(Layout<T, NC, NPL, PD, false>::THREADS, 1) k_f
                 const uint4 hd = hn;
                 {
                     const int kn = sk[v + 1 < n ? v + 1 : v];
-#pragma unroll
-                    for (int q = 0; q < Rec<NPL>::W; ++q)
-                        rn.w[q] = reinterpret_cast<const uint32_t*>(rec_base + (size_t)kn * 32 * Rec<NPL>::B)[q];
+                    rec_load<NPL>(rec_base + (size_t)kn * 32 * Rec<NPL>::B, lane, rn);
                     hn = *reinterpret_cast<const uint4*>(hdr_base + 4 * kn);
                 }
                 Planes<NC, NPL> D, Bv;
@@ -1147,9 +1163,7 @@ __global__ void __launch_bounds__(Layout<T, NC, NPL, PD, true, (int)sizeof(TE)>:
         auto decode_P = [&](uint2 vv, int (&P)[NPL]) {
             if constexpr (NPL == 4) { P[0] = vv.x & 0xffff; P[1] = vv.x >> 16; P[2] = vv.y & 0xffff; P[3] = vv.y >> 16; }
             else if constexpr (NPL == 2) { P[0] = vv.x & 0xffff; P[1] = vv.x >> 16; }
-            else { P[0] = vv.x; }
-#pragma unroll
-            for (int u = 0; u < NPL; ++u) P[u] = min(P[u], N - 1);
+            else { P[0] = vv.x; }   // table rows hold clamped exchange positions
         };
         auto load_D = [&](const uint8_t* sp, int ro, int k, Planes<NC, NPL>& D) {
             if constexpr (PD) {
@@ -1234,7 +1248,7 @@ __global__ void __launch_bounds__(Layout<T, NC, NPL, PD, true, (int)sizeof(TE)>:
             __syncwarp();
 #pragma unroll
             for (int u = 0; u < NPL; ++u) {
-                const SV xp = xbuf[pk[u]];
+                const SV xp = xbuf[xpos<NPL>(pk[u])];
                 xr[u] = br[u] + dr[u] * re_of<NC>(xp) + di[u] * im_of<NC>(xp);   // beta' + conj(d) x[pi]
                 xi[u] = bi[u] + dr[u] * im_of<NC>(xp) - di[u] * re_of<NC>(xp);
             }
