@@ -403,11 +403,12 @@ __device__ __forceinline__ void gather_sorted(const typename SVal<NC>::type* vbu
                                               const Rec<NPL>& r) {
 #pragma unroll
     for (int u = 0; u < NPL; ++u) {
-        float ar = 0.f, ai = 0.f;
         using SVT = typename SVal<NC>::type;
         const char* vb = reinterpret_cast<const char*>(vbuf);
+        const SVT v0 = *reinterpret_cast<const SVT*>(vb + rec_off<NPL>(r, rec_soff(u)));
+        float ar = re_of<NC>(v0), ai = im_of<NC>(v0);
 #pragma unroll
-        for (int q = 0; q < rec_scap(u); ++q) {
+        for (int q = 1; q < rec_scap(u); ++q) {
             const SVT v = *reinterpret_cast<const SVT*>(vb + rec_off<NPL>(r, rec_soff(u) + q));
             ar += re_of<NC>(v);
             if constexpr (NC == 2) ai += im_of<NC>(v);
@@ -529,6 +530,7 @@ __device__ __forceinline__ void apply_aggregate(int lane, int N, uint16_t* key, 
         xi[u] = im_of<NC>(o) + bim[u];
         if (mp) mp[u] = key[mp[u]];
     }
+    __syncwarp();   // the buffers alias the exchange rows of the next phase
 }
 
 
@@ -577,10 +579,15 @@ struct Layout {
     static constexpr size_t w_ring = 0;
     static constexpr size_t w_bar = al16(w_ring + (size_t)PF * SLOT);
     static constexpr size_t w_x = al16(w_bar + (size_t)PF * 8);              // exchange [2][N+1]
-    static constexpr size_t w_ob = al16(w_x + (size_t)2 * (N + 1) * SV);    // fwd chain result [N]
-    static constexpr size_t w_key = al16(w_ob + (BWD ? 0 : (size_t)N * SV)); // fwd chain keys u16 [N]
-    static constexpr size_t w_cnt = al16(w_key + (BWD ? 0 : (size_t)N * 2)); // fwd chain counts int [N]
-    static constexpr size_t w_k = al16(w_cnt + (BWD ? 0 : (size_t)N * 4));   // k* of the chunk [TAUMAX]
+    static constexpr size_t x_end = al16(w_x + (size_t)2 * (N + 1) * SV);
+    // fwd chain buffers (apply_aggregate runs between the phases, when the exchange rows
+    // are idle): complex -- result [N] over the second row, keys u16 [N] and counts int [N]
+    // over the first row below its zero sentinel; real -- separate
+    static constexpr bool ALIAS = NC == 2;
+    static constexpr size_t w_ob = ALIAS ? w_x + (size_t)(N + 1) * SV : x_end;
+    static constexpr size_t w_key = ALIAS ? w_x : al16(w_ob + (BWD ? 0 : (size_t)N * SV));
+    static constexpr size_t w_cnt = ALIAS ? w_x + (size_t)N * 2 : al16(w_key + (BWD ? 0 : (size_t)N * 2));
+    static constexpr size_t w_k = ALIAS ? x_end : al16(w_cnt + (BWD ? 0 : (size_t)N * 4));   // k* of the chunk [TAUMAX]
     static constexpr size_t w_g = al16(w_k + TAUMAX);                        // bwd g partials [32][33]
     static constexpr size_t w_bytes = al16(w_g + (BWD ? 32 * 33 * 4 : 0));
     static constexpr size_t bytes = (size_t)WARPS * w_bytes;
@@ -701,8 +708,8 @@ template <typename T, typename TE, int NC, int NPL, bool PD, bool BWD>
 __device__ __forceinline__ void issue_fill(const FusedArgs& a, const Item& it, int g, uint8_t* ring, uint64_t* bars,
                                            int slot, uint64_t pol_last, uint64_t pol_first) {
     using LY = Layout<T, NC, NPL, PD, BWD, (int)sizeof(TE)>;
-    const int N = a.N;
-    const size_t row = (size_t)NC * N;
+    constexpr int N = LY::N;
+    constexpr size_t row = (size_t)NC * N;
     const size_t seq0 = (size_t)it.s * a.L;
     const int ng = (it.n + LY::G - 1) / LY::G;
     const bool phC = g >= ng;
@@ -782,8 +789,8 @@ __global__ void __launch_bounds__(Layout<T, NC, NPL, PD, false>::THREADS, 1) k_f
     uint16_t* key = reinterpret_cast<uint16_t*>(base + LY::w_key);
     int* cnt = reinterpret_cast<int*>(base + LY::w_cnt);
     uint8_t* sk = base + LY::w_k;
-    const int N = a.N;
-    const size_t row = (size_t)NC * N;
+    constexpr int N = LY::N;
+    constexpr size_t row = (size_t)NC * N;
     if (lane == 0) {
         for (int i = 0; i < PF; ++i) mbar_init(bars + i, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -870,7 +877,9 @@ __global__ void __launch_bounds__(Layout<T, NC, NPL, PD, false>::THREADS, 1) k_f
             if (!(a.debug_nochain & 2)) mbar_wait(bars + slot, (consumed / PF) & 1);
             const uint8_t* sp = ring + (size_t)slot * LY::SLOT;
             const int len = min(LY::G, n - gi * LY::G);
-            for (int i = 0; i < len; ++i) {
+#pragma unroll
+            for (int i = 0; i < LY::G; ++i) {
+                if (i >= len) break;
                 const int v = gi * LY::G + i;
                 const int k = sk[v];
                 const Rec<NPL> r = rn;
@@ -1044,7 +1053,9 @@ __global__ void __launch_bounds__(Layout<T, NC, NPL, PD, false>::THREADS, 1) k_f
             if (!(a.debug_nochain & 2)) mbar_wait(bars + slot, (consumed / PF) & 1);
             const uint8_t* sp = ring + (size_t)slot * LY::SLOT;
             const int len = min(LY::G, n - gi * LY::G);
-            for (int i = 0; i < len; ++i) {
+#pragma unroll
+            for (int i = 0; i < LY::G; ++i) {
+                if (i >= len) break;
                 const int v = gi * LY::G + i;
                 const int k = sk[v];
                 const Rec<NPL> r = rn;
@@ -1113,8 +1124,8 @@ __global__ void __launch_bounds__(Layout<T, NC, NPL, PD, true, (int)sizeof(TE)>:
     SV* xb = reinterpret_cast<SV*>(base + LY::w_x);
     uint8_t* sk = base + LY::w_k;
     float* gbuf = reinterpret_cast<float*>(base + LY::w_g);   // [32][33] per-lane g partials
-    const int N = a.N;
-    const size_t row = (size_t)NC * N;
+    constexpr int N = LY::N;
+    constexpr size_t row = (size_t)NC * N;
     const TE* ein = static_cast<const TE*>(a.bias);
     if (lane == 0) {
         for (int i = 0; i < PF; ++i) mbar_init(bars + i, 1);
@@ -1193,7 +1204,9 @@ __global__ void __launch_bounds__(Layout<T, NC, NPL, PD, true, (int)sizeof(TE)>:
             if (!(a.debug_nochain & 2)) mbar_wait(bars + slot, (consumed / PF) & 1);
             const uint8_t* sp = ring + (size_t)slot * LY::SLOT;
             const int len = min(LY::G, n - gi * LY::G);
-            for (int i = 0; i < len; ++i) {
+#pragma unroll
+            for (int i = 0; i < LY::G; ++i) {
+                if (i >= len) break;
                 const int v = gi * LY::G + i;
                 const int t = t1 - 1 - v;
                 const int ro = len - 1 - i;           // row offset of time t in the slot
@@ -1339,7 +1352,9 @@ __global__ void __launch_bounds__(Layout<T, NC, NPL, PD, true, (int)sizeof(TE)>:
             if (!(a.debug_nochain & 2)) mbar_wait(bars + slot, (consumed / PF) & 1);
             const uint8_t* sp = ring + (size_t)slot * LY::SLOT;
             const int len = min(LY::G, n - gi * LY::G);
-            for (int i = 0; i < len; ++i) {
+#pragma unroll
+            for (int i = 0; i < LY::G; ++i) {
+                if (i >= len) break;
                 const int v = gi * LY::G + i;
                 const int t = t1 - 1 - v;
                 const int ro = len - 1 - i;

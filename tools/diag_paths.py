@@ -15,7 +15,7 @@ tau = int(os.environ.get("TAU", 0))
 inp = synth.scan_inputs(B, H, L, N, K, c, seed=2000, dh=True)
 d = {k: torch.from_numpy(v).cuda() for k, v in inp.items()}
 d["dict_idx"] = d["dict_idx"].to(torch.int16)
-for path in ["generic", "auto"]:
+for path in ["generic", "fused"]:
     os.environ["PDSSM_PATH"] = path
     f = P.scan_fwd(d["kstar"], d["dict_idx"], d["diag"], d["bias"], tau=tau)
     r = P.scan_bwd(d["kstar"], d["dict_idx"], d["diag"], f["h"], f["chunk_state"], f["dims"], dh=d["dh"])
