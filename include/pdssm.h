@@ -139,11 +139,33 @@ pdssm_status pdssm_sparsify(const float* M, uint16_t* dict_idx, const pdssm_dims
  *   P_opt    uint16 [B][H][L][N]  out (optional): P_t = dict_idx[h][k*]
  *   logits_opt f32  [B][H][L][K]  out (optional): the selector logits
  * Logits are accumulated in fp32 from the act-dtype products.
+ * Path: when x and S are 16-byte aligned, d_in * sizeof(act) % 16 == 0 and
+ * lcm(K, 16) <= 256, the logits are a tcgen05 GEMM (bf16: kind::f16; f32:
+ * 3xTF32 split, ~2^-21 relative per product) with the argmax and the P gather
+ * fused into the TMEM epilogue (no workspace used, ws may be NULL); otherwise a
+ * SIMT GEMM writes the logits to ws (pdssm_workspace_bytes(dims, OP_SELECT)) or
+ * logits_opt, then the argmax kernel runs.  Under PDSSM_CHECK_FINITE the tensor
+ * -core path reports non-finite logits, the SIMT path non-finite x.
  * ------------------------------------------------------------------------- */
 pdssm_status pdssm_select(const void* x, const void* S, const uint16_t* dict_idx,
                           uint8_t* kstar, uint16_t* P_opt, float* logits_opt,
                           const pdssm_dims* dims, void* ws, size_t ws_bytes,
                           pdssm_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * a5: input projection feeding the scan, b_t = B u_t (Eq. 1; "standard
+ * matrix multiplication"), static B (reading R4), written directly in
+ * the scan layout:
+ *   x      act [B][L][d_in]        tokens (dims.d_in)
+ *   Bw     act [H][c][N][d_in]     projection rows; plane c=0 real part, c=1 imaginary
+ *   b_out  act [B][H][L][c][N]     out: b[b][h][t][c][n] = sum_d Bw[h][c][n][d] x[b][t][d]
+ * Uses dims.batch, heads, len, state, is_complex, d_in, dtype.  fp32 accumulation.
+ * Path: tcgen05 GEMM (bf16: kind::f16; f32: 3xTF32) when x, Bw, b_out are 16-byte
+ * aligned, d_in * sizeof(act) % 16 == 0 and c*N % 16 == 0; otherwise a SIMT GEMM.
+ * Errors: ERR_NULL, ERR_SHAPE (d_in < 1 or bad dims), ERR_ALIGN (element misalignment).
+ * ------------------------------------------------------------------------- */
+pdssm_status pdssm_project(const void* x, const void* Bw, void* b_out, const pdssm_dims* dims,
+                           pdssm_stream_t stream);
 
 /* ---------------------------------------------------------------------------
  * a6-a8: forward chunked scan (Alg. 1; Kernels A/B/C

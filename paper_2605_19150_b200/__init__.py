@@ -67,6 +67,7 @@ def _load():
         "pdssm_summary_bytes": (sz, [D]),
         "pdssm_sparsify": (ctypes.c_int, [vp, vp, D, vp]),
         "pdssm_select": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, D, vp, sz, vp]),
+        "pdssm_project": (ctypes.c_int, [vp, vp, vp, D, vp]),
         "pdssm_scan_fwd": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, D, vp, sz, vp]),
         "pdssm_scan_bwd": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, D, vp, sz, vp]),
         "pdssm_segment_summary": (ctypes.c_int, [vp, vp, vp, vp, vp, D, vp, sz, vp]),
@@ -195,6 +196,22 @@ def select(x, S, dict_idx=None, want_P=False, want_logits=False, check_finite=Fa
     _check(lib.pdssm_select(_ptr(x), _ptr(S), _ptr(dict_idx), _ptr(kstar), _ptr(P), _ptr(logits),
                             ctypes.byref(dims), _ptr(ws), wsb, _stream()))
     return kstar, P, logits
+
+
+def project(x, Bw, out=None):
+    """a5: b_t = B x_t in the scan layout (Eq. 1).
+
+    x [B][L][d_in], Bw [H][c][N][d_in] (same dtype) -> b [B][H][L][c][N]."""
+    torch = _torch()
+    _contig(x, "x"), _contig(Bw, "Bw")
+    B, L, d_in = x.shape
+    H, c, N, _ = Bw.shape
+    if Bw.dtype != x.dtype:
+        raise TypeError("x and Bw must have the same dtype")
+    dims = make_dims(B, H, L, N, 1, c=c, dtype=_dtype_code(x), d_in=d_in)
+    b = out if out is not None else torch.empty((B, H, L, c, N), dtype=x.dtype, device=x.device)
+    _check(lib.pdssm_project(_ptr(x), _ptr(Bw), _ptr(b), ctypes.byref(dims), _stream()))
+    return b
 
 
 def scan_fwd(kstar, dict_idx, diag, bias, h0=None, C=None, tau=0, per_dict=False, want_h=True,

@@ -1,0 +1,339 @@
+// Dense contractions of the path on the 5th-generation tensor cores (tcgen05):
+//   a2/a3  selector logits  logits[(b,t)][(h,k)] = sum_d x[b,t,d] S[h,k,d]   (Eq. 6)
+//          with the hard-selection argmax fused into the TMEM epilogue      (Eq. 7)
+//          and the optional P_t = dict_idx[h][k*] gather                    (Eq. 8)
+//   a5     projection       b[b,h,t,(c,n)] = sum_d x[b,t,d] B[h,c,n,d]       (Eq. 1 b_t = B u_t,
+//          PAPER.md:94-95, :970), written straight into the scan layout [B][H][L][c][N].
+//
+// One CTA computes a BM x BN tile (BM = 128 tokens, BN <= 256 output columns):
+//   warp 0 (one lane)  TMA producer: 128-byte K slabs of x and of the weight rows into a
+//                      STAGES-deep ring (SWIZZLE_128B, full/empty mbarriers);
+//   warp 1 (one lane)  MMA issuer: tcgen05.mma cta_group::1, M=128, N=BN, K = 32 bytes per
+//                      instruction (bf16: kind::f16, K=16; fp32: kind::tf32, K=8), fp32
+//                      accumulators in TMEM; tcgen05.commit frees ring slots;
+//   warp 2             TMEM allocator (BN columns rounded to a power of two);
+//   warps 4-7          epilogue: warp 4+q reads TMEM lanes 32q..32q+31 (= tile rows) with
+//                      tcgen05.ld 32x32b and applies the fused epilogue.
+// Operands are K-major (the HBM layouts of x, S and B), so no transposes are needed.
+#pragma once
+#include "pdssm_common.cuh"
+
+#include <cuda.h>
+
+namespace pdssm {
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int ROWB = 128;   // K bytes per ring slot row = one 128-byte swizzle atom
+constexpr int THREADS = 256;
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t c) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(c) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "TC_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra TC_WAIT_%=;\n}" ::"r"(su32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            su32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(su32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// Shared-memory matrix descriptor, K-major SWIZZLE_128B: rows of 128 B, 8-row atoms
+// 1024 B apart (SBO), LBO unused (1), version 1 (sm_100), layout type 2.
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+    uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)1u << 16;
+    d |= (uint64_t)(1024u >> 4) << 32;
+    d |= (uint64_t)1u << 46;
+    d |= (uint64_t)2u << 61;
+    return d;
+}
+// Instruction descriptor: D f32, A/B format fmt (1 = bf16 under kind::f16, 2 = tf32 under
+// kind::tf32), both K-major, N = n, M = 128.
+__host__ __device__ constexpr uint32_t idesc(uint32_t fmt, int n) {
+    return (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+template <typename T>
+struct Kind;
+template <>
+struct Kind<__nv_bfloat16> {
+    static constexpr uint32_t FMT = 1;
+    __device__ static void mma(uint32_t tmem, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem),
+            "l"(a), "l"(b), "r"(id), "r"(acc)
+            : "memory");
+    }
+};
+template <>
+struct Kind<float> {
+    static constexpr uint32_t FMT = 2;
+    __device__ static void mma(uint32_t tmem, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem),
+            "l"(a), "l"(b), "r"(id), "r"(acc)
+            : "memory");
+    }
+};
+
+__device__ __forceinline__ void commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+                 : "memory");
+}
+
+// 16 consecutive accumulator columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__host__ __device__ constexpr int tmem_cols(int bn) { return bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 128 ? 128 : 256; }
+
+// --------------------------------------------------------------------------- epilogues
+// a3 (+a4): per row (token) and head, k* = smallest argmax_k of the K fp32 logits
+// (strict '>' over ascending k: ties -> smallest index, NaN never wins, all-NaN -> 0;
+// readings R7/R8); optional logits and P rows.
+struct EpiSelect {
+    uint8_t* kstar;
+    float* logits;             // [B][H][L][K] or null
+    const uint16_t* dict_idx;  // [H][K][N] (P gather) or null
+    uint16_t* P;               // [B][H][L][N] or null
+    int64_t M;                 // B * L
+    int L, H, K, N;
+    uint32_t flags;
+    __device__ void operator()(uint32_t taddr, int64_t m, int n0, int bn) const {
+        const bool valid = m < M;
+        const int64_t b = valid ? m / L : 0, t = valid ? m - b * L : 0;
+        const int h0 = n0 / K;
+        float best = -INFINITY;
+        int arg = K, kk = 0, hh = 0;
+        for (int c0 = 0; c0 < bn; c0 += 16) {
+            float v[16];
+            tmem_ld16(taddr + (uint32_t)c0, v);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const float x = v[i];
+                const int h = h0 + hh;
+                if (valid && h < H) {
+                    if ((flags & PDSSM_CHECK_FINITE) && !isfinite(x)) report(ERRBIT_NONFINITE);
+                    if (logits) logits[(((size_t)b * H + h) * L + t) * K + kk] = x;
+                }
+                if (x > best) {
+                    best = x;
+                    arg = kk;
+                }
+                if (++kk == K) {
+                    if (valid && h < H) {
+                        const int k = arg >= K ? 0 : arg;
+                        const size_t r = ((size_t)b * H + h) * L + t;
+                        kstar[r] = (uint8_t)k;
+                        if (P) {
+                            const uint16_t* src = dict_idx + ((size_t)h * K + k) * N;
+                            uint16_t* dst = P + r * N;
+                            for (int j = 0; j < N; ++j) dst[j] = __ldg(src + j);
+                        }
+                    }
+                    ++hh;
+                    kk = 0;
+                    best = -INFINITY;
+                    arg = K;
+                }
+            }
+        }
+    }
+};
+
+// a5: column j = (h, c, n) of the tile -> b[b][h][t][c][n] (activation dtype TO)
+template <typename TO>
+struct EpiProject {
+    TO* out;
+    int64_t M;
+    int L, H, cN;
+    int64_t NN;   // H * cN
+    __device__ void operator()(uint32_t taddr, int64_t m, int n0, int bn) const {
+        const bool valid = m < M;
+        const int64_t b = valid ? m / L : 0, t = valid ? m - b * L : 0;
+        for (int c0 = 0; c0 < bn; c0 += 16) {
+            float v[16];
+            tmem_ld16(taddr + (uint32_t)c0, v);
+            const int64_t j = (int64_t)n0 + c0;
+            if (!valid || j >= NN) continue;
+            const int64_t h = j / cN, w = j - h * cN;
+            TO* dst = out + (((size_t)b * H + h) * L + t) * cN + w;
+            if constexpr (std::is_same<TO, float>::value) {
+#pragma unroll
+                for (int i = 0; i < 16; i += 4)
+                    *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+            } else {
+                uint32_t p[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const __nv_bfloat162 q = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+                    p[i] = *reinterpret_cast<const uint32_t*>(&q);
+                }
+                reinterpret_cast<uint4*>(dst)[0] = make_uint4(p[0], p[1], p[2], p[3]);
+                reinterpret_cast<uint4*>(dst)[1] = make_uint4(p[4], p[5], p[6], p[7]);
+            }
+        }
+    }
+};
+
+// --------------------------------------------------------------------------- kernel
+// SPLIT (fp32 operands): 3xTF32.  Each landed fp32 slab is split in shared memory by the
+// epilogue warps (idle during the main loop) into hi = tf32_rna(a) (in place) and
+// lo = a - hi (a twin slab at the same swizzled offsets); the MMA warp then issues
+// lo*hi + hi*lo + hi*hi per K step, which keeps the products to ~2^-21 relative
+// (plain TF32 would be 2^-11), i.e. fp32-grade logits and projections.
+__device__ __forceinline__ uint32_t tf32_rna(float a) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(a));
+    return r;
+}
+
+template <typename T, int STAGES, bool SPLIT>
+struct Smem {
+    __host__ __device__ static constexpr size_t slot(int bn) { return (size_t)(BM + bn) * ROWB; }   // A rows then B rows
+    __host__ __device__ static constexpr size_t ring(int bn) { return (size_t)STAGES * slot(bn) * (SPLIT ? 2 : 1); }
+    __host__ __device__ static constexpr size_t bytes(int bn) { return 1024 + ring(bn) + 8 * (3 * STAGES + 1) + 16; }
+};
+
+template <typename T, int STAGES, bool SPLIT, class Epi>
+__global__ void __launch_bounds__(THREADS, 1)
+    k_gemm_tc(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, int nk, int bn, Epi epi) {
+    using SM = Smem<T, STAGES, SPLIT>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    const size_t SLOT = SM::slot(bn);                  // multiple of 1024 (bn % 8 == 0)
+    auto hi = [&](int s) { return smem + (size_t)s * SLOT; };
+    auto lo = [&](int s) { return smem + (size_t)(STAGES + s) * SLOT; };
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::ring(bn));
+    uint64_t* conv = full + STAGES;
+    uint64_t* empty = conv + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t ncols = (uint32_t)tmem_cols(bn);
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(conv + s, 4);   // one arrival per converter warp
+            mbar_init(empty + s, 1);
+        }
+        mbar_init(tfull, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mB)) : "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)), "r"(ncols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tslot;
+    const int64_t m0 = (int64_t)blockIdx.x * BM;
+    const int n0 = blockIdx.y * bn;
+    constexpr int EK = ROWB / (int)sizeof(T);   // elements of K per slab row
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint32_t bytes = (uint32_t)SLOT;
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % STAGES;
+                if (kb >= STAGES) mbar_wait(empty + s, (uint32_t)((kb / STAGES) + 1) & 1u);
+                mbar_expect_tx(full + s, bytes);
+                tma_2d(hi(s), &mA, kb * EK, (int)m0, full + s);
+                tma_2d(hi(s) + (size_t)BM * ROWB, &mB, kb * EK, n0, full + s);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t id = idesc(Kind<T>::FMT, bn);
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % STAGES;
+                mbar_wait((SPLIT ? conv : full) + s, (uint32_t)(kb / STAGES) & 1u);
+                fence_after();
+                const uint64_t ah = sdesc(su32(hi(s))), bh = sdesc(su32(hi(s) + (size_t)BM * ROWB));
+                const uint64_t al = sdesc(su32(lo(s))), bl = sdesc(su32(lo(s) + (size_t)BM * ROWB));
+#pragma unroll
+                for (int k = 0; k < ROWB / 32; ++k) {   // 32 bytes of K per instruction
+                    const uint32_t acc0 = (kb | k) != 0;
+                    if constexpr (SPLIT) {
+                        Kind<T>::mma(tmem, al + 2 * k, bh + 2 * k, id, acc0);
+                        Kind<T>::mma(tmem, ah + 2 * k, bl + 2 * k, id, 1u);
+                        Kind<T>::mma(tmem, ah + 2 * k, bh + 2 * k, id, 1u);
+                    } else {
+                        Kind<T>::mma(tmem, ah + 2 * k, bh + 2 * k, id, acc0);
+                    }
+                }
+                commit(empty + s);
+            }
+            commit(tfull);
+        }
+        __syncwarp();
+    } else if (warp >= 4) {
+        if constexpr (SPLIT) {
+            // converters: split every landed slab (the producer reused slot s only after the
+            // MMAs of its previous round completed, and full[s] completes after that reuse)
+            const int ct = threadIdx.x - 128;
+            const int nchunks = (BM + bn) * (ROWB / 16);
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % STAGES;
+                mbar_wait(full + s, (uint32_t)(kb / STAGES) & 1u);
+                float4* ph = reinterpret_cast<float4*>(hi(s));
+                float4* pl = reinterpret_cast<float4*>(lo(s));
+                for (int i = ct; i < nchunks; i += 128) {
+                    const float4 a = ph[i];
+                    const uint32_t h0 = tf32_rna(a.x), h1 = tf32_rna(a.y), h2 = tf32_rna(a.z), h3 = tf32_rna(a.w);
+                    ph[i] = make_float4(__uint_as_float(h0), __uint_as_float(h1), __uint_as_float(h2), __uint_as_float(h3));
+                    pl[i] = make_float4(a.x - __uint_as_float(h0), a.y - __uint_as_float(h1), a.z - __uint_as_float(h2),
+                                        a.w - __uint_as_float(h3));
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> MMA reads
+                __syncwarp();
+                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(conv + s)) : "memory");
+            }
+        }
+        mbar_wait(tfull, 0);
+        fence_after();
+        const int q = warp - 4;
+        epi(tmem + ((uint32_t)(32 * q) << 16), m0 + 32 * q + lane, n0, bn);
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols) : "memory");
+    }
+}
+
+}  // namespace tc
+}  // namespace pdssm

@@ -90,6 +90,60 @@ __global__ void __launch_bounds__(256) k_select_logits_simt(const T* __restrict_
     }
 }
 
+// a5 generic path (shapes TMA cannot take): b[b][h][t][w] = sum_d x[b][t][d] Bw[h][w][d],
+// w = (c, n); same SIMT tiling as the selector logits.
+template <typename T>
+__global__ void __launch_bounds__(256) k_project_simt(const T* __restrict__ x, const T* __restrict__ Bw,
+                                                      T* __restrict__ out, int B, int L, int H, int cN, int d_in) {
+    constexpr int TM = 64, TN = 64, TK = 32;
+    __shared__ float xs[TK][TM + 4];
+    __shared__ float ws[TK][TN + 4];
+    const int M = B * L, NN = H * cN;
+    const int m0 = blockIdx.x * TM, n0 = blockIdx.y * TN;
+    const int tid = threadIdx.x;
+    const int tm = (tid / 16) * 4, tn = (tid % 16) * 4;
+    float acc[4][4] = {};
+    for (int d0 = 0; d0 < d_in; d0 += TK) {
+        for (int q = tid; q < TM * TK; q += 256) {
+            const int r = q / TK, dd = q % TK;
+            const int m = m0 + r, d = d0 + dd;
+            xs[dd][r] = (m < M && d < d_in) ? ldact(x + (size_t)m * d_in + d) : 0.f;
+        }
+        for (int q = tid; q < TN * TK; q += 256) {
+            const int r = q / TK, dd = q % TK;
+            const int n = n0 + r, d = d0 + dd;
+            ws[dd][r] = (n < NN && d < d_in) ? ldact(Bw + (size_t)n * d_in + d) : 0.f;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int dd = 0; dd < TK; ++dd) {
+            float a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = xs[dd][tm + i];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) b[i] = ws[dd][tn + i];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[i][q] = fmaf(a[i], b[q], acc[i][q]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int m = m0 + tm + i;
+        if (m >= M) continue;
+        const int b = m / L, t = m % L;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int n = n0 + tn + q;
+            if (n >= NN) continue;
+            const int h = n / cN, w = n % cN;
+            stact(out + (((size_t)b * H + h) * L + t) * cN + w, acc[i][q]);
+        }
+    }
+}
+
 // k*[b,h,t] = argmax_k logits (smallest index on ties, NaN never wins); optional P gather.
 __global__ void k_select_argmax(const float* __restrict__ logits, const uint16_t* __restrict__ dict_idx,
                                 uint8_t* __restrict__ kstar, uint16_t* __restrict__ P, int64_t rows, int H, int L,

@@ -14,6 +14,9 @@
 #include "k_select.cuh"
 #include "k_sp.cuh"
 #include "k_scan_fused.cuh"
+#include "k_gemm_tc.cuh"
+
+#include <mutex>
 
 
 using namespace pdssm;
@@ -216,6 +219,86 @@ bool path_generic_forced() {
 bool path_fused_forced() {
     const char* p = getenv("PDSSM_PATH");
     return p && strcmp(p, "fused") == 0;
+}
+
+// ---------------------------------------------------------------------------
+// tcgen05 GEMMs (a2/a3 select, a5 projection): TMA descriptors and launch
+// ---------------------------------------------------------------------------
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+// K-major operand [rows][kdim] (row stride kdim elements): box = one 128-byte K slab x box_rows,
+// SWIZZLE_128B (the layout the UMMA descriptors describe); out-of-range boxes read zeros
+bool make_kmajor_map(CUtensorMap* m, const void* ptr, size_t esz, int64_t kdim, int64_t rows, int box_rows) {
+    EncodeTiledFn f = encode_tiled();
+    if (!f) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)kdim, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)(kdim * esz)};
+    cuuint32_t box[2] = {(cuuint32_t)(tc::ROWB / esz), (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1, 1};
+    return f(m, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr),
+             dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int64_t gcd64(int64_t a, int64_t b) { return b ? gcd64(b, a % b) : a; }
+
+// operands usable by TMA: 16-byte aligned base and row pitch
+bool tc_operands_ok(const Geo& g, std::initializer_list<const void*> ptrs) {
+    if (path_generic_forced() || !encode_tiled()) return false;
+    if ((g.d_in * (int64_t)g.act) % 16 != 0) return false;
+    for (const void* p : ptrs)
+        if (misaligned(p, 16)) return false;
+    return true;
+}
+
+// stages: bf16 4 x 48 KB ring; fp32 (3xTF32, hi + lo slabs) 2 x 96 KB
+template <typename T>
+constexpr int tc_stages() { return std::is_same<T, float>::value ? 2 : 4; }
+
+template <typename T, class Epi>
+pdssm_status launch_tc(const Geo& g, const void* A, int64_t rows_a, const void* Bm, int64_t rows_b, int bn, Epi epi,
+                       cudaStream_t st, const char* what) {
+    constexpr bool SPLIT = std::is_same<T, float>::value;
+    constexpr int STAGES = tc_stages<T>();
+    using SM = tc::Smem<T, STAGES, SPLIT>;
+    CUtensorMap mA, mB;
+    if (!make_kmajor_map(&mA, A, sizeof(T), g.d_in, rows_a, tc::BM) ||
+        !make_kmajor_map(&mB, Bm, sizeof(T), g.d_in, rows_b, bn))
+        return fail(PDSSM_ERR_CUDA, "%s: cuTensorMapEncodeTiled failed", what);
+    const size_t smem = SM::bytes(256);   // sized for the largest tile: one attribute per instantiation
+    auto kern = tc::k_gemm_tc<T, STAGES, SPLIT, Epi>;
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
+    if (attr_err != cudaSuccess) return fail(PDSSM_ERR_CUDA, "%s: cudaFuncSetAttribute: %s", what, cudaGetErrorString(attr_err));
+    const int nk = (int)ceil_div(g.d_in * (int64_t)sizeof(T), tc::ROWB);
+    dim3 grid((unsigned)ceil_div(rows_a, tc::BM), (unsigned)ceil_div(rows_b, bn));
+    kern<<<grid, tc::THREADS, SM::bytes(bn), st>>>(mA, mB, nk, bn, epi);
+    return cuda_check(what);
+}
+
+// select tile width: whole heads, a multiple of lcm(K, 16), <= 256 (0: not possible)
+int select_bn(const Geo& g) {
+    const int64_t l = g.K / gcd64(g.K, 16) * 16;
+    if (l > 256) return 0;
+    const int64_t full = (256 / l) * l;
+    const int64_t need = ceil_div(g.H * g.K, l) * l;
+    return (int)(need < full ? need : full);
 }
 
 template <typename F>
@@ -423,13 +506,22 @@ pdssm_status pdssm_select(const void* x, const void* S, const uint16_t* dict_idx
     if (misaligned(x, g.act) || misaligned(S, g.act) || misaligned(dict_idx, 2) || misaligned(P_opt, 2) ||
         misaligned(logits_opt, 4))
         return fail(PDSSM_ERR_ALIGN, "select: misaligned pointer");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    // tensor-core path (a2 logits in TMEM, a3 argmax + a4 P gather fused in the epilogue)
+    const int bn = select_bn(g);
+    if (bn > 0 && tc_operands_ok(g, {x, S})) {
+        tc::EpiSelect epi{kstar, logits_opt, dict_idx, P_opt, g.B * g.L, (int)g.L, (int)g.H, (int)g.K, (int)g.N, g.flags};
+        return with_act(g.dtype, [&](auto tv) {
+            using T = decltype(tv);
+            return launch_tc<T>(g, x, g.B * g.L, S, g.H * g.K, bn, epi, st, "select_tc");
+        });
+    }
     float* logits = logits_opt;
     if (!logits) {
         if (!ws || ws_bytes < ws_bytes_g(g, PDSSM_OP_SELECT))
             return fail(PDSSM_ERR_WORKSPACE, "select: workspace too small (need %zu)", ws_bytes_g(g, PDSSM_OP_SELECT));
         logits = static_cast<float*>(ws);
     }
-    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const int64_t M = g.B * g.L, NN = g.H * g.K;
     dim3 grid((unsigned)ceil_div(M, 64), (unsigned)ceil_div(NN, 64));
     r = with_act(g.dtype, [&](auto tv) {
@@ -443,6 +535,33 @@ pdssm_status pdssm_select(const void* x, const void* S, const uint16_t* dict_idx
     k_select_argmax<<<(unsigned)ceil_div(rows, 8), dim3(32, 8), 0, st>>>(logits, dict_idx, kstar, P_opt, rows,
                                                                        (int)g.H, (int)g.L, (int)g.N, (int)g.K);
     return cuda_check("select_argmax");
+}
+
+pdssm_status pdssm_project(const void* x, const void* Bw, void* b_out, const pdssm_dims* dims, pdssm_stream_t stream) {
+    Geo g;
+    pdssm_status r = geo_of(dims, &g);
+    if (r) return r;
+    if (g.d_in < 1) return fail(PDSSM_ERR_SHAPE, "project: d_in must be >= 1");
+    if (!x || !Bw || !b_out) return fail(PDSSM_ERR_NULL, "project: x, Bw, b_out are required");
+    if (misaligned(x, g.act) || misaligned(Bw, g.act) || misaligned(b_out, g.act))
+        return fail(PDSSM_ERR_ALIGN, "project: misaligned pointer");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t cN = g.nc * g.N, NN = g.H * cN;
+    if (cN % 16 == 0 && tc_operands_ok(g, {x, Bw, b_out})) {
+        return with_act(g.dtype, [&](auto tv) {
+            using T = decltype(tv);
+            tc::EpiProject<T> epi{static_cast<T*>(b_out), g.B * g.L, (int)g.L, (int)g.H, (int)cN, NN};
+            return launch_tc<T>(g, x, g.B * g.L, Bw, NN, (int)(NN < 256 ? NN : 256), epi, st, "project_tc");
+        });
+    }
+    dim3 grid((unsigned)ceil_div(g.B * g.L, 64), (unsigned)ceil_div(NN, 64));
+    return with_act(g.dtype, [&](auto tv) {
+        using T = decltype(tv);
+        k_project_simt<T><<<grid, 256, 0, st>>>(static_cast<const T*>(x), static_cast<const T*>(Bw),
+                                                static_cast<T*>(b_out), (int)g.B, (int)g.L, (int)g.H, (int)cN,
+                                                (int)g.d_in);
+        return cuda_check("project_simt");
+    });
 }
 
 static pdssm_status common_scan_checks(const Geo& g, const void* kstar, const void* dict_idx, const void* diag) {

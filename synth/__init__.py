@@ -140,6 +140,13 @@ def scan_inputs(B, H, L, N, K, c, seed, h0=False, per_dict=False, sticky=0.0, dh
     return out
 
 
+def projection_B(H, c, N, d_in, seed):
+    """Bw[H][c][N][d_in] ~ U(+-1/sqrt(d_in)) (plane 0 real part, 1 imaginary)."""
+    r = _rng(seed, "Bw")
+    lim = 1.0 / np.sqrt(d_in)
+    return r.uniform(-lim, lim, size=(H, c, N, d_in)).astype(np.float32)
+
+
 def readout_C(H, P, N, c, seed):
     """C[H][c][P][N] ~ U(+-1/sqrt(N))."""
     r = _rng(seed, "C")

@@ -19,6 +19,17 @@ def P():
     return mod
 
 
+@pytest.fixture(params=["generic", "auto"])
+def path(request, monkeypatch):
+    """generic: SIMT logits + argmax kernel; auto: tcgen05 logits with the argmax (and the
+    P gather) fused into the TMEM epilogue wherever the shape allows it."""
+    if request.param == "generic":
+        monkeypatch.setenv("PDSSM_PATH", "generic")
+    else:
+        monkeypatch.delenv("PDSSM_PATH", raising=False)
+    return request.param
+
+
 @pytest.mark.parametrize("H,K,N", [(1, 4, 8), (2, 3, 5), (8, 32, 128), (2, 5, 1000), (1, 1, 1)])
 def test_sparsify_bit_exact(P, H, K, N):
     M = synth.dictionary(H, K, N, seed=N)
@@ -41,13 +52,15 @@ def test_sparsify_nan_reported(P):
 @pytest.mark.parametrize("shape", [(1, 64, 16, 1, 4, 8), (2, 33, 40, 3, 7, 5), (2, 130, 1024, 8, 32, 128),
                                    (1, 70, 2048, 4, 48, 64)])
 @pytest.mark.parametrize("mode", ["integer", "tie_dense"])
-def test_select_integer_bit_exact(P, shape, mode):
+@pytest.mark.parametrize("bf16", [False, True])
+def test_select_integer_bit_exact(P, path, shape, mode, bf16):
     B, L, d_in, H, K, N = shape
     kw = {mode: True}
     x = synth.tokens_x(B, L, d_in, seed=L, **kw)
     S = synth.selector(H, K, d_in, seed=L, **kw)
     di = synth.random_maps(H, K, N, seed=L)
-    k, Pm, lg = P.select(torch.from_numpy(x).cuda(), torch.from_numpy(S).cuda(),
+    dt = torch.bfloat16 if bf16 else torch.float32          # |values| <= 8: exact in bf16 / tf32 too
+    k, Pm, lg = P.select(torch.from_numpy(x).cuda().to(dt), torch.from_numpy(S).cuda().to(dt),
                          torch.from_numpy(di.astype(np.int16)).cuda(), want_P=True, want_logits=True)
     k_ref, lg_ref = O.select(x, S)
     assert np.array_equal(lg.cpu().numpy().astype(np.float64), lg_ref)     # exact integers
@@ -56,7 +69,7 @@ def test_select_integer_bit_exact(P, shape, mode):
 
 
 @pytest.mark.parametrize("bf16", [False, True])
-def test_select_float_margin_rule(P, bf16):
+def test_select_float_margin_rule(P, path, bf16):
     B, L, d_in, H, K = 2, 300, 1024, 8, 32
     x = synth.tokens_x(B, L, d_in, seed=5)
     S = synth.selector(H, K, d_in, seed=5)
@@ -77,7 +90,10 @@ def test_select_float_margin_rule(P, bf16):
     absum = np.einsum("hkd,btd->bhtk", np.abs(S.astype(np.float64)), np.abs(x.astype(np.float64)))
     k1 = np.argsort(lg_ref, axis=-1)[..., -1:]
     k2 = np.argsort(lg_ref, axis=-1)[..., -2:-1]
-    gamma = (d_in * 2.0 ** -24) * (np.take_along_axis(absum, k1, -1)[..., 0] + np.take_along_axis(absum, k2, -1)[..., 0])
+    # u_in: 0 for bf16 inputs (products exact) and for the fp32 SIMT path; 2^-20 bounds the
+    # 3xTF32 split of the tensor-core fp32 path (dropped lo*lo term + lo truncation)
+    u_in = 2.0 ** -20 if (path == "auto" and not bf16) else 0.0
+    gamma = (u_in + d_in * 2.0 ** -24) * (np.take_along_axis(absum, k1, -1)[..., 0] + np.take_along_axis(absum, k2, -1)[..., 0])
     sure = gap > gamma
     assert np.array_equal(k[sure], k_ref[sure])
     # near-ties (gap <= gamma): the GPU's pick must be within gamma of the exact maximum
