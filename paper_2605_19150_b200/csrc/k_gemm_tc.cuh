@@ -51,6 +51,13 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(su32(bar))
         : "memory");
 }
+__device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+            su32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
+        : "memory");
+}
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -128,7 +135,8 @@ struct EpiSelect {
     int64_t M;                 // B * L
     int L, H, K, N;
     uint32_t flags;
-    __device__ void operator()(uint32_t taddr, int64_t m, int n0, int bn) const {
+    __device__ void operator()(uint32_t taddr, int64_t m, int n0, int bn, int z) const {
+        (void)z;
         const bool valid = m < M;
         const int64_t b = valid ? m / L : 0, t = valid ? m - b * L : 0;
         const int h0 = n0 / K;
@@ -177,7 +185,8 @@ struct EpiProject {
     int64_t M;
     int L, H, cN;
     int64_t NN;   // H * cN
-    __device__ void operator()(uint32_t taddr, int64_t m, int n0, int bn) const {
+    __device__ void operator()(uint32_t taddr, int64_t m, int n0, int bn, int z) const {
+        (void)z;
         const bool valid = m < M;
         const int64_t b = valid ? m / L : 0, t = valid ? m - b * L : 0;
         for (int c0 = 0; c0 < bn; c0 += 16) {
@@ -205,6 +214,79 @@ struct EpiProject {
     }
 };
 
+// store 16 consecutive fp32 values as TO (16-byte vector stores; dst 16-byte aligned)
+template <typename TO>
+__device__ __forceinline__ void st16(TO* dst, const float (&v)[16]) {
+    if constexpr (std::is_same<TO, float>::value) {
+#pragma unroll
+        for (int i = 0; i < 16; i += 4)
+            *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+    } else {
+        uint32_t p[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const __nv_bfloat162 q = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+            p[i] = *reinterpret_cast<const uint32_t*>(&q);
+        }
+        reinterpret_cast<uint4*>(dst)[0] = make_uint4(p[0], p[1], p[2], p[3]);
+        reinterpret_cast<uint4*>(dst)[1] = make_uint4(p[4], p[5], p[6], p[7]);
+    }
+}
+
+// a8 readout y_t = Re(C_h h_t) = C_re h_re - C_im h_im (Eq. 1): tile rows are
+// the steps t of one sequence z = b*H + h, columns the readout rows p -> y[b][t][h][p]
+template <typename TO>
+struct EpiReadout {
+    TO* y;
+    int L, H, P;
+    __device__ void operator()(uint32_t taddr, int64_t t, int n0, int bn, int z) const {
+        const bool valid = t < L;
+        const int b = z / H, h = z - (z / H) * H;
+        for (int c0 = 0; c0 < bn; c0 += 16) {
+            float v[16];
+            tmem_ld16(taddr + (uint32_t)c0, v);
+            const int p = n0 + c0;
+            if (valid && p < P) st16<TO>(y + (((size_t)b * L + t) * H + h) * P + p, v);
+        }
+    }
+};
+
+// readout adjoint (bwd with dy): e_t = dh_t + conj(C)^T dy_t per head (reading R13), rows
+// m = b*L + t, columns w = (c, n) of head z -> e[b][z][t][w] (fp32 scratch of the scan)
+template <typename TI>
+struct EpiAdjoint {
+    float* e;
+    const TI* dh;   // or null
+    int64_t M;
+    int L, H, cN;
+    __device__ void operator()(uint32_t taddr, int64_t m, int n0, int bn, int z) const {
+        const bool valid = m < M;
+        const int64_t b = valid ? m / L : 0, t = valid ? m - b * L : 0;
+        for (int c0 = 0; c0 < bn; c0 += 16) {
+            float v[16];
+            tmem_ld16(taddr + (uint32_t)c0, v);
+            const int w = n0 + c0;
+            if (!valid || w >= cN) continue;
+            const size_t off = (((size_t)b * H + z) * L + t) * cN + w;
+            if (dh) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] += ldact(dh + off + i);
+            }
+            st16<float>(e + off, v);
+        }
+    }
+};
+
+// How a CTA finds its A rows and B rows (the operand maps are 2-D or 3-D):
+//  mode 0: A rows m0 = blockIdx.x*BM of a 2-D map; B rows n0.
+//  mode 1: A is 3-D (K, rows, Z): z = blockIdx.x / tiles, m0 = (blockIdx.x % tiles)*BM;
+//          B rows (z % zmod)*brows + n0 (per-head weights stacked in one 2-D map).
+//  mode 2: A is 3-D (K, Z, rows) with box (EK, 1, BM): z = blockIdx.z, m0 = blockIdx.x*BM;
+//          B rows z*brows + n0.
+struct TileMap {
+    int mode, tiles, zmod, brows;
+};
+
 // --------------------------------------------------------------------------- kernel
 // SPLIT (fp32 operands): 3xTF32.  Each landed fp32 slab is split in shared memory by the
 // epilogue warps (idle during the main loop) into hi = tf32_rna(a) (in place) and
@@ -226,7 +308,8 @@ struct Smem {
 
 template <typename T, int STAGES, bool SPLIT, class Epi>
 __global__ void __launch_bounds__(THREADS, 1)
-    k_gemm_tc(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, int nk, int bn, Epi epi) {
+    k_gemm_tc(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, int nk, int bn, TileMap tm,
+              Epi epi) {
     using SM = Smem<T, STAGES, SPLIT>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -260,8 +343,22 @@ __global__ void __launch_bounds__(THREADS, 1)
     __syncthreads();
     fence_after();
     const uint32_t tmem = *tslot;
-    const int64_t m0 = (int64_t)blockIdx.x * BM;
     const int n0 = blockIdx.y * bn;
+    int64_t m0;
+    int z, brow;
+    if (tm.mode == 1) {
+        z = blockIdx.x / tm.tiles;
+        m0 = (int64_t)(blockIdx.x - z * tm.tiles) * BM;
+        brow = (z % tm.zmod) * tm.brows + n0;
+    } else if (tm.mode == 2) {
+        z = blockIdx.z;
+        m0 = (int64_t)blockIdx.x * BM;
+        brow = z * tm.brows + n0;
+    } else {
+        z = 0;
+        m0 = (int64_t)blockIdx.x * BM;
+        brow = n0;
+    }
     constexpr int EK = ROWB / (int)sizeof(T);   // elements of K per slab row
     if (warp == 0) {
         if (lane == 0) {
@@ -270,8 +367,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const int s = kb % STAGES;
                 if (kb >= STAGES) mbar_wait(empty + s, (uint32_t)((kb / STAGES) + 1) & 1u);
                 mbar_expect_tx(full + s, bytes);
-                tma_2d(hi(s), &mA, kb * EK, (int)m0, full + s);
-                tma_2d(hi(s) + (size_t)BM * ROWB, &mB, kb * EK, n0, full + s);
+                if (tm.mode == 1) tma_3d(hi(s), &mA, kb * EK, (int)m0, z, full + s);
+                else if (tm.mode == 2) tma_3d(hi(s), &mA, kb * EK, z, (int)m0, full + s);
+                else tma_2d(hi(s), &mA, kb * EK, (int)m0, full + s);
+                tma_2d(hi(s) + (size_t)BM * ROWB, &mB, kb * EK, brow, full + s);
             }
         }
     } else if (warp == 1) {
@@ -325,7 +424,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_wait(tfull, 0);
         fence_after();
         const int q = warp - 4;
-        epi(tmem + ((uint32_t)(32 * q) << 16), m0 + 32 * q + lane, n0, bn);
+        epi(tmem + ((uint32_t)(32 * q) << 16), m0 + 32 * q + lane, n0, bn, z);
     }
     fence_before();
     __syncthreads();

@@ -95,6 +95,8 @@ size_t cs_pi_bytes(const Geo& g) { return align256((size_t)g.S * g.C * g.N * 2);
 size_t cs_f_bytes(const Geo& g) { return align256((size_t)g.S * g.C * g.nc * g.N * 4); }
 size_t chunk_state_bytes_g(const Geo& g) { return cs_pi_bytes(g) + 3 * cs_f_bytes(g); }
 size_t seq_f_bytes(const Geo& g) { return align256((size_t)g.S * g.L * g.nc * g.N * 4); }
+// readout weights staged in act dtype (Cp or CT), H*P*c*N elements
+size_t readout_w_bytes(const Geo& g) { return g.P > 0 ? align256((size_t)g.H * g.P * g.nc * g.N * g.act) : 0; }
 size_t seq_act_bytes(const Geo& g) { return align256((size_t)g.S * g.L * g.nc * g.N * g.act); }
 int npad8(int64_t N) { return (int)((N + 7) & ~7); }
 size_t summary_block_bytes(const Geo& g) { return (size_t)npad8(g.N) * 2 + (size_t)2 * g.nc * g.N * 4; }
@@ -114,14 +116,14 @@ size_t ws_bytes_g(const Geo& g, int op) {
         case PDSSM_OP_SELECT:
             return align256((size_t)g.S * g.L * g.K * 4);
         case PDSSM_OP_FWD:
-            return plan_bytes(g) + (g.P > 0 ? seq_act_bytes(g) : 0) + fused_plan_bytes(g.H, g.K, g.N) +
-                   fused_ctrl_bytes(g.S, g.C, g.H);
+            return plan_bytes(g) + (g.P > 0 ? seq_act_bytes(g) + readout_w_bytes(g) : 0) +
+                   fused_plan_bytes(g.H, g.K, g.N) + fused_ctrl_bytes(g.S, g.C, g.H);
         case PDSSM_OP_BWD:
-            return 2 * cs_f_bytes(g) + (g.P > 0 ? seq_f_bytes(g) : 0) +
+            return 2 * cs_f_bytes(g) + (g.P > 0 ? seq_f_bytes(g) + readout_w_bytes(g) : 0) +
                    (g.diag_mode == PDSSM_DIAG_PER_DICT ? seq_f_bytes(g) : 0) + fused_ctrl_bytes(g.S, g.C, g.H);
         case PDSSM_OP_SEGMENT: {
             size_t fwd = plan_bytes(g) + chunk_state_bytes_g(g);
-            size_t bwd = 2 * cs_f_bytes(g) + (g.P > 0 ? seq_f_bytes(g) : 0);
+            size_t bwd = 2 * cs_f_bytes(g) + (g.P > 0 ? seq_f_bytes(g) + readout_w_bytes(g) : 0);
             return fwd > bwd ? fwd : bwd;
         }
         default:
@@ -255,6 +257,20 @@ bool make_kmajor_map(CUtensorMap* m, const void* ptr, size_t esz, int64_t kdim, 
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 3-D operand: dims {K, d1, d2} (elements), byte strides of d1 and d2, box {128 B of K, b1, b2}
+bool make_map3(CUtensorMap* m, const void* ptr, size_t esz, const int64_t (&dims)[3], const int64_t (&strides)[2],
+               int b1, int b2) {
+    EncodeTiledFn f = encode_tiled();
+    if (!f) return false;
+    cuuint64_t d[3] = {(cuuint64_t)dims[0], (cuuint64_t)dims[1], (cuuint64_t)dims[2]};
+    cuuint64_t st[2] = {(cuuint64_t)strides[0], (cuuint64_t)strides[1]};
+    cuuint32_t box[3] = {(cuuint32_t)(tc::ROWB / esz), (cuuint32_t)b1, (cuuint32_t)b2};
+    cuuint32_t es[3] = {1, 1, 1};
+    return f(m, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(ptr),
+             d, st, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int64_t gcd64(int64_t a, int64_t b) { return b ? gcd64(b, a % b) : a; }
 
 // operands usable by TMA: 16-byte aligned base and row pitch
@@ -271,25 +287,91 @@ template <typename T>
 constexpr int tc_stages() { return std::is_same<T, float>::value ? 2 : 4; }
 
 template <typename T, class Epi>
-pdssm_status launch_tc(const Geo& g, const void* A, int64_t rows_a, const void* Bm, int64_t rows_b, int bn, Epi epi,
-                       cudaStream_t st, const char* what) {
+pdssm_status launch_tc_maps(const CUtensorMap& mA, const CUtensorMap& mB, int64_t kdim, int bn, tc::TileMap tm,
+                            dim3 grid, Epi epi, cudaStream_t st, const char* what) {
     constexpr bool SPLIT = std::is_same<T, float>::value;
     constexpr int STAGES = tc_stages<T>();
     using SM = tc::Smem<T, STAGES, SPLIT>;
-    CUtensorMap mA, mB;
-    if (!make_kmajor_map(&mA, A, sizeof(T), g.d_in, rows_a, tc::BM) ||
-        !make_kmajor_map(&mB, Bm, sizeof(T), g.d_in, rows_b, bn))
-        return fail(PDSSM_ERR_CUDA, "%s: cuTensorMapEncodeTiled failed", what);
     const size_t smem = SM::bytes(256);   // sized for the largest tile: one attribute per instantiation
     auto kern = tc::k_gemm_tc<T, STAGES, SPLIT, Epi>;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
     if (attr_err != cudaSuccess) return fail(PDSSM_ERR_CUDA, "%s: cudaFuncSetAttribute: %s", what, cudaGetErrorString(attr_err));
-    const int nk = (int)ceil_div(g.d_in * (int64_t)sizeof(T), tc::ROWB);
-    dim3 grid((unsigned)ceil_div(rows_a, tc::BM), (unsigned)ceil_div(rows_b, bn));
-    kern<<<grid, tc::THREADS, SM::bytes(bn), st>>>(mA, mB, nk, bn, epi);
+    const int nk = (int)ceil_div(kdim * (int64_t)sizeof(T), tc::ROWB);
+    kern<<<grid, tc::THREADS, SM::bytes(bn), st>>>(mA, mB, nk, bn, tm, epi);
     return cuda_check(what);
+}
+
+// plain 2-D case: A [rows_a][d_in], B [rows_b][d_in]
+template <typename T, class Epi>
+pdssm_status launch_tc(const Geo& g, const void* A, int64_t rows_a, const void* Bm, int64_t rows_b, int bn, Epi epi,
+                       cudaStream_t st, const char* what) {
+    CUtensorMap mA, mB;
+    if (!make_kmajor_map(&mA, A, sizeof(T), g.d_in, rows_a, tc::BM) ||
+        !make_kmajor_map(&mB, Bm, sizeof(T), g.d_in, rows_b, bn))
+        return fail(PDSSM_ERR_CUDA, "%s: cuTensorMapEncodeTiled failed", what);
+    dim3 grid((unsigned)ceil_div(rows_a, tc::BM), (unsigned)ceil_div(rows_b, bn));
+    return launch_tc_maps<T>(mA, mB, g.d_in, bn, tc::TileMap{0, 1, 1, 0}, grid, epi, st, what);
+}
+
+// readout weights, act dtype: Cp[h][p][(c,n)] (y = Cp . h) and CT[h][(c,n)][p] (e = CT . dy),
+// both carrying the sign of Re(C h) = C_re h_re - C_im h_im
+template <typename T>
+__global__ void k_readout_weights(const float* __restrict__ C, T* __restrict__ Cp, T* __restrict__ CT, int H, int nc,
+                                  int P, int N) {
+    const int64_t total = (int64_t)H * nc * P * N;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int n = (int)(i % N);
+        const int p = (int)((i / N) % P);
+        const int c = (int)((i / ((int64_t)N * P)) % nc);
+        const int h = (int)(i / ((int64_t)N * P * nc));
+        const float v = c == 0 ? C[i] : -C[i];
+        const int cN = nc * N;
+        if (Cp) stact(Cp + ((size_t)h * P + p) * cN + c * N + n, v);
+        if (CT) stact(CT + ((size_t)h * cN + c * N + n) * P + p, v);
+    }
+}
+
+// tensor-core readout applicability: TMA row pitches, 16-column output groups
+bool tc_readout_ok(const Geo& g, std::initializer_list<const void*> ptrs) {
+    if (path_generic_forced() || !encode_tiled()) return false;
+    if ((g.nc * g.N * (int64_t)g.act) % 16 != 0 || g.P % 16 != 0 || (g.nc * g.N) % 16 != 0) return false;
+    if ((g.P * (int64_t)g.act) % 16 != 0) return false;
+    for (const void* p : ptrs)
+        if (misaligned(p, 16)) return false;
+    return true;
+}
+
+// y[b][t][h][p] = sum_w Cp[h][p][w] h[b][h][t][w]  (A: 3-D (cN, L, S) map, z = sequence)
+template <typename T>
+pdssm_status readout_tc(const Geo& g, const T* hseq, const T* Cp, T* y, cudaStream_t st) {
+    const int64_t cN = g.nc * g.N;
+    const int bn = (int)(g.P < 256 ? g.P : 256);
+    CUtensorMap mA, mB;
+    const int64_t da[3] = {cN, g.L, g.S};
+    const int64_t sa[2] = {cN * (int64_t)sizeof(T), g.L * cN * (int64_t)sizeof(T)};
+    if (!make_map3(&mA, hseq, sizeof(T), da, sa, tc::BM, 1) || !make_kmajor_map(&mB, Cp, sizeof(T), cN, g.H * g.P, bn))
+        return fail(PDSSM_ERR_CUDA, "readout_tc: cuTensorMapEncodeTiled failed");
+    const int tiles = (int)ceil_div(g.L, tc::BM);
+    dim3 grid((unsigned)(tiles * g.S), (unsigned)ceil_div(g.P, bn));
+    return launch_tc_maps<T>(mA, mB, cN, bn, tc::TileMap{1, tiles, (int)g.H, (int)g.P}, grid,
+                             tc::EpiReadout<T>{y, (int)g.L, (int)g.H, (int)g.P}, st, "readout_tc");
+}
+
+// e[b][h][t][w] = dh + sum_p CT[h][w][p] dy[b][t][h][p]  (A: 3-D (P, H, B*L) map, z = head)
+template <typename T>
+pdssm_status adjoint_tc(const Geo& g, const T* dy, const T* CT, const T* dh, float* e, cudaStream_t st) {
+    const int64_t cN = g.nc * g.N;
+    const int bn = (int)(cN < 256 ? cN : 256);
+    CUtensorMap mA, mB;
+    const int64_t da[3] = {g.P, g.H, g.B * g.L};
+    const int64_t sa[2] = {g.P * (int64_t)sizeof(T), g.H * g.P * (int64_t)sizeof(T)};
+    if (!make_map3(&mA, dy, sizeof(T), da, sa, 1, tc::BM) || !make_kmajor_map(&mB, CT, sizeof(T), g.P, g.H * cN, bn))
+        return fail(PDSSM_ERR_CUDA, "adjoint_tc: cuTensorMapEncodeTiled failed");
+    dim3 grid((unsigned)ceil_div(g.B * g.L, tc::BM), (unsigned)ceil_div(cN, bn), (unsigned)g.H);
+    return launch_tc_maps<T>(mA, mB, g.P, bn, tc::TileMap{2, 1, 1, (int)cN}, grid,
+                             tc::EpiAdjoint<T>{e, dh, g.B * g.L, (int)g.L, (int)g.H, (int)cN}, st, "adjoint_tc");
 }
 
 // select tile width: whole heads, a multiple of lcm(K, 16), <= 256 (0: not possible)
@@ -299,6 +381,24 @@ int select_bn(const Geo& g) {
     const int64_t full = (256 / l) * l;
     const int64_t need = ceil_div(g.H * g.K, l) * l;
     return (int)(need < full ? need : full);
+}
+
+// direct state gradient e = dh + conj(C)^T dy (bwd with a readout): tensor cores when the
+// shapes allow it (CT staged in wbuf), else the SIMT kernel
+template <typename T, int NC>
+pdssm_status prepare_e(const Geo& g, const void* dh, const void* dy, const float* C, float* e, void* wbuf,
+                       cudaStream_t st) {
+    if (tc_readout_ok(g, {dy, dh, e, wbuf})) {
+        T* CT = static_cast<T*>(wbuf);
+        k_readout_weights<T><<<(unsigned)ceil_div(g.H * g.nc * g.P * g.N, 256), 256, 0, st>>>(C, nullptr, CT, (int)g.H,
+                                                                                              (int)g.nc, (int)g.P, (int)g.N);
+        pdssm_status r = cuda_check("readout_weights");
+        if (r) return r;
+        return adjoint_tc<T>(g, static_cast<const T*>(dy), CT, static_cast<const T*>(dh), e, st);
+    }
+    k_bwd_prepare_e<T, NC><<<(unsigned)(g.S * g.L), 128, (size_t)g.P * 4, st>>>(
+        static_cast<const T*>(dh), static_cast<const T*>(dy), C, e, (int)g.H, (int)g.L, (int)g.N, (int)g.P);
+    return cuda_check("bwd_prepare_e");
 }
 
 template <typename F>
@@ -594,6 +694,7 @@ pdssm_status pdssm_scan_fwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
     uint16_t* pstart = bump.take<uint16_t>((size_t)g.H * g.K * (g.N + 1) * 2);
     uint16_t* psrc = bump.take<uint16_t>((size_t)g.H * g.K * g.N * 2);
     void* hscratch = g.P > 0 ? bump.take<char>(seq_act_bytes(g)) : nullptr;
+    void* wbuf = g.P > 0 ? bump.take<char>(readout_w_bytes(g)) : nullptr;
     uint8_t* frec = bump.take<uint8_t>(fused_rec_bytes(g.H, g.K));
     uint32_t* fhdr = bump.take<uint32_t>(fused_hdr_bytes(g.H, g.K));
     uint16_t* fpcl = bump.take<uint16_t>(fused_pclamp_bytes(g.H, g.K, g.N));
@@ -623,6 +724,14 @@ pdssm_status pdssm_scan_fwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
     if (y_opt) {
         r = with_act(g.dtype, [&](auto tv) {
             using T = decltype(tv);
+            if (tc_readout_ok(g, {hout, y_opt, wbuf})) {
+                T* Cp = static_cast<T*>(wbuf);
+                k_readout_weights<T><<<(unsigned)ceil_div(g.H * g.nc * g.P * g.N, 256), 256, 0, st>>>(
+                    C_opt, Cp, nullptr, (int)g.H, (int)g.nc, (int)g.P, (int)g.N);
+                pdssm_status rr = cuda_check("readout_weights");
+                if (rr) return rr;
+                return readout_tc<T>(g, static_cast<const T*>(hout), Cp, static_cast<T*>(y_opt), st);
+            }
             return with_nc(g.nc, [&](auto ncv) {
                 constexpr int NC = decltype(ncv)::value;
                 k_readout<T, NC><<<(unsigned)(g.S * g.L), 128, (size_t)NC * g.N * 4, st>>>(
@@ -659,6 +768,7 @@ pdssm_status pdssm_scan_bwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
     float* betap = bump.take<float>(cs_f_bytes(g));
     float* mu = bump.take<float>(cs_f_bytes(g));
     float* ebuf = g.P > 0 ? bump.take<float>(seq_f_bytes(g)) : nullptr;
+    void* wbuf = g.P > 0 ? bump.take<char>(readout_w_bytes(g)) : nullptr;
     float* dDbuf = g.diag_mode == PDSSM_DIAG_PER_DICT ? bump.take<float>(seq_f_bytes(g)) : nullptr;
     uint32_t* ctrl = bump.take<uint32_t>(fused_ctrl_bytes(g.S, g.C, g.H));
     ChunkStateView cs = cs_view(g, const_cast<void*>(chunk_state));
@@ -675,10 +785,7 @@ pdssm_status pdssm_scan_bwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
                 using T = decltype(tv);
                 return with_nc(g.nc, [&](auto ncv) {
                     constexpr int NC = decltype(ncv)::value;
-                    k_bwd_prepare_e<T, NC><<<(unsigned)(g.S * g.L), 128, (size_t)g.P * 4, st>>>(
-                        static_cast<const T*>(dh_opt), static_cast<const T*>(dy_opt), C_opt, ebuf, (int)g.H, (int)g.L,
-                        (int)g.N, (int)g.P);
-                    return cuda_check("bwd_prepare_e");
+                    return prepare_e<T, NC>(g, dh_opt, dy_opt, C_opt, ebuf, wbuf, st);
                 });
             });
             if (r) return r;
@@ -742,10 +849,7 @@ pdssm_status pdssm_scan_bwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
                     return PDSSM_OK;
                 };
                 if (dy_opt) {
-                    k_bwd_prepare_e<T, NC><<<(unsigned)(g.S * g.L), 128, (size_t)g.P * 4, st>>>(
-                        static_cast<const T*>(dh_opt), static_cast<const T*>(dy_opt), C_opt, ebuf, (int)g.H, (int)g.L,
-                        (int)g.N, (int)g.P);
-                    pdssm_status rr = cuda_check("bwd_prepare_e");
+                    pdssm_status rr = prepare_e<T, NC>(g, dh_opt, dy_opt, C_opt, ebuf, wbuf, st);
                     if (rr) return rr;
                     return run(float{});
                 }
@@ -822,6 +926,7 @@ pdssm_status pdssm_segment_summary_bwd(const uint8_t* kstar, const uint16_t* dic
     float* betap = bump.take<float>(cs_f_bytes(g));
     float* mu = bump.take<float>(cs_f_bytes(g));
     float* ebuf = g.P > 0 ? bump.take<float>(seq_f_bytes(g)) : nullptr;
+    void* wbuf = g.P > 0 ? bump.take<char>(readout_w_bytes(g)) : nullptr;
     ChunkStateView cs = cs_view(g, const_cast<void*>(chunk_state));
     const int thr = threads_for(g.N);
     const unsigned items = (unsigned)(g.S * g.C);
@@ -847,10 +952,7 @@ pdssm_status pdssm_segment_summary_bwd(const uint8_t* kstar, const uint16_t* dic
                     return cuda_check("bwd_phaseB");
                 };
                 if (dy_opt) {
-                    k_bwd_prepare_e<T, NC><<<(unsigned)(g.S * g.L), 128, (size_t)g.P * 4, st>>>(
-                        static_cast<const T*>(dh_opt), static_cast<const T*>(dy_opt), C_opt, ebuf, (int)g.H, (int)g.L,
-                        (int)g.N, (int)g.P);
-                    pdssm_status rr = cuda_check("bwd_prepare_e");
+                    pdssm_status rr = prepare_e<T, NC>(g, dh_opt, dy_opt, C_opt, ebuf, wbuf, st);
                     if (rr) return rr;
                     return run(float{});
                 }
