@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--tau", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-layer", action="store_true")
     ap.add_argument("--seed", type=int, default=2000)
     return ap.parse_args()
 
@@ -54,6 +55,38 @@ def peaks():
             j = json.load(f)
         return float(j["hbm_gbs"]), "measured"
     return 6650.0, "fallback"
+
+
+def peak_tflops(dtype):
+    """Dense tensor peak for the layer GEMMs: measured cuBLAS bf16 burst; fp32 runs use the
+    3xTF32 split (3 tf32 MMAs per product, tf32 = 1/2 bf16 nominal) -> bf16/6 useful."""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    bf = 1645.9
+    if os.path.exists(p):
+        with open(p) as f:
+            bf = float(json.load(f).get("bf16_tflops", bf))
+    return bf if dtype == "bf16" else bf / 6.0
+
+
+def traffic_of(kernel):
+    """dram read+write bytes per launch of `kernel` from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "traffic_latest.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        return json.load(f).get(kernel)
+
+
+def count_launches(fn):
+    """Kernels one call of fn launches (CUPTI via torch.profiler), counted outside the timed region."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        fn()
+        torch.cuda.synchronize()
+    names = [e.name for e in prof.events() if e.device_type.name == "CUDA" and "pdssm" in e.name]
+    return len(names), sorted(set(n.split("(")[0][:80] for n in names))
 
 
 def algo_bytes_per_seq_step(N, c, p):
@@ -149,6 +182,49 @@ def run_reference(a):
     print(json.dumps(line), flush=True)
 
 
+def layer_kernels(P, torch, dev, adt, dtype, B, L, H, N, K, c, stream):
+    """Time select (a2/a3), projection (a5) and readout (a8) at the config-2 layer shape
+    (d_in = d = H*N, readout rows P = d/H) with CUDA events on the launching stream."""
+    d_in, Pp = H * N, N
+    g = torch.Generator(device=dev).manual_seed(7)
+    x = torch.randn((B, L, d_in), device=dev, generator=g).to(adt)
+    S = ((torch.rand((H, K, d_in), device=dev, generator=g) * 2 - 1) / d_in ** 0.5).to(adt)
+    Bw = ((torch.rand((H, c, N, d_in), device=dev, generator=g) * 2 - 1) / d_in ** 0.5).to(adt)
+    Cw = (torch.rand((H, c, Pp, N), device=dev, generator=g) * 2 - 1) / N ** 0.5
+    bout = torch.empty((B, H, L, c, N), device=dev, dtype=adt)
+    y = torch.empty((B, L, H, Pp), device=dev, dtype=adt)
+    k_sel = torch.empty((B, H, L), device=dev, dtype=torch.uint8)
+    dims = P.make_dims(B, H, L, N, 1, c=c, dtype=P.BF16 if dtype == "bf16" else P.F32, p_out=Pp)
+    wsr = torch.empty(max(P.workspace_bytes(dims, P.OP_READOUT), 256), dtype=torch.uint8, device=dev)
+
+    def t(fn, n=10):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(n):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / n * 1e3   # us
+
+    ts = t(lambda: P.select(x, S))
+    tp = t(lambda: P.project(x, Bw, out=bout))
+    tr = t(lambda: P.readout(bout, Cw, out=y, ws=wsr))
+    peak = peak_tflops(dtype)
+    f_sel = 2.0 * B * L * H * K * d_in
+    f_prj = 2.0 * B * L * H * c * N * d_in
+    f_rd = 2.0 * B * L * H * c * N * Pp
+    out = {"dtype": dtype, "tensor_peak_tflops": peak,
+           "tensor_peak_kind": "measured bf16 burst" + (" / 6 (3xTF32)" if dtype != "bf16" else ""),
+           "shape": {"d_in": d_in, "P": Pp, "K": K}}
+    for name, us, fl in (("select", ts, f_sel), ("project", tp, f_prj), ("readout", tr, f_rd)):
+        tf = fl / (us * 1e-6) / 1e12
+        out[name] = {"us": us, "tflops": tf, "frac": tf / peak}
+    return out
+
+
 def main():
     a = parse()
     if a.impl == "reference":
@@ -199,6 +275,10 @@ def main():
     for _ in range(max(a.warmup, 3)):
         step_bwd(step_fwd())
     torch.cuda.synchronize()
+    try:
+        launches_per_step, kernel_names = count_launches(lambda: step_bwd(step_fwd()))
+    except Exception as ex:   # profiler unavailable: the fused path's documented count
+        launches_per_step, kernel_names = 4, [f"profiler failed: {ex}"[:80]]
 
     # ---- timed region: K steps, per-call CUDA events on the launching stream
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -291,7 +371,10 @@ def main():
                "sample": f"{reps} x one (b,h) sequence of {Lh} steps (N={N}, complex={c == 2}), fwd O5 + bwd O8, "
                          "float64 NumPy, single thread; tokens = steps/H"}
 
-    launches_per_step = 7   # fwd: plan, A, B, C ; bwd: A', B', C'
+    # ---- layer-level kernels of the path (a2/a3 select, a5 projection, a8 readout), timed alone
+    layer = None
+    if not a.no_layer:
+        layer = layer_kernels(P, torch, dev, adt, a.dtype, B, L, H, N, K, c, stream)
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
                 "ms_per_step": 1e3 * elapsed / a.steps, "higher_is_better": True, "scaling": "weak",
@@ -301,11 +384,14 @@ def main():
                            "tau": int(f["tau"]), "parallelism": f"dp{world} (batch x head shards, no collective)",
                            "l2": "inputs larger than L2 (>=1.3 GB per step), no flush"},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                             "frac": achieved / peak, "traffic": None, "kernel": dominant,
-                             "peak_kind": peak_kind},
+                             "frac": achieved / peak, "traffic": traffic_of(dominant), "kernel": dominant,
+                             "algo_bytes_per_launch": dom_bytes, "peak_kind": peak_kind,
+                             "traffic_source": "profiles/traffic_latest.json (ncu --set full, dram read+write per launch)"},
                 "step_hbm": {"achieved_gbs": step_gbs, "frac": step_gbs / peak, "fwd_ms": fwd_ms, "bwd_ms": bwd_ms,
                              "algo_bytes_fwd": fwd_bytes, "algo_bytes_bwd": bwd_bytes},
-                "clocks": clocks, "e2e": e2e, "gpu_launches": launches_per_step * a.steps, "cpu_baseline": cpu}
+                "clocks": clocks, "e2e": e2e, "gpu_launches": launches_per_step * a.steps,
+                "launches_per_step": {"count": launches_per_step, "kernels": kernel_names},
+                "layer_kernels": layer, "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -80,7 +80,7 @@ enum {
     PDSSM_EXPORT_MAPS = 8u     /* pdssm_scan_fwd also writes maps_opt                 */
 };
 
-enum { PDSSM_OP_SELECT = 0, PDSSM_OP_FWD = 1, PDSSM_OP_BWD = 2, PDSSM_OP_SEGMENT = 3 };
+enum { PDSSM_OP_SELECT = 0, PDSSM_OP_FWD = 1, PDSSM_OP_BWD = 2, PDSSM_OP_SEGMENT = 3, PDSSM_OP_READOUT = 4 };
 
 /* Problem statement (north_star: x, selector S, dictionary {P_k, D_k}, B, C,
  * L, N, K, batch, heads).  Plain C struct; all fields are read-only inputs. */
@@ -166,6 +166,20 @@ pdssm_status pdssm_select(const void* x, const void* S, const uint16_t* dict_idx
  * ------------------------------------------------------------------------- */
 pdssm_status pdssm_project(const void* x, const void* Bw, void* b_out, const pdssm_dims* dims,
                            pdssm_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * a8 readout, standalone (the same kernel pdssm_scan_fwd runs for y_opt):
+ * y_t = Re(C_h h_t) = C_re h_re - C_im h_im (Eq. 1 y_t = C x_t with psi = Re)
+ *   h   act [B][H][L][c][N]   states (e.g. h_out of pdssm_scan_fwd)
+ *   C   f32 [H][c][P][N]      readout (P = dims.p_out >= 1)
+ *   y   act [B][L][H][P]      out
+ *   ws  >= pdssm_workspace_bytes(dims, PDSSM_OP_READOUT): C staged in act dtype
+ * Path: tcgen05 GEMM per head (bf16: kind::f16; f32: 3xTF32) when P % 16 == 0, c*N % 16
+ * == 0, the row pitches are 16-byte multiples and h, y, ws are 16-byte aligned;
+ * otherwise a SIMT kernel.
+ * ------------------------------------------------------------------------- */
+pdssm_status pdssm_readout(const void* h, const float* C, void* y, const pdssm_dims* dims,
+                           void* ws, size_t ws_bytes, pdssm_stream_t stream);
 
 /* ---------------------------------------------------------------------------
  * a6-a8: forward chunked scan (Alg. 1; Kernels A/B/C

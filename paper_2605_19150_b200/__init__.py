@@ -30,7 +30,7 @@ if os.environ.get("PDSSM_LIB_VARIANT"):   # tuning experiments: variants/<name>.
 F32, BF16 = 0, 1
 PER_STEP, PER_DICT = 0, 1
 CHECK_FINITE, DETERMINISTIC, EXPORT_MAPS = 1, 2, 8
-OP_SELECT, OP_FWD, OP_BWD, OP_SEGMENT = 0, 1, 2, 3
+OP_SELECT, OP_FWD, OP_BWD, OP_SEGMENT, OP_READOUT = 0, 1, 2, 3, 4
 
 STATUS = {0: "PDSSM_OK", 1: "PDSSM_ERR_NULL", 2: "PDSSM_ERR_SHAPE", 3: "PDSSM_ERR_RANGE",
           4: "PDSSM_ERR_ALIGN", 5: "PDSSM_ERR_DTYPE", 6: "PDSSM_ERR_WORKSPACE",
@@ -68,6 +68,7 @@ def _load():
         "pdssm_sparsify": (ctypes.c_int, [vp, vp, D, vp]),
         "pdssm_select": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, D, vp, sz, vp]),
         "pdssm_project": (ctypes.c_int, [vp, vp, vp, D, vp]),
+        "pdssm_readout": (ctypes.c_int, [vp, vp, vp, D, vp, sz, vp]),
         "pdssm_scan_fwd": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, D, vp, sz, vp]),
         "pdssm_scan_bwd": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, D, vp, sz, vp]),
         "pdssm_segment_summary": (ctypes.c_int, [vp, vp, vp, vp, vp, D, vp, sz, vp]),
@@ -212,6 +213,23 @@ def project(x, Bw, out=None):
     b = out if out is not None else torch.empty((B, H, L, c, N), dtype=x.dtype, device=x.device)
     _check(lib.pdssm_project(_ptr(x), _ptr(Bw), _ptr(b), ctypes.byref(dims), _stream()))
     return b
+
+
+def readout(h, C, out=None, ws=None):
+    """a8: y_t = Re(C_h h_t) (Eq. 1).  h [B][H][L][c][N], C f32 [H][c][P][N]
+    -> y [B][L][H][P] in h's dtype."""
+    torch = _torch()
+    _contig(h, "h"), _contig(C, "C")
+    B, H, L, c, N = h.shape
+    Pp = C.shape[2]
+    dims = make_dims(B, H, L, N, 1, c=c, dtype=_dtype_code(h), p_out=Pp)
+    y = out if out is not None else torch.empty((B, L, H, Pp), dtype=h.dtype, device=h.device)
+    if ws is None:
+        ws, wsb = _workspace(dims, OP_READOUT, h.device)
+    else:
+        wsb = ws.numel()
+    _check(lib.pdssm_readout(_ptr(h), _ptr(C), _ptr(y), ctypes.byref(dims), _ptr(ws), wsb, _stream()))
+    return y
 
 
 def scan_fwd(kstar, dict_idx, diag, bias, h0=None, C=None, tau=0, per_dict=False, want_h=True,

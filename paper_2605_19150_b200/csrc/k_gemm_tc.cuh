@@ -135,11 +135,82 @@ struct EpiSelect {
     int64_t M;                 // B * L
     int L, H, K, N;
     uint32_t flags;
+    // P row copy (16-byte vectors when the rows allow it)
+    __device__ void copy_P(int h, int k, size_t r) const {
+        const uint16_t* src = dict_idx + ((size_t)h * K + k) * N;
+        uint16_t* dst = P + r * N;
+        if ((N & 7) == 0 && ((reinterpret_cast<uintptr_t>(P) | reinterpret_cast<uintptr_t>(dict_idx)) & 15) == 0) {
+            for (int j = 0; j < N; j += 8) *reinterpret_cast<uint4*>(dst + j) = __ldg(reinterpret_cast<const uint4*>(src + j));
+        } else {
+            for (int j = 0; j < N; ++j) dst[j] = __ldg(src + j);
+        }
+    }
     __device__ void operator()(uint32_t taddr, int64_t m, int n0, int bn, int z) const {
         (void)z;
         const bool valid = m < M;
         const int64_t b = valid ? m / L : 0, t = valid ? m - b * L : 0;
         const int h0 = n0 / K;
+        if ((K & 15) == 0) {
+            // whole 16-column groups per head: NaN -> -inf at the leaves, then a
+            // (value desc, index asc) tree per group and a strict '>' across groups --
+            // the same winner as the sequential rule (ties -> smallest k, NaN never wins,
+            // no finite value -> 0)
+            const int nh = bn / K;
+            for (int hh = 0; hh < nh; ++hh) {
+                const int h = h0 + hh;
+                const bool live = valid && h < H;
+                float best = -INFINITY;
+                int arg = 0;
+                for (int q = 0; q < K; q += 16) {
+                    float v[16];
+                    tmem_ld16(taddr + (uint32_t)(hh * K + q), v);
+                    if (live) {
+                        if (flags & PDSSM_CHECK_FINITE) {
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                if (!isfinite(v[i])) report(ERRBIT_NONFINITE);
+                        }
+                        if (logits) {
+                            float* lp = logits + (((size_t)b * H + h) * L + t) * K + q;
+                            if ((reinterpret_cast<uintptr_t>(logits) & 15) == 0) {
+#pragma unroll
+                                for (int i = 0; i < 16; i += 4)
+                                    *reinterpret_cast<float4*>(lp + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                            } else {
+#pragma unroll
+                                for (int i = 0; i < 16; ++i) lp[i] = v[i];
+                            }
+                        }
+                    }
+                    float w[16];
+                    int ix[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        w[i] = isnan(v[i]) ? -INFINITY : v[i];
+                        ix[i] = q + i;
+                    }
+#pragma unroll
+                    for (int st = 1; st < 16; st *= 2)
+#pragma unroll
+                        for (int i = 0; i < 16; i += 2 * st)
+                            if (w[i + st] > w[i]) {   // right operand has the larger index
+                                w[i] = w[i + st];
+                                ix[i] = ix[i + st];
+                            }
+                    if (w[0] > best || q == 0) {
+                        best = w[0];
+                        arg = ix[0];
+                    }
+                }
+                if (live) {
+                    const size_t r = ((size_t)b * H + h) * L + t;
+                    kstar[r] = (uint8_t)arg;
+                    if (P) copy_P(h, arg, r);
+                }
+            }
+            return;
+        }
+        // general K: sequential scan over the tile's columns
         float best = -INFINITY;
         int arg = K, kk = 0, hh = 0;
         for (int c0 = 0; c0 < bn; c0 += 16) {
@@ -162,11 +233,7 @@ struct EpiSelect {
                         const int k = arg >= K ? 0 : arg;
                         const size_t r = ((size_t)b * H + h) * L + t;
                         kstar[r] = (uint8_t)k;
-                        if (P) {
-                            const uint16_t* src = dict_idx + ((size_t)h * K + k) * N;
-                            uint16_t* dst = P + r * N;
-                            for (int j = 0; j < N; ++j) dst[j] = __ldg(src + j);
-                        }
+                        if (P) copy_P(h, k, r);
                     }
                     ++hh;
                     kk = 0;

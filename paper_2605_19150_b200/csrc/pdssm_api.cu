@@ -121,6 +121,8 @@ size_t ws_bytes_g(const Geo& g, int op) {
         case PDSSM_OP_BWD:
             return 2 * cs_f_bytes(g) + (g.P > 0 ? seq_f_bytes(g) + readout_w_bytes(g) : 0) +
                    (g.diag_mode == PDSSM_DIAG_PER_DICT ? seq_f_bytes(g) : 0) + fused_ctrl_bytes(g.S, g.C, g.H);
+        case PDSSM_OP_READOUT:
+            return readout_w_bytes(g);
         case PDSSM_OP_SEGMENT: {
             size_t fwd = plan_bytes(g) + chunk_state_bytes_g(g);
             size_t bwd = 2 * cs_f_bytes(g) + (g.P > 0 ? seq_f_bytes(g) + readout_w_bytes(g) : 0);
@@ -661,6 +663,36 @@ pdssm_status pdssm_project(const void* x, const void* Bw, void* b_out, const pds
                                                 static_cast<T*>(b_out), (int)g.B, (int)g.L, (int)g.H, (int)cN,
                                                 (int)g.d_in);
         return cuda_check("project_simt");
+    });
+}
+
+pdssm_status pdssm_readout(const void* h, const float* C, void* y, const pdssm_dims* dims, void* ws, size_t ws_bytes,
+                           pdssm_stream_t stream) {
+    Geo g;
+    pdssm_status r = geo_of(dims, &g);
+    if (r) return r;
+    if (!h || !C || !y) return fail(PDSSM_ERR_NULL, "readout: h, C, y are required");
+    if (g.P < 1) return fail(PDSSM_ERR_SHAPE, "readout: p_out must be >= 1");
+    if (misaligned(h, g.act) || misaligned(y, g.act) || misaligned(C, 4)) return fail(PDSSM_ERR_ALIGN, "readout: misaligned");
+    if (!ws || ws_bytes < readout_w_bytes(g))
+        return fail(PDSSM_ERR_WORKSPACE, "readout: workspace too small (need %zu)", readout_w_bytes(g));
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    return with_act(g.dtype, [&](auto tv) {
+        using T = decltype(tv);
+        if (tc_readout_ok(g, {h, y, ws})) {
+            T* Cp = static_cast<T*>(ws);
+            k_readout_weights<T><<<(unsigned)ceil_div(g.H * g.nc * g.P * g.N, 256), 256, 0, st>>>(
+                C, Cp, nullptr, (int)g.H, (int)g.nc, (int)g.P, (int)g.N);
+            pdssm_status rr = cuda_check("readout_weights");
+            if (rr) return rr;
+            return readout_tc<T>(g, static_cast<const T*>(h), Cp, static_cast<T*>(y), st);
+        }
+        return with_nc(g.nc, [&](auto ncv) {
+            constexpr int NC = decltype(ncv)::value;
+            k_readout<T, NC><<<(unsigned)(g.S * g.L), 128, (size_t)NC * g.N * 4, st>>>(
+                static_cast<const T*>(h), C, static_cast<T*>(y), (int)g.H, (int)g.L, (int)g.N, (int)g.P);
+            return cuda_check("readout");
+        });
     });
 }
 

@@ -79,3 +79,24 @@ def test_project_validation(P):
     Bw = torch.zeros((1, 1, 8, 8), device="cuda", dtype=torch.bfloat16)
     with pytest.raises(TypeError):
         P.project(x, Bw)
+
+
+@pytest.mark.parametrize("shape", [(2, 2, 300, 2, 64, 32), (1, 3, 129, 1, 32, 16), (2, 1, 70, 2, 16, 5),
+                                   (1, 8, 256, 2, 128, 128)])
+@pytest.mark.parametrize("bf16", [False, True])
+def test_readout_standalone(P, path, shape, bf16):
+    """a8 readout y_t = Re(C_h h_t) (Eq. 1) on given states, against oracle.readout."""
+    B, H, L, c, N, Pp = shape
+    rng = np.random.default_rng(L + N)
+    h = rng.standard_normal((B, H, L, c, N)).astype(np.float32)
+    if bf16:
+        h = synth.round_bf16(h)
+    Cw = synth.readout_C(H, Pp, N, c, seed=L)
+    dt = torch.bfloat16 if bf16 else torch.float32
+    y = P.readout(torch.from_numpy(h).cuda().to(dt), torch.from_numpy(Cw).cuda())
+    hz = O.planes_to_complex(h)                              # [B][H][L][N]
+    Cz = O.planes_to_complex(np.moveaxis(Cw, 1, -2))         # [H][P][N]
+    ref = O.readout(hz, Cz)
+    tol = 2e-2 if bf16 else 1e-4
+    err = np.max(np.abs(y.float().cpu().numpy() - ref)) / np.max(np.abs(ref))
+    assert err <= tol, err

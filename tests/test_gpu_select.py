@@ -100,3 +100,17 @@ def test_select_float_margin_rule(P, path, bf16):
     chosen = np.take_along_axis(lg_ref, k[..., None].astype(np.int64), -1)[..., 0]
     assert np.all(srt[..., -1][~sure] - chosen[~sure] <= gamma[~sure])
     assert np.max(np.abs(lg.cpu().numpy() - lg_ref)) <= 1e-4 * np.max(np.abs(lg_ref))
+
+
+@pytest.mark.parametrize("K", [32, 7])
+def test_select_nan_never_wins(P, path, K):
+    """Reading R8: a NaN logit never wins; a token whose logits are all NaN selects 0."""
+    B, L, d_in, H = 1, 150, 64, 2
+    x = synth.tokens_x(B, L, d_in, seed=3, integer=True)
+    S = synth.selector(H, K, d_in, seed=3, integer=True)
+    S[0, 3, 5] = np.nan                 # logit k=3 of head 0 is NaN at every token
+    x[0, 7, :] = np.nan                 # token 7: every logit NaN
+    k, _, _ = P.select(torch.from_numpy(x).cuda(), torch.from_numpy(S).cuda())
+    k_ref, _ = O.select(x, S)
+    assert np.array_equal(k.cpu().numpy(), k_ref)
+    assert np.all(k.cpu().numpy()[0, :, 7] == 0)

@@ -45,7 +45,8 @@ for b in blocks[1:]:
     if kname.split("I")[-1][:6] and True:
         rows = list(csv.reader(io.StringIO('"Kernel Name"' + b)))
         name = rows[0][1] if len(rows[0]) > 1 else ""
-        if ("fwd" in kname and "fwd" in name) or ("bwd" in kname and "bwd" in name):
+        sel = sys.argv[4] if len(sys.argv) > 4 else None
+        if (sel and sel in name) or (not sel and (("fwd" in kname and "fwd" in name) or ("bwd" in kname and "bwd" in name))):
             best = rows
             break
 rows = best
