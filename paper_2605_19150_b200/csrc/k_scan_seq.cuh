@@ -1,0 +1,587 @@
+// Single-chunk scan (tau >= L, C = 1): one CTA per (b, h) sequence, thread i owns state i.
+//
+// Alg. 1 with one chunk per sequence needs no Phase A aggregate and
+// no inter-chunk carry: the replay from carry_0 = h0 IS the scan.  When B*H fills the
+// GPU (config 2: 128 sequences on 148 SMs) this reads every step's D_t, b_t once
+// (evict-first TMA stream) instead of twice, and each step is one CTA barrier:
+//
+//   v_t = D_t (.) h_{t-1}   (own state, registers)   -> vbuf[t&1][i]      (STS, conflict-free)
+//   __syncthreads()                                   (double-buffered vbuf: one barrier/step)
+//   h_t[i] = b_t[i] + sum_{j : P_t[j] = i} v_t[j]    (the column-one-hot scatter, reading R1,
+//                                                      as a gather over the preimage of i)
+//
+// The preimage of i under entry k is a per-(k, i) record of up to 8 source indices (u8,
+// ascending, padded with the zero slot N); the warp-uniform trip count is the warp's
+// maximum in-degree of entry k.  Entries with an in-degree > 8 take the CSR plan.
+// AGG (PDSSM_EXPORT_MAPS): the chunk aggregate (pi_bar, d_bar, beta_bar) of the single chunk
+// and the final map are composed alongside (thread-local gathers).
+//
+// Backward (reverse, transposed; App. C): thread j owns source j;
+//   lbuf[t&1][j] = lambda_t;  __syncthreads();  lp = lambda_t[P_t[j]]  (a pure gather)
+//   dD_t[j] = conj(h_{t-1}[j]) lp;  g_t = sum_j Re(conj(lp) D_t[j] h_{t-1}[j]);
+//   lambda_{t-1}[j] = e_{t-1}[j] + conj(D_t[j]) lp.
+#pragma once
+#include "pdssm_common.cuh"
+#include "k_scan_fwd.cuh"
+#include "k_scan_fused.cuh"
+
+namespace pdssm {
+namespace seq {
+
+constexpr int CAP = 8;       // inline preimage capacity per (entry, target)
+constexpr int LMAX = 16384;  // k* of the whole sequence is staged in shared memory
+constexpr int MAXN = 128;    // states per CTA (one thread each)
+constexpr int WM_OVF = 15;   // trip-count code of an overflowing entry
+
+__host__ __device__ constexpr size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+// shared-memory carve-up (host and device agree)
+struct Layout {
+    size_t ring, bars, x, x2, kb, rec, wm, ovf, prow, dk, gs, bytes;
+    int slot;   // bytes per ring slot
+    __host__ __device__ Layout(int N, int K, int R, int G, int NC, int esz, int esz_e, bool PD, bool AGG, bool BWD, int L) {
+        const int row = NC * N * esz, erow = NC * N * esz_e;
+        const int NW = N / 32;
+        slot = (int)a16(BWD ? (size_t)(PD ? 0 : G * row) + (size_t)G * erow + (size_t)G * row
+                            : (size_t)(PD ? 0 : G * row) + (size_t)G * row);
+        size_t o = 0;
+        ring = o; o = a16(o + (size_t)R * slot);
+        bars = o; o = a16(o + (size_t)R * 8);
+        const int sv = NC == 2 ? 8 : 4;
+        x = o; o = a16(o + (size_t)2 * (N + 1) * sv);
+        x2 = o; o = a16(o + (AGG ? (size_t)2 * (N + 1) * sv : 0));
+        kb = o; o = a16(o + (size_t)L + 2);
+        rec = o; o = a16(o + (BWD ? 0 : (size_t)K * N * 8));
+        wm = o; o = a16(o + (BWD ? 0 : (size_t)K * NW));
+        ovf = o; o = a16(o + (BWD ? 0 : (size_t)K));
+        prow = o; o = a16(o + ((AGG || BWD) ? (size_t)K * N * 2 : 0));
+        dk = o; o = a16(o + (PD ? (size_t)K * NC * N * 4 : 0));
+        gs = o; o = a16(o + (BWD ? ((size_t)32 * (N + 1) + (size_t)32 * NW) * 4 : 0));
+        bytes = o;
+    }
+};
+
+struct SeqArgs {
+    const uint8_t* kstar;
+    const uint16_t* dict_idx;   // [H][K][N] (clamped on load)
+    const uint8_t* rec;         // [H][K][N][8] preimage records (fwd)
+    const uint8_t* wm;          // [H][K][NW] warp trip counts (fwd)
+    const uint8_t* ovf;         // [H][K] 1 = some preimage longer than CAP (fwd)
+    const uint16_t* pstart;     // CSR plan (overflow entries)
+    const uint16_t* psrc;
+    const void* diag;           // PER_STEP act rows
+    const float* diag_dict;     // PER_DICT f32 [H][K][NC][N]
+    const void* bias;           // fwd: b_t ; bwd: e_t (act or f32)
+    const void* hsaved;         // bwd
+    const float* h0;
+    const float* lam_in;        // bwd
+    ChunkStateView cs;          // C = 1
+    uint16_t* maps;             // fwd [S][2][N] (EXPORT_MAPS)
+    void* out0;                 // fwd: h ; bwd: dbias
+    void* out1;                 // bwd: ddiag (act) or f32 scratch (PER_DICT)
+    float* gsel;                // bwd
+    float* dh0;                 // bwd
+    int H, L, N, K, R, G;
+    uint32_t flags;
+};
+
+// per (entry, target) preimage records: sources ascending, padded with N; wm = warp max
+// in-degree (<= CAP); ovf = an in-degree above CAP occurred
+__global__ void k_build_seq_plan(const uint16_t* __restrict__ dict_idx, uint8_t* __restrict__ rec,
+                                 uint8_t* __restrict__ wm, uint8_t* __restrict__ ovf, int N, uint32_t flags) {
+    extern __shared__ uint16_t sP[];
+    __shared__ int sovf;
+    const int e = blockIdx.x;
+    const int i = threadIdx.x;   // blockDim.x == N (multiple of 32)
+    if (i == 0) sovf = 0;
+    int p = dict_idx[(size_t)e * N + i];
+    if (p >= N) {
+        if (flags & PDSSM_CHECK_FINITE) report(ERRBIT_RANGE);
+        p = N - 1;
+    }
+    sP[i] = (uint16_t)p;
+    __syncthreads();
+    uint8_t r[CAP];
+#pragma unroll
+    for (int q = 0; q < CAP; ++q) r[q] = (uint8_t)N;
+    int d = 0;
+    for (int j = 0; j < N; ++j) {
+        if (sP[j] == i) {
+            if (d < CAP) r[d] = (uint8_t)j;
+            ++d;
+        }
+    }
+    uint8_t* dst = rec + ((size_t)e * N + i) * CAP;
+#pragma unroll
+    for (int q = 0; q < CAP; ++q) dst[q] = r[q];
+    int m = d < CAP ? d : CAP;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (d > CAP) sovf = 1;
+    __syncthreads();
+    // warp trip count; WM_OVF marks an entry with a preimage longer than CAP (CSR fallback)
+    if ((i & 31) == 0) wm[(size_t)e * (N / 32) + (i >> 5)] = (uint8_t)(sovf ? WM_OVF : m);
+    if (i == 0) ovf[e] = (uint8_t)sovf;
+}
+
+__device__ __forceinline__ void stage_k(const SeqArgs& a, uint8_t* kb, size_t base, int L) {
+    for (int x = threadIdx.x; x < L; x += blockDim.x) {
+        int k = a.kstar[base + x];
+        if (k >= a.K) {
+            if (a.flags & PDSSM_CHECK_FINITE) report(ERRBIT_RANGE);
+            k = a.K - 1;
+        }
+        kb[x] = (uint8_t)k;
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void st_stream(T* p, float v, uint64_t pol) {
+    if constexpr (std::is_same<T, float>::value) {
+        asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol));
+    } else {
+        const __nv_bfloat16 b = __float2bfloat16_rn(v);
+        asm volatile("st.global.L2::cache_hint.b16 [%0], %1, %2;" ::"l"(p), "h"(*reinterpret_cast<const uint16_t*>(&b)),
+                     "l"(pol));
+    }
+}
+
+constexpr int SEQ_G = 8;   // steps per ring slot (one TMA group)
+
+// ============================================================================ forward
+// Step t (r = t mod 8 is compile-time inside a full group, so ring rows, the exchange
+// parity and pointer offsets are immediates; in-order issue: nothing waits on a load
+// issued in the same step except the gather itself):
+//   gather offsets (record read a step earlier) ; v_t = D_t h_{t-1} -> STS ; BARRIER ;
+//   8 gather loads (zero slot past the in-degree: branch-free) ; refill (group start) ;
+//   operands of step t+1 (record, trip code, D, b) and k*_{t+2} ; pairwise sum ;
+//   h_t = sum + b_t ; streaming store.
+template <typename T, int NC, bool PD, bool AGG, bool CHECK>
+__global__ void __launch_bounds__(MAXN, 1) k_fwd_seq(SeqArgs a) {
+    using SV = typename fused::SVal<NC>::type;
+    constexpr int G = SEQ_G;
+    constexpr int SVB = (int)sizeof(SV);
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int N = a.N, K = a.K, L = a.L, R = a.R;
+    const int i = threadIdx.x, w = i >> 5, NW = N >> 5;
+    const int s = blockIdx.x, h = s % a.H;
+    const Layout Ly(N, K, R, G, NC, (int)sizeof(T), (int)sizeof(T), PD, AGG, false, L);
+    uint8_t* ring = smem + Ly.ring;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Ly.bars);
+    char* xbc = reinterpret_cast<char*>(smem + Ly.x);
+    char* xbc2 = reinterpret_cast<char*>(smem + Ly.x2);
+    uint8_t* kb = smem + Ly.kb;
+    uint2* rec = reinterpret_cast<uint2*>(smem + Ly.rec);
+    uint8_t* wm = smem + Ly.wm;
+    uint16_t* prow = reinterpret_cast<uint16_t*>(smem + Ly.prow);
+    float* dk = reinterpret_cast<float*>(smem + Ly.dk);
+    const size_t row = (size_t)NC * N;
+    const size_t seq0 = (size_t)s * L;
+    const int ngroups = (L + G - 1) / G;
+    const uint64_t pol = fused::policy_evict_first();
+    {   // one-time tables of head h, and the sequence's k* (zero-padded by 2)
+        const uint2* gr = reinterpret_cast<const uint2*>(a.rec) + (size_t)h * K * N;
+        for (int x = i; x < K * N; x += N) rec[x] = __ldg(gr + x);
+        for (int x = i; x < K * NW; x += N) wm[x] = a.wm[(size_t)h * K * NW + x];
+        if constexpr (AGG)
+            for (int x = i; x < K * N; x += N) prow[x] = (uint16_t)min((int)__ldg(a.dict_idx + (size_t)h * K * N + x), N - 1);
+        if constexpr (PD)
+            for (int x = i; x < K * NC * N; x += N) dk[x] = __ldg(a.diag_dict + (size_t)h * K * NC * N + x);
+        if (i < 2) kb[L + i] = 0;
+    }
+    stage_k(a, kb, seq0, L);
+    const int XB = (N + 1) * SVB;   // bytes of one exchange row (N values + the zero slot)
+    if (i == 0) {
+        *reinterpret_cast<SV*>(xbc + N * SVB) = fused::mk<NC>(0.f, 0.f);
+        *reinterpret_cast<SV*>(xbc + XB + N * SVB) = fused::mk<NC>(0.f, 0.f);
+        if constexpr (AGG) {
+            *reinterpret_cast<SV*>(xbc2 + N * SVB) = fused::mk<NC>(0.f, 0.f);
+            *reinterpret_cast<SV*>(xbc2 + XB + N * SVB) = fused::mk<NC>(0.f, 0.f);
+        }
+        for (int q = 0; q < R; ++q) fused::mbar_init(bars + q, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int ROWB = (int)(row * sizeof(T));
+    const int OFF_B = PD ? 0 : G * ROWB;
+    auto issue = [&](int g, int slot) {   // thread 0: rows of steps [gG, gG+len) -> slot
+        const int t = g * G, len = min(G, L - t);
+        uint8_t* dst = ring + (size_t)slot * Ly.slot;
+        fused::mbar_expect_tx(bars + slot, (uint32_t)((PD ? 0 : len * ROWB) + len * ROWB));
+        if constexpr (!PD) fused::tma_1d_hint(dst, static_cast<const T*>(a.diag) + (seq0 + t) * row, len * ROWB, bars + slot, pol);
+        fused::tma_1d_hint(dst + OFF_B, static_cast<const T*>(a.bias) + (seq0 + t) * row, len * ROWB, bars + slot, pol);
+    };
+    if (i == 0)
+        for (int g = 0; g < R && g < ngroups; ++g) issue(g, g);
+    float hr = 0.f, hi = 0.f;
+    if (a.h0) {
+        hr = a.h0[(size_t)s * row + i];
+        if constexpr (NC == 2) hi = a.h0[(size_t)s * row + N + i];
+    }
+    float br = 0.f, bi = 0.f, dr = 1.f, di = 0.f;
+    int pi = i;
+    T* hout = static_cast<T*>(a.out0) + seq0 * row + i;
+    // operands of the current step
+    int k, k1, m;
+    uint2 rc;
+    float Dr, Di, Br, Bi;
+    auto load_ops = [&](const uint8_t* rp, int k_) {
+        if constexpr (PD) {
+            Dr = dk[(size_t)k_ * row + i];
+            Di = NC == 2 ? dk[(size_t)k_ * row + N + i] : 0.f;
+        } else {
+            const T* Dp = reinterpret_cast<const T*>(rp);
+            Dr = ldact_s(Dp + i);
+            Di = NC == 2 ? ldact_s(Dp + N + i) : 0.f;
+        }
+        const T* Bp = reinterpret_cast<const T*>(rp + OFF_B);
+        Br = ldact_s(Bp + i);
+        Bi = NC == 2 ? ldact_s(Bp + N + i) : 0.f;
+    };
+    int slot = 0;
+    uint32_t ph = 0;
+    const uint8_t* sb = ring;   // base of the current group's slot
+    fused::mbar_wait(bars, 0);
+    k = kb[0];
+    k1 = kb[1];
+    rc = rec[(size_t)k * N + i];
+    m = wm[k * NW + w];
+    load_ops(sb, k);
+    auto step = [&](const int r, const int g, const int t) {
+        char* vbc = xbc + (t & 1) * XB;
+        char* vbc2 = xbc2 + (t & 1) * XB;
+        uint32_t off[CAP];
+#pragma unroll
+        for (int q = 0; q < CAP; ++q) off[q] = __byte_perm(q < 4 ? rc.x : rc.y, 0u, 0x4440u + (uint32_t)(q & 3)) * SVB;
+        if constexpr (CHECK) {
+            check_cpx(cpx{Dr, Di}, a.flags);
+            check_cpx(cpx{Br, Bi}, a.flags);
+        }
+        *reinterpret_cast<SV*>(vbc + i * SVB) = fused::mk<NC>(Dr * hr - Di * hi, Dr * hi + Di * hr);
+        if constexpr (AGG) *reinterpret_cast<SV*>(vbc2 + i * SVB) = fused::mk<NC>(Dr * br - Di * bi, Dr * bi + Di * br);
+        const int mc = m, kc = k;
+        const float bcr = Br, bci = Bi;
+        const uint8_t* rpc = sb + r * ROWB;
+        __syncthreads();
+        SV v[CAP];
+#pragma unroll
+        for (int q = 0; q < CAP; ++q) v[q] = *reinterpret_cast<const SV*>(vbc + off[q]);
+        if (r == 0 && i == 0 && g >= 1 && g - 1 + R < ngroups) {   // previous group's slot is free
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(g - 1 + R, slot == 0 ? R - 1 : slot - 1);
+        }
+        // operands of step t+1 (consumed a step later)
+        if (r < G - 1) {
+            k = k1;
+            rc = rec[(size_t)k * N + i];
+            m = wm[k * NW + w];
+            load_ops(sb + (r + 1) * ROWB, k);
+        } else if (g + 1 < ngroups) {
+            if (++slot == R) {
+                slot = 0;
+                ph ^= 1u;
+            }
+            sb = ring + (size_t)slot * Ly.slot;
+            fused::mbar_wait(bars + slot, ph);
+            k = k1;
+            rc = rec[(size_t)k * N + i];
+            m = wm[k * NW + w];
+            load_ops(sb, k);
+        }
+        k1 = kb[t + 2];
+        // pairwise sum of the 8 slots (sources past the in-degree read the zero slot)
+        auto sum8 = [&](const SV (&x)[CAP], float& sr, float& si) {
+            sr = ((fused::re_of<NC>(x[0]) + fused::re_of<NC>(x[1])) + (fused::re_of<NC>(x[2]) + fused::re_of<NC>(x[3]))) +
+                 ((fused::re_of<NC>(x[4]) + fused::re_of<NC>(x[5])) + (fused::re_of<NC>(x[6]) + fused::re_of<NC>(x[7])));
+            si = ((fused::im_of<NC>(x[0]) + fused::im_of<NC>(x[1])) + (fused::im_of<NC>(x[2]) + fused::im_of<NC>(x[3]))) +
+                 ((fused::im_of<NC>(x[4]) + fused::im_of<NC>(x[5])) + (fused::im_of<NC>(x[6]) + fused::im_of<NC>(x[7])));
+        };
+        float ar, ai, cr = 0.f, ci = 0.f;
+        sum8(v, ar, ai);
+        if constexpr (AGG) {
+#pragma unroll
+            for (int q = 0; q < CAP; ++q) v[q] = *reinterpret_cast<const SV*>(vbc2 + off[q]);
+            sum8(v, cr, ci);
+        }
+        if (mc == WM_OVF) {   // preimage longer than CAP: CSR plan (rare, warp-uniform)
+            ar = ai = cr = ci = 0.f;
+            const SV* vb = reinterpret_cast<const SV*>(vbc);
+            const SV* vb2 = reinterpret_cast<const SV*>(vbc2);
+            const size_t e = (size_t)h * K + kc;
+            const int st = __ldg(a.pstart + e * (N + 1) + i), en = __ldg(a.pstart + e * (N + 1) + i + 1);
+            for (int q = st; q < en; ++q) {
+                const int j = __ldg(a.psrc + e * N + q);
+                ar += fused::re_of<NC>(vb[j]);
+                ai += fused::im_of<NC>(vb[j]);
+                if constexpr (AGG) {
+                    cr += fused::re_of<NC>(vb2[j]);
+                    ci += fused::im_of<NC>(vb2[j]);
+                }
+            }
+        }
+        hr = ar + bcr;
+        hi = NC == 2 ? ai + bci : 0.f;
+        st_stream<T>(hout, hr, pol);
+        if constexpr (NC == 2) st_stream<T>(hout + N, hi, pol);
+        hout += row;
+        if constexpr (AGG) {
+            br = cr + bcr;
+            bi = NC == 2 ? ci + bci : 0.f;
+            // pi / d composition: d <- D_t[pi] d, pi <- P_t[pi]
+            float pr, pm = 0.f;
+            if constexpr (PD) {
+                pr = dk[(size_t)kc * row + pi];
+                if constexpr (NC == 2) pm = dk[(size_t)kc * row + N + pi];
+            } else {
+                const T* Dp = reinterpret_cast<const T*>(rpc);
+                pr = ldact_s(Dp + pi);
+                if constexpr (NC == 2) pm = ldact_s(Dp + N + pi);
+            }
+            const float nr = pr * dr - pm * di, ni = pr * di + pm * dr;
+            dr = nr;
+            di = ni;
+            pi = prow[(size_t)kc * N + pi];
+        }
+    };
+    for (int g = 0; g < ngroups; ++g) {
+        const int t0 = g * G;
+        if (t0 + G <= L) {
+#pragma unroll
+            for (int r = 0; r < G; ++r) step(r, g, t0 + r);
+        } else {
+            for (int r = 0; r < L - t0; ++r) step(r, g, t0 + r);
+        }
+    }
+    // chunk_state of the single chunk: carry_0 = h0; aggregate (pi_bar, d_bar, beta_bar)
+    {
+        a.cs.carry[(size_t)s * row + i] = a.h0 ? a.h0[(size_t)s * row + i] : 0.f;
+        if constexpr (NC == 2) a.cs.carry[(size_t)s * row + N + i] = a.h0 ? a.h0[(size_t)s * row + N + i] : 0.f;
+        if constexpr (AGG) {
+            a.cs.pi[(size_t)s * N + i] = (uint16_t)pi;
+            a.cs.d[(size_t)s * row + i] = dr;
+            a.cs.beta[(size_t)s * row + i] = br;
+            if constexpr (NC == 2) {
+                a.cs.d[(size_t)s * row + N + i] = di;
+                a.cs.beta[(size_t)s * row + N + i] = bi;
+            }
+            if (a.maps) {
+                a.maps[((size_t)s * 2) * N + i] = (uint16_t)i;
+                a.maps[((size_t)s * 2 + 1) * N + i] = (uint16_t)pi;
+            }
+        }
+    }
+}
+
+// ============================================================================ backward
+// Step t (descending; rr = position from the top of the 8-step group, compile-time in a
+// full group): db_t store ; lambda_t -> STS ; BARRIER ; lp = lambda_t[P_t[j]] (P_t[j]
+// read a step earlier) ; refill ; operands of step t-1 (D, e, h from the ring row, P) ;
+// lambda_{t-1} = e_{t-1} + conj(D_t) lp ; dD_t store ; this thread's g_t term -> tile.
+template <typename T, typename TE, int NC, bool PD>
+__global__ void __launch_bounds__(MAXN, 1) k_bwd_seq(SeqArgs a) {
+    using SV = typename fused::SVal<NC>::type;
+    constexpr int G = SEQ_G;
+    constexpr int SVB = (int)sizeof(SV);
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int N = a.N, K = a.K, L = a.L, R = a.R;
+    const int j = threadIdx.x;
+    const int s = blockIdx.x, h = s % a.H;
+    const Layout Ly(N, K, R, G, NC, (int)sizeof(T), (int)sizeof(TE), PD, false, true, L);
+    uint8_t* ring = smem + Ly.ring;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Ly.bars);
+    char* xbc = reinterpret_cast<char*>(smem + Ly.x);
+    uint8_t* kb = smem + Ly.kb;
+    uint16_t* prow = reinterpret_cast<uint16_t*>(smem + Ly.prow);
+    float* dk = reinterpret_cast<float*>(smem + Ly.dk);
+    float* gs = reinterpret_cast<float*>(smem + Ly.gs);   // [32][N+1] g terms, then [32][NW] partials
+    const size_t row = (size_t)NC * N;
+    const size_t seq0 = (size_t)s * L;
+    const int ngroups = (L + G - 1) / G;
+    const uint64_t pol = fused::policy_evict_first();
+    const TE* ein = static_cast<const TE*>(a.bias);
+    for (int x = j; x < K * N; x += N) prow[x] = (uint16_t)min((int)__ldg(a.dict_idx + (size_t)h * K * N + x), N - 1);
+    if constexpr (PD)
+        for (int x = j; x < K * NC * N; x += N) dk[x] = __ldg(a.diag_dict + (size_t)h * K * NC * N + x);
+    stage_k(a, kb, seq0, L);
+    if (j == 0) {
+        for (int q = 0; q < R; ++q) fused::mbar_init(bars + q, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int ROWB = (int)(row * sizeof(T)), EROWB = (int)(row * sizeof(TE));
+    const int OFF_E = PD ? 0 : G * ROWB, OFF_H = OFF_E + G * EROWB;
+    // group g: times t_hi = L-1-gG down to t_lo; D_t at row t - t_lo, e_{t-1} and h_{t-1} likewise
+    auto issue = [&](int g, int slot) {
+        const int t_hi = L - 1 - g * G, t_lo = max(t_hi - G + 1, 0), len = t_hi - t_lo + 1;
+        uint8_t* dst = ring + (size_t)slot * Ly.slot;
+        const int f_first = max(t_lo - 1, 0);                 // e_{t-1}, h_{t-1} rows needed for t >= 1
+        const int f_cnt = max(0, t_hi - 1 - f_first + 1);
+        const int f_off = f_first - (t_lo - 1);
+        fused::mbar_expect_tx(bars + slot, (uint32_t)((PD ? 0 : len * ROWB) + (ein ? f_cnt * EROWB : 0) + f_cnt * ROWB));
+        if constexpr (!PD) fused::tma_1d_hint(dst, static_cast<const T*>(a.diag) + (seq0 + t_lo) * row, len * ROWB, bars + slot, pol);
+        if (ein && f_cnt > 0)
+            fused::tma_1d_hint(dst + OFF_E + (size_t)f_off * EROWB, ein + (seq0 + f_first) * row, f_cnt * EROWB, bars + slot, pol);
+        if (f_cnt > 0)
+            fused::tma_1d_hint(dst + OFF_H + (size_t)f_off * ROWB, static_cast<const T*>(a.hsaved) + (seq0 + f_first) * row,
+                               f_cnt * ROWB, bars + slot, pol);
+    };
+    if (j == 0)
+        for (int g = 0; g < R && g < ngroups; ++g) issue(g, g);
+    float lr = 0.f, li = 0.f;   // lambda_{L-1} = e_{L-1} + lam_in
+    if (ein) {
+        lr = ldact_s(ein + (seq0 + L - 1) * row + j);
+        if constexpr (NC == 2) li = ldact_s(ein + (seq0 + L - 1) * row + N + j);
+    }
+    if (a.lam_in) {
+        lr += a.lam_in[(size_t)s * row + j];
+        if constexpr (NC == 2) li += a.lam_in[(size_t)s * row + N + j];
+    }
+    float h0r = 0.f, h0i = 0.f;
+    if (a.h0) {
+        h0r = a.h0[(size_t)s * row + j];
+        if constexpr (NC == 2) h0i = a.h0[(size_t)s * row + N + j];
+    }
+    T* dbp = static_cast<T*>(a.out0) + (seq0 + L - 1) * row + j;
+    T* ddp = PD ? nullptr : static_cast<T*>(a.out1) + (seq0 + L - 1) * row + j;
+    float* ddf = PD ? static_cast<float*>(a.out1) + (seq0 + L - 1) * row + j : nullptr;
+    int p;
+    float Dr, Di, er, ei, hr, hi;
+    int slot = 0;
+    uint32_t ph = 0;
+    const uint8_t* sb = ring;
+    fused::mbar_wait(bars, 0);
+    // explicit row loads: (slot base, row index) -> operands of time t
+    auto load_row = [&](const uint8_t* sb_, int ro, int t, int k_) {
+        p = prow[(size_t)k_ * N + j];
+        if constexpr (PD) {
+            Dr = dk[(size_t)k_ * row + j];
+            Di = NC == 2 ? dk[(size_t)k_ * row + N + j] : 0.f;
+        } else {
+            const T* Dp = reinterpret_cast<const T*>(sb_ + ro * ROWB);
+            Dr = ldact_s(Dp + j);
+            Di = NC == 2 ? ldact_s(Dp + N + j) : 0.f;
+        }
+        if (t > 0) {
+            if (ein) {
+                const TE* ep = reinterpret_cast<const TE*>(sb_ + OFF_E + ro * EROWB);
+                er = ldact_s(ep + j);
+                ei = NC == 2 ? ldact_s(ep + N + j) : 0.f;
+            } else {
+                er = ei = 0.f;
+            }
+            const T* hp = reinterpret_cast<const T*>(sb_ + OFF_H + ro * ROWB);
+            hr = ldact_s(hp + j);
+            hi = NC == 2 ? ldact_s(hp + N + j) : 0.f;
+        } else {
+            er = ei = 0.f;
+            hr = h0r;
+            hi = h0i;
+        }
+    };
+    {
+        const int t_lo0 = max(L - G, 0);
+        load_row(sb, L - 1 - t_lo0, L - 1, kb[L - 1]);
+    }
+    int km1 = L > 1 ? kb[L - 2] : 0;   // k* of step t-1
+    auto step = [&](const int rr, const int g, const int t, const int t_lo, const bool inner) {
+        // inner: full group with t_lo > 0 -> rows of step t-1 are compile-time, t-1 > 0
+        const int v = L - 1 - t;
+        st_stream<T>(dbp, lr, pol);                       // db_t = lambda_t
+        if constexpr (NC == 2) st_stream<T>(dbp + N, li, pol);
+        dbp -= row;
+        char* lbc = xbc + (t & 1) * (N * SVB);
+        *reinterpret_cast<SV*>(lbc + j * SVB) = fused::mk<NC>(lr, li);
+        const int pc = p;
+        const float Dcr = Dr, Dci = Di, ecr = er, eci = ei, hcr = hr, hci = hi;
+        __syncthreads();
+        const SV lpv = *reinterpret_cast<const SV*>(lbc + pc * SVB);
+        if (rr == 0 && j == 0 && g >= 1 && g - 1 + R < ngroups) {   // previous group's slot is free
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(g - 1 + R, slot == 0 ? R - 1 : slot - 1);
+        }
+        if ((v & 31) == 0 && v > 0 && a.gsel) {   // g_t of the previous 32 steps
+            const int q = j & 31, part = j >> 5, NP = N >> 5;
+            const float* gr = gs + (size_t)q * (N + 1);
+            float acc = 0.f;
+            float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+            int x = part;
+            for (; x + 3 * NP < N; x += 4 * NP) {
+                a0 += gr[x];
+                a1 += gr[x + NP];
+                a2 += gr[x + 2 * NP];
+                a3 += gr[x + 3 * NP];
+            }
+            for (; x < N; x += NP) a0 += gr[x];
+            acc = (a0 + a1) + (a2 + a3);
+            float* red = gs + (size_t)32 * (N + 1);
+            red[part * 32 + q] = acc;
+            __syncthreads();
+            if (j < 32) {
+                float tot = 0.f;
+                for (int x = 0; x < NP; ++x) tot += red[x * 32 + j];
+                a.gsel[seq0 + (L - 1 - (v - 32 + j))] = tot;
+            }
+            __syncthreads();
+        }
+        // operands of step t-1 (consumed a step later)
+        if (inner && rr < G - 1) {
+            load_row(sb, G - 2 - rr, 1, km1);
+            km1 = kb[t - 2];
+        } else if (t > 0) {
+            if (t - 1 >= t_lo) {
+                load_row(sb, t - 1 - t_lo, t - 1, km1);
+            } else {
+                if (++slot == R) {
+                    slot = 0;
+                    ph ^= 1u;
+                }
+                sb = ring + (size_t)slot * Ly.slot;
+                fused::mbar_wait(bars + slot, ph);
+                const int tlo_n = max(t_lo - G, 0);
+                load_row(sb, t - 1 - tlo_n, t - 1, km1);
+            }
+            km1 = t >= 2 ? kb[t - 2] : 0;
+        }
+        const float pr = fused::re_of<NC>(lpv), pm = fused::im_of<NC>(lpv);
+        lr = ecr + Dcr * pr + Dci * pm;                   // lambda_{t-1} = e_{t-1} + conj(D_t) lp
+        li = NC == 2 ? eci + Dcr * pm - Dci * pr : 0.f;
+        const float ddr = hcr * pr + hci * pm, ddi = hcr * pm - hci * pr;   // dD_t = conj(h_{t-1}) lp
+        if constexpr (PD) {
+            ddf[0] = ddr;
+            if constexpr (NC == 2) ddf[N] = ddi;
+            ddf -= row;
+        } else {
+            st_stream<T>(ddp, ddr, pol);
+            if constexpr (NC == 2) st_stream<T>(ddp + N, ddi, pol);
+            ddp -= row;
+        }
+        const float qr = Dcr * hcr - Dci * hci, qi = Dcr * hci + Dci * hcr;
+        gs[(size_t)(v & 31) * (N + 1) + j] = pr * qr + pm * qi;   // this thread's term of g_t
+    };
+    for (int g = 0; g < ngroups; ++g) {
+        const int t_hi = L - 1 - g * G, t_lo = max(t_hi - G + 1, 0);
+        if (t_hi - t_lo + 1 == G && t_lo > 0) {
+#pragma unroll
+            for (int rr = 0; rr < G; ++rr) step(rr, g, t_hi - rr, t_lo, true);
+        } else {
+            for (int rr = 0; rr <= t_hi - t_lo; ++rr) step(rr, g, t_hi - rr, t_lo, false);
+        }
+    }
+    __syncthreads();
+    if (a.gsel) {   // the last (L % 32 or 32) steps
+        const int v0 = ((L - 1) / 32) * 32;
+        for (int x = j; x < 32 && v0 + x < L; x += N) {
+            const float* gr = gs + (size_t)x * (N + 1);
+            float acc = 0.f;
+            for (int y = 0; y < N; ++y) acc += gr[y];
+            a.gsel[seq0 + (L - 1 - (v0 + x))] = acc;
+        }
+    }
+    if (a.dh0) {   // after t = 0: lambda = A_0^T lambda_0 (no e_{-1} term)
+        a.dh0[(size_t)s * row + j] = lr;
+        if constexpr (NC == 2) a.dh0[(size_t)s * row + N + j] = li;
+    }
+}
+
+}  // namespace seq
+}  // namespace pdssm

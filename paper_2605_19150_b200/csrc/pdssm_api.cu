@@ -15,6 +15,7 @@
 #include "k_sp.cuh"
 #include "k_scan_fused.cuh"
 #include "k_gemm_tc.cuh"
+#include "k_scan_seq.cuh"
 
 #include <mutex>
 
@@ -44,8 +45,34 @@ struct Geo {
 
 constexpr uint32_t kKnownFlags = PDSSM_CHECK_FINITE | PDSSM_DETERMINISTIC | PDSSM_EXPORT_MAPS;
 
+// single-chunk (tau = L) scan kernels: one CTA of N threads per sequence
+bool seq_shape_ok(int64_t N, int64_t K, int64_t L, int nc, size_t act) {
+    (void)nc; (void)act;
+    return N % 32 == 0 && N <= seq::MAXN && (size_t)K * N * 8 <= 64 * 1024 && L <= seq::LMAX;
+}
+int num_sms_dev() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+    }
+    return sms;
+}
+bool env_path_is(const char* v) {
+    const char* p = getenv("PDSSM_PATH");
+    return p && strcmp(p, v) == 0;
+}
+
+// Library default chunk length (reading R20: tuning only).  When the B*H sequences
+// alone fill most of the SMs, one chunk per sequence (tau = L) runs the single-pass
+// CTA-per-sequence kernels; otherwise tau = 64 (chunked, decoupled look-back).
 int default_tau(const pdssm_dims* d) {
-    (void)d;
+    const int64_t S = d->batch * d->heads;
+    const bool forced_chunked = env_path_is("fused") || env_path_is("generic");
+    if (!forced_chunked && seq_shape_ok(d->state, d->dict, d->len, d->is_complex, d->dtype == PDSSM_BF16 ? 2 : 4) &&
+        (env_path_is("seq") || S * 10 >= (int64_t)num_sms_dev() * 6) && d->len <= (int64_t)1 << 30)
+        return (int)d->len;
     return 64;
 }
 
@@ -95,6 +122,11 @@ size_t cs_pi_bytes(const Geo& g) { return align256((size_t)g.S * g.C * g.N * 2);
 size_t cs_f_bytes(const Geo& g) { return align256((size_t)g.S * g.C * g.nc * g.N * 4); }
 size_t chunk_state_bytes_g(const Geo& g) { return cs_pi_bytes(g) + 3 * cs_f_bytes(g); }
 size_t seq_f_bytes(const Geo& g) { return align256((size_t)g.S * g.L * g.nc * g.N * 4); }
+// single-chunk plan: preimage records [H][K][N][8], warp trip counts, overflow flags
+size_t seq_rec_bytes(const Geo& g) { return align256((size_t)g.H * g.K * g.N * 8); }
+size_t seq_wm_bytes(const Geo& g) { return align256((size_t)g.H * g.K * (g.N / 32 > 0 ? g.N / 32 : 1)); }
+size_t seq_ovf_bytes(const Geo& g) { return align256((size_t)g.H * g.K); }
+size_t seq_plan_bytes(const Geo& g) { return seq_rec_bytes(g) + seq_wm_bytes(g) + seq_ovf_bytes(g); }
 // readout weights staged in act dtype (Cp or CT), H*P*c*N elements
 size_t readout_w_bytes(const Geo& g) { return g.P > 0 ? align256((size_t)g.H * g.P * g.nc * g.N * g.act) : 0; }
 size_t seq_act_bytes(const Geo& g) { return align256((size_t)g.S * g.L * g.nc * g.N * g.act); }
@@ -117,7 +149,7 @@ size_t ws_bytes_g(const Geo& g, int op) {
             return align256((size_t)g.S * g.L * g.K * 4);
         case PDSSM_OP_FWD:
             return plan_bytes(g) + (g.P > 0 ? seq_act_bytes(g) + readout_w_bytes(g) : 0) +
-                   fused_plan_bytes(g.H, g.K, g.N) + fused_ctrl_bytes(g.S, g.C, g.H);
+                   fused_plan_bytes(g.H, g.K, g.N) + fused_ctrl_bytes(g.S, g.C, g.H) + seq_plan_bytes(g);
         case PDSSM_OP_BWD:
             return 2 * cs_f_bytes(g) + (g.P > 0 ? seq_f_bytes(g) + readout_w_bytes(g) : 0) +
                    (g.diag_mode == PDSSM_DIAG_PER_DICT ? seq_f_bytes(g) : 0) + fused_ctrl_bytes(g.S, g.C, g.H);
@@ -403,6 +435,40 @@ pdssm_status prepare_e(const Geo& g, const void* dh, const void* dy, const float
     return cuda_check("bwd_prepare_e");
 }
 
+// ---------------------------------------------------------------------------
+// single-chunk path: plan, sizing, launches
+// ---------------------------------------------------------------------------
+
+constexpr size_t kSeqSmemBudget = 200 * 1024;
+constexpr int kSeqG = seq::SEQ_G;
+
+// ring depth R for this shape (0: the layout does not fit)
+int seq_ring(const Geo& g, bool bwd, bool agg, size_t esz_e) {
+    const int ngroups = (int)ceil_div(g.L, kSeqG);
+    int best = 0;
+    for (int R = 2; R <= 16 && R <= ngroups + 1; ++R) {
+        seq::Layout ly((int)g.N, (int)g.K, R, kSeqG, g.nc, (int)g.act, (int)esz_e, g.diag_mode == PDSSM_DIAG_PER_DICT, agg, bwd,
+                       (int)g.L);
+        if (ly.bytes <= kSeqSmemBudget) best = R;
+    }
+    if (best == 0 && ngroups <= 1) best = 2;
+    return best;
+}
+
+bool seq_applicable(const Geo& g, std::initializer_list<const void*> ptrs) {
+    if (g.C != 1 || env_path_is("fused") || env_path_is("generic")) return false;
+    if (!seq_shape_ok(g.N, g.K, g.L, g.nc, g.act)) return false;
+    for (const void* p : ptrs)
+        if (misaligned(p, 16)) return false;
+    return seq_ring(g, false, true, g.act) >= 2 && seq_ring(g, true, false, 4) >= 2;
+}
+
+pdssm_status seq_set_smem(const void* f, size_t bytes) {
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return fail(PDSSM_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    return PDSSM_OK;
+}
+
 template <typename F>
 pdssm_status with_npl(int npl, F&& f) {
     if (npl == 1) return f(std::integral_constant<int, 1>{});
@@ -481,6 +547,62 @@ pdssm_status fwd_fused(const Geo& g, fused::FusedArgs& fa, uint8_t* rec, uint32_
                     return launch_fused(fused::k_fwd_fused<T, NC, NPL, PD>, fa, WS::bytes + WS::t_bytes((int)g.K),
                                         WS::THREADS, g, st, "fwd_fused");
                 });
+            });
+        });
+    });
+}
+
+pdssm_status fwd_seq(const Geo& g, seq::SeqArgs& sa, uint8_t* rec, uint8_t* wm, uint8_t* ovf, cudaStream_t st) {
+    seq::k_build_seq_plan<<<(unsigned)(g.H * g.K), (unsigned)g.N, (size_t)g.N * 2, st>>>(sa.dict_idx, rec, wm, ovf,
+                                                                                     (int)g.N, g.flags);
+    pdssm_status r = cuda_check("build_seq_plan");
+    if (r) return r;
+    const bool agg = (g.flags & PDSSM_EXPORT_MAPS) != 0;
+    sa.R = seq_ring(g, false, agg, g.act);
+    sa.G = kSeqG;
+    return with_act(g.dtype, [&](auto tv) {
+        using T = decltype(tv);
+        return with_nc(g.nc, [&](auto ncv) {
+            constexpr int NC = decltype(ncv)::value;
+            return with_pd(g.diag_mode, [&](auto pdv) {
+                constexpr bool PD = decltype(pdv)::value;
+                auto go = [&](auto aggv, auto chkv) {
+                    constexpr bool AGG = decltype(aggv)::value;
+                    constexpr bool CHK = decltype(chkv)::value;
+                    seq::Layout ly((int)g.N, (int)g.K, sa.R, sa.G, NC, (int)sizeof(T), (int)sizeof(T), PD, AGG, false,
+                                   (int)g.L);
+                    auto kern = seq::k_fwd_seq<T, NC, PD, AGG, CHK>;
+                    pdssm_status rr = seq_set_smem((const void*)kern, ly.bytes);
+                    if (rr) return rr;
+                    kern<<<(unsigned)g.S, (unsigned)g.N, ly.bytes, st>>>(sa);
+                    return cuda_check("fwd_seq");
+                };
+                const bool chk = (g.flags & PDSSM_CHECK_FINITE) != 0;
+                if (agg) return chk ? go(std::true_type{}, std::true_type{}) : go(std::true_type{}, std::false_type{});
+                return chk ? go(std::false_type{}, std::true_type{}) : go(std::false_type{}, std::false_type{});
+            });
+        });
+    });
+}
+
+template <typename TE>
+pdssm_status bwd_seq(const Geo& g, seq::SeqArgs& sa, cudaStream_t st) {
+    return with_act(g.dtype, [&](auto tv) {
+        using T = decltype(tv);
+        using TEE = typename std::conditional<std::is_same<TE, void>::value, T, TE>::type;
+        sa.R = seq_ring(g, true, false, sizeof(TEE));
+        sa.G = kSeqG;
+        return with_nc(g.nc, [&](auto ncv) {
+            constexpr int NC = decltype(ncv)::value;
+            return with_pd(g.diag_mode, [&](auto pdv) {
+                constexpr bool PD = decltype(pdv)::value;
+                seq::Layout ly((int)g.N, (int)g.K, sa.R, sa.G, NC, (int)sizeof(T), (int)sizeof(TEE), PD, false, true,
+                               (int)g.L);
+                auto kern = seq::k_bwd_seq<T, TEE, NC, PD>;
+                pdssm_status rr = seq_set_smem((const void*)kern, ly.bytes);
+                if (rr) return rr;
+                kern<<<(unsigned)g.S, (unsigned)g.N, ly.bytes, st>>>(sa);
+                return cuda_check("bwd_seq");
             });
         });
     });
@@ -731,13 +853,28 @@ pdssm_status pdssm_scan_fwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
     uint32_t* fhdr = bump.take<uint32_t>(fused_hdr_bytes(g.H, g.K));
     uint16_t* fpcl = bump.take<uint16_t>(fused_pclamp_bytes(g.H, g.K, g.N));
     uint32_t* ctrl = bump.take<uint32_t>(fused_ctrl_bytes(g.S, g.C, g.H));
+    uint8_t* srec = bump.take<uint8_t>(seq_rec_bytes(g));
+    uint8_t* swm = bump.take<uint8_t>(seq_wm_bytes(g));
+    uint8_t* sovf = bump.take<uint8_t>(seq_ovf_bytes(g));
     void* hout = h_out_opt ? h_out_opt : hscratch;
     ChunkStateView cs = cs_view(g, chunk_state);
     if ((r = launch_plan(g, dict_idx, pstart, psrc, st))) return r;
     uint16_t* maps = (g.flags & PDSSM_EXPORT_MAPS) ? maps_opt : nullptr;
-    const bool use_fused = fused_applicable(
+    const bool use_seq = seq_applicable(g, {g.diag_mode == PDSSM_DIAG_PER_STEP ? diag : nullptr, bias, hout});
+    if (env_path_is("seq") && !use_seq)
+        return fail(PDSSM_ERR_UNSUPPORTED, "scan_fwd: PDSSM_PATH=seq but the single-chunk path does not apply");
+    const bool use_fused = !use_seq && fused_applicable(
         g, {g.diag_mode == PDSSM_DIAG_PER_STEP ? diag : nullptr, bias, hout, h0_opt, chunk_state, maps});
-    if (use_fused) {
+    if (use_seq) {
+        seq::SeqArgs sa{};
+        sa.kstar = kstar; sa.dict_idx = dict_idx; sa.rec = srec; sa.wm = swm; sa.ovf = sovf; sa.pstart = pstart;
+        sa.psrc = psrc;
+        sa.diag = g.diag_mode == PDSSM_DIAG_PER_STEP ? diag : nullptr;
+        sa.diag_dict = g.diag_mode == PDSSM_DIAG_PER_DICT ? static_cast<const float*>(diag) : nullptr;
+        sa.bias = bias; sa.h0 = h0_opt; sa.cs = cs; sa.maps = maps; sa.out0 = hout;
+        sa.H = (int)g.H; sa.L = (int)g.L; sa.N = (int)g.N; sa.K = (int)g.K; sa.flags = g.flags;
+        if ((r = fwd_seq(g, sa, srec, swm, sovf, st))) return r;
+    } else if (use_fused) {
         fused::FusedArgs fa{};
         fa.kstar = kstar; fa.dict_idx = dict_idx; fa.pstart = pstart; fa.psrc = psrc; fa.rec = frec; fa.hdr = fhdr;
         fa.pclamp = fpcl;
@@ -806,11 +943,46 @@ pdssm_status pdssm_scan_bwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
     ChunkStateView cs = cs_view(g, const_cast<void*>(chunk_state));
     const int thr = threads_for(g.N);
     const unsigned items = (unsigned)(g.S * g.C);
-    const bool use_fused =
+    const bool use_seq = seq_applicable(g, {g.diag_mode == PDSSM_DIAG_PER_STEP ? diag : nullptr, h_saved, dh_opt, ebuf});
+    if (env_path_is("seq") && !use_seq)
+        return fail(PDSSM_ERR_UNSUPPORTED, "scan_bwd: PDSSM_PATH=seq but the single-chunk path does not apply");
+    const bool use_fused = !use_seq &&
         fused_applicable(g, {g.diag_mode == PDSSM_DIAG_PER_STEP ? diag : nullptr, h_saved, dh_opt, h0_opt, lam_in_opt,
                              dbias, g.diag_mode == PDSSM_DIAG_PER_STEP ? ddiag : nullptr, dh0_opt, chunk_state});
-    if (!use_fused && path_fused_forced())
+    if (!use_fused && !use_seq && path_fused_forced())
         return fail(PDSSM_ERR_UNSUPPORTED, "scan_bwd: PDSSM_PATH=fused but the fused path does not apply to these dims");
+    if (use_seq) {
+        if (dy_opt) {
+            r = with_act(g.dtype, [&](auto tv) {
+                using T = decltype(tv);
+                return with_nc(g.nc, [&](auto ncv) {
+                    constexpr int NC = decltype(ncv)::value;
+                    return prepare_e<T, NC>(g, dh_opt, dy_opt, C_opt, ebuf, wbuf, st);
+                });
+            });
+            if (r) return r;
+        }
+        seq::SeqArgs sa{};
+        sa.kstar = kstar; sa.dict_idx = dict_idx;
+        sa.diag = g.diag_mode == PDSSM_DIAG_PER_STEP ? diag : nullptr;
+        sa.diag_dict = g.diag_mode == PDSSM_DIAG_PER_DICT ? static_cast<const float*>(diag) : nullptr;
+        sa.bias = dy_opt ? static_cast<const void*>(ebuf) : dh_opt;
+        sa.hsaved = h_saved; sa.h0 = h0_opt; sa.lam_in = lam_in_opt; sa.cs = cs;
+        sa.out0 = dbias; sa.out1 = g.diag_mode == PDSSM_DIAG_PER_DICT ? static_cast<void*>(dDbuf) : ddiag;
+        sa.gsel = gsel; sa.dh0 = dh0_opt;
+        sa.H = (int)g.H; sa.L = (int)g.L; sa.N = (int)g.N; sa.K = (int)g.K; sa.flags = g.flags;
+        r = dy_opt ? bwd_seq<float>(g, sa, st) : bwd_seq<void>(g, sa, st);
+        if (r) return r;
+        if (g.diag_mode == PDSSM_DIAG_PER_DICT) {
+            r = with_nc(g.nc, [&](auto ncv) {
+                constexpr int NC = decltype(ncv)::value;
+                k_bwd_reduce_dict<NC><<<(unsigned)(g.H * g.K), 256, 0, st>>>(
+                    kstar, dDbuf, static_cast<float*>(ddiag), (int)g.B, (int)g.H, (int)g.L, (int)g.N, (int)g.K);
+                return cuda_check("bwd_reduce_dict");
+            });
+        }
+        return r;
+    }
     if (use_fused) {
         if (dy_opt) {
             r = with_act(g.dtype, [&](auto tv) {

@@ -32,6 +32,9 @@ template <> struct Act<__nv_bfloat16> {
 
 template <typename T> __device__ __forceinline__ float ldact(const T* p) { return Act<T>::ld(p); }
 template <typename T> __device__ __forceinline__ void stact(T* p, float v) { Act<T>::st(p, v); }
+// plain (generic-pointer) load, valid for shared memory
+__device__ __forceinline__ float ldact_s(const float* p) { return *p; }
+__device__ __forceinline__ float ldact_s(const __nv_bfloat16* p) { return __bfloat162float(*p); }
 
 // ---------------------------------------------------------------- complex (split planes)
 struct cpx {

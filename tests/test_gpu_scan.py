@@ -276,3 +276,80 @@ def test_check_finite_reports(P):
         P.check_device()
     assert ei.value.status == 3
     P.check_device()      # cleared
+
+
+# ---------------------------------------------------------------------------
+# single-chunk path (tau >= L, C = 1): one CTA per sequence (csrc/k_scan_seq.cuh)
+SEQ_CASES = [
+    # B, H, L, N, K, c
+    (2, 2, 300, 128, 32, 2),
+    (1, 3, 129, 64, 16, 1),
+    (2, 1, 77, 32, 5, 2),
+    (1, 2, 1000, 96, 8, 2),
+    (1, 1, 4500, 32, 4, 1),       # crosses the 4096-step k* window
+    (3, 1, 1, 64, 3, 2),          # L = 1
+]
+
+
+@pytest.mark.parametrize("case", SEQ_CASES, ids=[str(c) for c in SEQ_CASES])
+@pytest.mark.parametrize("bf16", [False, True], ids=["f32", "bf16"])
+def test_seq_path_parity(P, case, bf16, monkeypatch):
+    monkeypatch.setenv("PDSSM_PATH", "seq")
+    B, H, L, N, K, c = case
+    inp, f, got, ch, ref, Pm, Dz = run_case(P, B, H, L, N, K, c, 0, bf16=bf16, seed=L + N)
+    assert f["tau"] == L
+    tol = TOL["bf16" if bf16 else "f32"]
+    assert rel(cpx(f["h"]), ch["h"]) <= tol
+    assert np.array_equal(f["maps"].cpu().numpy().astype(np.int64), ch["maps"])
+    pi, d_bar, beta_bar, carry = P.chunk_state_views(f["chunk_state"], f["dims"])
+    assert np.array_equal(pi.cpu().numpy().astype(np.int64), ch["pi_bar"])
+    assert rel(O.planes_to_complex(d_bar.cpu().numpy()), ch["d_bar"]) <= 1e-4
+    assert rel(O.planes_to_complex(beta_bar.cpu().numpy()), ch["beta_bar"]) <= 1e-4
+    assert rel(O.planes_to_complex(carry.cpu().numpy()), ch["carries"]) <= 1e-4
+    db, dD, g, dh0 = got
+    db_r, dD_r, g_r, dh0_r = ref
+    assert rel(cpx(db), db_r) <= tol
+    assert rel(cpx(dD), dD_r) <= (tol if not bf16 else 3e-2)
+    assert rel(g.cpu().numpy(), g_r) <= (tol if not bf16 else 3e-2)
+    assert rel(O.planes_to_complex(dh0.cpu().numpy()), dh0_r) <= tol
+
+
+@pytest.mark.parametrize("N", [64, 128])
+def test_seq_path_per_dict_and_overflow(P, N, monkeypatch):
+    """PER_DICT diagonals, and an entry whose preimage exceeds the 8-source records
+    (a constant map: in-degree N) so the CSR fallback runs."""
+    monkeypatch.setenv("PDSSM_PATH", "seq")
+    B, H, L, K, c = 2, 2, 200, 6, 2
+    inp = synth.scan_inputs(B, H, L, N, K, c, seed=N + 7, h0=True, dh=True, per_dict=True)
+    inp["dict_idx"][0, 1, :] = 3          # head 0, entry 1: every source -> state 3
+    inp["dict_idx"][1, 2, : N // 2] = 0   # head 1, entry 2: in-degree N/2 at state 0
+    d = to_dev(inp, False)
+    d["diag"] = torch.from_numpy(inp["diag"]).cuda()
+    f = P.scan_fwd(d["kstar"], d["dict_idx"], d["diag"], d["bias"], h0=d["h0"], per_dict=True)
+    db, dD, g, dh0 = P.scan_bwd(d["kstar"], d["dict_idx"], d["diag"], f["h"], f["chunk_state"], f["dims"],
+                                dh=d["dh"], h0=d["h0"])
+    torch.cuda.synchronize()
+    Pm = O.gather_P(inp["dict_idx"], inp["kstar"])
+    Dz = O.gather_D_per_dict(O.planes_to_complex(inp["diag"]), inp["kstar"])
+    bz, h0z, e = (O.planes_to_complex(inp[k]) for k in ("bias", "h0", "dh"))
+    h = O.scan_forward(Pm, Dz, bz, h0z)
+    assert rel(cpx(f["h"]), h) <= 1e-4
+    db_r, dD_r, g_r, dh0_r = O.scan_backward(Pm, Dz, h, e, h0z)
+    assert rel(cpx(db), db_r) <= 1e-4
+    assert rel(g.cpu().numpy(), g_r) <= 1e-4
+    # PER_DICT dD is reduced per entry: sum over the steps that selected it
+    dDk = np.zeros((H, K, N), np.complex128)
+    for b in range(B):
+        for hh in range(H):
+            np.add.at(dDk[hh], inp["kstar"][b, hh], dD_r[b, hh])
+    assert rel(O.planes_to_complex(dD.cpu().numpy()), dDk) <= 1e-4
+    assert rel(O.planes_to_complex(dh0.cpu().numpy()), dh0_r) <= 1e-4
+
+
+def test_seq_path_is_default_for_full_batches(P, monkeypatch):
+    """B*H >= 0.6 * #SMs: the library default chunk is tau = L (single chunk)."""
+    monkeypatch.delenv("PDSSM_PATH", raising=False)
+    dims = P.make_dims(16, 8, 2048, 128, 32, c=2)
+    assert P.default_chunk(dims) == 2048
+    dims = P.make_dims(1, 2, 2048, 128, 32, c=2)
+    assert P.default_chunk(dims) == 64

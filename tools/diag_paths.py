@@ -15,7 +15,8 @@ tau = int(os.environ.get("TAU", 0))
 inp = synth.scan_inputs(B, H, L, N, K, c, seed=2000, dh=True)
 d = {k: torch.from_numpy(v).cuda() for k, v in inp.items()}
 d["dict_idx"] = d["dict_idx"].to(torch.int16)
-for path in ["generic", "fused"]:
+ref = None
+for path in os.environ.get("PATHS", "fused,seq").split(","):
     os.environ["PDSSM_PATH"] = path
     f = P.scan_fwd(d["kstar"], d["dict_idx"], d["diag"], d["bias"], tau=tau)
     r = P.scan_bwd(d["kstar"], d["dict_idx"], d["diag"], f["h"], f["chunk_state"], f["dims"], dh=d["dh"])
@@ -32,9 +33,9 @@ for path in ["generic", "fused"]:
         ts.append((e0.elapsed_time(e1), e1.elapsed_time(e2)))
     ts = np.array(ts[2:])
     print(path, "tau", f["tau"], "fwd ms %.3f bwd ms %.3f" % tuple(ts.mean(0)), flush=True)
-    if path == "generic":
+    if ref is None:
         ref = (f["h"].clone(), r[0].clone(), r[1].clone(), r[2].clone())
     else:
         for name, a, b in zip(["h", "db", "dD", "g"], ref, (f["h"], r[0], r[1], r[2])):
             err = (a - b).abs().max().item() / max(a.abs().max().item(), 1e-30)
-            print("  rel diff generic vs fused", name, "%.2e" % err)
+            print("  rel diff vs first path", name, "%.2e" % err)

@@ -53,21 +53,25 @@ rows = best
 hi = [i for i, r in enumerate(rows) if "Address" in r and "Source" in r][0]
 h = rows[hi]
 ai, ei, wi = h.index("Address"), h.index("Instructions Executed"), h.index("Warp Stall Sampling (All Samples)")
+fi = h.index("L1 Wavefronts Shared") if "L1 Wavefronts Shared" in h else None
 data = []
 for r in rows[hi + 1:]:
     try:
-        data.append((int(r[ai], 16), int(r[ei] or 0), int(r[wi] or 0)))
+        data.append((int(r[ai], 16), int(r[ei] or 0), int(r[wi] or 0), int(r[fi] or 0) if fi is not None else 0))
     except (ValueError, IndexError):
         pass
 base = min(d[0] for d in data)
-byline = collections.defaultdict(lambda: [0, 0, 0])
-for addr, n, w in data:
+byline = collections.defaultdict(lambda: [0, 0, 0, 0])
+for addr, n, w, f in data:
     ln, ins = fmap.get(addr - base, ("?", "?"))
     byline[ln][0] += n
     byline[ln][1] += w
     byline[ln][2] += 1
+    byline[ln][3] += f
 tot = sum(v[0] for v in byline.values())
 tw = sum(v[1] for v in byline.values()) or 1
-print(f"total warp-inst {tot}  samples {tw}")
-for ln, (n, w, c) in sorted(byline.items(), key=lambda x: -x[1][0])[:topn]:
-    print(f"{ln:32s} inst={n:11d} ({100*n/tot:5.1f}%) stall={100*w/tw:5.1f}%  sass={c}")
+tf = sum(v[3] for v in byline.values()) or 1
+print(f"total warp-inst {tot}  samples {tw}  smem wavefronts {tf}")
+key = 3 if os.environ.get("SORT") == "wf" else 0
+for ln, (n, w, c, f) in sorted(byline.items(), key=lambda x: -x[1][key])[:topn]:
+    print(f"{ln:32s} inst={n:11d} ({100*n/tot:5.1f}%) stall={100*w/tw:5.1f}% wf={f:10d} ({100*f/tf:5.1f}%) sass={c}")
