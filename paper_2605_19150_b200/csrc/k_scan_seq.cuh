@@ -46,7 +46,7 @@ struct Layout {
                             : (size_t)(PD ? 0 : G * row) + (size_t)G * row);
         size_t o = 0;
         ring = o; o = a16(o + (size_t)R * slot);
-        bars = o; o = a16(o + (size_t)R * 8);
+        bars = o; o = a16(o + (size_t)2 * R * 8);   // full[R], then empty[R]
         const int sv = NC == 2 ? 8 : 4;
         x = o; o = a16(o + (size_t)2 * (N + 1) * sv);
         x2 = o; o = a16(o + (AGG ? (size_t)2 * (N + 1) * sv : 0));
@@ -135,6 +135,23 @@ __device__ __forceinline__ void stage_k(const SeqArgs& a, uint8_t* kb, size_t ba
     }
 }
 
+// the N compute threads synchronise on named barrier 1 (the producer warp never joins)
+__device__ __forceinline__ void compute_sync(int n) { asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(fused::smem_u32(b)) : "memory");
+}
+// producer warp (one elected lane): keeps the ring R groups ahead; a slot is refilled
+// once the compute threads released it (empty barrier, one arrival per consumed group)
+template <typename F>
+__device__ __forceinline__ void produce(uint64_t* bars, int R, int ngroups, F&& issue) {
+    if ((threadIdx.x & 31) != 0) return;
+    for (int g = 0; g < ngroups; ++g) {
+        const int slot = g % R;
+        if (g >= R) fused::mbar_wait(bars + R + slot, (uint32_t)((g / R) - 1) & 1u);
+        issue(g, slot);
+    }
+}
+
 template <typename T>
 __device__ __forceinline__ void st_stream(T* p, float v, uint64_t pol) {
     if constexpr (std::is_same<T, float>::value) {
@@ -157,7 +174,7 @@ constexpr int SEQ_G = 8;   // steps per ring slot (one TMA group)
 //   operands of step t+1 (record, trip code, D, b) and k*_{t+2} ; pairwise sum ;
 //   h_t = sum + b_t ; streaming store.
 template <typename T, int NC, bool PD, bool AGG, bool CHECK>
-__global__ void __launch_bounds__(MAXN, 1) k_fwd_seq(SeqArgs a) {
+__global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
     using SV = typename fused::SVal<NC>::type;
     constexpr int G = SEQ_G;
     constexpr int SVB = (int)sizeof(SV);
@@ -180,13 +197,14 @@ __global__ void __launch_bounds__(MAXN, 1) k_fwd_seq(SeqArgs a) {
     const int ngroups = (L + G - 1) / G;
     const uint64_t pol = fused::policy_evict_first();
     {   // one-time tables of head h, and the sequence's k* (zero-padded by 2)
+        const int NT = blockDim.x;
         const uint2* gr = reinterpret_cast<const uint2*>(a.rec) + (size_t)h * K * N;
-        for (int x = i; x < K * N; x += N) rec[x] = __ldg(gr + x);
-        for (int x = i; x < K * NW; x += N) wm[x] = a.wm[(size_t)h * K * NW + x];
+        for (int x = i; x < K * N; x += NT) rec[x] = __ldg(gr + x);
+        for (int x = i; x < K * NW; x += NT) wm[x] = a.wm[(size_t)h * K * NW + x];
         if constexpr (AGG)
-            for (int x = i; x < K * N; x += N) prow[x] = (uint16_t)min((int)__ldg(a.dict_idx + (size_t)h * K * N + x), N - 1);
+            for (int x = i; x < K * N; x += NT) prow[x] = (uint16_t)min((int)__ldg(a.dict_idx + (size_t)h * K * N + x), N - 1);
         if constexpr (PD)
-            for (int x = i; x < K * NC * N; x += N) dk[x] = __ldg(a.diag_dict + (size_t)h * K * NC * N + x);
+            for (int x = i; x < K * NC * N; x += NT) dk[x] = __ldg(a.diag_dict + (size_t)h * K * NC * N + x);
         if (i < 2) kb[L + i] = 0;
     }
     stage_k(a, kb, seq0, L);
@@ -198,7 +216,7 @@ __global__ void __launch_bounds__(MAXN, 1) k_fwd_seq(SeqArgs a) {
             *reinterpret_cast<SV*>(xbc2 + N * SVB) = fused::mk<NC>(0.f, 0.f);
             *reinterpret_cast<SV*>(xbc2 + XB + N * SVB) = fused::mk<NC>(0.f, 0.f);
         }
-        for (int q = 0; q < R; ++q) fused::mbar_init(bars + q, 1);
+        for (int q = 0; q < 2 * R; ++q) fused::mbar_init(bars + q, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -211,8 +229,10 @@ __global__ void __launch_bounds__(MAXN, 1) k_fwd_seq(SeqArgs a) {
         if constexpr (!PD) fused::tma_1d_hint(dst, static_cast<const T*>(a.diag) + (seq0 + t) * row, len * ROWB, bars + slot, pol);
         fused::tma_1d_hint(dst + OFF_B, static_cast<const T*>(a.bias) + (seq0 + t) * row, len * ROWB, bars + slot, pol);
     };
-    if (i == 0)
-        for (int g = 0; g < R && g < ngroups; ++g) issue(g, g);
+    if (i >= N) {   // producer warp
+        produce(bars, R, ngroups, issue);
+        return;
+    }
     float hr = 0.f, hi = 0.f;
     if (a.h0) {
         hr = a.h0[(size_t)s * row + i];
@@ -262,13 +282,13 @@ __global__ void __launch_bounds__(MAXN, 1) k_fwd_seq(SeqArgs a) {
         const int mc = m, kc = k;
         const float bcr = Br, bci = Bi;
         const uint8_t* rpc = sb + r * ROWB;
-        __syncthreads();
+        compute_sync(N);
         SV v[CAP];
 #pragma unroll
         for (int q = 0; q < CAP; ++q) v[q] = *reinterpret_cast<const SV*>(vbc + off[q]);
-        if (r == 0 && i == 0 && g >= 1 && g - 1 + R < ngroups) {   // previous group's slot is free
+        if (r == 0 && i == 0 && g >= 1) {   // every compute thread is done with the previous group's slot
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(g - 1 + R, slot == 0 ? R - 1 : slot - 1);
+            mbar_arrive(bars + R + (slot == 0 ? R - 1 : slot - 1));
         }
         // operands of step t+1 (consumed a step later)
         if (r < G - 1) {
@@ -378,7 +398,7 @@ __global__ void __launch_bounds__(MAXN, 1) k_fwd_seq(SeqArgs a) {
 // read a step earlier) ; refill ; operands of step t-1 (D, e, h from the ring row, P) ;
 // lambda_{t-1} = e_{t-1} + conj(D_t) lp ; dD_t store ; this thread's g_t term -> tile.
 template <typename T, typename TE, int NC, bool PD>
-__global__ void __launch_bounds__(MAXN, 1) k_bwd_seq(SeqArgs a) {
+__global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq(SeqArgs a) {
     using SV = typename fused::SVal<NC>::type;
     constexpr int G = SEQ_G;
     constexpr int SVB = (int)sizeof(SV);
@@ -399,12 +419,12 @@ __global__ void __launch_bounds__(MAXN, 1) k_bwd_seq(SeqArgs a) {
     const int ngroups = (L + G - 1) / G;
     const uint64_t pol = fused::policy_evict_first();
     const TE* ein = static_cast<const TE*>(a.bias);
-    for (int x = j; x < K * N; x += N) prow[x] = (uint16_t)min((int)__ldg(a.dict_idx + (size_t)h * K * N + x), N - 1);
+    for (int x = j; x < K * N; x += blockDim.x) prow[x] = (uint16_t)min((int)__ldg(a.dict_idx + (size_t)h * K * N + x), N - 1);
     if constexpr (PD)
-        for (int x = j; x < K * NC * N; x += N) dk[x] = __ldg(a.diag_dict + (size_t)h * K * NC * N + x);
+        for (int x = j; x < K * NC * N; x += blockDim.x) dk[x] = __ldg(a.diag_dict + (size_t)h * K * NC * N + x);
     stage_k(a, kb, seq0, L);
     if (j == 0) {
-        for (int q = 0; q < R; ++q) fused::mbar_init(bars + q, 1);
+        for (int q = 0; q < 2 * R; ++q) fused::mbar_init(bars + q, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -425,8 +445,10 @@ __global__ void __launch_bounds__(MAXN, 1) k_bwd_seq(SeqArgs a) {
             fused::tma_1d_hint(dst + OFF_H + (size_t)f_off * ROWB, static_cast<const T*>(a.hsaved) + (seq0 + f_first) * row,
                                f_cnt * ROWB, bars + slot, pol);
     };
-    if (j == 0)
-        for (int g = 0; g < R && g < ngroups; ++g) issue(g, g);
+    if (j >= N) {   // producer warp
+        produce(bars, R, ngroups, issue);
+        return;
+    }
     float lr = 0.f, li = 0.f;   // lambda_{L-1} = e_{L-1} + lam_in
     if (ein) {
         lr = ldact_s(ein + (seq0 + L - 1) * row + j);
@@ -493,11 +515,11 @@ __global__ void __launch_bounds__(MAXN, 1) k_bwd_seq(SeqArgs a) {
         *reinterpret_cast<SV*>(lbc + j * SVB) = fused::mk<NC>(lr, li);
         const int pc = p;
         const float Dcr = Dr, Dci = Di, ecr = er, eci = ei, hcr = hr, hci = hi;
-        __syncthreads();
+        compute_sync(N);
         const SV lpv = *reinterpret_cast<const SV*>(lbc + pc * SVB);
-        if (rr == 0 && j == 0 && g >= 1 && g - 1 + R < ngroups) {   // previous group's slot is free
+        if (rr == 0 && j == 0 && g >= 1) {   // every compute thread is done with the previous group's slot
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(g - 1 + R, slot == 0 ? R - 1 : slot - 1);
+            mbar_arrive(bars + R + (slot == 0 ? R - 1 : slot - 1));
         }
         if ((v & 31) == 0 && v > 0 && a.gsel) {   // g_t of the previous 32 steps
             const int q = j & 31, part = j >> 5, NP = N >> 5;
@@ -515,13 +537,13 @@ __global__ void __launch_bounds__(MAXN, 1) k_bwd_seq(SeqArgs a) {
             acc = (a0 + a1) + (a2 + a3);
             float* red = gs + (size_t)32 * (N + 1);
             red[part * 32 + q] = acc;
-            __syncthreads();
+            compute_sync(N);
             if (j < 32) {
                 float tot = 0.f;
                 for (int x = 0; x < NP; ++x) tot += red[x * 32 + j];
                 a.gsel[seq0 + (L - 1 - (v - 32 + j))] = tot;
             }
-            __syncthreads();
+            compute_sync(N);
         }
         // operands of step t-1 (consumed a step later)
         if (inner && rr < G - 1) {
@@ -567,7 +589,7 @@ __global__ void __launch_bounds__(MAXN, 1) k_bwd_seq(SeqArgs a) {
             for (int rr = 0; rr <= t_hi - t_lo; ++rr) step(rr, g, t_hi - rr, t_lo, false);
         }
     }
-    __syncthreads();
+    compute_sync(N);
     if (a.gsel) {   // the last (L % 32 or 32) steps
         const int v0 = ((L - 1) / 32) * 32;
         for (int x = j; x < 32 && v0 + x < L; x += N) {

@@ -574,7 +574,7 @@ pdssm_status fwd_seq(const Geo& g, seq::SeqArgs& sa, uint8_t* rec, uint8_t* wm, 
                     auto kern = seq::k_fwd_seq<T, NC, PD, AGG, CHK>;
                     pdssm_status rr = seq_set_smem((const void*)kern, ly.bytes);
                     if (rr) return rr;
-                    kern<<<(unsigned)g.S, (unsigned)g.N, ly.bytes, st>>>(sa);
+                    kern<<<(unsigned)g.S, (unsigned)g.N + 32, ly.bytes, st>>>(sa);   // + producer warp
                     return cuda_check("fwd_seq");
                 };
                 const bool chk = (g.flags & PDSSM_CHECK_FINITE) != 0;
@@ -601,7 +601,7 @@ pdssm_status bwd_seq(const Geo& g, seq::SeqArgs& sa, cudaStream_t st) {
                 auto kern = seq::k_bwd_seq<T, TEE, NC, PD>;
                 pdssm_status rr = seq_set_smem((const void*)kern, ly.bytes);
                 if (rr) return rr;
-                kern<<<(unsigned)g.S, (unsigned)g.N, ly.bytes, st>>>(sa);
+                kern<<<(unsigned)g.S, (unsigned)g.N + 32, ly.bytes, st>>>(sa);   // + producer warp
                 return cuda_check("bwd_seq");
             });
         });
