@@ -5,11 +5,11 @@ set -x
 mkdir -p gpurun_out
 TAG=${1:-r01}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem --format=csv > gpurun_out/gpu_${TAG}.txt
-ncu --set full --clock-control none --import-source on -k regex:"k_(fwd|bwd)_fused" -s 2 -c 2 \
+ncu --set full --clock-control none --import-source on -k regex:"k_(fwd|bwd)_(fused|seq)" -s 2 -c 2 \
     -o gpurun_out/prof_${TAG} python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-layer > /dev/null 2>&1
 python tools/traffic_json.py gpurun_out/prof_${TAG}.ncu-rep profiles/traffic_latest.json
-python tools/ncu_summary.py gpurun_out/prof_${TAG}.ncu-rep k_fwd_fused > gpurun_out/ncu_summary_fwd_${TAG}.txt 2>&1
-python tools/ncu_summary.py gpurun_out/prof_${TAG}.ncu-rep k_bwd_fused > gpurun_out/ncu_summary_bwd_${TAG}.txt 2>&1
+python tools/ncu_summary.py gpurun_out/prof_${TAG}.ncu-rep k_fwd_ > gpurun_out/ncu_summary_fwd_${TAG}.txt 2>&1
+python tools/ncu_summary.py gpurun_out/prof_${TAG}.ncu-rep k_bwd_ > gpurun_out/ncu_summary_bwd_${TAG}.txt 2>&1
 cp profiles/traffic_latest.json gpurun_out/traffic_${TAG}.json
 timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err
 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches_${TAG}.csv \

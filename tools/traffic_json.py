@@ -16,7 +16,7 @@ scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 res = {}
 for r in rows[2:]:
     name = r[k]
-    key = "scan_fwd" if "k_fwd_fused" in name else "scan_bwd" if "k_bwd_fused" in name else None
+    key = "scan_fwd" if ("k_fwd_fused" in name or "k_fwd_seq" in name) else "scan_bwd" if ("k_bwd_fused" in name or "k_bwd_seq" in name) else None
     if key is None:
         continue
     b = float(r[rd].replace(",", "")) * scale.get(unit_rd, 1) + float(r[wr].replace(",", "")) * scale.get(unit_wr, 1)
