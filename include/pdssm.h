@@ -103,7 +103,11 @@ typedef struct {
 /* ---------------------------------------------------------------------------
  * Sizes
  * ------------------------------------------------------------------------- */
-/* tau actually used for these dims (dims->chunk, or the tuned default). */
+/* tau actually used for these dims (dims->chunk, or the tuned default).  The default is
+ * tau = L (one chunk per sequence) when B*H >= 0.6 x the device's SM count, N is a
+ * multiple of 32 up to 128, K*N <= 4096 and L <= 16384: then the scans run one CTA per
+ * (b, h) sequence (a single barrier per step, no aggregate pass); otherwise tau = 64
+ * (chunked scan with decoupled look-back).  Reading R20: tau is tuning only. */
 int32_t pdssm_default_chunk(const pdssm_dims* dims);
 
 /* Bytes of device workspace `op` (PDSSM_OP_*) needs; 0 on invalid dims.
@@ -117,7 +121,10 @@ size_t pdssm_workspace_bytes(const pdssm_dims* dims, int op);
  *   section 2: beta_bar f32   [S][C][c][N]  chunk local-replay biases    (Alg. 1 B_c)
  *   section 3: carry   f32    [S][C][c][N]  state entering chunk c, carry_0 = h0
  *                                           (Alg. 1 Carry_c)
- * pdssm_chunk_state_offsets writes the 4 byte offsets. */
+ * pdssm_chunk_state_offsets writes the 4 byte offsets.
+ * With a single chunk (C = 1, tau >= L) on the one-CTA-per-sequence path, sections 0-2
+ * (the whole-sequence aggregate) are written only under PDSSM_EXPORT_MAPS -- no later
+ * chunk consumes them -- and section 3 always (carry_0 = h0). */
 size_t pdssm_chunk_state_bytes(const pdssm_dims* dims);
 pdssm_status pdssm_chunk_state_offsets(const pdssm_dims* dims, size_t offsets[4]);
 
