@@ -105,7 +105,7 @@ typedef struct {
  * ------------------------------------------------------------------------- */
 /* tau actually used for these dims (dims->chunk, or the tuned default).  The default is
  * tau = L (one chunk per sequence) when B*H >= 0.6 x the device's SM count, N is a
- * multiple of 32 up to 128, K*N <= 4096 and L <= 16384: then the scans run one CTA per
+ * multiple of 32 up to 128, K*N <= 8192 and L <= 16384: then the scans run one CTA per
  * (b, h) sequence (a single barrier per step, no aggregate pass); otherwise tau = 64
  * (chunked scan with decoupled look-back).  Reading R20: tau is tuning only. */
 int32_t pdssm_default_chunk(const pdssm_dims* dims);

@@ -1,6 +1,7 @@
 // C ABI of libpdssm.so (declarations and contracts: include/pdssm.h).
 // Validation is synchronous and happens before any CUDA call; every kernel is
 // enqueued on the caller's stream; nothing is allocated.
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -443,13 +444,17 @@ constexpr size_t kSeqSmemBudget = 200 * 1024;
 constexpr int kSeqG = seq::SEQ_G;
 
 // ring depth R for this shape (0: the layout does not fit)
+// ring depth R for this shape (0: the layout does not fit).  When there are more
+// sequences than SMs, the budget is split so that ceil(S / #SMs) CTAs (up to 4) fit per SM.
 int seq_ring(const Geo& g, bool bwd, bool agg, size_t esz_e) {
     const int ngroups = (int)ceil_div(g.L, kSeqG);
+    const int64_t per_sm = std::min<int64_t>(std::max<int64_t>(ceil_div(g.S, num_sms_dev()), 1), 4);
+    const size_t budget = std::min<size_t>(kSeqSmemBudget, (size_t)(226 * 1024) / (size_t)per_sm - 1024);
     int best = 0;
     for (int R = 2; R <= 16 && R <= ngroups + 1; ++R) {
         seq::Layout ly((int)g.N, (int)g.K, R, kSeqG, g.nc, (int)g.act, (int)esz_e, g.diag_mode == PDSSM_DIAG_PER_DICT, agg, bwd,
                        (int)g.L);
-        if (ly.bytes <= kSeqSmemBudget) best = R;
+        if (ly.bytes <= budget) best = R;
     }
     if (best == 0 && ngroups <= 1) best = 2;
     return best;
@@ -464,6 +469,7 @@ bool seq_applicable(const Geo& g, std::initializer_list<const void*> ptrs) {
 }
 
 pdssm_status seq_set_smem(const void* f, size_t bytes) {
+    cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return fail(PDSSM_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
     return PDSSM_OK;
