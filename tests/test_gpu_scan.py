@@ -353,3 +353,55 @@ def test_seq_path_is_default_for_full_batches(P, monkeypatch):
     assert P.default_chunk(dims) == 2048
     dims = P.make_dims(1, 2, 2048, 128, 32, c=2)
     assert P.default_chunk(dims) == 64
+
+
+SEQ_NOMAPS_CASES = [
+    # B, H, L, N, K, c   (single chunk, no EXPORT_MAPS: the production forward without aggregate chains)
+    (2, 2, 300, 128, 32, 2),
+    (1, 3, 129, 64, 16, 1),
+    (2, 1, 77, 32, 5, 2),
+    (1, 1, 64, 32, 4, 2),
+    (1, 2, 2048, 128, 32, 2),
+]
+
+
+@pytest.mark.parametrize("case", SEQ_NOMAPS_CASES, ids=[str(c) for c in SEQ_NOMAPS_CASES])
+@pytest.mark.parametrize("bf16", [False, True], ids=["f32", "bf16"])
+def test_seq_no_maps_parity(P, case, bf16, monkeypatch):
+    """Single-chunk scan as the bench runs it (no EXPORT_MAPS): states and the backward against the oracle."""
+    monkeypatch.setenv("PDSSM_PATH", "seq")
+    B, H, L, N, K, c = case
+    inp = synth.scan_inputs(B, H, L, N, K, c, seed=L + 3 * N, h0=True, dh=True, bf16=bf16)
+    d = to_dev(inp, bf16)
+    f = P.scan_fwd(d["kstar"], d["dict_idx"], d["diag"], d["bias"], h0=d["h0"])
+    assert f["tau"] == L
+    db, dD, g, dh0 = P.scan_bwd(d["kstar"], d["dict_idx"], d["diag"], f["h"], f["chunk_state"], f["dims"],
+                                dh=d["dh"], h0=d["h0"])
+    torch.cuda.synchronize()
+    Pm = O.gather_P(inp["dict_idx"], inp["kstar"])
+    Dz, bz, h0z, e = (O.planes_to_complex(inp[k]) for k in ("diag", "bias", "h0", "dh"))
+    h = O.scan_forward(Pm, Dz, bz, h0z)
+    tol = TOL["bf16" if bf16 else "f32"]
+    assert rel(cpx(f["h"]), h) <= tol
+    db_r, dD_r, g_r, dh0_r = O.scan_backward(Pm, Dz, h, e, h0z)
+    assert rel(cpx(db), db_r) <= tol
+    assert rel(cpx(dD), dD_r) <= (tol if not bf16 else 3e-2)
+    assert rel(g.cpu().numpy(), g_r) <= (tol if not bf16 else 3e-2)
+    # run-to-run bitwise determinism
+    f2 = P.scan_fwd(d["kstar"], d["dict_idx"], d["diag"], d["bias"], h0=d["h0"])
+    assert torch.equal(f["h"], f2["h"])
+
+
+def test_seq_no_maps_per_dict_and_overflow(P, monkeypatch):
+    monkeypatch.setenv("PDSSM_PATH", "seq")
+    B, H, L, N, K, c = 2, 2, 257, 64, 6, 2
+    inp = synth.scan_inputs(B, H, L, N, K, c, seed=91, h0=True, dh=True, per_dict=True)
+    inp["dict_idx"][0, 1, :] = 5
+    d = to_dev(inp, False)
+    d["diag"] = torch.from_numpy(inp["diag"]).cuda()
+    f = P.scan_fwd(d["kstar"], d["dict_idx"], d["diag"], d["bias"], h0=d["h0"], per_dict=True)
+    torch.cuda.synchronize()
+    Pm = O.gather_P(inp["dict_idx"], inp["kstar"])
+    Dz = O.gather_D_per_dict(O.planes_to_complex(inp["diag"]), inp["kstar"])
+    h = O.scan_forward(Pm, Dz, O.planes_to_complex(inp["bias"]), O.planes_to_complex(inp["h0"]))
+    assert rel(cpx(f["h"]), h) <= 1e-4
