@@ -152,6 +152,32 @@ __device__ __forceinline__ void produce(uint64_t* bars, int R, int ngroups, F&& 
     }
 }
 
+// shared-space addresses base + sv * byte_q(w), q = 0..3, pinned before whatever volatile
+// asm follows (the barrier): the compiler may not sink them onto the post-barrier path
+__device__ __forceinline__ void gather_addr4(uint32_t w, uint32_t base, uint32_t sv, uint32_t (&a)[4]) {
+    asm volatile(
+        "{\n\t.reg .b32 t0, t1, t2, t3;\n\t"
+        "prmt.b32 t0, %4, 0, 0x4440;\n\t"
+        "prmt.b32 t1, %4, 0, 0x4441;\n\t"
+        "prmt.b32 t2, %4, 0, 0x4442;\n\t"
+        "prmt.b32 t3, %4, 0, 0x4443;\n\t"
+        "mad.lo.u32 %0, t0, %6, %5;\n\t"
+        "mad.lo.u32 %1, t1, %6, %5;\n\t"
+        "mad.lo.u32 %2, t2, %6, %5;\n\t"
+        "mad.lo.u32 %3, t3, %6, %5;\n\t}"
+        : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3])
+        : "r"(w), "r"(base), "r"(sv));
+}
+template <int NC>
+__device__ __forceinline__ void lds_sv(uint32_t addr, float& re, float& im) {
+    if constexpr (NC == 2) {
+        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(re), "=f"(im) : "r"(addr));
+    } else {
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(re) : "r"(addr));
+        im = 0.f;
+    }
+}
+
 template <typename T>
 __device__ __forceinline__ void st_stream(T* p, float v, uint64_t pol) {
     if constexpr (std::is_same<T, float>::value) {
@@ -273,6 +299,18 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
         uint32_t off[CAP];
 #pragma unroll
         for (int q = 0; q < CAP; ++q) off[q] = __byte_perm(q < 4 ? rc.x : rc.y, 0u, 0x4440u + (uint32_t)(q & 3)) * SVB;
+        uint32_t ga[CAP];   // shared addresses of this step's gather, computed before the barrier
+        {
+            uint32_t lo[4], hi4[4];
+            const uint32_t vb_s = fused::smem_u32(vbc);
+            gather_addr4(rc.x, vb_s, SVB, lo);
+            gather_addr4(rc.y, vb_s, SVB, hi4);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                ga[q] = lo[q];
+                ga[4 + q] = hi4[q];
+            }
+        }
         if constexpr (CHECK) {
             check_cpx(cpx{Dr, Di}, a.flags);
             check_cpx(cpx{Br, Bi}, a.flags);
@@ -285,7 +323,11 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
         compute_sync(N);
         SV v[CAP];
 #pragma unroll
-        for (int q = 0; q < CAP; ++q) v[q] = *reinterpret_cast<const SV*>(vbc + off[q]);
+        for (int q = 0; q < CAP; ++q) {
+            float re, im;
+            lds_sv<NC>(ga[q], re, im);
+            v[q] = fused::mk<NC>(re, im);
+        }
         if (r == 0 && i == 0 && g >= 1) {   // every compute thread is done with the previous group's slot
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_arrive(bars + R + (slot == 0 ? R - 1 : slot - 1));
@@ -513,10 +555,16 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq(SeqArgs a) {
         dbp -= row;
         char* lbc = xbc + (t & 1) * (N * SVB);
         *reinterpret_cast<SV*>(lbc + j * SVB) = fused::mk<NC>(lr, li);
-        const int pc = p;
         const float Dcr = Dr, Dci = Di, ecr = er, eci = ei, hcr = hr, hci = hi;
+        uint32_t la;   // shared address of lambda_t[P_t[j]], computed before the barrier
+        asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(la) : "r"(p), "r"(SVB), "r"(fused::smem_u32(lbc)));
         compute_sync(N);
-        const SV lpv = *reinterpret_cast<const SV*>(lbc + pc * SVB);
+        SV lpv;
+        {
+            float re, im;
+            lds_sv<NC>(la, re, im);
+            lpv = fused::mk<NC>(re, im);
+        }
         if (rr == 0 && j == 0 && g >= 1) {   // every compute thread is done with the previous group's slot
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_arrive(bars + R + (slot == 0 ? R - 1 : slot - 1));
