@@ -25,7 +25,8 @@ namespace tc {
 
 constexpr int BM = 128;
 constexpr int ROWB = 128;   // K bytes per ring slot row = one 128-byte swizzle atom
-constexpr int THREADS = 256;
+constexpr int THREADS = 512;   // 0 TMA, 1 MMA, 2 TMEM, 4-7 epilogue, 8-15 tf32 split
+constexpr int NCONV = 8;       // converter warps
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -370,13 +371,22 @@ template <typename T, int STAGES, bool SPLIT>
 struct Smem {
     __host__ __device__ static constexpr size_t slot(int bn) { return (size_t)(BM + bn) * ROWB; }   // A rows then B rows
     __host__ __device__ static constexpr size_t ring(int bn) { return (size_t)STAGES * slot(bn) * (SPLIT ? 2 : 1); }
-    __host__ __device__ static constexpr size_t bytes(int bn) { return 1024 + ring(bn) + 8 * (3 * STAGES + 1) + 16; }
+    __host__ __device__ static constexpr size_t bytes(int bn) { return 1024 + ring(bn) + 8 * (3 * STAGES + 4) + 16; }
+};
+
+// Persistent: grid = min(#tiles, #SMs); CTA c takes tiles c, c + grid, ...  Tiles are
+// numbered with the column tile fastest (consecutive tiles share the A rows in L2).  TMEM
+// holds two accumulators (2 x 256 columns), so the epilogue of tile j overlaps the main loop
+// of tile j+1 (tmem_full / tmem_empty barriers).  Warps: 0 TMA, 1 MMA, 2 TMEM allocator,
+// 4-7 epilogue, 8-15 tf32 split (SPLIT only).
+struct TileGrid {
+    int gx, gy, gz;   // tiles along the A rows (x), the output columns (y), the z batch
 };
 
 template <typename T, int STAGES, bool SPLIT, class Epi>
 __global__ void __launch_bounds__(THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, int nk, int bn, TileMap tm,
-              Epi epi) {
+              TileGrid tg, Epi epi) {
     using SM = Smem<T, STAGES, SPLIT>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -386,23 +396,27 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::ring(bn));
     uint64_t* conv = full + STAGES;
     uint64_t* empty = conv + STAGES;
-    uint64_t* tfull = empty + STAGES;
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 1);
+    uint64_t* tfull = empty + STAGES;     // [2]
+    uint64_t* tempty = tfull + 2;         // [2]
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t ncols = (uint32_t)tmem_cols(bn);
+    constexpr uint32_t NCOLS = 512;       // two accumulators of up to 256 columns
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(full + s, 1);
-            mbar_init(conv + s, 4);   // one arrival per converter warp
+            mbar_init(conv + s, NCONV);   // one arrival per converter warp
             mbar_init(empty + s, 1);
         }
-        mbar_init(tfull, 1);
+        for (int q = 0; q < 2; ++q) {
+            mbar_init(tfull + q, 1);
+            mbar_init(tempty + q, 4);  // one arrival per epilogue warp
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mA)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mB)) : "memory");
     }
     if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)), "r"(ncols)
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)), "r"(NCOLS)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -410,94 +424,127 @@ __global__ void __launch_bounds__(THREADS, 1)
     __syncthreads();
     fence_after();
     const uint32_t tmem = *tslot;
-    const int n0 = blockIdx.y * bn;
-    int64_t m0;
-    int z, brow;
-    if (tm.mode == 1) {
-        z = blockIdx.x / tm.tiles;
-        m0 = (int64_t)(blockIdx.x - z * tm.tiles) * BM;
-        brow = (z % tm.zmod) * tm.brows + n0;
-    } else if (tm.mode == 2) {
-        z = blockIdx.z;
-        m0 = (int64_t)blockIdx.x * BM;
-        brow = z * tm.brows + n0;
-    } else {
-        z = 0;
-        m0 = (int64_t)blockIdx.x * BM;
-        brow = n0;
-    }
+    const int ntiles = tg.gx * tg.gy * tg.gz;
+    // tile id -> (A row m0, output column n0, z, weight row brow)
+    auto coords = [&](int id, int64_t& m0, int& n0, int& z, int& brow) {
+        const int by = id % tg.gy;
+        const int rest = id / tg.gy;
+        const int bx = rest % tg.gx;
+        const int bz = rest / tg.gx;
+        n0 = by * bn;
+        if (tm.mode == 1) {
+            z = bx / tm.tiles;
+            m0 = (int64_t)(bx - z * tm.tiles) * BM;
+            brow = (z % tm.zmod) * tm.brows + n0;
+        } else if (tm.mode == 2) {
+            z = bz;
+            m0 = (int64_t)bx * BM;
+            brow = z * tm.brows + n0;
+        } else {
+            z = 0;
+            m0 = (int64_t)bx * BM;
+            brow = n0;
+        }
+    };
     constexpr int EK = ROWB / (int)sizeof(T);   // elements of K per slab row
     if (warp == 0) {
         if (lane == 0) {
             const uint32_t bytes = (uint32_t)SLOT;
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % STAGES;
-                if (kb >= STAGES) mbar_wait(empty + s, (uint32_t)((kb / STAGES) + 1) & 1u);
-                mbar_expect_tx(full + s, bytes);
-                if (tm.mode == 1) tma_3d(hi(s), &mA, kb * EK, (int)m0, z, full + s);
-                else if (tm.mode == 2) tma_3d(hi(s), &mA, kb * EK, z, (int)m0, full + s);
-                else tma_2d(hi(s), &mA, kb * EK, (int)m0, full + s);
-                tma_2d(hi(s) + (size_t)BM * ROWB, &mB, kb * EK, brow, full + s);
+            int kg = 0;
+            for (int id = blockIdx.x; id < ntiles; id += gridDim.x) {
+                int64_t m0;
+                int n0, z, brow;
+                coords(id, m0, n0, z, brow);
+                for (int kb = 0; kb < nk; ++kb, ++kg) {
+                    const int s = kg % STAGES;
+                    if (kg >= STAGES) mbar_wait(empty + s, (uint32_t)((kg / STAGES) + 1) & 1u);
+                    mbar_expect_tx(full + s, bytes);
+                    if (tm.mode == 1) tma_3d(hi(s), &mA, kb * EK, (int)m0, z, full + s);
+                    else if (tm.mode == 2) tma_3d(hi(s), &mA, kb * EK, z, (int)m0, full + s);
+                    else tma_2d(hi(s), &mA, kb * EK, (int)m0, full + s);
+                    tma_2d(hi(s) + (size_t)BM * ROWB, &mB, kb * EK, brow, full + s);
+                }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            const uint32_t id = idesc(Kind<T>::FMT, bn);
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % STAGES;
-                mbar_wait((SPLIT ? conv : full) + s, (uint32_t)(kb / STAGES) & 1u);
+            const uint32_t id_ = idesc(Kind<T>::FMT, bn);
+            int kg = 0, j = 0;
+            for (int id = blockIdx.x; id < ntiles; id += gridDim.x, ++j) {
+                const int acc = j & 1;
+                if (j >= 2) mbar_wait(tempty + acc, (uint32_t)((j / 2) - 1) & 1u);   // epilogue drained it
                 fence_after();
-                const uint64_t ah = sdesc(su32(hi(s))), bh = sdesc(su32(hi(s) + (size_t)BM * ROWB));
-                const uint64_t al = sdesc(su32(lo(s))), bl = sdesc(su32(lo(s) + (size_t)BM * ROWB));
+                const uint32_t tacc = tmem + (uint32_t)(acc * 256);
+                for (int kb = 0; kb < nk; ++kb, ++kg) {
+                    const int s = kg % STAGES;
+                    mbar_wait((SPLIT ? conv : full) + s, (uint32_t)(kg / STAGES) & 1u);
+                    fence_after();
+                    const uint64_t ah = sdesc(su32(hi(s))), bh = sdesc(su32(hi(s) + (size_t)BM * ROWB));
+                    const uint64_t al = sdesc(su32(lo(s))), bl = sdesc(su32(lo(s) + (size_t)BM * ROWB));
 #pragma unroll
-                for (int k = 0; k < ROWB / 32; ++k) {   // 32 bytes of K per instruction
-                    const uint32_t acc0 = (kb | k) != 0;
-                    if constexpr (SPLIT) {
-                        Kind<T>::mma(tmem, al + 2 * k, bh + 2 * k, id, acc0);
-                        Kind<T>::mma(tmem, ah + 2 * k, bl + 2 * k, id, 1u);
-                        Kind<T>::mma(tmem, ah + 2 * k, bh + 2 * k, id, 1u);
-                    } else {
-                        Kind<T>::mma(tmem, ah + 2 * k, bh + 2 * k, id, acc0);
+                    for (int k = 0; k < ROWB / 32; ++k) {   // 32 bytes of K per instruction
+                        const uint32_t acc0 = (kb | k) != 0;
+                        if constexpr (SPLIT) {
+                            Kind<T>::mma(tacc, al + 2 * k, bh + 2 * k, id_, acc0);
+                            Kind<T>::mma(tacc, ah + 2 * k, bl + 2 * k, id_, 1u);
+                            Kind<T>::mma(tacc, ah + 2 * k, bh + 2 * k, id_, 1u);
+                        } else {
+                            Kind<T>::mma(tacc, ah + 2 * k, bh + 2 * k, id_, acc0);
+                        }
                     }
+                    commit(empty + s);
                 }
-                commit(empty + s);
+                commit(tfull + acc);
             }
-            commit(tfull);
         }
         __syncwarp();
-    } else if (warp >= 4) {
+    } else if (warp >= 4 && warp < 8) {
+        const int q = warp - 4;
+        int j = 0;
+        for (int id = blockIdx.x; id < ntiles; id += gridDim.x, ++j) {
+            const int acc = j & 1;
+            int64_t m0;
+            int n0, z, brow;
+            coords(id, m0, n0, z, brow);
+            mbar_wait(tfull + acc, (uint32_t)(j / 2) & 1u);
+            fence_after();
+            epi(tmem + (uint32_t)(acc * 256) + ((uint32_t)(32 * q) << 16), m0 + 32 * q + lane, n0, bn, z);
+            fence_before();
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(tempty + acc)) : "memory");
+        }
+    } else if (warp >= 8) {
         if constexpr (SPLIT) {
             // converters: split every landed slab (the producer reused slot s only after the
             // MMAs of its previous round completed, and full[s] completes after that reuse)
-            const int ct = threadIdx.x - 128;
+            const int ct = threadIdx.x - 256;
             const int nchunks = (BM + bn) * (ROWB / 16);
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % STAGES;
-                mbar_wait(full + s, (uint32_t)(kb / STAGES) & 1u);
-                float4* ph = reinterpret_cast<float4*>(hi(s));
-                float4* pl = reinterpret_cast<float4*>(lo(s));
-                for (int i = ct; i < nchunks; i += 128) {
-                    const float4 a = ph[i];
-                    const uint32_t h0 = tf32_rna(a.x), h1 = tf32_rna(a.y), h2 = tf32_rna(a.z), h3 = tf32_rna(a.w);
-                    ph[i] = make_float4(__uint_as_float(h0), __uint_as_float(h1), __uint_as_float(h2), __uint_as_float(h3));
-                    pl[i] = make_float4(a.x - __uint_as_float(h0), a.y - __uint_as_float(h1), a.z - __uint_as_float(h2),
-                                        a.w - __uint_as_float(h3));
+            int kg = 0;
+            for (int id = blockIdx.x; id < ntiles; id += gridDim.x) {
+                for (int kb = 0; kb < nk; ++kb, ++kg) {
+                    const int s = kg % STAGES;
+                    mbar_wait(full + s, (uint32_t)(kg / STAGES) & 1u);
+                    float4* ph = reinterpret_cast<float4*>(hi(s));
+                    float4* pl = reinterpret_cast<float4*>(lo(s));
+                    for (int i = ct; i < nchunks; i += NCONV * 32) {
+                        const float4 a = ph[i];
+                        const uint32_t h0 = tf32_rna(a.x), h1 = tf32_rna(a.y), h2 = tf32_rna(a.z), h3 = tf32_rna(a.w);
+                        ph[i] = make_float4(__uint_as_float(h0), __uint_as_float(h1), __uint_as_float(h2), __uint_as_float(h3));
+                        pl[i] = make_float4(a.x - __uint_as_float(h0), a.y - __uint_as_float(h1), a.z - __uint_as_float(h2),
+                                            a.w - __uint_as_float(h3));
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> MMA reads
+                    __syncwarp();
+                    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(conv + s)) : "memory");
                 }
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> MMA reads
-                __syncwarp();
-                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(conv + s)) : "memory");
             }
         }
-        mbar_wait(tfull, 0);
-        fence_after();
-        const int q = warp - 4;
-        epi(tmem + ((uint32_t)(32 * q) << 16), m0 + 32 * q + lane, n0, bn, z);
     }
     fence_before();
     __syncthreads();
     if (warp == 2) {
         fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(NCOLS) : "memory");
     }
 }
 

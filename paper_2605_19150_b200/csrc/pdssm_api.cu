@@ -334,7 +334,10 @@ pdssm_status launch_tc_maps(const CUtensorMap& mA, const CUtensorMap& mB, int64_
     std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
     if (attr_err != cudaSuccess) return fail(PDSSM_ERR_CUDA, "%s: cudaFuncSetAttribute: %s", what, cudaGetErrorString(attr_err));
     const int nk = (int)ceil_div(kdim * (int64_t)sizeof(T), tc::ROWB);
-    kern<<<grid, tc::THREADS, SM::bytes(bn), st>>>(mA, mB, nk, bn, tm, epi);
+    const tc::TileGrid tg{(int)grid.x, (int)grid.y, (int)grid.z};
+    const int ntiles = tg.gx * tg.gy * tg.gz;
+    const int nctas = ntiles < num_sms_dev() ? ntiles : num_sms_dev();   // persistent
+    kern<<<nctas, tc::THREADS, SM::bytes(bn), st>>>(mA, mB, nk, bn, tm, tg, epi);
     return cuda_check(what);
 }
 
