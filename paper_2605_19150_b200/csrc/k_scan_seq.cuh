@@ -329,7 +329,6 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
             v[q] = fused::mk<NC>(re, im);
         }
         if (r == 0 && i == 0 && g >= 1) {   // every compute thread is done with the previous group's slot
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_arrive(bars + R + (slot == 0 ? R - 1 : slot - 1));
         }
         // operands of step t+1 (consumed a step later)
@@ -566,7 +565,6 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq(SeqArgs a) {
             lpv = fused::mk<NC>(re, im);
         }
         if (rr == 0 && j == 0 && g >= 1) {   // every compute thread is done with the previous group's slot
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_arrive(bars + R + (slot == 0 ? R - 1 : slot - 1));
         }
         if ((v & 31) == 0 && v > 0 && a.gsel) {   // g_t of the previous 32 steps
