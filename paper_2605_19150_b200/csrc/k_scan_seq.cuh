@@ -245,7 +245,10 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
         for (int q = 0; q < 2 * R; ++q) fused::mbar_init(bars + q, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    __syncthreads();
+    // does any entry of this head need the CSR plan?  (selects the loop variant once)
+    int my_ovf = 0;
+    for (int x = i; x < K * NW; x += blockDim.x) my_ovf |= a.wm[(size_t)h * K * NW + x] == WM_OVF;
+    const bool any_ovf = __syncthreads_or(my_ovf) != 0;
     const int ROWB = (int)(row * sizeof(T));
     const int OFF_B = PD ? 0 : G * ROWB;
     auto issue = [&](int g, int slot) {   // thread 0: rows of steps [gG, gG+len) -> slot
@@ -293,7 +296,8 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
     rc = rec[(size_t)k * N + i];
     m = wm[k * NW + w];
     load_ops(sb, k);
-    auto step = [&](const int r, const int g, const int t) {
+    auto step = [&](const int r, const int g, const int t, auto ovfv) {
+        constexpr bool OVF = decltype(ovfv)::value;
         char* vbc = xbc + (t & 1) * XB;
         char* vbc2 = xbc2 + (t & 1) * XB;
         uint32_t off[CAP];
@@ -364,7 +368,7 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
             for (int q = 0; q < CAP; ++q) v[q] = *reinterpret_cast<const SV*>(vbc2 + off[q]);
             sum8(v, cr, ci);
         }
-        if (mc == WM_OVF) {   // preimage longer than CAP: CSR plan (rare, warp-uniform)
+        if (OVF && mc == WM_OVF) {   // preimage longer than CAP: CSR plan (rare, warp-uniform)
             ar = ai = cr = ci = 0.f;
             const SV* vb = reinterpret_cast<const SV*>(vbc);
             const SV* vb2 = reinterpret_cast<const SV*>(vbc2);
@@ -404,15 +408,19 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
             pi = prow[(size_t)kc * N + pi];
         }
     };
-    for (int g = 0; g < ngroups; ++g) {
-        const int t0 = g * G;
-        if (t0 + G <= L) {
+    auto run = [&](auto ovfv) {
+        for (int g = 0; g < ngroups; ++g) {
+            const int t0 = g * G;
+            if (t0 + G <= L) {
 #pragma unroll
-            for (int r = 0; r < G; ++r) step(r, g, t0 + r);
-        } else {
-            for (int r = 0; r < L - t0; ++r) step(r, g, t0 + r);
+                for (int r = 0; r < G; ++r) step(r, g, t0 + r, ovfv);
+            } else {
+                for (int r = 0; r < L - t0; ++r) step(r, g, t0 + r, ovfv);
+            }
         }
-    }
+    };
+    if (any_ovf) run(std::true_type{});
+    else run(std::false_type{});
     // chunk_state of the single chunk: carry_0 = h0; aggregate (pi_bar, d_bar, beta_bar)
     {
         a.cs.carry[(size_t)s * row + i] = a.h0 ? a.h0[(size_t)s * row + i] : 0.f;
