@@ -575,7 +575,8 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq(SeqArgs a) {
         if (rr == 0 && j == 0 && g >= 1) {   // every compute thread is done with the previous group's slot
             mbar_arrive(bars + R + (slot == 0 ? R - 1 : slot - 1));
         }
-        if ((v & 31) == 0 && v > 0 && a.gsel) {   // g_t of the previous 32 steps
+        // g_t of the previous 32 steps (v = 8 g + rr, so only the first step of every 4th group)
+        if (rr == 0 && (g & 3) == 0 && g > 0 && a.gsel) {
             const int q = j & 31, part = j >> 5, NP = N >> 5;
             const float* gr = gs + (size_t)q * (N + 1);
             float acc = 0.f;
