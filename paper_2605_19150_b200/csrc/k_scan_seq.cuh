@@ -199,13 +199,15 @@ constexpr int SEQ_G = 8;   // steps per ring slot (one TMA group)
 //   8 gather loads (zero slot past the in-degree: branch-free) ; refill (group start) ;
 //   operands of step t+1 (record, trip code, D, b) and k*_{t+2} ; pairwise sum ;
 //   h_t = sum + b_t ; streaming store.
-template <typename T, int NC, bool PD, bool AGG, bool CHECK>
+// NN: the state count as a compile-time constant (0 = runtime a.N): every row offset, ring
+// position and exchange address of an unrolled group becomes an immediate.
+template <typename T, int NC, bool PD, bool AGG, bool CHECK, int NN>
 __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
     using SV = typename fused::SVal<NC>::type;
     constexpr int G = SEQ_G;
     constexpr int SVB = (int)sizeof(SV);
     extern __shared__ __align__(128) uint8_t smem[];
-    const int N = a.N, K = a.K, L = a.L, R = a.R;
+    const int N = NN ? NN : a.N, K = a.K, L = a.L, R = a.R;
     const int i = threadIdx.x, w = i >> 5, NW = N >> 5;
     const int s = blockIdx.x, h = s % a.H;
     const Layout Ly(N, K, R, G, NC, (int)sizeof(T), (int)sizeof(T), PD, AGG, false, L);
@@ -446,13 +448,13 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
 // full group): db_t store ; lambda_t -> STS ; BARRIER ; lp = lambda_t[P_t[j]] (P_t[j]
 // read a step earlier) ; refill ; operands of step t-1 (D, e, h from the ring row, P) ;
 // lambda_{t-1} = e_{t-1} + conj(D_t) lp ; dD_t store ; this thread's g_t term -> tile.
-template <typename T, typename TE, int NC, bool PD>
+template <typename T, typename TE, int NC, bool PD, int NN>
 __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq(SeqArgs a) {
     using SV = typename fused::SVal<NC>::type;
     constexpr int G = SEQ_G;
     constexpr int SVB = (int)sizeof(SV);
     extern __shared__ __align__(128) uint8_t smem[];
-    const int N = a.N, K = a.K, L = a.L, R = a.R;
+    const int N = NN ? NN : a.N, K = a.K, L = a.L, R = a.R;
     const int j = threadIdx.x;
     const int s = blockIdx.x, h = s % a.H;
     const Layout Ly(N, K, R, G, NC, (int)sizeof(T), (int)sizeof(TE), PD, false, true, L);

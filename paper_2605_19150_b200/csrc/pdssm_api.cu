@@ -580,7 +580,12 @@ pdssm_status fwd_seq(const Geo& g, seq::SeqArgs& sa, uint8_t* rec, uint8_t* wm, 
                     constexpr bool CHK = decltype(chkv)::value;
                     seq::Layout ly((int)g.N, (int)g.K, sa.R, sa.G, NC, (int)sizeof(T), (int)sizeof(T), PD, AGG, false,
                                    (int)g.L);
-                    auto kern = seq::k_fwd_seq<T, NC, PD, AGG, CHK>;
+                    // compile-time N for the production variants (no maps, no checks)
+                    auto kern = seq::k_fwd_seq<T, NC, PD, AGG, CHK, 0>;
+                    if constexpr (!AGG && !CHK) {
+                        if (g.N == 128) kern = seq::k_fwd_seq<T, NC, PD, false, false, 128>;
+                        else if (g.N == 64) kern = seq::k_fwd_seq<T, NC, PD, false, false, 64>;
+                    }
                     pdssm_status rr = seq_set_smem((const void*)kern, ly.bytes);
                     if (rr) return rr;
                     kern<<<(unsigned)g.S, (unsigned)g.N + 32, ly.bytes, st>>>(sa);   // + producer warp
@@ -607,7 +612,9 @@ pdssm_status bwd_seq(const Geo& g, seq::SeqArgs& sa, cudaStream_t st) {
                 constexpr bool PD = decltype(pdv)::value;
                 seq::Layout ly((int)g.N, (int)g.K, sa.R, sa.G, NC, (int)sizeof(T), (int)sizeof(TEE), PD, false, true,
                                (int)g.L);
-                auto kern = seq::k_bwd_seq<T, TEE, NC, PD>;
+                auto kern = g.N == 128 ? seq::k_bwd_seq<T, TEE, NC, PD, 128>
+                            : g.N == 64    ? seq::k_bwd_seq<T, TEE, NC, PD, 64>
+                                           : seq::k_bwd_seq<T, TEE, NC, PD, 0>;
                 pdssm_status rr = seq_set_smem((const void*)kern, ly.bytes);
                 if (rr) return rr;
                 kern<<<(unsigned)g.S, (unsigned)g.N + 32, ly.bytes, st>>>(sa);   // + producer warp
