@@ -31,6 +31,7 @@ __all__ = [
     "exclusive_prefix_maps", "scan_chunked",
     "scan_backward", "scan_backward_chunked",
     "segment_summary", "compose_summaries",
+    "softmax_T", "selector_grad", "dictionary_outer", "dictionary_grad",
 ]
 
 
@@ -440,3 +441,81 @@ def compose_summaries(pis, ds, betas, rank, h0=None):
                 m[bb, hh] = np.asarray(pis[g], np.int64)[bb, hh][m[bb, hh]]
         cur = nxt + np.asarray(betas[g])
     return cur, m
+
+
+# ----------------------------------------------------------------------------
+# NEXT-1: Prop. 2 surrogate gradients (derivation App. C
+# PAPER.md:814-841).  Slope-annealed straight-through estimation: each hardmax of
+# the forward is a tempered softmax in the backward.
+# ----------------------------------------------------------------------------
+def softmax_T(z, T, axis=-1):
+    """Tempered softmax softmax_T(z) = exp(z / T) / sum exp(z / T) along ``axis``
+    ("softmax_tau ... the tempered softmax function", PAPER.md:210)."""
+    z = np.asarray(z, dtype=np.float64) / float(T)
+    z = z - z.max(axis=axis, keepdims=True)
+    ez = np.exp(z)
+    return ez / ez.sum(axis=axis, keepdims=True)
+
+
+def selector_grad(logits, kstar, g, T):
+    """Selector surrogate gradient, Prop. 2 second expression (App. C
+    Eq. grad_k):
+
+        dl/dk(u_t) = (dl/dx_t (P_t D_t x_{t-1})^T) dsoftmax_T(k(u_t))/dk(u_t)
+
+    The first factor, contracted with the activated entry only ("uses the activated
+    forward state"), is the scalar g_t of scan_backward (reading R14):
+    dl/dv_t = g_t e_{k*}.  Through the softmax Jacobian ds_j/dz_k = s_j (delta_jk - s_k) / T:
+
+        dlogits[b,h,t,k] = g_t s_{k*} (delta_{k,k*} - s_k) / T,   s = softmax_T(logits[b,h,t,:])
+
+    logits [B,H,L,K], kstar [B,H,L], g [B,H,L] -> [B,H,L,K] float64."""
+    logits = np.asarray(logits, dtype=np.float64)
+    K = logits.shape[-1]
+    s = softmax_T(logits, T, axis=-1)
+    ks = np.asarray(kstar, dtype=np.int64)[..., None]
+    s_k = np.take_along_axis(s, ks, axis=-1)
+    onehot = (np.arange(K) == ks).astype(np.float64)
+    return np.asarray(g, dtype=np.float64)[..., None] * s_k * (onehot - s) / float(T)
+
+
+def dictionary_outer(kstar, lam, D, h, K, h0=None):
+    """Outer-product sums of Prop. 2's first expression before the softmax Jacobian
+    (App. C: dl/dP_t = dl/dx_t (D_t x_{t-1})^T, summed over the
+    steps t with k*(u_t) = k):
+
+        G[h,k,i,j] = sum_{b,t : k*[b,h,t] = k} Re(conj(lambda_t[i]) (D_t h_{t-1})[j])
+
+    (real-linear split gradient of a real matrix entry, reading R13; h_{-1} = h0).
+    lam = db of scan_backward, D, h complex [B,H,L,N] (h the forward states) -> [H,K,N,N]."""
+    lam = np.asarray(lam, dtype=np.complex128)
+    D = np.asarray(D, dtype=np.complex128)
+    h = np.asarray(h, dtype=np.complex128)
+    B, H, L, N = lam.shape
+    first = np.zeros((B, H, 1, N), np.complex128) if h0 is None else np.asarray(h0, np.complex128)[:, :, None, :]
+    hprev = np.concatenate([first, h[:, :, :-1]], axis=2)
+    w = D * hprev
+    ks = np.asarray(kstar, dtype=np.int64)
+    G = np.zeros((H, K, N, N), dtype=np.float64)
+    for hh in range(H):
+        for k in range(K):
+            sel = ks[:, hh, :] == k                      # [B, L]
+            lk = lam[:, hh][sel]                          # [n_k, N]
+            wk = w[:, hh][sel]
+            G[hh, k] = np.real(np.conj(lk).T @ wk)        # sum over the selected steps
+    return G
+
+
+def dictionary_grad(M, G, T):
+    """Dictionary surrogate gradient, Prop. 2 first expression (App. C
+    Eq. grad_M): the outer-product sum G_k pushed through the
+    Jacobian of the tempered softmax of M_k, taken column-wise as the column hardmax
+    it replaces (Eq. 5; column one-hot; reading A15):
+
+        sigma_j = softmax_T(M_k[:, j]),   dM_k[:, j] = (diag(sigma_j) - sigma_j sigma_j^T) / T  G_k[:, j]
+
+    M, G [H,K,N,N] -> [H,K,N,N] float64."""
+    sig = softmax_T(M, T, axis=-2)                       # softmax over the rows i of column j
+    G = np.asarray(G, dtype=np.float64)
+    proj = (sig * G).sum(axis=-2, keepdims=True)         # sigma_j^T G[:, j]
+    return sig * (G - proj) / float(T)

@@ -432,3 +432,112 @@ def test_project_b_one_hot_columns_and_per_dict_gather():
     Dt = O.gather_D_per_dict(Dk, k)
     for bb, h, t in itertools.product(range(2), range(H), range(6)):
         assert np.array_equal(Dt[bb, h, t], Dk[h, k[bb, h, t]])
+
+
+# ---------------------------------------------------------------------------
+# NEXT-1: Prop. 2 surrogate gradients (App. C :814-841)
+# The pins differentiate, by central finite differences, the relaxed functionals the
+# straight-through estimator linearises (hardmax -> tempered softmax),
+# written here directly (softmax + inner products), not the oracle's Jacobian formulas.
+def _test_softmax(z, T, axis):
+    e = np.exp((z - z.max(axis=axis, keepdims=True)) / T)
+    return e / e.sum(axis=axis, keepdims=True)
+
+
+@pytest.mark.parametrize("T", [1.0, 0.3])
+def test_selector_grad_finite_differences(T):
+    rng = np.random.default_rng(71)
+    B, H, L, K = 2, 2, 5, 6
+    z = rng.normal(size=(B, H, L, K))
+    ks = rng.integers(0, K, size=(B, H, L))
+    g = rng.normal(size=(B, H, L))
+
+    def f(zz):   # sum_t g_t softmax_T(z_t)[k*_t]: the activated coordinate of v_t^soft
+        s = _test_softmax(zz, T, -1)
+        return float(np.sum(g * np.take_along_axis(s, ks[..., None], -1)[..., 0]))
+
+    got = O.selector_grad(z, ks, g, T)
+    eps = 1e-6
+    fd = np.zeros_like(z)
+    for idx in itertools.product(*(range(n) for n in z.shape)):
+        zp, zm = z.copy(), z.copy()
+        zp[idx] += eps
+        zm[idx] -= eps
+        fd[idx] = (f(zp) - f(zm)) / (2 * eps)
+    assert np.max(np.abs(got - fd)) <= 1e-7 * max(1.0, np.max(np.abs(fd)))
+    # softmax-Jacobian rows sum to zero; g = 0 (lambda = 0) gives zero
+    assert np.allclose(got.sum(-1), 0.0, atol=1e-12)
+    assert np.all(O.selector_grad(z, ks, np.zeros_like(g), T) == 0.0)
+
+
+def test_selector_grad_two_way_closed_form():
+    """K = 2, equal logits, k* = 0: s = (1/2, 1/2), so dl/dz = g (1/2)((1,0) - (1/2,1/2)) / T = g/T (1/4, -1/4)."""
+    g, T = 1.7, 0.5
+    got = O.selector_grad(np.zeros((1, 1, 1, 2)), np.zeros((1, 1, 1), np.int64), np.full((1, 1, 1), g), T)
+    assert np.allclose(got[0, 0, 0], [g / T / 4, -g / T / 4], rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("c", [1, 2])
+def test_dictionary_outer_is_dP_of_linear_functional(c):
+    """G_k = d/dP_k of sum_t Re<lambda_t, P_{k*_t} D_t h_{t-1}>, with P_k a free dense matrix
+    (linear in P, so central differences are exact up to rounding)."""
+    rng = np.random.default_rng(72 + c)
+    B, H, L, N, K = 2, 2, 7, 4, 3
+    cz = (lambda *s: rng.normal(size=s) + 1j * rng.normal(size=s)) if c == 2 else (lambda *s: rng.normal(size=s) + 0j)
+    lam, D, h, h0 = cz(B, H, L, N), cz(B, H, L, N), cz(B, H, L, N), cz(B, H, N)
+    ks = rng.integers(0, K, size=(B, H, L))
+    hprev = np.concatenate([h0[:, :, None], h[:, :, :-1]], axis=2)
+
+    def f(Pd):   # Pd [H,K,N,N] dense
+        tot = 0.0
+        for b in range(B):
+            for hh in range(H):
+                for t in range(L):
+                    v = Pd[hh, ks[b, hh, t]] @ (D[b, hh, t] * hprev[b, hh, t])
+                    tot += float(np.real(np.vdot(lam[b, hh, t], v)))
+        return tot
+
+    G = O.dictionary_outer(ks, lam, D, h, K, h0=h0)
+    P0 = rng.normal(size=(H, K, N, N))
+    fd = np.zeros_like(P0)
+    for idx in itertools.product(*(range(n) for n in P0.shape)):
+        Pp, Pm = P0.copy(), P0.copy()
+        Pp[idx] += 0.5
+        Pm[idx] -= 0.5
+        fd[idx] = f(Pp) - f(Pm)
+    assert np.max(np.abs(G - fd)) <= 1e-10 * max(1.0, np.max(np.abs(fd)))
+
+
+@pytest.mark.parametrize("T", [1.0, 0.25])
+def test_dictionary_grad_finite_differences(T):
+    """dM = d/dM of sum_t Re<lambda_t, softmax_T(M_{k*_t}) D_t h_{t-1}>, the column softmax
+    replacing the column hardmax of Eq. 5 with lambda, D, h held fixed."""
+    rng = np.random.default_rng(73)
+    B, H, L, N, K = 2, 1, 6, 4, 3
+    lam = rng.normal(size=(B, H, L, N)) + 1j * rng.normal(size=(B, H, L, N))
+    D = rng.normal(size=(B, H, L, N)) + 1j * rng.normal(size=(B, H, L, N))
+    h = rng.normal(size=(B, H, L, N)) + 1j * rng.normal(size=(B, H, L, N))
+    ks = np.array([[[0, 1, 0, 0, 1, 0]], [[1, 1, 0, 0, 0, 1]]])   # entry 2 never selected
+    hprev = np.concatenate([np.zeros((B, H, 1, N)), h[:, :, :-1]], axis=2)
+    M = rng.normal(size=(H, K, N, N))
+
+    def f(MM):
+        S = _test_softmax(MM, T, -2)   # column-wise (softmax over rows i of each column j)
+        tot = 0.0
+        for b in range(B):
+            for t in range(L):
+                v = S[0, ks[b, 0, t]] @ (D[b, 0, t] * hprev[b, 0, t])
+                tot += float(np.real(np.vdot(lam[b, 0, t], v)))
+        return tot
+
+    got = O.dictionary_grad(M, O.dictionary_outer(ks, lam, D, h, K), T)
+    eps = 1e-6
+    fd = np.zeros_like(M)
+    for idx in itertools.product(*(range(n) for n in M.shape)):
+        Mp, Mm = M.copy(), M.copy()
+        Mp[idx] += eps
+        Mm[idx] -= eps
+        fd[idx] = (f(Mp) - f(Mm)) / (2 * eps)
+    assert np.max(np.abs(got - fd)) <= 1e-7 * max(1.0, np.max(np.abs(fd)))
+    assert np.allclose(got.sum(axis=-2), 0.0, atol=1e-12)   # every column sums to zero
+    assert np.all(got[0, 2] == 0.0)                           # an unselected entry gets no gradient
