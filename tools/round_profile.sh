@@ -18,3 +18,6 @@ ncu --set full --clock-control none --import-source on -k regex:"k_gemm_tc" -c 3
     -o gpurun_out/prof_gemm_${TAG} python tools/time_gemm.py > /dev/null 2>&1
 python tools/ncu_summary.py gpurun_out/prof_gemm_${TAG}.ncu-rep k_gemm_tc > gpurun_out/ncu_summary_gemm_${TAG}.txt 2>&1
 ls -la gpurun_out
+# keep gpurun_out under the 64 MiB copy-back limit
+rm -f gpurun_out/prof_gemm_${TAG}.ncu-rep
+du -sh gpurun_out
