@@ -240,6 +240,43 @@ pdssm_status pdssm_scan_bwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
                             pdssm_stream_t stream);
 
 /* ---------------------------------------------------------------------------
+ * NEXT-1: Prop. 2 surrogate gradients (derivation App. C
+ * PAPER.md:814-841).  Slope-annealed straight-through estimation: every hardmax of
+ * the forward is a tempered softmax (temperature temp > 0) in the backward
+ * (PAPER.md:201-203).  Both calls consume the outputs of pdssm_scan_bwd.
+ *
+ * pdssm_select_grad -- selector logits gradient:
+ *   dlogits[b][h][t][k] = g_t s_{k*} (delta_{k,k*} - s_k) / temp,
+ *   s = softmax(logits[b][h][t][:] / temp),  g_t = gsel of pdssm_scan_bwd (reading R14)
+ *   logits   f32   [B][H][L][K]   (the logits_opt of pdssm_select)
+ *   kstar    uint8 [B][H][L]
+ *   gsel     f32   [B][H][L]
+ *   dlogits  f32   [B][H][L][K]   out
+ * Errors: NULL pointer -> ERR_NULL; temp not finite or <= 0 -> ERR_RANGE.
+ * One warp per (b, h, t); fp32 with expf; warp reductions in a fixed order.
+ * ------------------------------------------------------------------------- */
+pdssm_status pdssm_select_grad(const float* logits, const uint8_t* kstar, const float* gsel, float temp,
+                               float* dlogits, const pdssm_dims* dims, pdssm_stream_t stream);
+
+/* pdssm_dict_grad -- dense dictionary gradient:
+ *   G[h][k][i][j]  = sum_{b,t: k*[b][h][t] = k} Re(conj(lambda_t[i]) (D_t h_{t-1})[j])   (h_{-1} = h0)
+ *   dM[h][k][:][j] = (diag(sigma_j) - sigma_j sigma_j^T) / temp  G[h][k][:][j],
+ *   sigma_j = softmax(M[h][k][:][j] / temp)   (column-wise, the column hardmax of Eq. 5)
+ *   M        f32   [H][K][N][N]   the dense dictionary given to pdssm_sparsify
+ *   kstar    uint8 [B][H][L]
+ *   diag     PER_STEP act [B][H][L][c][N] | PER_DICT f32 [H][K][c][N]  (as in the scan)
+ *   h_saved  act   [B][H][L][c][N]  forward states;  h0_opt f32 [B][H][c][N] (NULL = 0)
+ *   dbias    act   [B][H][L][c][N]  lambda_t = dbias of pdssm_scan_bwd
+ *   dM       f32   [H][K][N][N]   out;   G_opt f32 [H][K][N][N] out (optional)
+ * Requires N <= 128 (ERR_UNSUPPORTED otherwise).  N = 128: tcgen05 kind::tf32 3xTF32
+ * grouped GEMM (one CTA per (h, k), fp32 accumulator in TMEM); other N: SIMT.  Steps are
+ * accumulated in ascending (b, t) order: results are run-to-run bitwise identical.
+ * ------------------------------------------------------------------------- */
+pdssm_status pdssm_dict_grad(const float* M, const uint8_t* kstar, const void* diag, const void* h_saved,
+                             const float* h0_opt, const void* dbias, float temp, float* dM, float* G_opt,
+                             const pdssm_dims* dims, pdssm_stream_t stream);
+
+/* ---------------------------------------------------------------------------
  * Sequence parallelism (the chunk algebra lifted to per-rank segments; the
  * associativity of PAPER.md:927-932).  A summary of a segment is, per (b,h):
  *   pi uint16[N] (padded to an even count), d f32[c][N], beta f32[c][N]

@@ -18,7 +18,7 @@ import re
 __all__ = [
     "PdssmError", "Dims", "lib", "sparsify", "select", "scan_fwd", "scan_bwd",
     "segment_summary", "compose_carry", "segment_summary_bwd", "compose_lambda",
-    "check_device", "chunk_state_views", "default_chunk", "workspace_bytes",
+    "check_device", "chunk_state_views", "select_grad", "dict_grad", "default_chunk", "workspace_bytes",
     "F32", "BF16", "PER_STEP", "PER_DICT", "CHECK_FINITE", "EXPORT_MAPS",
 ]
 
@@ -75,6 +75,8 @@ def _load():
         "pdssm_compose_carry": (ctypes.c_int, [vp, i32, i32, vp, vp, vp, D, vp]),
         "pdssm_segment_summary_bwd": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, D, vp, sz, vp]),
         "pdssm_compose_lambda": (ctypes.c_int, [vp, vp, i32, i32, vp, D, vp]),
+        "pdssm_select_grad": (ctypes.c_int, [vp, vp, vp, ctypes.c_float, vp, D, vp]),
+        "pdssm_dict_grad": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, ctypes.c_float, vp, vp, D, vp]),
         "pdssm_status_string": (ctypes.c_char_p, [ctypes.c_int]),
         "pdssm_last_error": (ctypes.c_char_p, []),
         "pdssm_version": (ctypes.c_char_p, []),
@@ -305,6 +307,27 @@ def scan_bwd(kstar, dict_idx, diag, h_saved, chunk_state, dims, dh=None, dy=None
                               _ptr(dh), _ptr(dy), _ptr(C), _ptr(lam_in), _ptr(db), _ptr(dD), _ptr(g), _ptr(dh0),
                               ctypes.byref(dims), _ptr(ws), wsb, _stream()))
     return db, dD, g, dh0
+
+
+def select_grad(logits, kstar, gsel, temp, out=None):
+    """NEXT-1 selector surrogate gradient (Prop. 2): -> dlogits f32 [B,H,L,K]."""
+    torch = _torch()
+    B, H, L, K = logits.shape
+    dims = make_dims(B, H, L, 1, K)
+    out = torch.empty_like(logits) if out is None else out
+    _check(lib.pdssm_select_grad(_ptr(_contig(logits, "logits")), _ptr(_contig(kstar, "kstar")), _ptr(_contig(gsel, "gsel")),
+                                 float(temp), _ptr(out), ctypes.byref(dims), _stream()))
+    return out
+
+
+def dict_grad(M, kstar, diag, h_saved, dbias, temp, dims, h0=None, want_G=False, out=None):
+    """NEXT-1 dictionary surrogate gradient (Prop. 2): -> (dM, G or None), f32 [H,K,N,N]."""
+    torch = _torch()
+    dM = torch.empty_like(M) if out is None else out
+    G = torch.empty_like(M) if want_G else None
+    _check(lib.pdssm_dict_grad(_ptr(_contig(M, "M")), _ptr(kstar), _ptr(diag), _ptr(h_saved), _ptr(h0), _ptr(dbias),
+                               float(temp), _ptr(dM), _ptr(G), ctypes.byref(dims), _stream()))
+    return dM, G
 
 
 def summary_bytes(dims):

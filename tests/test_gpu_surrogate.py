@@ -1,0 +1,126 @@
+"""GPU parity of the NEXT-1 surrogate gradients (Prop. 2) through the C ABI
+against the float64 oracle (oracle.selector_grad / dictionary_outer / dictionary_grad, pinned by
+finite differences in test_oracle_pins.py).  The oracle side runs its own forward and backward
+scans, so no GPU value enters the reference.  Bars (R19): max|gpu - oracle| /
+max|oracle| <= 1e-4 (fp32) per tensor; bf16 activations 3e-2 (G multiplies two bf16-rounded
+operands, as dD and g do)."""
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2605_19150_b200 as mod
+    return mod
+
+
+def rel(a, b):
+    return float(np.max(np.abs(np.asarray(a, np.float64) - b)) / max(np.max(np.abs(b)), 1e-30))
+
+
+@pytest.mark.parametrize("K,T", [(32, 1.0), (5, 0.5), (48, 0.1)])
+def test_select_grad_parity(P, K, T):
+    B, H, L = 2, 3, 77
+    rng = np.random.default_rng(K)
+    logits = rng.normal(size=(B, H, L, K)).astype(np.float32)
+    ks = rng.integers(0, K, size=(B, H, L)).astype(np.uint8)
+    g = rng.normal(size=(B, H, L)).astype(np.float32)
+    d = P.select_grad(torch.from_numpy(logits).cuda(), torch.from_numpy(ks).cuda(), torch.from_numpy(g).cuda(), T)
+    ref = O.selector_grad(logits.astype(np.float64), ks, g.astype(np.float64), T)
+    assert rel(d.cpu().numpy(), ref) <= 1e-5
+    # the argmax of the GPU's own select feeds it in practice; rows sum to 0
+    assert np.max(np.abs(d.cpu().numpy().astype(np.float64).sum(-1))) <= 1e-5 * max(1.0, np.max(np.abs(ref)))
+
+
+def run_dict_case(P, B, H, L, N, K, c, T, bf16=False, per_dict=False, unused_k=None, seed=0):
+    inp = synth.scan_inputs(B, H, L, N, K, c, seed=seed, h0=True, dh=True, per_dict=per_dict, bf16=bf16)
+    M = synth.dictionary(H, K, N, seed + 1).astype(np.float32)
+    if unused_k is not None:
+        inp["kstar"][inp["kstar"] == unused_k] = (unused_k + 1) % K
+    d = {}
+    for k, v in inp.items():
+        t = torch.from_numpy(np.ascontiguousarray(v)).cuda()
+        if k == "dict_idx":
+            t = t.to(torch.int16)
+        elif k in ("bias", "dh") or (k == "diag" and not per_dict):
+            if bf16:
+                t = t.to(torch.bfloat16)
+        d[k] = t
+    f = P.scan_fwd(d["kstar"], d["dict_idx"], d["diag"], d["bias"], h0=d["h0"], per_dict=per_dict)
+    db, dD, g, dh0 = P.scan_bwd(d["kstar"], d["dict_idx"], d["diag"], f["h"], f["chunk_state"], f["dims"],
+                                dh=d["dh"], h0=d["h0"])
+    Mt = torch.from_numpy(M).cuda()
+    dM, G = P.dict_grad(Mt, d["kstar"], d["diag"], f["h"], db, T, f["dims"], h0=d["h0"], want_G=True)
+    torch.cuda.synchronize()
+    # oracle: its own forward and backward from the same (rounded) inputs
+    Pm = O.gather_P(inp["dict_idx"], inp["kstar"])
+    Dz = O.planes_to_complex(inp["diag"])
+    if per_dict:
+        Dz = O.gather_D_per_dict(Dz, inp["kstar"])
+    bz, h0z, e = (O.planes_to_complex(inp[k]) for k in ("bias", "h0", "dh"))
+    h = O.scan_forward(Pm, Dz, bz, h0z)
+    lam = O.scan_backward(Pm, Dz, h, e, h0z)[0]
+    G_ref = O.dictionary_outer(inp["kstar"], lam, Dz, h, K, h0=h0z)
+    dM_ref = O.dictionary_grad(M.astype(np.float64), G_ref, T)
+    return dM.cpu().numpy(), G.cpu().numpy(), dM_ref, G_ref, (Mt, d, f, db)
+
+
+DICT_CASES = [
+    # B, H, L, N, K, c, bf16, per_dict
+    (2, 2, 300, 128, 32, 2, False, False),   # tcgen05 path, complex, ragged batches per entry
+    (1, 2, 517, 128, 7, 1, False, False),    # tcgen05 path, real
+    (2, 1, 200, 128, 6, 2, False, True),     # tcgen05 path, PER_DICT
+    (2, 2, 150, 64, 16, 2, False, False),    # SIMT path
+    (1, 1, 64, 8, 4, 2, False, False),       # config 1 (tiny), SIMT
+    (1, 2, 100, 32, 5, 1, False, True),      # SIMT, PER_DICT, real
+]
+
+
+@pytest.mark.parametrize("case", DICT_CASES, ids=[str(c) for c in DICT_CASES])
+@pytest.mark.parametrize("T", [1.0, 0.2])
+def test_dict_grad_parity(P, case, T):
+    B, H, L, N, K, c, bf16, pd = case
+    dM, G, dM_ref, G_ref, _ = run_dict_case(P, B, H, L, N, K, c, T, bf16=bf16, per_dict=pd, seed=N + L)
+    assert rel(G, G_ref) <= 1e-4
+    assert rel(dM, dM_ref) <= 1e-4
+    assert np.max(np.abs(dM.astype(np.float64).sum(axis=-2))) <= 1e-4 * max(1.0, np.max(np.abs(dM_ref)))
+
+
+@pytest.mark.parametrize("N", [128, 64])
+def test_dict_grad_bf16_and_unused_entry(P, N):
+    B, H, L, K, c = 2, 2, 180, 8, 2
+    dM, G, dM_ref, G_ref, _ = run_dict_case(P, B, H, L, N, K, c, 0.5, bf16=True, unused_k=3, seed=9)
+    assert rel(G, G_ref) <= 3e-2
+    assert rel(dM, dM_ref) <= 3e-2
+    assert np.all(G[:, 3] == 0.0) and np.all(dM[:, 3] == 0.0)   # no step selected entry 3
+
+
+def test_dict_grad_tc_matches_simt_and_is_deterministic(P, monkeypatch):
+    B, H, L, N, K, c = 2, 2, 400, 128, 16, 2
+    dM, G, dM_ref, G_ref, (Mt, d, f, db) = run_dict_case(P, B, H, L, N, K, c, 1.0, seed=3)
+    dM2, G2 = P.dict_grad(Mt, d["kstar"], d["diag"], f["h"], db, 1.0, f["dims"], h0=d["h0"], want_G=True)
+    assert torch.equal(dM2, torch.from_numpy(dM).cuda()) and torch.equal(G2, torch.from_numpy(G).cuda())
+    monkeypatch.setenv("PDSSM_PATH", "generic")   # SIMT kernel at N = 128
+    dM3, G3 = P.dict_grad(Mt, d["kstar"], d["diag"], f["h"], db, 1.0, f["dims"], h0=d["h0"], want_G=True)
+    assert rel(G3.cpu().numpy(), G_ref) <= 1e-4
+    assert rel(dM3.cpu().numpy(), dM_ref) <= 1e-4
+
+
+def test_grad_argument_errors(P):
+    dims = P.make_dims(1, 1, 4, 8, 2, c=1)
+    z = torch.zeros(1, 1, 4, 2, device="cuda")
+    ks = torch.zeros(1, 1, 4, dtype=torch.uint8, device="cuda")
+    g = torch.zeros(1, 1, 4, device="cuda")
+    with pytest.raises(P.PdssmError, match="ERR_RANGE"):
+        P.select_grad(z, ks, g, 0.0)
+    M = torch.zeros(1, 2, 8, 8, device="cuda")
+    with pytest.raises(P.PdssmError, match="ERR_NULL"):
+        P.dict_grad(M, ks, None, None, None, 1.0, dims)
