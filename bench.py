@@ -225,6 +225,54 @@ def layer_kernels(P, torch, dev, adt, dtype, B, L, H, N, K, c, stream):
     return out
 
 
+def surrogate_kernels(P, torch, dev, d, fo, bo, dims, dtype, B, L, H, N, K, c, p, stream):
+    """NEXT-1 (Prop. 2): selector dlogits and the dense dictionary gradient,
+    timed alone on the bench's own backward outputs (lambda = dbias, the saved h, D).
+    dict_grad algorithmic bytes per (b,h,t): read lambda, D, h_{t-1} (3cNp) + k* (1 per CTA scan,
+    counted once); flops 2 c N^2 per (b,h,t) (the grouped outer-product GEMM)."""
+    g = torch.Generator(device=dev).manual_seed(11)
+    M = (torch.rand((H, K, N, N), device=dev, generator=g) * 2 - 1) / N ** 0.5
+    logits = torch.randn((B, H, L, K), device=dev, generator=g)
+    dM = torch.empty_like(M)
+    dl = torch.empty_like(logits)
+
+    def t(fn, n=10):
+        """n calls captured in one CUDA graph (the calls are graph-safe), so host-side
+        argument marshalling does not pad the device time of these short kernels."""
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        gs = torch.cuda.Stream()
+        gs.wait_stream(stream)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(gs), torch.cuda.graph(graph, stream=gs):
+            for _ in range(n):
+                fn()
+        torch.cuda.synchronize()
+        graph.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        graph.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / n * 1e3   # us
+
+    td = t(lambda: P.dict_grad(M, d["kstar"], d["diag"], fo["h"], bo["dbias"], 1.0, dims, out=dM))
+    tsg = t(lambda: P.select_grad(logits, d["kstar"], bo["gsel"], 1.0, out=dl))
+    peak, _ = peaks()
+    dbytes = (3 * c * N * p + 1) * B * H * L + 2 * H * K * N * N * 4
+    dflops = 2.0 * c * N * N * B * H * L
+    sbytes = (8 * K + 5) * B * H * L
+    tpk = peak_tflops(dtype) if dtype == "bf16" else peak_tflops("f32")
+    return {"dict_grad": {"us": td, "gbs": dbytes / (td * 1e-6) / 1e9, "hbm_frac": dbytes / (td * 1e-6) / 1e9 / peak,
+                          "tflops": dflops / (td * 1e-6) / 1e12, "tensor_frac": dflops / (td * 1e-6) / 1e12 / tpk,
+                          "algo_bytes": dbytes, "flops": dflops,
+                          "path": "tcgen05 kind::tf32 3xTF32" if N == 128 else "simt"},
+            "select_grad": {"us": tsg, "gbs": sbytes / (tsg * 1e-6) / 1e9, "hbm_frac": sbytes / (tsg * 1e-6) / 1e9 / peak,
+                            "algo_bytes": sbytes}}
+
+
 def main():
     a = parse()
     if a.impl == "reference":
@@ -375,6 +423,8 @@ def main():
     layer = None
     if not a.no_layer:
         layer = layer_kernels(P, torch, dev, adt, a.dtype, B, L, H, N, K, c, stream)
+        layer["surrogate_grads"] = surrogate_kernels(P, torch, dev, d, fo, bo, dims, a.dtype, B, L, H, N, K, c, p,
+                                                     stream)
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
                 "ms_per_step": 1e3 * elapsed / a.steps, "higher_is_better": True, "scaling": "weak",

@@ -25,7 +25,8 @@ namespace pdssm {
 namespace sg {
 
 // ----------------------------------------------------------------------------- selector
-// one warp per (b, h, t) row of K logits
+// one warp per (b, h, t) row of K <= 256 logits, held in registers (lane owns k = lane + 32 m)
+template <int KM>   // ceil(K / 32) logits per lane
 __global__ void k_select_grad(const float* __restrict__ logits, const uint8_t* __restrict__ kstar,
                               const float* __restrict__ gsel, float* __restrict__ dlogits, int64_t rows, int K,
                               float invT) {
@@ -33,21 +34,39 @@ __global__ void k_select_grad(const float* __restrict__ logits, const uint8_t* _
     const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (r >= rows) return;
     const float* z = logits + r * K;
+    const int ks = min((int)kstar[r], K - 1);
+    const float gr = gsel[r];
+    float v[KM];
     float mx = -INFINITY;
-    for (int k = lane; k < K; k += 32) mx = fmaxf(mx, z[k] * invT);
+#pragma unroll
+    for (int m = 0; m < KM; ++m) {
+        const int k = lane + 32 * m;
+        v[m] = k < K ? z[k] * invT : -INFINITY;
+        mx = fmaxf(mx, v[m]);
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     float sum = 0.f;
-    for (int k = lane; k < K; k += 32) sum += expf(z[k] * invT - mx);
+#pragma unroll
+    for (int m = 0; m < KM; ++m) {
+        v[m] = lane + 32 * m < K ? expf(v[m] - mx) : 0.f;
+        sum += v[m];
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    const int ks = min((int)kstar[r], K - 1);
     const float rs = 1.f / sum;
-    const float sk = expf(z[ks] * invT - mx) * rs;
-    const float coef = gsel[r] * sk * invT;
-    for (int k = lane; k < K; k += 32) {
-        const float s = expf(z[k] * invT - mx) * rs;
-        dlogits[r * K + k] = coef * ((k == ks ? 1.f : 0.f) - s);
+    const float ek = __shfl_sync(0xffffffffu, v[0], ks & 31);   // exp of the selected logit: lane ks % 32, slot ks / 32
+    float eks = ek;
+#pragma unroll
+    for (int m = 1; m < KM; ++m) {
+        const float e = __shfl_sync(0xffffffffu, v[m], ks & 31);
+        if ((ks >> 5) == m) eks = e;
+    }
+    const float coef = gr * eks * rs * invT;
+#pragma unroll
+    for (int m = 0; m < KM; ++m) {
+        const int k = lane + 32 * m;
+        if (k < K) dlogits[r * K + k] = coef * ((k == ks ? 1.f : 0.f) - v[m] * rs);
     }
 }
 
@@ -219,18 +238,166 @@ __global__ void __launch_bounds__(256) k_dict_grad_simt(DictArgs a) {
 // one 128-byte K slab: K index kk = r * NC + plane.
 constexpr int TC_N = 128;
 constexpr int TC_SLAB = TC_N * 128;        // bytes of one 128-row x 128-byte operand tile
-constexpr int TC_STAGE = 4 * TC_SLAB;      // A hi, A lo, B hi, B lo
-constexpr int TC_THREADS = 256;
-__host__ __device__ constexpr size_t tc_smem_bytes() { return 1024 + 2 * (size_t)TC_STAGE + 4 * (32 + 256) + 64 + 64; }
+constexpr int TC_STAGE = 4 * TC_SLAB;      // A hi, A lo, B hi, B lo (one operand stage)
+constexpr int TC_THREADS = 512;
+constexpr int TC_PAIRS = TC_N * 8 / TC_THREADS;   // (row n, 16-byte chunk) pairs per thread per batch
+constexpr int TC_PPT = 4;                  // k* positions per thread per compaction window
+constexpr int TC_WIN = TC_PPT * TC_THREADS;
+constexpr int TC_QCAP = TC_WIN + 64;       // queue capacity (window + carried-over rows)
+// two operand stages | queue | window sums | mbarriers | TMEM slot.  The epilogue's G tile
+// [N][N+1] and M tile [N][N] reuse the operand stages.
+constexpr size_t TC_OFF_Q = 2 * (size_t)TC_STAGE;
+constexpr size_t TC_OFF_WSUM = TC_OFF_Q + 4 * (size_t)TC_QCAP;
+constexpr size_t TC_OFF_BAR = TC_OFF_WSUM + 4 * (size_t)(TC_THREADS / 32);
+__host__ __device__ constexpr size_t tc_smem_bytes() { return 1024 + TC_OFF_BAR + 64; }
+static_assert(TC_OFF_Q >= 4 * (size_t)(TC_N * (TC_N + 1) + TC_N * TC_N) - 4 * TC_QCAP, "epilogue tiles must fit");
+static_assert(1024 + TC_OFF_BAR + 64 <= 227 * 1024, "shared memory budget");
 
 // byte offset of (row n, 16-byte chunk ch) in a K-major SWIZZLE_128B tile (8-row atoms of 1024 B)
 __device__ __forceinline__ uint32_t sw128(int n, int ch) { return (uint32_t)((n >> 3) * 1024 + (n & 7) * 128 + ((ch ^ (n & 7)) << 4)); }
 
-__device__ __forceinline__ void split_store(uint8_t* hi, uint8_t* lo, uint32_t off, float x0, float x1, float x2, float x3) {
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+// hi = tf32_rna(x) and lo = x - hi at the same swizzled offset of the hi / lo tiles (shared addresses)
+__device__ __forceinline__ void split_store(uint32_t hi, uint32_t lo, uint32_t off, float x0, float x1, float x2, float x3) {
     const uint32_t h0 = tc::tf32_rna(x0), h1 = tc::tf32_rna(x1), h2 = tc::tf32_rna(x2), h3 = tc::tf32_rna(x3);
-    *reinterpret_cast<uint4*>(hi + off) = make_uint4(h0, h1, h2, h3);
-    *reinterpret_cast<float4*>(lo + off) = make_float4(x0 - __uint_as_float(h0), x1 - __uint_as_float(h1),
-                                                       x2 - __uint_as_float(h2), x3 - __uint_as_float(h3));
+    sts128(hi + off, h0, h1, h2, h3);
+    sts128(lo + off, __float_as_uint(x0 - __uint_as_float(h0)), __float_as_uint(x1 - __uint_as_float(h1)),
+           __float_as_uint(x2 - __uint_as_float(h2)), __float_as_uint(x3 - __uint_as_float(h3)));
+}
+
+// Stable compaction of a window of TC_WIN positions [pos, pos + TC_WIN) (TC_PPT consecutive
+// per thread, all loads in flight together) appended to q[qn ...] as row codes: the row
+// R = (b H + h) L + t of a step with t > 0, or -(b H + h) - 1 for t = 0.  Returns the new count.
+__device__ __forceinline__ int compact_window(const DictArgs& a, int h, int k, int64_t pos, int* q, int qn, int* wsum) {
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int64_t BL = (int64_t)a.B * a.L;
+    const int64_t p0 = pos + TC_PPT * (int64_t)tid;
+    // one 32-bit division per thread (B * L < 2^31), then carry t across sequence ends
+    int b = (int)(p0 / a.L), t = (int)(p0 - (int64_t)b * a.L);
+    uint32_t bits = 0;
+    int code[TC_PPT];
+#pragma unroll
+    for (int u = 0; u < TC_PPT; ++u) {
+        code[u] = 0;
+        if (p0 + u < BL) {
+            const int sq = b * a.H + h;
+            bits |= (uint32_t)(min((int)a.kstar[(int64_t)sq * a.L + t], a.K - 1) == k) << u;
+            code[u] = t > 0 ? sq * a.L + t : -sq - 1;
+        }
+        if (++t == a.L) {
+            t = 0;
+            ++b;
+        }
+    }
+    const int c = __popc(bits);
+    int inc = c;   // inclusive warp scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    int before = inc - c, tot = 0;
+    for (int x = 0; x < TC_THREADS / 32; ++x) {
+        const int v = wsum[x];
+        before += x < w ? v : 0;
+        tot += v;
+    }
+    int o = qn + before;
+#pragma unroll
+    for (int u = 0; u < TC_PPT; ++u)
+        if (bits >> u & 1u) q[o++] = code[u];
+    __syncthreads();
+    return qn + tot;
+}
+
+// Raw operand values of one batch for this thread: TC_PAIRS (row n, chunk) pairs x 12 values
+// (NC = 2: 2 steps x {lr, li, Dr, Di, hr, hi};  NC = 1: 4 steps x {l, D, h}).  Rows are the
+// row codes of compact_window (no division here).
+template <typename T, int NC, bool PD>
+__device__ __forceinline__ void load_raw(const DictArgs& a, int h, int k, const int* rows, int nb,
+                                         float (&raw)[TC_PAIRS][12]) {
+    constexpr int N = TC_N;
+#pragma unroll
+    for (int m = 0; m < TC_PAIRS; ++m) {
+        const int x = threadIdx.x + TC_THREADS * m;
+        const int n = x & (N - 1), ch = x >> 7;
+        constexpr int RPC = 4 / NC;   // steps per 16-byte chunk
+#pragma unroll
+        for (int u = 0; u < RPC; ++u) {
+            const int r = RPC * ch + u;
+            float* v = &raw[m][u * 3 * NC];
+            if (r < nb) {
+                const int c = rows[r];
+                const bool first = c < 0;
+                const size_t sq = first ? (size_t)(-c - 1) : 0;
+                const size_t R = first ? sq * (size_t)a.L : (size_t)c;
+                const size_t off = R * NC * N + n;
+                const T* lam = static_cast<const T*>(a.lam);
+                v[0] = ld_act(lam + off);
+                if constexpr (NC == 2) v[1] = ld_act(lam + off + N);
+                float* dv = v + NC;
+                if constexpr (PD) {
+                    const float* dk = a.diag_dict + ((size_t)h * a.K + k) * NC * N + n;
+                    dv[0] = __ldg(dk);
+                    if constexpr (NC == 2) dv[1] = __ldg(dk + N);
+                } else {
+                    const T* D = static_cast<const T*>(a.diag);
+                    dv[0] = ld_act(D + off);
+                    if constexpr (NC == 2) dv[1] = ld_act(D + off + N);
+                }
+                float* hv = v + 2 * NC;
+                if (!first) {
+                    const T* hs = static_cast<const T*>(a.hsaved);
+                    hv[0] = ld_act(hs + off - NC * N);
+                    if constexpr (NC == 2) hv[1] = ld_act(hs + off - NC * N + N);
+                } else if (a.h0) {
+                    hv[0] = __ldg(a.h0 + sq * NC * N + n);
+                    if constexpr (NC == 2) hv[1] = __ldg(a.h0 + sq * NC * N + N + n);
+                } else {
+                    hv[0] = 0.f;
+                    if constexpr (NC == 2) hv[1] = 0.f;
+                }
+            } else {
+#pragma unroll
+                for (int z = 0; z < 3 * NC; ++z) v[z] = 0.f;
+            }
+        }
+    }
+}
+
+// raw -> (lambda, w = D (.) h_{t-1}) -> tf32 hi/lo into the K-major SWIZZLE_128B operand tiles
+template <int NC>
+__device__ __forceinline__ void convert_store(const float (&raw)[TC_PAIRS][12], uint32_t st) {
+#pragma unroll
+    for (int m = 0; m < TC_PAIRS; ++m) {
+        const int x = threadIdx.x + TC_THREADS * m;
+        const int n = x & (TC_N - 1), ch = x >> 7;
+        float lv[4], wv[4];
+        if constexpr (NC == 2) {
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const float* v = &raw[m][6 * u];
+                lv[2 * u] = v[0];
+                lv[2 * u + 1] = v[1];
+                wv[2 * u] = v[2] * v[4] - v[3] * v[5];
+                wv[2 * u + 1] = v[2] * v[5] + v[3] * v[4];
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float* v = &raw[m][3 * u];
+                lv[u] = v[0];
+                wv[u] = v[1] * v[2];
+            }
+        }
+        const uint32_t off = sw128(n, ch);
+        split_store(st, st + TC_SLAB, off, lv[0], lv[1], lv[2], lv[3]);
+        split_store(st + 2 * TC_SLAB, st + 3 * TC_SLAB, off, wv[0], wv[1], wv[2], wv[3]);
+    }
 }
 
 template <typename T, int NC, bool PD>
@@ -240,9 +407,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_dict_grad_tc(DictArgs a) {
     constexpr int N = TC_N;
     constexpr int RB = 32 / NC;                // steps per K slab
     const int h = blockIdx.x / a.K, k = blockIdx.x % a.K;
-    int* q = reinterpret_cast<int*>(smem + 2 * TC_STAGE);      // [RB + 256] queue
-    int* wcnt = q + 32 + 256;                                  // [8]
-    uint64_t* done = reinterpret_cast<uint64_t*>(wcnt + 16);   // [2] MMA completion per buffer
+    int* q = reinterpret_cast<int*>(smem + TC_OFF_Q);          // queue of row codes
+    int* wsum = reinterpret_cast<int*>(smem + TC_OFF_WSUM);
+    uint64_t* done = reinterpret_cast<uint64_t*>(smem + TC_OFF_BAR);   // [2] MMA completion per operand stage
     uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 2);
     const int tid = threadIdx.x, warp = tid >> 5;
     if (tid == 0) {
@@ -262,46 +429,42 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_dict_grad_tc(DictArgs a) {
     const uint32_t id_ = tc::idesc(2u, N);   // kind::tf32, M = 128, N = 128
     const int64_t BL = (int64_t)a.B * a.L;
     int64_t pos = 0;
-    int qn = 0, nbatch = 0;
-    while (true) {
-        while (qn < RB && pos < BL) {
-            qn = compact_chunk(a, h, k, pos, q, qn, wcnt);
-            pos += blockDim.x;
+    int qh = 0, qn = 0;
+    auto refill = [&]() {   // >= 2 RB rows queued (or the head's positions exhausted)
+        while (qn - qh < 2 * RB && pos < BL) {
+            const int rem = qn - qh;   // < 2 RB <= blockDim
+            const int v = tid < rem ? q[qh + tid] : 0;
+            __syncthreads();
+            if (tid < rem) q[tid] = v;
+            qn = rem;
+            qh = 0;
+            qn = compact_window(a, h, k, pos, q, qn, wsum);   // (syncs before reading q)
+            pos += TC_WIN;
         }
-        const int nb = min(qn, RB);
-        if (nb == 0) break;
+    };
+    // three batches of raw values in registers, rotated by role (no copies: a register copy
+    // of a pending load would wait for it): batch n is converted while n+1 and n+2 are in flight
+    float R0[TC_PAIRS][12], R1[TC_PAIRS][12], R2[TC_PAIRS][12];
+    int nbs[3];
+    refill();
+    nbs[0] = min(qn - qh, RB);
+    if (nbs[0] > 0) load_raw<T, NC, PD>(a, h, k, q + qh, nbs[0], R0);
+    qh += nbs[0];
+    refill();
+    nbs[1] = min(qn - qh, RB);
+    if (nbs[1] > 0) load_raw<T, NC, PD>(a, h, k, q + qh, nbs[1], R1);
+    qh += nbs[1];
+    int nbatch = 0;
+    auto iter = [&](float (&cur)[TC_PAIRS][12], float (&ld)[TC_PAIRS][12], const int ic, const int il) -> bool {
+        if (nbs[ic] == 0) return false;
+        refill();
+        nbs[il] = min(qn - qh, RB);
+        if (nbs[il] > 0) load_raw<T, NC, PD>(a, h, k, q + qh, nbs[il], ld);   // two batches ahead
+        qh += nbs[il];
         const int s = nbatch & 1;
         uint8_t* st = smem + (size_t)s * TC_STAGE;
         if (nbatch >= 2) tc::mbar_wait(done + s, (uint32_t)((nbatch - 2) >> 1) & 1u);   // MMAs of batch n-2 read it
-        // stage: pair x = (n, chunk); chunk ch holds kk = 4ch..4ch+3 = (row, plane) pairs
-        for (int x = tid; x < N * 8; x += TC_THREADS) {
-            const int n = x & (N - 1), ch = x >> 7;
-            float lv[4], wv[4];
-            if constexpr (NC == 2) {
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    const int r = 2 * ch + u;
-                    float lr = 0.f, li = 0.f, wr = 0.f, wi = 0.f;
-                    if (r < nb) row_vals<T, NC, PD>(a, h, k, q[r], n, lr, li, wr, wi);
-                    lv[2 * u] = lr;
-                    lv[2 * u + 1] = li;
-                    wv[2 * u] = wr;
-                    wv[2 * u + 1] = wi;
-                }
-            } else {
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int r = 4 * ch + u;
-                    float lr = 0.f, li, wr = 0.f, wi;
-                    if (r < nb) row_vals<T, NC, PD>(a, h, k, q[r], n, lr, li, wr, wi);
-                    lv[u] = lr;
-                    wv[u] = wr;
-                }
-            }
-            const uint32_t off = sw128(n, ch);
-            split_store(st, st + TC_SLAB, off, lv[0], lv[1], lv[2], lv[3]);
-            split_store(st + 2 * TC_SLAB, st + 3 * TC_SLAB, off, wv[0], wv[1], wv[2], wv[3]);
-        }
+        convert_store<NC>(cur, tc::su32(st));
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> MMA reads
         __syncthreads();
         if (tid == 0) {
@@ -317,14 +480,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_dict_grad_tc(DictArgs a) {
             }
             tc::commit(done + s);
         }
-        pop_queue(q, qn, nb);   // (q is not read by the MMA)
-        qn -= nb;
         ++nbatch;
+        return true;
+    };
+    while (iter(R0, R2, 0, 2) && iter(R1, R0, 1, 0) && iter(R2, R1, 2, 1)) {
     }
     // drain: the last batch's commit covers every earlier MMA
     if (nbatch > 0) tc::mbar_wait(done + ((nbatch - 1) & 1), (uint32_t)((nbatch - 1) >> 1) & 1u);
     tc::fence_after();
-    float* Gs = reinterpret_cast<float*>(smem);   // [N][N+1] over the (now idle) operand buffers
+    __syncthreads();
+    float* Gs = reinterpret_cast<float*>(smem);   // [N][N+1] over the (now idle) operand stages
     if (warp < 4) {
         const int i = warp * 32 + (tid & 31);
         for (int j0 = 0; j0 < N; j0 += 16) {
@@ -339,13 +504,39 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_dict_grad_tc(DictArgs a) {
             for (int u = 0; u < 16; ++u) Gs[i * (N + 1) + j0 + u] = v[u];
         }
     }
+    // the dictionary tile M[h][k] next to it (row-major, read row-wise by the column threads)
+    float* Ms = Gs + N * (N + 1);
+    {
+        const float4* src = reinterpret_cast<const float4*>(a.M + ((size_t)h * a.K + k) * N * N);
+        for (int x = tid; x < N * N / 4; x += TC_THREADS) reinterpret_cast<float4*>(Ms)[x] = __ldg(src + x);
+    }
     tc::fence_before();
     __syncthreads();
     if (warp == 0) {
         tc::fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128) : "memory");
     }
-    jacobian_epilogue(a, h, k, Gs);
+    // softmax Jacobian: thread j owns column j (sigma_j over the rows i; ascending-i sums)
+    if (tid < N) {
+        const int j = tid;
+        float mx = -INFINITY;
+        for (int i = 0; i < N; ++i) mx = fmaxf(mx, Ms[i * N + j] * a.invT);
+        float sum = 0.f, pr = 0.f;
+        for (int i = 0; i < N; ++i) {
+            const float e = expf(Ms[i * N + j] * a.invT - mx);
+            sum += e;
+            pr += e * Gs[i * (N + 1) + j];
+        }
+        const float rs = 1.f / sum;
+        const float proj = pr * rs;
+        const size_t base = ((size_t)h * a.K + k) * N * N;
+        for (int i = 0; i < N; ++i) {
+            const float g = Gs[i * (N + 1) + j];
+            const float sg = expf(Ms[i * N + j] * a.invT - mx) * rs;
+            a.dM[base + (size_t)i * N + j] = sg * (g - proj) * a.invT;
+            if (a.G) a.G[base + (size_t)i * N + j] = g;
+        }
+    }
 }
 
 }  // namespace sg

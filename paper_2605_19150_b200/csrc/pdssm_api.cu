@@ -848,7 +848,10 @@ pdssm_status pdssm_select_grad(const float* logits, const uint8_t* kstar, const 
     if (misaligned(logits, 4) || misaligned(gsel, 4) || misaligned(dlogits, 4)) return fail(PDSSM_ERR_ALIGN, "select_grad: misaligned");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const int64_t rows = g.S * g.L;
-    sg::k_select_grad<<<(unsigned)ceil_div(rows, 8), 256, 0, st>>>(logits, kstar, gsel, dlogits, rows, (int)g.K, 1.f / temp);
+    const int km = (int)ceil_div(g.K, 32);
+    auto kern = km == 1 ? sg::k_select_grad<1> : km == 2 ? sg::k_select_grad<2> : km <= 4 ? sg::k_select_grad<4>
+                                                                                        : sg::k_select_grad<8>;
+    kern<<<(unsigned)ceil_div(rows, 8), 256, 0, st>>>(logits, kstar, gsel, dlogits, rows, (int)g.K, 1.f / temp);
     return cuda_check("select_grad");
 }
 
