@@ -87,8 +87,11 @@ struct SeqArgs {
 
 // per (entry, target) preimage records: sources ascending, padded with N; wm = warp max
 // in-degree (<= CAP); ovf = an in-degree above CAP occurred
+// The same launch writes the CSR plan of k_build_plan (pstart / psrc: preimage lists in
+// ascending source order) used by entries that overflow the records.
 __global__ void k_build_seq_plan(const uint16_t* __restrict__ dict_idx, uint8_t* __restrict__ rec,
-                                 uint8_t* __restrict__ wm, uint8_t* __restrict__ ovf, int N, uint32_t flags) {
+                                 uint8_t* __restrict__ wm, uint8_t* __restrict__ ovf, uint16_t* __restrict__ pstart,
+                                 uint16_t* __restrict__ psrc, int N, uint32_t flags) {
     extern __shared__ uint16_t sP[];
     __shared__ int sovf;
     const int e = blockIdx.x;
@@ -104,13 +107,20 @@ __global__ void k_build_seq_plan(const uint16_t* __restrict__ dict_idx, uint8_t*
     uint8_t r[CAP];
 #pragma unroll
     for (int q = 0; q < CAP; ++q) r[q] = (uint8_t)N;
-    int d = 0;
+    int d = 0, below = 0, rank = 0;
+    const int pi = sP[i];
     for (int j = 0; j < N; ++j) {
-        if (sP[j] == i) {
+        const int pj = sP[j];
+        if (pj == i) {
             if (d < CAP) r[d] = (uint8_t)j;
             ++d;
         }
+        below += pj < i;                              // pstart[i] = #{j : P[j] < i}
+        rank += (pj < pi) || (pj == pi && j < i);      // position of source i in the CSR order
     }
+    pstart[(size_t)e * (N + 1) + i] = (uint16_t)below;
+    if (i == 0) pstart[(size_t)e * (N + 1) + N] = (uint16_t)N;
+    psrc[(size_t)e * N + rank] = (uint16_t)i;
     uint8_t* dst = rec + ((size_t)e * N + i) * CAP;
 #pragma unroll
     for (int q = 0; q < CAP; ++q) dst[q] = r[q];

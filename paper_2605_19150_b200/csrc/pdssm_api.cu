@@ -563,8 +563,8 @@ pdssm_status fwd_fused(const Geo& g, fused::FusedArgs& fa, uint8_t* rec, uint32_
 }
 
 pdssm_status fwd_seq(const Geo& g, seq::SeqArgs& sa, uint8_t* rec, uint8_t* wm, uint8_t* ovf, cudaStream_t st) {
-    seq::k_build_seq_plan<<<(unsigned)(g.H * g.K), (unsigned)g.N, (size_t)g.N * 2, st>>>(sa.dict_idx, rec, wm, ovf,
-                                                                                     (int)g.N, g.flags);
+    seq::k_build_seq_plan<<<(unsigned)(g.H * g.K), (unsigned)g.N, (size_t)g.N * 2, st>>>(
+        sa.dict_idx, rec, wm, ovf, const_cast<uint16_t*>(sa.pstart), const_cast<uint16_t*>(sa.psrc), (int)g.N, g.flags);
     pdssm_status r = cuda_check("build_seq_plan");
     if (r) return r;
     const bool agg = (g.flags & PDSSM_EXPORT_MAPS) != 0;
@@ -950,9 +950,10 @@ pdssm_status pdssm_scan_fwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
     uint8_t* sovf = bump.take<uint8_t>(seq_ovf_bytes(g));
     void* hout = h_out_opt ? h_out_opt : hscratch;
     ChunkStateView cs = cs_view(g, chunk_state);
-    if ((r = launch_plan(g, dict_idx, pstart, psrc, st))) return r;
     uint16_t* maps = (g.flags & PDSSM_EXPORT_MAPS) ? maps_opt : nullptr;
     const bool use_seq = seq_applicable(g, {g.diag_mode == PDSSM_DIAG_PER_STEP ? diag : nullptr, bias, hout});
+    // the single-chunk path builds its records and the CSR plan in one launch (fwd_seq)
+    if (!use_seq && (r = launch_plan(g, dict_idx, pstart, psrc, st))) return r;
     if (env_path_is("seq") && !use_seq)
         return fail(PDSSM_ERR_UNSUPPORTED, "scan_fwd: PDSSM_PATH=seq but the single-chunk path does not apply");
     const bool use_fused = !use_seq && fused_applicable(
