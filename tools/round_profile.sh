@@ -21,3 +21,9 @@ ls -la gpurun_out
 # keep gpurun_out under the 64 MiB copy-back limit
 rm -f gpurun_out/prof_gemm_${TAG}.ncu-rep
 du -sh gpurun_out
+# NEXT-1 dictionary-gradient kernel (tcgen05 3xTF32 grouped outer products)
+ncu --set full --clock-control none --import-source on -k regex:"k_dict_grad_tc" -c 1 \
+    -o gpurun_out/prof_dict_${TAG} python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
+python tools/ncu_summary.py gpurun_out/prof_dict_${TAG}.ncu-rep k_dict_grad > gpurun_out/ncu_summary_dict_${TAG}.txt 2>&1
+rm -f gpurun_out/prof_dict_${TAG}.ncu-rep
+du -sh gpurun_out
