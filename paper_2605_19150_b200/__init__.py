@@ -18,7 +18,7 @@ import re
 __all__ = [
     "PdssmError", "Dims", "lib", "sparsify", "select", "scan_fwd", "scan_bwd",
     "segment_summary", "compose_carry", "segment_summary_bwd", "compose_lambda",
-    "check_device", "chunk_state_views", "select_grad", "dict_grad", "default_chunk", "workspace_bytes",
+    "check_device", "chunk_state_views", "select_grad", "dict_grad", "scan", "default_chunk", "workspace_bytes",
     "F32", "BF16", "PER_STEP", "PER_DICT", "CHECK_FINITE", "EXPORT_MAPS",
 ]
 
@@ -392,3 +392,42 @@ def compose_lambda(fwd_summaries, beta_bwd, rank, G, dims):
 def check_device():
     """Synchronise and read/clear the device error word (PDSSM_CHECK_FINITE)."""
     _check(lib.pdssm_check_device(_stream()))
+
+
+# ---------------------------------------------------------------- autograd glue
+_SCAN_FN = None
+
+
+def _scan_fn():
+    """torch.autograd.Function over pdssm_scan_fwd / pdssm_scan_bwd (built lazily so the
+    binding imports without touching autograd)."""
+    global _SCAN_FN
+    if _SCAN_FN is not None:
+        return _SCAN_FN
+    torch = _torch()
+
+    class _Scan(torch.autograd.Function):
+        @staticmethod
+        def forward(ctx, diag, bias, h0, kstar, dict_idx, per_dict):
+            f = scan_fwd(kstar, dict_idx, diag.contiguous(), bias.contiguous(),
+                         h0=None if h0 is None else h0.contiguous(), per_dict=per_dict)
+            ctx.save_for_backward(kstar, dict_idx, diag, f["h"], f["chunk_state"], h0)
+            ctx.dims = f["dims"]
+            return f["h"]
+
+        @staticmethod
+        def backward(ctx, dh):
+            kstar, dict_idx, diag, h, cs, h0 = ctx.saved_tensors
+            db, dD, _, dh0 = scan_bwd(kstar, dict_idx, diag, h, cs, ctx.dims, dh=dh.contiguous(), h0=h0,
+                                      want_g=False, want_dh0=h0 is not None)
+            return dD, db, dh0, None, None, None
+
+    _SCAN_FN = _Scan
+    return _Scan
+
+
+def scan(diag, bias, kstar, dict_idx, h0=None, per_dict=False):
+    """Differentiable h = scan(D, b; k*, dict) (Eq. 1 with the hard selection held fixed, PAPER.md:94-101,
+    :222): gradients flow to diag (PER_STEP: per step; PER_DICT: summed per entry), bias and h0 through
+    the reverse transposed scan (App. C).  Complex tensors use the [..., c, N] plane layout."""
+    return _scan_fn().apply(diag, bias, h0, kstar, dict_idx, per_dict)

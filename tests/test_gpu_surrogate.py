@@ -124,3 +124,27 @@ def test_grad_argument_errors(P):
     M = torch.zeros(1, 2, 8, 8, device="cuda")
     with pytest.raises(P.PdssmError, match="ERR_NULL"):
         P.dict_grad(M, ks, None, None, None, 1.0, dims)
+
+
+def test_autograd_scan_matches_oracle(P):
+    """The autograd glue (paper_2605_19150_b200.scan) routes a loss through pdssm_scan_bwd."""
+    B, H, L, N, K, c = 2, 2, 90, 64, 6, 2
+    inp = synth.scan_inputs(B, H, L, N, K, c, seed=5, h0=True, dh=True)
+    diag = torch.from_numpy(inp["diag"]).cuda().requires_grad_(True)
+    bias = torch.from_numpy(inp["bias"]).cuda().requires_grad_(True)
+    h0 = torch.from_numpy(inp["h0"]).cuda().requires_grad_(True)
+    w = torch.from_numpy(inp["dh"]).cuda()
+    ks = torch.from_numpy(inp["kstar"]).cuda()
+    di = torch.from_numpy(inp["dict_idx"]).cuda().to(torch.int16)
+    h = P.scan(diag, bias, ks, di, h0=h0)
+    (h * w).sum().backward()
+    Pm = O.gather_P(inp["dict_idx"], inp["kstar"])
+    Dz, bz, h0z, e = (O.planes_to_complex(inp[k]) for k in ("diag", "bias", "h0", "dh"))
+    hr = O.scan_forward(Pm, Dz, bz, h0z)
+    db_r, dD_r, _, dh0_r = O.scan_backward(Pm, Dz, hr, e, h0z)
+    cp = lambda t: O.planes_to_complex(t.detach().cpu().numpy())
+    rl = lambda a, b: float(np.max(np.abs(a - b)) / np.max(np.abs(b)))
+    assert rl(cp(h), hr) <= 1e-4
+    assert rl(cp(bias.grad), db_r) <= 1e-4
+    assert rl(cp(diag.grad), dD_r) <= 1e-4
+    assert rl(cp(h0.grad), dh0_r) <= 1e-4
