@@ -209,6 +209,11 @@ def layer_kernels(P, torch, dev, adt, dtype, B, L, H, N, K, c, stream):
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / n * 1e3   # us
 
+    # NEXT-2 layer-level forward (select -> b = Bx -> scan -> y), PER_DICT diagonals D_k
+    di = torch.randint(0, N, (H, K, N), device=dev, generator=g).to(torch.int16)
+    Dk = (torch.rand((H, K, c, N), device=dev, generator=g) * 2 - 1) * 0.7
+    lo = {"kstar": torch.empty((B, H, L), device=dev, dtype=torch.uint8), "h": bout, "y": y}
+    tl = t(lambda: P.layer_fwd(x, S, di, Dk, Bw, C=Cw, per_dict=True, out=lo))
     ts = t(lambda: P.select(x, S))
     tp = t(lambda: P.project(x, Bw, out=bout))
     tr = t(lambda: P.readout(bout, Cw, out=y, ws=wsr))
@@ -222,6 +227,8 @@ def layer_kernels(P, torch, dev, adt, dtype, B, L, H, N, K, c, stream):
     for name, us, fl in (("select", ts, f_sel), ("project", tp, f_prj), ("readout", tr, f_rd)):
         tf = fl / (us * 1e-6) / 1e12
         out[name] = {"us": us, "tflops": tf, "frac": tf / peak}
+    out["layer_fwd"] = {"us": tl, "tokens_per_s": B * L / (tl * 1e-6), "diag": "per_dict",
+                        "chain": "pdssm_layer_fwd = select + project + scan_fwd + readout"}
     return out
 
 

@@ -80,7 +80,8 @@ enum {
     PDSSM_EXPORT_MAPS = 8u     /* pdssm_scan_fwd also writes maps_opt                 */
 };
 
-enum { PDSSM_OP_SELECT = 0, PDSSM_OP_FWD = 1, PDSSM_OP_BWD = 2, PDSSM_OP_SEGMENT = 3, PDSSM_OP_READOUT = 4 };
+enum { PDSSM_OP_SELECT = 0, PDSSM_OP_FWD = 1, PDSSM_OP_BWD = 2, PDSSM_OP_SEGMENT = 3, PDSSM_OP_READOUT = 4,
+       PDSSM_OP_LAYER = 5 };
 
 /* Problem statement (north_star: x, selector S, dictionary {P_k, D_k}, B, C,
  * L, N, K, batch, heads).  Plain C struct; all fields are read-only inputs. */
@@ -238,6 +239,30 @@ pdssm_status pdssm_scan_bwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
                             const float* lam_in_opt, void* dbias, void* ddiag, float* gsel,
                             float* dh0_opt, const pdssm_dims* dims, void* ws, size_t ws_bytes,
                             pdssm_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * Layer-level forward with the north_star argument list (x, the selector weights, the
+ * dictionary {P_k, D_k}, B, C): the hot path end to end on the caller's stream,
+ *   a2-a4  k*_t = argmax_k S_{h,k} . x_t        (Eqs. 6-7)  pdssm_select
+ *   a5     b_t  = B x_t                         (Eq. 1)  pdssm_project
+ *   a6-a8  h_t  = P_t D_t h_{t-1} + b_t,  y_t = Re(C h_t)  (Alg. 1)
+ *   x         act  [B][L][d_in]       tokens (dims.d_in >= 1)
+ *   S         act  [H][K][d_in]       selector weights
+ *   dict_idx  uint16 [H][K][N]        sparsified dictionary maps (pdssm_sparsify)
+ *   diag      PER_DICT f32 [H][K][c][N] (the dictionary's D_k) | PER_STEP act [B][H][L][c][N]
+ *   Bw        act  [H][c][N][d_in]    input projection
+ *   C_opt     f32  [H][c][P][N]       readout (needed iff y_opt; dims.p_out = P)
+ *   h0_opt    f32  [B][H][c][N]       (NULL = 0)
+ *   kstar     uint8 [B][H][L]         out: the selections (needed by the backward)
+ *   h_out_opt act  [B][H][L][c][N]    out: states;   y_opt act [B][L][H][P] out
+ *   chunk_state                        out (pdssm_chunk_state_bytes)
+ *   ws  >= pdssm_workspace_bytes(dims, PDSSM_OP_LAYER)  (b_t plus the scan's workspace)
+ * Errors and paths: those of the three calls it chains.
+ * ------------------------------------------------------------------------- */
+pdssm_status pdssm_layer_fwd(const void* x, const void* S, const uint16_t* dict_idx, const void* diag,
+                             const void* Bw, const float* C_opt, const float* h0_opt, uint8_t* kstar,
+                             void* h_out_opt, void* y_opt, void* chunk_state, const pdssm_dims* dims,
+                             void* ws, size_t ws_bytes, pdssm_stream_t stream);
 
 /* ---------------------------------------------------------------------------
  * NEXT-1: Prop. 2 surrogate gradients (derivation App. C

@@ -18,7 +18,7 @@ import re
 __all__ = [
     "PdssmError", "Dims", "lib", "sparsify", "select", "scan_fwd", "scan_bwd",
     "segment_summary", "compose_carry", "segment_summary_bwd", "compose_lambda",
-    "check_device", "chunk_state_views", "select_grad", "dict_grad", "scan", "default_chunk", "workspace_bytes",
+    "check_device", "chunk_state_views", "select_grad", "dict_grad", "scan", "layer_fwd", "default_chunk", "workspace_bytes",
     "F32", "BF16", "PER_STEP", "PER_DICT", "CHECK_FINITE", "EXPORT_MAPS",
 ]
 
@@ -30,7 +30,7 @@ if os.environ.get("PDSSM_LIB_VARIANT"):   # tuning experiments: variants/<name>.
 F32, BF16 = 0, 1
 PER_STEP, PER_DICT = 0, 1
 CHECK_FINITE, DETERMINISTIC, EXPORT_MAPS = 1, 2, 8
-OP_SELECT, OP_FWD, OP_BWD, OP_SEGMENT, OP_READOUT = 0, 1, 2, 3, 4
+OP_SELECT, OP_FWD, OP_BWD, OP_SEGMENT, OP_READOUT, OP_LAYER = 0, 1, 2, 3, 4, 5
 
 STATUS = {0: "PDSSM_OK", 1: "PDSSM_ERR_NULL", 2: "PDSSM_ERR_SHAPE", 3: "PDSSM_ERR_RANGE",
           4: "PDSSM_ERR_ALIGN", 5: "PDSSM_ERR_DTYPE", 6: "PDSSM_ERR_WORKSPACE",
@@ -76,6 +76,7 @@ def _load():
         "pdssm_segment_summary_bwd": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, D, vp, sz, vp]),
         "pdssm_compose_lambda": (ctypes.c_int, [vp, vp, i32, i32, vp, D, vp]),
         "pdssm_select_grad": (ctypes.c_int, [vp, vp, vp, ctypes.c_float, vp, D, vp]),
+        "pdssm_layer_fwd": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, D, vp, sz, vp]),
         "pdssm_dict_grad": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, ctypes.c_float, vp, vp, D, vp]),
         "pdssm_status_string": (ctypes.c_char_p, [ctypes.c_int]),
         "pdssm_last_error": (ctypes.c_char_p, []),
@@ -307,6 +308,43 @@ def scan_bwd(kstar, dict_idx, diag, h_saved, chunk_state, dims, dh=None, dy=None
                               _ptr(dh), _ptr(dy), _ptr(C), _ptr(lam_in), _ptr(db), _ptr(dD), _ptr(g), _ptr(dh0),
                               ctypes.byref(dims), _ptr(ws), wsb, _stream()))
     return db, dD, g, dh0
+
+
+def layer_fwd(x, S, dict_idx, diag, Bw, C=None, h0=None, per_dict=True, want_h=True, out=None):
+    """Layer-level forward (select -> b = Bx -> scan -> y = Re(Ch)) with the north_star argument list.
+    Returns dict(kstar, h, y, chunk_state, dims)."""
+    torch = _torch()
+    for n, t in (("x", x), ("S", S), ("dict_idx", dict_idx), ("diag", diag), ("Bw", Bw), ("C", C), ("h0", h0)):
+        _contig(t, n)
+    B, L, d_in = x.shape
+    H, c, N, _ = Bw.shape
+    K = S.shape[1]
+    P = C.shape[-2] if C is not None else 0
+    dims = make_dims(B, H, L, N, K, c=c, dtype=_dtype_code(x), diag_mode=PER_DICT if per_dict else PER_STEP,
+                     d_in=d_in, p_out=P)
+    out = dict(out or {})
+    dev = x.device
+    ks = out.get("kstar")
+    if ks is None:
+        ks = torch.empty((B, H, L), dtype=torch.uint8, device=dev)
+    h = out.get("h") if want_h else None
+    if want_h and h is None:
+        h = torch.empty((B, H, L, c, N), dtype=x.dtype, device=dev)
+    y = out.get("y")
+    if C is not None and y is None:
+        y = torch.empty((B, L, H, P), dtype=x.dtype, device=dev)
+    cs = out.get("chunk_state")
+    if cs is None:
+        cs = torch.empty(lib.pdssm_chunk_state_bytes(ctypes.byref(dims)), dtype=torch.uint8, device=dev)
+    ws = out.get("ws")
+    wsb = workspace_bytes(dims, OP_LAYER)
+    if ws is None or ws.numel() < wsb:
+        ws, wsb = _workspace(dims, OP_LAYER, dev)
+    else:
+        wsb = ws.numel()
+    _check(lib.pdssm_layer_fwd(_ptr(x), _ptr(S), _ptr(dict_idx), _ptr(diag), _ptr(Bw), _ptr(C), _ptr(h0), _ptr(ks),
+                               _ptr(h), _ptr(y), _ptr(cs), ctypes.byref(dims), _ptr(ws), wsb, _stream()))
+    return dict(kstar=ks, h=h, y=y, chunk_state=cs, dims=dims)
 
 
 def select_grad(logits, kstar, gsel, temp, out=None):

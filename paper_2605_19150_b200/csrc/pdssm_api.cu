@@ -157,6 +157,10 @@ size_t ws_bytes_g(const Geo& g, int op) {
                    (g.diag_mode == PDSSM_DIAG_PER_DICT ? seq_f_bytes(g) : 0) + fused_ctrl_bytes(g.S, g.C, g.H);
         case PDSSM_OP_READOUT:
             return readout_w_bytes(g);
+        case PDSSM_OP_LAYER: {
+            const size_t sel = align256((size_t)g.S * g.L * g.K * 4), fwd = ws_bytes_g(g, PDSSM_OP_FWD);
+            return seq_act_bytes(g) + (sel > fwd ? sel : fwd);
+        }
         case PDSSM_OP_SEGMENT: {
             size_t fwd = plan_bytes(g) + chunk_state_bytes_g(g);
             size_t bwd = 2 * cs_f_bytes(g) + (g.P > 0 ? seq_f_bytes(g) + readout_w_bytes(g) : 0);
@@ -833,6 +837,30 @@ pdssm_status pdssm_readout(const void* h, const float* C, void* y, const pdssm_d
             return cuda_check("readout");
         });
     });
+}
+
+// ---------------------------------------------------------------------------
+// layer-level forward: select -> projection -> scan (+ readout)
+// ---------------------------------------------------------------------------
+pdssm_status pdssm_layer_fwd(const void* x, const void* S, const uint16_t* dict_idx, const void* diag, const void* Bw,
+                             const float* C_opt, const float* h0_opt, uint8_t* kstar, void* h_out_opt, void* y_opt,
+                             void* chunk_state, const pdssm_dims* dims, void* ws, size_t ws_bytes,
+                             pdssm_stream_t stream) {
+    Geo g;
+    pdssm_status r = geo_of(dims, &g);
+    if (r) return r;
+    if (!x || !S || !dict_idx || !diag || !Bw || !kstar || !chunk_state)
+        return fail(PDSSM_ERR_NULL, "layer_fwd: x, S, dict_idx, diag, Bw, kstar, chunk_state are required");
+    if (g.d_in < 1) return fail(PDSSM_ERR_SHAPE, "layer_fwd: d_in must be >= 1");
+    const size_t need = ws_bytes_g(g, PDSSM_OP_LAYER);
+    if (!ws || ws_bytes < need) return fail(PDSSM_ERR_WORKSPACE, "layer_fwd: workspace too small (need %zu)", need);
+    char* b = static_cast<char*>(ws);                 // b_t [B][H][L][c][N] act
+    char* rest = b + seq_act_bytes(g);
+    const size_t rest_bytes = ws_bytes - seq_act_bytes(g);
+    if ((r = pdssm_select(x, S, dict_idx, kstar, nullptr, nullptr, dims, rest, rest_bytes, stream))) return r;
+    if ((r = pdssm_project(x, Bw, b, dims, stream))) return r;
+    return pdssm_scan_fwd(kstar, dict_idx, diag, b, h0_opt, C_opt, h_out_opt, y_opt, chunk_state, nullptr, dims, rest,
+                          rest_bytes, stream);
 }
 
 // ---------------------------------------------------------------------------

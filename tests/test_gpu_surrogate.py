@@ -148,3 +148,34 @@ def test_autograd_scan_matches_oracle(P):
     assert rl(cp(bias.grad), db_r) <= 1e-4
     assert rl(cp(diag.grad), dD_r) <= 1e-4
     assert rl(cp(h0.grad), dh0_r) <= 1e-4
+
+
+@pytest.mark.parametrize("c,N,bf16", [(2, 128, False), (1, 64, False), (2, 64, True)])
+def test_layer_fwd_parity(P, c, N, bf16):
+    """pdssm_layer_fwd (select -> b = Bx -> scan -> y = Re(Ch)) against the oracle chain.
+    Integer-valued x, S make the selections exact (reading R18), so k* is compared bit for bit."""
+    B, H, L, K, d_in, Pp = 2, 2, 200, 8, 64, 32
+    x = synth.tokens_x(B, L, d_in, seed=N, integer=True)
+    S = synth.selector(H, K, d_in, seed=N, integer=True)
+    di = synth.random_maps(H, K, N, seed=N)
+    Dk = synth.diag((H, K), N, c, seed=N)
+    Bw = synth.projection_B(H, c, N, d_in, seed=N)
+    C = synth.readout_C(H, Pp, N, c, seed=N)
+    if bf16:
+        Bw = synth.round_bf16(Bw)
+    dt = torch.bfloat16 if bf16 else torch.float32
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    r = P.layer_fwd(cu(x).to(dt), cu(S).to(dt), cu(di).to(torch.int16), cu(Dk), cu(Bw).to(dt), C=cu(C), per_dict=True)
+    torch.cuda.synchronize()
+    ks_ref, _ = O.select(x.astype(np.float64), S.astype(np.float64))
+    assert np.array_equal(r["kstar"].cpu().numpy(), ks_ref)
+    Pm = O.gather_P(di, ks_ref)
+    Dz = O.gather_D_per_dict(O.planes_to_complex(Dk), ks_ref)
+    Bc = Bw[:, 0].astype(np.float64) + (1j * Bw[:, 1].astype(np.float64) if c == 2 else 0)
+    h = O.scan_forward(Pm, Dz, O.project_b(x.astype(np.float64), Bc))
+    Cc = C[:, 0].astype(np.float64) + (1j * C[:, 1].astype(np.float64) if c == 2 else 0)
+    y = O.readout(h, Cc)
+    tol = 3e-2 if bf16 else 1e-4
+    hg = O.planes_to_complex(r["h"].float().cpu().numpy())
+    assert float(np.max(np.abs(hg - h)) / np.max(np.abs(h))) <= tol
+    assert rel(r["y"].float().cpu().numpy(), y) <= tol
