@@ -25,48 +25,118 @@ namespace pdssm {
 namespace sg {
 
 // ----------------------------------------------------------------------------- selector
-// one warp per (b, h, t) row of K <= 256 logits, held in registers (lane owns k = lane + 32 m)
+// one warp per SG_ROWS consecutive (b, h, t) rows of K <= 256 logits, held in registers
+// (lane owns k = lane + 32 m); all rows' loads are issued before any reduction.
+constexpr int SG_ROWS = 4;
 template <int KM>   // ceil(K / 32) logits per lane
 __global__ void k_select_grad(const float* __restrict__ logits, const uint8_t* __restrict__ kstar,
                               const float* __restrict__ gsel, float* __restrict__ dlogits, int64_t rows, int K,
                               float invT) {
     const int lane = threadIdx.x & 31;
-    const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int64_t r0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * SG_ROWS;
+    if (r0 >= rows) return;
+    float v[SG_ROWS][KM], gr[SG_ROWS];
+    int ks[SG_ROWS];
+#pragma unroll
+    for (int q = 0; q < SG_ROWS; ++q) {
+        const int64_t r = r0 + q;
+        const bool ok = r < rows;
+        ks[q] = ok ? min((int)kstar[r], K - 1) : 0;
+        gr[q] = ok ? gsel[r] : 0.f;
+#pragma unroll
+        for (int m = 0; m < KM; ++m) {
+            const int k = lane + 32 * m;
+            v[q][m] = (ok && k < K) ? logits[r * K + k] * invT : -INFINITY;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < SG_ROWS; ++q) {
+        const int64_t r = r0 + q;
+        float mx = -INFINITY;
+#pragma unroll
+        for (int m = 0; m < KM; ++m) mx = fmaxf(mx, v[q][m]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        float sum = 0.f;
+#pragma unroll
+        for (int m = 0; m < KM; ++m) {
+            v[q][m] = lane + 32 * m < K ? expf(v[q][m] - mx) : 0.f;
+            sum += v[q][m];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        const float rs = 1.f / sum;
+        float eks = 0.f;   // exp of the selected logit: lane ks % 32, slot ks / 32
+#pragma unroll
+        for (int m = 0; m < KM; ++m) {
+            const float e = __shfl_sync(0xffffffffu, v[q][m], ks[q] & 31);
+            if ((ks[q] >> 5) == m) eks = e;
+        }
+        const float coef = gr[q] * eks * rs * invT;
+        if (r < rows) {
+#pragma unroll
+            for (int m = 0; m < KM; ++m) {
+                const int k = lane + 32 * m;
+                if (k < K) dlogits[r * K + k] = coef * ((k == ks[q] ? 1.f : 0.f) - v[q][m] * rs);
+            }
+        }
+    }
+}
+
+// small K (<= KP, KP in {32, 64}): one THREAD per row, the row's logits in registers
+// (fixed-order serial reductions): ~10x fewer warp instructions than the warp-per-row form.
+template <int KP>
+__global__ void __launch_bounds__(128) k_select_grad_row(const float* __restrict__ logits, const uint8_t* __restrict__ kstar,
+                                                         const float* __restrict__ gsel, float* __restrict__ dlogits,
+                                                         int64_t rows, int K, float invT) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= rows) return;
     const float* z = logits + r * K;
     const int ks = min((int)kstar[r], K - 1);
     const float gr = gsel[r];
-    float v[KM];
+    float v[KP];
+    const bool vec = (K & 3) == 0;   // 16-byte rows
+    if (vec) {
+#pragma unroll
+        for (int k = 0; k < KP; k += 4) {
+            if (k < K) {
+                const float4 q = __ldg(reinterpret_cast<const float4*>(z + k));
+                v[k] = q.x; v[k + 1] = q.y; v[k + 2] = q.z; v[k + 3] = q.w;
+            } else {
+                v[k] = v[k + 1] = v[k + 2] = v[k + 3] = -INFINITY;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < KP; ++k) v[k] = k < K ? __ldg(z + k) : -INFINITY;
+    }
     float mx = -INFINITY;
 #pragma unroll
-    for (int m = 0; m < KM; ++m) {
-        const int k = lane + 32 * m;
-        v[m] = k < K ? z[k] * invT : -INFINITY;
-        mx = fmaxf(mx, v[m]);
+    for (int k = 0; k < KP; ++k) {
+        v[k] *= invT;
+        mx = fmaxf(mx, v[k]);
     }
+    float sum = 0.f, eks = 0.f;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    float sum = 0.f;
-#pragma unroll
-    for (int m = 0; m < KM; ++m) {
-        v[m] = lane + 32 * m < K ? expf(v[m] - mx) : 0.f;
-        sum += v[m];
+    for (int k = 0; k < KP; ++k) {
+        v[k] = k < K ? expf(v[k] - mx) : 0.f;
+        sum += v[k];
+        if (k == ks) eks = v[k];
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
     const float rs = 1.f / sum;
-    const float ek = __shfl_sync(0xffffffffu, v[0], ks & 31);   // exp of the selected logit: lane ks % 32, slot ks / 32
-    float eks = ek;
-#pragma unroll
-    for (int m = 1; m < KM; ++m) {
-        const float e = __shfl_sync(0xffffffffu, v[m], ks & 31);
-        if ((ks >> 5) == m) eks = e;
-    }
     const float coef = gr * eks * rs * invT;
+    float* o = dlogits + r * K;
+    if (vec) {
 #pragma unroll
-    for (int m = 0; m < KM; ++m) {
-        const int k = lane + 32 * m;
-        if (k < K) dlogits[r * K + k] = coef * ((k == ks ? 1.f : 0.f) - v[m] * rs);
+        for (int k = 0; k < KP; k += 4)
+            if (k < K)
+                *reinterpret_cast<float4*>(o + k) =
+                    make_float4(coef * ((k == ks ? 1.f : 0.f) - v[k] * rs), coef * ((k + 1 == ks ? 1.f : 0.f) - v[k + 1] * rs),
+                                coef * ((k + 2 == ks ? 1.f : 0.f) - v[k + 2] * rs), coef * ((k + 3 == ks ? 1.f : 0.f) - v[k + 3] * rs));
+    } else {
+#pragma unroll
+        for (int k = 0; k < KP; ++k)
+            if (k < K) o[k] = coef * ((k == ks ? 1.f : 0.f) - v[k] * rs);
     }
 }
 
@@ -330,6 +400,12 @@ __device__ __forceinline__ void load_raw(const DictArgs& a, int h, int k, const 
         for (int u = 0; u < RPC; ++u) {
             const int r = RPC * ch + u;
             float* v = &raw[m][u * 3 * NC];
+#ifdef DG_NOLOAD   // timing experiment only: constant operands, no global loads
+            if (r < nb) {
+#pragma unroll
+                for (int z = 0; z < 3 * NC; ++z) v[z] = 0.5f + (float)(rows[r] & 7);
+            } else
+#else
             if (r < nb) {
                 const int c = rows[r];
                 const bool first = c < 0;
@@ -361,7 +437,9 @@ __device__ __forceinline__ void load_raw(const DictArgs& a, int h, int k, const 
                     hv[0] = 0.f;
                     if constexpr (NC == 2) hv[1] = 0.f;
                 }
-            } else {
+            } else
+#endif
+            {
 #pragma unroll
                 for (int z = 0; z < 3 * NC; ++z) v[z] = 0.f;
             }
@@ -463,11 +541,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_dict_grad_tc(DictArgs a) {
         qh += nbs[il];
         const int s = nbatch & 1;
         uint8_t* st = smem + (size_t)s * TC_STAGE;
+#ifndef DG_NOMMA
         if (nbatch >= 2) tc::mbar_wait(done + s, (uint32_t)((nbatch - 2) >> 1) & 1u);   // MMAs of batch n-2 read it
+#endif
         convert_store<NC>(cur, tc::su32(st));
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> MMA reads
         __syncthreads();
+#ifdef DG_NOMMA   // timing experiment only
+        if (false) {
+#else
         if (tid == 0) {
+#endif
             tc::fence_after();
             const uint64_t ah = tc::sdesc(tc::su32(st)), al = tc::sdesc(tc::su32(st + TC_SLAB));
             const uint64_t bh = tc::sdesc(tc::su32(st + 2 * TC_SLAB)), bl = tc::sdesc(tc::su32(st + 3 * TC_SLAB));
@@ -486,7 +570,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_dict_grad_tc(DictArgs a) {
     while (iter(R0, R2, 0, 2) && iter(R1, R0, 1, 0) && iter(R2, R1, 2, 1)) {
     }
     // drain: the last batch's commit covers every earlier MMA
+#ifndef DG_NOMMA
     if (nbatch > 0) tc::mbar_wait(done + ((nbatch - 1) & 1), (uint32_t)((nbatch - 1) >> 1) & 1u);
+#endif
     tc::fence_after();
     __syncthreads();
     float* Gs = reinterpret_cast<float*>(smem);   // [N][N+1] over the (now idle) operand stages

@@ -876,10 +876,15 @@ pdssm_status pdssm_select_grad(const float* logits, const uint8_t* kstar, const 
     if (misaligned(logits, 4) || misaligned(gsel, 4) || misaligned(dlogits, 4)) return fail(PDSSM_ERR_ALIGN, "select_grad: misaligned");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     const int64_t rows = g.S * g.L;
+    if (g.K <= 64 && !misaligned(logits, 16) && !misaligned(dlogits, 16)) {
+        auto kr = g.K <= 32 ? sg::k_select_grad_row<32> : sg::k_select_grad_row<64>;
+        kr<<<(unsigned)ceil_div(rows, 128), 128, 0, st>>>(logits, kstar, gsel, dlogits, rows, (int)g.K, 1.f / temp);
+        return cuda_check("select_grad");
+    }
     const int km = (int)ceil_div(g.K, 32);
     auto kern = km == 1 ? sg::k_select_grad<1> : km == 2 ? sg::k_select_grad<2> : km <= 4 ? sg::k_select_grad<4>
                                                                                         : sg::k_select_grad<8>;
-    kern<<<(unsigned)ceil_div(rows, 8), 256, 0, st>>>(logits, kstar, gsel, dlogits, rows, (int)g.K, 1.f / temp);
+    kern<<<(unsigned)ceil_div(rows, 8 * sg::SG_ROWS), 256, 0, st>>>(logits, kstar, gsel, dlogits, rows, (int)g.K, 1.f / temp);
     return cuda_check("select_grad");
 }
 
