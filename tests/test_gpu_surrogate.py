@@ -179,3 +179,41 @@ def test_layer_fwd_parity(P, c, N, bf16):
     hg = O.planes_to_complex(r["h"].float().cpu().numpy())
     assert float(np.max(np.abs(hg - h)) / np.max(np.abs(h))) <= tol
     assert rel(r["y"].float().cpu().numpy(), y) <= tol
+
+
+@pytest.mark.parametrize("K", [100, 256])
+def test_select_grad_warp_path(P, K):
+    """K > 64 takes the warp-per-row kernel (logits in registers, KM = ceil(K / 32))."""
+    B, H, L, T = 1, 2, 33, 0.7
+    rng = np.random.default_rng(K + 1)
+    logits = rng.normal(size=(B, H, L, K)).astype(np.float32)
+    ks = rng.integers(0, K, size=(B, H, L)).astype(np.uint8)
+    g = rng.normal(size=(B, H, L)).astype(np.float32)
+    d = P.select_grad(torch.from_numpy(logits).cuda(), torch.from_numpy(ks).cuda(), torch.from_numpy(g).cuda(), T)
+    ref = O.selector_grad(logits.astype(np.float64), ks, g.astype(np.float64), T)
+    assert rel(d.cpu().numpy(), ref) <= 1e-5
+
+
+@pytest.mark.parametrize("N", [128, 64])
+def test_dict_grad_first_steps_without_h0(P, N):
+    """L = 1 (every selected step is t = 0, h_{-1} = h0 = 0 -> w = 0 -> G = 0) and L = 2 without h0."""
+    for L in (1, 2):
+        B, H, K, c = 3, 2, 4, 2
+        inp = synth.scan_inputs(B, H, L, N, K, c, seed=L + N, dh=True)
+        d = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in inp.items()}
+        d["dict_idx"] = d["dict_idx"].to(torch.int16)
+        M = torch.from_numpy(synth.dictionary(H, K, N, 3)).cuda()
+        f = P.scan_fwd(d["kstar"], d["dict_idx"], d["diag"], d["bias"])
+        db = P.scan_bwd(d["kstar"], d["dict_idx"], d["diag"], f["h"], f["chunk_state"], f["dims"], dh=d["dh"])[0]
+        dM, G = P.dict_grad(M, d["kstar"], d["diag"], f["h"], db, 1.0, f["dims"], want_G=True)
+        torch.cuda.synchronize()
+        Pm = O.gather_P(inp["dict_idx"], inp["kstar"])
+        Dz, bz, e = (O.planes_to_complex(inp[k]) for k in ("diag", "bias", "dh"))
+        h = O.scan_forward(Pm, Dz, bz)
+        lam = O.scan_backward(Pm, Dz, h, e)[0]
+        G_ref = O.dictionary_outer(inp["kstar"], lam, Dz, h, K)
+        if L == 1:
+            assert np.all(G.cpu().numpy() == 0.0) and np.all(dM.cpu().numpy() == 0.0)
+        else:
+            assert rel(G.cpu().numpy(), G_ref) <= 1e-4
+            assert rel(dM.cpu().numpy(), O.dictionary_grad(M.cpu().numpy().astype(np.float64), G_ref, 1.0)) <= 1e-4
