@@ -336,14 +336,25 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
         const int mc = m, kc = k;
         const float bcr = Br, bci = Bi;
         const uint8_t* rpc = sb + r * ROWB;
+#ifndef FWD_EXP_NOBAR   // timing experiment only: no exchange barrier (wrong results)
         compute_sync(N);
+#endif
         SV v[CAP];
+#if defined(FWD_EXP_SLOTS)   // timing experiment only: FWD_EXP_SLOTS gather slots (wrong results)
+#pragma unroll
+        for (int q = 0; q < CAP; ++q) {
+            float re = 0.f, im = 0.f;
+            if (q < FWD_EXP_SLOTS) lds_sv<NC>(ga[q], re, im);
+            v[q] = fused::mk<NC>(re, im);
+        }
+#else
 #pragma unroll
         for (int q = 0; q < CAP; ++q) {
             float re, im;
             lds_sv<NC>(ga[q], re, im);
             v[q] = fused::mk<NC>(re, im);
         }
+#endif
         if (r == 0 && i == 0 && g >= 1) {   // every compute thread is done with the previous group's slot
             mbar_arrive(bars + R + (slot == 0 ? R - 1 : slot - 1));
         }
