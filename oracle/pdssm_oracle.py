@@ -32,6 +32,7 @@ __all__ = [
     "scan_backward", "scan_backward_chunked",
     "segment_summary", "compose_summaries",
     "softmax_T", "selector_grad", "dictionary_outer", "dictionary_grad",
+    "diag_generator",
 ]
 
 
@@ -519,3 +520,22 @@ def dictionary_grad(M, G, T):
     G = np.asarray(G, dtype=np.float64)
     proj = (sig * G).sum(axis=-2, keepdims=True)         # sigma_j^T G[:, j]
     return sig * (G - proj) / float(T)
+
+
+# ----------------------------------------------------------------------------
+# NEXT-2: the input-dependent diagonal D_t = D(u_t) (form fixed by
+# SPEC.md:367, reading R30): magnitude sigmoid(w^mag u_t + bias^mag) times phase exp(i w^phase u_t)
+# ----------------------------------------------------------------------------
+def diag_generator(x, W_mag, W_phase=None, bias_mag=None):
+    """D[b,h,t,n] = sigmoid((W_mag[h] x_t)[n] + bias_mag[h,n]) * exp(i (W_phase[h] x_t)[n])
+    (real mode, W_phase None: the magnitude alone).  x [B][L][d_in]; W_mag, W_phase [H][N][d_in];
+    bias_mag [H][N] or None -> complex128 [B][H][L][N]."""
+    x = np.asarray(x, dtype=np.float64)
+    a = np.einsum("hnd,btd->bhtn", np.asarray(W_mag, np.float64), x)
+    if bias_mag is not None:
+        a = a + np.asarray(bias_mag, np.float64)[None, :, None, :]
+    mag = 1.0 / (1.0 + np.exp(-a))
+    if W_phase is None:
+        return mag.astype(np.complex128)
+    th = np.einsum("hnd,btd->bhtn", np.asarray(W_phase, np.float64), x)
+    return mag * np.exp(1j * th)

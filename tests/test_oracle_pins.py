@@ -541,3 +541,28 @@ def test_dictionary_grad_finite_differences(T):
     assert np.max(np.abs(got - fd)) <= 1e-7 * max(1.0, np.max(np.abs(fd)))
     assert np.allclose(got.sum(axis=-2), 0.0, atol=1e-12)   # every column sums to zero
     assert np.all(got[0, 2] == 0.0)                           # an unselected entry gets no gradient
+
+
+# ---------------------------------------------------------------------------
+# NEXT-2: D_t generator (SPEC.md:367 form; reading R30)
+def test_diag_generator_special_cases():
+    rng = np.random.default_rng(81)
+    B, H, L, N, d = 2, 2, 5, 6, 4
+    x = rng.normal(size=(B, L, d))
+    Wm, Wp = rng.normal(size=(H, N, d)), rng.normal(size=(H, N, d))
+    beta = rng.normal(size=(H, N))
+    # zero weights: D = sigmoid(bias) exactly (real, in (0, 1)); sigmoid(0) = 1/2
+    D0 = O.diag_generator(x, np.zeros_like(Wm), np.zeros_like(Wp), beta)
+    assert np.allclose(D0.imag, 0.0) and np.allclose(D0.real, np.broadcast_to((1 / (1 + np.exp(-beta)))[None, :, None, :], D0.shape))
+    assert np.allclose(O.diag_generator(x, np.zeros_like(Wm)), 0.5)
+    # |D| < 1 always (the stability bound of SURVEY §8(d)); real mode = the magnitude of complex mode
+    D = O.diag_generator(x, Wm, Wp, beta)
+    assert np.all(np.abs(D) < 1.0)
+    assert np.allclose(np.abs(D), O.diag_generator(x, Wm, None, beta).real)
+    # doubling the phase weights squares the unit phase: D2 = |D| (D / |D|)^2
+    D2 = O.diag_generator(x, Wm, 2 * Wp, beta)
+    assert np.allclose(D2, np.abs(D) * (D / np.abs(D)) ** 2)
+    # the phase weights act linearly on x: flipping x's sign conjugates the phase
+    Dn = O.diag_generator(-x, np.zeros_like(Wm), Wp, np.zeros((H, N)))
+    Dp = O.diag_generator(x, np.zeros_like(Wm), Wp, np.zeros((H, N)))
+    assert np.allclose(Dn, np.conj(Dp))
