@@ -176,6 +176,22 @@ pdssm_status pdssm_project(const void* x, const void* Bw, void* b_out, const pds
                            pdssm_stream_t stream);
 
 /* ---------------------------------------------------------------------------
+ * NEXT-2: the input-dependent diagonal D_t = D(u_t) (the form is never
+ * given in the paper -- SPEC.md:367 fixes it, reading R30):
+ *   D[b][h][t][n] = sigmoid((W_mag x_t)[n] + bias[h][n]) * exp(i (W_phase x_t)[n])
+ * (real mode c = 1: the magnitude alone), written in the scan layout as PER_STEP diag.
+ *   x        act [B][L][d_in]
+ *   Wd       act [H][c][N][d_in]   plane 0 = W_mag rows, plane 1 = W_phase rows
+ *   bias_opt f32 [H][N]            magnitude bias (NULL = 0)
+ *   D_out    act [B][H][L][c][N]   out
+ * Path: tcgen05 GEMM with the sigmoid / sincos epilogue fused (one head's c*N <= 256 columns
+ * per tile; N % 16 == 0; 16-byte aligned operands); otherwise pdssm_project + an elementwise
+ * kernel.  fp32 accumulation (3xTF32 for f32 operands).
+ * ------------------------------------------------------------------------- */
+pdssm_status pdssm_diag_gen(const void* x, const void* Wd, const float* bias_opt, void* D_out,
+                            const pdssm_dims* dims, pdssm_stream_t stream);
+
+/* ---------------------------------------------------------------------------
  * a8 readout, standalone (the same kernel pdssm_scan_fwd runs for y_opt):
  * y_t = Re(C_h h_t) = C_re h_re - C_im h_im (Eq. 1 y_t = C x_t with psi = Re)
  *   h   act [B][H][L][c][N]   states (e.g. h_out of pdssm_scan_fwd)

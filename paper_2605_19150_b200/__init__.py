@@ -18,7 +18,7 @@ import re
 __all__ = [
     "PdssmError", "Dims", "lib", "sparsify", "select", "scan_fwd", "scan_bwd",
     "segment_summary", "compose_carry", "segment_summary_bwd", "compose_lambda",
-    "check_device", "chunk_state_views", "select_grad", "dict_grad", "scan", "layer_fwd", "default_chunk", "workspace_bytes",
+    "check_device", "chunk_state_views", "select_grad", "dict_grad", "scan", "layer_fwd", "diag_gen", "default_chunk", "workspace_bytes",
     "F32", "BF16", "PER_STEP", "PER_DICT", "CHECK_FINITE", "EXPORT_MAPS",
 ]
 
@@ -76,6 +76,7 @@ def _load():
         "pdssm_segment_summary_bwd": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, D, vp, sz, vp]),
         "pdssm_compose_lambda": (ctypes.c_int, [vp, vp, i32, i32, vp, D, vp]),
         "pdssm_select_grad": (ctypes.c_int, [vp, vp, vp, ctypes.c_float, vp, D, vp]),
+        "pdssm_diag_gen": (ctypes.c_int, [vp, vp, vp, vp, D, vp]),
         "pdssm_layer_fwd": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, D, vp, sz, vp]),
         "pdssm_dict_grad": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, ctypes.c_float, vp, vp, D, vp]),
         "pdssm_status_string": (ctypes.c_char_p, [ctypes.c_int]),
@@ -308,6 +309,19 @@ def scan_bwd(kstar, dict_idx, diag, h_saved, chunk_state, dims, dh=None, dy=None
                               _ptr(dh), _ptr(dy), _ptr(C), _ptr(lam_in), _ptr(db), _ptr(dD), _ptr(g), _ptr(dh0),
                               ctypes.byref(dims), _ptr(ws), wsb, _stream()))
     return db, dD, g, dh0
+
+
+def diag_gen(x, Wd, bias=None, out=None):
+    """NEXT-2 D_t generator: D = sigmoid(W_mag x + bias) exp(i W_phase x) -> act [B,H,L,c,N] (PER_STEP diag)."""
+    torch = _torch()
+    for n, t in (("x", x), ("Wd", Wd), ("bias", bias)):
+        _contig(t, n)
+    B, L, d_in = x.shape
+    H, c, N, _ = Wd.shape
+    dims = make_dims(B, H, L, N, 1, c=c, dtype=_dtype_code(x), d_in=d_in)
+    D = torch.empty((B, H, L, c, N), dtype=x.dtype, device=x.device) if out is None else out
+    _check(lib.pdssm_diag_gen(_ptr(x), _ptr(Wd), _ptr(bias), _ptr(D), ctypes.byref(dims), _stream()))
+    return D
 
 
 def layer_fwd(x, S, dict_idx, diag, Bw, C=None, h0=None, per_dict=True, want_h=True, out=None):

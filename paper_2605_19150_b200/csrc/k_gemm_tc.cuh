@@ -282,6 +282,64 @@ struct EpiProject {
     }
 };
 
+// NEXT-2 D_t generator (SPEC.md:367 form, reading R30): one tile = one head's c*N columns
+// [a_0..a_{N-1} | theta_0..theta_{N-1}] of a token row; the epilogue writes
+// D[b][h][t][c][n] = sigmoid(a + bias[h][n]) (cos theta, sin theta)   (c = 1: the magnitude)
+template <typename TO>
+struct EpiDiag {
+    TO* out;
+    const float* bias;   // [H][N] or null
+    int64_t M;
+    int L, H, N, nc;
+    __device__ void operator()(uint32_t taddr, int64_t m, int n0, int bn, int z) const {
+        (void)z;
+        (void)bn;
+        const bool valid = m < M;
+        const int64_t b = valid ? m / L : 0, t = valid ? m - b * L : 0;
+        const int cN = nc * N;
+        const int h = n0 / cN;
+        TO* dst = out + (((size_t)b * H + h) * L + t) * cN;
+        for (int c0 = 0; c0 < N; c0 += 16) {
+            float a[16], th[16];
+            tmem_ld16(taddr + (uint32_t)c0, a);
+            if (nc == 2) tmem_ld16(taddr + (uint32_t)(c0 + N), th);
+            if (!valid) continue;
+            float re[16], im[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const float mag = 1.f / (1.f + expf(-(a[i] + (bias ? bias[(size_t)h * N + c0 + i] : 0.f))));
+                if (nc == 2) {
+                    float sn, cs;
+                    sincosf(th[i], &sn, &cs);
+                    re[i] = mag * cs;
+                    im[i] = mag * sn;
+                } else {
+                    re[i] = mag;
+                    im[i] = 0.f;
+                }
+            }
+            st16_act(dst + c0, re);
+            if (nc == 2) st16_act(dst + N + c0, im);
+        }
+    }
+    template <typename T2>
+    __device__ static void st16_act(T2* d, const float (&v)[16]) {
+        if constexpr (std::is_same<T2, float>::value) {
+#pragma unroll
+            for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4*>(d + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        } else {
+            uint32_t p[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const __nv_bfloat162 q = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+                p[i] = *reinterpret_cast<const uint32_t*>(&q);
+            }
+            reinterpret_cast<uint4*>(d)[0] = make_uint4(p[0], p[1], p[2], p[3]);
+            reinterpret_cast<uint4*>(d)[1] = make_uint4(p[4], p[5], p[6], p[7]);
+        }
+    }
+};
+
 // store 16 consecutive fp32 values as TO (16-byte vector stores; dst 16-byte aligned)
 template <typename TO>
 __device__ __forceinline__ void st16(TO* dst, const float (&v)[16]) {

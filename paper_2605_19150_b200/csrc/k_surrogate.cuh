@@ -625,5 +625,28 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_dict_grad_tc(DictArgs a) {
     }
 }
 
+// NEXT-2 D_t generator, SIMT fallback: the projection writes raw (a, theta) planes, then
+// this kernel applies sigmoid / sincos in place.  rows = B*H*L in [B][H][L] order.
+template <typename T>
+__global__ void k_diag_activate(T* __restrict__ D, const float* __restrict__ bias, int64_t rows, int H, int L, int N,
+                                int nc) {
+    const int64_t total = rows * N;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / N;
+        const int n = (int)(i - r * N);
+        const int h = (int)((r / L) % H);
+        T* row = D + r * (int64_t)nc * N;
+        const float mag = 1.f / (1.f + expf(-(ldact(row + n) + (bias ? bias[(size_t)h * N + n] : 0.f))));
+        if (nc == 2) {
+            float sn, cs;
+            sincosf(ldact(row + N + n), &sn, &cs);
+            stact(row + n, mag * cs);
+            stact(row + N + n, mag * sn);
+        } else {
+            stact(row + n, mag);
+        }
+    }
+}
+
 }  // namespace sg
 }  // namespace pdssm

@@ -809,6 +809,34 @@ pdssm_status pdssm_project(const void* x, const void* Bw, void* b_out, const pds
     });
 }
 
+pdssm_status pdssm_diag_gen(const void* x, const void* Wd, const float* bias_opt, void* D_out, const pdssm_dims* dims,
+                            pdssm_stream_t stream) {
+    Geo g;
+    pdssm_status r = geo_of(dims, &g);
+    if (r) return r;
+    if (g.d_in < 1) return fail(PDSSM_ERR_SHAPE, "diag_gen: d_in must be >= 1");
+    if (!x || !Wd || !D_out) return fail(PDSSM_ERR_NULL, "diag_gen: x, Wd, D_out are required");
+    if (misaligned(x, g.act) || misaligned(Wd, g.act) || misaligned(D_out, g.act) || misaligned(bias_opt, 4))
+        return fail(PDSSM_ERR_ALIGN, "diag_gen: misaligned pointer");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t cN = g.nc * g.N, NN = g.H * cN;
+    if (g.N % 16 == 0 && cN <= 256 && tc_operands_ok(g, {x, Wd, D_out})) {
+        return with_act(g.dtype, [&](auto tv) {
+            using T = decltype(tv);
+            tc::EpiDiag<T> epi{static_cast<T*>(D_out), bias_opt, g.B * g.L, (int)g.L, (int)g.H, (int)g.N, (int)g.nc};
+            return launch_tc<T>(g, x, g.B * g.L, Wd, NN, (int)cN, epi, st, "diag_gen_tc");   // one head per tile
+        });
+    }
+    if ((r = pdssm_project(x, Wd, D_out, dims, stream))) return r;
+    return with_act(g.dtype, [&](auto tv) {
+        using T = decltype(tv);
+        const int64_t rows = g.S * g.L;
+        sg::k_diag_activate<T><<<(unsigned)std::min<int64_t>(ceil_div(rows * g.N, 256), 65535), 256, 0, st>>>(
+            static_cast<T*>(D_out), bias_opt, rows, (int)g.H, (int)g.L, (int)g.N, (int)g.nc);
+        return cuda_check("diag_activate");
+    });
+}
+
 pdssm_status pdssm_readout(const void* h, const float* C, void* y, const pdssm_dims* dims, void* ws, size_t ws_bytes,
                            pdssm_stream_t stream) {
     Geo g;

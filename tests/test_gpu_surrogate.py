@@ -217,3 +217,25 @@ def test_dict_grad_first_steps_without_h0(P, N):
         else:
             assert rel(G.cpu().numpy(), G_ref) <= 1e-4
             assert rel(dM.cpu().numpy(), O.dictionary_grad(M.cpu().numpy().astype(np.float64), G_ref, 1.0)) <= 1e-4
+
+
+@pytest.mark.parametrize("c,N,bf16,path", [(2, 128, False, "tc"), (1, 128, False, "tc"), (2, 64, True, "tc"),
+                                            (2, 128, False, "generic"), (1, 24, False, "tc")])
+def test_diag_gen_parity(P, c, N, bf16, path, monkeypatch):
+    """NEXT-2 D_t generator (fused sigmoid / sincos epilogue, or projection + elementwise) vs the oracle."""
+    if path == "generic":
+        monkeypatch.setenv("PDSSM_PATH", "generic")
+    B, H, L, d_in = 2, 3, 150, 64
+    rng = np.random.default_rng(N + c)
+    x = rng.normal(size=(B, L, d_in)).astype(np.float32)
+    Wd = (rng.uniform(-1, 1, size=(H, c, N, d_in)) / np.sqrt(d_in)).astype(np.float32)
+    bias = rng.normal(2.0, 1.0, size=(H, N)).astype(np.float32)
+    if bf16:
+        x, Wd = synth.round_bf16(x), synth.round_bf16(Wd)
+    dt = torch.bfloat16 if bf16 else torch.float32
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    D = P.diag_gen(cu(x).to(dt), cu(Wd).to(dt), cu(bias))
+    torch.cuda.synchronize()
+    ref = O.diag_generator(x, Wd[:, 0], Wd[:, 1] if c == 2 else None, bias)
+    got = O.planes_to_complex(D.float().cpu().numpy())
+    assert float(np.max(np.abs(got - ref)) / np.max(np.abs(ref))) <= (2e-2 if bf16 else 1e-4)
