@@ -214,6 +214,9 @@ def layer_kernels(P, torch, dev, adt, dtype, B, L, H, N, K, c, stream):
     Dk = (torch.rand((H, K, c, N), device=dev, generator=g) * 2 - 1) * 0.7
     lo = {"kstar": torch.empty((B, H, L), device=dev, dtype=torch.uint8), "h": bout, "y": y}
     tl = t(lambda: P.layer_fwd(x, S, di, Dk, Bw, C=Cw, per_dict=True, out=lo))
+    Dout = torch.empty((B, H, L, c, N), device=dev, dtype=adt)
+    bmag = torch.randn((H, N), device=dev, generator=g) + 2.0
+    tg_ = t(lambda: P.diag_gen(x, Bw, bmag, out=Dout))   # NEXT-2 D_t generator (fused sigmoid/sincos epilogue)
     ts = t(lambda: P.select(x, S))
     tp = t(lambda: P.project(x, Bw, out=bout))
     tr = t(lambda: P.readout(bout, Cw, out=y, ws=wsr))
@@ -224,7 +227,7 @@ def layer_kernels(P, torch, dev, adt, dtype, B, L, H, N, K, c, stream):
     out = {"dtype": dtype, "tensor_peak_tflops": peak,
            "tensor_peak_kind": "measured bf16 burst" + (" / 6 (3xTF32)" if dtype != "bf16" else ""),
            "shape": {"d_in": d_in, "P": Pp, "K": K}}
-    for name, us, fl in (("select", ts, f_sel), ("project", tp, f_prj), ("readout", tr, f_rd)):
+    for name, us, fl in (("select", ts, f_sel), ("project", tp, f_prj), ("readout", tr, f_rd), ("diag_gen", tg_, f_prj)):
         tf = fl / (us * 1e-6) / 1e12
         out[name] = {"us": us, "tflops": tf, "frac": tf / peak}
     out["layer_fwd"] = {"us": tl, "tokens_per_s": B * L / (tl * 1e-6), "diag": "per_dict",
