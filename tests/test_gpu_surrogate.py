@@ -239,3 +239,29 @@ def test_diag_gen_parity(P, c, N, bf16, path, monkeypatch):
     ref = O.diag_generator(x, Wd[:, 0], Wd[:, 1] if c == 2 else None, bias)
     got = O.planes_to_complex(D.float().cpu().numpy())
     assert float(np.max(np.abs(got - ref)) / np.max(np.abs(ref))) <= (2e-2 if bf16 else 1e-4)
+
+
+def test_layer_fwd_with_generated_diag(P):
+    """NEXT-2 chain with input-dependent D_t: pdssm_diag_gen -> pdssm_layer_fwd (PER_STEP), vs the oracle
+    chain select -> D(u_t) -> b = Bx -> scan -> y."""
+    B, H, L, N, K, c, d_in, Pp = 2, 2, 160, 128, 8, 2, 64, 16
+    x = synth.tokens_x(B, L, d_in, seed=3, integer=True)
+    S = synth.selector(H, K, d_in, seed=3, integer=True)
+    di = synth.random_maps(H, K, N, seed=3)
+    rng = np.random.default_rng(3)
+    Wd = (rng.uniform(-1, 1, size=(H, c, N, d_in)) / (8 * np.sqrt(d_in))).astype(np.float32)
+    bias = rng.normal(2.0, 1.0, size=(H, N)).astype(np.float32)
+    Bw = synth.projection_B(H, c, N, d_in, seed=3)
+    C = synth.readout_C(H, Pp, N, c, seed=3)
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    D = P.diag_gen(cu(x), cu(Wd), cu(bias))
+    r = P.layer_fwd(cu(x), cu(S), cu(di).to(torch.int16), D, cu(Bw), C=cu(C), per_dict=False)
+    torch.cuda.synchronize()
+    ks_ref, _ = O.select(x.astype(np.float64), S.astype(np.float64))
+    assert np.array_equal(r["kstar"].cpu().numpy(), ks_ref)
+    Dz = O.diag_generator(x, Wd[:, 0], Wd[:, 1], bias)
+    h = O.scan_forward(O.gather_P(di, ks_ref), Dz, O.project_b(x.astype(np.float64), Bw[:, 0] + 1j * Bw[:, 1]))
+    y = O.readout(h, C[:, 0] + 1j * C[:, 1])
+    hg = O.planes_to_complex(r["h"].cpu().numpy())
+    assert float(np.max(np.abs(hg - h)) / np.max(np.abs(h))) <= 1e-4
+    assert rel(r["y"].cpu().numpy(), y) <= 1e-4
