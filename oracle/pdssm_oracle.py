@@ -32,7 +32,7 @@ __all__ = [
     "scan_backward", "scan_backward_chunked",
     "segment_summary", "compose_summaries",
     "softmax_T", "selector_grad", "dictionary_outer", "dictionary_grad",
-    "diag_generator",
+    "diag_generator", "soft_generator_P",
 ]
 
 
@@ -539,3 +539,16 @@ def diag_generator(x, W_mag, W_phase=None, bias_mag=None):
         return mag.astype(np.complex128)
     th = np.einsum("hnd,btd->bhtn", np.asarray(W_phase, np.float64), x)
     return mag * np.exp(1j * th)
+
+
+# ----------------------------------------------------------------------------
+# NEXT-3: the PD-SSM (soft) generator Flash PD-SSM replaces (Eqs. 2-4)
+# ----------------------------------------------------------------------------
+def soft_generator_P(logits, M):
+    """P(u_t) of PD-SSM: s = softmax(S u_t) (Eq. 2), M(u_t) = sum_k s_k M_k (Eq. 3),
+    P_{:,j} = column_hardmax(M_{:,j}(u_t)) (Eq. 4), as the index map of the one-hot column
+    (smallest row on ties, reading R7).  Materialises the L N^2 mixture the paper names as the
+    bottleneck.  logits [B,H,L,K] (= S u_t), M [H,K,N,N] -> int [B,H,L,N]."""
+    s = softmax_T(logits, 1.0, axis=-1)
+    mix = np.einsum("bhtk,hkij->bhtij", s, np.asarray(M, np.float64))
+    return argmax_smallest(mix, axis=-2)

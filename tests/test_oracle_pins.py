@@ -566,3 +566,23 @@ def test_diag_generator_special_cases():
     Dn = O.diag_generator(-x, np.zeros_like(Wm), Wp, np.zeros((H, N)))
     Dp = O.diag_generator(x, np.zeros_like(Wm), Wp, np.zeros((H, N)))
     assert np.allclose(Dn, np.conj(Dp))
+
+
+# ---------------------------------------------------------------------------
+# NEXT-3: PD-SSM soft generator (Eqs. 2-4)
+def test_soft_generator_reduces_to_the_hard_path():
+    rng = np.random.default_rng(91)
+    B, H, L, N, K = 2, 2, 7, 6, 4
+    M = rng.normal(size=(H, K, N, N))
+    z = rng.normal(size=(B, H, L, K))
+    # a (numerically) one-hot softmax selects one entry: Eq. 4 of M_{k*} = the Flash path (Eqs. 5-8)
+    P_soft = O.soft_generator_P(z * 1e4, M)
+    P_hard = O.gather_P(O.sparsify(M), O.argmax_smallest(z, axis=-1))
+    assert np.array_equal(P_soft, P_hard)
+    # K = 1: every step is the sparsified single matrix; identical entries: s does not matter
+    P1 = O.soft_generator_P(z[..., :1], M[:, :1])
+    assert np.array_equal(P1, np.broadcast_to(O.sparsify(M[:, :1])[:, 0][None, :, None, :], P1.shape))
+    Msame = np.repeat(M[:, :1], K, axis=1)
+    assert np.array_equal(O.soft_generator_P(z, Msame), np.broadcast_to(O.sparsify(M[:, :1])[:, 0][None, :, None, :], P1.shape))
+    # a genuine mixture differs from the hard path somewhere (the relaxation is not the selection)
+    assert not np.array_equal(O.soft_generator_P(z, M), O.gather_P(O.sparsify(M), O.argmax_smallest(z, axis=-1)))
