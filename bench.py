@@ -217,6 +217,13 @@ def layer_kernels(P, torch, dev, adt, dtype, B, L, H, N, K, c, stream):
     Dout = torch.empty((B, H, L, c, N), device=dev, dtype=adt)
     bmag = torch.randn((H, N), device=dev, generator=g) + 2.0
     tg_ = t(lambda: P.diag_gen(x, Bw, bmag, out=Dout))   # NEXT-2 D_t generator (fused sigmoid/sincos epilogue)
+    # NEXT-3 PD-SSM soft generator (Eqs. 2-4) as the comparison baseline of the hard selection
+    lg = torch.randn((B, H, L, K), device=dev, generator=g)
+    Md = (torch.rand((H, K, N, N), device=dev, generator=g) * 2 - 1) / N ** 0.5
+    Pso = torch.empty((B, H, L, N), device=dev, dtype=torch.int16)
+    dso = P.make_dims(B, H, L, N, K, dtype=P.BF16 if dtype == "bf16" else P.F32)
+    wso = torch.empty(P.workspace_bytes(dso, P.OP_SOFT), dtype=torch.uint8, device=dev)
+    tso = t(lambda: P.soft_select(lg, Md, bf16=dtype == "bf16", out=Pso, ws=wso))
     ts = t(lambda: P.select(x, S))
     tp = t(lambda: P.project(x, Bw, out=bout))
     tr = t(lambda: P.readout(bout, Cw, out=y, ws=wsr))
@@ -230,6 +237,11 @@ def layer_kernels(P, torch, dev, adt, dtype, B, L, H, N, K, c, stream):
     for name, us, fl in (("select", ts, f_sel), ("project", tp, f_prj), ("readout", tr, f_rd), ("diag_gen", tg_, f_prj)):
         tf = fl / (us * 1e-6) / 1e12
         out[name] = {"us": us, "tflops": tf, "frac": tf / peak}
+    f_soft = 2.0 * B * L * H * K * N * N
+    out["soft_select_baseline"] = {"us": tso, "tflops": f_soft / (tso * 1e-6) / 1e12,
+                                   "frac": f_soft / (tso * 1e-6) / 1e12 / peak,
+                                   "vs_hard_select": tso / ts,
+                                   "what": "PD-SSM generator (Eqs. 2-4): mixture GEMM + column hardmax epilogue"}
     out["layer_fwd"] = {"us": tl, "tokens_per_s": B * L / (tl * 1e-6), "diag": "per_dict",
                         "chain": "pdssm_layer_fwd = select + project + scan_fwd + readout"}
     return out

@@ -81,7 +81,7 @@ enum {
 };
 
 enum { PDSSM_OP_SELECT = 0, PDSSM_OP_FWD = 1, PDSSM_OP_BWD = 2, PDSSM_OP_SEGMENT = 3, PDSSM_OP_READOUT = 4,
-       PDSSM_OP_LAYER = 5 };
+       PDSSM_OP_LAYER = 5, PDSSM_OP_SOFT = 6 };
 
 /* Problem statement (north_star: x, selector S, dictionary {P_k, D_k}, B, C,
  * L, N, K, batch, heads).  Plain C struct; all fields are read-only inputs. */
@@ -190,6 +190,22 @@ pdssm_status pdssm_project(const void* x, const void* Bw, void* b_out, const pds
  * ------------------------------------------------------------------------- */
 pdssm_status pdssm_diag_gen(const void* x, const void* Wd, const float* bias_opt, void* D_out,
                             const pdssm_dims* dims, pdssm_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * NEXT-3: the PD-SSM (soft) generator that Flash PD-SSM replaces (Eqs. 2-4):
+ *   s = softmax(S u_t) (Eq. 2),  M(u_t) = sum_k s_k M_k (Eq. 3),
+ *   P_t[j] = column_hardmax_i(M(u_t)[i][j]) (Eq. 4; smallest i on ties, NaN never wins)
+ *   logits  f32    [B][H][L][K]   S u_t (the logits_opt of pdssm_select)
+ *   M       f32    [H][K][N][N]   dense dictionary
+ *   P_out   uint16 [B][H][L][N]   out
+ *   ws  >= pdssm_workspace_bytes(dims, PDSSM_OP_SOFT)   (s and the transposed dictionary)
+ * The mixture is a (B L) x N^2 x K GEMM per head on tcgen05 (3xTF32 for f32 dims, kind::f16
+ * for bf16 dims) whose epilogue takes the column hardmax: the L N^2 mixture is never stored.
+ * A comparison baseline for the hard selection of pdssm_select (the cost the paper removes).
+ * Requires N % 16 == 0, N <= 256.
+ * ------------------------------------------------------------------------- */
+pdssm_status pdssm_soft_select(const float* logits, const float* M, uint16_t* P_out, const pdssm_dims* dims,
+                               void* ws, size_t ws_bytes, pdssm_stream_t stream);
 
 /* ---------------------------------------------------------------------------
  * a8 readout, standalone (the same kernel pdssm_scan_fwd runs for y_opt):

@@ -18,7 +18,7 @@ import re
 __all__ = [
     "PdssmError", "Dims", "lib", "sparsify", "select", "scan_fwd", "scan_bwd",
     "segment_summary", "compose_carry", "segment_summary_bwd", "compose_lambda",
-    "check_device", "chunk_state_views", "select_grad", "dict_grad", "scan", "layer_fwd", "diag_gen", "default_chunk", "workspace_bytes",
+    "check_device", "chunk_state_views", "select_grad", "dict_grad", "scan", "layer_fwd", "diag_gen", "soft_select", "default_chunk", "workspace_bytes",
     "F32", "BF16", "PER_STEP", "PER_DICT", "CHECK_FINITE", "EXPORT_MAPS",
 ]
 
@@ -30,7 +30,7 @@ if os.environ.get("PDSSM_LIB_VARIANT"):   # tuning experiments: variants/<name>.
 F32, BF16 = 0, 1
 PER_STEP, PER_DICT = 0, 1
 CHECK_FINITE, DETERMINISTIC, EXPORT_MAPS = 1, 2, 8
-OP_SELECT, OP_FWD, OP_BWD, OP_SEGMENT, OP_READOUT, OP_LAYER = 0, 1, 2, 3, 4, 5
+OP_SELECT, OP_FWD, OP_BWD, OP_SEGMENT, OP_READOUT, OP_LAYER, OP_SOFT = 0, 1, 2, 3, 4, 5, 6
 
 STATUS = {0: "PDSSM_OK", 1: "PDSSM_ERR_NULL", 2: "PDSSM_ERR_SHAPE", 3: "PDSSM_ERR_RANGE",
           4: "PDSSM_ERR_ALIGN", 5: "PDSSM_ERR_DTYPE", 6: "PDSSM_ERR_WORKSPACE",
@@ -76,6 +76,7 @@ def _load():
         "pdssm_segment_summary_bwd": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, D, vp, sz, vp]),
         "pdssm_compose_lambda": (ctypes.c_int, [vp, vp, i32, i32, vp, D, vp]),
         "pdssm_select_grad": (ctypes.c_int, [vp, vp, vp, ctypes.c_float, vp, D, vp]),
+        "pdssm_soft_select": (ctypes.c_int, [vp, vp, vp, D, vp, sz, vp]),
         "pdssm_diag_gen": (ctypes.c_int, [vp, vp, vp, vp, D, vp]),
         "pdssm_layer_fwd": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, D, vp, sz, vp]),
         "pdssm_dict_grad": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, ctypes.c_float, vp, vp, D, vp]),
@@ -309,6 +310,24 @@ def scan_bwd(kstar, dict_idx, diag, h_saved, chunk_state, dims, dh=None, dy=None
                               _ptr(dh), _ptr(dy), _ptr(C), _ptr(lam_in), _ptr(db), _ptr(dD), _ptr(g), _ptr(dh0),
                               ctypes.byref(dims), _ptr(ws), wsb, _stream()))
     return db, dD, g, dh0
+
+
+def soft_select(logits, M, bf16=False, out=None, ws=None):
+    """NEXT-3 PD-SSM soft generator (Eqs. 2-4): P_t = column_hardmax(sum_k softmax(logits)_k M_k) -> int16 [B,H,L,N].
+    bf16=True runs the mixture GEMM in bf16 (kind::f16), else 3xTF32."""
+    torch = _torch()
+    B, H, L, K = logits.shape
+    N = M.shape[-1]
+    dims = make_dims(B, H, L, N, K, dtype=BF16 if bf16 else F32)
+    P = torch.empty((B, H, L, N), dtype=torch.int16, device=logits.device) if out is None else out
+    wsb = workspace_bytes(dims, OP_SOFT)
+    if ws is None or ws.numel() < wsb:
+        ws, wsb = _workspace(dims, OP_SOFT, logits.device)
+    else:
+        wsb = ws.numel()
+    _check(lib.pdssm_soft_select(_ptr(_contig(logits, "logits")), _ptr(_contig(M, "M")), _ptr(P), ctypes.byref(dims),
+                                 _ptr(ws), wsb, _stream()))
+    return P
 
 
 def diag_gen(x, Wd, bias=None, out=None):

@@ -340,6 +340,37 @@ struct EpiDiag {
     }
 };
 
+// NEXT-3 PD-SSM soft generator (Eqs. 2-4): the tile holds the mixture
+// M(u_t)[i][j] = sum_k s_k M_k[i][j] of one head for bn / N columns j (column index j * N + i,
+// i fastest); the epilogue takes the column hardmax over i (smallest i on ties, NaN never
+// wins, all-NaN -> 0) and writes P[b][h][t][j] -- the L N^2 mixture is never stored.
+struct EpiColArgmax {
+    uint16_t* P;   // [B][H][L][N]
+    int64_t M;     // B * L
+    int L, H, N, h;
+    __device__ void operator()(uint32_t taddr, int64_t m, int n0, int bn, int z) const {
+        (void)z;
+        const bool valid = m < M;
+        const int64_t b = valid ? m / L : 0, t = valid ? m - b * L : 0;
+        uint16_t* dst = P + (((size_t)b * H + h) * L + t) * N;
+        for (int j0 = 0; j0 < bn; j0 += N) {
+            float best = -INFINITY;
+            int arg = N;
+            for (int c0 = 0; c0 < N; c0 += 16) {
+                float v[16];
+                tmem_ld16(taddr + (uint32_t)(j0 + c0), v);
+#pragma unroll
+                for (int q = 0; q < 16; ++q)
+                    if (v[q] > best) {
+                        best = v[q];
+                        arg = c0 + q;
+                    }
+            }
+            if (valid) dst[(n0 + j0) / N] = (uint16_t)(arg >= N ? 0 : arg);
+        }
+    }
+};
+
 // store 16 consecutive fp32 values as TO (16-byte vector stores; dst 16-byte aligned)
 template <typename TO>
 __device__ __forceinline__ void st16(TO* dst, const float (&v)[16]) {

@@ -648,5 +648,35 @@ __global__ void k_diag_activate(T* __restrict__ D, const float* __restrict__ bia
     }
 }
 
+// NEXT-3 staging for the soft generator GEMM: s = softmax(logits) per (b, h, t) into the per-head
+// K-major operand [H][B*L][Kp] (zero-padded to Kp), and the dictionary transposed to
+// Mt[H][j * N + i][Kp] = M[H][k][i][j].
+template <typename T>
+__global__ void k_soft_stage_s(const float* __restrict__ logits, T* __restrict__ s, int64_t BL, int H, int L, int K, int Kp) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // (b, h, t) row
+    if (r >= BL * H) return;
+    const int64_t b = r / ((int64_t)H * L), rem = r - b * H * L;
+    const int h = (int)(rem / L);
+    const int64_t t = rem - (int64_t)h * L;
+    const float* z = logits + r * K;
+    float mx = -INFINITY;
+    for (int k = 0; k < K; ++k) mx = fmaxf(mx, z[k]);
+    float sum = 0.f;
+    for (int k = 0; k < K; ++k) sum += expf(z[k] - mx);
+    const float rs = 1.f / sum;
+    T* o = s + ((size_t)h * BL + b * L + t) * Kp;
+    for (int k = 0; k < Kp; ++k) stact(o + k, k < K ? expf(z[k] - mx) * rs : 0.f);
+}
+template <typename T>
+__global__ void k_soft_stage_M(const float* __restrict__ M, T* __restrict__ Mt, int H, int K, int N, int Kp) {
+    const int64_t total = (int64_t)H * N * N * Kp;
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
+        const int k = (int)(x % Kp);
+        const int64_t rest = x / Kp;   // (h, j, i)
+        const int i = (int)(rest % N), j = (int)((rest / N) % N), h = (int)(rest / ((int64_t)N * N));
+        stact(Mt + x, k < K ? M[(((size_t)h * K + k) * N + i) * N + j] : 0.f);
+    }
+}
+
 }  // namespace sg
 }  // namespace pdssm

@@ -157,6 +157,10 @@ size_t ws_bytes_g(const Geo& g, int op) {
                    (g.diag_mode == PDSSM_DIAG_PER_DICT ? seq_f_bytes(g) : 0) + fused_ctrl_bytes(g.S, g.C, g.H);
         case PDSSM_OP_READOUT:
             return readout_w_bytes(g);
+        case PDSSM_OP_SOFT: {   // s [H][B L][Kp] and Mt [H][N^2][Kp] in the act dtype
+            const int64_t kp = (g.K + 7) / 8 * 8;
+            return align256((size_t)g.H * g.B * g.L * kp * g.act) + align256((size_t)g.H * g.N * g.N * kp * g.act);
+        }
         case PDSSM_OP_LAYER: {
             const size_t sel = align256((size_t)g.S * g.L * g.K * 4), fwd = ws_bytes_g(g, PDSSM_OP_FWD);
             return seq_act_bytes(g) + (sel > fwd ? sel : fwd);
@@ -834,6 +838,43 @@ pdssm_status pdssm_diag_gen(const void* x, const void* Wd, const float* bias_opt
         sg::k_diag_activate<T><<<(unsigned)std::min<int64_t>(ceil_div(rows * g.N, 256), 65535), 256, 0, st>>>(
             static_cast<T*>(D_out), bias_opt, rows, (int)g.H, (int)g.L, (int)g.N, (int)g.nc);
         return cuda_check("diag_activate");
+    });
+}
+
+pdssm_status pdssm_soft_select(const float* logits, const float* M, uint16_t* P_out, const pdssm_dims* dims, void* ws,
+                               size_t ws_bytes, pdssm_stream_t stream) {
+    Geo g;
+    pdssm_status r = geo_of(dims, &g);
+    if (r) return r;
+    if (!logits || !M || !P_out) return fail(PDSSM_ERR_NULL, "soft_select: logits, M, P_out are required");
+    if (g.N % 16 != 0 || g.N > 256) return fail(PDSSM_ERR_UNSUPPORTED, "soft_select: N must be a multiple of 16 <= 256");
+    if (misaligned(logits, 4) || misaligned(M, 4) || misaligned(P_out, 2) || misaligned(ws, 256))
+        return fail(PDSSM_ERR_ALIGN, "soft_select: misaligned pointer");
+    const size_t need = ws_bytes_g(g, PDSSM_OP_SOFT);
+    if (!ws || ws_bytes < need) return fail(PDSSM_ERR_WORKSPACE, "soft_select: workspace too small (need %zu)", need);
+    if (!encode_tiled()) return fail(PDSSM_ERR_UNSUPPORTED, "soft_select: tensor-map encoder unavailable");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t kp = (g.K + 7) / 8 * 8, BL = g.B * g.L;
+    Geo gk = g;
+    gk.d_in = kp;   // the GEMM's K dimension
+    const int bn = (256 / (int)g.N) * (int)g.N;
+    return with_act(g.dtype, [&](auto tv) {
+        using T = decltype(tv);
+        T* sbuf = static_cast<T*>(ws);
+        T* Mt = reinterpret_cast<T*>(static_cast<char*>(ws) + align256((size_t)g.H * BL * kp * g.act));
+        sg::k_soft_stage_s<T><<<(unsigned)ceil_div(BL * g.H, 128), 128, 0, st>>>(logits, sbuf, BL, (int)g.H, (int)g.L,
+                                                                               (int)g.K, (int)kp);
+        sg::k_soft_stage_M<T><<<(unsigned)std::min<int64_t>(ceil_div(g.H * g.N * g.N * kp, 256), 65535), 256, 0, st>>>(
+            M, Mt, (int)g.H, (int)g.K, (int)g.N, (int)kp);
+        pdssm_status rr = cuda_check("soft_stage");
+        if (rr) return rr;
+        for (int64_t h = 0; h < g.H; ++h) {
+            tc::EpiColArgmax epi{P_out, BL, (int)g.L, (int)g.H, (int)g.N, (int)h};
+            rr = launch_tc<T>(gk, sbuf + (size_t)h * BL * kp, BL, Mt + (size_t)h * g.N * g.N * kp, g.N * g.N, bn, epi, st,
+                              "soft_select_tc");
+            if (rr) return rr;
+        }
+        return PDSSM_OK;
     });
 }
 
