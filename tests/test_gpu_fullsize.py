@@ -1,0 +1,119 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times (the library
+default path: one CTA per sequence at config 2), on sampled outputs the float64 oracle computes
+one sequence at a time, plus properties that hold at any size (finite, run-to-run bitwise).
+Sampled sequences are sliced out of the same seeded inputs the bench generates."""
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2605_19150_b200 as mod
+    return mod
+
+
+def rel(a, b):
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30))
+
+
+def sampled_check(inp, f, bwd, seqs, tol, tol2):
+    db, dD, g, _ = bwd
+    h_all = f["h"]
+    for (b, hh) in seqs:
+        sl = lambda a: a[b:b + 1, hh:hh + 1]
+        Pm = O.gather_P(inp["dict_idx"][hh:hh + 1], sl(inp["kstar"]))
+        Dz, bz, e = (O.planes_to_complex(sl(inp[k])) for k in ("diag", "bias", "dh"))
+        h = O.scan_forward(Pm, Dz, bz)
+        db_r, dD_r, g_r, _ = O.scan_backward(Pm, Dz, h, e)
+        cp = lambda t: O.planes_to_complex(t[b:b + 1, hh:hh + 1].float().cpu().numpy())
+        assert rel(cp(h_all), h) <= tol, (b, hh)
+        assert rel(cp(db), db_r) <= tol, (b, hh)
+        assert rel(cp(dD), dD_r) <= tol2, (b, hh)
+        assert rel(g[b:b + 1, hh:hh + 1].cpu().numpy(), g_r) <= tol2, (b, hh)
+
+
+def run(P, inp, bf16):
+    d = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in inp.items()}
+    d["dict_idx"] = d["dict_idx"].to(torch.int16)
+    if bf16:
+        for k in ("diag", "bias", "dh"):
+            d[k] = d[k].to(torch.bfloat16)
+    f = P.scan_fwd(d["kstar"], d["dict_idx"], d["diag"], d["bias"])
+    bwd = P.scan_bwd(d["kstar"], d["dict_idx"], d["diag"], f["h"], f["chunk_state"], f["dims"], dh=d["dh"])
+    torch.cuda.synchronize()
+    return d, f, bwd
+
+
+def test_config2_bench_launch(P):
+    """Config 2 (B 16, L 2048, H 8, N 128, K 32, complex fp32): the bench's exact shape and path."""
+    B, H, L, N, K, c = 16, 8, 2048, 128, 32, 2
+    inp = synth.scan_inputs(B, H, L, N, K, c, seed=2000, dh=True)   # bench.py's default seed, rank 0
+    d, f, bwd = run(P, inp, False)
+    assert f["tau"] == L   # single-chunk path, as timed
+    for t in (f["h"],) + tuple(x for x in bwd if x is not None):
+        assert bool(torch.isfinite(t).all())
+    sampled_check(inp, f, bwd, [(0, 0), (7, 3), (15, 7), (9, 5)], 1e-4, 1e-4)
+    f2 = P.scan_fwd(d["kstar"], d["dict_idx"], d["diag"], d["bias"])
+    b2 = P.scan_bwd(d["kstar"], d["dict_idx"], d["diag"], f2["h"], f2["chunk_state"], f2["dims"], dh=d["dh"])
+    torch.cuda.synchronize()
+    assert torch.equal(f["h"], f2["h"]) and torch.equal(bwd[0], b2[0]) and torch.equal(bwd[1], b2[1])
+    assert torch.equal(bwd[2], b2[2])
+
+
+def test_config2_dict_grad_sampled(P):
+    """NEXT-1 dictionary gradient at config 2: G[h, k] for sampled (h, k) from the oracle's own scans
+    over every sequence of head h."""
+    B, H, L, N, K, c = 16, 8, 2048, 128, 32, 2
+    inp = synth.scan_inputs(B, H, L, N, K, c, seed=2000, dh=True)
+    d, f, bwd = run(P, inp, False)
+    M = torch.from_numpy(synth.dictionary(H, K, N, 2001)).cuda()
+    dM, G = P.dict_grad(M, d["kstar"], d["diag"], f["h"], bwd[0], 1.0, f["dims"], want_G=True)
+    torch.cuda.synchronize()
+    hh = 5
+    sl = lambda a: a[:, hh:hh + 1]
+    Pm = O.gather_P(inp["dict_idx"][hh:hh + 1], sl(inp["kstar"]))
+    Dz, bz, e = (O.planes_to_complex(sl(inp[k])) for k in ("diag", "bias", "dh"))
+    h = O.scan_forward(Pm, Dz, bz)
+    lam = O.scan_backward(Pm, Dz, h, e)[0]
+    G_ref = O.dictionary_outer(sl(inp["kstar"]), lam, Dz, h, K)[0]
+    assert rel(G[hh].cpu().numpy(), G_ref) <= 1e-4
+    dM_ref = O.dictionary_grad(M[hh:hh + 1].cpu().numpy().astype(np.float64), G_ref[None], 1.0)[0]
+    assert rel(dM[hh].cpu().numpy(), dM_ref) <= 1e-4
+
+
+def test_config4_bf16_sampled(P):
+    """Config 4 (B 32, H 32, L 4096, N 64, K 48, real bf16): 1024 sequences, several CTAs per SM."""
+    B, H, L, N, K, c = 32, 32, 4096, 64, 48, 1
+    inp = synth.scan_inputs(B, H, L, N, K, c, seed=4000, dh=True, bf16=True)
+    d, f, bwd = run(P, inp, True)
+    sampled_check(inp, f, bwd, [(0, 0), (31, 31), (17, 9)], 2e-2, 3e-2)
+
+
+def test_config5_s5_full_length(P):
+    """Config 5 (S_5 word problem, L = 65536, N 64, K 16, B 4, H 4, PER_DICT D = 1, b = 0,
+    h0 = arange): exact permuted states at the end and exact final maps, every sequence."""
+    dict_idx, _, _ = synth.s5_dictionary(64, 16, seed=5000)
+    B, H, L, N = 4, 4, 65536, 64
+    k = synth.kstar(B, H, L, 16, seed=5001)
+    di = torch.from_numpy(np.tile(dict_idx[None], (H, 1, 1)).astype(np.int16)).cuda()
+    diag = torch.ones((H, 16, 1, N), dtype=torch.float32, device="cuda")
+    bias = torch.zeros((B, H, L, 1, N), dtype=torch.float32, device="cuda")
+    h0 = torch.arange(N, dtype=torch.float32, device="cuda").view(1, 1, 1, N).repeat(B, H, 1, 1).contiguous()
+    f = P.scan_fwd(torch.from_numpy(k).cuda(), di, diag, bias, h0=h0, per_dict=True, export_maps=True)
+    torch.cuda.synchronize()
+    # final composed map by the oracle's own fold (integer, exact)
+    Pm = O.gather_P(np.tile(dict_idx[None], (H, 1, 1)), k)
+    Pi, _ = O.prefix_maps(Pm, np.ones(Pm.shape))
+    assert np.array_equal(f["maps"].cpu().numpy().astype(np.int64)[:, :, -1], Pi[:, :, -1])
+    hlast = f["h"][:, :, -1, 0].cpu().numpy()
+    expect = np.zeros((B, H, N))
+    np.put_along_axis(expect, Pi[:, :, -1], np.arange(float(N))[None, None].repeat(B, 0).repeat(H, 1), axis=2)
+    assert np.array_equal(hlast, expect)
