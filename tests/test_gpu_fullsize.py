@@ -117,3 +117,36 @@ def test_config5_s5_full_length(P):
     expect = np.zeros((B, H, N))
     np.put_along_axis(expect, Pi[:, :, -1], np.arange(float(N))[None, None].repeat(B, 0).repeat(H, 1), axis=2)
     assert np.array_equal(hlast, expect)
+
+
+def test_config3_sequence_parallel_full_length(P):
+    """Config 3 (L = 17984, B 4, H 8, N 128, real fp32, temporally persistent k*): the sequence-
+    parallel construction with G = 8 virtual ranks (segments of 2248 steps, ragged against tau)
+    -- segment summaries, rank-ordered composition, local scans -- against the oracle on
+    sampled sequences, and the composed carries' index maps bit-exact."""
+    B, H, L, N, K, c, G = 4, 8, 17984, 128, 32, 1, 8
+    inp = synth.scan_inputs(B, H, L, N, K, c, seed=3000, h0=True, sticky=0.9)
+    dev = {k: torch.from_numpy(v).cuda() for k, v in inp.items()}
+    di = dev["dict_idx"].to(torch.int16)
+    bounds = [(g * L // G, (g + 1) * L // G) for g in range(G)]
+    seg = lambda t, s, e: t[:, :, s:e].contiguous()
+    dims_g = [P.make_dims(B, H, e - s, N, K, c=c) for (s, e) in bounds]
+    gathered = torch.cat([P.segment_summary(seg(dev["kstar"], s, e), di, seg(dev["diag"], s, e),
+                                            seg(dev["bias"], s, e), dims_g[g]) for g, (s, e) in enumerate(bounds)])
+    hs, maps = [], []
+    for g, (s, e) in enumerate(bounds):
+        carry, m = P.compose_carry(gathered, g, G, dims_g[g], h0=dev["h0"])
+        maps.append(m)
+        hs.append(P.scan_fwd(seg(dev["kstar"], s, e), di, seg(dev["diag"], s, e), seg(dev["bias"], s, e), h0=carry)["h"])
+    torch.cuda.synchronize()
+    for (b, hh) in [(0, 0), (3, 7), (2, 4)]:
+        sl = lambda a: a[b:b + 1, hh:hh + 1]
+        Pm = O.gather_P(inp["dict_idx"][hh:hh + 1], sl(inp["kstar"]))
+        Dz, bz, h0z = (O.planes_to_complex(sl(inp[k])) for k in ("diag", "bias", "h0"))
+        h_ref = O.scan_forward(Pm, Dz, bz, h0z)
+        Pi, _ = O.prefix_maps(Pm, np.ones(Pm.shape))
+        got = np.concatenate([O.planes_to_complex(x[b:b + 1, hh:hh + 1].cpu().numpy()) for x in hs], axis=2)
+        assert rel(got, h_ref) <= 1e-4, (b, hh)
+        for g, (s, e) in enumerate(bounds):
+            if s > 0:
+                assert np.array_equal(maps[g][b, hh].cpu().numpy().astype(np.int64), Pi[0, 0, s - 1])
