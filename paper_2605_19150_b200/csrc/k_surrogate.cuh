@@ -664,19 +664,25 @@ __global__ void k_diag_activate(T* __restrict__ D, const float* __restrict__ bia
 // Mt[H][j * N + i][Kp] = M[H][k][i][j].
 template <typename T>
 __global__ void k_soft_stage_s(const float* __restrict__ logits, T* __restrict__ s, int64_t BL, int H, int L, int K, int Kp) {
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // (b, h, t) row
+    // one warp per (b, h, t) row: lanes own k = lane + 32 m (coalesced row reads and writes)
+    const int lane = threadIdx.x & 31;
+    const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);   // (b, h, t) row
     if (r >= BL * H) return;
     const int64_t b = r / ((int64_t)H * L), rem = r - b * H * L;
     const int h = (int)(rem / L);
     const int64_t t = rem - (int64_t)h * L;
     const float* z = logits + r * K;
     float mx = -INFINITY;
-    for (int k = 0; k < K; ++k) mx = fmaxf(mx, z[k]);
+    for (int k = lane; k < K; k += 32) mx = fmaxf(mx, z[k]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     float sum = 0.f;
-    for (int k = 0; k < K; ++k) sum += expf(z[k] - mx);
+    for (int k = lane; k < K; k += 32) sum += expf(z[k] - mx);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
     const float rs = 1.f / sum;
     T* o = s + ((size_t)h * BL + b * L + t) * Kp;
-    for (int k = 0; k < Kp; ++k) stact(o + k, k < K ? expf(z[k] - mx) * rs : 0.f);
+    for (int k = lane; k < Kp; k += 32) stact(o + k, k < K ? expf(z[k] - mx) * rs : 0.f);
 }
 template <typename T>
 __global__ void k_soft_stage_M(const float* __restrict__ M, T* __restrict__ Mt, int H, int K, int N, int Kp) {

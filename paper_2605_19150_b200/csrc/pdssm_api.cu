@@ -862,7 +862,7 @@ pdssm_status pdssm_soft_select(const float* logits, const float* M, uint16_t* P_
         using T = decltype(tv);
         T* sbuf = static_cast<T*>(ws);
         T* Mt = reinterpret_cast<T*>(static_cast<char*>(ws) + align256((size_t)g.H * BL * kp * g.act));
-        sg::k_soft_stage_s<T><<<(unsigned)ceil_div(BL * g.H, 128), 128, 0, st>>>(logits, sbuf, BL, (int)g.H, (int)g.L,
+        sg::k_soft_stage_s<T><<<(unsigned)ceil_div(BL * g.H, 8), 256, 0, st>>>(logits, sbuf, BL, (int)g.H, (int)g.L,
                                                                                (int)g.K, (int)kp);
         sg::k_soft_stage_M<T><<<(unsigned)std::min<int64_t>(ceil_div(g.H * g.N * g.N * kp, 256), 65535), 256, 0, st>>>(
             M, Mt, (int)g.H, (int)g.K, (int)g.N, (int)kp);
