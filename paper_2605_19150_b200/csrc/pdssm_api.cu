@@ -986,7 +986,7 @@ pdssm_status pdssm_dict_grad(const float* M, const uint8_t* kstar, const void* d
     a.B = (int)g.B; a.H = (int)g.H; a.L = (int)g.L; a.N = (int)g.N; a.K = (int)g.K;
     a.invT = 1.f / temp;
     const unsigned grid = (unsigned)(g.H * g.K);
-    const bool tc = g.N == sg::TC_N && !env_path_is("generic");
+    const bool tc = g.N == sg::TC_N && !env_path_is("generic") && !misaligned(M, 16);   // (float4 M-tile loads)
     return with_act(g.dtype, [&](auto tv) {
         using T = decltype(tv);
         return with_nc(g.nc, [&](auto ncv) {
