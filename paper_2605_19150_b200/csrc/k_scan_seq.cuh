@@ -199,7 +199,7 @@ __device__ __forceinline__ void st_stream(T* p, float v, uint64_t pol) {
     }
 }
 
-constexpr int SEQ_G = 8;   // steps per ring slot (one TMA group)
+constexpr int SEQ_G = 16;   // steps per ring slot (one TMA group)
 
 // ============================================================================ forward
 // Step t (r = t mod 8 is compile-time inside a full group, so ring rows, the exchange
@@ -599,7 +599,7 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq(SeqArgs a) {
             mbar_arrive(bars + R + (slot == 0 ? R - 1 : slot - 1));
         }
         // g_t of the previous 32 steps (v = 8 g + rr, so only the first step of every 4th group)
-        if (rr == 0 && (g & 3) == 0 && g > 0 && a.gsel) {
+        if (rr == 0 && (g % (32 / G)) == 0 && g > 0 && a.gsel) {
             const int q = j & 31, part = j >> 5, NP = N >> 5;
             const float* gr = gs + (size_t)q * (N + 1);
             float acc = 0.f;
