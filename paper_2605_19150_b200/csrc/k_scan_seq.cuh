@@ -199,7 +199,8 @@ __device__ __forceinline__ void st_stream(T* p, float v, uint64_t pol) {
     }
 }
 
-constexpr int SEQ_G = 16;   // steps per ring slot (one TMA group)
+constexpr int SEQ_G = 16;    // backward: steps per ring slot (one TMA group)
+constexpr int SEQ_GF = 32;   // forward: steps per ring slot
 
 // ============================================================================ forward
 // Step t (r = t mod 8 is compile-time inside a full group, so ring rows, the exchange
@@ -214,7 +215,7 @@ constexpr int SEQ_G = 16;   // steps per ring slot (one TMA group)
 template <typename T, int NC, bool PD, bool AGG, bool CHECK, int NN>
 __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
     using SV = typename fused::SVal<NC>::type;
-    constexpr int G = SEQ_G;
+    constexpr int G = SEQ_GF;
     constexpr int SVB = (int)sizeof(SV);
     extern __shared__ __align__(128) uint8_t smem[];
     const int N = NN ? NN : a.N, K = a.K, L = a.L, R = a.R;

@@ -453,18 +453,20 @@ pdssm_status prepare_e(const Geo& g, const void* dh, const void* dy, const float
 // ---------------------------------------------------------------------------
 
 constexpr size_t kSeqSmemBudget = 200 * 1024;
-constexpr int kSeqG = seq::SEQ_G;
+constexpr int kSeqG = seq::SEQ_G;     // backward group
+constexpr int kSeqGF = seq::SEQ_GF;   // forward group
 
 // ring depth R for this shape (0: the layout does not fit)
 // ring depth R for this shape (0: the layout does not fit).  When there are more
 // sequences than SMs, the budget is split so that ceil(S / #SMs) CTAs (up to 4) fit per SM.
 int seq_ring(const Geo& g, bool bwd, bool agg, size_t esz_e) {
-    const int ngroups = (int)ceil_div(g.L, kSeqG);
+    const int G = bwd ? kSeqG : kSeqGF;
+    const int ngroups = (int)ceil_div(g.L, G);
     const int64_t per_sm = std::min<int64_t>(std::max<int64_t>(ceil_div(g.S, num_sms_dev()), 1), 4);
     const size_t budget = std::min<size_t>(kSeqSmemBudget, (size_t)(226 * 1024) / (size_t)per_sm - 1024);
     int best = 0;
     for (int R = 2; R <= 16 && R <= ngroups + 1; ++R) {
-        seq::Layout ly((int)g.N, (int)g.K, R, kSeqG, g.nc, (int)g.act, (int)esz_e, g.diag_mode == PDSSM_DIAG_PER_DICT, agg, bwd,
+        seq::Layout ly((int)g.N, (int)g.K, R, G, g.nc, (int)g.act, (int)esz_e, g.diag_mode == PDSSM_DIAG_PER_DICT, agg, bwd,
                        (int)g.L);
         if (ly.bytes <= budget) best = R;
     }
@@ -577,7 +579,7 @@ pdssm_status fwd_seq(const Geo& g, seq::SeqArgs& sa, uint8_t* rec, uint8_t* wm, 
     if (r) return r;
     const bool agg = (g.flags & PDSSM_EXPORT_MAPS) != 0;
     sa.R = seq_ring(g, false, agg, g.act);
-    sa.G = kSeqG;
+    sa.G = kSeqGF;
     return with_act(g.dtype, [&](auto tv) {
         using T = decltype(tv);
         return with_nc(g.nc, [&](auto ncv) {
