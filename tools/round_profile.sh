@@ -27,3 +27,5 @@ ncu --set full --clock-control none --import-source on -k regex:"k_dict_grad_tc"
 python tools/ncu_summary.py gpurun_out/prof_dict_${TAG}.ncu-rep k_dict_grad > gpurun_out/ncu_summary_dict_${TAG}.txt 2>&1
 rm -f gpurun_out/prof_dict_${TAG}.ncu-rep
 du -sh gpurun_out
+rm -f gpurun_out/prof_${TAG}.ncu-rep
+du -sh gpurun_out
