@@ -433,13 +433,14 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
         }
     };
     auto run = [&](auto ovfv) {
+        constexpr bool OVF = decltype(ovfv)::value;
         for (int g = 0; g < ngroups; ++g) {
             const int t0 = g * G;
-            if (t0 + G <= L) {
+            if (!OVF && t0 + G <= L) {
 #pragma unroll
                 for (int r = 0; r < G; ++r) step(r, g, t0 + r, ovfv);
-            } else {
-                for (int r = 0; r < L - t0; ++r) step(r, g, t0 + r, ovfv);
+            } else {   // ragged last group, or a head with CSR-overflow entries (rare): not unrolled
+                for (int r = 0; r < min(G, L - t0); ++r) step(r, g, t0 + r, ovfv);
             }
         }
     };
