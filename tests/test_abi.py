@@ -88,3 +88,28 @@ def test_null_and_workspace_and_alignment_checks():
 
 def test_dims_struct_layout():
     assert ctypes.sizeof(P.Dims) == 80
+
+
+def test_next_rows_validate_before_any_cuda_call():
+    """NEXT-1/2/3 entry points: synchronous argument validation (no GPU needed)."""
+    fake = ctypes.c_void_p(4096)   # never dereferenced: every case fails validation first
+    d = dims(N=16, K=4)
+    # selector gradient: NULL -> ERR_NULL (1), temperature <= 0 -> ERR_RANGE (3)
+    assert P.lib.pdssm_select_grad(None, fake, fake, 1.0, fake, ctypes.byref(d), None) == 1
+    assert P.lib.pdssm_select_grad(fake, fake, fake, 0.0, fake, ctypes.byref(d), None) == 3
+    assert P.lib.pdssm_select_grad(fake, fake, fake, float("nan"), fake, ctypes.byref(d), None) == 3
+    # dictionary gradient: NULL -> 1; N > 128 -> ERR_UNSUPPORTED (9)
+    assert P.lib.pdssm_dict_grad(None, fake, fake, fake, None, fake, 1.0, fake, None, ctypes.byref(d), None) == 1
+    big = dims(N=200, K=4)
+    assert P.lib.pdssm_dict_grad(fake, fake, fake, fake, None, fake, 1.0, fake, None, ctypes.byref(big), None) == 9
+    # soft generator: N not a multiple of 16 -> 9; too little workspace -> ERR_WORKSPACE (6)
+    odd = dims(N=24, K=4)
+    assert P.lib.pdssm_soft_select(fake, fake, fake, ctypes.byref(odd), fake, 1 << 30, None) == 9
+    assert P.lib.pdssm_soft_select(fake, fake, fake, ctypes.byref(d), fake, 16, None) == 6
+    assert P.workspace_bytes(d, P.OP_SOFT) >= 3 * 2 * 100 * 8 * 4 + 3 * 16 * 16 * 8 * 4
+    # layer forward and D generator: d_in must be >= 1 -> ERR_SHAPE (2)
+    assert P.lib.pdssm_layer_fwd(fake, fake, fake, fake, fake, None, None, fake, None, None, fake,
+                                 ctypes.byref(d), fake, 1 << 30, None) == 2
+    assert P.lib.pdssm_diag_gen(fake, fake, None, fake, ctypes.byref(d), None) == 2
+    dl = P.make_dims(2, 3, 100, 16, 4, c=2, d_in=32)
+    assert P.workspace_bytes(dl, P.OP_LAYER) >= 2 * 3 * 100 * 2 * 16 * 4
