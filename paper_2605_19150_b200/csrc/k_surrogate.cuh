@@ -320,7 +320,8 @@ constexpr size_t TC_OFF_Q = 2 * (size_t)TC_STAGE;
 constexpr size_t TC_OFF_WSUM = TC_OFF_Q + 4 * (size_t)TC_QCAP;
 constexpr size_t TC_OFF_BAR = TC_OFF_WSUM + 4 * (size_t)(TC_THREADS / 32);
 __host__ __device__ constexpr size_t tc_smem_bytes() { return 1024 + TC_OFF_BAR + 64; }
-static_assert(TC_OFF_Q >= 4 * (size_t)(TC_N * (TC_N + 1) + TC_N * TC_N) - 4 * TC_QCAP, "epilogue tiles must fit");
+static_assert(TC_OFF_Q >= 4 * (size_t)(TC_N * (TC_N + 1) + TC_N * TC_N) - 1024, "epilogue tiles must fit");
+static_assert(1024 + 3 * 4 * (size_t)TC_THREADS <= 4 * (size_t)TC_QCAP, "Jacobian partials must fit after the M tile");
 static_assert(1024 + TC_OFF_BAR + 64 <= 227 * 1024, "shared memory budget");
 
 // byte offset of (row n, 16-byte chunk ch) in a K-major SWIZZLE_128B tile (8-row atoms of 1024 B)
@@ -609,31 +610,49 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_dict_grad_tc(DictArgs a) {
         tc::fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128) : "memory");
     }
-    // softmax Jacobian: thread j owns column j (sigma_j over the rows i; ascending-i sums)
-#ifdef DG_NOEPI   // timing experiment only
-    if (tid < 0) {
-#else
-    if (tid < N) {
-#endif
-        const int j = tid;
+    // softmax Jacobian over the 512 threads: thread (q, j) = tid / N, tid % N owns rows
+    // [q N/4, (q+1) N/4) of column j; the four partial max / sums / projections combine in a
+    // fixed order (q = 0..3) through shared memory, so the result is run-to-run identical
+#ifndef DG_NOEPI
+    {
+        constexpr int QN = TC_THREADS / N;   // 4 row quarters
+        constexpr int RQ = N / QN;
+        float* part = reinterpret_cast<float*>(smem + TC_OFF_Q + 1024);   // [3][QN][N] (after Ms)
+        const int j = tid % N, qq = tid / N, i0 = qq * RQ;
         float mx = -INFINITY;
-        for (int i = 0; i < N; ++i) mx = fmaxf(mx, Ms[i * N + j] * a.invT);
+        for (int i = i0; i < i0 + RQ; ++i) mx = fmaxf(mx, Ms[i * N + j] * a.invT);
+        part[qq * N + j] = mx;
+        __syncthreads();
+        mx = part[j];
+#pragma unroll
+        for (int x = 1; x < QN; ++x) mx = fmaxf(mx, part[x * N + j]);
         float sum = 0.f, pr = 0.f;
-        for (int i = 0; i < N; ++i) {
+        for (int i = i0; i < i0 + RQ; ++i) {
             const float e = expf(Ms[i * N + j] * a.invT - mx);
             sum += e;
             pr += e * Gs[i * (N + 1) + j];
         }
+        part[(QN + qq) * N + j] = sum;
+        part[(2 * QN + qq) * N + j] = pr;
+        __syncthreads();
+        sum = part[QN * N + j];
+        pr = part[2 * QN * N + j];
+#pragma unroll
+        for (int x = 1; x < QN; ++x) {
+            sum += part[(QN + x) * N + j];
+            pr += part[(2 * QN + x) * N + j];
+        }
         const float rs = 1.f / sum;
         const float proj = pr * rs;
         const size_t base = ((size_t)h * a.K + k) * N * N;
-        for (int i = 0; i < N; ++i) {
+        for (int i = i0; i < i0 + RQ; ++i) {
             const float g = Gs[i * (N + 1) + j];
             const float sg = expf(Ms[i * N + j] * a.invT - mx) * rs;
             a.dM[base + (size_t)i * N + j] = sg * (g - proj) * a.invT;
             if (a.G) a.G[base + (size_t)i * N + j] = g;
         }
     }
+#endif
 }
 
 // NEXT-2 D_t generator, SIMT fallback: the projection writes raw (a, theta) planes, then
