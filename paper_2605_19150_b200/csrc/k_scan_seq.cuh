@@ -94,6 +94,7 @@ __global__ void k_build_seq_plan(const uint16_t* __restrict__ dict_idx, uint8_t*
                                  uint16_t* __restrict__ psrc, int N, uint32_t flags) {
     extern __shared__ uint16_t sP[];
     __shared__ int sovf;
+    asm volatile("griddepcontrol.launch_dependents;");   // the forward scan may start its prologue
     const int e = blockIdx.x;
     const int i = threadIdx.x;   // blockDim.x == N (multiple of 32)
     if (i == 0) sovf = 0;
@@ -235,7 +236,12 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
     const size_t seq0 = (size_t)s * L;
     const int ngroups = (L + G - 1) / G;
     const uint64_t pol = fused::policy_evict_first();
-    {   // one-time tables of head h, and the sequence's k* (zero-padded by 2)
+    // The sequence's k* first: it does not depend on the plan launch that precedes this
+    // kernel, which may still be running (programmatic dependent launch); wait for it only
+    // before the tables it writes are read.
+    stage_k(a, kb, seq0, L);
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    {   // one-time tables of head h (k* zero-padded by 2)
         const int NT = blockDim.x;
         const uint2* gr = reinterpret_cast<const uint2*>(a.rec) + (size_t)h * K * N;
         for (int x = i; x < K * N; x += NT) rec[x] = __ldg(gr + x);
@@ -246,7 +252,6 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
             for (int x = i; x < K * NC * N; x += NT) dk[x] = __ldg(a.diag_dict + (size_t)h * K * NC * N + x);
         if (i < 2) kb[L + i] = 0;
     }
-    stage_k(a, kb, seq0, L);
     const int XB = (N + 1) * SVB;   // bytes of one exchange row (N values + the zero slot)
     if (i == 0) {
         *reinterpret_cast<SV*>(xbc + N * SVB) = fused::mk<NC>(0.f, 0.f);

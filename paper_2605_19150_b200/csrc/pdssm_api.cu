@@ -599,7 +599,19 @@ pdssm_status fwd_seq(const Geo& g, seq::SeqArgs& sa, uint8_t* rec, uint8_t* wm, 
                     }
                     pdssm_status rr = seq_set_smem((const void*)kern, ly.bytes);
                     if (rr) return rr;
-                    kern<<<(unsigned)g.S, (unsigned)g.N + 32, ly.bytes, st>>>(sa);   // + producer warp
+                    // programmatic dependent launch: the prologue overlaps the plan kernel's tail
+                    cudaLaunchConfig_t cfg = {};
+                    cfg.gridDim = dim3((unsigned)g.S);
+                    cfg.blockDim = dim3((unsigned)g.N + 32);   // + producer warp
+                    cfg.dynamicSmemBytes = ly.bytes;
+                    cfg.stream = st;
+                    cudaLaunchAttribute attr[1];
+                    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                    attr[0].val.programmaticStreamSerializationAllowed = 1;
+                    cfg.attrs = attr;
+                    cfg.numAttrs = 1;
+                    cudaError_t le = cudaLaunchKernelEx(&cfg, kern, sa);
+                    if (le != cudaSuccess) return fail(PDSSM_ERR_CUDA, "fwd_seq launch: %s", cudaGetErrorString(le));
                     return cuda_check("fwd_seq");
                 };
                 const bool chk = (g.flags & PDSSM_CHECK_FINITE) != 0;
