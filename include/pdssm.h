@@ -77,6 +77,10 @@ typedef enum { PDSSM_DIAG_PER_STEP = 0, PDSSM_DIAG_PER_DICT = 1 } pdssm_diag_mod
 enum {
     PDSSM_CHECK_FINITE = 1u,   /* scan inputs for NaN/Inf and out-of-range indices   */
     PDSSM_DETERMINISTIC = 2u,  /* accepted; the library is always deterministic      */
+    PDSSM_SAVE_STATES = 4u,    /* pdssm_scan_fwd must write h_out_opt (the caller keeps
+                                  the states for the backward); without it h_out_opt may
+                                  be NULL and pdssm_scan_bwd(h_saved = NULL, bias_opt)
+                                  recomputes them from bias + the chunk carries          */
     PDSSM_EXPORT_MAPS = 8u     /* pdssm_scan_fwd also writes maps_opt                 */
 };
 
@@ -235,7 +239,10 @@ pdssm_status pdssm_readout(const void* h, const float* C, void* y, const pdssm_d
  *   chunk_state                          out: see pdssm_chunk_state_bytes (required)
  *   maps_opt   uint16 [B][H][C+1][N]     out (PDSSM_EXPORT_MAPS): exclusive prefix
  *              maps Pi before chunk c (maps[0] = identity) and the final map Pi_{L-1}
- * At least one of h_out_opt / y_opt must be given.
+ * At least one of h_out_opt / y_opt must be given; PDSSM_SAVE_STATES requires h_out_opt.
+ * chunk_state always holds, per (sequence, chunk c): the aggregate (pi_bar_c, d_bar_c,
+ * beta_bar_c) and the carry h_{c tau - 1} (carry_0 = h0) -- the O(C N) state from which the
+ * backward can recompute the chunk's states (recompute mode, pdssm_scan_bwd).
  * ------------------------------------------------------------------------- */
 pdssm_status pdssm_scan_fwd(const uint8_t* kstar, const uint16_t* dict_idx, const void* diag,
                             const void* bias, const float* h0_opt, const float* C_opt,
@@ -254,8 +261,15 @@ pdssm_status pdssm_scan_fwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
  *   dh0 = A_0^T lambda_0
  * with the direct gradient e_t = dh_t + conj(C_h)^T dy_t.
  *   kstar, dict_idx, diag, h0_opt : the SAME tensors given to pdssm_scan_fwd
- *   h_saved    act [B][H][L][c][N]  the forward states h_t (required)
- *   chunk_state                      the forward's chunk_state (reused Abar_c)
+ *   h_saved    act [B][H][L][c][N]  the forward states h_t, or NULL: recompute mode
+ *   bias_opt   act [B][H][L][c][N]  b_t, the forward's bias (required iff h_saved is NULL).
+ *              Recompute mode (the O(L N)-activation-free backward of PAPER.md:190, :280):
+ *              every (sequence, chunk) item replays its chunk forward from the carry in
+ *              chunk_state (Alg. 1 Phase C) into shared memory and reads
+ *              h_{t-1} from there; needs chunk * c * N * 4 <= ~200 KB, i.e. the forward and
+ *              the backward must be called with the same (small) dims.chunk, else
+ *              PDSSM_ERR_UNSUPPORTED.
+ *   chunk_state                      the forward's chunk_state (reused Abar_c; carries)
  *   dh_opt     act [B][H][L][c][N]  direct state gradient (NULL = 0)
  *   dy_opt     act [B][L][H][P] with C_opt f32 [H][c][P][N] (NULL = 0)
  *   lam_in_opt f32 [B][H][c][N]     adjoint entering h_{L-1} from a later
@@ -266,7 +280,8 @@ pdssm_status pdssm_scan_fwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
  *   dh0_opt    f32 [B][H][c][N]     out (optional)
  * ------------------------------------------------------------------------- */
 pdssm_status pdssm_scan_bwd(const uint8_t* kstar, const uint16_t* dict_idx, const void* diag,
-                            const void* h_saved, const float* h0_opt, const void* chunk_state,
+                            const void* h_saved_opt, const void* bias_opt, const float* h0_opt,
+                            const void* chunk_state,
                             const void* dh_opt, const void* dy_opt, const float* C_opt,
                             const float* lam_in_opt, void* dbias, void* ddiag, float* gsel,
                             float* dh0_opt, const pdssm_dims* dims, void* ws, size_t ws_bytes,

@@ -29,7 +29,7 @@ if os.environ.get("PDSSM_LIB_VARIANT"):   # tuning experiments: variants/<name>.
 
 F32, BF16 = 0, 1
 PER_STEP, PER_DICT = 0, 1
-CHECK_FINITE, DETERMINISTIC, EXPORT_MAPS = 1, 2, 8
+CHECK_FINITE, DETERMINISTIC, SAVE_STATES, EXPORT_MAPS = 1, 2, 4, 8
 OP_SELECT, OP_FWD, OP_BWD, OP_SEGMENT, OP_READOUT, OP_LAYER, OP_SOFT = 0, 1, 2, 3, 4, 5, 6
 
 STATUS = {0: "PDSSM_OK", 1: "PDSSM_ERR_NULL", 2: "PDSSM_ERR_SHAPE", 3: "PDSSM_ERR_RANGE",
@@ -70,7 +70,7 @@ def _load():
         "pdssm_project": (ctypes.c_int, [vp, vp, vp, D, vp]),
         "pdssm_readout": (ctypes.c_int, [vp, vp, vp, D, vp, sz, vp]),
         "pdssm_scan_fwd": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, D, vp, sz, vp]),
-        "pdssm_scan_bwd": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, D, vp, sz, vp]),
+        "pdssm_scan_bwd": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, D, vp, sz, vp]),
         "pdssm_segment_summary": (ctypes.c_int, [vp, vp, vp, vp, vp, D, vp, sz, vp]),
         "pdssm_compose_carry": (ctypes.c_int, [vp, i32, i32, vp, vp, vp, D, vp]),
         "pdssm_segment_summary_bwd": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, D, vp, sz, vp]),
@@ -281,19 +281,24 @@ def scan_fwd(kstar, dict_idx, diag, bias, h0=None, C=None, tau=0, per_dict=False
 
 
 def scan_bwd(kstar, dict_idx, diag, h_saved, chunk_state, dims, dh=None, dy=None, C=None, h0=None,
-             lam_in=None, want_g=True, want_dh0=True, out=None):
-    """a9: reverse transposed scan -> (dbias, ddiag, gsel, dh0) (App. C)."""
+             lam_in=None, want_g=True, want_dh0=True, out=None, bias=None):
+    """a9: reverse transposed scan -> (dbias, ddiag, gsel, dh0) (App. C).
+    h_saved=None with bias=b_t: recompute mode (states replayed per chunk from chunk_state)."""
     torch = _torch()
+    for n, t in (("kstar", kstar), ("dict_idx", dict_idx), ("diag", diag), ("h_saved", h_saved), ("bias", bias),
+                 ("chunk_state", chunk_state), ("dh", dh), ("dy", dy), ("C", C), ("h0", h0), ("lam_in", lam_in)):
+        _contig(t, n)
     B, H, L = kstar.shape
     N, c = dims.state, dims.is_complex
-    dev = h_saved.device
+    dev = chunk_state.device
     out = dict(out or {})
+    act = h_saved if h_saved is not None else bias
     db = out.get("dbias")
     if db is None:
-        db = torch.empty_like(h_saved)
+        db = torch.empty_like(act)
     dD = out.get("ddiag")
     if dD is None:
-        dD = torch.empty(diag.shape, dtype=torch.float32 if dims.diag_mode == PER_DICT else h_saved.dtype, device=dev)
+        dD = torch.empty(diag.shape, dtype=torch.float32 if dims.diag_mode == PER_DICT else act.dtype, device=dev)
     g = out.get("gsel") if want_g else None
     if want_g and g is None:
         g = torch.empty((B, H, L), dtype=torch.float32, device=dev)
@@ -306,7 +311,8 @@ def scan_bwd(kstar, dict_idx, diag, h_saved, chunk_state, dims, dh=None, dy=None
         ws, wsb = _workspace(dims, OP_BWD, dev)
     else:
         wsb = ws.numel()
-    _check(lib.pdssm_scan_bwd(_ptr(kstar), _ptr(dict_idx), _ptr(diag), _ptr(h_saved), _ptr(h0), _ptr(chunk_state),
+    _check(lib.pdssm_scan_bwd(_ptr(kstar), _ptr(dict_idx), _ptr(diag), _ptr(h_saved), _ptr(bias), _ptr(h0),
+                              _ptr(chunk_state),
                               _ptr(dh), _ptr(dy), _ptr(C), _ptr(lam_in), _ptr(db), _ptr(dD), _ptr(g), _ptr(dh0),
                               ctypes.byref(dims), _ptr(ws), wsb, _stream()))
     return db, dD, g, dh0
@@ -480,9 +486,12 @@ def _scan_fn():
     class _Scan(torch.autograd.Function):
         @staticmethod
         def forward(ctx, diag, bias, h0, kstar, dict_idx, per_dict):
-            f = scan_fwd(kstar, dict_idx, diag.contiguous(), bias.contiguous(),
-                         h0=None if h0 is None else h0.contiguous(), per_dict=per_dict)
-            ctx.save_for_backward(kstar, dict_idx, diag, f["h"], f["chunk_state"], h0)
+            # the backward must see exactly the (contiguous) tensors the forward consumed
+            diag_c, bias_c = diag.contiguous(), bias.contiguous()
+            h0_c = None if h0 is None else h0.contiguous()
+            kstar_c, dict_c = kstar.contiguous(), dict_idx.contiguous()
+            f = scan_fwd(kstar_c, dict_c, diag_c, bias_c, h0=h0_c, per_dict=per_dict)
+            ctx.save_for_backward(kstar_c, dict_c, diag_c, f["h"], f["chunk_state"], h0_c)
             ctx.dims = f["dims"]
             return f["h"]
 

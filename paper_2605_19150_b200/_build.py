@@ -1,21 +1,33 @@
-"""Build libpdssm.so in-tree for sm_100a (nvcc cross-compiles without a GPU)."""
+"""Build libpdssm.so in-tree for sm_100a (nvcc cross-compiles without a GPU).
+
+The library is several translation units (csrc/*.cu) compiled in parallel into
+objects under paper_2605_19150_b200/build/ and linked into one shared object.
+The ptxas resource logs (registers, spills, shared memory) go to build/ptxas_<unit>.txt
+(git-ignored); commit a copy under profiles/ when it is evidence for a change.
+"""
 from __future__ import annotations
 
 import os
 import subprocess
+from concurrent.futures import ThreadPoolExecutor
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
+BUILD = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "libpdssm.so")
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
     "-Xptxas", "-v",
     "-I", os.path.join(ROOT, "include"),
 ]
+
+
+def units():
+    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
 
 
 def sources():
@@ -30,26 +42,41 @@ def needs_build():
     return any(os.path.getmtime(s) > t for s in deps)
 
 
-def build(force=False, verbose=False):
-    """Compile the single translation unit csrc/pdssm_api.cu into libpdssm.so."""
+def _nvcc():
+    return os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+
+def _compile(src, extra):
+    name = os.path.splitext(os.path.basename(src))[0]
+    obj = os.path.join(BUILD, name + ".o")
+    cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-c", src, "-o", obj + ".tmp"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    with open(os.path.join(BUILD, f"ptxas_{name}.txt"), "w") as f:
+        f.write(" ".join(cmd) + "\n" + r.stderr)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed on {name}:\n" + r.stderr[-8000:])
+    os.replace(obj + ".tmp", obj)
+    return obj
+
+
+def build(force=False, verbose=False, extra=()):
+    """Compile every csrc/*.cu unit (in parallel) and link libpdssm.so."""
     if not force and not needs_build():
         return LIB
-    nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-o", LIB + ".tmp", os.path.join(CSRC, "pdssm_api.cu")]
+    os.makedirs(BUILD, exist_ok=True)
+    srcs = units()
+    with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(lambda s: _compile(s, list(extra)), srcs))
+    cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC", "-o", LIB + ".tmp",
+           *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + r.stderr[-8000:])
+        raise RuntimeError("nvcc link failed:\n" + r.stderr[-8000:])
     os.replace(LIB + ".tmp", LIB)
-    log = os.path.join(ROOT, "profiles", "ptxas_latest.txt")
-    try:
-        os.makedirs(os.path.dirname(log), exist_ok=True)
-        with open(log, "w") as f:
-            f.write(" ".join(cmd) + "\n")
-            f.write(r.stderr)
-    except OSError:
-        pass
     if verbose:
-        print(r.stderr)
+        for s in srcs:
+            n = os.path.splitext(os.path.basename(s))[0]
+            print(open(os.path.join(BUILD, f"ptxas_{n}.txt")).read())
     return LIB
 
 

@@ -1,0 +1,399 @@
+// libpdssm.so: tcgen05 GEMMs (select a2-a4, projection a5, readout a8, adjoint, D_t generator, soft generator).
+#include "api_internal.cuh"
+#include "k_select.cuh"
+#include "k_scan_bwd.cuh"
+#include "k_gemm_tc.cuh"
+#include "k_surrogate.cuh"
+
+using namespace pdssm;
+using namespace pdssm::api;
+
+namespace pdssm {
+namespace api {
+
+// ---------------------------------------------------------------------------
+// tcgen05 GEMMs (a2/a3 select, a5 projection): TMA descriptors and launch
+// ---------------------------------------------------------------------------
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+// K-major operand [rows][kdim] (row stride kdim elements): box = one 128-byte K slab x box_rows,
+// SWIZZLE_128B (the layout the UMMA descriptors describe); out-of-range boxes read zeros
+bool make_kmajor_map(CUtensorMap* m, const void* ptr, size_t esz, int64_t kdim, int64_t rows, int box_rows) {
+    EncodeTiledFn f = encode_tiled();
+    if (!f) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)kdim, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)(kdim * esz)};
+    cuuint32_t box[2] = {(cuuint32_t)(tc::ROWB / esz), (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1, 1};
+    return f(m, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr),
+             dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// 3-D operand: dims {K, d1, d2} (elements), byte strides of d1 and d2, box {128 B of K, b1, b2}
+bool make_map3(CUtensorMap* m, const void* ptr, size_t esz, const int64_t (&dims)[3], const int64_t (&strides)[2],
+               int b1, int b2) {
+    EncodeTiledFn f = encode_tiled();
+    if (!f) return false;
+    cuuint64_t d[3] = {(cuuint64_t)dims[0], (cuuint64_t)dims[1], (cuuint64_t)dims[2]};
+    cuuint64_t st[2] = {(cuuint64_t)strides[0], (cuuint64_t)strides[1]};
+    cuuint32_t box[3] = {(cuuint32_t)(tc::ROWB / esz), (cuuint32_t)b1, (cuuint32_t)b2};
+    cuuint32_t es[3] = {1, 1, 1};
+    return f(m, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(ptr),
+             d, st, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int64_t gcd64(int64_t a, int64_t b) { return b ? gcd64(b, a % b) : a; }
+
+// operands usable by TMA: 16-byte aligned base and row pitch
+bool tc_operands_ok(const Geo& g, std::initializer_list<const void*> ptrs) {
+    if (path_generic_forced() || !encode_tiled()) return false;
+    if ((g.d_in * (int64_t)g.act) % 16 != 0) return false;
+    for (const void* p : ptrs)
+        if (misaligned(p, 16)) return false;
+    return true;
+}
+
+// stages: bf16 4 x 48 KB ring; fp32 (3xTF32, hi + lo slabs) 2 x 96 KB
+template <typename T>
+constexpr int tc_stages() { return std::is_same<T, float>::value ? 2 : 4; }
+
+template <typename T, class Epi>
+pdssm_status launch_tc_maps(const CUtensorMap& mA, const CUtensorMap& mB, int64_t kdim, int bn, tc::TileMap tm,
+                            dim3 grid, Epi epi, cudaStream_t st, const char* what) {
+    constexpr bool SPLIT = std::is_same<T, float>::value;
+    constexpr int STAGES = tc_stages<T>();
+    using SM = tc::Smem<T, STAGES, SPLIT>;
+    const size_t smem = SM::bytes(256);   // sized for the largest tile: one attribute per instantiation
+    auto kern = tc::k_gemm_tc<T, STAGES, SPLIT, Epi>;
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
+    if (attr_err != cudaSuccess) return fail(PDSSM_ERR_CUDA, "%s: cudaFuncSetAttribute: %s", what, cudaGetErrorString(attr_err));
+    const int nk = (int)ceil_div(kdim * (int64_t)sizeof(T), tc::ROWB);
+    const tc::TileGrid tg{(int)grid.x, (int)grid.y, (int)grid.z};
+    const int ntiles = tg.gx * tg.gy * tg.gz;
+    const int nctas = ntiles < num_sms_dev() ? ntiles : num_sms_dev();   // persistent
+    kern<<<nctas, tc::THREADS, SM::bytes(bn), st>>>(mA, mB, nk, bn, tm, tg, epi);
+    return cuda_check(what);
+}
+
+// plain 2-D case: A [rows_a][d_in], B [rows_b][d_in]
+template <typename T, class Epi>
+pdssm_status launch_tc(const Geo& g, const void* A, int64_t rows_a, const void* Bm, int64_t rows_b, int bn, Epi epi,
+                       cudaStream_t st, const char* what) {
+    CUtensorMap mA, mB;
+    if (!make_kmajor_map(&mA, A, sizeof(T), g.d_in, rows_a, tc::BM) ||
+        !make_kmajor_map(&mB, Bm, sizeof(T), g.d_in, rows_b, bn))
+        return fail(PDSSM_ERR_CUDA, "%s: cuTensorMapEncodeTiled failed", what);
+    dim3 grid((unsigned)ceil_div(rows_a, tc::BM), (unsigned)ceil_div(rows_b, bn));
+    return launch_tc_maps<T>(mA, mB, g.d_in, bn, tc::TileMap{0, 1, 1, 0}, grid, epi, st, what);
+}
+
+// readout weights, act dtype: Cp[h][p][(c,n)] (y = Cp . h) and CT[h][(c,n)][p] (e = CT . dy),
+// both carrying the sign of Re(C h) = C_re h_re - C_im h_im
+template <typename T>
+__global__ void k_readout_weights(const float* __restrict__ C, T* __restrict__ Cp, T* __restrict__ CT, int H, int nc,
+                                  int P, int N) {
+    const int64_t total = (int64_t)H * nc * P * N;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int n = (int)(i % N);
+        const int p = (int)((i / N) % P);
+        const int c = (int)((i / ((int64_t)N * P)) % nc);
+        const int h = (int)(i / ((int64_t)N * P * nc));
+        const float v = c == 0 ? C[i] : -C[i];
+        const int cN = nc * N;
+        if (Cp) stact(Cp + ((size_t)h * P + p) * cN + c * N + n, v);
+        if (CT) stact(CT + ((size_t)h * cN + c * N + n) * P + p, v);
+    }
+}
+
+// tensor-core readout applicability: TMA row pitches, 16-column output groups
+bool tc_readout_ok(const Geo& g, std::initializer_list<const void*> ptrs) {
+    if (path_generic_forced() || !encode_tiled()) return false;
+    if ((g.nc * g.N * (int64_t)g.act) % 16 != 0 || g.P % 16 != 0 || (g.nc * g.N) % 16 != 0) return false;
+    if ((g.P * (int64_t)g.act) % 16 != 0) return false;
+    for (const void* p : ptrs)
+        if (misaligned(p, 16)) return false;
+    return true;
+}
+
+// y[b][t][h][p] = sum_w Cp[h][p][w] h[b][h][t][w]  (A: 3-D (cN, L, S) map, z = sequence)
+template <typename T>
+pdssm_status readout_tc(const Geo& g, const T* hseq, const T* Cp, T* y, cudaStream_t st) {
+    const int64_t cN = g.nc * g.N;
+    const int bn = (int)(g.P < 256 ? g.P : 256);
+    CUtensorMap mA, mB;
+    const int64_t da[3] = {cN, g.L, g.S};
+    const int64_t sa[2] = {cN * (int64_t)sizeof(T), g.L * cN * (int64_t)sizeof(T)};
+    if (!make_map3(&mA, hseq, sizeof(T), da, sa, tc::BM, 1) || !make_kmajor_map(&mB, Cp, sizeof(T), cN, g.H * g.P, bn))
+        return fail(PDSSM_ERR_CUDA, "readout_tc: cuTensorMapEncodeTiled failed");
+    const int tiles = (int)ceil_div(g.L, tc::BM);
+    dim3 grid((unsigned)(tiles * g.S), (unsigned)ceil_div(g.P, bn));
+    return launch_tc_maps<T>(mA, mB, cN, bn, tc::TileMap{1, tiles, (int)g.H, (int)g.P}, grid,
+                             tc::EpiReadout<T>{y, (int)g.L, (int)g.H, (int)g.P}, st, "readout_tc");
+}
+
+// e[b][h][t][w] = dh + sum_p CT[h][w][p] dy[b][t][h][p]  (A: 3-D (P, H, B*L) map, z = head)
+template <typename T>
+pdssm_status adjoint_tc(const Geo& g, const T* dy, const T* CT, const T* dh, float* e, cudaStream_t st) {
+    const int64_t cN = g.nc * g.N;
+    const int bn = (int)(cN < 256 ? cN : 256);
+    CUtensorMap mA, mB;
+    const int64_t da[3] = {g.P, g.H, g.B * g.L};
+    const int64_t sa[2] = {g.P * (int64_t)sizeof(T), g.H * g.P * (int64_t)sizeof(T)};
+    if (!make_map3(&mA, dy, sizeof(T), da, sa, 1, tc::BM) || !make_kmajor_map(&mB, CT, sizeof(T), g.P, g.H * cN, bn))
+        return fail(PDSSM_ERR_CUDA, "adjoint_tc: cuTensorMapEncodeTiled failed");
+    dim3 grid((unsigned)ceil_div(g.B * g.L, tc::BM), (unsigned)ceil_div(cN, bn), (unsigned)g.H);
+    return launch_tc_maps<T>(mA, mB, g.P, bn, tc::TileMap{2, 1, 1, (int)cN}, grid,
+                             tc::EpiAdjoint<T>{e, dh, g.B * g.L, (int)g.L, (int)g.H, (int)cN}, st, "adjoint_tc");
+}
+
+// select tile width: whole heads, a multiple of lcm(K, 16), <= 256 (0: not possible)
+int select_bn(const Geo& g) {
+    const int64_t l = g.K / gcd64(g.K, 16) * 16;
+    if (l > 256) return 0;
+    const int64_t full = (256 / l) * l;
+    const int64_t need = ceil_div(g.H * g.K, l) * l;
+    return (int)(need < full ? need : full);
+}
+
+// direct state gradient e = dh + conj(C)^T dy (bwd with a readout): tensor cores when the
+// shapes allow it (CT staged in wbuf), else the SIMT kernel
+template <typename T, int NC>
+pdssm_status prepare_e(const Geo& g, const void* dh, const void* dy, const float* C, float* e, void* wbuf,
+                       cudaStream_t st) {
+    if (tc_readout_ok(g, {dy, dh, e, wbuf})) {
+        T* CT = static_cast<T*>(wbuf);
+        k_readout_weights<T><<<(unsigned)ceil_div(g.H * g.nc * g.P * g.N, 256), 256, 0, st>>>(C, nullptr, CT, (int)g.H,
+                                                                                              (int)g.nc, (int)g.P, (int)g.N);
+        pdssm_status r = cuda_check("readout_weights");
+        if (r) return r;
+        return adjoint_tc<T>(g, static_cast<const T*>(dy), CT, static_cast<const T*>(dh), e, st);
+    }
+    k_bwd_prepare_e<T, NC><<<(unsigned)(g.S * g.L), 128, (size_t)g.P * 4, st>>>(
+        static_cast<const T*>(dh), static_cast<const T*>(dy), C, e, (int)g.H, (int)g.L, (int)g.N, (int)g.P);
+    return cuda_check("bwd_prepare_e");
+}
+
+// y = Re(C h) right after the scan: tensor cores when the shapes allow it, else SIMT
+pdssm_status readout_run(const Geo& g, const void* hout, const float* C_opt, void* y_opt, void* wbuf, cudaStream_t st) {
+    return with_act(g.dtype, [&](auto tv) {
+        using T = decltype(tv);
+        if (tc_readout_ok(g, {hout, y_opt, wbuf})) {
+            T* Cp = static_cast<T*>(wbuf);
+            k_readout_weights<T><<<(unsigned)ceil_div(g.H * g.nc * g.P * g.N, 256), 256, 0, st>>>(
+                C_opt, Cp, nullptr, (int)g.H, (int)g.nc, (int)g.P, (int)g.N);
+            pdssm_status rr = cuda_check("readout_weights");
+            if (rr) return rr;
+            return readout_tc<T>(g, static_cast<const T*>(hout), Cp, static_cast<T*>(y_opt), st);
+        }
+        return with_nc(g.nc, [&](auto ncv) {
+            constexpr int NC = decltype(ncv)::value;
+            k_readout<T, NC><<<(unsigned)(g.S * g.L), 128, (size_t)NC * g.N * 4, st>>>(
+                static_cast<const T*>(hout), C_opt, static_cast<T*>(y_opt), (int)g.H, (int)g.L, (int)g.N, (int)g.P);
+            return cuda_check("readout");
+        });
+    });
+}
+
+pdssm_status prepare_e_run(const Geo& g, const void* dh, const void* dy, const float* C, float* e, void* wbuf,
+                           cudaStream_t st) {
+    return with_act(g.dtype, [&](auto tv) {
+        using T = decltype(tv);
+        return with_nc(g.nc, [&](auto ncv) {
+            constexpr int NC = decltype(ncv)::value;
+            return prepare_e<T, NC>(g, dh, dy, C, e, wbuf, st);
+        });
+    });
+}
+
+}  // namespace api
+}  // namespace pdssm
+
+PDSSM_DEFINE_ERRWORD(gemm)
+
+extern "C" {
+
+pdssm_status pdssm_select(const void* x, const void* S, const uint16_t* dict_idx, uint8_t* kstar, uint16_t* P_opt,
+                          float* logits_opt, const pdssm_dims* dims, void* ws, size_t ws_bytes,
+                          pdssm_stream_t stream) {
+    Geo g;
+    pdssm_status r = geo_of(dims, &g);
+    if (r) return r;
+    if (g.d_in < 1) return fail(PDSSM_ERR_SHAPE, "select: d_in must be >= 1");
+    if (!x || !S || !kstar) return fail(PDSSM_ERR_NULL, "select: x, S, kstar are required");
+    if (P_opt && !dict_idx) return fail(PDSSM_ERR_NULL, "select: P_opt needs dict_idx");
+    if (misaligned(x, g.act) || misaligned(S, g.act) || misaligned(dict_idx, 2) || misaligned(P_opt, 2) ||
+        misaligned(logits_opt, 4))
+        return fail(PDSSM_ERR_ALIGN, "select: misaligned pointer");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    // tensor-core path (a2 logits in TMEM, a3 argmax + a4 P gather fused in the epilogue)
+    const int bn = select_bn(g);
+    if (bn > 0 && tc_operands_ok(g, {x, S})) {
+        tc::EpiSelect epi{kstar, logits_opt, dict_idx, P_opt, g.B * g.L, (int)g.L, (int)g.H, (int)g.K, (int)g.N, g.flags};
+        return with_act(g.dtype, [&](auto tv) {
+            using T = decltype(tv);
+            return launch_tc<T>(g, x, g.B * g.L, S, g.H * g.K, bn, epi, st, "select_tc");
+        });
+    }
+    float* logits = logits_opt;
+    if (!logits) {
+        if (!ws || ws_bytes < ws_bytes_g(g, PDSSM_OP_SELECT))
+            return fail(PDSSM_ERR_WORKSPACE, "select: workspace too small (need %zu)", ws_bytes_g(g, PDSSM_OP_SELECT));
+        logits = static_cast<float*>(ws);
+    }
+    const int64_t M = g.B * g.L, NN = g.H * g.K;
+    dim3 grid((unsigned)ceil_div(M, 64), (unsigned)ceil_div(NN, 64));
+    r = with_act(g.dtype, [&](auto tv) {
+        using T = decltype(tv);
+        k_select_logits_simt<T><<<grid, 256, 0, st>>>(static_cast<const T*>(x), static_cast<const T*>(S), logits,
+                                                      (int)g.B, (int)g.L, (int)g.H, (int)g.K, (int)g.d_in, g.flags);
+        return cuda_check("select_logits");
+    });
+    if (r) return r;
+    const int64_t rows = g.S * g.L;
+    k_select_argmax<<<(unsigned)ceil_div(rows, 8), dim3(32, 8), 0, st>>>(logits, dict_idx, kstar, P_opt, rows,
+                                                                       (int)g.H, (int)g.L, (int)g.N, (int)g.K);
+    return cuda_check("select_argmax");
+}
+
+pdssm_status pdssm_project(const void* x, const void* Bw, void* b_out, const pdssm_dims* dims, pdssm_stream_t stream) {
+    Geo g;
+    pdssm_status r = geo_of(dims, &g);
+    if (r) return r;
+    if (g.d_in < 1) return fail(PDSSM_ERR_SHAPE, "project: d_in must be >= 1");
+    if (!x || !Bw || !b_out) return fail(PDSSM_ERR_NULL, "project: x, Bw, b_out are required");
+    if (misaligned(x, g.act) || misaligned(Bw, g.act) || misaligned(b_out, g.act))
+        return fail(PDSSM_ERR_ALIGN, "project: misaligned pointer");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t cN = g.nc * g.N, NN = g.H * cN;
+    if (cN % 16 == 0 && tc_operands_ok(g, {x, Bw, b_out})) {
+        return with_act(g.dtype, [&](auto tv) {
+            using T = decltype(tv);
+            tc::EpiProject<T> epi{static_cast<T*>(b_out), g.B * g.L, (int)g.L, (int)g.H, (int)cN, NN};
+            return launch_tc<T>(g, x, g.B * g.L, Bw, NN, (int)(NN < 256 ? NN : 256), epi, st, "project_tc");
+        });
+    }
+    dim3 grid((unsigned)ceil_div(g.B * g.L, 64), (unsigned)ceil_div(NN, 64));
+    return with_act(g.dtype, [&](auto tv) {
+        using T = decltype(tv);
+        k_project_simt<T><<<grid, 256, 0, st>>>(static_cast<const T*>(x), static_cast<const T*>(Bw),
+                                                static_cast<T*>(b_out), (int)g.B, (int)g.L, (int)g.H, (int)cN,
+                                                (int)g.d_in);
+        return cuda_check("project_simt");
+    });
+}
+
+pdssm_status pdssm_diag_gen(const void* x, const void* Wd, const float* bias_opt, void* D_out, const pdssm_dims* dims,
+                            pdssm_stream_t stream) {
+    Geo g;
+    pdssm_status r = geo_of(dims, &g);
+    if (r) return r;
+    if (g.d_in < 1) return fail(PDSSM_ERR_SHAPE, "diag_gen: d_in must be >= 1");
+    if (!x || !Wd || !D_out) return fail(PDSSM_ERR_NULL, "diag_gen: x, Wd, D_out are required");
+    if (misaligned(x, g.act) || misaligned(Wd, g.act) || misaligned(D_out, g.act) || misaligned(bias_opt, 4))
+        return fail(PDSSM_ERR_ALIGN, "diag_gen: misaligned pointer");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t cN = g.nc * g.N, NN = g.H * cN;
+    if (g.N % 16 == 0 && cN <= 256 && tc_operands_ok(g, {x, Wd, D_out})) {
+        return with_act(g.dtype, [&](auto tv) {
+            using T = decltype(tv);
+            tc::EpiDiag<T> epi{static_cast<T*>(D_out), bias_opt, g.B * g.L, (int)g.L, (int)g.H, (int)g.N, (int)g.nc};
+            return launch_tc<T>(g, x, g.B * g.L, Wd, NN, (int)cN, epi, st, "diag_gen_tc");   // one head per tile
+        });
+    }
+    if ((r = pdssm_project(x, Wd, D_out, dims, stream))) return r;
+    return with_act(g.dtype, [&](auto tv) {
+        using T = decltype(tv);
+        const int64_t rows = g.S * g.L;
+        sg::k_diag_activate<T><<<(unsigned)std::min<int64_t>(ceil_div(rows * g.N, 256), 65535), 256, 0, st>>>(
+            static_cast<T*>(D_out), bias_opt, rows, (int)g.H, (int)g.L, (int)g.N, (int)g.nc);
+        return cuda_check("diag_activate");
+    });
+}
+
+pdssm_status pdssm_soft_select(const float* logits, const float* M, uint16_t* P_out, const pdssm_dims* dims, void* ws,
+                               size_t ws_bytes, pdssm_stream_t stream) {
+    Geo g;
+    pdssm_status r = geo_of(dims, &g);
+    if (r) return r;
+    if (!logits || !M || !P_out) return fail(PDSSM_ERR_NULL, "soft_select: logits, M, P_out are required");
+    if (g.N % 16 != 0 || g.N > 256) return fail(PDSSM_ERR_UNSUPPORTED, "soft_select: N must be a multiple of 16 <= 256");
+    if (misaligned(logits, 4) || misaligned(M, 4) || misaligned(P_out, 2) || misaligned(ws, 256))
+        return fail(PDSSM_ERR_ALIGN, "soft_select: misaligned pointer");
+    const size_t need = ws_bytes_g(g, PDSSM_OP_SOFT);
+    if (!ws || ws_bytes < need) return fail(PDSSM_ERR_WORKSPACE, "soft_select: workspace too small (need %zu)", need);
+    if (!encode_tiled()) return fail(PDSSM_ERR_UNSUPPORTED, "soft_select: tensor-map encoder unavailable");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t kp = (g.K + 7) / 8 * 8, BL = g.B * g.L;
+    Geo gk = g;
+    gk.d_in = kp;   // the GEMM's K dimension
+    const int bn = (256 / (int)g.N) * (int)g.N;
+    return with_act(g.dtype, [&](auto tv) {
+        using T = decltype(tv);
+        T* sbuf = static_cast<T*>(ws);
+        T* Mt = reinterpret_cast<T*>(static_cast<char*>(ws) + align256((size_t)g.H * BL * kp * g.act));
+        sg::k_soft_stage_s<T><<<(unsigned)ceil_div(BL * g.H, 8), 256, 0, st>>>(logits, sbuf, BL, (int)g.H, (int)g.L,
+                                                                               (int)g.K, (int)kp);
+        sg::k_soft_stage_M<T><<<(unsigned)std::min<int64_t>(ceil_div(g.H * g.N * g.N * kp, 256), 65535), 256, 0, st>>>(
+            M, Mt, (int)g.H, (int)g.K, (int)g.N, (int)kp);
+        pdssm_status rr = cuda_check("soft_stage");
+        if (rr) return rr;
+        for (int64_t h = 0; h < g.H; ++h) {
+            tc::EpiColArgmax epi{P_out, BL, (int)g.L, (int)g.H, (int)g.N, (int)h};
+            rr = launch_tc<T>(gk, sbuf + (size_t)h * BL * kp, BL, Mt + (size_t)h * g.N * g.N * kp, g.N * g.N, bn, epi, st,
+                              "soft_select_tc");
+            if (rr) return rr;
+        }
+        return PDSSM_OK;
+    });
+}
+
+pdssm_status pdssm_readout(const void* h, const float* C, void* y, const pdssm_dims* dims, void* ws, size_t ws_bytes,
+                           pdssm_stream_t stream) {
+    Geo g;
+    pdssm_status r = geo_of(dims, &g);
+    if (r) return r;
+    if (!h || !C || !y) return fail(PDSSM_ERR_NULL, "readout: h, C, y are required");
+    if (g.P < 1) return fail(PDSSM_ERR_SHAPE, "readout: p_out must be >= 1");
+    if (misaligned(h, g.act) || misaligned(y, g.act) || misaligned(C, 4)) return fail(PDSSM_ERR_ALIGN, "readout: misaligned");
+    if (!ws || ws_bytes < readout_w_bytes(g))
+        return fail(PDSSM_ERR_WORKSPACE, "readout: workspace too small (need %zu)", readout_w_bytes(g));
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    return with_act(g.dtype, [&](auto tv) {
+        using T = decltype(tv);
+        if (tc_readout_ok(g, {h, y, ws})) {
+            T* Cp = static_cast<T*>(ws);
+            k_readout_weights<T><<<(unsigned)ceil_div(g.H * g.nc * g.P * g.N, 256), 256, 0, st>>>(
+                C, Cp, nullptr, (int)g.H, (int)g.nc, (int)g.P, (int)g.N);
+            pdssm_status rr = cuda_check("readout_weights");
+            if (rr) return rr;
+            return readout_tc<T>(g, static_cast<const T*>(h), Cp, static_cast<T*>(y), st);
+        }
+        return with_nc(g.nc, [&](auto ncv) {
+            constexpr int NC = decltype(ncv)::value;
+            k_readout<T, NC><<<(unsigned)(g.S * g.L), 128, (size_t)NC * g.N * 4, st>>>(
+                static_cast<const T*>(h), C, static_cast<T*>(y), (int)g.H, (int)g.L, (int)g.N, (int)g.P);
+            return cuda_check("readout");
+        });
+    });
+}
+
+}  // extern "C"

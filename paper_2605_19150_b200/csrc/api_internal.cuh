@@ -1,0 +1,278 @@
+// Internal host-side helpers shared by the library's translation units (not part of the ABI).
+// The library is split into several .cu files that nvcc compiles in parallel
+// (paper_2605_19150_b200/_build.py); this header holds the dims/geometry logic, the
+// workspace carve-up and the declarations of the per-file launchers.
+#pragma once
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <cmath>
+#include <mutex>
+#include <string>
+#include <type_traits>
+#include <utility>
+
+#include "pdssm_common.cuh"
+#include "k_scan_seq.cuh"   // + k_scan_fwd.cuh, k_scan_fused.cuh (Args and Layout types)
+
+namespace pdssm {
+namespace api {
+
+// records the message for pdssm_last_error (thread-local) and returns s (pdssm_api.cu)
+pdssm_status fail(pdssm_status s, const char* fmt, ...);
+
+struct Geo {
+    int64_t B, H, L, N, K, S, d_in, P;
+    int tau, C, nc, dtype, diag_mode;
+    uint32_t flags;
+    size_t act;   // bytes per act element
+};
+
+constexpr uint32_t kKnownFlags = PDSSM_CHECK_FINITE | PDSSM_DETERMINISTIC | PDSSM_SAVE_STATES | PDSSM_EXPORT_MAPS;
+
+// single-chunk (tau = L) scan kernels: one CTA of N threads per sequence
+inline bool seq_shape_ok(int64_t N, int64_t K, int64_t L, int nc, size_t act) {
+    (void)nc; (void)act;
+    return N % 32 == 0 && N <= seq::MAXN && (size_t)K * N * 8 <= 64 * 1024 && L <= seq::LMAX;
+}
+// SM count of the current device (cached per device ordinal)
+inline int num_sms_dev() { return num_sms(); }
+inline bool env_path_is(const char* v) {
+    const char* p = getenv("PDSSM_PATH");
+    return p && strcmp(p, v) == 0;
+}
+
+// Library default chunk length (reading R20: tuning only).  When the B*H sequences
+// alone fill most of the SMs, one chunk per sequence (tau = L) runs the single-pass
+// CTA-per-sequence kernels; otherwise tau = 64 (chunked, decoupled look-back).
+inline int default_tau(const pdssm_dims* d) {
+    const int64_t S = d->batch * d->heads;
+    const bool forced_chunked = env_path_is("fused") || env_path_is("generic");
+    if (!forced_chunked && seq_shape_ok(d->state, d->dict, d->len, d->is_complex, d->dtype == PDSSM_BF16 ? 2 : 4) &&
+        (env_path_is("seq") || S * 10 >= (int64_t)num_sms_dev() * 6) && d->len <= (int64_t)1 << 30)
+        return (int)d->len;
+    return 64;
+}
+
+inline pdssm_status geo_of(const pdssm_dims* d, Geo* g) {
+    if (!d) return fail(PDSSM_ERR_NULL, "dims is NULL");
+    if (d->batch < 1 || d->heads < 1 || d->len < 1)
+        return fail(PDSSM_ERR_SHAPE, "batch, heads, len must be >= 1 (got %lld, %lld, %lld)", (long long)d->batch,
+                    (long long)d->heads, (long long)d->len);
+    if (d->state < 1 || d->state > 1024) return fail(PDSSM_ERR_SHAPE, "state N must be in [1, 1024] (got %lld)", (long long)d->state);
+    if (d->dict < 1 || d->dict > 256) return fail(PDSSM_ERR_SHAPE, "dict K must be in [1, 256] (got %lld)", (long long)d->dict);
+    if (d->is_complex != 1 && d->is_complex != 2) return fail(PDSSM_ERR_SHAPE, "is_complex must be 1 or 2");
+    if (d->dtype != PDSSM_F32 && d->dtype != PDSSM_BF16) return fail(PDSSM_ERR_DTYPE, "unknown dtype %d", d->dtype);
+    if (d->diag_mode != PDSSM_DIAG_PER_STEP && d->diag_mode != PDSSM_DIAG_PER_DICT)
+        return fail(PDSSM_ERR_DTYPE, "unknown diag_mode %d", d->diag_mode);
+    if (d->flags & ~kKnownFlags) return fail(PDSSM_ERR_DTYPE, "unknown flag bits 0x%x", d->flags & ~kKnownFlags);
+    if (d->reserved != 0) return fail(PDSSM_ERR_DTYPE, "reserved must be 0");
+    if (d->chunk < 0) return fail(PDSSM_ERR_SHAPE, "chunk must be >= 0");
+    if (d->p_out < 0 || d->d_in < 0) return fail(PDSSM_ERR_SHAPE, "p_out, d_in must be >= 0");
+    g->B = d->batch; g->H = d->heads; g->L = d->len; g->N = d->state; g->K = d->dict;
+    g->S = g->B * g->H; g->d_in = d->d_in; g->P = d->p_out;
+    g->tau = d->chunk ? d->chunk : default_tau(d);
+    if (g->tau > g->L) g->tau = (int)g->L;
+    g->C = (int)ceil_div(g->L, g->tau);
+    if ((int64_t)g->S * g->C > (int64_t)1 << 31) return fail(PDSSM_ERR_SHAPE, "too many (sequence, chunk) items");
+    g->nc = d->is_complex; g->dtype = d->dtype; g->diag_mode = d->diag_mode; g->flags = d->flags;
+    g->act = d->dtype == PDSSM_BF16 ? 2 : 4;
+    return PDSSM_OK;
+}
+
+inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct Bump {
+    char* base;
+    size_t off = 0;
+    explicit Bump(void* p) : base(static_cast<char*>(p)) {}
+    template <typename T> T* take(size_t bytes) {
+        T* r = reinterpret_cast<T*>(base ? base + off : nullptr);
+        off += align256(bytes);
+        return r;
+    }
+};
+
+inline size_t plan_bytes(const Geo& g) {
+    return align256((size_t)g.H * g.K * (g.N + 1) * 2) + align256((size_t)g.H * g.K * g.N * 2);
+}
+inline size_t cs_pi_bytes(const Geo& g) { return align256((size_t)g.S * g.C * g.N * 2); }
+inline size_t cs_f_bytes(const Geo& g) { return align256((size_t)g.S * g.C * g.nc * g.N * 4); }
+inline size_t chunk_state_bytes_g(const Geo& g) { return cs_pi_bytes(g) + 3 * cs_f_bytes(g); }
+inline size_t seq_f_bytes(const Geo& g) { return align256((size_t)g.S * g.L * g.nc * g.N * 4); }
+// single-chunk plan: preimage records [H][K][N][8], warp trip counts, overflow flags
+inline size_t seq_rec_bytes(const Geo& g) { return align256((size_t)g.H * g.K * g.N * 8); }
+inline size_t seq_wm_bytes(const Geo& g) { return align256((size_t)g.H * g.K * (g.N / 32 > 0 ? g.N / 32 : 1)); }
+inline size_t seq_ovf_bytes(const Geo& g) { return align256((size_t)g.H * g.K); }
+inline size_t seq_plan_bytes(const Geo& g) { return seq_rec_bytes(g) + seq_wm_bytes(g) + seq_ovf_bytes(g); }
+// readout weights staged in act dtype (Cp or CT), H*P*c*N elements
+inline size_t readout_w_bytes(const Geo& g) { return g.P > 0 ? align256((size_t)g.H * g.P * g.nc * g.N * g.act) : 0; }
+inline size_t seq_act_bytes(const Geo& g) { return align256((size_t)g.S * g.L * g.nc * g.N * g.act); }
+inline int npad8(int64_t N) { return (int)((N + 7) & ~7); }
+inline size_t summary_block_bytes(const Geo& g) { return (size_t)npad8(g.N) * 2 + (size_t)2 * g.nc * g.N * 4; }
+
+inline ChunkStateView cs_view(const Geo& g, void* p) {
+    char* b = static_cast<char*>(p);
+    ChunkStateView v;
+    v.pi = reinterpret_cast<uint16_t*>(b);
+    v.d = reinterpret_cast<float*>(b + cs_pi_bytes(g));
+    v.beta = reinterpret_cast<float*>(b + cs_pi_bytes(g) + cs_f_bytes(g));
+    v.carry = reinterpret_cast<float*>(b + cs_pi_bytes(g) + 2 * cs_f_bytes(g));
+    return v;
+}
+
+inline size_t ws_bytes_g(const Geo& g, int op) {
+    switch (op) {
+        case PDSSM_OP_SELECT:
+            return align256((size_t)g.S * g.L * g.K * 4);
+        case PDSSM_OP_FWD:
+            return plan_bytes(g) + (g.P > 0 ? seq_act_bytes(g) + readout_w_bytes(g) : 0) +
+                   fused_plan_bytes(g.H, g.K, g.N) + fused_ctrl_bytes(g.S, g.C, g.H) + seq_plan_bytes(g);
+        case PDSSM_OP_BWD:
+            return 2 * cs_f_bytes(g) + (g.P > 0 ? seq_f_bytes(g) + readout_w_bytes(g) : 0) +
+                   (g.diag_mode == PDSSM_DIAG_PER_DICT ? seq_f_bytes(g) : 0) + fused_ctrl_bytes(g.S, g.C, g.H) +
+                   plan_bytes(g);
+        case PDSSM_OP_READOUT:
+            return readout_w_bytes(g);
+        case PDSSM_OP_SOFT: {   // s [H][B L][Kp] and Mt [H][N^2][Kp] in the act dtype
+            const int64_t kp = (g.K + 7) / 8 * 8;
+            return align256((size_t)g.H * g.B * g.L * kp * g.act) + align256((size_t)g.H * g.N * g.N * kp * g.act);
+        }
+        case PDSSM_OP_LAYER: {
+            const size_t sel = align256((size_t)g.S * g.L * g.K * 4), fwd = ws_bytes_g(g, PDSSM_OP_FWD);
+            return seq_act_bytes(g) + (sel > fwd ? sel : fwd);
+        }
+        case PDSSM_OP_SEGMENT: {
+            size_t fwd = plan_bytes(g) + chunk_state_bytes_g(g);
+            size_t bwd = 2 * cs_f_bytes(g) + (g.P > 0 ? seq_f_bytes(g) + readout_w_bytes(g) : 0);
+            return fwd > bwd ? fwd : bwd;
+        }
+        default:
+            return 0;
+    }
+}
+
+inline bool misaligned(const void* p, size_t a) { return p && (reinterpret_cast<uintptr_t>(p) % a) != 0; }
+
+inline pdssm_status cuda_check(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(PDSSM_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    return PDSSM_OK;
+}
+
+inline int threads_for(int64_t N) { return (int)((N + 31) / 32 * 32); }
+
+template <typename F>
+inline pdssm_status with_nc(int nc, F&& f) {
+    if (nc == 1) return f(std::integral_constant<int, 1>{});
+    return f(std::integral_constant<int, 2>{});
+}
+
+template <typename F>
+inline pdssm_status with_act(int dtype, F&& f) {
+    if (dtype == PDSSM_BF16) return f(__nv_bfloat16{});
+    return f(float{});
+}
+
+template <typename F>
+inline pdssm_status with_pd(int mode, F&& f) {
+    if (mode == PDSSM_DIAG_PER_DICT) return f(std::true_type{});
+    return f(std::false_type{});
+}
+
+inline pdssm_status set_smem(const void* fn, size_t bytes) {
+    if (bytes > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        if (e != cudaSuccess) return fail(PDSSM_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    }
+    return PDSSM_OK;
+}
+
+// ------------------------------------------------------------------ fused fast path
+// PDSSM_PATH=generic forces the three-phase kernels (used by the tests to cover both).
+inline bool path_generic_forced() {
+    const char* p = getenv("PDSSM_PATH");
+    return p && strcmp(p, "generic") == 0;
+}
+// PDSSM_PATH=fused makes the fused path mandatory (tests): a shape it cannot take is an error
+inline bool path_fused_forced() {
+    const char* p = getenv("PDSSM_PATH");
+    return p && strcmp(p, "fused") == 0;
+}
+// ---------------------------------------------------------------------------
+// single-chunk path: plan, sizing, launches
+// ---------------------------------------------------------------------------
+
+constexpr size_t kSeqSmemBudget = 200 * 1024;
+constexpr int kSeqG = seq::SEQ_G;     // backward group
+constexpr int kSeqGF = seq::SEQ_GF;   // forward group
+
+// ring depth R for this shape (0: the layout does not fit)
+// ring depth R for this shape (0: the layout does not fit).  When there are more
+// sequences than SMs, the budget is split so that ceil(S / #SMs) CTAs (up to 4) fit per SM.
+inline int seq_ring(const Geo& g, bool bwd, bool agg, size_t esz_e) {
+    const int G = bwd ? kSeqG : kSeqGF;
+    const int ngroups = (int)ceil_div(g.L, G);
+    const int64_t per_sm = std::min<int64_t>(std::max<int64_t>(ceil_div(g.S, num_sms_dev()), 1), 4);
+    const size_t budget = std::min<size_t>(kSeqSmemBudget, (size_t)(226 * 1024) / (size_t)per_sm - 1024);
+    int best = 0;
+    for (int R = 2; R <= 16 && R <= ngroups + 1; ++R) {
+        seq::Layout ly((int)g.N, (int)g.K, R, G, g.nc, (int)g.act, (int)esz_e, g.diag_mode == PDSSM_DIAG_PER_DICT, agg, bwd,
+                       (int)g.L);
+        if (ly.bytes <= budget) best = R;
+    }
+    if (best == 0 && ngroups <= 1) best = 2;
+    return best;
+}
+
+inline bool seq_applicable(const Geo& g, std::initializer_list<const void*> ptrs) {
+    if (g.C != 1 || env_path_is("fused") || env_path_is("generic")) return false;
+    if (!seq_shape_ok(g.N, g.K, g.L, g.nc, g.act)) return false;
+    for (const void* p : ptrs)
+        if (misaligned(p, 16)) return false;
+    return seq_ring(g, false, true, g.act) >= 2 && seq_ring(g, true, false, 4) >= 2;
+}
+
+inline pdssm_status seq_set_smem(const void* f, size_t bytes) {
+    cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return fail(PDSSM_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    return PDSSM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// launchers defined in the other translation units
+// ---------------------------------------------------------------------------
+// api_seq_fwd.cu / api_seq_bwd.cu: single-chunk path (one CTA per sequence)
+pdssm_status fwd_seq(const Geo& g, seq::SeqArgs& sa, uint8_t* rec, uint8_t* wm, uint8_t* ovf, cudaStream_t st);
+pdssm_status bwd_seq_run(const Geo& g, seq::SeqArgs& sa, bool e_f32, cudaStream_t st);
+// api_fused.cu: chunked warp-per-item path with decoupled look-back
+bool fused_applicable(const Geo& g, std::initializer_list<const void*> ptrs);
+pdssm_status fwd_fused(const Geo& g, fused::FusedArgs& fa, uint8_t* rec, uint32_t* hdr, cudaStream_t st);
+pdssm_status bwd_fused_run(const Geo& g, fused::FusedArgs& fa, bool e_f32, cudaStream_t st);
+// api_gemm.cu: readout y = Re(C h) after the scan, and the backward's e = dh + conj(C)^T dy
+pdssm_status readout_run(const Geo& g, const void* h, const float* C, void* y, void* wbuf, cudaStream_t st);
+pdssm_status prepare_e_run(const Geo& g, const void* dh, const void* dy, const float* C, float* e, void* wbuf,
+                           cudaStream_t st);
+
+// device error words: one per translation unit (internal linkage, pdssm_common.cuh);
+// each reader copies its unit's word out and clears it
+cudaError_t errword_core(uint32_t* w);
+cudaError_t errword_seq_fwd(uint32_t* w);
+cudaError_t errword_seq_bwd(uint32_t* w);
+cudaError_t errword_fused(uint32_t* w);
+cudaError_t errword_gemm(uint32_t* w);
+cudaError_t errword_grad(uint32_t* w);
+
+}  // namespace api
+}  // namespace pdssm
+
+#define PDSSM_DEFINE_ERRWORD(name)                                                       \
+    cudaError_t pdssm::api::errword_##name(uint32_t* w) {                                 \
+        cudaError_t e = cudaMemcpyFromSymbol(w, pdssm::g_err_word, sizeof(uint32_t));     \
+        if (e != cudaSuccess) return e;                                                  \
+        const uint32_t z = 0;                                                            \
+        return cudaMemcpyToSymbol(pdssm::g_err_word, &z, sizeof(uint32_t));              \
+    }

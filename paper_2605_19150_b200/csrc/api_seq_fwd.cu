@@ -1,0 +1,64 @@
+// libpdssm.so: single-chunk forward scan launcher (k_fwd_seq, csrc/k_scan_seq.cuh).
+#include "api_internal.cuh"
+
+using namespace pdssm;
+using namespace pdssm::api;
+
+namespace pdssm {
+namespace api {
+
+pdssm_status fwd_seq(const Geo& g, seq::SeqArgs& sa, uint8_t* rec, uint8_t* wm, uint8_t* ovf, cudaStream_t st) {
+    seq::k_build_seq_plan<<<(unsigned)(g.H * g.K), (unsigned)g.N, (size_t)g.N * 2, st>>>(
+        sa.dict_idx, rec, wm, ovf, const_cast<uint16_t*>(sa.pstart), const_cast<uint16_t*>(sa.psrc), (int)g.N, g.flags);
+    pdssm_status r = cuda_check("build_seq_plan");
+    if (r) return r;
+    // beta_bar needs its own replay from a zero carry unless h0 is zero (then it is the final state)
+    const bool agg = (g.flags & PDSSM_EXPORT_MAPS) != 0 || sa.h0 != nullptr;
+    sa.R = seq_ring(g, false, agg, g.act);
+    sa.G = kSeqGF;
+    return with_act(g.dtype, [&](auto tv) {
+        using T = decltype(tv);
+        return with_nc(g.nc, [&](auto ncv) {
+            constexpr int NC = decltype(ncv)::value;
+            return with_pd(g.diag_mode, [&](auto pdv) {
+                constexpr bool PD = decltype(pdv)::value;
+                auto go = [&](auto aggv, auto chkv) {
+                    constexpr bool AGG = decltype(aggv)::value;
+                    constexpr bool CHK = decltype(chkv)::value;
+                    seq::Layout ly((int)g.N, (int)g.K, sa.R, sa.G, NC, (int)sizeof(T), (int)sizeof(T), PD, AGG, false,
+                                   (int)g.L);
+                    // compile-time N for the production variants (no maps, no checks)
+                    auto kern = seq::k_fwd_seq<T, NC, PD, AGG, CHK, 0>;
+                    if constexpr (!AGG && !CHK) {
+                        if (g.N == 128) kern = seq::k_fwd_seq<T, NC, PD, false, false, 128>;
+                        else if (g.N == 64) kern = seq::k_fwd_seq<T, NC, PD, false, false, 64>;
+                    }
+                    pdssm_status rr = seq_set_smem((const void*)kern, ly.bytes);
+                    if (rr) return rr;
+                    // programmatic dependent launch: the prologue overlaps the plan kernel's tail
+                    cudaLaunchConfig_t cfg = {};
+                    cfg.gridDim = dim3((unsigned)g.S);
+                    cfg.blockDim = dim3((unsigned)g.N + 32);   // + producer warp
+                    cfg.dynamicSmemBytes = ly.bytes;
+                    cfg.stream = st;
+                    cudaLaunchAttribute attr[1];
+                    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                    attr[0].val.programmaticStreamSerializationAllowed = 1;
+                    cfg.attrs = attr;
+                    cfg.numAttrs = 1;
+                    cudaError_t le = cudaLaunchKernelEx(&cfg, kern, sa);
+                    if (le != cudaSuccess) return fail(PDSSM_ERR_CUDA, "fwd_seq launch: %s", cudaGetErrorString(le));
+                    return cuda_check("fwd_seq");
+                };
+                const bool chk = (g.flags & PDSSM_CHECK_FINITE) != 0;
+                if (agg) return chk ? go(std::true_type{}, std::true_type{}) : go(std::true_type{}, std::false_type{});
+                return chk ? go(std::false_type{}, std::true_type{}) : go(std::false_type{}, std::false_type{});
+            });
+        });
+    });
+}
+
+}  // namespace api
+}  // namespace pdssm
+
+PDSSM_DEFINE_ERRWORD(seq_fwd)

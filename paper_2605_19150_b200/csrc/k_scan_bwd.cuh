@@ -82,11 +82,15 @@ __global__ void k_bwd_phaseB(ChunkStateView cs, const float* __restrict__ betap,
         }
         __syncthreads();
         if (act) {
-            const int pj = cs.pi[ci * N + j];
-            cpx db{cs.d[ci * NC * N + j], NC == 2 ? cs.d[ci * NC * N + N + j] : 0.f};
             cpx bp{betap[ci * NC * N + j], NC == 2 ? betap[ci * NC * N + N + j] : 0.f};
-            cpx mP{msh[pj], NC == 2 ? msh[N + pj] : 0.f};
-            mu = cadd(bp, cmulc(db, mP));
+            if (c == C_ch - 1 && !lam_in) {
+                mu = bp;   // mu_{C-1} = 0: the Abar^T term vanishes (and the aggregate is not read)
+            } else {
+                const int pj = min((int)cs.pi[ci * N + j], N - 1);
+                cpx db{cs.d[ci * NC * N + j], NC == 2 ? cs.d[ci * NC * N + N + j] : 0.f};
+                cpx mP{msh[pj], NC == 2 ? msh[N + pj] : 0.f};
+                mu = cadd(bp, cmulc(db, mP));
+            }
         }
         __syncthreads();
     }
@@ -181,6 +185,132 @@ __global__ void k_bwd_phaseC(const uint8_t* __restrict__ kstar, const uint16_t* 
             gsel[(size_t)s * L + (t1 - 1 - qq)] = acc;
         }
     }
+}
+
+// Phase C' in recompute mode (pdssm_scan_bwd with h_saved_opt = NULL; include/pdssm.h):
+// the forward states are not kept between the passes.  Each (sequence, chunk) item first
+// replays its chunk forward from the chunk's carry (Alg. 1 Phase C: the
+// carries in chunk_state are the only O(C N) state the forward leaves), h_t -> shared memory
+// (tau x c x N f32), then runs the reverse pass of k_bwd_phaseC reading h_{t-1} from there
+// (h_{s_c - 1} = carry_c, which is h0 at c = 0).  Same gradients, no O(L N) activation memory.
+template <typename T, typename TE, int NC, bool PERDICT>
+__global__ void k_bwd_phaseC_rc(const uint8_t* __restrict__ kstar, const uint16_t* __restrict__ dict_idx,
+                                const uint16_t* __restrict__ pstart, const uint16_t* __restrict__ psrc,
+                                const T* __restrict__ diag, const float* __restrict__ diag_dict,
+                                const T* __restrict__ bias, ChunkStateView cs, const TE* __restrict__ e,
+                                const float* __restrict__ mu_in, T* __restrict__ dbias, T* __restrict__ ddiag,
+                                float* __restrict__ ddiag_f32, float* __restrict__ gsel, int H, int L, int N, int K,
+                                int tau, int C_ch) {
+    extern __shared__ float smem[];
+    const int nw = blockDim.x / 32;
+    float* vsh = smem;                          // [2][NC][N]: forward exchange, then lambda rows
+    float* gpart = smem + 2 * NC * N;           // ring [64][nw] of per-warp partials of g
+    float* hbuf = gpart + 64 * nw;              // [tau][NC][N] recomputed states of this chunk
+    const int item = blockIdx.x;
+    const int s = item / C_ch, c = item % C_ch, h = s % H;
+    const int t0 = c * tau, t1 = min(t0 + tau, L);
+    const int j = threadIdx.x;
+    const int lane = j & 31, w = j >> 5;
+    const bool act = j < N;
+    const size_t ci = (size_t)s * C_ch + c;
+    cpx carry{0.f, 0.f};
+    if (act) {
+        carry.re = cs.carry[ci * NC * N + j];
+        if (NC == 2) carry.im = cs.carry[ci * NC * N + N + j];
+    }
+    // ---- forward replay of the chunk (the scatter as a gather over the preimage plan)
+    {
+        cpx cur = carry;
+        for (int t = t0; t < t1; ++t) {
+            const int buf = (t - t0) & 1;
+            const int k = load_k(kstar, (size_t)s * L + t, K, 0);
+            const size_t off = ((size_t)s * L + t) * NC * N;
+            float* v_b = vsh + buf * NC * N;
+            cpx bj{0.f, 0.f};
+            if (act) {
+                cpx Dj = load_diag<T, NC, PERDICT>(diag, diag_dict, off, h, k, K, N, j);
+                bj = load_plane<T, NC>(bias, off, N, j);
+                cpx v = cmul(Dj, cur);
+                v_b[j] = v.re;
+                if (NC == 2) v_b[N + j] = v.im;
+            }
+            __syncthreads();
+            if (act) {
+                cur = cadd(scatter_gather<NC>(v_b, pstart, psrc, h * K + k, N, j), bj);
+                float* hr = hbuf + (size_t)(t - t0) * NC * N;
+                hr[j] = cur.re;
+                if (NC == 2) hr[N + j] = cur.im;
+            }
+        }
+        __syncthreads();   // the exchange rows are reused by the reverse pass
+    }
+    // ---- reverse pass (k_bwd_phaseC with h_{t-1} from hbuf)
+    cpx lam{0.f, 0.f};
+    if (act) {
+        lam = load_e<TE, NC>(e, ((size_t)s * L + (t1 - 1)) * NC * N, N, j);
+        lam.re += mu_in[ci * NC * N + j];
+        if (NC == 2) lam.im += mu_in[ci * NC * N + N + j];
+    }
+    for (int t = t1 - 1; t >= t0; --t) {
+        const int buf = (t1 - 1 - t) & 1;
+        float* l_b = vsh + buf * NC * N;
+        const size_t off = ((size_t)s * L + t) * NC * N;
+        if (act) {
+            l_b[j] = lam.re;
+            if (NC == 2) l_b[N + j] = lam.im;
+            stact(dbias + off + j, lam.re);
+            if (NC == 2) stact(dbias + off + N + j, lam.im);
+        }
+        __syncthreads();
+        const int q = t1 - 1 - t;
+        if (gsel && q > 0 && (q & 31) == 0 && j < 32) {
+            const int qq = q - 32 + j;
+            float acc = 0.f;
+            for (int ww = 0; ww < nw; ++ww) acc += gpart[(qq & 63) * nw + ww];
+            gsel[(size_t)s * L + (t1 - 1 - qq)] = acc;
+        }
+        float gval = 0.f;
+        if (act) {
+            const int k = load_k(kstar, (size_t)s * L + t, K, 0);
+            const int pj = clamp_idx(__ldg(dict_idx + (size_t)(h * K + k) * N + j), N, 0);
+            cpx lamP{l_b[pj], NC == 2 ? l_b[N + pj] : 0.f};
+            cpx Dj = load_diag<T, NC, PERDICT>(diag, diag_dict, off, h, k, K, N, j);
+            cpx hp = carry;
+            if (t > t0) {
+                const float* hr = hbuf + (size_t)(t - 1 - t0) * NC * N;
+                hp.re = hr[j];
+                hp.im = NC == 2 ? hr[N + j] : 0.f;
+            }
+            cpx dD = cmulc(hp, lamP);
+            if (PERDICT) {
+                ddiag_f32[off + j] = dD.re;
+                if (NC == 2) ddiag_f32[off + N + j] = dD.im;
+            } else {
+                stact(ddiag + off + j, dD.re);
+                if (NC == 2) stact(ddiag + off + N + j, dD.im);
+            }
+            cpx prod = cmul(Dj, hp);
+            gval = lamP.re * prod.re + lamP.im * prod.im;
+            if (t > t0) lam = cadd(load_e<TE, NC>(e, off - (size_t)NC * N, N, j), cmulc(Dj, lamP));
+        }
+        for (int o = 16; o > 0; o >>= 1) gval += __shfl_xor_sync(0xffffffffu, gval, o);
+        if (lane == 0) gpart[(q & 63) * nw + w] = gval;
+    }
+    __syncthreads();
+    if (gsel) {
+        const int nsteps = t1 - t0;
+        const int qlast = ((nsteps - 1) / 32) * 32;
+        for (int qq = qlast + j; qq < nsteps; qq += blockDim.x) {
+            float acc = 0.f;
+            for (int ww = 0; ww < nw; ++ww) acc += gpart[(qq & 63) * nw + ww];
+            gsel[(size_t)s * L + (t1 - 1 - qq)] = acc;
+        }
+    }
+}
+
+// shared memory of k_bwd_phaseC_rc (host and device agree)
+__host__ __device__ inline size_t rc_smem_bytes(int tau, int nc, int N, int threads) {
+    return ((size_t)2 * nc * N + (size_t)64 * (threads / 32) + (size_t)tau * nc * N) * 4;
 }
 
 // e_t = dh_t + conj(C_h)^T dy_t  (readout adjoint, reading R13) into f32 scratch.

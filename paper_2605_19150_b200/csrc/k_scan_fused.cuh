@@ -1459,15 +1459,21 @@ inline int fused_npl(int64_t N) {
     return 0;
 }
 
+// SM count of the current device, cached per device ordinal (a process may drive several GPUs)
 inline int num_sms() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
+    static int cache[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) dev = 0;
+    if (dev >= 64) {
+        int s = 0;
+        return cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && s > 0 ? s : 148;
     }
-    return sms;
+    if (!cache[dev]) {
+        int s = 0;
+        if (cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || s <= 0) s = 148;
+        cache[dev] = s;
+    }
+    return cache[dev];
 }
 
 // persistent grid, one CTA per SM: the same number of CTAs for every head (CTA i serves

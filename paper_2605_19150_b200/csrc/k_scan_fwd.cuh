@@ -26,7 +26,7 @@ struct ChunkStateView {
 //   pstart[e][i] = #{j : P[j] < i} (i = 0..N),  psrc[e][pstart[e][P[j]] + rank_j] = j
 // with rank_j = #{j' < j : P[j'] = P[j]}; e = h*K + k.
 // ---------------------------------------------------------------------------
-__global__ void k_build_plan(const uint16_t* __restrict__ dict_idx, uint16_t* __restrict__ pstart,
+static __global__ void k_build_plan(const uint16_t* __restrict__ dict_idx, uint16_t* __restrict__ pstart,
                              uint16_t* __restrict__ psrc, int N, uint32_t flags) {
     extern __shared__ uint16_t sP[];
     const int e = blockIdx.x;

@@ -9,7 +9,7 @@ namespace pdssm {
 
 // dict_idx[h][k][j] = argmax_i M[h][k][i][j]; one CTA per (h,k), thread per column j
 // (coalesced: for fixed i the warp reads a contiguous row segment).
-__global__ void k_sparsify(const float* __restrict__ M, uint16_t* __restrict__ dict_idx, int N, uint32_t flags) {
+static __global__ void k_sparsify(const float* __restrict__ M, uint16_t* __restrict__ dict_idx, int N, uint32_t flags) {
     const int e = blockIdx.x;
     const float* Me = M + (size_t)e * N * N;
     for (int j = threadIdx.x; j < N; j += blockDim.x) {
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(256) k_project_simt(const T* __restrict__ x, c
 }
 
 // k*[b,h,t] = argmax_k logits (smallest index on ties, NaN never wins); optional P gather.
-__global__ void k_select_argmax(const float* __restrict__ logits, const uint16_t* __restrict__ dict_idx,
+static __global__ void k_select_argmax(const float* __restrict__ logits, const uint16_t* __restrict__ dict_idx,
                                 uint8_t* __restrict__ kstar, uint16_t* __restrict__ P, int64_t rows, int H, int L,
                                 int N, int K) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.y + threadIdx.y;   // row = (b*H + h)*L + t

@@ -11,9 +11,11 @@
 
 namespace pdssm {
 
-// device error word (PDSSM_CHECK_FINITE): bit 0 = out-of-range index, bit 1 = NaN/Inf
-// defined once here: the library is built as a single translation unit (pdssm_api.cu)
-__device__ uint32_t g_err_word = 0;
+// device error word (PDSSM_CHECK_FINITE): bit 0 = out-of-range index, bit 1 = NaN/Inf.
+// Internal linkage: every translation unit of the library has its own word (the units are
+// compiled separately, without relocatable device code); pdssm_check_device reads and
+// clears all of them (api_internal.cuh, PDSSM_DEFINE_ERRWORD).
+static __device__ uint32_t g_err_word = 0;
 
 enum : uint32_t { ERRBIT_RANGE = 1u, ERRBIT_NONFINITE = 2u };
 

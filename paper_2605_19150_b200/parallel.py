@@ -41,9 +41,11 @@ def all_gather_rank_order(t, group=None):
         out = torch.empty((world * t.numel(),), dtype=t.dtype, device=t.device)
         dist.all_gather_into_tensor(out, t.reshape(-1), group=group)
         return out.view(world, *t.shape)
-    parts = [torch.empty_like(t) for _ in range(world)]
-    dist.all_gather(parts, t, group=group)
-    return torch.stack(parts)
+    # gloo (CPU tests, or several ranks sharing one GPU): stage device tensors through the host
+    src = t.cpu() if t.is_cuda else t
+    parts = [torch.empty_like(src) for _ in range(world)]
+    dist.all_gather(parts, src, group=group)
+    return torch.stack(parts).to(t.device)
 
 
 def shard_sequences(t, world, rank):

@@ -73,9 +73,13 @@ def test_null_and_workspace_and_alignment_checks():
     assert P.lib.pdssm_scan_fwd(p, p, p, q, None, None, p, None, p, None, ctypes.byref(d), p, 1 << 30, None) == 4
     # readout without C
     assert P.lib.pdssm_scan_fwd(p, p, p, p, None, None, None, p, p, None, ctypes.byref(d), p, 1 << 30, None) == 1
-    # backward requires h_saved
-    assert P.lib.pdssm_scan_bwd(p, p, p, None, None, p, None, None, None, None, p, p, None, None,
+    # backward requires h_saved or (recompute mode) the bias
+    assert P.lib.pdssm_scan_bwd(p, p, p, None, None, None, p, None, None, None, None, p, p, None, None,
                                 ctypes.byref(d), p, 1 << 30, None) == 1
+    # recompute mode with a chunk too long for shared memory -> ERR_UNSUPPORTED (9)
+    dr = dims(N=128, L=4096, c=2, tau=4096)
+    assert P.lib.pdssm_scan_bwd(p, p, p, None, p, None, p, None, None, None, None, p, p, None, None,
+                                ctypes.byref(dr), p, 1 << 30, None) == 9
     # select requires d_in >= 1
     assert P.lib.pdssm_select(p, p, None, p, None, None, ctypes.byref(d), p, 1 << 30, None) == 2
     ds = dims(d_in=8)

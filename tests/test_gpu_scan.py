@@ -1,7 +1,9 @@
 """GPU parity of the scan path (a4-a9) through the C ABI against the float64
-oracle.  Bars (BASELINE.json north_star): index maps and
+oracle.  Bars (BASELINE.json north_star, R19): index maps and
 integer outputs bit-exact; floats within max|gpu - oracle| / max|oracle|
-<= 1e-4 (fp32) / 2e-2 (bf16) per tensor."""
+<= 1e-4 (fp32) / 2e-2 (bf16), per tensor AND per (b, h) sequence (tests/parity.py).
+bf16 runs: the oracle reads the bf16-rounded inputs, and its backward reads its own states
+rounded to bf16 -- the activation-dtype h_saved the backward consumes (reading R16)."""
 import numpy as np
 import pytest
 
@@ -11,7 +13,7 @@ import synth
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-TOL = {"f32": 1e-4, "bf16": 2e-2}
+from parity import TOL, check, rel
 
 
 @pytest.fixture(scope="module")
@@ -22,9 +24,11 @@ def P():
     return mod
 
 
-def rel(a, b):
-    a = np.asarray(a, dtype=np.complex128 if np.iscomplexobj(a) or np.iscomplexobj(b) else np.float64)
-    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30)) if np.size(b) else 0.0
+def saved_states(h, c, bf16):
+    """The states the backward consumes: the oracle's own h, rounded to bf16 for bf16 runs (R16)."""
+    if not bf16:
+        return h
+    return O.planes_to_complex(synth.round_bf16(O.complex_to_planes(h, c).astype(np.float32)))
 
 
 def to_dev(inp, bf16):
@@ -61,7 +65,7 @@ def run_case(P, B, H, L, N, K, c, tau, bf16=False, per_dict=False, h0=True, seed
     h0z = O.planes_to_complex(inp["h0"]) if h0 else None
     ch = O.scan_chunked(Pm, Dz, bz, f["tau"], h0z)
     e = O.planes_to_complex(inp["dh"])
-    db_r, dD_r, g_r, dh0_r = O.scan_backward(Pm, Dz, ch["h"], e, h0z)
+    db_r, dD_r, g_r, dh0_r = O.scan_backward(Pm, Dz, saved_states(ch["h"], c, bf16), e, h0z)
     return inp, f, (db, dD, g, dh0), ch, (db_r, dD_r, g_r, dh0_r), Pm, Dz
 
 
@@ -107,31 +111,30 @@ def test_scan_fwd_bwd_parity(P, case, bf16, path, monkeypatch):
     use_path(monkeypatch, path, N, tau if tau else 64)
     inp, f, got, ch, ref, Pm, Dz = run_case(P, B, H, L, N, K, c, tau, bf16=bf16, seed=hash(case) % 1000)
     tol = TOL["bf16" if bf16 else "f32"]
-    assert rel(cpx(f["h"]), ch["h"]) <= tol
+    check("h", cpx(f["h"]), ch["h"], tol)
     # integer maps: bit-exact
     assert np.array_equal(f["maps"].cpu().numpy().astype(np.int64), ch["maps"])
     pi, d_bar, beta_bar, carry = P.chunk_state_views(f["chunk_state"], f["dims"])
     assert np.array_equal(pi.cpu().numpy().astype(np.int64), ch["pi_bar"])
-    assert rel(O.planes_to_complex(d_bar.cpu().numpy()), ch["d_bar"]) <= 1e-4
-    assert rel(O.planes_to_complex(beta_bar.cpu().numpy()), ch["beta_bar"]) <= 1e-4
-    assert rel(O.planes_to_complex(carry.cpu().numpy()), ch["carries"]) <= 1e-4
+    check("d_bar", O.planes_to_complex(d_bar.cpu().numpy()), ch["d_bar"], 1e-4)
+    check("beta_bar", O.planes_to_complex(beta_bar.cpu().numpy()), ch["beta_bar"], 1e-4)
+    check("carry", O.planes_to_complex(carry.cpu().numpy()), ch["carries"], 1e-4)
     db, dD, g, dh0 = got
     db_r, dD_r, g_r, dh0_r = ref
-    # the backward consumes the GPU's own (rounded) h; compare against the oracle's
-    assert rel(cpx(db), db_r) <= tol
-    assert rel(cpx(dD), dD_r) <= (tol if not bf16 else 3e-2)
-    assert rel(g.cpu().numpy(), g_r) <= (tol if not bf16 else 3e-2)
-    assert rel(O.planes_to_complex(dh0.cpu().numpy()), dh0_r) <= tol
+    check("db", cpx(db), db_r, tol)
+    check("dD", cpx(dD), dD_r, tol)
+    check("g", g.cpu().numpy(), g_r, tol)
+    check("dh0", O.planes_to_complex(dh0.cpu().numpy()), dh0_r, tol)
 
 
 @pytest.mark.parametrize("N", [16, 64])
 def test_scan_per_dict_and_no_h0(P, N, path, monkeypatch):
     use_path(monkeypatch, path, N, 16)
     inp, f, got, ch, ref, Pm, Dz = run_case(P, 2, 2, 90, N, 5, 2, 16, per_dict=True, h0=False, seed=7)
-    assert rel(cpx(f["h"]), ch["h"]) <= 1e-4
+    check("h", cpx(f["h"]), ch["h"], 1e-4)
     db, dD, g, dh0 = got
     db_r, dD_r, g_r, dh0_r = ref
-    assert rel(cpx(db), db_r) <= 1e-4
+    check("db", cpx(db), db_r, 1e-4)
     # PER_DICT ddiag = sum over steps selecting k of dD_t
     kst = inp["kstar"]
     H, K = 2, 5
@@ -140,8 +143,8 @@ def test_scan_per_dict_and_no_h0(P, N, path, monkeypatch):
         for k in range(K):
             sel = kst[:, h, :] == k
             want[h, k] = dD_r[:, h][sel].sum(axis=0)
-    assert rel(O.planes_to_complex(dD.cpu().numpy()), want) <= 1e-4
-    assert rel(g.cpu().numpy(), g_r) <= 1e-4
+    check("dD_k", O.planes_to_complex(dD.cpu().numpy()), want, 1e-4)
+    check("g", g.cpu().numpy(), g_r, 1e-4)
 
 
 def test_determinism_bitwise(P, path, monkeypatch):
@@ -233,6 +236,8 @@ def test_readout_fused_and_dy_backward(P, rc, path, monkeypatch):
     B, H, K = 2, 2, 4
     inp = synth.scan_inputs(B, H, L, N, K, c, seed=21, h0=True, bf16=bf16)
     Cw = synth.readout_C(H, Pp, N, c, seed=21)
+    if bf16:
+        Cw = synth.round_bf16(Cw)          # the kernels stage C in the activation dtype (R24)
     d = to_dev(inp, bf16)
     Ct = torch.from_numpy(Cw).cuda()
     f = P.scan_fwd(d["kstar"], d["dict_idx"], d["diag"], d["bias"], h0=d["h0"], C=Ct, tau=16, want_y=True)
@@ -250,12 +255,12 @@ def test_readout_fused_and_dy_backward(P, rc, path, monkeypatch):
     h = O.scan_forward(Pm, Dz, bz, h0z)
     Cz = O.planes_to_complex(np.moveaxis(Cw, 1, -2))          # [H][P][N] complex
     y = O.readout(h, Cz)
-    assert rel(f["y"].float().cpu().numpy(), y) <= tol
+    check("y", f["y"].float().cpu().numpy(), y, tol, bh_axes=(0, 2))
     e = O.readout_adjoint(dy, Cz)
-    db_r, dD_r, g_r, dh0_r = O.scan_backward(Pm, Dz, h, e, h0z)
-    assert rel(cpx(db), db_r) <= tol
-    assert rel(cpx(dD), dD_r) <= (tol if not bf16 else 3e-2)
-    assert rel(g.cpu().numpy(), g_r) <= (tol if not bf16 else 3e-2)
+    db_r, dD_r, g_r, dh0_r = O.scan_backward(Pm, Dz, saved_states(h, c, bf16), e, h0z)
+    check("db", cpx(db), db_r, tol)
+    check("dD", cpx(dD), dD_r, tol)
+    check("g", g.cpu().numpy(), g_r, tol)
 
 
 def test_check_finite_reports(P):
@@ -299,19 +304,19 @@ def test_seq_path_parity(P, case, bf16, monkeypatch):
     inp, f, got, ch, ref, Pm, Dz = run_case(P, B, H, L, N, K, c, 0, bf16=bf16, seed=L + N)
     assert f["tau"] == L
     tol = TOL["bf16" if bf16 else "f32"]
-    assert rel(cpx(f["h"]), ch["h"]) <= tol
+    check("h", cpx(f["h"]), ch["h"], tol)
     assert np.array_equal(f["maps"].cpu().numpy().astype(np.int64), ch["maps"])
     pi, d_bar, beta_bar, carry = P.chunk_state_views(f["chunk_state"], f["dims"])
     assert np.array_equal(pi.cpu().numpy().astype(np.int64), ch["pi_bar"])
-    assert rel(O.planes_to_complex(d_bar.cpu().numpy()), ch["d_bar"]) <= 1e-4
-    assert rel(O.planes_to_complex(beta_bar.cpu().numpy()), ch["beta_bar"]) <= 1e-4
-    assert rel(O.planes_to_complex(carry.cpu().numpy()), ch["carries"]) <= 1e-4
+    check("d_bar", O.planes_to_complex(d_bar.cpu().numpy()), ch["d_bar"], 1e-4)
+    check("beta_bar", O.planes_to_complex(beta_bar.cpu().numpy()), ch["beta_bar"], 1e-4)
+    check("carry", O.planes_to_complex(carry.cpu().numpy()), ch["carries"], 1e-4)
     db, dD, g, dh0 = got
     db_r, dD_r, g_r, dh0_r = ref
-    assert rel(cpx(db), db_r) <= tol
-    assert rel(cpx(dD), dD_r) <= (tol if not bf16 else 3e-2)
-    assert rel(g.cpu().numpy(), g_r) <= (tol if not bf16 else 3e-2)
-    assert rel(O.planes_to_complex(dh0.cpu().numpy()), dh0_r) <= tol
+    check("db", cpx(db), db_r, tol)
+    check("dD", cpx(dD), dD_r, tol)
+    check("g", g.cpu().numpy(), g_r, tol)
+    check("dh0", O.planes_to_complex(dh0.cpu().numpy()), dh0_r, tol)
 
 
 @pytest.mark.parametrize("N", [64, 128])
@@ -333,17 +338,17 @@ def test_seq_path_per_dict_and_overflow(P, N, monkeypatch):
     Dz = O.gather_D_per_dict(O.planes_to_complex(inp["diag"]), inp["kstar"])
     bz, h0z, e = (O.planes_to_complex(inp[k]) for k in ("bias", "h0", "dh"))
     h = O.scan_forward(Pm, Dz, bz, h0z)
-    assert rel(cpx(f["h"]), h) <= 1e-4
+    check("h", cpx(f["h"]), h, 1e-4)
     db_r, dD_r, g_r, dh0_r = O.scan_backward(Pm, Dz, h, e, h0z)
-    assert rel(cpx(db), db_r) <= 1e-4
-    assert rel(g.cpu().numpy(), g_r) <= 1e-4
+    check("db", cpx(db), db_r, 1e-4)
+    check("g", g.cpu().numpy(), g_r, 1e-4)
     # PER_DICT dD is reduced per entry: sum over the steps that selected it
     dDk = np.zeros((H, K, N), np.complex128)
     for b in range(B):
         for hh in range(H):
             np.add.at(dDk[hh], inp["kstar"][b, hh], dD_r[b, hh])
-    assert rel(O.planes_to_complex(dD.cpu().numpy()), dDk) <= 1e-4
-    assert rel(O.planes_to_complex(dh0.cpu().numpy()), dh0_r) <= 1e-4
+    check("dD_k", O.planes_to_complex(dD.cpu().numpy()), dDk, 1e-4)
+    check("dh0", O.planes_to_complex(dh0.cpu().numpy()), dh0_r, 1e-4)
 
 
 def test_seq_path_is_default_for_full_batches(P, monkeypatch):
@@ -382,11 +387,12 @@ def test_seq_no_maps_parity(P, case, bf16, monkeypatch):
     Dz, bz, h0z, e = (O.planes_to_complex(inp[k]) for k in ("diag", "bias", "h0", "dh"))
     h = O.scan_forward(Pm, Dz, bz, h0z)
     tol = TOL["bf16" if bf16 else "f32"]
-    assert rel(cpx(f["h"]), h) <= tol
-    db_r, dD_r, g_r, dh0_r = O.scan_backward(Pm, Dz, h, e, h0z)
-    assert rel(cpx(db), db_r) <= tol
-    assert rel(cpx(dD), dD_r) <= (tol if not bf16 else 3e-2)
-    assert rel(g.cpu().numpy(), g_r) <= (tol if not bf16 else 3e-2)
+    check("h", cpx(f["h"]), h, tol)
+    db_r, dD_r, g_r, dh0_r = O.scan_backward(Pm, Dz, saved_states(h, c, bf16), e, h0z)
+    check("db", cpx(db), db_r, tol)
+    check("dD", cpx(dD), dD_r, tol)
+    check("g", g.cpu().numpy(), g_r, tol)
+    check("dh0", O.planes_to_complex(dh0.cpu().numpy()), dh0_r, tol)
     # run-to-run bitwise determinism
     f2 = P.scan_fwd(d["kstar"], d["dict_idx"], d["diag"], d["bias"], h0=d["h0"])
     assert torch.equal(f["h"], f2["h"])
@@ -404,4 +410,4 @@ def test_seq_no_maps_per_dict_and_overflow(P, monkeypatch):
     Pm = O.gather_P(inp["dict_idx"], inp["kstar"])
     Dz = O.gather_D_per_dict(O.planes_to_complex(inp["diag"]), inp["kstar"])
     h = O.scan_forward(Pm, Dz, O.planes_to_complex(inp["bias"]), O.planes_to_complex(inp["h0"]))
-    assert rel(cpx(f["h"]), h) <= 1e-4
+    check("h", cpx(f["h"]), h, 1e-4)

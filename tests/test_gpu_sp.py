@@ -6,6 +6,7 @@ import pytest
 
 import oracle as O
 import synth
+from parity import check
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -17,10 +18,6 @@ def P():
         pytest.skip("no GPU")
     import paper_2605_19150_b200 as mod
     return mod
-
-
-def rel(a, b):
-    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30))
 
 
 @pytest.fixture(params=["auto", "generic"])
@@ -55,10 +52,10 @@ def test_sp_virtual_ranks(P, G, c, path):
         carry, m = P.compose_carry(gathered, g, G, dims_g[g], h0=dev["h0"])
         if s > 0:
             assert np.array_equal(m.cpu().numpy().astype(np.int64), Pi[:, :, s - 1])
-            assert rel(O.planes_to_complex(carry.cpu().numpy()), h_ref[:, :, s - 1]) <= 1e-4
+            check("sp_1", O.planes_to_complex(carry.cpu().numpy()), h_ref[:, :, s - 1], 1e-4)
         f = P.scan_fwd(seg(dev["kstar"], s, e), di, seg(dev["diag"], s, e), seg(dev["bias"], s, e), h0=carry, tau=tau)
         fwd_out.append((f, carry))
-        assert rel(O.planes_to_complex(f["h"].cpu().numpy()), h_ref[:, :, s:e]) <= 1e-4
+        check("sp_2", O.planes_to_complex(f["h"].cpu().numpy()), h_ref[:, :, s:e], 1e-4)
     # backward: per-rank beta' summaries, gathered, composed from the right
     betas = []
     for g, (s, e) in enumerate(bounds):
@@ -71,8 +68,8 @@ def test_sp_virtual_ranks(P, G, c, path):
         lam_in = P.compose_lambda(gathered, beta_all, g, G, dims_g[g])
         db, dD, gs, dh0 = P.scan_bwd(seg(dev["kstar"], s, e), di, seg(dev["diag"], s, e), f["h"], f["chunk_state"],
                                      dims_g[g], dh=seg(dev["dh"], s, e), h0=carry, lam_in=lam_in)
-        assert rel(O.planes_to_complex(db.cpu().numpy()), db_ref[:, :, s:e]) <= 1e-4
-        assert rel(O.planes_to_complex(dD.cpu().numpy()), dD_ref[:, :, s:e]) <= 1e-4
-        assert rel(gs.cpu().numpy(), g_ref[:, :, s:e]) <= 1e-4
+        check("sp_3", O.planes_to_complex(db.cpu().numpy()), db_ref[:, :, s:e], 1e-4)
+        check("sp_4", O.planes_to_complex(dD.cpu().numpy()), dD_ref[:, :, s:e], 1e-4)
+        check("sp_5", gs.cpu().numpy(), g_ref[:, :, s:e], 1e-4)
         if g == 0:
-            assert rel(O.planes_to_complex(dh0.cpu().numpy()), dh0_ref) <= 1e-4
+            check("sp_6", O.planes_to_complex(dh0.cpu().numpy()), dh0_ref, 1e-4)

@@ -2,13 +2,15 @@
 against the float64 oracle (oracle.selector_grad / dictionary_outer / dictionary_grad, pinned by
 finite differences in test_oracle_pins.py).  The oracle side runs its own forward and backward
 scans, so no GPU value enters the reference.  Bars (R19): max|gpu - oracle| /
-max|oracle| <= 1e-4 (fp32) per tensor; bf16 activations 3e-2 (G multiplies two bf16-rounded
-operands, as dD and g do)."""
+max|oracle| <= 1e-4 (fp32) and 2e-2 (bf16) per tensor; for bf16 activations the oracle's
+dictionary gradient reads its own lambda and h rounded to bf16, the activation-dtype tensors
+the GPU kernel consumes (reading R16)."""
 import numpy as np
 import pytest
 
 import oracle as O
 import synth
+from parity import check
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -68,6 +70,9 @@ def run_dict_case(P, B, H, L, N, K, c, T, bf16=False, per_dict=False, unused_k=N
     bz, h0z, e = (O.planes_to_complex(inp[k]) for k in ("bias", "h0", "dh"))
     h = O.scan_forward(Pm, Dz, bz, h0z)
     lam = O.scan_backward(Pm, Dz, h, e, h0z)[0]
+    if bf16:   # the kernel reads lambda (dbias) and h_saved in the activation dtype
+        rnd = lambda z: O.planes_to_complex(synth.round_bf16(O.complex_to_planes(z, c).astype(np.float32)))
+        lam, h = rnd(lam), rnd(h)
     G_ref = O.dictionary_outer(inp["kstar"], lam, Dz, h, K, h0=h0z)
     dM_ref = O.dictionary_grad(M.astype(np.float64), G_ref, T)
     return dM.cpu().numpy(), G.cpu().numpy(), dM_ref, G_ref, (Mt, d, f, db)
@@ -98,8 +103,8 @@ def test_dict_grad_parity(P, case, T):
 def test_dict_grad_bf16_and_unused_entry(P, N):
     B, H, L, K, c = 2, 2, 180, 8, 2
     dM, G, dM_ref, G_ref, _ = run_dict_case(P, B, H, L, N, K, c, 0.5, bf16=True, unused_k=3, seed=9)
-    assert rel(G, G_ref) <= 3e-2
-    assert rel(dM, dM_ref) <= 3e-2
+    assert rel(G, G_ref) <= 2e-2
+    assert rel(dM, dM_ref) <= 2e-2
     assert np.all(G[:, 3] == 0.0) and np.all(dM[:, 3] == 0.0)   # no step selected entry 3
 
 
@@ -163,6 +168,7 @@ def test_layer_fwd_parity(P, c, N, bf16):
     C = synth.readout_C(H, Pp, N, c, seed=N)
     if bf16:
         Bw = synth.round_bf16(Bw)
+        C = synth.round_bf16(C)          # the readout stages C in the activation dtype (R24)
     dt = torch.bfloat16 if bf16 else torch.float32
     cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
     r = P.layer_fwd(cu(x).to(dt), cu(S).to(dt), cu(di).to(torch.int16), cu(Dk), cu(Bw).to(dt), C=cu(C), per_dict=True)
@@ -175,10 +181,10 @@ def test_layer_fwd_parity(P, c, N, bf16):
     h = O.scan_forward(Pm, Dz, O.project_b(x.astype(np.float64), Bc))
     Cc = C[:, 0].astype(np.float64) + (1j * C[:, 1].astype(np.float64) if c == 2 else 0)
     y = O.readout(h, Cc)
-    tol = 3e-2 if bf16 else 1e-4
+    tol = 2e-2 if bf16 else 1e-4
     hg = O.planes_to_complex(r["h"].float().cpu().numpy())
-    assert float(np.max(np.abs(hg - h)) / np.max(np.abs(h))) <= tol
-    assert rel(r["y"].float().cpu().numpy(), y) <= tol
+    check("layer_h", hg, h, tol)
+    check("layer_y", r["y"].float().cpu().numpy(), y, tol, bh_axes=(0, 2))
 
 
 @pytest.mark.parametrize("K", [100, 256])

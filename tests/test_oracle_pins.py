@@ -4,6 +4,7 @@ definition, closed forms, FSA emulation vs independent interpreters (Prop. 1),
 S_5 group products via sympy, central finite differences, brute-force argmax.
 All CPU (`-m "not gpu"`)."""
 import itertools
+import math
 
 import numpy as np
 import pytest
@@ -566,6 +567,32 @@ def test_diag_generator_special_cases():
     Dn = O.diag_generator(-x, np.zeros_like(Wm), Wp, np.zeros((H, N)))
     Dp = O.diag_generator(x, np.zeros_like(Wm), Wp, np.zeros((H, N)))
     assert np.allclose(Dn, np.conj(Dp))
+
+
+def test_diag_generator_one_hot_tokens_pick_a_weight_column():
+    """A one-hot token x_t = e_m reduces the generator to column m of the weights:
+    D[b,h,t,n] = sigmoid(W_mag[h,n,m] + bias[h,n]) * exp(i W_phase[h,n,m]) (SPEC.md:367 form,
+    PAPER.md:133, :211; reading R30).  Chosen phase weights pin the phase coefficient to exactly 1
+    (pi/2 -> i, pi -> -1, 1 rad -> cos 1 + i sin 1) and the contraction index to d."""
+    H, N, d = 2, 3, 4
+    L = d
+    x = np.eye(d)[None]                                   # token t is e_t (B = 1, L = d)
+    Wm = np.arange(H * N * d, dtype=np.float64).reshape(H, N, d) / 10.0 - 1.0
+    Wp = np.zeros((H, N, d))
+    Wp[0, 0, :] = [np.pi / 2, np.pi, 1.0, -np.pi / 3]
+    Wp[1, 2, :] = [0.25, -0.5, 2.0, 3.0]
+    beta = np.array([[0.5, -0.25, 0.0], [1.0, 0.0, -2.0]])
+    D = O.diag_generator(x, Wm, Wp, beta)
+    for h in range(H):
+        for n in range(N):
+            for t in range(L):
+                mag = 1.0 / (1.0 + math.exp(-(Wm[h, n, t] + beta[h, n])))
+                want = complex(mag * math.cos(Wp[h, n, t]), mag * math.sin(Wp[h, n, t]))
+                assert abs(D[0, h, t, n] - want) <= 1e-15
+    mag00 = 1.0 / (1.0 + math.exp(-(Wm[0, 0, 0] + beta[0, 0])))
+    assert abs(D[0, 0, 0, 0] - 1j * mag00) <= 1e-15          # phase pi/2: purely imaginary
+    mag01 = 1.0 / (1.0 + math.exp(-(Wm[0, 0, 1] + beta[0, 0])))
+    assert abs(D[0, 0, 1, 0] + mag01) <= 1e-15               # phase pi: negative real
 
 
 # ---------------------------------------------------------------------------
