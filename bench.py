@@ -2,15 +2,27 @@
 """Benchmark of the Flash PD-SSM fwd+bwd scan on B200 (BASELINE.json metric:
 "PD-SSM fwd+bwd scan tokens/s at L=2048, d=1024; HBM GB/s vs peak; 1/2/4/8 GPU").
 
-A step = pdssm_scan_fwd (h_t + chunk_state) followed by pdssm_scan_bwd (db, dD, g)
-over one batch of the headline workload (config 2: B=16, L=2048, H=8, N=128,
-K=32, complex fp32, per-step D), inputs resident in HBM (>= 1.3 GB per step, larger
-than the 126 MB L2, so no flush is needed).  Multi-GPU: one process per GPU,
-batch x head sharding with no data-path collective -- every rank runs its own
-full batch (weak scaling); value = all ranks' tokens / max-over-ranks time.
+A step = pdssm_scan_fwd (h_t + chunk_state) followed by pdssm_scan_bwd (db, dD, g) over one
+batch of the chosen workload, inputs resident in HBM (every config moves >= 0.5 GB per step,
+more than the 126 MB L2, so no flush is needed).  Workloads (BASELINE.json configs):
 
---impl reference times the float64 CPU oracle (oracle/, the only reference this
-paper-only tier has) on a bounded sample of the same workload.
+  --config 2 (default, the headline): B=16 per GPU, L=2048, H=8, N=128 (d = 1024), K=32, complex,
+             PER_STEP D; batch x head, weak scaling: the global batch is 16*G rows generated once
+             (row-wise seeded streams) and rank r takes rows [16r, 16r+16) -- no collective.
+  --config 4: hybrid-LLM layer, B=32, H=32, L=4096, N=64, K=48, real, bf16; batch x head, STRONG
+             scaling: the 1024 (b, h) sequences are split over the G ranks.
+  --config 3: long time series, B=4, H=8, L=17984, N=128, K=32, real fp32, temporally persistent
+             k*; sequence parallel (strong): rank g owns steps [gL/G, (g+1)L/G) of every sequence,
+             one all-gather of segment summaries per direction over NCCL.
+  --config 5: S_5 word problem, B=4, H=4, L=65536, N=64, K=16, PER_DICT D = 1, b = 0,
+             h0 = arange; sequence parallel (strong).
+  --dtype f32|bf16, --mode bh|sp override the config's natural choice; --recompute runs the
+  backward in recompute mode (no saved states; chunk 64).
+
+Multi-GPU: one process per GPU (torchrun), barrier + synchronize around exactly K timed steps,
+max over ranks; value = all ranks' tokens / that time.  --impl reference times the float64 CPU
+oracle (oracle/, the only reference this paper-only tier has) on a bounded sample of the same
+workload.
 """
 from __future__ import annotations
 
@@ -29,6 +41,18 @@ sys.path.insert(0, ROOT)
 METRIC = "PD-SSM fwd+bwd scan tokens/s at L=2048,d=1024; HBM GB/s vs peak; 1/2/4/8 GPU"
 UNIT = "tokens/s"
 
+# name, B, H, L, N, K, c, dtype, mode, scaling, extras
+BENCH_CONFIGS = {
+    2: dict(workload="config2: paper Fig.1 shape, fwd+bwd scan", B=16, H=8, L=2048, N=128, K=32, c=2,
+            dtype="f32", mode="bh", scaling="weak", seed=2000),
+    3: dict(workload="config3: long time series (EigenWorms-like), fwd+bwd scan", B=4, H=8, L=17984, N=128, K=32,
+            c=1, dtype="f32", mode="sp", scaling="strong", seed=3000, sticky=0.9),
+    4: dict(workload="config4: hybrid-LLM layer, fwd+bwd scan", B=32, H=32, L=4096, N=64, K=48, c=1,
+            dtype="bf16", mode="bh", scaling="strong", seed=4000),
+    5: dict(workload="config5: S_5 word problem stress, fwd+bwd scan", B=4, H=4, L=65536, N=64, K=16, c=1,
+            dtype="f32", mode="sp", scaling="strong", seed=5000, s5=True),
+}
+
 
 def parse():
     ap = argparse.ArgumentParser()
@@ -36,15 +60,16 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
-    ap.add_argument("--complex", type=int, default=2, choices=[1, 2])
-    ap.add_argument("--heads", type=int, default=8)
-    ap.add_argument("--state", type=int, default=128)
+    ap.add_argument("--config", type=int, default=2, choices=sorted(BENCH_CONFIGS))
+    ap.add_argument("--dtype", default=None, choices=["f32", "bf16"])
+    ap.add_argument("--mode", default=None, choices=["bh", "sp"])
+    ap.add_argument("--recompute", action="store_true", help="backward without saved states (chunk 64)")
     ap.add_argument("--tau", type=int, default=0)
+    ap.add_argument("--seeds", type=int, default=3, help="seeds 0..n-1 timed (value from seed 0; min/max reported)")
+    ap.add_argument("--stat-steps", type=int, default=50, help="extra steps for the per-step median")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-layer", action="store_true")
-    ap.add_argument("--seed", type=int, default=2000)
     return ap.parse_args()
 
 
@@ -61,20 +86,21 @@ def peak_tflops(dtype):
     """Dense tensor peak for the layer GEMMs: measured cuBLAS bf16 burst; fp32 runs use the
     3xTF32 split (3 tf32 MMAs per product, tf32 = 1/2 bf16 nominal) -> bf16/6 useful."""
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    bf = 1645.9
+    bf = 1590.0
     if os.path.exists(p):
         with open(p) as f:
             bf = float(json.load(f).get("bf16_tflops", bf))
     return bf if dtype == "bf16" else bf / 6.0
 
 
-def traffic_of(kernel):
+def traffic_of(kernel, config):
     """dram read+write bytes per launch of `kernel` from the committed ncu --set full capture."""
     p = os.path.join(ROOT, "profiles", "traffic_latest.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
-        return json.load(f).get(kernel)
+        j = json.load(f)
+    return j.get(f"config{config}:{kernel}", j.get(kernel) if config == 2 else None)
 
 
 def count_launches(fn):
@@ -89,10 +115,12 @@ def count_launches(fn):
     return len(names), sorted(set(n.split("(")[0][:80] for n in names))
 
 
-def algo_bytes_per_seq_step(N, c, p):
+def algo_bytes_per_seq_step(N, c, p, per_dict=False, recompute=False):
     """SURVEY §8(d): fwd reads D, b, k*, writes h -> 3cNp + 1;
-    bwd reads dh, D, h_{t-1}, k*, writes db, dD, g -> 5cNp + 5."""
-    return 3 * c * N * p + 1, 5 * c * N * p + 5
+    bwd reads dh, D, h_{t-1}, k*, writes db, dD, g -> 5cNp + 5.  PER_DICT drops the D stream
+    (2cNp + 1, 4cNp + 5).  Recompute mode reads b instead of h_{t-1} (same count)."""
+    d = 0 if per_dict else 1
+    return (2 + d) * c * N * p + 1, (4 + d) * c * N * p + 5
 
 
 class Clocks:
@@ -144,40 +172,87 @@ class Clocks:
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_oracle_sample(L, N, K, c, seed, seqs=1):
-    """Oracle (O5 + O8, float64 NumPy) on `seqs` (b,h) sequences of the workload."""
+# ---------------------------------------------------------------- CPU oracle baseline
+def _cpu_info():
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except AttributeError:
+        cores = os.cpu_count() or 1
+    return model, cores
+
+
+def _oracle_task(args):
+    """Oracle O5 + O8 (float64 NumPy, sequential; one thread) on the (b, h) sequences `rows` x all
+    heads of the workload's global inputs; returns (compute start, compute end) wall times."""
+    os.environ["OMP_NUM_THREADS"] = "1"
+    cfg, seed, b, L = args
     import oracle as O
     import synth
-    inp = synth.scan_inputs(1, seqs, L, N, K, c, seed=seed, dh=True)
+    H, N, K, c = cfg["H"], cfg["N"], cfg["K"], cfg["c"]
+    if cfg.get("s5"):
+        dict5, _, _ = synth.s5_dictionary(N, K, seed=5000)
+        inp = synth.scan_inputs_rows(cfg["B"], H, L, N, K, c, seed, rows=(b, b + 1), dh=True, per_dict=True)
+        inp["dict_idx"] = np.tile(dict5[None], (H, 1, 1))
+        Dz = np.ones((1, H, L, N), np.complex128)
+        bz = np.zeros((1, H, L, N), np.complex128)
+    else:
+        inp = synth.scan_inputs_rows(cfg["B"], H, L, N, K, c, seed, rows=(b, b + 1), dh=True,
+                                     sticky=cfg.get("sticky", 0.0))
+        Dz, bz = (O.planes_to_complex(inp[k]) for k in ("diag", "bias"))
     Pm = O.gather_P(inp["dict_idx"], inp["kstar"])
-    Dz, bz, ez = (O.planes_to_complex(inp[k]) for k in ("diag", "bias", "dh"))
-    t0 = time.perf_counter()
+    ez = O.planes_to_complex(inp["dh"])
+    t0 = time.time()
     h = O.scan_forward(Pm, Dz, bz)
     O.scan_backward(Pm, Dz, h, ez)
-    return time.perf_counter() - t0
+    return t0, time.time()
+
+
+def cpu_oracle_baseline(cfg, budget_s=8.0):
+    """The oracle as it stands on the host cores, on the workload's own shape (full L, its global
+    inputs): batch rows (each = H head sequences) on 1 core in turn, and on all affinity cores as a
+    process pool (one row per task).  Rows are added until ~budget_s of single-core work; the all-core
+    leg runs up to cores x that many rows.  tokens = rows x L; throughput = tokens / compute wall span."""
+    import multiprocessing as mp
+    model, cores = _cpu_info()
+    L = cfg["L"]
+    t0, t1 = _oracle_task((cfg, cfg["seed"], 0, L))
+    per_row = t1 - t0
+    n1 = int(max(1, min(cfg["B"], budget_s // max(per_row, 1e-3))))
+    spans = [_oracle_task((cfg, cfg["seed"], b, L)) for b in range(n1)]
+    one = n1 * L / sum(e - s for s, e in spans)
+    nall = int(max(1, min(cfg["B"] * 8, cores * max(1, budget_s // max(per_row, 1e-3)))))
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        spans = pool.map(_oracle_task, [(cfg, cfg["seed"] + 1 + b // cfg["B"], b % cfg["B"], L) for b in range(nall)])
+    wall = max(e for _, e in spans) - min(s for s, _ in spans)
+    allc = nall * L / wall
+    return {"value": allc, "unit": UNIT, "cores": cores, "kind": "oracle", "value_1core": one, "cpu_model": model,
+            "sample": f"{cfg['workload'].split(':')[0]} at full shape (L={L}, H={cfg['H']}, N={cfg['N']}, K={cfg['K']}, "
+                      f"c={cfg['c']}): 1 core {n1} batch rows in turn, all {cores} affinity cores {nall} rows as a "
+                      f"process pool; fwd O5 + bwd O8, float64 NumPy, one thread per process; tokens = rows x L"}
 
 
 def run_reference(a):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    B, L, H, N, K, c = 16, 2048, a.heads, a.state, 32, a.complex
-    Lh = 512                                    # bounded sample: one (b,h) sequence, 512 steps
-    cpu_oracle_sample(64, N, K, c, a.seed)     # warm numpy
-    for _ in range(a.warmup):
-        pass
-    times = [cpu_oracle_sample(Lh, N, K, c, a.seed + i) for i in range(a.steps)]
-    t = float(np.sum(times))
-    tokens = a.steps * Lh / H                   # one head of Lh tokens = Lh/H token-equivalents
-    v = tokens / t
-    cores = 1
+    cfg = BENCH_CONFIGS[a.config]
+    cb = cpu_oracle_baseline(cfg)
+    v = cb["value"]
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": 1e3 * t / a.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": a.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": cfg["scaling"],
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "config2 fig1-shape scan fwd+bwd (oracle sample)", "batch": B, "seq_len": L,
-                       "heads": H, "state": N, "dict": K, "complex": c == 2},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": f"1 (b,h) sequence x {Lh} steps per step, N={N}, complex={c == 2}"},
+            "config": {"workload": cfg["workload"] + " (oracle sample)", "batch": cfg["B"], "seq_len": cfg["L"],
+                       "heads": cfg["H"], "state": cfg["N"], "dict": cfg["K"], "complex": cfg["c"] == 2},
+            "cpu_baseline": cb,
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -295,6 +370,127 @@ def surrogate_kernels(P, torch, dev, d, fo, bo, dims, dtype, B, L, H, N, K, c, p
                             "algo_bytes": sbytes}}
 
 
+def make_inputs(cfg, a, seed, world, rank, bf16):
+    """Host inputs of this rank: generated globally (row-wise streams), then sliced.
+    Returns (inp dict of numpy arrays, B_local, L_local, description of the shard)."""
+    import synth
+    from paper_2605_19150_b200.parallel import shard_range
+    B, H, L, N, K, c = cfg["B"], cfg["H"], cfg["L"], cfg["N"], cfg["K"], cfg["c"]
+    mode = a.mode or cfg["mode"]
+    if mode == "bh" and cfg["scaling"] == "weak":
+        Bg, rows, t0, t1 = B * world, (B * rank, B * rank + B), 0, L
+        shard = f"dp{world}: rows [{rows[0]}, {rows[1]}) of a global batch of {Bg} (weak scaling, no collective)"
+    elif mode == "bh":
+        Bg, rows, t0, t1 = B, shard_range(B, world, rank), 0, L
+        shard = f"dp{world}: batch rows [{rows[0]}, {rows[1]}) x {H} heads of {B * H} sequences (strong, no collective)"
+    else:
+        Bg, rows = B, (0, B)
+        t0, t1 = shard_range(L, world, rank)
+        shard = f"sp{world}: steps [{t0}, {t1}) of L = {L} (strong; one all-gather of segment summaries per direction)"
+    if cfg.get("s5"):
+        dict5, _, _ = synth.s5_dictionary(N, K, seed=5000)
+        inp = synth.scan_inputs_rows(Bg, H, L, N, K, c, seed, rows=rows, dh=True, per_dict=True)
+        inp["dict_idx"] = np.tile(dict5[None], (H, 1, 1))
+        inp["diag"] = np.ones((H, K, c, N), np.float32)
+        inp["bias"] = np.zeros_like(inp["bias"])
+        inp["h0"] = np.tile(np.arange(N, dtype=np.float32).reshape(1, 1, 1, N), (rows[1] - rows[0], H, c, 1))
+    else:
+        inp = synth.scan_inputs_rows(Bg, H, L, N, K, c, seed, rows=rows, dh=True, sticky=cfg.get("sticky", 0.0),
+                                     bf16=bf16)
+    if (t0, t1) != (0, L):
+        for k in ("kstar", "diag", "bias", "dh"):
+            if k in inp and not (k == "diag" and cfg.get("s5")):
+                inp[k] = np.ascontiguousarray(inp[k][:, :, t0:t1])
+    return inp, rows[1] - rows[0], t1 - t0, shard, Bg
+
+
+class Step:
+    """One fwd+bwd scan step through the public API on this rank's shard."""
+
+    def __init__(self, P, torch, dev, cfg, a, inp, bf16, world):
+        self.P, self.torch = P, torch
+        adt = torch.bfloat16 if bf16 else torch.float32
+        self.pd = bool(cfg.get("s5"))
+        self.host = {k: torch.from_numpy(np.ascontiguousarray(v)) for k, v in inp.items()}
+        d = {k: v.to(dev) for k, v in self.host.items()}
+        d["dict_idx"] = d["dict_idx"].to(torch.int16)
+        for k in ("diag", "bias", "dh"):
+            if not (k == "diag" and self.pd):
+                d[k] = d[k].to(adt)
+        self.d = d
+        self.adt = adt
+        self.world = world
+        self.mode = a.mode or cfg["mode"]
+        self.recompute = a.recompute
+        self.tau = a.tau if a.tau else (64 if a.recompute else 0)
+        self.h0 = d.get("h0")
+        f = P.scan_fwd(d["kstar"], d["dict_idx"], d["diag"], d["bias"], h0=self.h0, tau=self.tau, per_dict=self.pd)
+        self.dims = f["dims"]
+        self.tau_eff = int(f["tau"])
+        self.fo = {"h": f["h"], "chunk_state": f["chunk_state"],
+                   "ws": torch.empty(P.workspace_bytes(self.dims, P.OP_FWD), dtype=torch.uint8, device=dev)}
+        self.bo = {"ws": torch.empty(P.workspace_bytes(self.dims, P.OP_BWD), dtype=torch.uint8, device=dev),
+                   "dbias": torch.empty_like(f["h"]),
+                   "ddiag": torch.empty(d["diag"].shape, dtype=torch.float32 if self.pd else adt, device=dev),
+                   "gsel": torch.empty(d["kstar"].shape, dtype=torch.float32, device=dev)}
+        self.sp = None
+        if self.mode == "sp" and world > 1:
+            from paper_2605_19150_b200.parallel import CudaOps, SequenceParallelScan
+            self.sp = SequenceParallelScan(CudaOps(cfg["N"], cfg["K"], cfg["c"], tau=self.tau, per_dict=self.pd))
+
+    def fwd(self):
+        d = self.d
+        if self.sp is not None:
+            out, ctx = self.sp.forward(d["kstar"], d["dict_idx"], d["diag"], d["bias"], h0=self.h0)
+            return (out, ctx)
+        return self.P.scan_fwd(d["kstar"], d["dict_idx"], d["diag"], d["bias"], h0=self.h0, tau=self.tau,
+                               per_dict=self.pd, out=self.fo)
+
+    def bwd(self, fr):
+        d = self.d
+        if self.sp is not None:
+            out, ctx = fr
+            return self.sp.backward(d["kstar"], d["dict_idx"], d["diag"], out, ctx, d["dh"])
+        hs = None if self.recompute else fr["h"]
+        return self.P.scan_bwd(d["kstar"], d["dict_idx"], d["diag"], hs, fr["chunk_state"], self.dims, dh=d["dh"],
+                               h0=self.h0, want_dh0=False, out=self.bo, bias=d["bias"] if self.recompute else None)
+
+    def step(self):
+        return self.bwd(self.fwd())
+
+
+def timed(torch, dist, st, stream, steps, world, dev, per_step=True):
+    """Exactly `steps` steps between a barrier + synchronize on both sides; CUDA events on the
+    launching stream; returns (elapsed s max over ranks, [fwd ms], [bwd ms])."""
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)] if per_step else []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for i in range(steps):
+        if per_step:
+            ev[i][0].record(stream)
+            fr = st.fwd()
+            ev[i][1].record(stream)
+            st.bwd(fr)
+            ev[i][2].record(stream)
+        else:
+            st.step()
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    el = t_start.elapsed_time(t_end) / 1e3
+    if world > 1:
+        tt = torch.tensor([el], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        el = float(tt.item())
+    fw = [e[0].elapsed_time(e[1]) for e in ev]
+    bw = [e[1].elapsed_time(e[2]) for e in ev]
+    return el, fw, bw
+
+
 def main():
     a = parse()
     if a.impl == "reference":
@@ -304,7 +500,6 @@ def main():
     import torch.distributed as dist
 
     import paper_2605_19150_b200 as P
-    import synth
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -313,110 +508,87 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-
-    B, L, H, N, K, c = 16, 2048, a.heads, a.state, 32, a.complex
-    bf16 = a.dtype == "bf16"
+    cfg = BENCH_CONFIGS[a.config]
+    dtype = a.dtype or cfg["dtype"]
+    bf16 = dtype == "bf16"
     p = 2 if bf16 else 4
-    adt = torch.bfloat16 if bf16 else torch.float32
-    # global inputs are generated per rank-shard (batch x head sharding: rank r owns batch block r)
-    inp = synth.scan_inputs(B, H, L, N, K, c, seed=a.seed + 17 * rank, dh=True, bf16=bf16)
-    host = {k: torch.from_numpy(v) for k, v in inp.items()}
-    d = {k: v.to(dev) for k, v in host.items()}
-    d["dict_idx"] = d["dict_idx"].to(torch.int16)
-    for k in ("diag", "bias", "dh"):
-        d[k] = d[k].to(adt)
-    # outputs / workspaces preallocated once (calls are allocation-free)
-    f = P.scan_fwd(d["kstar"], d["dict_idx"], d["diag"], d["bias"], tau=a.tau)
-    dims = f["dims"]
-    fo = {"h": f["h"], "chunk_state": f["chunk_state"],
-          "ws": torch.empty(P.workspace_bytes(dims, P.OP_FWD), dtype=torch.uint8, device=dev)}
-    bo = {"ws": torch.empty(P.workspace_bytes(dims, P.OP_BWD), dtype=torch.uint8, device=dev),
-          "dbias": torch.empty_like(f["h"]), "ddiag": torch.empty_like(f["h"]),
-          "gsel": torch.empty((B, H, L), dtype=torch.float32, device=dev)}
+    B, H, L, N, K, c = cfg["B"], cfg["H"], cfg["L"], cfg["N"], cfg["K"], cfg["c"]
+    mode = a.mode or cfg["mode"]
+    scaling = cfg["scaling"] if mode == cfg["mode"] else ("strong" if mode == "sp" else "weak")
     stream = torch.cuda.current_stream()
 
-    def step_fwd():
-        return P.scan_fwd(d["kstar"], d["dict_idx"], d["diag"], d["bias"], tau=a.tau, out=fo)
-
-    def step_bwd(fr):
-        return P.scan_bwd(d["kstar"], d["dict_idx"], d["diag"], fr["h"], fr["chunk_state"], dims, dh=d["dh"],
-                          want_dh0=False, out=bo)
-
-    for _ in range(max(a.warmup, 3)):
-        step_bwd(step_fwd())
-    torch.cuda.synchronize()
+    seed_vals = []
+    main_res = None
+    for si in range(max(1, a.seeds)):
+        inp, B_loc, L_loc, shard, Bg = make_inputs(cfg, a, cfg["seed"] + si, world, rank, bf16)
+        st = Step(P, torch, dev, cfg, a, inp, bf16, world)
+        for _ in range(max(a.warmup, 3)):
+            st.step()
+        torch.cuda.synchronize()
+        if si == 0:   # nvidia-smi sampling spans the timed region of the reported value
+            clk = Clocks(local)
+            clk.start()
+            time.sleep(0.3)
+        el, fw, bw = timed(torch, dist, st, stream, a.steps, world, dev)
+        if si == 0:
+            timed(torch, dist, st, stream, max(a.steps, 200), world, dev, per_step=False)
+            clocks = clk.stop()
+        tokens_all = (Bg if cfg["scaling"] == "weak" and mode == "bh" else B) * L   # whole-job tokens per step
+        v = tokens_all * a.steps / el
+        seed_vals.append(v)
+        if si == 0:
+            main_res = (st, inp, B_loc, L_loc, shard, Bg, el, fw, bw, tokens_all)
+        else:
+            del st
+    st, inp, B_loc, L_loc, shard, Bg, elapsed, fw, bw, tokens_all = main_res
+    value = seed_vals[0]
     try:
-        launches_per_step, kernel_names = count_launches(lambda: step_bwd(step_fwd()))
-    except Exception as ex:   # profiler unavailable: the fused path's documented count
-        launches_per_step, kernel_names = 4, [f"profiler failed: {ex}"[:80]]
+        launches_per_step, kernel_names = count_launches(st.step)
+    except Exception as ex:
+        launches_per_step, kernel_names = None, [f"profiler failed: {ex}"[:80]]
+    # per-step median over --stat-steps further steps (seed 0)
+    _, sfw, sbw = timed(torch, dist, st, stream, max(a.stat_steps, 1), world, dev)
+    step_ms = [f_ + b_ for f_, b_ in zip(sfw, sbw)]
+    fwd_ms, bwd_ms = float(np.median(sfw)), float(np.median(sbw))
 
-    # ---- timed region: K steps, per-call CUDA events on the launching stream
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(a.steps)]
-    clk = Clocks(local)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    clk.start()
-    time.sleep(0.3)
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
-    t_start.record(stream)
-    for i in range(a.steps):
-        ev[i][0].record(stream)
-        fr = step_fwd()
-        ev[i][1].record(stream)
-        step_bwd(fr)
-        ev[i][2].record(stream)
-    t_end.record(stream)
-    torch.cuda.synchronize()
-    clocks = clk.stop()
-    if world > 1:
-        dist.barrier()
-    elapsed = t_start.elapsed_time(t_end) / 1e3
-    fwd_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
-    bwd_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
-    if world > 1:
-        tt = torch.tensor([elapsed], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        elapsed = float(tt.item())
-    tokens_per_rank = B * L
-    value = world * tokens_per_rank * a.steps / elapsed
 
-    fb, bb = algo_bytes_per_seq_step(N, c, p)
-    S = B * H
-    fwd_bytes = fb * S * L
-    bwd_bytes = bb * S * L
+    fb, bb = algo_bytes_per_seq_step(N, c, p, per_dict=bool(cfg.get("s5")))
+    S_loc = B_loc * H
+    fwd_bytes, bwd_bytes = fb * S_loc * L_loc, bb * S_loc * L_loc
     peak, peak_kind = peaks()
     dominant = "scan_bwd" if bwd_ms >= fwd_ms else "scan_fwd"
     dom_bytes, dom_ms = (bwd_bytes, bwd_ms) if dominant == "scan_bwd" else (fwd_bytes, fwd_ms)
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9
-    step_gbs = (fwd_bytes + bwd_bytes) / (elapsed / a.steps) / 1e9
+    step_gbs = (fwd_bytes + bwd_bytes) / (np.median(step_ms) / 1e3) / 1e9
 
-    # ---- end-to-end through the public API with pinned host buffers
+    # ---- end to end through the public API: H2D of the step's inputs from pinned host memory,
+    #      fwd + bwd, D2H of the gradients (db, dD, g) into pinned host memory, every step
     e2e = None
-    if not a.no_e2e:
-        pin = {k: host[k].pin_memory() for k in ("kstar", "diag", "bias", "dh")}
-        if bf16:
-            pin = {k: (v.to(adt).pin_memory() if k in ("diag", "bias", "dh") else v) for k, v in pin.items()}
-        g_host = torch.empty((B, H, L), dtype=torch.float32).pin_memory()
+    if not a.no_e2e and st.sp is None:
+        keys = ["kstar", "diag", "bias", "dh"] if not st.pd else ["kstar", "bias", "dh"]
+        pin = {}
+        for k in keys:
+            t = st.host[k]
+            if bf16 and k in ("diag", "bias", "dh"):
+                t = t.to(torch.bfloat16)
+            pin[k] = t.pin_memory()
+        outs = {k: torch.empty(st.bo[k].shape, dtype=st.bo[k].dtype).pin_memory() for k in ("dbias", "ddiag", "gsel")}
         h2d = sum(v.numel() * v.element_size() for v in pin.values())
-        d2h = g_host.numel() * 4
-        e_steps = max(3, min(a.steps, 10))
+        d2h = sum(v.numel() * v.element_size() for v in outs.values())
+        e_steps = max(3, min(a.steps, 5))
 
         def e2e_step():
             for k, v in pin.items():
-                d[k].copy_(v, non_blocking=True)
-            fr = step_fwd()
-            step_bwd(fr)
-            g_host.copy_(bo["gsel"], non_blocking=True)
+                st.d[k].copy_(v, non_blocking=True)
+            st.step()
+            for k, v in outs.items():
+                v.copy_(st.bo[k], non_blocking=True)
 
         e2e_step()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        s0 = torch.cuda.Event(enable_timing=True)
-        s1 = torch.cuda.Event(enable_timing=True)
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record(stream)
         for _ in range(e_steps):
             e2e_step()
@@ -427,41 +599,41 @@ def main():
             tt = torch.tensor([et], device=dev, dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             et = float(tt.item())
-        e2e = {"value": world * tokens_per_rank * e_steps / et, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h)}
+        e2e = {"value": tokens_all * e_steps / et, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "copies": "H2D " + ", ".join(keys) + "; D2H db, dD, g"}
 
-    # ---- CPU oracle baseline on a bounded sample (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        Lh = 512
-        cpu_oracle_sample(64, N, K, c, a.seed)
-        reps = 3
-        t = sum(cpu_oracle_sample(Lh, N, K, c, a.seed + i) for i in range(reps))
-        cpu = {"value": reps * Lh / H / t, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"{reps} x one (b,h) sequence of {Lh} steps (N={N}, complex={c == 2}), fwd O5 + bwd O8, "
-                         "float64 NumPy, single thread; tokens = steps/H"}
+        cpu = cpu_oracle_baseline(cfg)
 
-    # ---- layer-level kernels of the path (a2/a3 select, a5 projection, a8 readout), timed alone
     layer = None
-    if not a.no_layer:
-        layer = layer_kernels(P, torch, dev, adt, a.dtype, B, L, H, N, K, c, stream)
-        layer["surrogate_grads"] = surrogate_kernels(P, torch, dev, d, fo, bo, dims, a.dtype, B, L, H, N, K, c, p,
-                                                     stream)
+    if a.config == 2 and world == 1 and not a.no_layer and not a.recompute:
+        layer = layer_kernels(P, torch, dev, st.adt, dtype, B, L, H, N, K, c, stream)
+        layer["surrogate_grads"] = surrogate_kernels(P, torch, dev, st.d, st.fo, st.bo, st.dims, dtype, B, L, H, N,
+                                                     K, c, p, stream)
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
-                "ms_per_step": 1e3 * elapsed / a.steps, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": a.dtype, "data": "synthetic",
-                "config": {"workload": "config2: paper Fig.1 shape, fwd+bwd scan", "batch_per_gpu": B, "seq_len": L,
-                           "heads": H, "state": N, "d": H * N, "dict": K, "complex": c == 2, "diag": "per_step",
-                           "tau": int(f["tau"]), "parallelism": f"dp{world} (batch x head shards, no collective)",
-                           "l2": "inputs larger than L2 (>=1.3 GB per step), no flush"},
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+                "warmup": a.warmup, "ms_per_step": 1e3 * elapsed / a.steps, "higher_is_better": True,
+                "scaling": scaling, "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+                "config": {"workload": cfg["workload"], "config_id": a.config, "batch": Bg,
+                           "batch_per_gpu": B_loc if mode == "bh" else Bg, "seq_len": L, "seq_len_per_gpu": L_loc,
+                           "heads": H, "state": N, "d": H * N, "dict": K, "complex": c == 2,
+                           "diag": "per_dict (D = 1)" if cfg.get("s5") else "per_step", "tau": st.tau_eff,
+                           "backward": "recompute (no saved states)" if a.recompute else "saved states",
+                           "parallelism": shard,
+                           "l2": "inputs larger than L2 (>= 0.5 GB per step), no flush"},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                             "frac": achieved / peak, "traffic": traffic_of(dominant), "kernel": dominant,
+                             "frac": achieved / peak, "traffic": traffic_of(dominant, a.config), "kernel": dominant,
                              "algo_bytes_per_launch": dom_bytes, "peak_kind": peak_kind,
                              "traffic_source": "profiles/traffic_latest.json (ncu --set full, dram read+write per launch)"},
-                "step_hbm": {"achieved_gbs": step_gbs, "frac": step_gbs / peak, "fwd_ms": fwd_ms, "bwd_ms": bwd_ms,
-                             "algo_bytes_fwd": fwd_bytes, "algo_bytes_bwd": bwd_bytes},
-                "clocks": clocks, "e2e": e2e, "gpu_launches": launches_per_step * a.steps,
+                "step_hbm": {"achieved_gbs": step_gbs, "frac": step_gbs / peak, "fwd_ms_median": fwd_ms,
+                             "bwd_ms_median": bwd_ms, "step_ms_median": float(np.median(step_ms)),
+                             "stat_steps": len(step_ms), "algo_bytes_fwd": fwd_bytes, "algo_bytes_bwd": bwd_bytes,
+                             "per_rank": world > 1},
+                "seeds": {"values": seed_vals, "min": min(seed_vals), "max": max(seed_vals),
+                          "seeds": [cfg["seed"] + i for i in range(len(seed_vals))]},
+                "clocks": clocks, "e2e": e2e,
+                "gpu_launches": None if launches_per_step is None else launches_per_step * a.steps,
                 "launches_per_step": {"count": launches_per_step, "kernels": kernel_names},
                 "layer_kernels": layer, "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)

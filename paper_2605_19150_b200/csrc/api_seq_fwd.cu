@@ -12,8 +12,9 @@ pdssm_status fwd_seq(const Geo& g, seq::SeqArgs& sa, uint8_t* rec, uint8_t* wm, 
         sa.dict_idx, rec, wm, ovf, const_cast<uint16_t*>(sa.pstart), const_cast<uint16_t*>(sa.psrc), (int)g.N, g.flags);
     pdssm_status r = cuda_check("build_seq_plan");
     if (r) return r;
-    // beta_bar needs its own replay from a zero carry unless h0 is zero (then it is the final state)
-    const bool agg = (g.flags & PDSSM_EXPORT_MAPS) != 0 || sa.h0 != nullptr;
+    // the single chunk's aggregate is composed only on request: no backward reads it (dh0 comes
+    // from the chunk-0 replay, PDSSM_EXPORT_MAPS exports it for tests and SP)
+    const bool agg = (g.flags & PDSSM_EXPORT_MAPS) != 0;
     sa.R = seq_ring(g, false, agg, g.act);
     sa.G = kSeqGF;
     return with_act(g.dtype, [&](auto tv) {

@@ -58,7 +58,9 @@ __global__ void k_bwd_phaseA(const uint8_t* __restrict__ kstar, const uint16_t* 
     }
 }
 
-// Phase B': reverse carry chain per sequence; also dh0 = beta'_0 + Abar_0^T mu_0.
+// Phase B': reverse carry chain per sequence (mu_{c-1} for c >= 1).  With dh0 given it also
+// takes the final step dh0 = beta'_0 + Abar_0^T mu_0 (pdssm_segment_summary_bwd's beta'; the full
+// backward instead takes dh0 from the chunk-0 replay of Phase C', so it never reads Abar_0).
 template <int NC>
 __global__ void k_bwd_phaseB(ChunkStateView cs, const float* __restrict__ betap, const float* __restrict__ lam_in,
                              float* __restrict__ mu_out, float* __restrict__ dh0, int N, int C_ch) {
@@ -72,6 +74,7 @@ __global__ void k_bwd_phaseB(ChunkStateView cs, const float* __restrict__ betap,
         mu.re = lam_in[(size_t)s * NC * N + j];
         if (NC == 2) mu.im = lam_in[(size_t)s * NC * N + N + j];
     }
+    const int c_last = dh0 ? 0 : 1;
     for (int c = C_ch - 1; c >= 0; --c) {
         const size_t ci = (size_t)s * C_ch + c;
         if (act) {
@@ -81,6 +84,7 @@ __global__ void k_bwd_phaseB(ChunkStateView cs, const float* __restrict__ betap,
             if (NC == 2) msh[N + j] = mu.im;
         }
         __syncthreads();
+        if (c < c_last) break;
         if (act) {
             cpx bp{betap[ci * NC * N + j], NC == 2 ? betap[ci * NC * N + N + j] : 0.f};
             if (c == C_ch - 1 && !lam_in) {
@@ -110,7 +114,7 @@ __global__ void k_bwd_phaseC(const uint8_t* __restrict__ kstar, const uint16_t* 
                              const T* __restrict__ hsaved, const float* __restrict__ h0,
                              const TE* __restrict__ e, const float* __restrict__ mu_in, T* __restrict__ dbias,
                              T* __restrict__ ddiag, float* __restrict__ ddiag_f32, float* __restrict__ gsel,
-                             int H, int L, int N, int K, int tau, int C_ch) {
+                             float* __restrict__ dh0, int H, int L, int N, int K, int tau, int C_ch) {
     extern __shared__ float smem[];
     const int nw = blockDim.x / 32;
     float* lsh = smem;                   // [2][NC][N]
@@ -171,6 +175,11 @@ __global__ void k_bwd_phaseC(const uint8_t* __restrict__ kstar, const uint16_t* 
             cpx prod = cmul(Dj, hp);
             gval = lamP.re * prod.re + lamP.im * prod.im;
             if (t > t0) lam = cadd(load_e<TE, NC>(e, off - (size_t)NC * N, N, j), cmulc(Dj, lamP));
+            else if (t == 0 && dh0) {   // chunk 0 ends at t = 0: dh0 = A_0^T lambda_0 (no e_{-1})
+                const cpx d0 = cmulc(Dj, lamP);
+                dh0[(size_t)s * NC * N + j] = d0.re;
+                if (NC == 2) dh0[(size_t)s * NC * N + N + j] = d0.im;
+            }
         }
         for (int o = 16; o > 0; o >>= 1) gval += __shfl_xor_sync(0xffffffffu, gval, o);
         if (lane == 0) gpart[(q & 63) * nw + w] = gval;
@@ -199,7 +208,7 @@ __global__ void k_bwd_phaseC_rc(const uint8_t* __restrict__ kstar, const uint16_
                                 const T* __restrict__ diag, const float* __restrict__ diag_dict,
                                 const T* __restrict__ bias, ChunkStateView cs, const TE* __restrict__ e,
                                 const float* __restrict__ mu_in, T* __restrict__ dbias, T* __restrict__ ddiag,
-                                float* __restrict__ ddiag_f32, float* __restrict__ gsel, int H, int L, int N, int K,
+                                float* __restrict__ ddiag_f32, float* __restrict__ gsel, float* __restrict__ dh0, int H, int L, int N, int K,
                                 int tau, int C_ch) {
     extern __shared__ float smem[];
     const int nw = blockDim.x / 32;
@@ -292,6 +301,11 @@ __global__ void k_bwd_phaseC_rc(const uint8_t* __restrict__ kstar, const uint16_
             cpx prod = cmul(Dj, hp);
             gval = lamP.re * prod.re + lamP.im * prod.im;
             if (t > t0) lam = cadd(load_e<TE, NC>(e, off - (size_t)NC * N, N, j), cmulc(Dj, lamP));
+            else if (t == 0 && dh0) {   // chunk 0 ends at t = 0: dh0 = A_0^T lambda_0 (no e_{-1})
+                const cpx d0 = cmulc(Dj, lamP);
+                dh0[(size_t)s * NC * N + j] = d0.re;
+                if (NC == 2) dh0[(size_t)s * NC * N + N + j] = d0.im;
+            }
         }
         for (int o = 16; o > 0; o >>= 1) gval += __shfl_xor_sync(0xffffffffu, gval, o);
         if (lane == 0) gpart[(q & 63) * nw + w] = gval;

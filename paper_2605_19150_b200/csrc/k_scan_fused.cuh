@@ -1315,8 +1315,10 @@ __global__ void __launch_bounds__(Layout<T, NC, NPL, PD, true, (int)sizeof(TE)>:
                 applyT(pk, dr, di, br, bi, mre, mim);
             }
         }
-        // ---------------- inclusive mu_{c-1} = beta'_c + Abar_c^T mu_c, flag = 2 (or dh0 at c = 0)
-        {
+        // ---------------- inclusive mu_{c-1} = beta'_c + Abar_c^T mu_c, flag = 2 (c > 0).  Chunk 0's
+        // dh0 = A_0^T lambda_0 falls out of its replay below, so Abar_0 is never read (a chunk_state
+        // written by the single-chunk forward carries no aggregate unless maps were exported).
+        if (c > 0) {
             int pk[NPL];
             float dr[NPL], di[NPL], nr[NPL], ni[NPL];
             load_fwd_agg(ci, pk, dr, di);
@@ -1330,9 +1332,6 @@ __global__ void __launch_bounds__(Layout<T, NC, NPL, PD, true, (int)sizeof(TE)>:
                 __threadfence();
                 __syncwarp();
                 if (lane == 0) st_release(flag_ptr(a, ci), 2u);
-            } else if (a.dh0) {
-                vst_f<NPL>(a.dh0 + (size_t)s * row + lane * NPL, nr);
-                if constexpr (NC == 2) vst_f<NPL>(a.dh0 + (size_t)s * row + N + lane * NPL, ni);
             }
             __syncwarp();
         }
@@ -1429,6 +1428,10 @@ __global__ void __launch_bounds__(Layout<T, NC, NPL, PD, true, (int)sizeof(TE)>:
             __syncwarp();
             ++consumed;
             pump<T, TE, NC, NPL, PD, true>(a, fc, consumed, ring, bars, lane, pol_last, pol_out);
+        }
+        if (c == 0 && a.dh0) {   // after t = 0 (no e_{-1} term): lambda = A_0^T lambda_0 = dh0
+            vst_f<NPL>(a.dh0 + (size_t)s * row + lane * NPL, lre);
+            if constexpr (NC == 2) vst_f<NPL>(a.dh0 + (size_t)s * row + N + lane * NPL, lim);
         }
         have = has_next;
         it = nx;

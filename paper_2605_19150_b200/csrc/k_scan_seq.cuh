@@ -13,9 +13,8 @@
 // The preimage of i under entry k is a per-(k, i) record of up to 8 source indices (u8,
 // ascending, padded with the zero slot N); the warp-uniform trip count is the warp's
 // maximum in-degree of entry k.  Entries with an in-degree > 8 take the CSR plan.
-// The map part of the chunk aggregate (pi_bar, d_bar) is always composed alongside (thread-local
-// gathers); AGG (PDSSM_EXPORT_MAPS, or a nonzero h0) adds the local replay
-// beta_bar from a zero carry (a second gather per step) and exports the maps.
+// AGG (PDSSM_EXPORT_MAPS): the chunk aggregate (pi_bar, d_bar, beta_bar) of the single chunk
+// and the final map are composed alongside (thread-local gathers).
 //
 // Backward (reverse, transposed; App. C): thread j owns source j;
 //   lbuf[t&1][j] = lambda_t;  __syncthreads();  lp = lambda_t[P_t[j]]  (a pure gather)
@@ -55,7 +54,7 @@ struct Layout {
         rec = o; o = a16(o + (BWD ? 0 : (size_t)K * N * 8));
         wm = o; o = a16(o + (BWD ? 0 : (size_t)K * NW));
         ovf = o; o = a16(o + (BWD ? 0 : (size_t)K));
-        prow = o; o = a16(o + (size_t)K * N * 2);   // fwd: map composition; bwd: P_t rows
+        prow = o; o = a16(o + ((AGG || BWD) ? (size_t)K * N * 2 : 0));
         dk = o; o = a16(o + (PD ? (size_t)K * NC * N * 4 : 0));
         gs = o; o = a16(o + (BWD ? ((size_t)32 * (N + 1) + (size_t)32 * NW) * 4 : 0));
         bytes = o;
@@ -247,7 +246,8 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
         const uint2* gr = reinterpret_cast<const uint2*>(a.rec) + (size_t)h * K * N;
         for (int x = i; x < K * N; x += NT) rec[x] = __ldg(gr + x);
         for (int x = i; x < K * NW; x += NT) wm[x] = a.wm[(size_t)h * K * NW + x];
-        for (int x = i; x < K * N; x += NT) prow[x] = (uint16_t)min((int)__ldg(a.dict_idx + (size_t)h * K * N + x), N - 1);
+        if constexpr (AGG)
+            for (int x = i; x < K * N; x += NT) prow[x] = (uint16_t)min((int)__ldg(a.dict_idx + (size_t)h * K * N + x), N - 1);
         if constexpr (PD)
             for (int x = i; x < K * NC * N; x += NT) dk[x] = __ldg(a.diag_dict + (size_t)h * K * NC * N + x);
         if (i < 2) kb[L + i] = 0;
@@ -421,9 +421,7 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
         if constexpr (AGG) {
             br = cr + bcr;
             bi = NC == 2 ? ci + bci : 0.f;
-        }
-        {   // pi / d composition (always: the chunk aggregate of the single chunk is part of
-            // chunk_state for every consumer): d <- D_t[pi] d, pi <- P_t[pi]
+            // pi / d composition: d <- D_t[pi] d, pi <- P_t[pi]
             float pr, pm = 0.f;
             if constexpr (PD) {
                 pr = dk[(size_t)kc * row + pi];
@@ -453,20 +451,18 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
     };
     if (any_ovf) run(std::true_type{});
     else run(std::false_type{});
-    // chunk_state of the single chunk: carry_0 = h0; aggregate (pi_bar, d_bar, beta_bar).
-    // Without AGG the host guarantees h0 == NULL, so beta_bar (the replay from a zero carry)
-    // is the final state itself.
+    // chunk_state of the single chunk: carry_0 = h0; aggregate (pi_bar, d_bar, beta_bar)
     {
         a.cs.carry[(size_t)s * row + i] = a.h0 ? a.h0[(size_t)s * row + i] : 0.f;
         if constexpr (NC == 2) a.cs.carry[(size_t)s * row + N + i] = a.h0 ? a.h0[(size_t)s * row + N + i] : 0.f;
-        a.cs.pi[(size_t)s * N + i] = (uint16_t)pi;
-        a.cs.d[(size_t)s * row + i] = dr;
-        a.cs.beta[(size_t)s * row + i] = AGG ? br : hr;
-        if constexpr (NC == 2) {
-            a.cs.d[(size_t)s * row + N + i] = di;
-            a.cs.beta[(size_t)s * row + N + i] = AGG ? bi : hi;
-        }
         if constexpr (AGG) {
+            a.cs.pi[(size_t)s * N + i] = (uint16_t)pi;
+            a.cs.d[(size_t)s * row + i] = dr;
+            a.cs.beta[(size_t)s * row + i] = br;
+            if constexpr (NC == 2) {
+                a.cs.d[(size_t)s * row + N + i] = di;
+                a.cs.beta[(size_t)s * row + N + i] = bi;
+            }
             if (a.maps) {
                 a.maps[((size_t)s * 2) * N + i] = (uint16_t)i;
                 a.maps[((size_t)s * 2 + 1) * N + i] = (uint16_t)pi;

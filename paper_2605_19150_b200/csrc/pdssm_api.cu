@@ -381,8 +381,9 @@ pdssm_status pdssm_scan_bwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
                                                                          (int)g.L, (int)g.N, (int)g.K, g.tau, g.C);
                     pdssm_status rr = cuda_check("bwd_phaseA");
                     if (rr) return rr;
+                    // dh0 comes from the chunk-0 replay (Phase C'), not from Abar_0
                     k_bwd_phaseB<NC><<<(unsigned)g.S, thr, (size_t)NC * g.N * 4, st>>>(cs, betap, lam_in_opt, mu,
-                                                                                         dh0_opt, (int)g.N, g.C);
+                                                                                         nullptr, (int)g.N, g.C);
                     if ((rr = cuda_check("bwd_phaseB"))) return rr;
                     const int nw = thr / 32;
                     if (recompute) {
@@ -391,8 +392,8 @@ pdssm_status pdssm_scan_bwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
                         if ((rr = set_smem((const void*)k_bwd_phaseC_rc<T, TE, NC, PD>, smR))) return rr;
                         k_bwd_phaseC_rc<T, TE, NC, PD><<<items, thr, smR, st>>>(
                             kstar, dict_idx, pstart, psrc, dg, dd, static_cast<const T*>(bias_opt), cs, e, mu,
-                            static_cast<T*>(dbias), PD ? nullptr : static_cast<T*>(ddiag), dDbuf, gsel, (int)g.H,
-                            (int)g.L, (int)g.N, (int)g.K, g.tau, g.C);
+                            static_cast<T*>(dbias), PD ? nullptr : static_cast<T*>(ddiag), dDbuf, gsel, dh0_opt,
+                            (int)g.H, (int)g.L, (int)g.N, (int)g.K, g.tau, g.C);
                         if ((rr = cuda_check("bwd_phaseC_rc"))) return rr;
                         if (PD) {
                             k_bwd_reduce_dict<NC><<<(unsigned)(g.H * g.K), 256, 0, st>>>(
@@ -406,8 +407,8 @@ pdssm_status pdssm_scan_bwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
                     if ((rr = set_smem((const void*)k_bwd_phaseC<T, TE, NC, PD>, smC))) return rr;
                     k_bwd_phaseC<T, TE, NC, PD><<<items, thr, smC, st>>>(
                         kstar, dict_idx, dg, dd, static_cast<const T*>(h_saved), h0_opt, e, mu, static_cast<T*>(dbias),
-                        PD ? nullptr : static_cast<T*>(ddiag), dDbuf, gsel, (int)g.H, (int)g.L, (int)g.N, (int)g.K,
-                        g.tau, g.C);
+                        PD ? nullptr : static_cast<T*>(ddiag), dDbuf, gsel, dh0_opt, (int)g.H, (int)g.L, (int)g.N,
+                        (int)g.K, g.tau, g.C);
                     if ((rr = cuda_check("bwd_phaseC"))) return rr;
                     if (PD) {
                         k_bwd_reduce_dict<NC><<<(unsigned)(g.H * g.K), 256, 0, st>>>(

@@ -84,13 +84,14 @@ class SequenceParallelScan:
 class CudaOps:
     """The C-ABI library as SequenceParallelScan ops (device tensors, one rank = one GPU)."""
 
-    def __init__(self, N, K, c, tau=0):
+    def __init__(self, N, K, c, tau=0, per_dict=False):
         import paper_2605_19150_b200 as P
-        self.P, self.N, self.K, self.c, self.tau = P, N, K, c, tau
+        self.P, self.N, self.K, self.c, self.tau, self.pd = P, N, K, c, tau, per_dict
 
     def _dims(self, kstar):
         B, H, L = kstar.shape
-        return self.P.make_dims(B, H, L, self.N, self.K, c=self.c, tau=self.tau)
+        return self.P.make_dims(B, H, L, self.N, self.K, c=self.c, tau=self.tau,
+                                diag_mode=self.P.PER_DICT if self.pd else self.P.PER_STEP)
 
     def segment_summary(self, kstar, dict_idx, diag, bias):
         self._seg_dims = self._dims(kstar)   # every rank's segment has the same B, H, N, c
@@ -100,7 +101,7 @@ class CudaOps:
         return self.P.compose_carry(gathered.reshape(-1), rank, world, self._seg_dims, h0=h0)
 
     def scan_fwd(self, kstar, dict_idx, diag, bias, carry):
-        return self.P.scan_fwd(kstar, dict_idx, diag, bias, h0=carry, tau=self.tau)
+        return self.P.scan_fwd(kstar, dict_idx, diag, bias, h0=carry, tau=self.tau, per_dict=self.pd)
 
     def segment_summary_bwd(self, kstar, dict_idx, diag, fwd_out, dh):
         return self.P.segment_summary_bwd(kstar, dict_idx, diag, fwd_out["chunk_state"], fwd_out["dims"], dh=dh)

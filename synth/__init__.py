@@ -140,6 +140,64 @@ def scan_inputs(B, H, L, N, K, c, seed, h0=False, per_dict=False, sticky=0.0, dh
     return out
 
 
+def _rng_row(seed, stream, b):
+    """Stream of batch row b of tensor `stream`: rows are independent of each other, so any
+    contiguous block of a global batch can be generated alone (bench.py: inputs are generated
+    globally and each rank draws only its own rows)."""
+    ss = np.random.SeedSequence(seed, spawn_key=(_STREAMS.index(stream), int(b)))
+    return np.random.Generator(np.random.PCG64(ss))
+
+
+def scan_inputs_rows(B, H, L, N, K, c, seed, rows=None, h0=False, per_dict=False, sticky=0.0, dh=False,
+                     bf16=False):
+    """scan_inputs of a global batch of B rows, generated row by row: `rows` = (b0, b1) returns
+    only rows b0..b1-1 (the same values those rows have in the full batch).  Same distributions
+    as scan_inputs; the dictionary is global."""
+    b0, b1 = (0, B) if rows is None else rows
+    n = b1 - b0
+    out = dict(dict_idx=random_maps(H, K, N, seed))
+    ks = np.empty((n, H, L), np.uint8)
+    bias = np.empty((n, H, L, c, N), np.float32)
+    D = None if per_dict else np.empty((n, H, L, c, N), np.float32)
+    dhv = np.empty((n, H, L, c, N), np.float32) if dh else None
+    h0v = np.empty((n, H, c, N), np.float32) if h0 else None
+    for i, b in enumerate(range(b0, b1)):
+        r = _rng_row(seed, "kstar", b)
+        k = r.integers(0, K, size=(H, L)).astype(np.uint8)
+        if sticky > 0:
+            keep = r.random(size=(H, L)) < sticky
+            for t in range(1, L):
+                k[:, t] = np.where(keep[:, t], k[:, t - 1], k[:, t])
+        ks[i] = k
+        if D is not None:
+            r = _rng_row(seed, "D", b)
+            a = r.normal(2.0, 1.0, size=(H, L, N))
+            mag = 1.0 / (1.0 + np.exp(-a))
+            if c == 1:
+                D[i, :, :, 0] = mag
+            else:
+                th = r.uniform(-np.pi, np.pi, size=(H, L, N))
+                D[i, :, :, 0] = mag * np.cos(th)
+                D[i, :, :, 1] = mag * np.sin(th)
+        bias[i] = _rng_row(seed, "b", b).standard_normal(size=(H, L, c, N), dtype=np.float32)
+        if dhv is not None:
+            dhv[i] = _rng_row(seed, "dh", b).standard_normal(size=(H, L, c, N), dtype=np.float32)
+        if h0v is not None:
+            h0v[i] = _rng_row(seed, "h0", b).standard_normal(size=(H, c, N), dtype=np.float32)
+    out["kstar"] = ks
+    out["diag"] = diag((H, K), N, c, seed, "Dk") if per_dict else D
+    out["bias"] = bias
+    if dhv is not None:
+        out["dh"] = dhv
+    if h0v is not None:
+        out["h0"] = h0v
+    if bf16:
+        for k in ("diag", "bias", "dh"):
+            if k in out and not (k == "diag" and per_dict):
+                out[k] = round_bf16(out[k])
+    return out
+
+
 def projection_B(H, c, N, d_in, seed):
     """Bw[H][c][N][d_in] ~ U(+-1/sqrt(d_in)) (plane 0 real part, 1 imaginary)."""
     r = _rng(seed, "Bw")

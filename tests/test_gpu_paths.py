@@ -3,8 +3,8 @@
 * the ABI's extreme shapes: K = 256 (N = 32 and 128, chunked fast path and generic) and
   N = 1024 (generic);
 * hypothesis-randomised small shapes (B, H, L, N, K, c, tau, dtype) through the default dispatch;
-* a forward taken by the single-chunk kernel followed by a backward that takes another path
-  (chunk_state must be complete whichever kernel wrote it), with an incoming adjoint;
+* a forward taken by the single-chunk kernel followed by a backward that takes another path,
+  with an incoming adjoint;
 * the sequence-parallel backward summary after a single-chunk forward (tau = 0, many sequences);
 * the autograd glue with non-contiguous (permuted) inputs."""
 import os
@@ -72,7 +72,10 @@ def fwd_bwd_check(P, B, H, L, N, K, c, tau, bf16=False, seed=0, h0=True):
 @pytest.mark.parametrize("N,c", [(32, 2), (128, 1)])
 def test_dictionary_of_256_entries(P, N, c, path, monkeypatch):
     """K = 256 (the largest K of the paper, and the ABI maximum: k* is uint8)."""
-    monkeypatch.setenv("PDSSM_PATH", "fused" if path == "auto" else "generic")
+    if path == "auto":
+        monkeypatch.delenv("PDSSM_PATH", raising=False)    # the library's own dispatch for K = 256
+    else:
+        monkeypatch.setenv("PDSSM_PATH", "generic")
     fwd_bwd_check(P, 2, 2, 400, N, 256, c, 32, seed=N + c)
 
 
@@ -104,14 +107,15 @@ def test_hypothesis_random_shapes(P, monkeypatch):
 
 
 def test_single_chunk_forward_then_other_backward_path(P, monkeypatch):
-    """The forward runs the single-chunk kernel (tau = L, EXPORT_MAPS off, h0 = 0), the backward is
-    forced onto the chunked / generic kernels, which read the forward's chunk aggregate for the
-    incoming adjoint lam_in (the path a misaligned dh selects)."""
+    """The forward runs the single-chunk kernel (tau = L, EXPORT_MAPS off, h0 = 0: it composes no
+    chunk aggregate), the backward is forced onto the chunked / generic kernels (the path a
+    misaligned dh selects) with an incoming adjoint lam_in: they must not read the aggregate
+    (dh0 comes from the chunk-0 replay)."""
     B, H, L, N, K, c = 2, 2, 160, 64, 8, 2
     inp = synth.scan_inputs(B, H, L, N, K, c, seed=77, dh=True)
     d = to_dev(inp, False)
     monkeypatch.setenv("PDSSM_PATH", "seq")
-    f = P.scan_fwd(d["kstar"], d["dict_idx"], d["diag"], d["bias"])
+    f = P.scan_fwd(d["kstar"], d["dict_idx"], d["diag"], d["bias"], tau=L)   # dims.chunk = L for every path
     assert f["tau"] == L
     rng = np.random.default_rng(3)
     lam = rng.standard_normal((B, H, c, N)).astype(np.float32)
