@@ -70,7 +70,12 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-layer", action="store_true")
-    return ap.parse_args()
+    ap.add_argument("--profile", action="store_true",
+                    help="under ncu: one seed, no clock block, no per-step statistics, no CPU / e2e / layer legs")
+    a = ap.parse_args()
+    if a.profile:
+        a.seeds, a.stat_steps, a.no_cpu_baseline, a.no_e2e, a.no_layer = 1, 1, True, True, True
+    return a
 
 
 def peaks():
@@ -525,14 +530,16 @@ def main():
         for _ in range(max(a.warmup, 3)):
             st.step()
         torch.cuda.synchronize()
-        if si == 0:   # nvidia-smi sampling spans the timed region of the reported value
+        if si == 0 and not a.profile:   # nvidia-smi sampling spans the timed region of the reported value
             clk = Clocks(local)
             clk.start()
             time.sleep(0.3)
         el, fw, bw = timed(torch, dist, st, stream, a.steps, world, dev)
-        if si == 0:
+        if si == 0 and not a.profile:
             timed(torch, dist, st, stream, max(a.steps, 200), world, dev, per_step=False)
             clocks = clk.stop()
+        elif si == 0:
+            clocks = None
         tokens_all = (Bg if cfg["scaling"] == "weak" and mode == "bh" else B) * L   # whole-job tokens per step
         v = tokens_all * a.steps / el
         seed_vals.append(v)
@@ -543,6 +550,8 @@ def main():
     st, inp, B_loc, L_loc, shard, Bg, elapsed, fw, bw, tokens_all = main_res
     value = seed_vals[0]
     try:
+        if a.profile:
+            raise RuntimeError("not counted under --profile")
         launches_per_step, kernel_names = count_launches(st.step)
     except Exception as ex:
         launches_per_step, kernel_names = None, [f"profiler failed: {ex}"[:80]]

@@ -209,18 +209,28 @@ constexpr size_t kSeqSmemBudget = 200 * 1024;
 constexpr int kSeqG = seq::SEQ_G;     // backward group
 constexpr int kSeqGF = seq::SEQ_GF;   // forward group
 
-// ring depth R for this shape (0: the layout does not fit)
-// ring depth R for this shape (0: the layout does not fit).  When there are more
-// sequences than SMs, the budget is split so that ceil(S / #SMs) CTAs (up to 4) fit per SM.
-inline int seq_ring(const Geo& g, bool bwd, bool agg, size_t esz_e) {
-    const int G = bwd ? kSeqG : kSeqGF;
+// Sequences per CTA of the single-chunk kernels: with N <= 64 and more sequences than SMs, two
+// sequences (batch rows b, b + 1) of one head share a CTA, its per-head tables, producer warp and
+// step barrier -- the per-sequence shared memory shrinks, so every CTA is resident in one wave
+// (config 4: 1024 sequences as 512 CTAs, 4 per SM).
+inline int seq_spc(const Geo& g) {
+    return (g.N <= 64 && g.N % 32 == 0 && g.B % 2 == 0 && g.S > (int64_t)num_sms_dev()) ? 2 : 1;
+}
+// steps per TMA group: the paired variants use shorter groups to fit 4 CTAs per SM
+inline int seq_group(bool bwd, int spc) { return bwd ? (spc > 1 ? 8 : kSeqG) : (spc > 1 ? 16 : kSeqGF); }
+
+// ring depth R for this shape (0: the layout does not fit).  When there are more CTAs than
+// SMs, the budget is split so that ceil(#CTAs / #SMs) CTAs (up to 4) fit per SM.
+inline int seq_ring(const Geo& g, bool bwd, bool agg, size_t esz_e, int spc = 1) {
+    const int G = seq_group(bwd, spc);
     const int ngroups = (int)ceil_div(g.L, G);
-    const int64_t per_sm = std::min<int64_t>(std::max<int64_t>(ceil_div(g.S, num_sms_dev()), 1), 4);
+    const int64_t ctas = g.S / spc;
+    const int64_t per_sm = std::min<int64_t>(std::max<int64_t>(ceil_div(ctas, num_sms_dev()), 1), 4);
     const size_t budget = std::min<size_t>(kSeqSmemBudget, (size_t)(226 * 1024) / (size_t)per_sm - 1024);
     int best = 0;
     for (int R = 2; R <= 16 && R <= ngroups + 1; ++R) {
         seq::Layout ly((int)g.N, (int)g.K, R, G, g.nc, (int)g.act, (int)esz_e, g.diag_mode == PDSSM_DIAG_PER_DICT, agg, bwd,
-                       (int)g.L);
+                       (int)g.L, spc);
         if (ly.bytes <= budget) best = R;
     }
     if (best == 0 && ngroups <= 1) best = 2;

@@ -12,20 +12,26 @@ pdssm_status bwd_seq(const Geo& g, seq::SeqArgs& sa, cudaStream_t st) {
     return with_act(g.dtype, [&](auto tv) {
         using T = decltype(tv);
         using TEE = typename std::conditional<std::is_same<TE, void>::value, T, TE>::type;
-        sa.R = seq_ring(g, true, false, sizeof(TEE));
-        sa.G = kSeqG;
+        int spc = g.N == 64 ? seq_spc(g) : 1;   // paired sequences per CTA (see seq_spc)
+        sa.R = seq_ring(g, true, false, sizeof(TEE), spc);
+        if (spc > 1 && sa.R < 2) {
+            spc = 1;
+            sa.R = seq_ring(g, true, false, sizeof(TEE), 1);
+        }
+        sa.G = seq_group(true, spc);
+        sa.spc = spc;
         return with_nc(g.nc, [&](auto ncv) {
             constexpr int NC = decltype(ncv)::value;
             return with_pd(g.diag_mode, [&](auto pdv) {
                 constexpr bool PD = decltype(pdv)::value;
                 seq::Layout ly((int)g.N, (int)g.K, sa.R, sa.G, NC, (int)sizeof(T), (int)sizeof(TEE), PD, false, true,
-                               (int)g.L);
+                               (int)g.L, spc);
                 auto kern = g.N == 128 ? seq::k_bwd_seq<T, TEE, NC, PD, 128>
-                            : g.N == 64    ? seq::k_bwd_seq<T, TEE, NC, PD, 64>
-                                           : seq::k_bwd_seq<T, TEE, NC, PD, 0>;
+                            : g.N == 64 ? (spc == 2 ? seq::k_bwd_seq<T, TEE, NC, PD, 64, 2, 8> : seq::k_bwd_seq<T, TEE, NC, PD, 64>)
+                                        : seq::k_bwd_seq<T, TEE, NC, PD, 0>;
                 pdssm_status rr = seq_set_smem((const void*)kern, ly.bytes);
                 if (rr) return rr;
-                kern<<<(unsigned)g.S, (unsigned)g.N + 32, ly.bytes, st>>>(sa);   // + producer warp
+                kern<<<(unsigned)(g.S / spc), (unsigned)(spc * g.N) + 32, ly.bytes, st>>>(sa);   // + producer warp
                 return cuda_check("bwd_seq");
             });
         });

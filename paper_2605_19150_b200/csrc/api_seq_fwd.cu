@@ -15,8 +15,16 @@ pdssm_status fwd_seq(const Geo& g, seq::SeqArgs& sa, uint8_t* rec, uint8_t* wm, 
     // the single chunk's aggregate is composed only on request: no backward reads it (dh0 comes
     // from the chunk-0 replay, PDSSM_EXPORT_MAPS exports it for tests and SP)
     const bool agg = (g.flags & PDSSM_EXPORT_MAPS) != 0;
-    sa.R = seq_ring(g, false, agg, g.act);
-    sa.G = kSeqGF;
+    const bool chk = (g.flags & PDSSM_CHECK_FINITE) != 0;
+    // paired sequences per CTA: production variant (no maps, no checks) at N = 64 only
+    int spc = (agg || chk || g.N != 64) ? 1 : seq_spc(g);
+    sa.R = seq_ring(g, false, agg, g.act, spc);
+    if (spc > 1 && sa.R < 2) {
+        spc = 1;
+        sa.R = seq_ring(g, false, agg, g.act, 1);
+    }
+    sa.G = seq_group(false, spc);
+    sa.spc = spc;
     return with_act(g.dtype, [&](auto tv) {
         using T = decltype(tv);
         return with_nc(g.nc, [&](auto ncv) {
@@ -27,19 +35,21 @@ pdssm_status fwd_seq(const Geo& g, seq::SeqArgs& sa, uint8_t* rec, uint8_t* wm, 
                     constexpr bool AGG = decltype(aggv)::value;
                     constexpr bool CHK = decltype(chkv)::value;
                     seq::Layout ly((int)g.N, (int)g.K, sa.R, sa.G, NC, (int)sizeof(T), (int)sizeof(T), PD, AGG, false,
-                                   (int)g.L);
+                                   (int)g.L, spc);
                     // compile-time N for the production variants (no maps, no checks)
                     auto kern = seq::k_fwd_seq<T, NC, PD, AGG, CHK, 0>;
                     if constexpr (!AGG && !CHK) {
                         if (g.N == 128) kern = seq::k_fwd_seq<T, NC, PD, false, false, 128>;
-                        else if (g.N == 64) kern = seq::k_fwd_seq<T, NC, PD, false, false, 64>;
+                        else if (g.N == 64)
+                            kern = spc == 2 ? seq::k_fwd_seq<T, NC, PD, false, false, 64, 2, 16>
+                                            : seq::k_fwd_seq<T, NC, PD, false, false, 64>;
                     }
                     pdssm_status rr = seq_set_smem((const void*)kern, ly.bytes);
                     if (rr) return rr;
                     // programmatic dependent launch: the prologue overlaps the plan kernel's tail
                     cudaLaunchConfig_t cfg = {};
-                    cfg.gridDim = dim3((unsigned)g.S);
-                    cfg.blockDim = dim3((unsigned)g.N + 32);   // + producer warp
+                    cfg.gridDim = dim3((unsigned)(g.S / spc));
+                    cfg.blockDim = dim3((unsigned)(spc * g.N) + 32);   // + producer warp
                     cfg.dynamicSmemBytes = ly.bytes;
                     cfg.stream = st;
                     cudaLaunchAttribute attr[1];
@@ -51,7 +61,6 @@ pdssm_status fwd_seq(const Geo& g, seq::SeqArgs& sa, uint8_t* rec, uint8_t* wm, 
                     if (le != cudaSuccess) return fail(PDSSM_ERR_CUDA, "fwd_seq launch: %s", cudaGetErrorString(le));
                     return cuda_check("fwd_seq");
                 };
-                const bool chk = (g.flags & PDSSM_CHECK_FINITE) != 0;
                 if (agg) return chk ? go(std::true_type{}, std::true_type{}) : go(std::true_type{}, std::false_type{});
                 return chk ? go(std::false_type{}, std::true_type{}) : go(std::false_type{}, std::false_type{});
             });

@@ -36,27 +36,36 @@ constexpr int WM_OVF = 15;   // trip-count code of an overflowing entry
 __host__ __device__ constexpr size_t a16(size_t x) { return (x + 15) & ~(size_t)15; }
 
 // shared-memory carve-up (host and device agree)
+// SPC sequences of one head share a CTA (and its per-head tables): the ring slot holds, per
+// stream, SPC blocks of G rows; the exchange rows, k* staging and g tiles are per sequence.
 struct Layout {
     size_t ring, bars, x, x2, kb, rec, wm, ovf, prow, dk, gs, bytes;
-    int slot;   // bytes per ring slot
-    __host__ __device__ Layout(int N, int K, int R, int G, int NC, int esz, int esz_e, bool PD, bool AGG, bool BWD, int L) {
+    int slot;     // bytes per ring slot
+    size_t xs;    // bytes of one sequence's exchange rows (two rows of N + 1 values)
+    size_t kbs;   // bytes of one sequence's k* staging
+    size_t gss;   // bytes of one sequence's g tiles
+    __host__ __device__ Layout(int N, int K, int R, int G, int NC, int esz, int esz_e, bool PD, bool AGG, bool BWD, int L,
+                               int SPC = 1) {
         const int row = NC * N * esz, erow = NC * N * esz_e;
         const int NW = N / 32;
-        slot = (int)a16(BWD ? (size_t)(PD ? 0 : G * row) + (size_t)G * erow + (size_t)G * row
-                            : (size_t)(PD ? 0 : G * row) + (size_t)G * row);
+        slot = (int)a16((size_t)SPC * (BWD ? (size_t)(PD ? 0 : G * row) + (size_t)G * erow + (size_t)G * row
+                                           : (size_t)(PD ? 0 : G * row) + (size_t)G * row));
         size_t o = 0;
         ring = o; o = a16(o + (size_t)R * slot);
         bars = o; o = a16(o + (size_t)2 * R * 8);   // full[R], then empty[R]
         const int sv = NC == 2 ? 8 : 4;
-        x = o; o = a16(o + (size_t)2 * (N + 1) * sv);
-        x2 = o; o = a16(o + (AGG ? (size_t)2 * (N + 1) * sv : 0));
-        kb = o; o = a16(o + (size_t)L + 2);
+        xs = a16((size_t)2 * (N + 1) * sv);
+        x = o; o = a16(o + (size_t)SPC * xs);
+        x2 = o; o = a16(o + (AGG ? (size_t)SPC * xs : 0));
+        kbs = a16((size_t)L + 2);
+        kb = o; o = a16(o + (size_t)SPC * kbs);
         rec = o; o = a16(o + (BWD ? 0 : (size_t)K * N * 8));
         wm = o; o = a16(o + (BWD ? 0 : (size_t)K * NW));
         ovf = o; o = a16(o + (BWD ? 0 : (size_t)K));
         prow = o; o = a16(o + ((AGG || BWD) ? (size_t)K * N * 2 : 0));
         dk = o; o = a16(o + (PD ? (size_t)K * NC * N * 4 : 0));
-        gs = o; o = a16(o + (BWD ? ((size_t)32 * (N + 1) + (size_t)32 * NW) * 4 : 0));
+        gss = BWD ? a16(((size_t)32 * (N + 1) + (size_t)32 * NW) * 4) : 0;
+        gs = o; o = a16(o + (size_t)SPC * gss);
         bytes = o;
     }
 };
@@ -82,6 +91,7 @@ struct SeqArgs {
     float* gsel;                // bwd
     float* dh0;                 // bwd
     int H, L, N, K, R, G;
+    int spc;                    // sequences per CTA (the host requires B % spc == 0)
     uint32_t flags;
 };
 
@@ -213,21 +223,28 @@ constexpr int SEQ_GF = 32;   // forward: steps per ring slot
 //   h_t = sum + b_t ; streaming store.
 // NN: the state count as a compile-time constant (0 = runtime a.N): every row offset, ring
 // position and exchange address of an unrolled group becomes an immediate.
-template <typename T, int NC, bool PD, bool AGG, bool CHECK, int NN>
+// SPC > 1 (N <= 64): SPC sequences (b, b+1, ...) of the same head h share the CTA, its per-head
+// tables, the producer warp and the step barrier; blockIdx.x = p * H + h serves batch rows
+// p * SPC .. p * SPC + SPC - 1.  GF: steps per TMA group.
+template <typename T, int NC, bool PD, bool AGG, bool CHECK, int NN, int SPC = 1, int GF = SEQ_GF>
 __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
     using SV = typename fused::SVal<NC>::type;
-    constexpr int G = SEQ_GF;
+    constexpr int G = GF;
     constexpr int SVB = (int)sizeof(SV);
     extern __shared__ __align__(128) uint8_t smem[];
     const int N = NN ? NN : a.N, K = a.K, L = a.L, R = a.R;
-    const int i = threadIdx.x, w = i >> 5, NW = N >> 5;
-    const int s = blockIdx.x, h = s % a.H;
-    const Layout Ly(N, K, R, G, NC, (int)sizeof(T), (int)sizeof(T), PD, AGG, false, L);
+    const int i = threadIdx.x, NW = N >> 5;
+    const int h = blockIdx.x % a.H, pidx = blockIdx.x / a.H;
+    const int sub = (SPC > 1 && i < SPC * N) ? i / N : 0;   // this thread's sequence within the CTA
+    const int il = i - sub * N;                             // its state
+    const int w = il >> 5;                                  // its warp within the sequence
+    const int s = (pidx * SPC + sub) * a.H + h;
+    const Layout Ly(N, K, R, G, NC, (int)sizeof(T), (int)sizeof(T), PD, AGG, false, L, SPC);
     uint8_t* ring = smem + Ly.ring;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Ly.bars);
-    char* xbc = reinterpret_cast<char*>(smem + Ly.x);
-    char* xbc2 = reinterpret_cast<char*>(smem + Ly.x2);
-    uint8_t* kb = smem + Ly.kb;
+    char* xbc = reinterpret_cast<char*>(smem + Ly.x + sub * Ly.xs);
+    char* xbc2 = reinterpret_cast<char*>(smem + Ly.x2 + sub * Ly.xs);
+    uint8_t* kb = smem + Ly.kb + sub * Ly.kbs;
     uint2* rec = reinterpret_cast<uint2*>(smem + Ly.rec);
     uint8_t* wm = smem + Ly.wm;
     uint16_t* prow = reinterpret_cast<uint16_t*>(smem + Ly.prow);
@@ -239,7 +256,7 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
     // The sequence's k* first: it does not depend on the plan launch that precedes this
     // kernel, which may still be running (programmatic dependent launch); wait for it only
     // before the tables it writes are read.
-    stage_k(a, kb, seq0, L);
+    for (int j = 0; j < SPC; ++j) stage_k(a, smem + Ly.kb + j * Ly.kbs, (size_t)((pidx * SPC + j) * a.H + h) * L, L);
     asm volatile("griddepcontrol.wait;" ::: "memory");
     {   // one-time tables of head h (k* zero-padded by 2)
         const int NT = blockDim.x;
@@ -250,16 +267,18 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
             for (int x = i; x < K * N; x += NT) prow[x] = (uint16_t)min((int)__ldg(a.dict_idx + (size_t)h * K * N + x), N - 1);
         if constexpr (PD)
             for (int x = i; x < K * NC * N; x += NT) dk[x] = __ldg(a.diag_dict + (size_t)h * K * NC * N + x);
-        if (i < 2) kb[L + i] = 0;
+        if (i < 2 * SPC) (smem + Ly.kb + (i >> 1) * Ly.kbs)[L + (i & 1)] = 0;
     }
     const int XB = (N + 1) * SVB;   // bytes of one exchange row (N values + the zero slot)
-    if (i == 0) {
+    if (il == 0 && i < SPC * N) {   // the zero slots of this sequence's exchange rows
         *reinterpret_cast<SV*>(xbc + N * SVB) = fused::mk<NC>(0.f, 0.f);
         *reinterpret_cast<SV*>(xbc + XB + N * SVB) = fused::mk<NC>(0.f, 0.f);
         if constexpr (AGG) {
             *reinterpret_cast<SV*>(xbc2 + N * SVB) = fused::mk<NC>(0.f, 0.f);
             *reinterpret_cast<SV*>(xbc2 + XB + N * SVB) = fused::mk<NC>(0.f, 0.f);
         }
+    }
+    if (i == 0) {
         for (int q = 0; q < 2 * R; ++q) fused::mbar_init(bars + q, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -268,50 +287,57 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
     for (int x = i; x < K * NW; x += blockDim.x) my_ovf |= a.wm[(size_t)h * K * NW + x] == WM_OVF;
     const bool any_ovf = __syncthreads_or(my_ovf) != 0;
     const int ROWB = (int)(row * sizeof(T));
-    const int OFF_B = PD ? 0 : G * ROWB;
-    auto issue = [&](int g, int slot) {   // thread 0: rows of steps [gG, gG+len) -> slot
+    const int OFF_B = PD ? 0 : SPC * G * ROWB;   // slot: [D rows of seq 0..SPC-1][b rows of seq 0..SPC-1]
+    const int SUBOFF = sub * G * ROWB;           // this sequence's block inside each stream
+    auto issue = [&](int g, int slot) {   // producer lane 0: rows of steps [gG, gG+len) -> slot
         const int t = g * G, len = min(G, L - t);
         uint8_t* dst = ring + (size_t)slot * Ly.slot;
-        fused::mbar_expect_tx(bars + slot, (uint32_t)((PD ? 0 : len * ROWB) + len * ROWB));
-        if constexpr (!PD) fused::tma_1d_hint(dst, static_cast<const T*>(a.diag) + (seq0 + t) * row, len * ROWB, bars + slot, pol);
-        fused::tma_1d_hint(dst + OFF_B, static_cast<const T*>(a.bias) + (seq0 + t) * row, len * ROWB, bars + slot, pol);
+        fused::mbar_expect_tx(bars + slot, (uint32_t)(SPC * ((PD ? 0 : len * ROWB) + len * ROWB)));
+        for (int j = 0; j < SPC; ++j) {
+            const size_t sj0 = (size_t)((pidx * SPC + j) * a.H + h) * L;
+            if constexpr (!PD)
+                fused::tma_1d_hint(dst + j * G * ROWB, static_cast<const T*>(a.diag) + (sj0 + t) * row, len * ROWB,
+                                   bars + slot, pol);
+            fused::tma_1d_hint(dst + OFF_B + j * G * ROWB, static_cast<const T*>(a.bias) + (sj0 + t) * row, len * ROWB,
+                               bars + slot, pol);
+        }
     };
-    if (i >= N) {   // producer warp
+    if (i >= SPC * N) {   // producer warp
         produce(bars, R, ngroups, issue);
         return;
     }
     float hr = 0.f, hi = 0.f;
     if (a.h0) {
-        hr = a.h0[(size_t)s * row + i];
-        if constexpr (NC == 2) hi = a.h0[(size_t)s * row + N + i];
+        hr = a.h0[(size_t)s * row + il];
+        if constexpr (NC == 2) hi = a.h0[(size_t)s * row + N + il];
     }
     float br = 0.f, bi = 0.f, dr = 1.f, di = 0.f;
-    int pi = i;
-    T* hout = static_cast<T*>(a.out0) + seq0 * row + i;
+    int pi = il;
+    T* hout = static_cast<T*>(a.out0) + seq0 * row + il;
     // operands of the current step
     int k, k1, m;
     uint2 rc;
     float Dr, Di, Br, Bi;
     auto load_ops = [&](const uint8_t* rp, int k_) {
         if constexpr (PD) {
-            Dr = dk[(size_t)k_ * row + i];
-            Di = NC == 2 ? dk[(size_t)k_ * row + N + i] : 0.f;
+            Dr = dk[(size_t)k_ * row + il];
+            Di = NC == 2 ? dk[(size_t)k_ * row + N + il] : 0.f;
         } else {
             const T* Dp = reinterpret_cast<const T*>(rp);
-            Dr = ldact_s(Dp + i);
-            Di = NC == 2 ? ldact_s(Dp + N + i) : 0.f;
+            Dr = ldact_s(Dp + il);
+            Di = NC == 2 ? ldact_s(Dp + N + il) : 0.f;
         }
         const T* Bp = reinterpret_cast<const T*>(rp + OFF_B);
-        Br = ldact_s(Bp + i);
-        Bi = NC == 2 ? ldact_s(Bp + N + i) : 0.f;
+        Br = ldact_s(Bp + il);
+        Bi = NC == 2 ? ldact_s(Bp + N + il) : 0.f;
     };
     int slot = 0;
     uint32_t ph = 0;
-    const uint8_t* sb = ring;   // base of the current group's slot
+    const uint8_t* sb = ring + SUBOFF;   // this sequence's rows in the current group's slot
     fused::mbar_wait(bars, 0);
     k = kb[0];
     k1 = kb[1];
-    rc = rec[(size_t)k * N + i];
+    rc = rec[(size_t)k * N + il];
     m = wm[k * NW + w];
     load_ops(sb, k);
     auto step = [&](const int r, const int g, const int t, auto ovfv) {
@@ -337,13 +363,13 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
             check_cpx(cpx{Dr, Di}, a.flags);
             check_cpx(cpx{Br, Bi}, a.flags);
         }
-        *reinterpret_cast<SV*>(vbc + i * SVB) = fused::mk<NC>(Dr * hr - Di * hi, Dr * hi + Di * hr);
-        if constexpr (AGG) *reinterpret_cast<SV*>(vbc2 + i * SVB) = fused::mk<NC>(Dr * br - Di * bi, Dr * bi + Di * br);
+        *reinterpret_cast<SV*>(vbc + il * SVB) = fused::mk<NC>(Dr * hr - Di * hi, Dr * hi + Di * hr);
+        if constexpr (AGG) *reinterpret_cast<SV*>(vbc2 + il * SVB) = fused::mk<NC>(Dr * br - Di * bi, Dr * bi + Di * br);
         const int mc = m, kc = k;
         const float bcr = Br, bci = Bi;
         const uint8_t* rpc = sb + r * ROWB;
 #ifndef FWD_EXP_NOBAR   // timing experiment only: no exchange barrier (wrong results)
-        compute_sync(N);
+        compute_sync(SPC * N);
 #endif
         SV v[CAP];
 #if defined(FWD_EXP_SLOTS)   // timing experiment only: FWD_EXP_SLOTS gather slots (wrong results)
@@ -367,7 +393,7 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
         // operands of step t+1 (consumed a step later)
         if (r < G - 1) {
             k = k1;
-            rc = rec[(size_t)k * N + i];
+            rc = rec[(size_t)k * N + il];
             m = wm[k * NW + w];
             load_ops(sb + (r + 1) * ROWB, k);
         } else if (g + 1 < ngroups) {
@@ -375,10 +401,10 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
                 slot = 0;
                 ph ^= 1u;
             }
-            sb = ring + (size_t)slot * Ly.slot;
+            sb = ring + (size_t)slot * Ly.slot + SUBOFF;
             fused::mbar_wait(bars + slot, ph);
             k = k1;
-            rc = rec[(size_t)k * N + i];
+            rc = rec[(size_t)k * N + il];
             m = wm[k * NW + w];
             load_ops(sb, k);
         }
@@ -402,7 +428,7 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
             const SV* vb = reinterpret_cast<const SV*>(vbc);
             const SV* vb2 = reinterpret_cast<const SV*>(vbc2);
             const size_t e = (size_t)h * K + kc;
-            const int st = __ldg(a.pstart + e * (N + 1) + i), en = __ldg(a.pstart + e * (N + 1) + i + 1);
+            const int st = __ldg(a.pstart + e * (N + 1) + il), en = __ldg(a.pstart + e * (N + 1) + il + 1);
             for (int q = st; q < en; ++q) {
                 const int j = __ldg(a.psrc + e * N + q);
                 ar += fused::re_of<NC>(vb[j]);
@@ -453,19 +479,19 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
     else run(std::false_type{});
     // chunk_state of the single chunk: carry_0 = h0; aggregate (pi_bar, d_bar, beta_bar)
     {
-        a.cs.carry[(size_t)s * row + i] = a.h0 ? a.h0[(size_t)s * row + i] : 0.f;
-        if constexpr (NC == 2) a.cs.carry[(size_t)s * row + N + i] = a.h0 ? a.h0[(size_t)s * row + N + i] : 0.f;
+        a.cs.carry[(size_t)s * row + il] = a.h0 ? a.h0[(size_t)s * row + il] : 0.f;
+        if constexpr (NC == 2) a.cs.carry[(size_t)s * row + N + il] = a.h0 ? a.h0[(size_t)s * row + N + il] : 0.f;
         if constexpr (AGG) {
-            a.cs.pi[(size_t)s * N + i] = (uint16_t)pi;
-            a.cs.d[(size_t)s * row + i] = dr;
-            a.cs.beta[(size_t)s * row + i] = br;
+            a.cs.pi[(size_t)s * N + il] = (uint16_t)pi;
+            a.cs.d[(size_t)s * row + il] = dr;
+            a.cs.beta[(size_t)s * row + il] = br;
             if constexpr (NC == 2) {
-                a.cs.d[(size_t)s * row + N + i] = di;
-                a.cs.beta[(size_t)s * row + N + i] = bi;
+                a.cs.d[(size_t)s * row + N + il] = di;
+                a.cs.beta[(size_t)s * row + N + il] = bi;
             }
             if (a.maps) {
-                a.maps[((size_t)s * 2) * N + i] = (uint16_t)i;
-                a.maps[((size_t)s * 2 + 1) * N + i] = (uint16_t)pi;
+                a.maps[((size_t)s * 2) * N + il] = (uint16_t)il;
+                a.maps[((size_t)s * 2 + 1) * N + il] = (uint16_t)pi;
             }
         }
     }
@@ -476,39 +502,46 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
 // full group): db_t store ; lambda_t -> STS ; BARRIER ; lp = lambda_t[P_t[j]] (P_t[j]
 // read a step earlier) ; refill ; operands of step t-1 (D, e, h from the ring row, P) ;
 // lambda_{t-1} = e_{t-1} + conj(D_t) lp ; dD_t store ; this thread's g_t term -> tile.
-template <typename T, typename TE, int NC, bool PD, int NN>
+// SPC > 1 (N <= 64): SPC sequences of one head per CTA, as in k_fwd_seq.
+template <typename T, typename TE, int NC, bool PD, int NN, int SPC = 1, int GB = SEQ_G>
 __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq(SeqArgs a) {
     using SV = typename fused::SVal<NC>::type;
-    constexpr int G = SEQ_G;
+    constexpr int G = GB;
+    static_assert(32 % G == 0, "g_t is reduced every 32 steps: G must divide 32");
     constexpr int SVB = (int)sizeof(SV);
     extern __shared__ __align__(128) uint8_t smem[];
     const int N = NN ? NN : a.N, K = a.K, L = a.L, R = a.R;
-    const int j = threadIdx.x;
-    const int s = blockIdx.x, h = s % a.H;
-    const Layout Ly(N, K, R, G, NC, (int)sizeof(T), (int)sizeof(TE), PD, false, true, L);
+    const int jt = threadIdx.x;
+    const int h = blockIdx.x % a.H, pidx = blockIdx.x / a.H;
+    const int sub = (SPC > 1 && jt < SPC * N) ? jt / N : 0;
+    const int j = jt - sub * N;                           // this thread's source state
+    const int s = (pidx * SPC + sub) * a.H + h;
+    const Layout Ly(N, K, R, G, NC, (int)sizeof(T), (int)sizeof(TE), PD, false, true, L, SPC);
     uint8_t* ring = smem + Ly.ring;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Ly.bars);
-    char* xbc = reinterpret_cast<char*>(smem + Ly.x);
-    uint8_t* kb = smem + Ly.kb;
+    char* xbc = reinterpret_cast<char*>(smem + Ly.x + sub * Ly.xs);
+    uint8_t* kb = smem + Ly.kb + sub * Ly.kbs;
     uint16_t* prow = reinterpret_cast<uint16_t*>(smem + Ly.prow);
     float* dk = reinterpret_cast<float*>(smem + Ly.dk);
-    float* gs = reinterpret_cast<float*>(smem + Ly.gs);   // [32][N+1] g terms, then [32][NW] partials
+    float* gs = reinterpret_cast<float*>(smem + Ly.gs + sub * Ly.gss);   // [32][N+1] g terms, then [32][NW] partials
     const size_t row = (size_t)NC * N;
     const size_t seq0 = (size_t)s * L;
     const int ngroups = (L + G - 1) / G;
     const uint64_t pol = fused::policy_evict_first();
     const TE* ein = static_cast<const TE*>(a.bias);
-    for (int x = j; x < K * N; x += blockDim.x) prow[x] = (uint16_t)min((int)__ldg(a.dict_idx + (size_t)h * K * N + x), N - 1);
+    for (int x = jt; x < K * N; x += blockDim.x) prow[x] = (uint16_t)min((int)__ldg(a.dict_idx + (size_t)h * K * N + x), N - 1);
     if constexpr (PD)
-        for (int x = j; x < K * NC * N; x += blockDim.x) dk[x] = __ldg(a.diag_dict + (size_t)h * K * NC * N + x);
-    stage_k(a, kb, seq0, L);
-    if (j == 0) {
+        for (int x = jt; x < K * NC * N; x += blockDim.x) dk[x] = __ldg(a.diag_dict + (size_t)h * K * NC * N + x);
+    for (int q = 0; q < SPC; ++q) stage_k(a, smem + Ly.kb + q * Ly.kbs, (size_t)((pidx * SPC + q) * a.H + h) * L, L);
+    if (jt == 0) {
         for (int q = 0; q < 2 * R; ++q) fused::mbar_init(bars + q, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     const int ROWB = (int)(row * sizeof(T)), EROWB = (int)(row * sizeof(TE));
-    const int OFF_E = PD ? 0 : G * ROWB, OFF_H = OFF_E + G * EROWB;
+    // slot: [D rows of seq 0..SPC-1][e rows ...][h rows ...], G rows per sequence and stream
+    const int OFF_E = PD ? 0 : SPC * G * ROWB, OFF_H = OFF_E + SPC * G * EROWB;
+    const int SUB_D = sub * G * ROWB, SUB_E = sub * G * EROWB;
     // group g: times t_hi = L-1-gG down to t_lo; D_t at row t - t_lo, e_{t-1} and h_{t-1} likewise
     auto issue = [&](int g, int slot) {
         const int t_hi = L - 1 - g * G, t_lo = max(t_hi - G + 1, 0), len = t_hi - t_lo + 1;
@@ -516,15 +549,22 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq(SeqArgs a) {
         const int f_first = max(t_lo - 1, 0);                 // e_{t-1}, h_{t-1} rows needed for t >= 1
         const int f_cnt = max(0, t_hi - 1 - f_first + 1);
         const int f_off = f_first - (t_lo - 1);
-        fused::mbar_expect_tx(bars + slot, (uint32_t)((PD ? 0 : len * ROWB) + (ein ? f_cnt * EROWB : 0) + f_cnt * ROWB));
-        if constexpr (!PD) fused::tma_1d_hint(dst, static_cast<const T*>(a.diag) + (seq0 + t_lo) * row, len * ROWB, bars + slot, pol);
-        if (ein && f_cnt > 0)
-            fused::tma_1d_hint(dst + OFF_E + (size_t)f_off * EROWB, ein + (seq0 + f_first) * row, f_cnt * EROWB, bars + slot, pol);
-        if (f_cnt > 0)
-            fused::tma_1d_hint(dst + OFF_H + (size_t)f_off * ROWB, static_cast<const T*>(a.hsaved) + (seq0 + f_first) * row,
-                               f_cnt * ROWB, bars + slot, pol);
+        fused::mbar_expect_tx(bars + slot,
+                              (uint32_t)(SPC * ((PD ? 0 : len * ROWB) + (ein ? f_cnt * EROWB : 0) + f_cnt * ROWB)));
+        for (int q = 0; q < SPC; ++q) {
+            const size_t sq0 = (size_t)((pidx * SPC + q) * a.H + h) * L;
+            if constexpr (!PD)
+                fused::tma_1d_hint(dst + q * G * ROWB, static_cast<const T*>(a.diag) + (sq0 + t_lo) * row, len * ROWB,
+                                   bars + slot, pol);
+            if (ein && f_cnt > 0)
+                fused::tma_1d_hint(dst + OFF_E + q * G * EROWB + (size_t)f_off * EROWB, ein + (sq0 + f_first) * row,
+                                   f_cnt * EROWB, bars + slot, pol);
+            if (f_cnt > 0)
+                fused::tma_1d_hint(dst + OFF_H + q * G * ROWB + (size_t)f_off * ROWB,
+                                   static_cast<const T*>(a.hsaved) + (sq0 + f_first) * row, f_cnt * ROWB, bars + slot, pol);
+        }
     };
-    if (j >= N) {   // producer warp
+    if (jt >= SPC * N) {   // producer warp
         produce(bars, R, ngroups, issue);
         return;
     }
@@ -558,19 +598,19 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq(SeqArgs a) {
             Dr = dk[(size_t)k_ * row + j];
             Di = NC == 2 ? dk[(size_t)k_ * row + N + j] : 0.f;
         } else {
-            const T* Dp = reinterpret_cast<const T*>(sb_ + ro * ROWB);
+            const T* Dp = reinterpret_cast<const T*>(sb_ + SUB_D + ro * ROWB);
             Dr = ldact_s(Dp + j);
             Di = NC == 2 ? ldact_s(Dp + N + j) : 0.f;
         }
         if (t > 0) {
             if (ein) {
-                const TE* ep = reinterpret_cast<const TE*>(sb_ + OFF_E + ro * EROWB);
+                const TE* ep = reinterpret_cast<const TE*>(sb_ + OFF_E + SUB_E + ro * EROWB);
                 er = ldact_s(ep + j);
                 ei = NC == 2 ? ldact_s(ep + N + j) : 0.f;
             } else {
                 er = ei = 0.f;
             }
-            const T* hp = reinterpret_cast<const T*>(sb_ + OFF_H + ro * ROWB);
+            const T* hp = reinterpret_cast<const T*>(sb_ + OFF_H + SUB_D + ro * ROWB);
             hr = ldact_s(hp + j);
             hi = NC == 2 ? ldact_s(hp + N + j) : 0.f;
         } else {
@@ -595,14 +635,14 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq(SeqArgs a) {
         const float Dcr = Dr, Dci = Di, ecr = er, eci = ei, hcr = hr, hci = hi;
         uint32_t la;   // shared address of lambda_t[P_t[j]], computed before the barrier
         asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(la) : "r"(p), "r"(SVB), "r"(fused::smem_u32(lbc)));
-        compute_sync(N);
+        compute_sync(SPC * N);
         SV lpv;
         {
             float re, im;
             lds_sv<NC>(la, re, im);
             lpv = fused::mk<NC>(re, im);
         }
-        if (rr == 0 && j == 0 && g >= 1) {   // every compute thread is done with the previous group's slot
+        if (rr == 0 && jt == 0 && g >= 1) {   // every compute thread is done with the previous group's slot
             mbar_arrive(bars + R + (slot == 0 ? R - 1 : slot - 1));
         }
         // g_t of the previous 32 steps (v = 8 g + rr, so only the first step of every 4th group)
@@ -622,13 +662,13 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq(SeqArgs a) {
             acc = (a0 + a1) + (a2 + a3);
             float* red = gs + (size_t)32 * (N + 1);
             red[part * 32 + q] = acc;
-            compute_sync(N);
+            compute_sync(SPC * N);
             if (j < 32) {
                 float tot = 0.f;
                 for (int x = 0; x < NP; ++x) tot += red[x * 32 + j];
                 a.gsel[seq0 + (L - 1 - (v - 32 + j))] = tot;
             }
-            compute_sync(N);
+            compute_sync(SPC * N);
         }
         // operands of step t-1 (consumed a step later)
         if (inner && rr < G - 1) {
@@ -674,7 +714,7 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq(SeqArgs a) {
             for (int rr = 0; rr <= t_hi - t_lo; ++rr) step(rr, g, t_hi - rr, t_lo, false);
         }
     }
-    compute_sync(N);
+    compute_sync(SPC * N);
     if (a.gsel) {   // the last (L % 32 or 32) steps
         const int v0 = ((L - 1) / 32) * 32;
         for (int x = j; x < 32 && v0 + x < L; x += N) {

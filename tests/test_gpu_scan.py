@@ -411,3 +411,38 @@ def test_seq_no_maps_per_dict_and_overflow(P, monkeypatch):
     Dz = O.gather_D_per_dict(O.planes_to_complex(inp["diag"]), inp["kstar"])
     h = O.scan_forward(Pm, Dz, O.planes_to_complex(inp["bias"]), O.planes_to_complex(inp["h0"]))
     check("h", cpx(f["h"]), h, 1e-4)
+
+
+PAIRED_CASES = [
+    # B, H, L, N, K, c, bf16: N = 64, B even, B*H > #SMs -> two sequences of a head per CTA
+    (20, 8, 300, 64, 48, 1, True),
+    (20, 8, 77, 64, 16, 2, False),
+    (38, 4, 129, 64, 5, 1, False),
+]
+
+
+@pytest.mark.parametrize("case", PAIRED_CASES, ids=[str(c) for c in PAIRED_CASES])
+def test_seq_paired_sequences_per_cta(P, case, monkeypatch):
+    """Single-chunk kernels with two sequences (batch rows b, b+1) of one head per CTA (the config-4
+    launch shape): every sequence against the oracle, and bitwise run-to-run repeatability."""
+    monkeypatch.delenv("PDSSM_PATH", raising=False)
+    B, H, L, N, K, c, bf16 = case
+    inp = synth.scan_inputs(B, H, L, N, K, c, seed=B + L, dh=True, bf16=bf16)
+    d = to_dev(inp, bf16)
+    f = P.scan_fwd(d["kstar"], d["dict_idx"], d["diag"], d["bias"])
+    assert f["tau"] == L
+    db, dD, g, _ = P.scan_bwd(d["kstar"], d["dict_idx"], d["diag"], f["h"], f["chunk_state"], f["dims"], dh=d["dh"],
+                              want_dh0=False)
+    torch.cuda.synchronize()
+    Pm = O.gather_P(inp["dict_idx"], inp["kstar"])
+    Dz, bz, e = (O.planes_to_complex(inp[k]) for k in ("diag", "bias", "dh"))
+    h = O.scan_forward(Pm, Dz, bz)
+    tol = TOL["bf16" if bf16 else "f32"]
+    check("paired_h", cpx(f["h"]), h, tol)
+    db_r, dD_r, g_r, _ = O.scan_backward(Pm, Dz, saved_states(h, c, bf16), e)
+    check("paired_db", cpx(db), db_r, tol)
+    check("paired_dD", cpx(dD), dD_r, tol)
+    check("paired_g", g.cpu().numpy(), g_r, tol)
+    f2 = P.scan_fwd(d["kstar"], d["dict_idx"], d["diag"], d["bias"])
+    torch.cuda.synchronize()
+    assert torch.equal(f["h"], f2["h"])
