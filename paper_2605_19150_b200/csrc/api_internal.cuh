@@ -16,6 +16,7 @@
 
 #include "pdssm_common.cuh"
 #include "k_scan_seq.cuh"   // + k_scan_fwd.cuh, k_scan_fused.cuh (Args and Layout types)
+#include "k_scan_bwd.cuh"   // reduce_dict_ws_bytes
 
 namespace pdssm {
 namespace api {
@@ -132,8 +133,9 @@ inline size_t ws_bytes_g(const Geo& g, int op) {
                    fused_plan_bytes(g.H, g.K, g.N) + fused_ctrl_bytes(g.S, g.C, g.H) + seq_plan_bytes(g);
         case PDSSM_OP_BWD:
             return 2 * cs_f_bytes(g) + (g.P > 0 ? seq_f_bytes(g) + readout_w_bytes(g) : 0) +
-                   (g.diag_mode == PDSSM_DIAG_PER_DICT ? seq_f_bytes(g) : 0) + fused_ctrl_bytes(g.S, g.C, g.H) +
-                   plan_bytes(g);
+                   (g.diag_mode == PDSSM_DIAG_PER_DICT ? seq_f_bytes(g) + reduce_dict_ws_bytes(g.S, g.L, g.K, g.nc * g.N)
+                                                        : 0) +
+                   fused_ctrl_bytes(g.S, g.C, g.H) + plan_bytes(g);
         case PDSSM_OP_READOUT:
             return readout_w_bytes(g);
         case PDSSM_OP_SOFT: {   // s [H][B L][Kp] and Mt [H][N^2][Kp] in the act dtype

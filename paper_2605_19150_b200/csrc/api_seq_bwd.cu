@@ -12,7 +12,9 @@ pdssm_status bwd_seq(const Geo& g, seq::SeqArgs& sa, cudaStream_t st) {
     return with_act(g.dtype, [&](auto tv) {
         using T = decltype(tv);
         using TEE = typename std::conditional<std::is_same<TE, void>::value, T, TE>::type;
-        int spc = g.N == 64 ? seq_spc(g) : 1;   // paired sequences per CTA (see seq_spc)
+        // paired sequences per CTA (seq_spc) measured slower for the backward at config 4 (0.86 vs
+        // 0.72 ms: 16 compute warps per SM make it issue-bound); kept selectable via PDSSM_SEQ_PAIR_BWD
+        int spc = (g.N == 64 && getenv("PDSSM_SEQ_PAIR_BWD")) ? seq_spc(g) : 1;
         sa.R = seq_ring(g, true, false, sizeof(TEE), spc);
         if (spc > 1 && sa.R < 2) {
             spc = 1;

@@ -351,23 +351,61 @@ __global__ void k_bwd_prepare_e(const T* __restrict__ dh, const T* __restrict__ 
 }
 
 // PER_DICT: ddiag[h][k][pl][j] = sum over (b, t) with k*[b,h,t] = k of dD (fixed order).
-template <int NC>
-__global__ void k_bwd_reduce_dict(const uint8_t* __restrict__ kstar, const float* __restrict__ dD,
-                                  float* __restrict__ ddiag, int B, int H, int L, int N, int K) {
-    const int e = blockIdx.x;   // h*K + k
-    const int h = e / K, k = e % K;
-    for (int q = threadIdx.x; q < NC * N; q += blockDim.x) {
-        float acc = 0.f;
-        for (int b = 0; b < B; ++b) {
-            const size_t s = (size_t)b * H + h;
-            for (int t = 0; t < L; ++t) {
-                int kk = __ldg(kstar + s * L + t);
-                if (kk >= K) kk = K - 1;
-                if (kk == k) acc += dD[(s * L + t) * NC * N + q];
-            }
+// PER_DICT: dD_k = sum over the steps that selected entry k of the per-step dD_t (f32 scratch),
+// deterministically in two stages.  Stage 1: one CTA per (sequence, slice of RD_SLICE steps,
+// tile of RD_COLS columns of the c N plane); thread q owns column q and accumulates per entry
+// in shared memory (its own column: no conflicts), ascending t.  Stage 2: one thread per (h, k,
+// column) sums the partials over (b, slice) in ascending order.
+constexpr int RD_SLICE = 512;
+constexpr int RD_COLS = 128;
+
+inline size_t reduce_dict_ws_bytes(int64_t S, int64_t L, int64_t K, int64_t cN) {
+    const int64_t ns = (L + RD_SLICE - 1) / RD_SLICE;
+    return (((size_t)S * ns * K * cN * 4) + 255) & ~(size_t)255;
+}
+
+static __global__ void __launch_bounds__(RD_COLS) k_reduce_dict_partial(const uint8_t* __restrict__ kstar,
+                                                                 const float* __restrict__ dD,
+                                                                 float* __restrict__ part, int L, int K, int cN) {
+    extern __shared__ float acc[];   // [K][RD_COLS]
+    const int ns = (L + RD_SLICE - 1) / RD_SLICE;
+    const int ntile = (cN + RD_COLS - 1) / RD_COLS;
+    const int tile = blockIdx.x % ntile;
+    const int sl = (blockIdx.x / ntile) % ns;
+    const size_t s = blockIdx.x / ((size_t)ntile * ns);
+    const int q = tile * RD_COLS + threadIdx.x;
+    const bool act = q < cN;
+    for (int k = 0; k < K; ++k) acc[k * RD_COLS + threadIdx.x] = 0.f;
+    const int t0 = sl * RD_SLICE, t1 = min(t0 + RD_SLICE, L);
+    if (act) {
+        const float* src = dD + ((size_t)s * L + t0) * cN + q;
+        for (int t = t0; t < t1; ++t, src += cN) {
+            int k = __ldg(kstar + (size_t)s * L + t);
+            if (k >= K) k = K - 1;
+            acc[k * RD_COLS + threadIdx.x] += __ldg(src);
         }
-        ddiag[(size_t)e * NC * N + q] = acc;
+    }
+    if (act) {
+        float* dst = part + (((size_t)s * ns + sl) * K) * cN + q;
+        for (int k = 0; k < K; ++k) dst[(size_t)k * cN] = acc[k * RD_COLS + threadIdx.x];
     }
 }
+
+static __global__ void k_reduce_dict_final(const float* __restrict__ part, float* __restrict__ ddiag, int B, int H, int L, int K,
+                                    int cN) {
+    const int ns = (L + RD_SLICE - 1) / RD_SLICE;
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // over H * K * cN
+    if (idx >= (int64_t)H * K * cN) return;
+    const int q = (int)(idx % cN);
+    const int k = (int)((idx / cN) % K);
+    const int h = (int)(idx / ((int64_t)cN * K));
+    float acc = 0.f;
+    for (int b = 0; b < B; ++b) {
+        const size_t s = (size_t)b * H + h;
+        for (int sl = 0; sl < ns; ++sl) acc += part[(((size_t)s * ns + sl) * K + k) * cN + q];
+    }
+    ddiag[idx] = acc;
+}
+
 
 }  // namespace pdssm

@@ -76,6 +76,21 @@ pdssm_status fwd_three_phase(const Geo& g, const uint8_t* kstar, const uint16_t*
     });
 }
 
+// PER_DICT dD_k: two-stage deterministic reduction of the per-step f32 dD_t (k_scan_bwd.cuh)
+pdssm_status reduce_dict(const Geo& g, const uint8_t* kstar, const float* dDbuf, float* ddiag, float* part,
+                         cudaStream_t st) {
+    const int cN = g.nc * (int)g.N;
+    const int64_t ns = ceil_div(g.L, RD_SLICE), ntile = ceil_div(cN, RD_COLS);
+    const size_t sm = (size_t)g.K * RD_COLS * 4;
+    pdssm_status r = set_smem((const void*)k_reduce_dict_partial, sm);
+    if (r) return r;
+    k_reduce_dict_partial<<<(unsigned)(g.S * ns * ntile), RD_COLS, sm, st>>>(kstar, dDbuf, part, (int)g.L, (int)g.K, cN);
+    if ((r = cuda_check("reduce_dict_partial"))) return r;
+    const int64_t n = g.H * g.K * cN;
+    k_reduce_dict_final<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(part, ddiag, (int)g.B, (int)g.H, (int)g.L, (int)g.K, cN);
+    return cuda_check("reduce_dict_final");
+}
+
 }  // namespace api
 }  // namespace pdssm
 
@@ -302,6 +317,8 @@ pdssm_status pdssm_scan_bwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
     float* ebuf = g.P > 0 ? bump.take<float>(seq_f_bytes(g)) : nullptr;
     void* wbuf = g.P > 0 ? bump.take<char>(readout_w_bytes(g)) : nullptr;
     float* dDbuf = g.diag_mode == PDSSM_DIAG_PER_DICT ? bump.take<float>(seq_f_bytes(g)) : nullptr;
+    float* rdpart = g.diag_mode == PDSSM_DIAG_PER_DICT
+                        ? bump.take<float>(reduce_dict_ws_bytes(g.S, g.L, g.K, g.nc * g.N)) : nullptr;
     uint32_t* ctrl = bump.take<uint32_t>(fused_ctrl_bytes(g.S, g.C, g.H));
     uint16_t* pstart = bump.take<uint16_t>((size_t)g.H * g.K * (g.N + 1) * 2);   // recompute: forward plan
     uint16_t* psrc = bump.take<uint16_t>((size_t)g.H * g.K * g.N * 2);
@@ -332,9 +349,7 @@ pdssm_status pdssm_scan_bwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
         if (g.diag_mode == PDSSM_DIAG_PER_DICT) {
             r = with_nc(g.nc, [&](auto ncv) {
                 constexpr int NC = decltype(ncv)::value;
-                k_bwd_reduce_dict<NC><<<(unsigned)(g.H * g.K), 256, 0, st>>>(
-                    kstar, dDbuf, static_cast<float*>(ddiag), (int)g.B, (int)g.H, (int)g.L, (int)g.N, (int)g.K);
-                return cuda_check("bwd_reduce_dict");
+                return reduce_dict(g, kstar, dDbuf, static_cast<float*>(ddiag), rdpart, st);
             });
         }
         return r;
@@ -356,9 +371,7 @@ pdssm_status pdssm_scan_bwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
         if (g.diag_mode == PDSSM_DIAG_PER_DICT) {
             r = with_nc(g.nc, [&](auto ncv) {
                 constexpr int NC = decltype(ncv)::value;
-                k_bwd_reduce_dict<NC><<<(unsigned)(g.H * g.K), 256, 0, st>>>(
-                    kstar, dDbuf, static_cast<float*>(ddiag), (int)g.B, (int)g.H, (int)g.L, (int)g.N, (int)g.K);
-                return cuda_check("bwd_reduce_dict");
+                return reduce_dict(g, kstar, dDbuf, static_cast<float*>(ddiag), rdpart, st);
             });
         }
         return r;
@@ -396,10 +409,7 @@ pdssm_status pdssm_scan_bwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
                             (int)g.H, (int)g.L, (int)g.N, (int)g.K, g.tau, g.C);
                         if ((rr = cuda_check("bwd_phaseC_rc"))) return rr;
                         if (PD) {
-                            k_bwd_reduce_dict<NC><<<(unsigned)(g.H * g.K), 256, 0, st>>>(
-                                kstar, dDbuf, static_cast<float*>(ddiag), (int)g.B, (int)g.H, (int)g.L, (int)g.N,
-                                (int)g.K);
-                            if ((rr = cuda_check("bwd_reduce_dict"))) return rr;
+                            if ((rr = reduce_dict(g, kstar, dDbuf, static_cast<float*>(ddiag), rdpart, st))) return rr;
                         }
                         return PDSSM_OK;
                     }
@@ -411,9 +421,7 @@ pdssm_status pdssm_scan_bwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
                         (int)g.K, g.tau, g.C);
                     if ((rr = cuda_check("bwd_phaseC"))) return rr;
                     if (PD) {
-                        k_bwd_reduce_dict<NC><<<(unsigned)(g.H * g.K), 256, 0, st>>>(
-                            kstar, dDbuf, static_cast<float*>(ddiag), (int)g.B, (int)g.H, (int)g.L, (int)g.N, (int)g.K);
-                        if ((rr = cuda_check("bwd_reduce_dict"))) return rr;
+                        if ((rr = reduce_dict(g, kstar, dDbuf, static_cast<float*>(ddiag), rdpart, st))) return rr;
                     }
                     return PDSSM_OK;
                 };

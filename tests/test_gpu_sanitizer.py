@@ -1,0 +1,48 @@
+"""compute-sanitizer over small invocations of every kernel family (tests/sanitize_driver.py):
+racecheck (shared-memory hazards: the exchange rows, the TMA rings, the g tiles), synccheck
+(barrier use: named barriers, __syncwarp, mbarrier rings) and memcheck (out-of-bounds / misaligned
+accesses).  The paper argues its barrier placement in prose only; this checks
+this build's synchronisation with a tool."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+FAMILIES = ["seq", "seq_paired", "fused", "generic", "gemm", "surrogate"]
+TOOLS = ["memcheck", "racecheck", "synccheck"]
+
+
+def _sanitizer():
+    for c in (shutil.which("compute-sanitizer"), "/usr/local/cuda/bin/compute-sanitizer"):
+        if c and os.path.exists(c):
+            return c
+    return None
+
+
+@pytest.mark.parametrize("tool", TOOLS)
+@pytest.mark.parametrize("family", FAMILIES)
+def test_compute_sanitizer(tool, family):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    cs = _sanitizer()
+    if cs is None:
+        pytest.skip("compute-sanitizer not found")
+    cmd = [cs, "--tool", tool, "--error-exitcode", "17", "--print-limit", "20"]
+    if tool == "racecheck":
+        cmd += ["--racecheck-report", "hazard"]
+    cmd += [sys.executable, os.path.join(ROOT, "tests", "sanitize_driver.py"), family]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1500, cwd=ROOT)
+    out = r.stdout + r.stderr
+    log = os.environ.get("PDSSM_SANITIZER_LOG")
+    if log:
+        with open(log, "a") as f:
+            f.write(f"==== {tool} {family} rc={r.returncode}\n" + out[-3000:] + "\n")
+    assert r.returncode == 0, out[-4000:]
+    assert "ERROR SUMMARY: 0 errors" in out, out[-4000:]
+    assert f"done {family}" in out

@@ -422,10 +422,16 @@ PAIRED_CASES = [
 
 
 @pytest.mark.parametrize("case", PAIRED_CASES, ids=[str(c) for c in PAIRED_CASES])
-def test_seq_paired_sequences_per_cta(P, case, monkeypatch):
+@pytest.mark.parametrize("pair_bwd", [False, True], ids=["bwd_single", "bwd_paired"])
+def test_seq_paired_sequences_per_cta(P, case, pair_bwd, monkeypatch):
     """Single-chunk kernels with two sequences (batch rows b, b+1) of one head per CTA (the config-4
-    launch shape): every sequence against the oracle, and bitwise run-to-run repeatability."""
+    launch shape of the forward; the paired backward is opt-in, PDSSM_SEQ_PAIR_BWD): every sequence
+    against the oracle, and bitwise run-to-run repeatability."""
     monkeypatch.delenv("PDSSM_PATH", raising=False)
+    if pair_bwd:
+        monkeypatch.setenv("PDSSM_SEQ_PAIR_BWD", "1")
+    else:
+        monkeypatch.delenv("PDSSM_SEQ_PAIR_BWD", raising=False)
     B, H, L, N, K, c, bf16 = case
     inp = synth.scan_inputs(B, H, L, N, K, c, seed=B + L, dh=True, bf16=bf16)
     d = to_dev(inp, bf16)
