@@ -1325,16 +1325,14 @@ __global__ void __launch_bounds__(Layout<T, NC, NPL, PD, true, (int)sizeof(TE)>:
 #pragma unroll
             for (int u = 0; u < NPL; ++u) { nr[u] = mre[u]; ni[u] = mim[u]; }
             applyT(pk, dr, di, bpre, bpim, nr, ni);
-            if (c > 0) {
-                const size_t cp = ci - 1;
-                vst_f<NPL>(a.mu + cp * row + lane * NPL, nr);
-                if constexpr (NC == 2) vst_f<NPL>(a.mu + cp * row + N + lane * NPL, ni);
-                __threadfence();
-                __syncwarp();
-                if (lane == 0) st_release(flag_ptr(a, ci), 2u);
-            }
+            const size_t cp = ci - 1;
+            vst_f<NPL>(a.mu + cp * row + lane * NPL, nr);
+            if constexpr (NC == 2) vst_f<NPL>(a.mu + cp * row + N + lane * NPL, ni);
+            __threadfence();
             __syncwarp();
+            if (lane == 0) st_release(flag_ptr(a, ci), 2u);
         }
+        __syncwarp();   // the exchange-row reads above (applyT) precede the replay's writes
         // ---------------- Phase C': replay, emit db, dD, g
         {
             float er0[NPL], ei0[NPL];

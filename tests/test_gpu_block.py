@@ -1,0 +1,65 @@
+"""NEXT-4: the Flash PD-SSM block (paper_2605_19150_b200/block.py).
+
+* The autograd function of the mixer (selection + sparsification + scan with Prop. 2's
+  straight-through gradients) against the float64 oracle chain: select ->
+  sparsify -> scan forward -> scan backward -> selector_grad / dictionary_outer / dictionary_grad,
+  with the selector's d(logits) pushed to S and u by the chain rule.
+* A few hundred training steps on parity reduce the loss (the Table 1 pipeline runs end to end)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from parity import check
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def blk():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2605_19150_b200 import block
+    return block
+
+
+def test_mixer_function_surrogate_gradients(blk):
+    rng = np.random.default_rng(3)
+    B, L, d, H, K, N, T = 2, 37, 64, 2, 5, 32, 0.7
+    u = rng.normal(size=(B, L, d)).astype(np.float32)
+    S = (rng.uniform(-1, 1, size=(H, K, d)) / 8).astype(np.float32)
+    M = (rng.uniform(-1, 1, size=(H, K, N, N)) / np.sqrt(N)).astype(np.float32)
+    mag = 1 / (1 + np.exp(-rng.normal(2, 1, size=(B, H, L, N))))
+    th = rng.uniform(-np.pi, np.pi, size=(B, H, L, N))
+    diag = np.stack([mag * np.cos(th), mag * np.sin(th)], axis=3).astype(np.float32)
+    bias = rng.normal(size=(B, H, L, 2, N)).astype(np.float32)
+    dh = rng.normal(size=(B, H, L, 2, N)).astype(np.float32)
+    cu = lambda a: torch.from_numpy(a).cuda().requires_grad_(True)
+    ut, St, Mt, Dt, bt = (cu(a) for a in (u, S, M, diag, bias))
+    h, kstar = blk._FlashPDSSMFn.apply(ut, St, Mt, Dt, bt, T)
+    (h * torch.from_numpy(dh).cuda()).sum().backward()
+    torch.cuda.synchronize()
+    # oracle chain (float64)
+    k_ref, logits = O.select(u.astype(np.float64), S.astype(np.float64))
+    assert np.array_equal(kstar.cpu().numpy(), k_ref)        # float margins are wide here; bit-exact
+    di = O.sparsify(M.astype(np.float64))
+    Pm = O.gather_P(di, k_ref)
+    Dz, bz, e = (O.planes_to_complex(a) for a in (diag, bias, dh))
+    hz = O.scan_forward(Pm, Dz, bz)
+    check("block_h", O.planes_to_complex(h.detach().cpu().numpy()), hz, 1e-4)
+    lam, dD_r, g_r, _ = O.scan_backward(Pm, Dz, hz, e)
+    check("block_db", O.planes_to_complex(bt.grad.cpu().numpy()), lam, 1e-4)
+    check("block_dD", O.planes_to_complex(Dt.grad.cpu().numpy()), dD_r, 1e-4)
+    dlog = O.selector_grad(logits, k_ref, g_r, T)
+    check("block_dS", St.grad.cpu().numpy(), np.einsum("bhtk,btd->hkd", dlog, u.astype(np.float64)), 1e-4, bh_axes=None)
+    check("block_du", ut.grad.cpu().numpy(), np.einsum("bhtk,hkd->btd", dlog, S.astype(np.float64)), 1e-4, bh_axes=None)
+    G = O.dictionary_outer(k_ref, lam, Dz, hz, K)
+    check("block_dM", Mt.grad.cpu().numpy(), O.dictionary_grad(M.astype(np.float64), G, T), 1e-4, bh_axes=None)
+
+
+def test_parity_training_reduces_loss(blk):
+    from paper_2605_19150_b200 import train_fsa
+    r = train_fsa.train_task("parity", steps=300, batch=64, max_len=16, seed=0)
+    assert np.isfinite(r["final_train_loss"])
+    assert r["final_train_loss"] < 0.6          # chance level is ln 2 = 0.693
+    assert set(r["val_acc_by_len"]) == set(train_fsa.EVAL_LENGTHS)
