@@ -74,14 +74,16 @@ bool tc_operands_ok(const Geo& g, std::initializer_list<const void*> ptrs) {
 template <typename T>
 constexpr int tc_stages() { return std::is_same<T, float>::value ? 2 : 4; }
 
-template <typename T, class Epi>
+template <typename T, class Epi, bool BPRE = false>
 pdssm_status launch_tc_maps(const CUtensorMap& mA, const CUtensorMap& mB, int64_t kdim, int bn, tc::TileMap tm,
-                            dim3 grid, Epi epi, cudaStream_t st, const char* what) {
+                            dim3 grid, Epi epi, cudaStream_t st, const char* what, const CUtensorMap* mBlo = nullptr) {
     constexpr bool SPLIT = std::is_same<T, float>::value;
-    constexpr int STAGES = tc_stages<T>();
+    // pre-split weights (bn <= 128): three stages of (A hi/lo + B hi/lo) slabs fit
+    constexpr int STAGES = BPRE ? 3 : tc_stages<T>();
     using SM = tc::Smem<T, STAGES, SPLIT>;
-    const size_t smem = SM::bytes(256);   // sized for the largest tile: one attribute per instantiation
-    auto kern = tc::k_gemm_tc<T, STAGES, SPLIT, Epi>;
+    const size_t smem = SM::bytes(BPRE ? 128 : 256);   // sized for the largest tile: one attribute per instantiation
+    if (BPRE && bn > 128) return fail(PDSSM_ERR_UNSUPPORTED, "%s: pre-split weights need bn <= 128", what);
+    auto kern = tc::k_gemm_tc<T, STAGES, SPLIT, Epi, BPRE>;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
@@ -90,7 +92,7 @@ pdssm_status launch_tc_maps(const CUtensorMap& mA, const CUtensorMap& mB, int64_
     const tc::TileGrid tg{(int)grid.x, (int)grid.y, (int)grid.z};
     const int ntiles = tg.gx * tg.gy * tg.gz;
     const int nctas = ntiles < num_sms_dev() ? ntiles : num_sms_dev();   // persistent
-    kern<<<nctas, tc::THREADS, SM::bytes(bn), st>>>(mA, mB, nk, bn, tm, tg, epi);
+    kern<<<nctas, tc::THREADS, SM::bytes(bn), st>>>(mA, mB, mBlo ? *mBlo : mB, nk, bn, tm, tg, epi);
     return cuda_check(what);
 }
 
@@ -108,9 +110,11 @@ pdssm_status launch_tc(const Geo& g, const void* A, int64_t rows_a, const void* 
 
 // readout weights, act dtype: Cp[h][p][(c,n)] (y = Cp . h) and CT[h][(c,n)][p] (e = CT . dy),
 // both carrying the sign of Re(C h) = C_re h_re - C_im h_im
+// With Cp_lo (fp32 only) Cp receives the tf32 hi part and Cp_lo the rest (the 3xTF32 split of the
+// GEMM, done once here instead of per tile: k_gemm_tc BPRE).
 template <typename T>
 __global__ void k_readout_weights(const float* __restrict__ C, T* __restrict__ Cp, T* __restrict__ CT, int H, int nc,
-                                  int P, int N) {
+                                  int P, int N, float* __restrict__ Cp_lo = nullptr) {
     const int64_t total = (int64_t)H * nc * P * N;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int n = (int)(i % N);
@@ -119,7 +123,13 @@ __global__ void k_readout_weights(const float* __restrict__ C, T* __restrict__ C
         const int h = (int)(i / ((int64_t)N * P * nc));
         const float v = c == 0 ? C[i] : -C[i];
         const int cN = nc * N;
-        if (Cp) stact(Cp + ((size_t)h * P + p) * cN + c * N + n, v);
+        if (Cp && Cp_lo) {
+            const float vh = __uint_as_float(tc::tf32_rna(v));
+            Cp[((size_t)h * P + p) * cN + c * N + n] = vh;
+            Cp_lo[((size_t)h * P + p) * cN + c * N + n] = v - vh;
+        } else if (Cp) {
+            stact(Cp + ((size_t)h * P + p) * cN + c * N + n, v);
+        }
         if (CT) stact(CT + ((size_t)h * cN + c * N + n) * P + p, v);
     }
 }
@@ -135,17 +145,27 @@ bool tc_readout_ok(const Geo& g, std::initializer_list<const void*> ptrs) {
 }
 
 // y[b][t][h][p] = sum_w Cp[h][p][w] h[b][h][t][w]  (A: 3-D (cN, L, S) map, z = sequence)
+// fp32 with P <= 128: the weights come pre-split (Cp_lo, k_readout_weights) and the GEMM splits
+// only the states (k_gemm_tc BPRE, three stages)
 template <typename T>
-pdssm_status readout_tc(const Geo& g, const T* hseq, const T* Cp, T* y, cudaStream_t st) {
+pdssm_status readout_tc(const Geo& g, const T* hseq, const T* Cp, T* y, cudaStream_t st, const float* Cp_lo = nullptr) {
     const int64_t cN = g.nc * g.N;
+    const bool pre = std::is_same<T, float>::value && Cp_lo != nullptr && g.P <= 128;
     const int bn = (int)(g.P < 256 ? g.P : 256);
-    CUtensorMap mA, mB;
+    CUtensorMap mA, mB, mBl;
     const int64_t da[3] = {cN, g.L, g.S};
     const int64_t sa[2] = {cN * (int64_t)sizeof(T), g.L * cN * (int64_t)sizeof(T)};
-    if (!make_map3(&mA, hseq, sizeof(T), da, sa, tc::BM, 1) || !make_kmajor_map(&mB, Cp, sizeof(T), cN, g.H * g.P, bn))
+    if (!make_map3(&mA, hseq, sizeof(T), da, sa, tc::BM, 1) || !make_kmajor_map(&mB, Cp, sizeof(T), cN, g.H * g.P, bn) ||
+        (pre && !make_kmajor_map(&mBl, Cp_lo, sizeof(T), cN, g.H * g.P, bn)))
         return fail(PDSSM_ERR_CUDA, "readout_tc: cuTensorMapEncodeTiled failed");
     const int tiles = (int)ceil_div(g.L, tc::BM);
     dim3 grid((unsigned)(tiles * g.S), (unsigned)ceil_div(g.P, bn));
+    if constexpr (std::is_same<T, float>::value) {
+        if (pre)
+            return launch_tc_maps<T, tc::EpiReadout<T>, true>(mA, mB, cN, bn, tc::TileMap{1, tiles, (int)g.H, (int)g.P},
+                                                              grid, tc::EpiReadout<T>{y, (int)g.L, (int)g.H, (int)g.P}, st,
+                                                              "readout_tc", &mBl);
+    }
     return launch_tc_maps<T>(mA, mB, cN, bn, tc::TileMap{1, tiles, (int)g.H, (int)g.P}, grid,
                              tc::EpiReadout<T>{y, (int)g.L, (int)g.H, (int)g.P}, st, "readout_tc");
 }
@@ -198,11 +218,12 @@ pdssm_status readout_run(const Geo& g, const void* hout, const float* C_opt, voi
         using T = decltype(tv);
         if (tc_readout_ok(g, {hout, y_opt, wbuf})) {
             T* Cp = static_cast<T*>(wbuf);
+            float* Cl = readout_lo_part(g, wbuf);
             k_readout_weights<T><<<(unsigned)ceil_div(g.H * g.nc * g.P * g.N, 256), 256, 0, st>>>(
-                C_opt, Cp, nullptr, (int)g.H, (int)g.nc, (int)g.P, (int)g.N);
+                C_opt, Cp, nullptr, (int)g.H, (int)g.nc, (int)g.P, (int)g.N, Cl);
             pdssm_status rr = cuda_check("readout_weights");
             if (rr) return rr;
-            return readout_tc<T>(g, static_cast<const T*>(hout), Cp, static_cast<T*>(y_opt), st);
+            return readout_tc<T>(g, static_cast<const T*>(hout), Cp, static_cast<T*>(y_opt), st, Cl);
         }
         return with_nc(g.nc, [&](auto ncv) {
             constexpr int NC = decltype(ncv)::value;
@@ -381,11 +402,12 @@ pdssm_status pdssm_readout(const void* h, const float* C, void* y, const pdssm_d
         using T = decltype(tv);
         if (tc_readout_ok(g, {h, y, ws})) {
             T* Cp = static_cast<T*>(ws);
+            float* Cl = readout_lo_part(g, ws);
             k_readout_weights<T><<<(unsigned)ceil_div(g.H * g.nc * g.P * g.N, 256), 256, 0, st>>>(
-                C, Cp, nullptr, (int)g.H, (int)g.nc, (int)g.P, (int)g.N);
+                C, Cp, nullptr, (int)g.H, (int)g.nc, (int)g.P, (int)g.N, Cl);
             pdssm_status rr = cuda_check("readout_weights");
             if (rr) return rr;
-            return readout_tc<T>(g, static_cast<const T*>(h), Cp, static_cast<T*>(y), st);
+            return readout_tc<T>(g, static_cast<const T*>(h), Cp, static_cast<T*>(y), st, Cl);
         }
         return with_nc(g.nc, [&](auto ncv) {
             constexpr int NC = decltype(ncv)::value;

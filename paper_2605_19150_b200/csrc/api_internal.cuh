@@ -109,7 +109,15 @@ inline size_t seq_wm_bytes(const Geo& g) { return align256((size_t)g.H * g.K * (
 inline size_t seq_ovf_bytes(const Geo& g) { return align256((size_t)g.H * g.K); }
 inline size_t seq_plan_bytes(const Geo& g) { return seq_rec_bytes(g) + seq_wm_bytes(g) + seq_ovf_bytes(g); }
 // readout weights staged in act dtype (Cp or CT), H*P*c*N elements
-inline size_t readout_w_bytes(const Geo& g) { return g.P > 0 ? align256((size_t)g.H * g.P * g.nc * g.N * g.act) : 0; }
+inline size_t readout_w_bytes(const Geo& g) {   // fp32: hi part + tf32 lo part (pre-split weights)
+    return g.P > 0 ? align256((size_t)g.H * g.P * g.nc * g.N * g.act) * (g.act == 4 ? 2 : 1) : 0;
+}
+// the lo part of the pre-split fp32 readout weights inside the readout workspace (else NULL)
+inline float* readout_lo_part(const Geo& g, void* wbuf) {
+    return g.act == 4 && g.P <= 128 ? reinterpret_cast<float*>(static_cast<char*>(wbuf) +
+                                                                 align256((size_t)g.H * g.P * g.nc * g.N * 4))
+                                    : nullptr;
+}
 inline size_t seq_act_bytes(const Geo& g) { return align256((size_t)g.S * g.L * g.nc * g.N * g.act); }
 inline int npad8(int64_t N) { return (int)((N + 7) & ~7); }
 inline size_t summary_block_bytes(const Geo& g) { return (size_t)npad8(g.N) * 2 + (size_t)2 * g.nc * g.N * 4; }

@@ -472,10 +472,14 @@ struct TileGrid {
     int gx, gy, gz;   // tiles along the A rows (x), the output columns (y), the z batch
 };
 
-template <typename T, int STAGES, bool SPLIT, class Epi>
+// BPRE (with SPLIT): the weights B arrive pre-split in global memory (mB = tf32 hi part, mBlo = the
+// lo part, written once per call by the host path), so the converter warps split only the A rows
+// of each slab -- half the shared-memory traffic of the split (readout: B = the readout weights).
+template <typename T, int STAGES, bool SPLIT, class Epi, bool BPRE = false>
 __global__ void __launch_bounds__(THREADS, 1)
-    k_gemm_tc(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, int nk, int bn, TileMap tm,
-              TileGrid tg, Epi epi) {
+    k_gemm_tc(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB,
+              const __grid_constant__ CUtensorMap mBlo, int nk, int bn, TileMap tm, TileGrid tg, Epi epi) {
+    static_assert(!BPRE || SPLIT, "pre-split weights only with the 3xTF32 split");
     using SM = Smem<T, STAGES, SPLIT>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -503,6 +507,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mA)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mB)) : "memory");
+        if constexpr (BPRE) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mBlo)) : "memory");
     }
     if (warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)), "r"(NCOLS)
@@ -538,7 +543,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     constexpr int EK = ROWB / (int)sizeof(T);   // elements of K per slab row
     if (warp == 0) {
         if (lane == 0) {
-            const uint32_t bytes = (uint32_t)SLOT;
+            const uint32_t bytes = (uint32_t)(SLOT + (BPRE ? (size_t)bn * ROWB : 0));
             int kg = 0;
             for (int id = blockIdx.x; id < ntiles; id += gridDim.x) {
                 int64_t m0;
@@ -552,6 +557,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                     else if (tm.mode == 2) tma_3d(hi(s), &mA, kb * EK, z, (int)m0, full + s);
                     else tma_2d(hi(s), &mA, kb * EK, (int)m0, full + s);
                     tma_2d(hi(s) + (size_t)BM * ROWB, &mB, kb * EK, brow, full + s);
+                    if constexpr (BPRE) tma_2d(lo(s) + (size_t)BM * ROWB, &mBlo, kb * EK, brow, full + s);
                 }
             }
         }
@@ -607,7 +613,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             // converters: split every landed slab (the producer reused slot s only after the
             // MMAs of its previous round completed, and full[s] completes after that reuse)
             const int ct = threadIdx.x - 256;
-            const int nchunks = (BM + bn) * (ROWB / 16);
+            const int nchunks = (BPRE ? BM : BM + bn) * (ROWB / 16);   // BPRE: the B rows arrive split
             int kg = 0;
             for (int id = blockIdx.x; id < ntiles; id += gridDim.x) {
                 for (int kb = 0; kb < nk; ++kb, ++kg) {

@@ -24,11 +24,15 @@ from paper_2605_19150_b200.block import FSAClassifier
 EVAL_LENGTHS = (40, 64, 100, 128, 160, 200, 256)
 
 
-def train_task(task, steps=2000, batch=256, max_len=40, lr=2e-3, seed=0, device="cuda", log_every=0):
+def train_task(task, steps=2000, batch=256, max_len=40, lr=2e-3, seed=0, device="cuda", log_every=0, t0=1.0,
+               t1=0.1, bmag=2.0):
     spec = fsa_tasks.TASKS[task]
     torch.manual_seed(seed)
     rng = np.random.default_rng(seed)
     model = FSAClassifier(spec["vocab"], spec["classes"]).to(device)
+    with torch.no_grad():
+        for b in model.blocks:
+            b.mixer.b_mag.fill_(bmag)
     opt = torch.optim.Adam(model.parameters(), lr=lr)
     warm = max(1, steps // 20)
     sched = torch.optim.lr_scheduler.LambdaLR(
@@ -36,7 +40,7 @@ def train_task(task, steps=2000, batch=256, max_len=40, lr=2e-3, seed=0, device=
     t0 = time.time()
     losses = []
     for step in range(steps):
-        model.set_temperature(max(0.1, 0.1 ** (step / max(1, steps - 1))))
+        model.set_temperature(t0 * (t1 / t0) ** (step / max(1, steps - 1)))   # exponential t0 -> t1
         L = int(rng.integers(2, max_len + 1))
         x, y = fsa_tasks.sample(task, batch, L, rng)
         x = torch.from_numpy(x).to(device)
@@ -47,7 +51,7 @@ def train_task(task, steps=2000, batch=256, max_len=40, lr=2e-3, seed=0, device=
         torch.nn.utils.clip_grad_norm_(model.parameters(), 1.0)
         opt.step()
         sched.step()
-        losses.append(float(loss))
+        losses.append(float(loss.detach()))
         if log_every and step % log_every == 0:
             print(f"{task} step {step} loss {np.mean(losses[-log_every:]):.4f}", flush=True)
     torch.cuda.synchronize()
@@ -59,7 +63,8 @@ def train_task(task, steps=2000, batch=256, max_len=40, lr=2e-3, seed=0, device=
             x, y = fsa_tasks.sample(task, 512, L, np.random.default_rng(10_000 + L))
             pred = model(torch.from_numpy(x).to(device)).argmax(-1).cpu().numpy()
             accs[L] = float((pred == y).mean())
-    return {"task": task, "steps": steps, "batch": batch, "train_max_len": max_len, "seed": seed,
+    return {"task": task, "steps": steps, "batch": batch, "train_max_len": max_len, "seed": seed, "lr": lr,
+            "temperature": [t0, t1], "b_mag_init": bmag,
             "final_train_loss": float(np.mean(losses[-50:])), "val_acc_by_len": accs,
             "val_acc_mean": float(np.mean(list(accs.values()))), "train_seconds": train_s,
             "ms_per_step": 1e3 * train_s / steps}
@@ -72,10 +77,15 @@ def main():
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--seeds", type=int, default=1)
     ap.add_argument("--log-every", type=int, default=0)
+    ap.add_argument("--lr", type=float, default=2e-3)
+    ap.add_argument("--t0", type=float, default=1.0)
+    ap.add_argument("--t1", type=float, default=0.1)
+    ap.add_argument("--bmag", type=float, default=2.0)
     a = ap.parse_args()
     for task in a.tasks.split(","):
         for seed in range(a.seeds):
-            print(json.dumps(train_task(task, a.steps, a.batch, seed=seed, log_every=a.log_every)), flush=True)
+            print(json.dumps(train_task(task, a.steps, a.batch, lr=a.lr, seed=seed, log_every=a.log_every, t0=a.t0,
+                                        t1=a.t1, bmag=a.bmag)), flush=True)
 
 
 if __name__ == "__main__":
