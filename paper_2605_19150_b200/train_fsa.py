@@ -37,7 +37,7 @@ def train_task(task, steps=2000, batch=256, max_len=40, lr=2e-3, seed=0, device=
     warm = max(1, steps // 20)
     sched = torch.optim.lr_scheduler.LambdaLR(
         opt, lambda s: (s + 1) / warm if s < warm else 0.5 * (1 + math.cos(math.pi * (s - warm) / max(1, steps - warm))))
-    t0 = time.time()
+    tic = time.time()
     losses = []
     for step in range(steps):
         model.set_temperature(t0 * (t1 / t0) ** (step / max(1, steps - 1)))   # exponential t0 -> t1
@@ -55,7 +55,7 @@ def train_task(task, steps=2000, batch=256, max_len=40, lr=2e-3, seed=0, device=
         if log_every and step % log_every == 0:
             print(f"{task} step {step} loss {np.mean(losses[-log_every:]):.4f}", flush=True)
     torch.cuda.synchronize()
-    train_s = time.time() - t0
+    train_s = time.time() - tic
     model.eval()
     accs = {}
     with torch.no_grad():
