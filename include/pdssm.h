@@ -304,12 +304,31 @@ pdssm_status pdssm_scan_bwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
  *   h_out_opt act  [B][H][L][c][N]    out: states;   y_opt act [B][L][H][P] out
  *   chunk_state                        out (pdssm_chunk_state_bytes)
  *   ws  >= pdssm_workspace_bytes(dims, PDSSM_OP_LAYER)  (b_t plus the scan's workspace)
- * Errors and paths: those of the three calls it chains.
+ * Paths (NEXT-2): when the shapes allow one common tile width (fp32: 128; bf16: 256 or 128) the
+ * selector logits + argmax and the projection run as ONE tcgen05 launch over the stacked weight
+ * rows [S | B] (the x slabs of a token block are read once per tile set and shared through L2;
+ * fp32 weights are stacked pre-split for 3xTF32); otherwise pdssm_select + pdssm_project.
+ * Errors: those of the calls it chains.
  * ------------------------------------------------------------------------- */
 pdssm_status pdssm_layer_fwd(const void* x, const void* S, const uint16_t* dict_idx, const void* diag,
                              const void* Bw, const float* C_opt, const float* h0_opt, uint8_t* kstar,
                              void* h_out_opt, void* y_opt, void* chunk_state, const pdssm_dims* dims,
                              void* ws, size_t ws_bytes, pdssm_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * NEXT-2 layer-level forward with the input-dependent diagonal generated in the same GEMM:
+ *   D_t = sigmoid(W_mag x_t + bias_mag) exp(i W_phase x_t)   (reading R30)
+ * fused with the selector and the projection as one tcgen05 launch (stacked rows [S | B | W_d],
+ * the D range tiled per (head, block of states)), then the scan (PER_STEP) and readout.
+ *   Wd        act [H][c][N][d_in]  rows W_mag (c = 0) and W_phase (c = 1)
+ *   bias_mag_opt f32 [H][N]        (NULL = 0)
+ *   other arguments as pdssm_layer_fwd (dims.diag_mode must be PDSSM_DIAG_PER_STEP);
+ *   ws >= pdssm_workspace_bytes(dims, PDSSM_OP_LAYER).
+ * ------------------------------------------------------------------------- */
+pdssm_status pdssm_layer_fwd_gen(const void* x, const void* S, const uint16_t* dict_idx, const void* Wd,
+                                 const float* bias_mag_opt, const void* Bw, const float* C_opt, const float* h0_opt,
+                                 uint8_t* kstar, void* h_out_opt, void* y_opt, void* chunk_state,
+                                 const pdssm_dims* dims, void* ws, size_t ws_bytes, pdssm_stream_t stream);
 
 /* ---------------------------------------------------------------------------
  * NEXT-1: Prop. 2 surrogate gradients (derivation App. C

@@ -18,7 +18,7 @@ import re
 __all__ = [
     "PdssmError", "Dims", "lib", "sparsify", "select", "scan_fwd", "scan_bwd",
     "segment_summary", "compose_carry", "segment_summary_bwd", "compose_lambda",
-    "check_device", "chunk_state_views", "select_grad", "dict_grad", "scan", "layer_fwd", "diag_gen", "soft_select", "default_chunk", "workspace_bytes",
+    "check_device", "chunk_state_views", "select_grad", "dict_grad", "scan", "layer_fwd", "layer_fwd_gen", "diag_gen", "soft_select", "default_chunk", "workspace_bytes",
     "F32", "BF16", "PER_STEP", "PER_DICT", "CHECK_FINITE", "EXPORT_MAPS",
 ]
 
@@ -79,6 +79,7 @@ def _load():
         "pdssm_soft_select": (ctypes.c_int, [vp, vp, vp, D, vp, sz, vp]),
         "pdssm_diag_gen": (ctypes.c_int, [vp, vp, vp, vp, D, vp]),
         "pdssm_layer_fwd": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, D, vp, sz, vp]),
+        "pdssm_layer_fwd_gen": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, D, vp, sz, vp]),
         "pdssm_dict_grad": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, ctypes.c_float, vp, vp, D, vp]),
         "pdssm_status_string": (ctypes.c_char_p, [ctypes.c_int]),
         "pdssm_last_error": (ctypes.c_char_p, []),
@@ -349,12 +350,18 @@ def diag_gen(x, Wd, bias=None, out=None):
     return D
 
 
-def layer_fwd(x, S, dict_idx, diag, Bw, C=None, h0=None, per_dict=True, want_h=True, out=None):
+def layer_fwd(x, S, dict_idx, diag, Bw, C=None, h0=None, per_dict=True, want_h=True, out=None, Wd=None,
+              bias_mag=None):
     """Layer-level forward (select -> b = Bx -> scan -> y = Re(Ch)) with the north_star argument list.
+    Wd (with diag=None): the D_t generator weights [H][c][N][d_in] (+ bias_mag [H][N]) fused into the
+    same GEMM as the selector and the projection (pdssm_layer_fwd_gen; PER_STEP).
     Returns dict(kstar, h, y, chunk_state, dims)."""
     torch = _torch()
-    for n, t in (("x", x), ("S", S), ("dict_idx", dict_idx), ("diag", diag), ("Bw", Bw), ("C", C), ("h0", h0)):
+    for n, t in (("x", x), ("S", S), ("dict_idx", dict_idx), ("diag", diag), ("Bw", Bw), ("C", C), ("h0", h0),
+                 ("Wd", Wd), ("bias_mag", bias_mag)):
         _contig(t, n)
+    if Wd is not None:
+        per_dict = False
     B, L, d_in = x.shape
     H, c, N, _ = Bw.shape
     K = S.shape[1]
@@ -381,8 +388,13 @@ def layer_fwd(x, S, dict_idx, diag, Bw, C=None, h0=None, per_dict=True, want_h=T
         ws, wsb = _workspace(dims, OP_LAYER, dev)
     else:
         wsb = ws.numel()
-    _check(lib.pdssm_layer_fwd(_ptr(x), _ptr(S), _ptr(dict_idx), _ptr(diag), _ptr(Bw), _ptr(C), _ptr(h0), _ptr(ks),
-                               _ptr(h), _ptr(y), _ptr(cs), ctypes.byref(dims), _ptr(ws), wsb, _stream()))
+    if Wd is not None:
+        _check(lib.pdssm_layer_fwd_gen(_ptr(x), _ptr(S), _ptr(dict_idx), _ptr(Wd), _ptr(bias_mag), _ptr(Bw), _ptr(C),
+                                       _ptr(h0), _ptr(ks), _ptr(h), _ptr(y), _ptr(cs), ctypes.byref(dims), _ptr(ws), wsb,
+                                       _stream()))
+    else:
+        _check(lib.pdssm_layer_fwd(_ptr(x), _ptr(S), _ptr(dict_idx), _ptr(diag), _ptr(Bw), _ptr(C), _ptr(h0), _ptr(ks),
+                                   _ptr(h), _ptr(y), _ptr(cs), ctypes.byref(dims), _ptr(ws), wsb, _stream()))
     return dict(kstar=ks, h=h, y=y, chunk_state=cs, dims=dims)
 
 

@@ -245,6 +245,114 @@ pdssm_status prepare_e_run(const Geo& g, const void* dh, const void* dy, const f
     });
 }
 
+
+// ---------------------------------------------------------------------------
+// NEXT-2 fused layer GEMM: selector logits + argmax (a2-a4), projection b = B x
+// (a5) and optionally the D_t generator (R30) as ONE tcgen05 launch over the stacked weight rows
+// [S | zero pad to n_sel | B | W_d]: every tile of a token block reads the same x slabs (the tiles
+// of one block run concurrently on neighbouring SMs and share them through L2), the column range
+// picks the epilogue (tc::EpiLayer).  fp32 weights are stacked pre-split (tf32 hi / lo, BPRE).
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_stack_layer_weights(const T* __restrict__ S, const T* __restrict__ Bw, const T* __restrict__ Wd,
+                                      T* __restrict__ Whi, float* __restrict__ Wlo, int H, int K, int N, int nc,
+                                      int64_t d, int n_sel, int n_prj, int ns, int64_t n_tot) {
+    const int64_t total = n_tot * d;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / d, k = i - r * d;
+        float v = 0.f;
+        if (r < (int64_t)H * K) {
+            v = ldact(S + r * d + k);
+        } else if (r >= n_sel && r < n_sel + n_prj) {
+            v = ldact(Bw + (r - n_sel) * d + k);
+        } else if (r >= n_sel + n_prj) {   // D rows: tile jt holds [mag of ns states | phase of the same states]
+            const int64_t q = r - n_sel - n_prj;
+            const int64_t jt = q / (nc * ns), c2 = q - jt * (nc * ns);
+            const int h = (int)(jt / (N / ns)), s0 = (int)(jt % (N / ns)) * ns;
+            const int plane = (int)(c2 / ns), st = s0 + (int)(c2 % ns);
+            v = ldact(Wd + (((int64_t)h * nc + plane) * N + st) * d + k);
+        }
+        if (Wlo) {
+            const float vh = __uint_as_float(tc::tf32_rna(v));
+            stact(Whi + i, vh);
+            Wlo[i] = v - vh;
+        } else {
+            stact(Whi + i, v);
+        }
+    }
+}
+
+struct LayerTiles {
+    int bn, n_sel, n_prj, n_dg, ns;
+};
+
+// the common tile width of the three ranges (0: the fused GEMM does not apply to these shapes)
+inline LayerTiles layer_tiles(const Geo& g, bool with_dg) {
+    LayerTiles lt{0, 0, 0, 0, 0};
+    const int64_t K = g.K, cN = g.nc * g.N, l = K / gcd64(K, 16) * 16;
+    const int cands_f32[] = {128};
+    const int cands_bf16[] = {256, 128};
+    const int* cands = g.act == 4 ? cands_f32 : cands_bf16;
+    const int nc_ = g.act == 4 ? 1 : 2;
+    for (int i = 0; i < nc_; ++i) {
+        const int bn = cands[i];
+        if (bn % l != 0 || (g.H * cN) % bn != 0 || cN % 16 != 0) continue;
+        if (with_dg) {
+            if (bn % g.nc != 0) continue;
+            const int ns = bn / g.nc;
+            if (ns % 16 != 0 || g.N % ns != 0) continue;
+            lt.ns = ns;
+            lt.n_dg = (int)(g.H * cN);
+        }
+        lt.bn = bn;
+        lt.n_sel = (int)(ceil_div(g.H * K, bn) * bn);
+        lt.n_prj = (int)(g.H * cN);
+        return lt;
+    }
+    return lt;
+}
+
+pdssm_status layer_gemm(const Geo& g, const void* x, const void* S, const uint16_t* dict_idx, const void* Bw, const void* Wd,
+                        const float* bias_mag, uint8_t* kstar, void* b_out, void* D_out, void* wbuf, cudaStream_t st,
+                        bool* done) {
+    *done = false;
+    const LayerTiles lt = layer_tiles(g, Wd != nullptr);
+    if (lt.bn == 0 || !tc_operands_ok(g, {x, S, Bw, Wd, b_out, D_out, wbuf}) || (Wd && g.N % 16 != 0)) return PDSSM_OK;
+    const int64_t n_tot = (int64_t)lt.n_sel + lt.n_prj + lt.n_dg;
+    if (n_tot > layer_w_rows(g)) return PDSSM_OK;
+    return with_act(g.dtype, [&](auto tv) -> pdssm_status {
+        using T = decltype(tv);
+        constexpr bool F32 = std::is_same<T, float>::value;
+        T* Whi = static_cast<T*>(wbuf);
+        float* Wlo = F32 ? reinterpret_cast<float*>(static_cast<char*>(wbuf) + align256((size_t)layer_w_rows(g) * g.d_in * sizeof(T)))
+                         : nullptr;
+        const int64_t total = n_tot * g.d_in;
+        k_stack_layer_weights<T><<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 4 * 148 * 8), 256, 0, st>>>(
+            static_cast<const T*>(S), static_cast<const T*>(Bw), static_cast<const T*>(Wd), Whi, Wlo, (int)g.H, (int)g.K,
+            (int)g.N, g.nc, g.d_in, lt.n_sel, lt.n_prj, lt.ns ? lt.ns : 1, n_tot);
+        pdssm_status r = cuda_check("stack_layer_weights");
+        if (r) return r;
+        CUtensorMap mA, mB, mBl;
+        if (!make_kmajor_map(&mA, x, sizeof(T), g.d_in, g.B * g.L, tc::BM) ||
+            !make_kmajor_map(&mB, Whi, sizeof(T), g.d_in, n_tot, lt.bn) ||
+            (F32 && !make_kmajor_map(&mBl, Wlo, sizeof(T), g.d_in, n_tot, lt.bn)))
+            return fail(PDSSM_ERR_CUDA, "layer_gemm: cuTensorMapEncodeTiled failed");
+        const int64_t M = g.B * g.L, cN = g.nc * g.N;
+        tc::EpiLayer<T> epi{tc::EpiSelect{kstar, nullptr, dict_idx, nullptr, M, (int)g.L, (int)g.H, (int)g.K, (int)g.N,
+                                          g.flags},
+                            tc::EpiProject<T>{static_cast<T*>(b_out), M, (int)g.L, (int)g.H, (int)cN, g.H * cN},
+                            tc::EpiDiag<T>{static_cast<T*>(D_out), bias_mag, M, (int)g.L, (int)g.H, (int)g.N, g.nc, lt.ns},
+                            lt.n_sel, lt.n_prj};
+        dim3 grid((unsigned)ceil_div(M, tc::BM), (unsigned)(n_tot / lt.bn));
+        *done = true;
+        if constexpr (F32)
+            return launch_tc_maps<T, tc::EpiLayer<T>, true>(mA, mB, g.d_in, lt.bn, tc::TileMap{0, 1, 1, 0}, grid, epi, st,
+                                                            "layer_gemm", &mBl);
+        else
+            return launch_tc_maps<T>(mA, mB, g.d_in, lt.bn, tc::TileMap{0, 1, 1, 0}, grid, epi, st, "layer_gemm");
+    });
+}
+
 }  // namespace api
 }  // namespace pdssm
 
@@ -416,6 +524,57 @@ pdssm_status pdssm_readout(const void* h, const float* C, void* y, const pdssm_d
             return cuda_check("readout");
         });
     });
+}
+
+// ---------------------------------------------------------------------------
+// layer-level forward: (select + projection [+ D_t generator]) -> scan (+ readout)
+// ---------------------------------------------------------------------------
+static pdssm_status layer_common(const void* x, const void* S, const uint16_t* dict_idx, const void* diag, const void* Wd,
+                                 const float* bias_mag, const void* Bw, const float* C_opt, const float* h0_opt,
+                                 uint8_t* kstar, void* h_out_opt, void* y_opt, void* chunk_state, const pdssm_dims* dims,
+                                 void* ws, size_t ws_bytes, pdssm_stream_t stream) {
+    Geo g;
+    pdssm_status r = geo_of(dims, &g);
+    if (r) return r;
+    if (!x || !S || !dict_idx || !(diag || Wd) || !Bw || !kstar || !chunk_state)
+        return fail(PDSSM_ERR_NULL, "layer_fwd: x, S, dict_idx, diag (or Wd), Bw, kstar, chunk_state are required");
+    if (g.d_in < 1) return fail(PDSSM_ERR_SHAPE, "layer_fwd: d_in must be >= 1");
+    if (Wd && g.diag_mode != PDSSM_DIAG_PER_STEP) return fail(PDSSM_ERR_DTYPE, "layer_fwd_gen: generated D_t is PER_STEP");
+    const size_t need = ws_bytes_g(g, PDSSM_OP_LAYER);
+    if (!ws || ws_bytes < need) return fail(PDSSM_ERR_WORKSPACE, "layer_fwd: workspace too small (need %zu)", need);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    char* b = static_cast<char*>(ws);                   // b_t [B][H][L][c][N] act
+    char* D = b + seq_act_bytes(g);                      // generated D_t (layer_fwd_gen)
+    char* W = D + seq_act_bytes(g);                      // stacked weights of the fused GEMM
+    char* rest = W + layer_w_bytes(g);
+    const size_t rest_bytes = ws_bytes - (size_t)(rest - static_cast<char*>(ws));
+    bool fused = false;
+    if ((r = layer_gemm(g, x, S, dict_idx, Bw, Wd, bias_mag, kstar, b, Wd ? D : nullptr, W, st, &fused))) return r;
+    if (!fused) {   // shapes the fused GEMM does not take: the separate launches
+        if ((r = pdssm_select(x, S, dict_idx, kstar, nullptr, nullptr, dims, rest, rest_bytes, stream))) return r;
+        if ((r = pdssm_project(x, Bw, b, dims, stream))) return r;
+        if (Wd && (r = pdssm_diag_gen(x, Wd, bias_mag, D, dims, stream))) return r;
+    }
+    return pdssm_scan_fwd(kstar, dict_idx, Wd ? D : diag, b, h0_opt, C_opt, h_out_opt, y_opt, chunk_state, nullptr, dims,
+                          rest, rest_bytes, stream);
+}
+
+pdssm_status pdssm_layer_fwd(const void* x, const void* S, const uint16_t* dict_idx, const void* diag, const void* Bw,
+                             const float* C_opt, const float* h0_opt, uint8_t* kstar, void* h_out_opt, void* y_opt,
+                             void* chunk_state, const pdssm_dims* dims, void* ws, size_t ws_bytes,
+                             pdssm_stream_t stream) {
+    if (!diag) return fail(PDSSM_ERR_NULL, "layer_fwd: diag is required");
+    return layer_common(x, S, dict_idx, diag, nullptr, nullptr, Bw, C_opt, h0_opt, kstar, h_out_opt, y_opt, chunk_state,
+                        dims, ws, ws_bytes, stream);
+}
+
+pdssm_status pdssm_layer_fwd_gen(const void* x, const void* S, const uint16_t* dict_idx, const void* Wd,
+                                 const float* bias_mag_opt, const void* Bw, const float* C_opt, const float* h0_opt,
+                                 uint8_t* kstar, void* h_out_opt, void* y_opt, void* chunk_state,
+                                 const pdssm_dims* dims, void* ws, size_t ws_bytes, pdssm_stream_t stream) {
+    if (!Wd) return fail(PDSSM_ERR_NULL, "layer_fwd_gen: Wd is required");
+    return layer_common(x, S, dict_idx, nullptr, Wd, bias_mag_opt, Bw, C_opt, h0_opt, kstar, h_out_opt, y_opt,
+                        chunk_state, dims, ws, ws_bytes, stream);
 }
 
 }  // extern "C"

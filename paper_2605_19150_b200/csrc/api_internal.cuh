@@ -119,6 +119,12 @@ inline float* readout_lo_part(const Geo& g, void* wbuf) {
                                     : nullptr;
 }
 inline size_t seq_act_bytes(const Geo& g) { return align256((size_t)g.S * g.L * g.nc * g.N * g.act); }
+// NEXT-2 fused layer GEMM: stacked weight rows [S | pad | B | W_d] (upper bound), fp32 adds the tf32 lo part
+inline int64_t layer_w_rows(const Geo& g) { return g.H * g.K + 256 + 2 * g.H * g.nc * g.N; }
+inline size_t layer_w_bytes(const Geo& g) {
+    return g.d_in > 0 ? align256((size_t)layer_w_rows(g) * g.d_in * g.act) + (g.act == 4 ? align256((size_t)layer_w_rows(g) * g.d_in * 4) : 0)
+                      : 0;
+}
 inline int npad8(int64_t N) { return (int)((N + 7) & ~7); }
 inline size_t summary_block_bytes(const Geo& g) { return (size_t)npad8(g.N) * 2 + (size_t)2 * g.nc * g.N * 4; }
 
@@ -150,9 +156,9 @@ inline size_t ws_bytes_g(const Geo& g, int op) {
             const int64_t kp = (g.K + 7) / 8 * 8;
             return align256((size_t)g.H * g.B * g.L * kp * g.act) + align256((size_t)g.H * g.N * g.N * kp * g.act);
         }
-        case PDSSM_OP_LAYER: {
+        case PDSSM_OP_LAYER: {   // b_t, D_t (generator), stacked weights of the fused layer GEMM, scan ws
             const size_t sel = align256((size_t)g.S * g.L * g.K * 4), fwd = ws_bytes_g(g, PDSSM_OP_FWD);
-            return seq_act_bytes(g) + (sel > fwd ? sel : fwd);
+            return 2 * seq_act_bytes(g) + layer_w_bytes(g) + (sel > fwd ? sel : fwd);
         }
         case PDSSM_OP_SEGMENT: {
             size_t fwd = plan_bytes(g) + chunk_state_bytes_g(g);

@@ -285,29 +285,34 @@ struct EpiProject {
 // NEXT-2 D_t generator (SPEC.md:367 form, reading R30): one tile = one head's c*N columns
 // [a_0..a_{N-1} | theta_0..theta_{N-1}] of a token row; the epilogue writes
 // D[b][h][t][c][n] = sigmoid(a + bias[h][n]) (cos theta, sin theta)   (c = 1: the magnitude)
+// ns (0 = N): states per tile -- a tile of nc * ns columns holds [a_s0..a_{s0+ns-1} | theta_s0..]
+// of the head's states s0 .. s0 + ns - 1 (tile jt = n0 / (nc ns): head jt / (N / ns), s0 = ns (jt % (N / ns))).
 template <typename TO>
 struct EpiDiag {
     TO* out;
     const float* bias;   // [H][N] or null
     int64_t M;
     int L, H, N, nc;
+    int ns = 0;
     __device__ void operator()(uint32_t taddr, int64_t m, int n0, int bn, int z) const {
         (void)z;
         (void)bn;
         const bool valid = m < M;
         const int64_t b = valid ? m / L : 0, t = valid ? m - b * L : 0;
         const int cN = nc * N;
-        const int h = n0 / cN;
-        TO* dst = out + (((size_t)b * H + h) * L + t) * cN;
-        for (int c0 = 0; c0 < N; c0 += 16) {
+        const int S = ns ? ns : N;
+        const int jt = n0 / (nc * S);
+        const int h = jt / (N / S), s0 = (jt % (N / S)) * S;
+        TO* dst = out + (((size_t)b * H + h) * L + t) * cN + s0;
+        for (int c0 = 0; c0 < S; c0 += 16) {
             float a[16], th[16];
             tmem_ld16(taddr + (uint32_t)c0, a);
-            if (nc == 2) tmem_ld16(taddr + (uint32_t)(c0 + N), th);
+            if (nc == 2) tmem_ld16(taddr + (uint32_t)(c0 + S), th);
             if (!valid) continue;
             float re[16], im[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-                const float mag = 1.f / (1.f + expf(-(a[i] + (bias ? bias[(size_t)h * N + c0 + i] : 0.f))));
+                const float mag = 1.f / (1.f + expf(-(a[i] + (bias ? bias[(size_t)h * N + s0 + c0 + i] : 0.f))));
                 if (nc == 2) {
                     float sn, cs;
                     sincosf(th[i], &sn, &cs);
@@ -337,6 +342,24 @@ struct EpiDiag {
             reinterpret_cast<uint4*>(d)[0] = make_uint4(p[0], p[1], p[2], p[3]);
             reinterpret_cast<uint4*>(d)[1] = make_uint4(p[4], p[5], p[6], p[7]);
         }
+    }
+};
+
+// NEXT-2 fused layer GEMM: one launch over the stacked weight rows [S (padded to n_sel) | B
+// (n_prj) | W_d (optional)] of the layer (api_gemm.cu layer_gemm): every tile reads the same x
+// slabs (consecutive tiles of one token block run concurrently and share them through L2), and
+// the tile's column range picks its epilogue -- the argmax of Eq. 7, the projection of Eq. 1, or
+// the D_t generator (R30).  bn divides n_sel and n_prj, and equals nc * ns for the D range.
+template <typename TO>
+struct EpiLayer {
+    EpiSelect sel;
+    EpiProject<TO> prj;
+    EpiDiag<TO> dg;
+    int n_sel, n_prj;
+    __device__ void operator()(uint32_t taddr, int64_t m, int n0, int bn, int z) const {
+        if (n0 < n_sel) sel(taddr, m, n0, bn, z);
+        else if (n0 < n_sel + n_prj) prj(taddr, m, n0 - n_sel, bn, z);
+        else dg(taddr, m, n0 - n_sel - n_prj, bn, z);
     }
 };
 

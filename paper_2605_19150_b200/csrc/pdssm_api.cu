@@ -182,29 +182,6 @@ pdssm_status pdssm_sparsify(const float* M, uint16_t* dict_idx, const pdssm_dims
     return cuda_check("sparsify");
 }
 
-// ---------------------------------------------------------------------------
-// layer-level forward: select -> projection -> scan (+ readout)
-// ---------------------------------------------------------------------------
-pdssm_status pdssm_layer_fwd(const void* x, const void* S, const uint16_t* dict_idx, const void* diag, const void* Bw,
-                             const float* C_opt, const float* h0_opt, uint8_t* kstar, void* h_out_opt, void* y_opt,
-                             void* chunk_state, const pdssm_dims* dims, void* ws, size_t ws_bytes,
-                             pdssm_stream_t stream) {
-    Geo g;
-    pdssm_status r = geo_of(dims, &g);
-    if (r) return r;
-    if (!x || !S || !dict_idx || !diag || !Bw || !kstar || !chunk_state)
-        return fail(PDSSM_ERR_NULL, "layer_fwd: x, S, dict_idx, diag, Bw, kstar, chunk_state are required");
-    if (g.d_in < 1) return fail(PDSSM_ERR_SHAPE, "layer_fwd: d_in must be >= 1");
-    const size_t need = ws_bytes_g(g, PDSSM_OP_LAYER);
-    if (!ws || ws_bytes < need) return fail(PDSSM_ERR_WORKSPACE, "layer_fwd: workspace too small (need %zu)", need);
-    char* b = static_cast<char*>(ws);                 // b_t [B][H][L][c][N] act
-    char* rest = b + seq_act_bytes(g);
-    const size_t rest_bytes = ws_bytes - seq_act_bytes(g);
-    if ((r = pdssm_select(x, S, dict_idx, kstar, nullptr, nullptr, dims, rest, rest_bytes, stream))) return r;
-    if ((r = pdssm_project(x, Bw, b, dims, stream))) return r;
-    return pdssm_scan_fwd(kstar, dict_idx, diag, b, h0_opt, C_opt, h_out_opt, y_opt, chunk_state, nullptr, dims, rest,
-                          rest_bytes, stream);
-}
 
 static pdssm_status common_scan_checks(const Geo& g, const void* kstar, const void* dict_idx, const void* diag) {
     if (!kstar || !dict_idx || !diag) return fail(PDSSM_ERR_NULL, "kstar, dict_idx and diag are required");

@@ -297,3 +297,66 @@ def test_soft_select_parity(P, N, K, bf16):
     if not bf16:   # bf16 operands (s, M rounded to 8 bits) leave more columns inside the margin
         assert np.mean(got != ref) <= 2e-3
     assert got.min() >= 0 and got.max() < N
+
+
+@pytest.mark.parametrize("c,N,bf16", [(2, 128, False), (1, 64, False), (2, 64, True)])
+def test_layer_fwd_gen_parity(P, c, N, bf16):
+    """NEXT-2: selector + projection + D_t generator as one fused tcgen05 GEMM (pdssm_layer_fwd_gen),
+    then the scan and the readout, against the oracle chain select -> project_b -> diag_generator ->
+    scan_forward -> readout (R30).  Integer-valued x, S: the selections are exact (R18)."""
+    B, H, L, K, d_in, Pp = 2, 2, 150, 8, 64, 32
+    x = synth.tokens_x(B, L, d_in, seed=N + 1, integer=True)
+    S = synth.selector(H, K, d_in, seed=N + 1, integer=True)
+    di = synth.random_maps(H, K, N, seed=N + 1)
+    Bw = synth.projection_B(H, c, N, d_in, seed=N + 1)
+    Wd = synth.projection_B(H, c, N, d_in, seed=N + 2) / 8.0
+    bmag = np.random.default_rng(N).normal(2.0, 0.5, size=(H, N)).astype(np.float32)
+    C = synth.readout_C(H, Pp, N, c, seed=N + 1)
+    if bf16:
+        Bw, Wd, C = synth.round_bf16(Bw), synth.round_bf16(Wd), synth.round_bf16(C)
+    dt = torch.bfloat16 if bf16 else torch.float32
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    r = P.layer_fwd(cu(x).to(dt), cu(S).to(dt), cu(di).to(torch.int16), None, cu(Bw).to(dt), C=cu(C), Wd=cu(Wd).to(dt),
+                    bias_mag=cu(bmag))
+    torch.cuda.synchronize()
+    ks_ref, _ = O.select(x.astype(np.float64), S.astype(np.float64))
+    assert np.array_equal(r["kstar"].cpu().numpy(), ks_ref)
+    Pm = O.gather_P(di, ks_ref)
+    W = Wd.astype(np.float64)
+    D = O.diag_generator(x.astype(np.float64), W[:, 0], W[:, 1] if c == 2 else None, bmag)
+    if bf16:   # the generator writes D_t in the activation dtype, which the scan then reads (R16)
+        D = O.planes_to_complex(synth.round_bf16(O.complex_to_planes(D, c).astype(np.float32)))
+    Bc = Bw[:, 0].astype(np.float64) + (1j * Bw[:, 1].astype(np.float64) if c == 2 else 0)
+    bz = O.project_b(x.astype(np.float64), Bc)
+    if bf16:
+        bz = O.planes_to_complex(synth.round_bf16(O.complex_to_planes(bz, c).astype(np.float32)))
+    h = O.scan_forward(Pm, D, bz)
+    Cc = C[:, 0].astype(np.float64) + (1j * C[:, 1].astype(np.float64) if c == 2 else 0)
+    y = O.readout(h, Cc)
+    tol = 2e-2 if bf16 else 1e-4
+    check("gen_h", O.planes_to_complex(r["h"].float().cpu().numpy()), h, tol)
+    check("gen_y", r["y"].float().cpu().numpy(), y, tol, bh_axes=(0, 2))
+
+
+def test_layer_fwd_runs_one_fused_gemm(P):
+    """The config-2-shaped layer call launches a single tcgen05 GEMM (EpiLayer: select + projection
+    + D_t generator) before the scan, instead of three."""
+    from torch.profiler import ProfilerActivity, profile
+    B, H, L, K, d_in, N, c, Pp = 2, 8, 256, 32, 1024, 128, 2, 128
+    g = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.randn(B, L, d_in, device="cuda", generator=g)
+    S = torch.randn(H, K, d_in, device="cuda", generator=g) / 32
+    Bw = torch.randn(H, c, N, d_in, device="cuda", generator=g) / 32
+    Wd = torch.randn(H, c, N, d_in, device="cuda", generator=g) / 32
+    C = torch.randn(H, c, Pp, N, device="cuda", generator=g) / 12
+    di = torch.randint(0, N, (H, K, N), device="cuda", generator=g).to(torch.int16)
+    P.layer_fwd(x, S, di, None, Bw, C=C, Wd=Wd)
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        P.layer_fwd(x, S, di, None, Bw, C=C, Wd=Wd)
+        torch.cuda.synchronize()
+    names = [e.name for e in prof.events() if e.device_type.name == "CUDA"]
+    gemms = [n for n in names if "k_gemm_tc" in n]
+    assert any("EpiLayer" in n for n in gemms), gemms
+    assert not any("EpiSelect" in n.split("EpiLayer")[0] or "EpiProject" in n.split("EpiLayer")[0] for n in gemms
+                   if "EpiLayer" not in n)
