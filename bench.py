@@ -297,6 +297,10 @@ def layer_kernels(P, torch, dev, adt, dtype, B, L, H, N, K, c, stream):
     Dout = torch.empty((B, H, L, c, N), device=dev, dtype=adt)
     bmag = torch.randn((H, N), device=dev, generator=g) + 2.0
     tg_ = t(lambda: P.diag_gen(x, Bw, bmag, out=Dout))   # NEXT-2 D_t generator (fused sigmoid/sincos epilogue)
+    # NEXT-2 layer forward with D_t generated in the same GEMM as the selector and the projection
+    Wd = ((torch.rand((H, c, N, d_in), device=dev, generator=g) * 2 - 1) / d_in ** 0.5).to(adt)
+    lo2 = {"kstar": torch.empty((B, H, L), device=dev, dtype=torch.uint8), "h": bout, "y": y}
+    tgen = t(lambda: P.layer_fwd(x, S, di, None, Bw, C=Cw, Wd=Wd, bias_mag=bmag, out=lo2))
     # NEXT-3 PD-SSM soft generator (Eqs. 2-4) as the comparison baseline of the hard selection
     lg = torch.randn((B, H, L, K), device=dev, generator=g)
     Md = (torch.rand((H, K, N, N), device=dev, generator=g) * 2 - 1) / N ** 0.5
@@ -323,7 +327,11 @@ def layer_kernels(P, torch, dev, adt, dtype, B, L, H, N, K, c, stream):
                                    "vs_hard_select": tso / ts,
                                    "what": "PD-SSM generator (Eqs. 2-4): mixture GEMM + column hardmax epilogue"}
     out["layer_fwd"] = {"us": tl, "tokens_per_s": B * L / (tl * 1e-6), "diag": "per_dict",
-                        "chain": "pdssm_layer_fwd = select + project + scan_fwd + readout"}
+                        "chain": "pdssm_layer_fwd = fused (select + project) GEMM + scan_fwd + readout"}
+    out["layer_fwd_gen"] = {"us": tgen, "tokens_per_s": B * L / (tgen * 1e-6), "diag": "per_step, generated",
+                            "chain": "pdssm_layer_fwd_gen = fused (select + project + D_t generator) GEMM + scan_fwd + readout",
+                            "unfused_sum_us": ts + tp + tg_ + tr,
+                            "unfused_parts": "select + project + diag_gen + readout timed alone (scan excluded)"}
     return out
 
 
