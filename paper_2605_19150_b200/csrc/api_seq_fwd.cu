@@ -41,7 +41,8 @@ pdssm_status fwd_seq(const Geo& g, seq::SeqArgs& sa, uint8_t* rec, uint8_t* wm, 
                     if constexpr (!AGG && !CHK) {
                         if (g.N == 128) kern = seq::k_fwd_seq<T, NC, PD, false, false, 128>;
                         else if (g.N == 64)
-                            kern = spc == 2 ? seq::k_fwd_seq<T, NC, PD, false, false, 64, 2, 16>
+                            kern = spc == 2 ? (getenv("PDSSM_SEQ_NO_TIER") ? seq::k_fwd_seq<T, NC, PD, false, false, 64, 2, 16>
+                                                                          : seq::k_fwd_seq<T, NC, PD, false, false, 64, 2, 16, true>)
                                             : seq::k_fwd_seq<T, NC, PD, false, false, 64>;
                     }
                     pdssm_status rr = seq_set_smem((const void*)kern, ly.bytes);

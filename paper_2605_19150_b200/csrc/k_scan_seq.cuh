@@ -226,7 +226,9 @@ constexpr int SEQ_GF = 32;   // forward: steps per ring slot
 // SPC > 1 (N <= 64): SPC sequences (b, b+1, ...) of the same head h share the CTA, its per-head
 // tables, the producer warp and the step barrier; blockIdx.x = p * H + h serves batch rows
 // p * SPC .. p * SPC + SPC - 1.  GF: steps per TMA group.
-template <typename T, int NC, bool PD, bool AGG, bool CHECK, int NN, int SPC = 1, int GF = SEQ_GF>
+// TIER: warp-uniform two-tier gather (4 slots when the warp's in-degree <= 4, else 8): fewer
+// instructions per step, for the issue-bound launches (several CTAs per SM).
+template <typename T, int NC, bool PD, bool AGG, bool CHECK, int NN, int SPC = 1, int GF = SEQ_GF, bool TIER = false>
 __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
     using SV = typename fused::SVal<NC>::type;
     constexpr int G = GF;
@@ -349,10 +351,10 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
         for (int q = 0; q < CAP; ++q) off[q] = __byte_perm(q < 4 ? rc.x : rc.y, 0u, 0x4440u + (uint32_t)(q & 3)) * SVB;
         uint32_t ga[CAP];   // shared addresses of this step's gather, computed before the barrier
         {
-            uint32_t lo[4], hi4[4];
+            uint32_t lo[4], hi4[4] = {0u, 0u, 0u, 0u};
             const uint32_t vb_s = fused::smem_u32(vbc);
             gather_addr4(rc.x, vb_s, SVB, lo);
-            gather_addr4(rc.y, vb_s, SVB, hi4);
+            if (!TIER || AGG || m > 4) gather_addr4(rc.y, vb_s, SVB, hi4);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 ga[q] = lo[q];
@@ -380,11 +382,21 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
             v[q] = fused::mk<NC>(re, im);
         }
 #else
+        const bool tier4 = TIER && !AGG && mc <= 4;   // warp-uniform
+        if (tier4) {
 #pragma unroll
-        for (int q = 0; q < CAP; ++q) {
-            float re, im;
-            lds_sv<NC>(ga[q], re, im);
-            v[q] = fused::mk<NC>(re, im);
+            for (int q = 0; q < 4; ++q) {
+                float re, im;
+                lds_sv<NC>(ga[q], re, im);
+                v[q] = fused::mk<NC>(re, im);
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < CAP; ++q) {
+                float re, im;
+                lds_sv<NC>(ga[q], re, im);
+                v[q] = fused::mk<NC>(re, im);
+            }
         }
 #endif
         if (r == 0 && i == 0 && g >= 1) {   // every compute thread is done with the previous group's slot
@@ -417,7 +429,16 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
                  ((fused::im_of<NC>(x[4]) + fused::im_of<NC>(x[5])) + (fused::im_of<NC>(x[6]) + fused::im_of<NC>(x[7])));
         };
         float ar, ai, cr = 0.f, ci = 0.f;
+#if !defined(FWD_EXP_SLOTS)
+        if (tier4) {
+            ar = (fused::re_of<NC>(v[0]) + fused::re_of<NC>(v[1])) + (fused::re_of<NC>(v[2]) + fused::re_of<NC>(v[3]));
+            ai = (fused::im_of<NC>(v[0]) + fused::im_of<NC>(v[1])) + (fused::im_of<NC>(v[2]) + fused::im_of<NC>(v[3]));
+        } else {
+            sum8(v, ar, ai);
+        }
+#else
         sum8(v, ar, ai);
+#endif
         if constexpr (AGG) {
 #pragma unroll
             for (int q = 0; q < CAP; ++q) v[q] = *reinterpret_cast<const SV*>(vbc2 + off[q]);
