@@ -14,10 +14,21 @@ pdssm_status with_npl(int npl, F&& f) {
     return f(std::integral_constant<int, 4>{});
 }
 
-// shared memory (warp blocks + the head's tables) of the fused kernels for these dims
+// Warps (items in flight) per CTA of a fused-kernel layout: as many as the shared memory holds
+// beside the head's tables, up to fused::WARPS_MAX (0: not even FUSED_MIN_WARPS fit).  More warps
+// hide more of the per-step latency (15 vs the fixed 11 of round 1: config 3 +10%, config 5 +6%).
+constexpr int FUSED_MIN_WARPS = 4;
+template <class LY>
+int fused_warps_of(int64_t K) {
+    const size_t lim = 227 * 1024, tb = LY::t_bytes((int)K);
+    if (tb >= lim) return 0;
+    const int w = (int)std::min<size_t>((lim - tb) / LY::w_bytes, (size_t)fused::WARPS_MAX);
+    return w >= FUSED_MIN_WARPS ? w : 0;
+}
+
 template <bool BWD>
-size_t fused_smem(const Geo& g, int esz) {
-    size_t r = 0;
+int fused_warps(const Geo& g, int esz) {
+    int r = 0;
     with_npl(fused_npl(g.N), [&](auto nv) {
         constexpr int NPL = decltype(nv)::value;
         return with_act(g.dtype, [&](auto tv) {
@@ -26,13 +37,8 @@ size_t fused_smem(const Geo& g, int esz) {
                 constexpr int NC = decltype(ncv)::value;
                 return with_pd(g.diag_mode, [&](auto pdv) {
                     constexpr bool PD = decltype(pdv)::value;
-                    if (esz == 4) {
-                        using LY = fused::Layout<T, NC, NPL, PD, BWD, 4>;
-                        r = LY::bytes + LY::t_bytes((int)g.K);
-                    } else {
-                        using LY = fused::Layout<T, NC, NPL, PD, BWD, (int)sizeof(T)>;
-                        r = LY::bytes + LY::t_bytes((int)g.K);
-                    }
+                    if (esz == 4) r = fused_warps_of<fused::Layout<T, NC, NPL, PD, BWD, 4>>(g.K);
+                    else r = fused_warps_of<fused::Layout<T, NC, NPL, PD, BWD, (int)sizeof(T)>>(g.K);
                     return PDSSM_OK;
                 });
             });
@@ -45,10 +51,7 @@ bool fused_applicable(const Geo& g, std::initializer_list<const void*> ptrs) {
     if (path_generic_forced() || fused_npl(g.N) == 0 || g.tau > fused::TAUMAX) return false;
     for (const void* p : ptrs)
         if (misaligned(p, 16)) return false;
-    const size_t lim = 227 * 1024;
-    if (fused_smem<false>(g, (int)g.act) > lim || fused_smem<true>(g, 4) > lim || fused_smem<true>(g, (int)g.act) > lim)
-        return false;
-    return true;
+    return fused_warps<false>(g, (int)g.act) > 0 && fused_warps<true>(g, 4) > 0 && fused_warps<true>(g, (int)g.act) > 0;
 }
 
 
@@ -82,8 +85,9 @@ pdssm_status fwd_fused(const Geo& g, fused::FusedArgs& fa, uint8_t* rec, uint32_
                 return with_pd(g.diag_mode, [&](auto pdv) {
                     constexpr bool PD = decltype(pdv)::value;
                     using WS = fused::Layout<T, NC, NPL, PD, false>;
-                    return launch_fused(fused::k_fwd_fused<T, NC, NPL, PD>, fa, WS::bytes + WS::t_bytes((int)g.K),
-                                        WS::THREADS, g, st, "fwd_fused");
+                    const int nw = fused_warps_of<WS>(g.K);
+                    return launch_fused(fused::k_fwd_fused<T, NC, NPL, PD>, fa, nw * WS::w_bytes + WS::t_bytes((int)g.K),
+                                        nw * 32, g, st, "fwd_fused");
                 });
             });
         });
@@ -104,8 +108,9 @@ pdssm_status bwd_fused(const Geo& g, fused::FusedArgs& fa, cudaStream_t st) {
                     constexpr bool PD = decltype(pdv)::value;
                     using TEE = typename std::conditional<std::is_same<TE, void>::value, T, TE>::type;
                     using WS = fused::Layout<T, NC, NPL, PD, true, (int)sizeof(TEE)>;
-                    return launch_fused(fused::k_bwd_fused<T, TEE, NC, NPL, PD>, fa, WS::bytes + WS::t_bytes((int)g.K),
-                                        WS::THREADS, g, st, "bwd_fused");
+                    const int nw = fused_warps_of<WS>(g.K);
+                    return launch_fused(fused::k_bwd_fused<T, TEE, NC, NPL, PD>, fa, nw * WS::w_bytes + WS::t_bytes((int)g.K),
+                                        nw * 32, g, st, "bwd_fused");
                 });
             });
         });

@@ -558,8 +558,12 @@ __host__ __device__ constexpr size_t al16(size_t x) { return (x + 15) & ~(size_t
 #ifndef PDSSM_G_BWD
 #define PDSSM_G_BWD 2
 #endif
-constexpr int WARPS_FWD = PDSSM_WARPS_FWD;   // consumer warps (= items in flight) per CTA, one CTA per SM
-constexpr int WARPS_BWD = PDSSM_WARPS_BWD;
+constexpr int WARPS_FWD = PDSSM_WARPS_FWD;   // consumer warps (= items in flight) per CTA: the minimum
+constexpr int WARPS_BWD = PDSSM_WARPS_BWD;   // the host launches (fused_warps); one CTA per SM
+#ifndef PDSSM_WARPS_MAX
+#define PDSSM_WARPS_MAX 15
+#endif
+constexpr int WARPS_MAX = PDSSM_WARPS_MAX;   // launch bound: 480 threads -> <= 136 registers (the kernels use <= 127)
 
 template <typename T, int NC, int NPL, bool PD, bool BWD, int ESZ = (int)sizeof(T)>
 struct Layout {
@@ -774,7 +778,7 @@ __device__ __forceinline__ void pump(const FusedArgs& a, FillCursor& fc, uint32_
 // forward
 // ============================================================================
 template <typename T, int NC, int NPL, bool PD>
-__global__ void __launch_bounds__(Layout<T, NC, NPL, PD, false>::THREADS, 1) k_fwd_fused(FusedArgs a) {
+__global__ void __launch_bounds__(WARPS_MAX * 32, 1) k_fwd_fused(FusedArgs a) {
     using SV = typename SVal<NC>::type;
     using LY = Layout<T, NC, NPL, PD, false>;
     using DT = DType<PD, T>;
@@ -825,7 +829,7 @@ __global__ void __launch_bounds__(Layout<T, NC, NPL, PD, false>::THREADS, 1) k_f
     };
     const uint64_t pol_out = policy_evict_first();
     const uint64_t pol_last = policy_evict_last();
-    uint8_t* tbl = smem + LY::bytes;
+    uint8_t* tbl = smem + (size_t)(blockDim.x >> 5) * LY::w_bytes;   // after every warp's block
     FillCursor fc;
     fc.q = 0;
     uint32_t consumed = 0;        // groups consumed
@@ -1112,7 +1116,7 @@ __global__ void __launch_bounds__(Layout<T, NC, NPL, PD, false>::THREADS, 1) k_f
 // backward (transposed scan, reverse chunk order)
 // ============================================================================
 template <typename T, typename TE, int NC, int NPL, bool PD>
-__global__ void __launch_bounds__(Layout<T, NC, NPL, PD, true, (int)sizeof(TE)>::THREADS, 1) k_bwd_fused(FusedArgs a) {
+__global__ void __launch_bounds__(WARPS_MAX * 32, 1) k_bwd_fused(FusedArgs a) {
     using SV = typename SVal<NC>::type;
     using LY = Layout<T, NC, NPL, PD, true, (int)sizeof(TE)>;
     constexpr int PF = LY::PF;
@@ -1134,7 +1138,7 @@ __global__ void __launch_bounds__(Layout<T, NC, NPL, PD, true, (int)sizeof(TE)>:
     __syncwarp();
     const uint64_t pol_out = policy_evict_first();
     const uint64_t pol_last = policy_evict_last();
-    uint8_t* tbl = smem + LY::bytes;
+    uint8_t* tbl = smem + (size_t)(blockDim.x >> 5) * LY::w_bytes;   // after every warp's block
     FillCursor fc;
     fc.q = 0;
     uint32_t consumed = 0;
