@@ -25,11 +25,11 @@ EVAL_LENGTHS = (40, 64, 100, 128, 160, 200, 256)
 
 
 def train_task(task, steps=2000, batch=256, max_len=40, lr=2e-3, seed=0, device="cuda", log_every=0, t0=1.0,
-               t1=0.1, bmag=2.0):
+               t1=0.1, bmag=2.0, dict_size=None):
     spec = fsa_tasks.TASKS[task]
     torch.manual_seed(seed)
     rng = np.random.default_rng(seed)
-    model = FSAClassifier(spec["vocab"], spec["classes"]).to(device)
+    model = FSAClassifier(spec["vocab"], spec["classes"], dict_size=dict_size).to(device)
     with torch.no_grad():
         for b in model.blocks:
             b.mixer.b_mag.fill_(bmag)
@@ -64,7 +64,7 @@ def train_task(task, steps=2000, batch=256, max_len=40, lr=2e-3, seed=0, device=
             pred = model(torch.from_numpy(x).to(device)).argmax(-1).cpu().numpy()
             accs[L] = float((pred == y).mean())
     return {"task": task, "steps": steps, "batch": batch, "train_max_len": max_len, "seed": seed, "lr": lr,
-            "temperature": [t0, t1], "b_mag_init": bmag,
+            "temperature": [t0, t1], "b_mag_init": bmag, "dict_size": model.blocks[0].mixer.K,
             "final_train_loss": float(np.mean(losses[-50:])), "val_acc_by_len": accs,
             "val_acc_mean": float(np.mean(list(accs.values()))), "train_seconds": train_s,
             "ms_per_step": 1e3 * train_s / steps}
@@ -81,11 +81,13 @@ def main():
     ap.add_argument("--t0", type=float, default=1.0)
     ap.add_argument("--t1", type=float, default=0.1)
     ap.add_argument("--bmag", type=float, default=2.0)
+    ap.add_argument("--dict", type=int, default=0, help="dictionary size K (0: round(sqrt(d_model)))")
     a = ap.parse_args()
     for task in a.tasks.split(","):
         for seed in range(a.seeds):
             print(json.dumps(train_task(task, a.steps, a.batch, lr=a.lr, seed=seed, log_every=a.log_every, t0=a.t0,
-                                        t1=a.t1, bmag=a.bmag)), flush=True)
+                                        t1=a.t1, bmag=a.bmag,
+                                        dict_size=a.dict or None)), flush=True)
 
 
 if __name__ == "__main__":

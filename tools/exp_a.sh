@@ -11,4 +11,4 @@ PDSSM_LIB_VARIANT=w15 b c3_w15 --config 3
 b c5 --config 5
 PDSSM_LIB_VARIANT=w15 b c5_w15 --config 5
 timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:EpiReadout \
-  -s 2 -c 1 -o gpurun_out/${tag}_readout python tools/gemm_driver.py > /dev/null 2>&1; echo "ncu readout $?"
+  -s 1 -c 1 -o gpurun_out/${tag}_readout python tools/gemm_driver.py > /dev/null 2>&1; echo "ncu readout $?"
