@@ -17,6 +17,7 @@
 #include "pdssm_common.cuh"
 #include "k_scan_seq.cuh"   // + k_scan_fwd.cuh, k_scan_fused.cuh (Args and Layout types)
 #include "k_scan_bwd.cuh"   // reduce_dict_ws_bytes
+#include "k_scan_rc.cuh"    // RcArgs
 
 namespace pdssm {
 namespace api {
@@ -149,7 +150,7 @@ inline size_t ws_bytes_g(const Geo& g, int op) {
             return 2 * cs_f_bytes(g) + (g.P > 0 ? seq_f_bytes(g) + readout_w_bytes(g) : 0) +
                    (g.diag_mode == PDSSM_DIAG_PER_DICT ? seq_f_bytes(g) + reduce_dict_ws_bytes(g.S, g.L, g.K, g.nc * g.N)
                                                         : 0) +
-                   fused_ctrl_bytes(g.S, g.C, g.H) + plan_bytes(g);
+                   fused_ctrl_bytes(g.S, g.C, g.H) + plan_bytes(g) + seq_plan_bytes(g);
         case PDSSM_OP_READOUT:
             return readout_w_bytes(g);
         case PDSSM_OP_SOFT: {   // s [H][B L][Kp] and Mt [H][N^2][Kp] in the act dtype
@@ -274,6 +275,10 @@ inline pdssm_status seq_set_smem(const void* f, size_t bytes) {
 // api_seq_fwd.cu / api_seq_bwd.cu: single-chunk path (one CTA per sequence)
 pdssm_status fwd_seq(const Geo& g, seq::SeqArgs& sa, uint8_t* rec, uint8_t* wm, uint8_t* ovf, cudaStream_t st);
 pdssm_status bwd_seq_run(const Geo& g, seq::SeqArgs& sa, bool e_f32, cudaStream_t st);
+// api_seq_bwd.cu: recompute-mode backward, one CTA per sequence (k_scan_rc.cuh)
+bool bwd_seq_rc_applicable(const Geo& g, std::initializer_list<const void*> ptrs);
+pdssm_status bwd_seq_rc_run(const Geo& g, seq::RcArgs& ra, bool e_f32, uint8_t* rec, uint8_t* wm, uint8_t* ovf,
+                            cudaStream_t st);
 // api_fused.cu: chunked warp-per-item path with decoupled look-back
 bool fused_applicable(const Geo& g, std::initializer_list<const void*> ptrs);
 pdssm_status fwd_fused(const Geo& g, fused::FusedArgs& fa, uint8_t* rec, uint32_t* hdr, cudaStream_t st);

@@ -1,5 +1,6 @@
 // libpdssm.so: single-chunk backward scan launcher (k_bwd_seq, csrc/k_scan_seq.cuh).
 #include "api_internal.cuh"
+#include "k_scan_rc.cuh"
 
 using namespace pdssm;
 using namespace pdssm::api;
@@ -43,6 +44,56 @@ pdssm_status bwd_seq(const Geo& g, seq::SeqArgs& sa, cudaStream_t st) {
 // e_f32: the direct state gradient e is the f32 buffer prepared from dy (else dh in the act dtype)
 pdssm_status bwd_seq_run(const Geo& g, seq::SeqArgs& sa, bool e_f32, cudaStream_t st) {
     return e_f32 ? bwd_seq<float>(g, sa, st) : bwd_seq<void>(g, sa, st);
+}
+
+
+// recompute-mode backward, one CTA per sequence (k_scan_rc.cuh); 0 rings: does not fit
+int rc_ring(const Geo& g, size_t esz_e) {
+    int best = 0;
+    for (int R = 2; R <= 8; ++R) {
+        seq::RcLayout ly((int)g.N, (int)g.K, R, g.nc, (int)g.act, (int)esz_e, g.diag_mode == PDSSM_DIAG_PER_DICT, (int)g.L,
+                         g.tau);
+        if (ly.bytes <= kSeqSmemBudget) best = R;
+    }
+    return best;
+}
+
+bool bwd_seq_rc_applicable(const Geo& g, std::initializer_list<const void*> ptrs) {
+    if (env_path_is("generic") || env_path_is("fused")) return false;
+    if (g.N % 32 != 0 || g.N > seq::MAXN || (size_t)g.K * g.N * 8 > 64 * 1024 || g.L > seq::LMAX) return false;
+    for (const void* p : ptrs)
+        if (misaligned(p, 16)) return false;
+    return rc_ring(g, 4) >= 2 && rc_ring(g, g.act) >= 2;
+}
+
+pdssm_status bwd_seq_rc_run(const Geo& g, seq::RcArgs& ra, bool e_f32, uint8_t* rec, uint8_t* wm, uint8_t* ovf,
+                            cudaStream_t st) {
+    seq::k_build_seq_plan<<<(unsigned)(g.H * g.K), (unsigned)g.N, (size_t)g.N * 2, st>>>(
+        ra.dict_idx, rec, wm, ovf, const_cast<uint16_t*>(ra.pstart), const_cast<uint16_t*>(ra.psrc), (int)g.N, g.flags);
+    pdssm_status r = cuda_check("build_seq_plan");
+    if (r) return r;
+    ra.rec = rec;
+    ra.wm = wm;
+    return with_act(g.dtype, [&](auto tv) {
+        using T = decltype(tv);
+        return with_nc(g.nc, [&](auto ncv) {
+            constexpr int NC = decltype(ncv)::value;
+            return with_pd(g.diag_mode, [&](auto pdv) {
+                constexpr bool PD = decltype(pdv)::value;
+                auto go = [&](auto ev) -> pdssm_status {
+                    using TE = decltype(ev);
+                    ra.R = rc_ring(g, sizeof(TE));
+                    seq::RcLayout ly((int)g.N, (int)g.K, ra.R, NC, (int)sizeof(T), (int)sizeof(TE), PD, (int)g.L, g.tau);
+                    auto kern = seq::k_bwd_seq_rc<T, TE, NC, PD>;
+                    pdssm_status rr = seq_set_smem((const void*)kern, ly.bytes);
+                    if (rr) return rr;
+                    kern<<<(unsigned)g.S, (unsigned)g.N + 32, ly.bytes, st>>>(ra);
+                    return cuda_check("bwd_seq_rc");
+                };
+                return e_f32 ? go(float{}) : go(T{});
+            });
+        });
+    });
 }
 
 }  // namespace api

@@ -299,9 +299,28 @@ pdssm_status pdssm_scan_bwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
     uint32_t* ctrl = bump.take<uint32_t>(fused_ctrl_bytes(g.S, g.C, g.H));
     uint16_t* pstart = bump.take<uint16_t>((size_t)g.H * g.K * (g.N + 1) * 2);   // recompute: forward plan
     uint16_t* psrc = bump.take<uint16_t>((size_t)g.H * g.K * g.N * 2);
+    uint8_t* srec = bump.take<uint8_t>(seq_rec_bytes(g));   // recompute (one CTA per sequence): gather records
+    uint8_t* swm = bump.take<uint8_t>(seq_wm_bytes(g));
+    uint8_t* sovf = bump.take<uint8_t>(seq_ovf_bytes(g));
     ChunkStateView cs = cs_view(g, const_cast<void*>(chunk_state));
     const int thr = threads_for(g.N);
     const unsigned items = (unsigned)(g.S * g.C);
+    if (recompute && bwd_seq_rc_applicable(g, {g.diag_mode == PDSSM_DIAG_PER_STEP ? diag : nullptr, bias_opt, dh_opt,
+                                                ebuf, dbias, g.diag_mode == PDSSM_DIAG_PER_STEP ? ddiag : nullptr})) {
+        if (dy_opt && (r = prepare_e_run(g, dh_opt, dy_opt, C_opt, ebuf, wbuf, st))) return r;
+        seq::RcArgs ra{};
+        ra.kstar = kstar; ra.dict_idx = dict_idx; ra.pstart = pstart; ra.psrc = psrc;
+        ra.diag = g.diag_mode == PDSSM_DIAG_PER_STEP ? diag : nullptr;
+        ra.diag_dict = g.diag_mode == PDSSM_DIAG_PER_DICT ? static_cast<const float*>(diag) : nullptr;
+        ra.bias = bias_opt; ra.e = dy_opt ? static_cast<const void*>(ebuf) : dh_opt; ra.lam_in = lam_in_opt; ra.cs = cs;
+        ra.dbias = dbias; ra.ddiag = g.diag_mode == PDSSM_DIAG_PER_DICT ? static_cast<void*>(dDbuf) : ddiag;
+        ra.gsel = gsel; ra.dh0 = dh0_opt;
+        ra.H = (int)g.H; ra.L = (int)g.L; ra.N = (int)g.N; ra.K = (int)g.K; ra.tau = g.tau; ra.C = g.C; ra.flags = g.flags;
+        if ((r = bwd_seq_rc_run(g, ra, dy_opt != nullptr, srec, swm, sovf, st))) return r;
+        if (g.diag_mode == PDSSM_DIAG_PER_DICT)
+            return reduce_dict(g, kstar, dDbuf, static_cast<float*>(ddiag), rdpart, st);
+        return PDSSM_OK;
+    }
     const bool use_seq = !recompute && seq_applicable(g, {g.diag_mode == PDSSM_DIAG_PER_STEP ? diag : nullptr, h_saved, dh_opt, ebuf});
     if (env_path_is("seq") && !use_seq)
         return fail(PDSSM_ERR_UNSUPPORTED, "scan_bwd: PDSSM_PATH=seq but the single-chunk path does not apply");

@@ -49,8 +49,15 @@ RC_CASES = [
 
 
 @pytest.mark.parametrize("case", RC_CASES, ids=[str(c) for c in RC_CASES])
-def test_recompute_backward_parity(P, case, monkeypatch):
+@pytest.mark.parametrize("path", ["auto", "generic"])
+def test_recompute_backward_parity(P, case, path, monkeypatch):
+    """auto: one CTA per sequence (k_bwd_seq_rc) where N % 32 == 0 and N <= 128, else the generic
+    per-(sequence, chunk) kernel; generic: always the latter."""
     B, H, L, N, K, c, tau, bf16, pd, use_h0 = case
+    if path == "generic":
+        monkeypatch.setenv("PDSSM_PATH", "generic")
+    else:
+        monkeypatch.delenv("PDSSM_PATH", raising=False)
     inp = synth.scan_inputs(B, H, L, N, K, c, seed=L + N + tau, h0=use_h0, dh=True, per_dict=pd, bf16=bf16)
     d = dev_inputs(inp, bf16, pd)
     h0 = d.get("h0")
