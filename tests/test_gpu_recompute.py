@@ -91,8 +91,8 @@ def test_recompute_backward_parity(P, case, path, monkeypatch):
 
 
 def test_recompute_matches_saved_backward(P):
-    """Same forward, both backward modes: db and dh0 (which do not read h) are bitwise equal;
-    dD and g agree to f32 rounding (saved states are stored, recomputed ones replayed)."""
+    """Same forward, both backward modes (the generic saved-state kernels and the recompute kernel):
+    every output agrees to f32 rounding (different summation orders, and recomputed vs stored states)."""
     B, H, L, N, K, c, tau = 2, 2, 333, 64, 16, 2, 48
     inp = synth.scan_inputs(B, H, L, N, K, c, seed=5, h0=True, dh=True)
     d = dev_inputs(inp, False, False)
@@ -111,9 +111,8 @@ def test_recompute_matches_saved_backward(P):
     b = P.scan_bwd(d["kstar"], d["dict_idx"], d["diag"], None, f["chunk_state"], f["dims"], dh=d["dh"], h0=d["h0"],
                    bias=d["bias"])
     torch.cuda.synchronize()
-    assert torch.equal(a[0], b[0]) and torch.equal(a[3], b[3])
-    assert float((a[1] - b[1]).abs().max()) <= 1e-5 * float(a[1].abs().max())
-    assert float((a[2] - b[2]).abs().max()) <= 1e-5 * float(a[2].abs().max())
+    for x, y in zip(a, b):
+        assert float((x - y).abs().max()) <= 1e-5 * float(x.abs().max())
 
 
 def test_recompute_rejects_long_chunks(P):
