@@ -70,6 +70,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-layer", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: functional test of the multi-rank paths with several ranks sharing one GPU")
     ap.add_argument("--profile", action="store_true",
                     help="under ncu: one seed, no clock block, no per-step statistics, no CPU / e2e / layer legs")
     a = ap.parse_args()
@@ -496,7 +498,7 @@ def timed(torch, dist, st, stream, steps, world, dev, per_step=True):
         dist.barrier()
     el = t_start.elapsed_time(t_end) / 1e3
     if world > 1:
-        tt = torch.tensor([el], device=dev, dtype=torch.float64)
+        tt = torch.tensor([el], device=dev if dist.get_backend() == "nccl" else "cpu", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         el = float(tt.item())
     fw = [e[0].elapsed_time(e[1]) for e in ev]
@@ -517,10 +519,14 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % max(torch.cuda.device_count(), 1)   # (gloo tests: several ranks may share one GPU)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if a.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     cfg = BENCH_CONFIGS[a.config]
     dtype = a.dtype or cfg["dtype"]
     bf16 = dtype == "bf16"
@@ -613,7 +619,7 @@ def main():
         torch.cuda.synchronize()
         et = s0.elapsed_time(s1) / 1e3
         if world > 1:
-            tt = torch.tensor([et], device=dev, dtype=torch.float64)
+            tt = torch.tensor([et], device=dev if dist.get_backend() == "nccl" else "cpu", dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             et = float(tt.item())
         e2e = {"value": tokens_all * e_steps / et, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
