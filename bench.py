@@ -100,14 +100,14 @@ def peak_tflops(dtype):
     return bf if dtype == "bf16" else bf / 6.0
 
 
-def traffic_of(kernel, config):
+def traffic_of(kernel, config, dsuffix=""):
     """dram read+write bytes per launch of `kernel` from the committed ncu --set full capture."""
     p = os.path.join(ROOT, "profiles", "traffic_latest.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
         j = json.load(f)
-    return j.get(f"config{config}:{kernel}", j.get(kernel) if config == 2 else None)
+    return j.get(f"config{config}{dsuffix}:{kernel}", j.get(kernel) if (config == 2 and not dsuffix) else None)
 
 
 def count_launches(fn):
@@ -646,7 +646,7 @@ def main():
                            "parallelism": shard,
                            "l2": "inputs larger than L2 (>= 0.5 GB per step), no flush"},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                             "frac": achieved / peak, "traffic": traffic_of(dominant, a.config), "kernel": dominant,
+                             "frac": achieved / peak, "traffic": traffic_of(dominant, a.config, "" if dtype == BENCH_CONFIGS[a.config]["dtype"] else "_" + dtype), "kernel": dominant,
                              "algo_bytes_per_launch": dom_bytes, "peak_kind": peak_kind,
                              "traffic_source": "profiles/traffic_latest.json (ncu --set full, dram read+write per launch)"},
                 "step_hbm": {"achieved_gbs": step_gbs, "frac": step_gbs / peak, "fwd_ms_median": fwd_ms,

@@ -7,6 +7,7 @@ import subprocess
 import sys
 
 rep, out = sys.argv[1], sys.argv[2]
+prefix = sys.argv[3] if len(sys.argv) > 3 else ""   # e.g. "config4:" (merged into an existing file)
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 h = rows[0]
@@ -21,8 +22,14 @@ for r in rows[2:]:
         continue
     b = float(r[rd].replace(",", "")) * scale.get(unit_rd, 1) + float(r[wr].replace(",", "")) * scale.get(unit_wr, 1)
     res.setdefault(key, []).append(b)
-res = {key: sum(v) / len(v) for key, v in res.items()}
-res["source"] = rep
+res = {prefix + key: sum(v) / len(v) for key, v in res.items()}
+try:
+    old = json.load(open(out))
+except (OSError, ValueError):
+    old = {}
+old.update(res)
+old.setdefault("sources", {})[prefix or "config2:"] = rep
+old.pop("source", None)
 with open(out, "w") as f:
-    json.dump(res, f, indent=1)
+    json.dump(old, f, indent=1)
 print(json.dumps(res))
