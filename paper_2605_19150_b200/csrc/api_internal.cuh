@@ -223,6 +223,9 @@ inline bool path_fused_forced() {
 // ---------------------------------------------------------------------------
 
 constexpr size_t kSeqSmemBudget = 200 * 1024;
+// CTAs of the single-chunk kernels per SM when sequences outnumber the SMs: enough for one wave
+// of config 4 (1024 sequences: 7 per SM for the backward, whose CTA needs ~31 KB at N = 64 bf16)
+constexpr int kSeqMaxPerSm = 8;
 constexpr int kSeqG = seq::SEQ_G;     // backward group
 constexpr int kSeqGF = seq::SEQ_GF;   // forward group
 
@@ -242,7 +245,7 @@ inline int seq_ring(const Geo& g, bool bwd, bool agg, size_t esz_e, int spc = 1)
     const int G = seq_group(bwd, spc);
     const int ngroups = (int)ceil_div(g.L, G);
     const int64_t ctas = g.S / spc;
-    const int64_t per_sm = std::min<int64_t>(std::max<int64_t>(ceil_div(ctas, num_sms_dev()), 1), 4);
+    const int64_t per_sm = std::min<int64_t>(std::max<int64_t>(ceil_div(ctas, num_sms_dev()), 1), kSeqMaxPerSm);
     const size_t budget = std::min<size_t>(kSeqSmemBudget, (size_t)(226 * 1024) / (size_t)per_sm - 1024);
     int best = 0;
     for (int R = 2; R <= 16 && R <= ngroups + 1; ++R) {
