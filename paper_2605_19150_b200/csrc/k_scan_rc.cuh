@@ -186,6 +186,8 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq_rc(RcArgs a) {
             for (int r = 0; r < len; ++r) {
                 const int t = t0 + r;
                 const int k = kb[t];
+                const uint2 rc = rec[(size_t)k * N + i];   // this step's preimage record and trip code
+                const int m = wm[k * NW + w];
                 float Dr, Di = 0.f;
                 if constexpr (PD) {
                     Dr = dk[(size_t)k * row + i];
@@ -199,12 +201,23 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq_rc(RcArgs a) {
                 const float Br = ldact_s(Bp + i), Bi = NC == 2 ? ldact_s(Bp + N + i) : 0.f;
                 SV* vb = xf + fx * (N + 1);
                 vb[i] = fused::mk<NC>(Dr * hr - Di * hi_, Dr * hi_ + Di * hr);
-                const uint2 rc = rec[(size_t)k * N + i];
-                const int m = wm[k * NW + w];
+                uint32_t ga[CAP];   // shared addresses of the gather, before the barrier
+                {
+                    uint32_t lo4[4], hi4[4];
+                    const uint32_t vb_s = fused::smem_u32(vb);
+                    gather_addr4(rc.x, vb_s, SVB, lo4);
+                    gather_addr4(rc.y, vb_s, SVB, hi4);
+#pragma unroll
+                    for (int x = 0; x < 4; ++x) {
+                        ga[x] = lo4[x];
+                        ga[4 + x] = hi4[x];
+                    }
+                }
                 compute_sync(N);
                 if (r == 0 && i == 0 && gi >= 1) mbar_arrive(bars + R + ((gi - 1) % R));   // previous group consumed
-                float ar = 0.f, ai = 0.f;
+                float ar, ai;
                 if (m == WM_OVF) {   // preimage longer than the records: CSR plan (rare, warp-uniform)
+                    ar = ai = 0.f;
                     const size_t e = (size_t)h * K + k;
                     const int st = __ldg(a.pstart + e * (N + 1) + i), en = __ldg(a.pstart + e * (N + 1) + i + 1);
                     for (int x = st; x < en; ++x) {
@@ -212,14 +225,18 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq_rc(RcArgs a) {
                         ar += fused::re_of<NC>(v);
                         ai += fused::im_of<NC>(v);
                     }
-                } else {
+                } else if (m <= 4) {   // warp-uniform: the warp's in-degree fits 4 slots
+                    float vr[4], vi[4];
 #pragma unroll
-                    for (int x = 0; x < CAP; ++x) {
-                        const int src = __byte_perm(x < 4 ? rc.x : rc.y, 0u, 0x4440u + (uint32_t)(x & 3));
-                        const SV v = vb[src];   // past the in-degree: the zero slot N
-                        ar += fused::re_of<NC>(v);
-                        ai += fused::im_of<NC>(v);
-                    }
+                    for (int x = 0; x < 4; ++x) lds_sv<NC>(ga[x], vr[x], vi[x]);
+                    ar = (vr[0] + vr[1]) + (vr[2] + vr[3]);
+                    ai = (vi[0] + vi[1]) + (vi[2] + vi[3]);
+                } else {
+                    float vr[CAP], vi[CAP];
+#pragma unroll
+                    for (int x = 0; x < CAP; ++x) lds_sv<NC>(ga[x], vr[x], vi[x]);   // past the in-degree: zero slot
+                    ar = ((vr[0] + vr[1]) + (vr[2] + vr[3])) + ((vr[4] + vr[5]) + (vr[6] + vr[7]));
+                    ai = ((vi[0] + vi[1]) + (vi[2] + vi[3])) + ((vi[4] + vi[5]) + (vi[6] + vi[7]));
                 }
                 hr = ar + Br;
                 hi_ = NC == 2 ? ai + Bi : 0.f;
@@ -272,6 +289,12 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq_rc(RcArgs a) {
                 if (rr == 0 && i == 0) mbar_arrive(bars + R + ((gi - 1) % R));   // previous group consumed
                 const SV lp = lb[p];
                 const float pr = fused::re_of<NC>(lp), pm = fused::im_of<NC>(lp);
+                // the chain first: lambda_{t-1} = e_{t-1} + conj(D_t) lp (the next step's exchange waits on it)
+                const float lr_old = lr, li_old = li;
+                if (t > 0) {
+                    lr = er + Dr * pr + Di * pm;
+                    li = NC == 2 ? ei + Dr * pm - Di * pr : 0.f;
+                }
                 const float ddr = hr0 * pr + hi0 * pm, ddi = hr0 * pm - hi0 * pr;   // dD_t = conj(h_{t-1}) lp
                 if constexpr (PD) {
                     float* dd = static_cast<float*>(a.ddiag) + off;
@@ -286,10 +309,9 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq_rc(RcArgs a) {
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) gv += __shfl_xor_sync(0xffffffffu, gv, o);
                 if ((i & 31) == 0) gp[(size_t)(t - lo) * NW + w] = gv;
-                if (t > 0) {
-                    lr = er + Dr * pr + Di * pm;                                // lambda_{t-1} = e_{t-1} + conj(D_t) lp
-                    li = NC == 2 ? ei + Dr * pm - Di * pr : 0.f;
-                } else if (a.dh0) {                                          // dh0 = A_0^T lambda_0
+                (void)lr_old;
+                (void)li_old;
+                if (t == 0 && a.dh0) {                                       // dh0 = A_0^T lambda_0
                     a.dh0[(size_t)s * row + i] = Dr * pr + Di * pm;
                     if constexpr (NC == 2) a.dh0[(size_t)s * row + N + i] = Dr * pm - Di * pr;
                 }
