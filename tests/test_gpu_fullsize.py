@@ -126,10 +126,11 @@ def test_config5_s5_full_length(P):
 def test_config3_sequence_parallel_full_length(P):
     """Config 3 (L = 17984, B 4, H 8, N 128, real fp32, temporally persistent k*): the sequence-
     parallel construction with G = 8 virtual ranks (segments of 2248 steps, ragged against tau)
-    -- segment summaries, rank-ordered composition, local scans -- against the oracle on
-    sampled sequences, and the composed carries' index maps bit-exact."""
+    -- segment summaries, rank-ordered composition, local scans, and the mirrored backward (beta'
+    summaries composed from the right into each segment's incoming adjoint) -- against the oracle
+    on sampled sequences, and the composed carries' index maps bit-exact."""
     B, H, L, N, K, c, G = 4, 8, 17984, 128, 32, 1, 8
-    inp = synth.scan_inputs(B, H, L, N, K, c, seed=3000, h0=True, sticky=0.9)
+    inp = synth.scan_inputs(B, H, L, N, K, c, seed=3000, h0=True, sticky=0.9, dh=True)
     dev = {k: torch.from_numpy(v).cuda() for k, v in inp.items()}
     di = dev["dict_idx"].to(torch.int16)
     bounds = [(g * L // G, (g + 1) * L // G) for g in range(G)]
@@ -137,11 +138,24 @@ def test_config3_sequence_parallel_full_length(P):
     dims_g = [P.make_dims(B, H, e - s, N, K, c=c) for (s, e) in bounds]
     gathered = torch.cat([P.segment_summary(seg(dev["kstar"], s, e), di, seg(dev["diag"], s, e),
                                             seg(dev["bias"], s, e), dims_g[g]) for g, (s, e) in enumerate(bounds)])
-    hs, maps = [], []
+    hs, maps, fwd = [], [], []
     for g, (s, e) in enumerate(bounds):
         carry, m = P.compose_carry(gathered, g, G, dims_g[g], h0=dev["h0"])
         maps.append(m)
-        hs.append(P.scan_fwd(seg(dev["kstar"], s, e), di, seg(dev["diag"], s, e), seg(dev["bias"], s, e), h0=carry)["h"])
+        f = P.scan_fwd(seg(dev["kstar"], s, e), di, seg(dev["diag"], s, e), seg(dev["bias"], s, e), h0=carry)
+        fwd.append((f, carry))
+        hs.append(f["h"])
+    # the mirrored backward: per-segment beta' summaries, composed from the right (lam_in)
+    betas = torch.stack([P.segment_summary_bwd(seg(dev["kstar"], s, e), di, seg(dev["diag"], s, e), fwd[g][0]["chunk_state"],
+                                               dims_g[g], dh=seg(dev["dh"], s, e)) for g, (s, e) in enumerate(bounds)])
+    dbs, gs = [], []
+    for g, (s, e) in enumerate(bounds):
+        f, carry = fwd[g]
+        lam_in = P.compose_lambda(gathered, betas, g, G, dims_g[g])
+        db, _, gg, _ = P.scan_bwd(seg(dev["kstar"], s, e), di, seg(dev["diag"], s, e), f["h"], f["chunk_state"], dims_g[g],
+                                  dh=seg(dev["dh"], s, e), h0=carry, lam_in=lam_in, want_dh0=False)
+        dbs.append(db)
+        gs.append(gg)
     torch.cuda.synchronize()
     for (b, hh) in [(0, 0), (3, 7), (2, 4)]:
         sl = lambda a: a[b:b + 1, hh:hh + 1]
@@ -150,7 +164,11 @@ def test_config3_sequence_parallel_full_length(P):
         h_ref = O.scan_forward(Pm, Dz, bz, h0z)
         Pi, _ = O.prefix_maps(Pm, np.ones(Pm.shape))
         got = np.concatenate([O.planes_to_complex(x[b:b + 1, hh:hh + 1].cpu().numpy()) for x in hs], axis=2)
-        assert rel(got, h_ref) <= 1e-4, (b, hh)
+        check("sp8_h", got, h_ref, 1e-4)
+        db_r, _, g_r, _ = O.scan_backward(Pm, Dz, h_ref, O.planes_to_complex(sl(inp["dh"])), h0z)
+        check("sp8_db", np.concatenate([O.planes_to_complex(x[b:b + 1, hh:hh + 1].cpu().numpy()) for x in dbs], axis=2),
+              db_r, 1e-4)
+        check("sp8_g", np.concatenate([x[b:b + 1, hh:hh + 1].cpu().numpy() for x in gs], axis=2), g_r, 1e-4)
         for g, (s, e) in enumerate(bounds):
             if s > 0:
                 assert np.array_equal(maps[g][b, hh].cpu().numpy().astype(np.int64), Pi[0, 0, s - 1])
