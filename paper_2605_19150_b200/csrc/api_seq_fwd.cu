@@ -7,6 +7,8 @@ using namespace pdssm::api;
 namespace pdssm {
 namespace api {
 
+constexpr int SEQ_GF_ = seq::SEQ_GF;
+
 pdssm_status fwd_seq(const Geo& g, seq::SeqArgs& sa, uint8_t* rec, uint8_t* wm, uint8_t* ovf, cudaStream_t st) {
     seq::k_build_seq_plan<<<(unsigned)(g.H * g.K), (unsigned)g.N, (size_t)g.N * 2, st>>>(
         sa.dict_idx, rec, wm, ovf, const_cast<uint16_t*>(sa.pstart), const_cast<uint16_t*>(sa.psrc), (int)g.N, g.flags);
@@ -39,7 +41,9 @@ pdssm_status fwd_seq(const Geo& g, seq::SeqArgs& sa, uint8_t* rec, uint8_t* wm, 
                     // compile-time N for the production variants (no maps, no checks)
                     auto kern = seq::k_fwd_seq<T, NC, PD, AGG, CHK, 0>;
                     if constexpr (!AGG && !CHK) {
-                        if (g.N == 128) kern = seq::k_fwd_seq<T, NC, PD, false, false, 128>;
+                        if (g.N == 128)
+                            kern = getenv("PDSSM_SEQ_TIER") ? seq::k_fwd_seq<T, NC, PD, false, false, 128, 1, SEQ_GF_, true>
+                                                            : seq::k_fwd_seq<T, NC, PD, false, false, 128>;
                         else if (g.N == 64)
                             kern = spc == 2 ? (getenv("PDSSM_SEQ_NO_TIER") ? seq::k_fwd_seq<T, NC, PD, false, false, 64, 2, 16>
                                                                           : seq::k_fwd_seq<T, NC, PD, false, false, 64, 2, 16, true>)
