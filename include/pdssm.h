@@ -264,10 +264,11 @@ pdssm_status pdssm_scan_fwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
  *   h_saved    act [B][H][L][c][N]  the forward states h_t, or NULL: recompute mode
  *   bias_opt   act [B][H][L][c][N]  b_t, the forward's bias (required iff h_saved is NULL).
  *              Recompute mode (the O(L N)-activation-free backward of PAPER.md:190, :280):
- *              every (sequence, chunk) item replays its chunk forward from the carry in
- *              chunk_state (Alg. 1 Phase C) into shared memory and reads
- *              h_{t-1} from there; needs chunk * c * N * 4 <= ~200 KB, i.e. the forward and
- *              the backward must be called with the same (small) dims.chunk, else
+ *              each chunk is replayed forward from its carry in chunk_state (Alg. 1 Phase C,
+ *              PAPER.md:905-913) into shared memory and h_{t-1} is read from there -- one CTA per
+ *              sequence walking the chunks backwards (N % 32 == 0, N <= 128), else one CTA per
+ *              (sequence, chunk); needs chunk * c * N * 4 <= ~200 KB, i.e. the forward and the
+ *              backward must be called with the same (small) dims.chunk, else
  *              PDSSM_ERR_UNSUPPORTED.
  *   chunk_state                      the forward's chunk_state (reused Abar_c; carries)
  *   dh_opt     act [B][H][L][c][N]  direct state gradient (NULL = 0)
