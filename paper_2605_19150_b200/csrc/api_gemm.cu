@@ -74,15 +74,16 @@ bool tc_operands_ok(const Geo& g, std::initializer_list<const void*> ptrs) {
 template <typename T>
 constexpr int tc_stages() { return std::is_same<T, float>::value ? 2 : 4; }
 
-template <typename T, class Epi, bool BPRE = false>
+template <typename T, class Epi, bool BPRE = false, int BPRE_STAGES = 3>
 pdssm_status launch_tc_maps(const CUtensorMap& mA, const CUtensorMap& mB, int64_t kdim, int bn, tc::TileMap tm,
                             dim3 grid, Epi epi, cudaStream_t st, const char* what, const CUtensorMap* mBlo = nullptr) {
     constexpr bool SPLIT = std::is_same<T, float>::value;
-    // pre-split weights (bn <= 128): three stages of (A hi/lo + B hi/lo) slabs fit
-    constexpr int STAGES = BPRE ? 3 : tc_stages<T>();
+    // pre-split weights: three stages of (A hi/lo + B hi/lo) slabs fit at bn <= 128, four at bn <= 64
+    constexpr int STAGES = BPRE ? BPRE_STAGES : tc_stages<T>();
+    constexpr int BN_MAX = BPRE ? (BPRE_STAGES >= 4 ? 64 : 128) : 256;
     using SM = tc::Smem<T, STAGES, SPLIT>;
-    const size_t smem = SM::bytes(BPRE ? 128 : 256);   // sized for the largest tile: one attribute per instantiation
-    if (BPRE && bn > 128) return fail(PDSSM_ERR_UNSUPPORTED, "%s: pre-split weights need bn <= 128", what);
+    const size_t smem = SM::bytes(BN_MAX);   // sized for the largest tile: one attribute per instantiation
+    if (bn > BN_MAX) return fail(PDSSM_ERR_UNSUPPORTED, "%s: tile width %d above %d", what, bn, BN_MAX);
     auto kern = tc::k_gemm_tc<T, STAGES, SPLIT, Epi, BPRE>;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
@@ -151,7 +152,9 @@ template <typename T>
 pdssm_status readout_tc(const Geo& g, const T* hseq, const T* Cp, T* y, cudaStream_t st, const float* Cp_lo = nullptr) {
     const int64_t cN = g.nc * g.N;
     const bool pre = std::is_same<T, float>::value && Cp_lo != nullptr && g.P <= 128;
-    const int bn = (int)(g.P < 256 ? g.P : 256);
+    // pre-split fp32: 64-column tiles with four stages keep more of the states in flight
+    const bool narrow = pre && g.P % 64 == 0 && !getenv("PDSSM_READOUT_WIDE");
+    const int bn = narrow ? 64 : (int)(g.P < 256 ? g.P : 256);
     CUtensorMap mA, mB, mBl;
     const int64_t da[3] = {cN, g.L, g.S};
     const int64_t sa[2] = {cN * (int64_t)sizeof(T), g.L * cN * (int64_t)sizeof(T)};
@@ -161,6 +164,10 @@ pdssm_status readout_tc(const Geo& g, const T* hseq, const T* Cp, T* y, cudaStre
     const int tiles = (int)ceil_div(g.L, tc::BM);
     dim3 grid((unsigned)(tiles * g.S), (unsigned)ceil_div(g.P, bn));
     if constexpr (std::is_same<T, float>::value) {
+        if (pre && narrow)
+            return launch_tc_maps<T, tc::EpiReadout<T>, true, 4>(mA, mB, cN, bn, tc::TileMap{1, tiles, (int)g.H, (int)g.P},
+                                                                 grid, tc::EpiReadout<T>{y, (int)g.L, (int)g.H, (int)g.P},
+                                                                 st, "readout_tc", &mBl);
         if (pre)
             return launch_tc_maps<T, tc::EpiReadout<T>, true>(mA, mB, cN, bn, tc::TileMap{1, tiles, (int)g.H, (int)g.P},
                                                               grid, tc::EpiReadout<T>{y, (int)g.L, (int)g.H, (int)g.P}, st,

@@ -226,6 +226,8 @@ READOUT_CASES = [
     (32, 1, 16, 129, False),
     (16, 2, 32, 70, True),
     (64, 2, 128, 200, True),
+    (64, 2, 128, 300, False),    # fp32, P % 64 == 0: pre-split weights, 64-column tiles, four stages
+    (32, 1, 64, 129, False),
 ]
 
 
