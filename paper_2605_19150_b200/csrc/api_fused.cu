@@ -18,11 +18,14 @@ pdssm_status with_npl(int npl, F&& f) {
 // beside the head's tables, up to fused::WARPS_MAX (0: not even FUSED_MIN_WARPS fit).  More warps
 // hide more of the per-step latency (15 vs the fixed 11 of round 1: config 3 +10%, config 5 +6%).
 constexpr int FUSED_MIN_WARPS = 4;
+// Complex fp32 layouts stay at the round-1 count (11): more items in flight measured slower there
+// (config 2 at tau 64: 0.41 vs 0.34 ms forward -- the chunk replay's L2 reuse suffers).
 template <class LY>
 int fused_warps_of(int64_t K) {
     const size_t lim = 227 * 1024, tb = LY::t_bytes((int)K);
     if (tb >= lim) return 0;
-    const int w = (int)std::min<size_t>((lim - tb) / LY::w_bytes, (size_t)fused::WARPS_MAX);
+    const int cap = LY::ROW >= 2 * 128 * 4 ? fused::WARPS_FWD : fused::WARPS_MAX;
+    const int w = (int)std::min<size_t>((lim - tb) / LY::w_bytes, (size_t)cap);
     return w >= FUSED_MIN_WARPS ? w : 0;
 }
 

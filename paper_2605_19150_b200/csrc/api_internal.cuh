@@ -245,16 +245,25 @@ inline int seq_ring(const Geo& g, bool bwd, bool agg, size_t esz_e, int spc = 1)
     const int G = seq_group(bwd, spc);
     const int ngroups = (int)ceil_div(g.L, G);
     const int64_t ctas = g.S / spc;
-    const int64_t per_sm = std::min<int64_t>(std::max<int64_t>(ceil_div(ctas, num_sms_dev()), 1), kSeqMaxPerSm);
-    const size_t budget = std::min<size_t>(kSeqSmemBudget, (size_t)(226 * 1024) / (size_t)per_sm - 1024);
-    int best = 0;
-    for (int R = 2; R <= 16 && R <= ngroups + 1; ++R) {
-        seq::Layout ly((int)g.N, (int)g.K, R, G, g.nc, (int)g.act, (int)esz_e, g.diag_mode == PDSSM_DIAG_PER_DICT, agg, bwd,
-                       (int)g.L, spc);
-        if (ly.bytes <= budget) best = R;
+    const int64_t want = std::min<int64_t>(std::max<int64_t>(ceil_div(ctas, num_sms_dev()), 1), kSeqMaxPerSm);
+    // the largest ring at the wanted occupancy; if even two slots do not fit there, fewer CTAs per SM
+    // (down to one): occupancy degrades, applicability does not depend on the batch size
+    for (int64_t per_sm = want; per_sm >= 1; --per_sm) {
+        const size_t budget = std::min<size_t>(kSeqSmemBudget, (size_t)(226 * 1024) / (size_t)per_sm - 1024);
+        int best = 0;
+        for (int R = 2; R <= 16 && R <= ngroups + 1; ++R) {
+            seq::Layout ly((int)g.N, (int)g.K, R, G, g.nc, (int)g.act, (int)esz_e, g.diag_mode == PDSSM_DIAG_PER_DICT,
+                           agg, bwd, (int)g.L, spc);
+            if (ly.bytes <= budget) best = R;
+        }
+        if (best == 0 && ngroups <= 1) {
+            seq::Layout ly((int)g.N, (int)g.K, 2, G, g.nc, (int)g.act, (int)esz_e, g.diag_mode == PDSSM_DIAG_PER_DICT, agg,
+                           bwd, (int)g.L, spc);
+            if (ly.bytes <= budget) best = 2;
+        }
+        if (best >= 2) return best;
     }
-    if (best == 0 && ngroups <= 1) best = 2;
-    return best;
+    return 0;
 }
 
 inline bool seq_applicable(const Geo& g, std::initializer_list<const void*> ptrs) {
