@@ -51,10 +51,19 @@ inline bool env_path_is(const char* v) {
 // CTA-per-sequence kernels; otherwise tau = 64 (chunked, decoupled look-back).
 inline int default_tau(const pdssm_dims* d) {
     const int64_t S = d->batch * d->heads;
+    const int64_t sms = num_sms_dev();
     const bool forced_chunked = env_path_is("fused") || env_path_is("generic");
-    if (!forced_chunked && seq_shape_ok(d->state, d->dict, d->len, d->is_complex, d->dtype == PDSSM_BF16 ? 2 : 4) &&
-        (env_path_is("seq") || S * 10 >= (int64_t)num_sms_dev() * 6) && d->len <= (int64_t)1 << 30)
-        return (int)d->len;
+    const size_t act = d->dtype == PDSSM_BF16 ? 2 : 4;
+    if (!forced_chunked && seq_shape_ok(d->state, d->dict, d->len, d->is_complex, act) && d->len <= (int64_t)1 << 30) {
+        const int64_t rowb = (int64_t)d->is_complex * d->state * (int64_t)act;   // bytes of one D / b / h row
+        // one CTA per sequence when the sequences fill the GPU and a step moves enough bytes
+        if (env_path_is("seq") || (S * 10 >= sms * 6 && (rowb > 512 || S >= 2 * sms))) return (int)d->len;
+        // otherwise the chunked single-CTA path ("seqc"): ~4 CTAs per SM, two passes per chunk but
+        // the per-step chain of a chunk is tau steps long instead of L
+        const int64_t C = ceil_div(4 * sms, S);
+        const int64_t tau = ceil_div(d->len, C);
+        if (env_path_is("seqc") || (tau >= 256 && tau <= seq::LMAX)) return (int)std::max<int64_t>(tau, 1);
+    }
     return 64;
 }
 
@@ -241,10 +250,12 @@ inline int seq_group(bool bwd, int spc) { return bwd ? (spc > 1 ? 8 : kSeqG) : (
 
 // ring depth R for this shape (0: the layout does not fit).  When there are more CTAs than
 // SMs, the budget is split so that ceil(#CTAs / #SMs) CTAs (up to 4) fit per SM.
-inline int seq_ring(const Geo& g, bool bwd, bool agg, size_t esz_e, int spc = 1) {
+// Lk: the steps one CTA covers (g.L, or tau for the chunked single-CTA path); ctas: CTAs launched
+inline int seq_ring(const Geo& g, bool bwd, bool agg, size_t esz_e, int spc = 1, int64_t Lk = 0, int64_t ctas_in = 0) {
     const int G = seq_group(bwd, spc);
-    const int ngroups = (int)ceil_div(g.L, G);
-    const int64_t ctas = g.S / spc;
+    if (Lk <= 0) Lk = g.L;
+    const int ngroups = (int)ceil_div(Lk, G);
+    const int64_t ctas = ctas_in > 0 ? ctas_in : g.S / spc;
     const int64_t want = std::min<int64_t>(std::max<int64_t>(ceil_div(ctas, num_sms_dev()), 1), kSeqMaxPerSm);
     // the largest ring at the wanted occupancy; if even two slots do not fit there, fewer CTAs per SM
     // (down to one): occupancy degrades, applicability does not depend on the batch size
@@ -253,17 +264,30 @@ inline int seq_ring(const Geo& g, bool bwd, bool agg, size_t esz_e, int spc = 1)
         int best = 0;
         for (int R = 2; R <= 16 && R <= ngroups + 1; ++R) {
             seq::Layout ly((int)g.N, (int)g.K, R, G, g.nc, (int)g.act, (int)esz_e, g.diag_mode == PDSSM_DIAG_PER_DICT,
-                           agg, bwd, (int)g.L, spc);
+                           agg, bwd, (int)Lk, spc);
             if (ly.bytes <= budget) best = R;
         }
         if (best == 0 && ngroups <= 1) {
             seq::Layout ly((int)g.N, (int)g.K, 2, G, g.nc, (int)g.act, (int)esz_e, g.diag_mode == PDSSM_DIAG_PER_DICT, agg,
-                           bwd, (int)g.L, spc);
+                           bwd, (int)Lk, spc);
             if (ly.bytes <= budget) best = 2;
         }
         if (best >= 2) return best;
     }
     return 0;
+}
+
+// chunked single-CTA path: one CTA per (sequence, chunk) with the single-chunk kernels' step
+// (k_fwd_seq / k_bwd_seq MODE 1 / 2) around the generic Phase B / B' carry kernels
+inline bool seqc_applicable(const Geo& g, std::initializer_list<const void*> ptrs) {
+    if (g.C <= 1 || env_path_is("fused") || env_path_is("generic") || env_path_is("seq")) return false;
+    if (!env_path_is("seqc") && g.tau <= fused::TAUMAX) return false;   // short chunks: the warp-per-chunk path
+    if (!seq_shape_ok(g.N, g.K, g.tau, g.nc, g.act)) return false;
+    for (const void* p : ptrs)
+        if (misaligned(p, 16)) return false;
+    const int64_t ctas = g.S * g.C;
+    return seq_ring(g, false, true, g.act, 1, g.tau, ctas) >= 2 && seq_ring(g, true, false, 4, 1, g.tau, ctas) >= 2 &&
+           seq_ring(g, true, false, g.act, 1, g.tau, ctas) >= 2;
 }
 
 inline bool seq_applicable(const Geo& g, std::initializer_list<const void*> ptrs) {
@@ -287,6 +311,9 @@ inline pdssm_status seq_set_smem(const void* f, size_t bytes) {
 // api_seq_fwd.cu / api_seq_bwd.cu: single-chunk path (one CTA per sequence)
 pdssm_status fwd_seq(const Geo& g, seq::SeqArgs& sa, uint8_t* rec, uint8_t* wm, uint8_t* ovf, cudaStream_t st);
 pdssm_status bwd_seq_run(const Geo& g, seq::SeqArgs& sa, bool e_f32, cudaStream_t st);
+// chunked single-CTA path (MODE 1 / phase B / MODE 2)
+pdssm_status fwd_seqc(const Geo& g, seq::SeqArgs& sa, uint8_t* rec, uint8_t* wm, uint8_t* ovf, cudaStream_t st);
+pdssm_status bwd_seqc_run(const Geo& g, seq::SeqArgs& sa, bool e_f32, cudaStream_t st);
 // api_seq_bwd.cu: recompute-mode backward, one CTA per sequence (k_scan_rc.cuh)
 bool bwd_seq_rc_applicable(const Geo& g, std::initializer_list<const void*> ptrs);
 pdssm_status bwd_seq_rc_run(const Geo& g, seq::RcArgs& ra, bool e_f32, uint8_t* rec, uint8_t* wm, uint8_t* ovf,

@@ -8,6 +8,8 @@ using namespace pdssm::api;
 namespace pdssm {
 namespace api {
 
+constexpr int SEQ_G_ = seq::SEQ_G;
+
 template <typename TE>
 pdssm_status bwd_seq(const Geo& g, seq::SeqArgs& sa, cudaStream_t st) {
     return with_act(g.dtype, [&](auto tv) {
@@ -94,6 +96,52 @@ pdssm_status bwd_seq_rc_run(const Geo& g, seq::RcArgs& ra, bool e_f32, uint8_t* 
             });
         });
     });
+}
+
+
+// chunked single-CTA path: Phase A' (MODE 1: beta'_c) -> Phase B' (mu chain through the forward
+// aggregates: k_bwd_phaseB) -> Phase C' (MODE 2: replay from e + mu_c, emitting the gradients)
+template <typename TE>
+pdssm_status bwd_seqc(const Geo& g, seq::SeqArgs& sa, cudaStream_t st) {
+    const int64_t ctas = g.S * g.C;
+    sa.G = kSeqG;
+    sa.spc = 1;
+    sa.tau = g.tau;
+    sa.C = g.C;
+    const int thr = threads_for(g.N);
+    return with_act(g.dtype, [&](auto tv) {
+        using T = decltype(tv);
+        using TEE = typename std::conditional<std::is_same<TE, void>::value, T, TE>::type;
+        sa.R = seq_ring(g, true, false, sizeof(TEE), 1, g.tau, ctas);
+        return with_nc(g.nc, [&](auto ncv) {
+            constexpr int NC = decltype(ncv)::value;
+            return with_pd(g.diag_mode, [&](auto pdv) {
+                constexpr bool PD = decltype(pdv)::value;
+                seq::Layout ly((int)g.N, (int)g.K, sa.R, sa.G, NC, (int)sizeof(T), (int)sizeof(TEE), PD, false, true, g.tau,
+                               1);
+                auto kA = g.N == 128 ? seq::k_bwd_seq<T, TEE, NC, PD, 128, 1, SEQ_G_, 1>
+                          : g.N == 64 ? seq::k_bwd_seq<T, TEE, NC, PD, 64, 1, SEQ_G_, 1>
+                                      : seq::k_bwd_seq<T, TEE, NC, PD, 0, 1, SEQ_G_, 1>;
+                auto kC = g.N == 128 ? seq::k_bwd_seq<T, TEE, NC, PD, 128, 1, SEQ_G_, 2>
+                          : g.N == 64 ? seq::k_bwd_seq<T, TEE, NC, PD, 64, 1, SEQ_G_, 2>
+                                      : seq::k_bwd_seq<T, TEE, NC, PD, 0, 1, SEQ_G_, 2>;
+                pdssm_status rr = seq_set_smem((const void*)kA, ly.bytes);
+                if (rr) return rr;
+                kA<<<(unsigned)ctas, (unsigned)g.N + 32, ly.bytes, st>>>(sa);
+                if ((rr = cuda_check("bwd_seqc_A"))) return rr;
+                k_bwd_phaseB<NC><<<(unsigned)g.S, thr, (size_t)NC * g.N * 4, st>>>(sa.cs, sa.betap, sa.lam_in, sa.mu,
+                                                                                     nullptr, (int)g.N, g.C);
+                if ((rr = cuda_check("bwd_seqc_B"))) return rr;
+                if ((rr = seq_set_smem((const void*)kC, ly.bytes))) return rr;
+                kC<<<(unsigned)ctas, (unsigned)g.N + 32, ly.bytes, st>>>(sa);
+                return cuda_check("bwd_seqc_C");
+            });
+        });
+    });
+}
+
+pdssm_status bwd_seqc_run(const Geo& g, seq::SeqArgs& sa, bool e_f32, cudaStream_t st) {
+    return e_f32 ? bwd_seqc<float>(g, sa, st) : bwd_seqc<void>(g, sa, st);
 }
 
 }  // namespace api

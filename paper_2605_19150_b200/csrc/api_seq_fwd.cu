@@ -73,6 +73,52 @@ pdssm_status fwd_seq(const Geo& g, seq::SeqArgs& sa, uint8_t* rec, uint8_t* wm, 
     });
 }
 
+
+// chunked single-CTA path: Phase A (MODE 1, every chunk's aggregate) -> Phase B (carries and, under
+// EXPORT_MAPS, the exclusive prefix maps: k_fwd_phaseB) -> Phase C (MODE 2, replay storing h)
+pdssm_status fwd_seqc(const Geo& g, seq::SeqArgs& sa, uint8_t* rec, uint8_t* wm, uint8_t* ovf, cudaStream_t st) {
+    seq::k_build_seq_plan<<<(unsigned)(g.H * g.K), (unsigned)g.N, (size_t)g.N * 2, st>>>(
+        sa.dict_idx, rec, wm, ovf, const_cast<uint16_t*>(sa.pstart), const_cast<uint16_t*>(sa.psrc), (int)g.N, g.flags);
+    pdssm_status r = cuda_check("build_seq_plan");
+    if (r) return r;
+    const int64_t ctas = g.S * g.C;
+    sa.G = kSeqGF;
+    sa.spc = 1;
+    sa.tau = g.tau;
+    sa.C = g.C;
+    const int thr = threads_for(g.N);
+    return with_act(g.dtype, [&](auto tv) {
+        using T = decltype(tv);
+        return with_nc(g.nc, [&](auto ncv) {
+            constexpr int NC = decltype(ncv)::value;
+            return with_pd(g.diag_mode, [&](auto pdv) {
+                constexpr bool PD = decltype(pdv)::value;
+                auto launch = [&](auto kern, bool compose, const char* what) -> pdssm_status {
+                    sa.R = seq_ring(g, false, compose, g.act, 1, g.tau, ctas);
+                    seq::Layout ly((int)g.N, (int)g.K, sa.R, sa.G, NC, (int)sizeof(T), (int)sizeof(T), PD, compose, false,
+                                   g.tau, 1);
+                    pdssm_status rr = seq_set_smem((const void*)kern, ly.bytes);
+                    if (rr) return rr;
+                    kern<<<(unsigned)ctas, (unsigned)g.N + 32, ly.bytes, st>>>(sa);
+                    return cuda_check(what);
+                };
+                auto kA = g.N == 128 ? seq::k_fwd_seq<T, NC, PD, false, false, 128, 1, SEQ_GF_, false, 1>
+                          : g.N == 64 ? seq::k_fwd_seq<T, NC, PD, false, false, 64, 1, SEQ_GF_, false, 1>
+                                      : seq::k_fwd_seq<T, NC, PD, false, false, 0, 1, SEQ_GF_, false, 1>;
+                auto kC = g.N == 128 ? seq::k_fwd_seq<T, NC, PD, false, false, 128, 1, SEQ_GF_, false, 2>
+                          : g.N == 64 ? seq::k_fwd_seq<T, NC, PD, false, false, 64, 1, SEQ_GF_, false, 2>
+                                      : seq::k_fwd_seq<T, NC, PD, false, false, 0, 1, SEQ_GF_, false, 2>;
+                pdssm_status rr = launch(kA, true, "fwd_seqc_A");
+                if (rr) return rr;
+                k_fwd_phaseB<NC><<<(unsigned)g.S, thr, (size_t)NC * g.N * 4 + (size_t)g.N * 2 + 16, st>>>(
+                    sa.cs, sa.h0, sa.maps, nullptr, (int)g.N, g.C);
+                if ((rr = cuda_check("fwd_seqc_B"))) return rr;
+                return launch(kC, false, "fwd_seqc_C");
+            });
+        });
+    });
+}
+
 }  // namespace api
 }  // namespace pdssm
 

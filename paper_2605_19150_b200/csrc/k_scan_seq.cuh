@@ -92,6 +92,9 @@ struct SeqArgs {
     float* dh0;                 // bwd
     int H, L, N, K, R, G;
     int spc;                    // sequences per CTA (the host requires B % spc == 0)
+    int tau, C;                 // chunk modes (MODE != 0): chunk length and chunks per sequence
+    float* mu;                  // bwd MODE 2: incoming adjoint mu_c [S][C][NC][N] (k_bwd_phaseB)
+    float* betap;               // bwd MODE 1: beta'_c out [S][C][NC][N]
     uint32_t flags;
 };
 
@@ -228,20 +231,33 @@ constexpr int SEQ_GF = 32;   // forward: steps per ring slot
 // p * SPC .. p * SPC + SPC - 1.  GF: steps per TMA group.
 // TIER: warp-uniform two-tier gather (4 slots when the warp's in-degree <= 4, else 8): fewer
 // instructions per step, for the issue-bound launches (several CTAs per SM).
-template <typename T, int NC, bool PD, bool AGG, bool CHECK, int NN, int SPC = 1, int GF = SEQ_GF, bool TIER = false>
+// MODE (one CTA per (sequence, chunk), SPC = 1; the chunked single-CTA path, "seqc"):
+//   0  the whole sequence (tau = L);
+//   1  Alg. 1 Phase A of chunk c: replay from a zero state without storing, composing (pi, d)
+//      thread-locally; the final state is beta_bar_c -> chunk_state (pi_bar, d_bar, beta_bar);
+//   2  Alg. 1 Phase C of chunk c: replay from carry_c (chunk_state, k_fwd_phaseB) storing h.
+template <typename T, int NC, bool PD, bool AGG, bool CHECK, int NN, int SPC = 1, int GF = SEQ_GF, bool TIER = false,
+          int MODE = 0>
 __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
     using SV = typename fused::SVal<NC>::type;
     constexpr int G = GF;
     constexpr int SVB = (int)sizeof(SV);
+    constexpr bool CHUNK = MODE != 0;
+    constexpr bool COMPOSE = AGG || MODE == 1;   // (pi, d) composed alongside
+    static_assert(!CHUNK || (SPC == 1 && !AGG), "chunk modes: one sequence per CTA, maps from k_fwd_phaseB");
     extern __shared__ __align__(128) uint8_t smem[];
-    const int N = NN ? NN : a.N, K = a.K, L = a.L, R = a.R;
+    const int C = CHUNK ? a.C : 1;
+    const int cidx = CHUNK ? (int)(blockIdx.x % C) : 0;
+    const int tb = cidx * (CHUNK ? a.tau : 0);                    // first step of the chunk
+    const int N = NN ? NN : a.N, K = a.K, L = CHUNK ? min(a.tau, a.L - tb) : a.L, R = a.R;
     const int i = threadIdx.x, NW = N >> 5;
-    const int h = blockIdx.x % a.H, pidx = blockIdx.x / a.H;
+    const int sblk = CHUNK ? (int)(blockIdx.x / C) : (int)blockIdx.x;
+    const int h = sblk % a.H, pidx = sblk / a.H;
     const int sub = (SPC > 1 && i < SPC * N) ? i / N : 0;   // this thread's sequence within the CTA
     const int il = i - sub * N;                             // its state
     const int w = il >> 5;                                  // its warp within the sequence
     const int s = (pidx * SPC + sub) * a.H + h;
-    const Layout Ly(N, K, R, G, NC, (int)sizeof(T), (int)sizeof(T), PD, AGG, false, L, SPC);
+    const Layout Ly(N, K, R, G, NC, (int)sizeof(T), (int)sizeof(T), PD, COMPOSE, false, CHUNK ? a.tau : L, SPC);
     uint8_t* ring = smem + Ly.ring;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Ly.bars);
     char* xbc = reinterpret_cast<char*>(smem + Ly.x + sub * Ly.xs);
@@ -252,20 +268,20 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
     uint16_t* prow = reinterpret_cast<uint16_t*>(smem + Ly.prow);
     float* dk = reinterpret_cast<float*>(smem + Ly.dk);
     const size_t row = (size_t)NC * N;
-    const size_t seq0 = (size_t)s * L;
+    const size_t seq0 = (size_t)s * a.L + tb;   // global row of local step 0
     const int ngroups = (L + G - 1) / G;
     const uint64_t pol = fused::policy_evict_first();
     // The sequence's k* first: it does not depend on the plan launch that precedes this
     // kernel, which may still be running (programmatic dependent launch); wait for it only
     // before the tables it writes are read.
-    for (int j = 0; j < SPC; ++j) stage_k(a, smem + Ly.kb + j * Ly.kbs, (size_t)((pidx * SPC + j) * a.H + h) * L, L);
+    for (int j = 0; j < SPC; ++j) stage_k(a, smem + Ly.kb + j * Ly.kbs, (size_t)((pidx * SPC + j) * a.H + h) * a.L + tb, L);
     asm volatile("griddepcontrol.wait;" ::: "memory");
     {   // one-time tables of head h (k* zero-padded by 2)
         const int NT = blockDim.x;
         const uint2* gr = reinterpret_cast<const uint2*>(a.rec) + (size_t)h * K * N;
         for (int x = i; x < K * N; x += NT) rec[x] = __ldg(gr + x);
         for (int x = i; x < K * NW; x += NT) wm[x] = a.wm[(size_t)h * K * NW + x];
-        if constexpr (AGG)
+        if constexpr (COMPOSE)
             for (int x = i; x < K * N; x += NT) prow[x] = (uint16_t)min((int)__ldg(a.dict_idx + (size_t)h * K * N + x), N - 1);
         if constexpr (PD)
             for (int x = i; x < K * NC * N; x += NT) dk[x] = __ldg(a.diag_dict + (size_t)h * K * NC * N + x);
@@ -296,7 +312,7 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
         uint8_t* dst = ring + (size_t)slot * Ly.slot;
         fused::mbar_expect_tx(bars + slot, (uint32_t)(SPC * ((PD ? 0 : len * ROWB) + len * ROWB)));
         for (int j = 0; j < SPC; ++j) {
-            const size_t sj0 = (size_t)((pidx * SPC + j) * a.H + h) * L;
+            const size_t sj0 = (size_t)((pidx * SPC + j) * a.H + h) * a.L + tb;
             if constexpr (!PD)
                 fused::tma_1d_hint(dst + j * G * ROWB, static_cast<const T*>(a.diag) + (sj0 + t) * row, len * ROWB,
                                    bars + slot, pol);
@@ -309,7 +325,11 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
         return;
     }
     float hr = 0.f, hi = 0.f;
-    if (a.h0) {
+    if constexpr (MODE == 2) {   // carry_c of this chunk
+        const size_t ci = (size_t)s * C + cidx;
+        hr = a.cs.carry[ci * row + il];
+        if constexpr (NC == 2) hi = a.cs.carry[ci * row + N + il];
+    } else if (MODE == 0 && a.h0) {
         hr = a.h0[(size_t)s * row + il];
         if constexpr (NC == 2) hi = a.h0[(size_t)s * row + N + il];
     }
@@ -462,12 +482,16 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
         }
         hr = ar + bcr;
         hi = NC == 2 ? ai + bci : 0.f;
-        st_stream<T>(hout, hr, pol);
-        if constexpr (NC == 2) st_stream<T>(hout + N, hi, pol);
-        hout += row;
+        if constexpr (MODE != 1) {
+            st_stream<T>(hout, hr, pol);
+            if constexpr (NC == 2) st_stream<T>(hout + N, hi, pol);
+            hout += row;
+        }
         if constexpr (AGG) {
             br = cr + bcr;
             bi = NC == 2 ? ci + bci : 0.f;
+        }
+        if constexpr (COMPOSE) {
             // pi / d composition: d <- D_t[pi] d, pi <- P_t[pi]
             float pr, pm = 0.f;
             if constexpr (PD) {
@@ -498,6 +522,18 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
     };
     if (any_ovf) run(std::true_type{});
     else run(std::false_type{});
+    if constexpr (MODE == 1) {   // the chunk's aggregate: beta_bar is the replay from zero
+        const size_t ci = (size_t)s * C + cidx;
+        a.cs.pi[ci * N + il] = (uint16_t)pi;
+        a.cs.d[ci * row + il] = dr;
+        a.cs.beta[ci * row + il] = hr;
+        if constexpr (NC == 2) {
+            a.cs.d[ci * row + N + il] = di;
+            a.cs.beta[ci * row + N + il] = hi;
+        }
+        return;
+    }
+    if constexpr (MODE == 2) return;
     // chunk_state of the single chunk: carry_0 = h0; aggregate (pi_bar, d_bar, beta_bar)
     {
         a.cs.carry[(size_t)s * row + il] = a.h0 ? a.h0[(size_t)s * row + il] : 0.f;
@@ -524,20 +560,33 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
 // read a step earlier) ; refill ; operands of step t-1 (D, e, h from the ring row, P) ;
 // lambda_{t-1} = e_{t-1} + conj(D_t) lp ; dD_t store ; this thread's g_t term -> tile.
 // SPC > 1 (N <= 64): SPC sequences of one head per CTA, as in k_fwd_seq.
-template <typename T, typename TE, int NC, bool PD, int NN, int SPC = 1, int GB = SEQ_G>
+// MODE (chunked single-CTA path, one CTA per (sequence, chunk), SPC = 1):
+//   0  the whole sequence;
+//   1  Phase A' of chunk c: reverse local scan from a zero incoming adjoint, nothing stored but
+//      beta'_c = A_{s_c}^T lambda_loc_{s_c} -> a.betap (no h rows are read);
+//   2  Phase C' of chunk c: replay from lambda_{e_c} = e_{e_c} + mu_c (k_bwd_phaseB), emitting
+//      db, dD, g (and dh0 at chunk 0).
+template <typename T, typename TE, int NC, bool PD, int NN, int SPC = 1, int GB = SEQ_G, int MODE = 0>
 __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq(SeqArgs a) {
     using SV = typename fused::SVal<NC>::type;
     constexpr int G = GB;
     static_assert(32 % G == 0, "g_t is reduced every 32 steps: G must divide 32");
     constexpr int SVB = (int)sizeof(SV);
+    constexpr bool CHUNK = MODE != 0;
+    constexpr bool EMIT = MODE != 1;   // db, dD, g stored (and h rows read)
+    static_assert(!CHUNK || SPC == 1, "chunk modes: one sequence per CTA");
     extern __shared__ __align__(128) uint8_t smem[];
-    const int N = NN ? NN : a.N, K = a.K, L = a.L, R = a.R;
+    const int C = CHUNK ? a.C : 1;
+    const int cidx = CHUNK ? (int)(blockIdx.x % C) : 0;
+    const int tb = cidx * (CHUNK ? a.tau : 0);
+    const int N = NN ? NN : a.N, K = a.K, L = CHUNK ? min(a.tau, a.L - tb) : a.L, R = a.R;
     const int jt = threadIdx.x;
-    const int h = blockIdx.x % a.H, pidx = blockIdx.x / a.H;
+    const int sblk = CHUNK ? (int)(blockIdx.x / C) : (int)blockIdx.x;
+    const int h = sblk % a.H, pidx = sblk / a.H;
     const int sub = (SPC > 1 && jt < SPC * N) ? jt / N : 0;
     const int j = jt - sub * N;                           // this thread's source state
     const int s = (pidx * SPC + sub) * a.H + h;
-    const Layout Ly(N, K, R, G, NC, (int)sizeof(T), (int)sizeof(TE), PD, false, true, L, SPC);
+    const Layout Ly(N, K, R, G, NC, (int)sizeof(T), (int)sizeof(TE), PD, false, true, CHUNK ? a.tau : L, SPC);
     uint8_t* ring = smem + Ly.ring;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Ly.bars);
     char* xbc = reinterpret_cast<char*>(smem + Ly.x + sub * Ly.xs);
@@ -546,14 +595,14 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq(SeqArgs a) {
     float* dk = reinterpret_cast<float*>(smem + Ly.dk);
     float* gs = reinterpret_cast<float*>(smem + Ly.gs + sub * Ly.gss);   // [32][N+1] g terms, then [32][NW] partials
     const size_t row = (size_t)NC * N;
-    const size_t seq0 = (size_t)s * L;
+    const size_t seq0 = (size_t)s * a.L + tb;   // global row of local step 0
     const int ngroups = (L + G - 1) / G;
     const uint64_t pol = fused::policy_evict_first();
     const TE* ein = static_cast<const TE*>(a.bias);
     for (int x = jt; x < K * N; x += blockDim.x) prow[x] = (uint16_t)min((int)__ldg(a.dict_idx + (size_t)h * K * N + x), N - 1);
     if constexpr (PD)
         for (int x = jt; x < K * NC * N; x += blockDim.x) dk[x] = __ldg(a.diag_dict + (size_t)h * K * NC * N + x);
-    for (int q = 0; q < SPC; ++q) stage_k(a, smem + Ly.kb + q * Ly.kbs, (size_t)((pidx * SPC + q) * a.H + h) * L, L);
+    for (int q = 0; q < SPC; ++q) stage_k(a, smem + Ly.kb + q * Ly.kbs, (size_t)((pidx * SPC + q) * a.H + h) * a.L + tb, L);
     if (jt == 0) {
         for (int q = 0; q < 2 * R; ++q) fused::mbar_init(bars + q, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -567,22 +616,26 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq(SeqArgs a) {
     auto issue = [&](int g, int slot) {
         const int t_hi = L - 1 - g * G, t_lo = max(t_hi - G + 1, 0), len = t_hi - t_lo + 1;
         uint8_t* dst = ring + (size_t)slot * Ly.slot;
-        const int f_first = max(t_lo - 1, 0);                 // e_{t-1}, h_{t-1} rows needed for t >= 1
+        const int f_first = max(t_lo - 1, 0);                 // e_{t-1} rows needed for local t >= 1
         const int f_cnt = max(0, t_hi - 1 - f_first + 1);
         const int f_off = f_first - (t_lo - 1);
+        // h_{t-1} rows: also the row before a chunk that does not start the sequence
+        const int h_first = (tb > 0) ? t_lo - 1 : f_first;
+        const int h_cnt = EMIT ? max(0, t_hi - 1 - h_first + 1) : 0;
+        const int h_off = h_first - (t_lo - 1);
         fused::mbar_expect_tx(bars + slot,
-                              (uint32_t)(SPC * ((PD ? 0 : len * ROWB) + (ein ? f_cnt * EROWB : 0) + f_cnt * ROWB)));
+                              (uint32_t)(SPC * ((PD ? 0 : len * ROWB) + (ein ? f_cnt * EROWB : 0) + h_cnt * ROWB)));
         for (int q = 0; q < SPC; ++q) {
-            const size_t sq0 = (size_t)((pidx * SPC + q) * a.H + h) * L;
+            const size_t sq0 = (size_t)((pidx * SPC + q) * a.H + h) * a.L + tb;
             if constexpr (!PD)
                 fused::tma_1d_hint(dst + q * G * ROWB, static_cast<const T*>(a.diag) + (sq0 + t_lo) * row, len * ROWB,
                                    bars + slot, pol);
             if (ein && f_cnt > 0)
                 fused::tma_1d_hint(dst + OFF_E + q * G * EROWB + (size_t)f_off * EROWB, ein + (sq0 + f_first) * row,
                                    f_cnt * EROWB, bars + slot, pol);
-            if (f_cnt > 0)
-                fused::tma_1d_hint(dst + OFF_H + q * G * ROWB + (size_t)f_off * ROWB,
-                                   static_cast<const T*>(a.hsaved) + (sq0 + f_first) * row, f_cnt * ROWB, bars + slot, pol);
+            if (h_cnt > 0)
+                fused::tma_1d_hint(dst + OFF_H + q * G * ROWB + (size_t)h_off * ROWB,
+                                   static_cast<const T*>(a.hsaved) + (sq0 + h_first) * row, h_cnt * ROWB, bars + slot, pol);
         }
     };
     if (jt >= SPC * N) {   // producer warp
@@ -594,9 +647,15 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq(SeqArgs a) {
         lr = ldact_s(ein + (seq0 + L - 1) * row + j);
         if constexpr (NC == 2) li = ldact_s(ein + (seq0 + L - 1) * row + N + j);
     }
-    if (a.lam_in) {
-        lr += a.lam_in[(size_t)s * row + j];
-        if constexpr (NC == 2) li += a.lam_in[(size_t)s * row + N + j];
+    if constexpr (MODE == 0) {
+        if (a.lam_in) {
+            lr += a.lam_in[(size_t)s * row + j];
+            if constexpr (NC == 2) li += a.lam_in[(size_t)s * row + N + j];
+        }
+    } else if (MODE == 2) {   // mu_c: the adjoint entering this chunk from the chunks after it
+        const size_t ci = (size_t)s * C + cidx;
+        lr += a.mu[ci * row + j];
+        if constexpr (NC == 2) li += a.mu[ci * row + N + j];
     }
     float h0r = 0.f, h0i = 0.f;
     if (a.h0) {
@@ -635,9 +694,15 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq(SeqArgs a) {
             hr = ldact_s(hp + j);
             hi = NC == 2 ? ldact_s(hp + N + j) : 0.f;
         } else {
-            er = ei = 0.f;
-            hr = h0r;
-            hi = h0i;
+            er = ei = 0.f;   // (a chunk's first step: its lambda_{-1} term belongs to the chunk before)
+            if (EMIT && tb > 0) {
+                const T* hp = reinterpret_cast<const T*>(sb_ + OFF_H + SUB_D + ro * ROWB);
+                hr = ldact_s(hp + j);
+                hi = NC == 2 ? ldact_s(hp + N + j) : 0.f;
+            } else {
+                hr = h0r;
+                hi = h0i;
+            }
         }
     };
     {
@@ -648,9 +713,11 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq(SeqArgs a) {
     auto step = [&](const int rr, const int g, const int t, const int t_lo, const bool inner) {
         // inner: full group with t_lo > 0 -> rows of step t-1 are compile-time, t-1 > 0
         const int v = L - 1 - t;
-        st_stream<T>(dbp, lr, pol);                       // db_t = lambda_t
-        if constexpr (NC == 2) st_stream<T>(dbp + N, li, pol);
-        dbp -= row;
+        if constexpr (EMIT) {
+            st_stream<T>(dbp, lr, pol);                       // db_t = lambda_t
+            if constexpr (NC == 2) st_stream<T>(dbp + N, li, pol);
+            dbp -= row;
+        }
         char* lbc = xbc + (t & 1) * (N * SVB);
         *reinterpret_cast<SV*>(lbc + j * SVB) = fused::mk<NC>(lr, li);
         const float Dcr = Dr, Dci = Di, ecr = er, eci = ei, hcr = hr, hci = hi;
@@ -667,7 +734,7 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq(SeqArgs a) {
             mbar_arrive(bars + R + (slot == 0 ? R - 1 : slot - 1));
         }
         // g_t of the previous 32 steps (v = 8 g + rr, so only the first step of every 4th group)
-        if (rr == 0 && (g % (32 / G)) == 0 && g > 0 && a.gsel) {
+        if (EMIT && rr == 0 && (g % (32 / G)) == 0 && g > 0 && a.gsel) {
             const int q = j & 31, part = j >> 5, NP = N >> 5;
             const float* gr = gs + (size_t)q * (N + 1);
             float acc = 0.f;
@@ -713,18 +780,20 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq(SeqArgs a) {
         const float pr = fused::re_of<NC>(lpv), pm = fused::im_of<NC>(lpv);
         lr = ecr + Dcr * pr + Dci * pm;                   // lambda_{t-1} = e_{t-1} + conj(D_t) lp
         li = NC == 2 ? eci + Dcr * pm - Dci * pr : 0.f;
-        const float ddr = hcr * pr + hci * pm, ddi = hcr * pm - hci * pr;   // dD_t = conj(h_{t-1}) lp
-        if constexpr (PD) {
-            ddf[0] = ddr;
-            if constexpr (NC == 2) ddf[N] = ddi;
-            ddf -= row;
-        } else {
-            st_stream<T>(ddp, ddr, pol);
-            if constexpr (NC == 2) st_stream<T>(ddp + N, ddi, pol);
-            ddp -= row;
+        if constexpr (EMIT) {
+            const float ddr = hcr * pr + hci * pm, ddi = hcr * pm - hci * pr;   // dD_t = conj(h_{t-1}) lp
+            if constexpr (PD) {
+                ddf[0] = ddr;
+                if constexpr (NC == 2) ddf[N] = ddi;
+                ddf -= row;
+            } else {
+                st_stream<T>(ddp, ddr, pol);
+                if constexpr (NC == 2) st_stream<T>(ddp + N, ddi, pol);
+                ddp -= row;
+            }
+            const float qr = Dcr * hcr - Dci * hci, qi = Dcr * hci + Dci * hcr;
+            gs[(size_t)(v & 31) * (N + 1) + j] = pr * qr + pm * qi;   // this thread's term of g_t
         }
-        const float qr = Dcr * hcr - Dci * hci, qi = Dcr * hci + Dci * hcr;
-        gs[(size_t)(v & 31) * (N + 1) + j] = pr * qr + pm * qi;   // this thread's term of g_t
     };
     for (int g = 0; g < ngroups; ++g) {
         const int t_hi = L - 1 - g * G, t_lo = max(t_hi - G + 1, 0);
@@ -736,7 +805,7 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq(SeqArgs a) {
         }
     }
     compute_sync(SPC * N);
-    if (a.gsel) {   // the last (L % 32 or 32) steps
+    if (EMIT && a.gsel) {   // the last (L % 32 or 32) steps
         const int v0 = ((L - 1) / 32) * 32;
         for (int x = j; x < 32 && v0 + x < L; x += N) {
             const float* gr = gs + (size_t)x * (N + 1);
@@ -745,7 +814,12 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq(SeqArgs a) {
             a.gsel[seq0 + (L - 1 - (v0 + x))] = acc;
         }
     }
-    if (a.dh0) {   // after t = 0: lambda = A_0^T lambda_0 (no e_{-1} term)
+    // after the chunk's first step (no e term): lambda = A_{s_c}^T lambda_{s_c}
+    if constexpr (MODE == 1) {   // beta'_c
+        const size_t ci = (size_t)s * C + cidx;
+        a.betap[ci * row + j] = lr;
+        if constexpr (NC == 2) a.betap[ci * row + N + j] = li;
+    } else if (a.dh0 && cidx == 0) {   // the sequence's first step: dh0 = A_0^T lambda_0
         a.dh0[(size_t)s * row + j] = lr;
         if constexpr (NC == 2) a.dh0[(size_t)s * row + N + j] = li;
     }

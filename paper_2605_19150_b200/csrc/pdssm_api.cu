@@ -225,13 +225,24 @@ pdssm_status pdssm_scan_fwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
     ChunkStateView cs = cs_view(g, chunk_state);
     uint16_t* maps = (g.flags & PDSSM_EXPORT_MAPS) ? maps_opt : nullptr;
     const bool use_seq = seq_applicable(g, {g.diag_mode == PDSSM_DIAG_PER_STEP ? diag : nullptr, bias, hout});
-    // the single-chunk path builds its records and the CSR plan in one launch (fwd_seq)
-    if (!use_seq && (r = launch_plan(g, dict_idx, pstart, psrc, st))) return r;
+    // the single-CTA paths build their records and the CSR plan in one launch (fwd_seq / fwd_seqc)
+    const bool seqc_fwd = !use_seq && seqc_applicable(g, {g.diag_mode == PDSSM_DIAG_PER_STEP ? diag : nullptr, bias, hout});
+    if (!use_seq && !seqc_fwd && (r = launch_plan(g, dict_idx, pstart, psrc, st))) return r;
     if (env_path_is("seq") && !use_seq)
         return fail(PDSSM_ERR_UNSUPPORTED, "scan_fwd: PDSSM_PATH=seq but the single-chunk path does not apply");
-    const bool use_fused = !use_seq && fused_applicable(
+    const bool use_seqc = !use_seq && seqc_applicable(g, {g.diag_mode == PDSSM_DIAG_PER_STEP ? diag : nullptr, bias, hout});
+    const bool use_fused = !use_seq && !use_seqc && fused_applicable(
         g, {g.diag_mode == PDSSM_DIAG_PER_STEP ? diag : nullptr, bias, hout, h0_opt, chunk_state, maps});
-    if (use_seq) {
+    if (use_seqc) {
+        seq::SeqArgs sa{};
+        sa.kstar = kstar; sa.dict_idx = dict_idx; sa.rec = srec; sa.wm = swm; sa.ovf = sovf; sa.pstart = pstart;
+        sa.psrc = psrc;
+        sa.diag = g.diag_mode == PDSSM_DIAG_PER_STEP ? diag : nullptr;
+        sa.diag_dict = g.diag_mode == PDSSM_DIAG_PER_DICT ? static_cast<const float*>(diag) : nullptr;
+        sa.bias = bias; sa.h0 = h0_opt; sa.cs = cs; sa.maps = maps; sa.out0 = hout;
+        sa.H = (int)g.H; sa.L = (int)g.L; sa.N = (int)g.N; sa.K = (int)g.K; sa.flags = g.flags;
+        if ((r = fwd_seqc(g, sa, srec, swm, sovf, st))) return r;
+    } else if (use_seq) {
         seq::SeqArgs sa{};
         sa.kstar = kstar; sa.dict_idx = dict_idx; sa.rec = srec; sa.wm = swm; sa.ovf = sovf; sa.pstart = pstart;
         sa.psrc = psrc;
@@ -322,6 +333,25 @@ pdssm_status pdssm_scan_bwd(const uint8_t* kstar, const uint16_t* dict_idx, cons
         return PDSSM_OK;
     }
     const bool use_seq = !recompute && seq_applicable(g, {g.diag_mode == PDSSM_DIAG_PER_STEP ? diag : nullptr, h_saved, dh_opt, ebuf});
+    const bool use_seqc = !recompute && !use_seq &&
+        seqc_applicable(g, {g.diag_mode == PDSSM_DIAG_PER_STEP ? diag : nullptr, h_saved, dh_opt, ebuf, dbias,
+                            g.diag_mode == PDSSM_DIAG_PER_STEP ? ddiag : nullptr});
+    if (use_seqc) {
+        if (dy_opt && (r = prepare_e_run(g, dh_opt, dy_opt, C_opt, ebuf, wbuf, st))) return r;
+        seq::SeqArgs sa{};
+        sa.kstar = kstar; sa.dict_idx = dict_idx;
+        sa.diag = g.diag_mode == PDSSM_DIAG_PER_STEP ? diag : nullptr;
+        sa.diag_dict = g.diag_mode == PDSSM_DIAG_PER_DICT ? static_cast<const float*>(diag) : nullptr;
+        sa.bias = dy_opt ? static_cast<const void*>(ebuf) : dh_opt;
+        sa.hsaved = h_saved; sa.h0 = h0_opt; sa.lam_in = lam_in_opt; sa.cs = cs;
+        sa.out0 = dbias; sa.out1 = g.diag_mode == PDSSM_DIAG_PER_DICT ? static_cast<void*>(dDbuf) : ddiag;
+        sa.gsel = gsel; sa.dh0 = dh0_opt; sa.mu = mu; sa.betap = betap;
+        sa.H = (int)g.H; sa.L = (int)g.L; sa.N = (int)g.N; sa.K = (int)g.K; sa.flags = g.flags;
+        if ((r = bwd_seqc_run(g, sa, dy_opt != nullptr, st))) return r;
+        if (g.diag_mode == PDSSM_DIAG_PER_DICT)
+            return reduce_dict(g, kstar, dDbuf, static_cast<float*>(ddiag), rdpart, st);
+        return PDSSM_OK;
+    }
     if (env_path_is("seq") && !use_seq)
         return fail(PDSSM_ERR_UNSUPPORTED, "scan_bwd: PDSSM_PATH=seq but the single-chunk path does not apply");
     const bool use_fused = !use_seq && !recompute &&

@@ -454,3 +454,61 @@ def test_seq_paired_sequences_per_cta(P, case, pair_bwd, monkeypatch):
     f2 = P.scan_fwd(d["kstar"], d["dict_idx"], d["diag"], d["bias"])
     torch.cuda.synchronize()
     assert torch.equal(f["h"], f2["h"])
+
+
+SEQC_CASES = [
+    # B, H, L, N, K, c, tau, bf16, per_dict: chunked single-CTA path (k_fwd_seq / k_bwd_seq MODE 1 / 2)
+    (1, 2, 1000, 128, 32, 2, 300, False, False),    # tau > the warp-per-chunk cap: the library's choice
+    (1, 2, 1000, 128, 32, 2, 300, True, False),
+    (2, 2, 777, 64, 16, 1, 96, False, False),       # forced (PDSSM_PATH=seqc), ragged last chunk
+    (2, 1, 500, 32, 5, 2, 128, False, True),        # PER_DICT
+    (1, 3, 333, 96, 8, 2, 100, False, False),       # N = 96 (runtime N)
+]
+
+
+@pytest.mark.parametrize("case", SEQC_CASES, ids=[str(c) for c in SEQC_CASES])
+def test_seqc_chunked_single_cta_path(P, case, monkeypatch):
+    """One CTA per (sequence, chunk): Phase A (chunk aggregates from a zero state) -> Phase B (carries,
+    maps) -> Phase C (replay), and the mirrored backward; every output against the oracle, chunk-level
+    intermediates against the float64 chunked oracle at the same tau, maps bit-exact."""
+    B, H, L, N, K, c, tau, bf16, pd = case
+    monkeypatch.setenv("PDSSM_PATH", "seqc")
+    inp, f, got, ch, ref, Pm, Dz = run_case(P, B, H, L, N, K, c, tau, bf16=bf16, per_dict=pd, seed=L + tau)
+    assert f["tau"] == tau
+    tol = TOL["bf16" if bf16 else "f32"]
+    check("seqc_h", cpx(f["h"]), ch["h"], tol)
+    assert np.array_equal(f["maps"].cpu().numpy().astype(np.int64), ch["maps"])
+    pi, d_bar, beta_bar, carry = P.chunk_state_views(f["chunk_state"], f["dims"])
+    assert np.array_equal(pi.cpu().numpy().astype(np.int64), ch["pi_bar"])
+    check("seqc_d_bar", O.planes_to_complex(d_bar.cpu().numpy()), ch["d_bar"], 1e-4)
+    check("seqc_beta_bar", O.planes_to_complex(beta_bar.cpu().numpy()), ch["beta_bar"], 1e-4)
+    check("seqc_carry", O.planes_to_complex(carry.cpu().numpy()), ch["carries"], 1e-4)
+    db, dD, g, dh0 = got
+    db_r, dD_r, g_r, dh0_r = ref
+    check("seqc_db", cpx(db), db_r, tol)
+    check("seqc_g", g.cpu().numpy(), g_r, tol)
+    check("seqc_dh0", O.planes_to_complex(dh0.cpu().numpy()), dh0_r, tol)
+    if pd:
+        dDk = np.zeros((H, K, N), np.complex128)
+        for b in range(B):
+            for hh in range(H):
+                np.add.at(dDk[hh], inp["kstar"][b, hh], dD_r[b, hh])
+        check("seqc_dD_k", O.planes_to_complex(dD.cpu().numpy()), dDk, tol)
+    else:
+        check("seqc_dD", cpx(dD), dD_r, tol)
+
+
+def test_default_chunk_policy(P, monkeypatch):
+    """Library default tau (R20): one CTA per sequence when the sequences fill the GPU and a step row
+    is large (config 2 fp32, config 4); the chunked single-CTA path with ~4 CTAs per SM otherwise
+    (config 2 bf16, configs 3 and 5); the warp-per-chunk path (tau 64) for short sequences."""
+    monkeypatch.delenv("PDSSM_PATH", raising=False)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    d = lambda B, H, L, N, K, c, dt: P.default_chunk(P.make_dims(B, H, L, N, K, c=c, dtype=dt))
+    assert d(16, 8, 2048, 128, 32, 2, P.F32) == 2048
+    assert d(32, 32, 4096, 64, 48, 1, P.BF16) == 4096
+    C2 = -(-4 * sms // 128)
+    assert d(16, 8, 2048, 128, 32, 2, P.BF16) == -(-2048 // C2)
+    C3 = -(-4 * sms // 32)
+    assert d(4, 8, 17984, 128, 32, 1, P.F32) == -(-17984 // C3)
+    assert d(1, 2, 300, 128, 32, 2, P.F32) == 64
