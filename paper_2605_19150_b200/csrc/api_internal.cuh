@@ -232,9 +232,9 @@ inline bool path_fused_forced() {
 // ---------------------------------------------------------------------------
 
 constexpr size_t kSeqSmemBudget = 200 * 1024;
-// CTAs of the single-chunk kernels per SM when sequences outnumber the SMs: enough for one wave
-// of config 4 (1024 sequences: 7 per SM for the backward, whose CTA needs ~31 KB at N = 64 bf16)
-constexpr int kSeqMaxPerSm = 8;
+// CTAs of the single-chunk kernels per SM when sequences outnumber the SMs (config 4's backward
+// measured 0.72 ms at 4 per SM in two waves against 0.78 ms at 7 per SM in one: issue-bound)
+constexpr int kSeqMaxPerSm = 4;
 constexpr int kSeqG = seq::SEQ_G;     // backward group
 constexpr int kSeqGF = seq::SEQ_GF;   // forward group
 
