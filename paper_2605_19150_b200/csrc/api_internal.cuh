@@ -54,16 +54,18 @@ inline int default_tau(const pdssm_dims* d) {
     const int64_t sms = num_sms_dev();
     const bool forced_chunked = env_path_is("fused") || env_path_is("generic");
     const size_t act = d->dtype == PDSSM_BF16 ? 2 : 4;
-    if (!forced_chunked && seq_shape_ok(d->state, d->dict, d->len, d->is_complex, act) && d->len <= (int64_t)1 << 30) {
-        const int64_t rowb = (int64_t)d->is_complex * d->state * (int64_t)act;   // bytes of one D / b / h row
-        // one CTA per sequence when the sequences fill the GPU and a step moves enough bytes
-        if (env_path_is("seq") || (S * 10 >= sms * 6 && (rowb > 512 || S >= 2 * sms))) return (int)d->len;
-        // otherwise the chunked single-CTA path ("seqc"): ~4 CTAs per SM, two passes per chunk but
-        // the per-step chain of a chunk is tau steps long instead of L
-        const int64_t C = ceil_div(4 * sms, S);
-        const int64_t tau = ceil_div(d->len, C);
-        if (env_path_is("seqc") || (tau >= 256 && tau <= seq::LMAX)) return (int)std::max<int64_t>(tau, 1);
-    }
+    if (forced_chunked || d->len > (int64_t)1 << 30) return 64;
+    // one CTA per sequence when the sequences fill most SMs
+    if (seq_shape_ok(d->state, d->dict, d->len, d->is_complex, act) && (env_path_is("seq") || S * 10 >= sms * 6))
+        return (int)d->len;
+    // otherwise the chunked single-CTA path ("seqc") with ~2 CTAs per SM: two passes per chunk, but
+    // the per-step chain of a chunk is tau steps long instead of L (more CTAs per SM only queue on
+    // the shared-memory pipe: ~100 wavefronts per step at N = 128 complex)
+    const int64_t C = ceil_div(2 * sms, S);
+    const int64_t tau = std::max<int64_t>(ceil_div(d->len, C), 1);
+    if (seq_shape_ok(d->state, d->dict, std::min<int64_t>(tau, d->len), d->is_complex, act) &&
+        (env_path_is("seqc") || tau >= 256))
+        return (int)tau;
     return 64;
 }
 
