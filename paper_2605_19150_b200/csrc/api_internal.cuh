@@ -58,13 +58,15 @@ inline int default_tau(const pdssm_dims* d) {
     // one CTA per sequence when the sequences fill most SMs
     if (seq_shape_ok(d->state, d->dict, d->len, d->is_complex, act) && (env_path_is("seq") || S * 10 >= sms * 6))
         return (int)d->len;
-    // otherwise the chunked single-CTA path ("seqc") with ~2 CTAs per SM: two passes per chunk, but
-    // the per-step chain of a chunk is tau steps long instead of L (more CTAs per SM only queue on
-    // the shared-memory pipe: ~100 wavefronts per step at N = 128 complex)
+    // otherwise, for N <= 64, the chunked single-CTA path ("seqc") with ~2 CTAs per SM: two passes
+    // per chunk, but the per-step chain of a chunk is tau steps long instead of L (config 5: 163 ->
+    // 197 M tok/s).  At N = 128 the SM's shared-memory pipe (~100 wavefronts per step) is already
+    // the bound at one CTA per SM, so the second pass does not pay (config 3: 56 vs 62 M tok/s for
+    // the warp-per-chunk path) -- tau = 64 there.
     const int64_t C = ceil_div(2 * sms, S);
     const int64_t tau = std::max<int64_t>(ceil_div(d->len, C), 1);
     if (seq_shape_ok(d->state, d->dict, std::min<int64_t>(tau, d->len), d->is_complex, act) &&
-        (env_path_is("seqc") || tau >= 256))
+        (env_path_is("seqc") || (tau >= 256 && d->state <= 64)))
         return (int)tau;
     return 64;
 }
