@@ -184,3 +184,23 @@ def test_autograd_with_permuted_inputs(P):
     check("autograd_dD", gD, dD_r, 1e-4)
     check("autograd_db", gb, db_r, 1e-4)
     check("autograd_dh0", O.planes_to_complex(h0.grad.cpu().numpy()), dh0_r, 1e-4)
+
+
+def test_hypothesis_chunked_single_cta(P, monkeypatch):
+    """Randomised shapes forced onto the chunked single-CTA path (PDSSM_PATH=seqc): ragged chunks,
+    L = 1, one chunk, PER_STEP complex / real, fp32 / bf16, with and without h0."""
+    pytest.importorskip("hypothesis")
+    from hypothesis import given, settings, HealthCheck
+    from hypothesis import strategies as st
+
+    monkeypatch.setenv("PDSSM_PATH", "seqc")
+
+    @settings(max_examples=20, deadline=None, derandomize=True,
+              suppress_health_check=[HealthCheck.function_scoped_fixture, HealthCheck.too_slow])
+    @given(B=st.integers(1, 3), H=st.integers(1, 2), L=st.integers(1, 400), N=st.sampled_from([32, 64, 96, 128]),
+           K=st.integers(1, 33), c=st.sampled_from([1, 2]), tau=st.integers(1, 200), bf16=st.booleans(),
+           h0=st.booleans(), seed=st.integers(0, 10 ** 6))
+    def run(B, H, L, N, K, c, tau, bf16, h0, seed):
+        fwd_bwd_check(P, B, H, L, N, K, c, tau, bf16=bf16, seed=seed, h0=h0)
+
+    run()
