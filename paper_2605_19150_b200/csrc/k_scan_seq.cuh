@@ -28,7 +28,12 @@
 namespace pdssm {
 namespace seq {
 
-constexpr int CAP = 8;       // inline preimage capacity per (entry, target)
+constexpr int CAP = 8;       // record slots per (entry, target) (u8 sources, padded with the zero slot N)
+#ifndef PDSSM_SEQ_GCAP
+#define PDSSM_SEQ_GCAP 8
+#endif
+constexpr int GCAP = PDSSM_SEQ_GCAP;   // sources gathered inline (<= CAP); longer preimages take the CSR plan
+static_assert(GCAP == 6 || GCAP == 8, "gather capacity");
 constexpr int LMAX = 16384;  // k* of the whole sequence is staged in shared memory
 constexpr int MAXN = 128;    // states per CTA (one thread each)
 constexpr int WM_OVF = 15;   // trip-count code of an overflowing entry
@@ -126,7 +131,7 @@ static __global__ void k_build_seq_plan(const uint16_t* __restrict__ dict_idx, u
     for (int j = 0; j < N; ++j) {
         const int pj = sP[j];
         if (pj == i) {
-            if (d < CAP) r[d] = (uint8_t)j;
+            if (d < GCAP) r[d] = (uint8_t)j;
             ++d;
         }
         below += pj < i;                              // pstart[i] = #{j : P[j] < i}
@@ -138,10 +143,10 @@ static __global__ void k_build_seq_plan(const uint16_t* __restrict__ dict_idx, u
     uint8_t* dst = rec + ((size_t)e * N + i) * CAP;
 #pragma unroll
     for (int q = 0; q < CAP; ++q) dst[q] = r[q];
-    int m = d < CAP ? d : CAP;
+    int m = d < GCAP ? d : GCAP;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (d > CAP) sovf = 1;
+    if (d > GCAP) sovf = 1;
     __syncthreads();
     // warp trip count; WM_OVF marks an entry with a preimage longer than CAP (CSR fallback)
     if ((i & 31) == 0) wm[(size_t)e * (N / 32) + (i >> 5)] = (uint8_t)(sovf ? WM_OVF : m);
@@ -413,8 +418,8 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
         } else {
 #pragma unroll
             for (int q = 0; q < CAP; ++q) {
-                float re, im;
-                lds_sv<NC>(ga[q], re, im);
+                float re = 0.f, im = 0.f;
+                if (q < GCAP) lds_sv<NC>(ga[q], re, im);   // (compile-time: slots past GCAP hold the zero slot)
                 v[q] = fused::mk<NC>(re, im);
             }
         }
@@ -443,10 +448,17 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
         k1 = kb[t + 2];
         // pairwise sum of the 8 slots (sources past the in-degree read the zero slot)
         auto sum8 = [&](const SV (&x)[CAP], float& sr, float& si) {
-            sr = ((fused::re_of<NC>(x[0]) + fused::re_of<NC>(x[1])) + (fused::re_of<NC>(x[2]) + fused::re_of<NC>(x[3]))) +
-                 ((fused::re_of<NC>(x[4]) + fused::re_of<NC>(x[5])) + (fused::re_of<NC>(x[6]) + fused::re_of<NC>(x[7])));
-            si = ((fused::im_of<NC>(x[0]) + fused::im_of<NC>(x[1])) + (fused::im_of<NC>(x[2]) + fused::im_of<NC>(x[3]))) +
-                 ((fused::im_of<NC>(x[4]) + fused::im_of<NC>(x[5])) + (fused::im_of<NC>(x[6]) + fused::im_of<NC>(x[7])));
+            if constexpr (GCAP == 6) {
+                sr = ((fused::re_of<NC>(x[0]) + fused::re_of<NC>(x[1])) + (fused::re_of<NC>(x[2]) + fused::re_of<NC>(x[3]))) +
+                     (fused::re_of<NC>(x[4]) + fused::re_of<NC>(x[5]));
+                si = ((fused::im_of<NC>(x[0]) + fused::im_of<NC>(x[1])) + (fused::im_of<NC>(x[2]) + fused::im_of<NC>(x[3]))) +
+                     (fused::im_of<NC>(x[4]) + fused::im_of<NC>(x[5]));
+            } else {
+                sr = ((fused::re_of<NC>(x[0]) + fused::re_of<NC>(x[1])) + (fused::re_of<NC>(x[2]) + fused::re_of<NC>(x[3]))) +
+                     ((fused::re_of<NC>(x[4]) + fused::re_of<NC>(x[5])) + (fused::re_of<NC>(x[6]) + fused::re_of<NC>(x[7])));
+                si = ((fused::im_of<NC>(x[0]) + fused::im_of<NC>(x[1])) + (fused::im_of<NC>(x[2]) + fused::im_of<NC>(x[3]))) +
+                     ((fused::im_of<NC>(x[4]) + fused::im_of<NC>(x[5])) + (fused::im_of<NC>(x[6]) + fused::im_of<NC>(x[7])));
+            }
         };
         float ar, ai, cr = 0.f, ci = 0.f;
 #if !defined(FWD_EXP_SLOTS)
