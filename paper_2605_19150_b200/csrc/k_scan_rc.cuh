@@ -37,7 +37,7 @@ struct RcLayout {
         prow = o; o = a16(o + (size_t)K * N * 2);
         dk = o; o = a16(o + (PD ? (size_t)K * NC * N * 4 : 0));
         hbuf = o; o = a16(o + (size_t)tau * NC * N * 4);     // the chunk's recomputed states (f32)
-        gp = o; o = a16(o + (size_t)tau * NW * 4);           // per-warp g_t partials of the chunk
+        gp = o; o = a16(o + (size_t)tau * N * 4);            // the chunk's g_t terms [tau][N] (summed after it)
         bytes = o;
     }
 };
@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq_rc(RcArgs a) {
     uint16_t* prow = reinterpret_cast<uint16_t*>(smem + Ly.prow);
     float* dk = reinterpret_cast<float*>(smem + Ly.dk);
     float* hbuf = reinterpret_cast<float*>(smem + Ly.hbuf);
-    float* gp = reinterpret_cast<float*>(smem + Ly.gp);
+    float* gp = reinterpret_cast<float*>(smem + Ly.gp);   // [tau][N]
     const size_t row = (size_t)NC * N;
     const size_t seq0 = (size_t)s * L;
     const uint64_t pol = fused::policy_evict_first();
@@ -176,19 +176,22 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq_rc(RcArgs a) {
         const size_t ci = (size_t)s * C + c;
         const float c_r = a.cs.carry[ci * row + i];
         const float c_i = NC == 2 ? a.cs.carry[ci * row + N + i] : 0.f;
-        // ---------------- F: forward replay of the chunk into hbuf
+        // ---------------- F: forward replay of the chunk into hbuf (the next step's operands are
+        // loaded while this step's gather is in flight, within a group)
         float hr = c_r, hi_ = c_i;
         for (int q = 0; q < ng; ++q, ++gi) {
             const int slot = gi % R;
             fused::mbar_wait(bars + slot, (uint32_t)(gi / R) & 1u);
             const uint8_t* sb = ring + (size_t)slot * Ly.slot;
             const int t0 = lo + q * G, len = min(G, hi - t0 + 1);
-            for (int r = 0; r < len; ++r) {
-                const int t = t0 + r;
-                const int k = kb[t];
-                const uint2 rc = rec[(size_t)k * N + i];   // this step's preimage record and trip code
-                const int m = wm[k * NW + w];
-                float Dr, Di = 0.f;
+            int k, m;
+            uint2 rc;
+            float Dr, Di, Br, Bi;
+            auto load_f = [&](int r) {
+                k = kb[t0 + r];
+                rc = rec[(size_t)k * N + i];
+                m = wm[k * NW + w];
+                Di = 0.f;
                 if constexpr (PD) {
                     Dr = dk[(size_t)k * row + i];
                     if constexpr (NC == 2) Di = dk[(size_t)k * row + N + i];
@@ -198,7 +201,12 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq_rc(RcArgs a) {
                     if constexpr (NC == 2) Di = ldact_s(Dp + N + i);
                 }
                 const T* Bp = reinterpret_cast<const T*>(sb + OFF2 + r * ROWB);
-                const float Br = ldact_s(Bp + i), Bi = NC == 2 ? ldact_s(Bp + N + i) : 0.f;
+                Br = ldact_s(Bp + i);
+                Bi = NC == 2 ? ldact_s(Bp + N + i) : 0.f;
+            };
+            load_f(0);
+            for (int r = 0; r < len; ++r) {
+                const int t = t0 + r;
                 SV* vb = xf + fx * (N + 1);
                 vb[i] = fused::mk<NC>(Dr * hr - Di * hi_, Dr * hi_ + Di * hr);
                 uint32_t ga[CAP];   // shared addresses of the gather, before the barrier
@@ -213,33 +221,38 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq_rc(RcArgs a) {
                         ga[4 + x] = hi4[x];
                     }
                 }
+                const int kc = k, mc = m;
+                const float bcr = Br, bci = Bi;
                 compute_sync(N);
                 if (r == 0 && i == 0 && gi >= 1) mbar_arrive(bars + R + ((gi - 1) % R));   // previous group consumed
                 float ar, ai;
-                if (m == WM_OVF) {   // preimage longer than the records: CSR plan (rare, warp-uniform)
+                if (mc == WM_OVF) {   // preimage longer than the records: CSR plan (rare, warp-uniform)
                     ar = ai = 0.f;
-                    const size_t e = (size_t)h * K + k;
+                    const size_t e = (size_t)h * K + kc;
                     const int st = __ldg(a.pstart + e * (N + 1) + i), en = __ldg(a.pstart + e * (N + 1) + i + 1);
                     for (int x = st; x < en; ++x) {
                         const SV v = vb[__ldg(a.psrc + e * N + x)];
                         ar += fused::re_of<NC>(v);
                         ai += fused::im_of<NC>(v);
                     }
-                } else if (m <= 4) {   // warp-uniform: the warp's in-degree fits 4 slots
+                    if (r + 1 < len) load_f(r + 1);
+                } else if (mc <= 4) {   // warp-uniform: the warp's in-degree fits 4 slots
                     float vr[4], vi[4];
 #pragma unroll
                     for (int x = 0; x < 4; ++x) lds_sv<NC>(ga[x], vr[x], vi[x]);
+                    if (r + 1 < len) load_f(r + 1);
                     ar = (vr[0] + vr[1]) + (vr[2] + vr[3]);
                     ai = (vi[0] + vi[1]) + (vi[2] + vi[3]);
                 } else {
                     float vr[CAP], vi[CAP];
 #pragma unroll
                     for (int x = 0; x < CAP; ++x) lds_sv<NC>(ga[x], vr[x], vi[x]);   // past the in-degree: zero slot
+                    if (r + 1 < len) load_f(r + 1);
                     ar = ((vr[0] + vr[1]) + (vr[2] + vr[3])) + ((vr[4] + vr[5]) + (vr[6] + vr[7]));
                     ai = ((vi[0] + vi[1]) + (vi[2] + vi[3])) + ((vi[4] + vi[5]) + (vi[6] + vi[7]));
                 }
-                hr = ar + Br;
-                hi_ = NC == 2 ? ai + Bi : 0.f;
+                hr = ar + bcr;
+                hi_ = NC == 2 ? ai + bci : 0.f;
                 float* hrow = hbuf + (size_t)(t - lo) * row;
                 hrow[i] = hr;
                 if constexpr (NC == 2) hrow[N + i] = hi_;
@@ -305,10 +318,7 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq_rc(RcArgs a) {
                     if constexpr (NC == 2) stact(static_cast<T*>(a.ddiag) + off + N, ddi);
                 }
                 const float qr = Dr * hr0 - Di * hi0, qi = Dr * hi0 + Di * hr0;
-                float gv = pr * qr + pm * qi;                                // this source's term of g_t
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) gv += __shfl_xor_sync(0xffffffffu, gv, o);
-                if ((i & 31) == 0) gp[(size_t)(t - lo) * NW + w] = gv;
+                gp[(size_t)(t - lo) * N + i] = pr * qr + pm * qi;            // this source's term of g_t (off the chain)
                 (void)lr_old;
                 (void)li_old;
                 if (t == 0 && a.dh0) {                                       // dh0 = A_0^T lambda_0
@@ -319,11 +329,17 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq_rc(RcArgs a) {
             }
         }
         compute_sync(N);   // the chunk's g partials are complete (and hbuf is free for the next chunk)
-        if (a.gsel) {
+        if (a.gsel) {   // g_t = sum over the N sources, in a fixed order (deterministic)
             for (int t = lo + i; t <= hi; t += N) {
-                float acc = 0.f;
-                for (int x = 0; x < NW; ++x) acc += gp[(size_t)(t - lo) * NW + x];
-                a.gsel[seq0 + t] = acc;
+                const float* gr = gp + (size_t)(t - lo) * N;
+                float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+                for (int x = 0; x < N; x += 4) {
+                    a0 += gr[x];
+                    a1 += gr[x + 1];
+                    a2 += gr[x + 2];
+                    a3 += gr[x + 3];
+                }
+                a.gsel[seq0 + t] = (a0 + a1) + (a2 + a3);
             }
         }
         compute_sync(N);   // partials read before the next chunk overwrites them
