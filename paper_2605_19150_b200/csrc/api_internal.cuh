@@ -58,15 +58,15 @@ inline int default_tau(const pdssm_dims* d) {
     // one CTA per sequence when the sequences fill most SMs
     if (seq_shape_ok(d->state, d->dict, d->len, d->is_complex, act) && (env_path_is("seq") || S * 10 >= sms * 6))
         return (int)d->len;
-    // otherwise, for N <= 64, the chunked single-CTA path ("seqc") with ~2 CTAs per SM: two passes
-    // per chunk, but the per-step chain of a chunk is tau steps long instead of L (config 5: 163 ->
-    // 197 M tok/s).  At N = 128 the SM's shared-memory pipe (~100 wavefronts per step) is already
-    // the bound at one CTA per SM, so the second pass does not pay (config 3: 56 vs 62 M tok/s for
-    // the warp-per-chunk path) -- tau = 64 there.
-    const int64_t C = ceil_div(2 * sms, S);
+    // otherwise the chunked single-CTA path ("seqc"): two passes per chunk, but the per-step chain of
+    // a chunk is tau steps long instead of L, and with small TMA groups (seqc_group) two or three
+    // (sequence, chunk) CTAs share an SM and interleave their chains.  ~2.8 chunks per SM measured
+    // best (tau sweeps, profiles/r02s_*: config 3 tau 1384 -> 92 M tok/s vs 60 for the
+    // warp-per-chunk path; config 5 tau 2521 -> 247 vs 197 M tok/s at 2 chunks per SM).
+    const int64_t C = ceil_div(28 * sms, 10 * S);
     const int64_t tau = std::max<int64_t>(ceil_div(d->len, C), 1);
     if (seq_shape_ok(d->state, d->dict, std::min<int64_t>(tau, d->len), d->is_complex, act) &&
-        (env_path_is("seqc") || (tau >= 256 && d->state <= 64)))
+        (env_path_is("seqc") || tau >= 256))
         return (int)tau;
     return 64;
 }
@@ -241,6 +241,11 @@ constexpr size_t kSeqSmemBudget = 200 * 1024;
 constexpr int kSeqMaxPerSm = 4;
 constexpr int kSeqG = seq::SEQ_G;     // backward group
 constexpr int kSeqGF = seq::SEQ_GF;   // forward group
+// group of the chunked single-CTA kernels (fwd and bwd): small, so that the rings of two or more
+// (sequence, chunk) CTAs fit one SM and their step chains interleave (measured, config 3 / 5:
+// 8 steps at N = 128, 16 at N = 64; the single-chunk kernels' 32 / 16 allow one CTA per SM)
+constexpr int kSeqcG128 = 8, kSeqcG64 = 16;
+inline int seqc_group(int64_t N) { return N == 64 ? kSeqcG64 : kSeqcG128; }   // (as instantiated)
 
 // Sequences per CTA of the single-chunk kernels: with N <= 64 and more sequences than SMs, two
 // sequences (batch rows b, b + 1) of one head share a CTA, its per-head tables, producer warp and
@@ -255,8 +260,9 @@ inline int seq_group(bool bwd, int spc) { return bwd ? (spc > 1 ? 8 : kSeqG) : (
 // ring depth R for this shape (0: the layout does not fit).  When there are more CTAs than
 // SMs, the budget is split so that ceil(#CTAs / #SMs) CTAs (up to 4) fit per SM.
 // Lk: the steps one CTA covers (g.L, or tau for the chunked single-CTA path); ctas: CTAs launched
-inline int seq_ring(const Geo& g, bool bwd, bool agg, size_t esz_e, int spc = 1, int64_t Lk = 0, int64_t ctas_in = 0) {
-    const int G = seq_group(bwd, spc);
+inline int seq_ring(const Geo& g, bool bwd, bool agg, size_t esz_e, int spc = 1, int64_t Lk = 0, int64_t ctas_in = 0,
+                    int G_in = 0) {
+    const int G = G_in > 0 ? G_in : seq_group(bwd, spc);
     if (Lk <= 0) Lk = g.L;
     const int ngroups = (int)ceil_div(Lk, G);
     const int64_t ctas = ctas_in > 0 ? ctas_in : g.S / spc;
@@ -290,8 +296,9 @@ inline bool seqc_applicable(const Geo& g, std::initializer_list<const void*> ptr
     for (const void* p : ptrs)
         if (misaligned(p, 16)) return false;
     const int64_t ctas = g.S * g.C;
-    return seq_ring(g, false, true, g.act, 1, g.tau, ctas) >= 2 && seq_ring(g, true, false, 4, 1, g.tau, ctas) >= 2 &&
-           seq_ring(g, true, false, g.act, 1, g.tau, ctas) >= 2;
+    const int G = seqc_group(g.N);
+    return seq_ring(g, false, true, g.act, 1, g.tau, ctas, G) >= 2 && seq_ring(g, true, false, 4, 1, g.tau, ctas, G) >= 2 &&
+           seq_ring(g, true, false, g.act, 1, g.tau, ctas, G) >= 2;
 }
 
 inline bool seq_applicable(const Geo& g, std::initializer_list<const void*> ptrs) {

@@ -104,7 +104,7 @@ pdssm_status bwd_seq_rc_run(const Geo& g, seq::RcArgs& ra, bool e_f32, uint8_t* 
 template <typename TE>
 pdssm_status bwd_seqc(const Geo& g, seq::SeqArgs& sa, cudaStream_t st) {
     const int64_t ctas = g.S * g.C;
-    sa.G = kSeqG;
+    sa.G = seqc_group(g.N);
     sa.spc = 1;
     sa.tau = g.tau;
     sa.C = g.C;
@@ -112,19 +112,19 @@ pdssm_status bwd_seqc(const Geo& g, seq::SeqArgs& sa, cudaStream_t st) {
     return with_act(g.dtype, [&](auto tv) {
         using T = decltype(tv);
         using TEE = typename std::conditional<std::is_same<TE, void>::value, T, TE>::type;
-        sa.R = seq_ring(g, true, false, sizeof(TEE), 1, g.tau, ctas);
+        sa.R = seq_ring(g, true, false, sizeof(TEE), 1, g.tau, ctas, sa.G);
         return with_nc(g.nc, [&](auto ncv) {
             constexpr int NC = decltype(ncv)::value;
             return with_pd(g.diag_mode, [&](auto pdv) {
                 constexpr bool PD = decltype(pdv)::value;
                 seq::Layout ly((int)g.N, (int)g.K, sa.R, sa.G, NC, (int)sizeof(T), (int)sizeof(TEE), PD, false, true, g.tau,
                                1);
-                auto kA = g.N == 128 ? seq::k_bwd_seq<T, TEE, NC, PD, 128, 1, SEQ_G_, 1>
-                          : g.N == 64 ? seq::k_bwd_seq<T, TEE, NC, PD, 64, 1, SEQ_G_, 1>
-                                      : seq::k_bwd_seq<T, TEE, NC, PD, 0, 1, SEQ_G_, 1>;
-                auto kC = g.N == 128 ? seq::k_bwd_seq<T, TEE, NC, PD, 128, 1, SEQ_G_, 2>
-                          : g.N == 64 ? seq::k_bwd_seq<T, TEE, NC, PD, 64, 1, SEQ_G_, 2>
-                                      : seq::k_bwd_seq<T, TEE, NC, PD, 0, 1, SEQ_G_, 2>;
+                auto kA = g.N == 128 ? seq::k_bwd_seq<T, TEE, NC, PD, 128, 1, kSeqcG128, 1>
+                          : g.N == 64 ? seq::k_bwd_seq<T, TEE, NC, PD, 64, 1, kSeqcG64, 1>
+                                      : seq::k_bwd_seq<T, TEE, NC, PD, 0, 1, kSeqcG128, 1>;
+                auto kC = g.N == 128 ? seq::k_bwd_seq<T, TEE, NC, PD, 128, 1, kSeqcG128, 2>
+                          : g.N == 64 ? seq::k_bwd_seq<T, TEE, NC, PD, 64, 1, kSeqcG64, 2>
+                                      : seq::k_bwd_seq<T, TEE, NC, PD, 0, 1, kSeqcG128, 2>;
                 pdssm_status rr = seq_set_smem((const void*)kA, ly.bytes);
                 if (rr) return rr;
                 kA<<<(unsigned)ctas, (unsigned)g.N + 32, ly.bytes, st>>>(sa);

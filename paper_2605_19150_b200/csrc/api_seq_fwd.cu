@@ -82,7 +82,7 @@ pdssm_status fwd_seqc(const Geo& g, seq::SeqArgs& sa, uint8_t* rec, uint8_t* wm,
     pdssm_status r = cuda_check("build_seq_plan");
     if (r) return r;
     const int64_t ctas = g.S * g.C;
-    sa.G = kSeqGF;
+    sa.G = seqc_group(g.N);
     sa.spc = 1;
     sa.tau = g.tau;
     sa.C = g.C;
@@ -94,7 +94,7 @@ pdssm_status fwd_seqc(const Geo& g, seq::SeqArgs& sa, uint8_t* rec, uint8_t* wm,
             return with_pd(g.diag_mode, [&](auto pdv) {
                 constexpr bool PD = decltype(pdv)::value;
                 auto launch = [&](auto kern, bool compose, const char* what) -> pdssm_status {
-                    sa.R = seq_ring(g, false, compose, g.act, 1, g.tau, ctas);
+                    sa.R = seq_ring(g, false, compose, g.act, 1, g.tau, ctas, sa.G);
                     seq::Layout ly((int)g.N, (int)g.K, sa.R, sa.G, NC, (int)sizeof(T), (int)sizeof(T), PD, compose, false,
                                    g.tau, 1);
                     pdssm_status rr = seq_set_smem((const void*)kern, ly.bytes);
@@ -102,12 +102,12 @@ pdssm_status fwd_seqc(const Geo& g, seq::SeqArgs& sa, uint8_t* rec, uint8_t* wm,
                     kern<<<(unsigned)ctas, (unsigned)g.N + 32, ly.bytes, st>>>(sa);
                     return cuda_check(what);
                 };
-                auto kA = g.N == 128 ? seq::k_fwd_seq<T, NC, PD, false, false, 128, 1, SEQ_GF_, false, 1>
-                          : g.N == 64 ? seq::k_fwd_seq<T, NC, PD, false, false, 64, 1, SEQ_GF_, false, 1>
-                                      : seq::k_fwd_seq<T, NC, PD, false, false, 0, 1, SEQ_GF_, false, 1>;
-                auto kC = g.N == 128 ? seq::k_fwd_seq<T, NC, PD, false, false, 128, 1, SEQ_GF_, false, 2>
-                          : g.N == 64 ? seq::k_fwd_seq<T, NC, PD, false, false, 64, 1, SEQ_GF_, false, 2>
-                                      : seq::k_fwd_seq<T, NC, PD, false, false, 0, 1, SEQ_GF_, false, 2>;
+                auto kA = g.N == 128 ? seq::k_fwd_seq<T, NC, PD, false, false, 128, 1, kSeqcG128, false, 1>
+                          : g.N == 64 ? seq::k_fwd_seq<T, NC, PD, false, false, 64, 1, kSeqcG64, false, 1>
+                                      : seq::k_fwd_seq<T, NC, PD, false, false, 0, 1, kSeqcG128, false, 1>;
+                auto kC = g.N == 128 ? seq::k_fwd_seq<T, NC, PD, false, false, 128, 1, kSeqcG128, false, 2>
+                          : g.N == 64 ? seq::k_fwd_seq<T, NC, PD, false, false, 64, 1, kSeqcG64, false, 2>
+                                      : seq::k_fwd_seq<T, NC, PD, false, false, 0, 1, kSeqcG128, false, 2>;
                 pdssm_status rr = launch(kA, true, "fwd_seqc_A");
                 if (rr) return rr;
                 k_fwd_phaseB<NC><<<(unsigned)g.S, thr, (size_t)NC * g.N * 4 + (size_t)g.N * 2 + 16, st>>>(

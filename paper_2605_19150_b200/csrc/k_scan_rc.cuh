@@ -8,8 +8,8 @@
 // so lambda flows across chunk boundaries in registers and no O(L N) state is read from HBM.
 // A producer warp streams, group by group, the rows each phase consumes through a TMA ring:
 // F groups [D_t | b_t], R groups [D_t | e_{t-1}] (D_t of a chunk is read twice; the second read of
-// the chunk's 2 x tau rows is normally served by L2).  g_t partials of the chunk are parked per
-// warp and summed in warp order after its R phase (deterministic).
+// the chunk's 2 x tau rows is normally served by L2).  The g_t terms of the chunk are parked per
+// source and summed in source order after its R phase (deterministic, off the lambda chain).
 #pragma once
 #include "k_scan_seq.cuh"
 
@@ -28,10 +28,10 @@ struct RcLayout {
         slot = (int)a16((size_t)(PD ? 0 : RC_G * row) + (size_t)RC_G * (row > erow ? row : erow));
         size_t o = 0;
         ring = o; o = a16(o + (size_t)R * slot);
-        bars = o; o = a16(o + (size_t)2 * R * 8);
+        bars = o; o = a16(o + (size_t)(2 * R + 1) * 8);      // full[R], empty[R], table barrier
         xf = o; o = a16(o + (size_t)2 * (N + 1) * sv);       // forward exchange rows (+ zero slot)
         xb = o; o = a16(o + (size_t)2 * N * sv);             // reverse exchange rows
-        kb = o; o = a16(o + (size_t)L + 2);
+        kb = o; o = a16(o + (size_t)L + 2 + 15);             // k* row at its address mod 16 (stage_k)
         rec = o; o = a16(o + (size_t)K * N * 8);
         wm = o; o = a16(o + (size_t)K * NW);
         prow = o; o = a16(o + (size_t)K * N * 2);
@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq_rc(RcArgs a) {
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Ly.bars);
     SV* xf = reinterpret_cast<SV*>(smem + Ly.xf);
     SV* xb = reinterpret_cast<SV*>(smem + Ly.xb);
-    uint8_t* kb = smem + Ly.kb;
+    uint8_t* kb = smem + Ly.kb;   // (re-pointed by stage_k below)
     uint2* rec = reinterpret_cast<uint2*>(smem + Ly.rec);
     uint8_t* wm = smem + Ly.wm;
     uint16_t* prow = reinterpret_cast<uint16_t*>(smem + Ly.prow);
@@ -88,27 +88,20 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq_rc(RcArgs a) {
     const size_t seq0 = (size_t)s * L;
     const uint64_t pol = fused::policy_evict_first();
     const TE* ein = static_cast<const TE*>(a.e);
-    for (int x = i; x < L; x += blockDim.x) {   // the sequence's k* (clamped; reported under CHECK_FINITE)
-        int k = a.kstar[seq0 + x];
-        if (k >= K) {
-            if (a.flags & PDSSM_CHECK_FINITE) report(ERRBIT_RANGE);
-            k = K - 1;
-        }
-        kb[x] = (uint8_t)k;
+    kb = stage_k(a.kstar + seq0, K, a.flags, kb, L);   // the sequence's k* (clamped; reported under CHECK_FINITE)
+    if (i == 0) {
+        for (int q = 0; q < 2 * R + 1; ++q) fused::mbar_init(bars + q, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    stage_rec(a.rec + (size_t)h * K * N * CAP, rec, K * N, bars + 2 * R);
     {
-        const uint2* gr = reinterpret_cast<const uint2*>(a.rec) + (size_t)h * K * N;
-        for (int x = i; x < K * N; x += blockDim.x) rec[x] = __ldg(gr + x);
         for (int x = i; x < K * NW; x += blockDim.x) wm[x] = a.wm[(size_t)h * K * NW + x];
-        for (int x = i; x < K * N; x += blockDim.x) prow[x] = (uint16_t)min((int)__ldg(a.dict_idx + (size_t)h * K * N + x), N - 1);
-        if constexpr (PD)
-            for (int x = i; x < K * NC * N; x += blockDim.x) dk[x] = __ldg(a.diag_dict + (size_t)h * K * NC * N + x);
+        stage_prow(a.dict_idx + (size_t)h * K * N, prow, K * N, N);
+        if constexpr (PD) stage_f32(a.diag_dict + (size_t)h * K * NC * N, dk, K * NC * N);
     }
     if (i == 0) {
         xf[N] = fused::mk<NC>(0.f, 0.f);
         xf[(N + 1) + N] = fused::mk<NC>(0.f, 0.f);
-        for (int q = 0; q < 2 * R; ++q) fused::mbar_init(bars + q, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     const int ROWB = (int)(row * sizeof(T)), EROWB = (int)(row * sizeof(TE));
@@ -160,6 +153,7 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq_rc(RcArgs a) {
         return;
     }
     // ---- compute threads: thread i owns state i (forward) / source i (reverse)
+    fused::mbar_wait(bars + 2 * R, 0);   // the records (stage_rec)
     float lr = 0.f, li = 0.f;   // lambda_{L-1} = e_{L-1} + lam_in
     if (ein) {
         lr = ldact(ein + (seq0 + L - 1) * row + i);

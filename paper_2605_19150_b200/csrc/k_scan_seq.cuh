@@ -57,12 +57,12 @@ struct Layout {
                                            : (size_t)(PD ? 0 : G * row) + (size_t)G * row));
         size_t o = 0;
         ring = o; o = a16(o + (size_t)R * slot);
-        bars = o; o = a16(o + (size_t)2 * R * 8);   // full[R], then empty[R]
+        bars = o; o = a16(o + (size_t)(2 * R + 1) * 8);   // full[R], empty[R], then the table barrier
         const int sv = NC == 2 ? 8 : 4;
         xs = a16((size_t)2 * (N + 1) * sv);
         x = o; o = a16(o + (size_t)SPC * xs);
         x2 = o; o = a16(o + (AGG ? (size_t)SPC * xs : 0));
-        kbs = a16((size_t)L + 2);
+        kbs = a16((size_t)L + 2 + 15);   // + slack: the row starts at the k* address mod 16 (stage_k)
         kb = o; o = a16(o + (size_t)SPC * kbs);
         rec = o; o = a16(o + (BWD ? 0 : (size_t)K * N * 8));
         wm = o; o = a16(o + (BWD ? 0 : (size_t)K * NW));
@@ -123,15 +123,15 @@ static __global__ void k_build_seq_plan(const uint16_t* __restrict__ dict_idx, u
     }
     sP[i] = (uint16_t)p;
     __syncthreads();
-    uint8_t r[CAP];
-#pragma unroll
-    for (int q = 0; q < CAP; ++q) r[q] = (uint8_t)N;
+    // the record in a register (byte q = q-th source; a local array indexed by d would live
+    // in local memory)
+    unsigned long long r = 0x0101010101010101ull * (unsigned long long)(uint8_t)N;
     int d = 0, below = 0, rank = 0;
     const int pi = sP[i];
     for (int j = 0; j < N; ++j) {
         const int pj = sP[j];
         if (pj == i) {
-            if (d < GCAP) r[d] = (uint8_t)j;
+            if (d < GCAP) r = (r & ~(0xffull << (8 * d))) | ((unsigned long long)j << (8 * d));
             ++d;
         }
         below += pj < i;                              // pstart[i] = #{j : P[j] < i}
@@ -140,9 +140,7 @@ static __global__ void k_build_seq_plan(const uint16_t* __restrict__ dict_idx, u
     pstart[(size_t)e * (N + 1) + i] = (uint16_t)below;
     if (i == 0) pstart[(size_t)e * (N + 1) + N] = (uint16_t)N;
     psrc[(size_t)e * N + rank] = (uint16_t)i;
-    uint8_t* dst = rec + ((size_t)e * N + i) * CAP;
-#pragma unroll
-    for (int q = 0; q < CAP; ++q) dst[q] = r[q];
+    reinterpret_cast<unsigned long long*>(rec)[(size_t)e * N + i] = r;   // (CAP == 8 bytes, aligned)
     int m = d < GCAP ? d : GCAP;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -153,22 +151,113 @@ static __global__ void k_build_seq_plan(const uint16_t* __restrict__ dict_idx, u
     if (i == 0) ovf[e] = (uint8_t)sovf;
 }
 
-__device__ __forceinline__ void stage_k(const SeqArgs& a, uint8_t* kb, size_t base, int L) {
-    for (int x = threadIdx.x; x < L; x += blockDim.x) {
-        int k = a.kstar[base + x];
-        if (k >= a.K) {
-            if (a.flags & PDSSM_CHECK_FINITE) report(ERRBIT_RANGE);
-            k = a.K - 1;
-        }
-        kb[x] = (uint8_t)k;
-    }
-}
-
-// the N compute threads synchronise on named barrier 1 (the producer warp never joins)
-__device__ __forceinline__ void compute_sync(int n) { asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory"); }
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(fused::smem_u32(b)) : "memory");
 }
+
+// ---- prologue staging (global -> shared, every thread of the CTA).  The prologue is latency
+// bound: each thread issues all of its loads of a pass before its first store, so a table costs
+// one HBM round trip per pass instead of one per element (an element-wise loop cost ~15 us of the
+// ~190 us config-2 forward).  src and dst 16-byte aligned; f transforms each loaded word.  U is
+// small (the staging registers count against the kernel's peak); the largest table, the forward's
+// preimage records, goes by one bulk copy instead (stage_rec).
+template <int U = 4, typename F>
+__device__ __forceinline__ void stage16(const uint4* __restrict__ src, uint4* dst, int n4, F&& f) {
+    const int nt = blockDim.x;
+    for (int x0 = threadIdx.x; x0 < n4; x0 += U * nt) {
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (x0 + u * nt < n4) v[u] = __ldg(src + x0 + u * nt);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (x0 + u * nt < n4) dst[x0 + u * nt] = f(v[u]);
+    }
+}
+struct Ident {
+    __device__ uint4 operator()(uint4 v) const { return v; }
+};
+__device__ __forceinline__ bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+// the staged k* row of a sequence starts at (its global address mod 16) inside its buffer, so the
+// bulk of it moves as aligned 16-byte words (the buffers carry 16 bytes of slack)
+__device__ __forceinline__ int kshift(const uint8_t* g) { return (int)((uintptr_t)g & 15); }
+
+// k* of one sequence (L bytes at src) -> kbuf + kshift(src), clamped to K - 1 (reported under
+// CHECK_FINITE), zero-padded by two; returns the staged row
+__device__ __forceinline__ uint8_t* stage_k(const uint8_t* src, int K, uint32_t flags, uint8_t* kbuf, int L) {
+    uint8_t* kb = kbuf + kshift(src);
+    const int tid = threadIdx.x;
+    const int head = min(L, (16 - kshift(src)) & 15);
+    const int n4 = (L - head) >> 4, tail0 = head + n4 * 16;
+    bool bad = false;
+    auto fixb = [&](int k) {
+        if (k >= K) {
+            bad = true;
+            k = K - 1;
+        }
+        return (uint8_t)k;
+    };
+    if (tid < head) kb[tid] = fixb(src[tid]);
+    if (tid < L - tail0) kb[tail0 + tid] = fixb(src[tail0 + tid]);
+    if (tid < 2) kb[L + tid] = 0;
+    const uint32_t kx4 = (uint32_t)(K & 255) * 0x01010101u, km4 = (uint32_t)((K - 1) & 255) * 0x01010101u;
+    auto fixw = [&](uint32_t w) {
+        if (K < 256 && __vcmpgeu4(w, kx4)) {
+            bad = true;
+            w = __vminu4(w, km4);
+        }
+        return w;
+    };
+    stage16(reinterpret_cast<const uint4*>(src + head), reinterpret_cast<uint4*>(kb + head), n4, [&](uint4 v) {
+        return make_uint4(fixw(v.x), fixw(v.y), fixw(v.z), fixw(v.w));
+    });
+    if (bad && (flags & PDSSM_CHECK_FINITE)) report(ERRBIT_RANGE);
+    return kb;
+}
+__device__ __forceinline__ void stage_k(const SeqArgs& a, uint8_t* kbuf, size_t base, int L) {
+    stage_k(a.kstar + base, a.K, a.flags, kbuf, L);
+}
+// P_k rows of head h ([K][N] u16, clamped to N - 1) -> prow
+__device__ __forceinline__ void stage_prow(const uint16_t* src, uint16_t* prow, int KN, int N) {
+    if (aligned16(src) && (KN & 7) == 0) {
+        const uint32_t m2 = (uint32_t)(N - 1) * 0x10001u;
+        stage16(reinterpret_cast<const uint4*>(src), reinterpret_cast<uint4*>(prow), KN >> 3, [&](uint4 v) {
+            return make_uint4(__vminu2(v.x, m2), __vminu2(v.y, m2), __vminu2(v.z, m2), __vminu2(v.w, m2));
+        });
+    } else {
+        for (int x = threadIdx.x; x < KN; x += blockDim.x) prow[x] = (uint16_t)min((int)__ldg(src + x), N - 1);
+    }
+}
+// the forward's preimage records of head h (n = K * N records of CAP bytes): one bulk copy by
+// thread 0 completing on tbar (initialised, arrival count 1) when the source is 16-byte aligned,
+// else an element loop (visible after the caller's next __syncthreads); either way tbar's phase 0
+// completes, so the consumers wait on it unconditionally
+__device__ __forceinline__ void stage_rec(const uint8_t* src, uint2* rec, int n, uint64_t* tbar) {
+    const uint32_t bytes = (uint32_t)n * CAP;
+    if (aligned16(src)) {
+        if (threadIdx.x == 0) {
+            fused::mbar_expect_tx(tbar, bytes);
+            fused::tma_1d(rec, src, bytes, tbar);
+        }
+    } else {
+        for (int x = threadIdx.x; x < n; x += blockDim.x) rec[x] = __ldg(reinterpret_cast<const uint2*>(src) + x);
+        if (threadIdx.x == 0) mbar_arrive(tbar);
+    }
+}
+// f32 table (n floats) -> shared
+__device__ __forceinline__ void stage_f32(const float* src, float* dst, int n) {
+    if (aligned16(src) && (n & 3) == 0) {
+        stage16(reinterpret_cast<const uint4*>(src), reinterpret_cast<uint4*>(dst), n >> 2, Ident{});
+    } else {
+        for (int x = threadIdx.x; x < n; x += blockDim.x) dst[x] = __ldg(src + x);
+    }
+}
+
+// global row of local step 0 of batch row b, head h, chunk start tb
+__device__ __forceinline__ size_t seq0_of(const SeqArgs& a, int b, int h, int tb) { return (size_t)(b * a.H + h) * a.L + tb; }
+
+// the N compute threads synchronise on named barrier 1 (the producer warp never joins)
+__device__ __forceinline__ void compute_sync(int n) { asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory"); }
 // producer warp (one elected lane): keeps the ring R groups ahead; a slot is refilled
 // once the compute threads released it (empty barrier, one arrival per consumed group)
 template <typename F>
@@ -206,6 +295,25 @@ __device__ __forceinline__ void lds_sv(uint32_t addr, float& re, float& im) {
         im = 0.f;
     }
 }
+
+// slot q of the gather, issued only when q < m (m: the warp's maximum in-degree, warp-uniform):
+// a predicated load, no branch; re / im keep their zero otherwise.  Slots past m would all read
+// the zero slot -- one shared-memory wavefront per warp and slot for nothing.
+template <int NC>
+__device__ __forceinline__ void lds_sv_pred(uint32_t addr, int q, int m, float& re, float& im) {
+    if constexpr (NC == 2) {
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.lt.s32 p, %3, %4;\n\t@p ld.shared.v2.f32 {%0, %1}, [%2];\n\t}"
+                     : "+f"(re), "+f"(im)
+                     : "r"(addr), "r"(q), "r"(m));
+    } else {
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.lt.s32 p, %2, %3;\n\t@p ld.shared.f32 %0, [%1];\n\t}"
+                     : "+f"(re)
+                     : "r"(addr), "r"(q), "r"(m));
+    }
+}
+#ifndef PDSSM_SEQ_PRED
+#define PDSSM_SEQ_PRED 0   // measured slower (config 2 fwd 0.185 -> 0.27 ms): the zero-slot reads stay
+#endif
 
 template <typename T>
 __device__ __forceinline__ void st_stream(T* p, float v, uint64_t pol) {
@@ -267,7 +375,7 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Ly.bars);
     char* xbc = reinterpret_cast<char*>(smem + Ly.x + sub * Ly.xs);
     char* xbc2 = reinterpret_cast<char*>(smem + Ly.x2 + sub * Ly.xs);
-    uint8_t* kb = smem + Ly.kb + sub * Ly.kbs;
+    uint8_t* kb = smem + Ly.kb + sub * Ly.kbs + kshift(a.kstar + seq0_of(a, pidx * SPC + sub, h, tb));
     uint2* rec = reinterpret_cast<uint2*>(smem + Ly.rec);
     uint8_t* wm = smem + Ly.wm;
     uint16_t* prow = reinterpret_cast<uint16_t*>(smem + Ly.prow);
@@ -279,18 +387,22 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
     // The sequence's k* first: it does not depend on the plan launch that precedes this
     // kernel, which may still be running (programmatic dependent launch); wait for it only
     // before the tables it writes are read.
-    for (int j = 0; j < SPC; ++j) stage_k(a, smem + Ly.kb + j * Ly.kbs, (size_t)((pidx * SPC + j) * a.H + h) * a.L + tb, L);
+    for (int j = 0; j < SPC; ++j) stage_k(a, smem + Ly.kb + j * Ly.kbs, seq0_of(a, pidx * SPC + j, h, tb), L);
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    {   // one-time tables of head h (k* zero-padded by 2)
-        const int NT = blockDim.x;
-        const uint2* gr = reinterpret_cast<const uint2*>(a.rec) + (size_t)h * K * N;
-        for (int x = i; x < K * N; x += NT) rec[x] = __ldg(gr + x);
-        for (int x = i; x < K * NW; x += NT) wm[x] = a.wm[(size_t)h * K * NW + x];
-        if constexpr (COMPOSE)
-            for (int x = i; x < K * N; x += NT) prow[x] = (uint16_t)min((int)__ldg(a.dict_idx + (size_t)h * K * N + x), N - 1);
-        if constexpr (PD)
-            for (int x = i; x < K * NC * N; x += NT) dk[x] = __ldg(a.diag_dict + (size_t)h * K * NC * N + x);
-        if (i < 2 * SPC) (smem + Ly.kb + (i >> 1) * Ly.kbs)[L + (i & 1)] = 0;
+    int my_ovf = 0;
+    if (i == 0) {
+        for (int q = 0; q < 2 * R + 1; ++q) fused::mbar_init(bars + q, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    stage_rec(a.rec + (size_t)h * K * N * CAP, rec, K * N, bars + 2 * R);
+    {   // the other one-time tables of head h
+        for (int x = i; x < K * NW; x += blockDim.x) {
+            const uint8_t v = a.wm[(size_t)h * K * NW + x];
+            wm[x] = v;
+            my_ovf |= v == WM_OVF;   // does any entry of this head need the CSR plan?
+        }
+        if constexpr (COMPOSE) stage_prow(a.dict_idx + (size_t)h * K * N, prow, K * N, N);
+        if constexpr (PD) stage_f32(a.diag_dict + (size_t)h * K * NC * N, dk, K * NC * N);
     }
     const int XB = (N + 1) * SVB;   // bytes of one exchange row (N values + the zero slot)
     if (il == 0 && i < SPC * N) {   // the zero slots of this sequence's exchange rows
@@ -301,13 +413,6 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
             *reinterpret_cast<SV*>(xbc2 + XB + N * SVB) = fused::mk<NC>(0.f, 0.f);
         }
     }
-    if (i == 0) {
-        for (int q = 0; q < 2 * R; ++q) fused::mbar_init(bars + q, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    // does any entry of this head need the CSR plan?  (selects the loop variant once)
-    int my_ovf = 0;
-    for (int x = i; x < K * NW; x += blockDim.x) my_ovf |= a.wm[(size_t)h * K * NW + x] == WM_OVF;
     const bool any_ovf = __syncthreads_or(my_ovf) != 0;
     const int ROWB = (int)(row * sizeof(T));
     const int OFF_B = PD ? 0 : SPC * G * ROWB;   // slot: [D rows of seq 0..SPC-1][b rows of seq 0..SPC-1]
@@ -361,6 +466,7 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
     int slot = 0;
     uint32_t ph = 0;
     const uint8_t* sb = ring + SUBOFF;   // this sequence's rows in the current group's slot
+    fused::mbar_wait(bars + 2 * R, 0);   // the records (stage_rec)
     fused::mbar_wait(bars, 0);
     k = kb[0];
     k1 = kb[1];
@@ -419,7 +525,10 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
 #pragma unroll
             for (int q = 0; q < CAP; ++q) {
                 float re = 0.f, im = 0.f;
-                if (q < GCAP) lds_sv<NC>(ga[q], re, im);   // (compile-time: slots past GCAP hold the zero slot)
+                if (q < GCAP) {   // (compile-time: slots past GCAP hold the zero slot)
+                    if (PDSSM_SEQ_PRED && q > 0 && !AGG) lds_sv_pred<NC>(ga[q], q, mc, re, im);
+                    else lds_sv<NC>(ga[q], re, im);
+                }
                 v[q] = fused::mk<NC>(re, im);
             }
         }
@@ -602,7 +711,7 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq(SeqArgs a) {
     uint8_t* ring = smem + Ly.ring;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Ly.bars);
     char* xbc = reinterpret_cast<char*>(smem + Ly.x + sub * Ly.xs);
-    uint8_t* kb = smem + Ly.kb + sub * Ly.kbs;
+    uint8_t* kb = smem + Ly.kb + sub * Ly.kbs + kshift(a.kstar + seq0_of(a, pidx * SPC + sub, h, tb));
     uint16_t* prow = reinterpret_cast<uint16_t*>(smem + Ly.prow);
     float* dk = reinterpret_cast<float*>(smem + Ly.dk);
     float* gs = reinterpret_cast<float*>(smem + Ly.gs + sub * Ly.gss);   // [32][N+1] g terms, then [32][NW] partials
@@ -611,10 +720,9 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq(SeqArgs a) {
     const int ngroups = (L + G - 1) / G;
     const uint64_t pol = fused::policy_evict_first();
     const TE* ein = static_cast<const TE*>(a.bias);
-    for (int x = jt; x < K * N; x += blockDim.x) prow[x] = (uint16_t)min((int)__ldg(a.dict_idx + (size_t)h * K * N + x), N - 1);
-    if constexpr (PD)
-        for (int x = jt; x < K * NC * N; x += blockDim.x) dk[x] = __ldg(a.diag_dict + (size_t)h * K * NC * N + x);
-    for (int q = 0; q < SPC; ++q) stage_k(a, smem + Ly.kb + q * Ly.kbs, (size_t)((pidx * SPC + q) * a.H + h) * a.L + tb, L);
+    for (int q = 0; q < SPC; ++q) stage_k(a, smem + Ly.kb + q * Ly.kbs, seq0_of(a, pidx * SPC + q, h, tb), L);
+    stage_prow(a.dict_idx + (size_t)h * K * N, prow, K * N, N);
+    if constexpr (PD) stage_f32(a.diag_dict + (size_t)h * K * NC * N, dk, K * NC * N);
     if (jt == 0) {
         for (int q = 0; q < 2 * R; ++q) fused::mbar_init(bars + q, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");

@@ -500,15 +500,15 @@ def test_seqc_chunked_single_cta_path(P, case, monkeypatch):
 
 def test_default_chunk_policy(P, monkeypatch):
     """Library default tau (R20): one CTA per sequence when the sequences fill most SMs (config 2
-    fp32 and bf16, config 4); the chunked single-CTA path with ~2 CTAs per SM for few, long
-    sequences at N <= 64 (config 5); the warp-per-chunk path (tau 64) otherwise (config 3)."""
+    fp32 and bf16, config 4); the chunked single-CTA path with ~2.8 chunks per SM for few, long
+    sequences (configs 3 and 5); the warp-per-chunk path (tau 64) when chunks would be short."""
     monkeypatch.delenv("PDSSM_PATH", raising=False)
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     d = lambda B, H, L, N, K, c, dt: P.default_chunk(P.make_dims(B, H, L, N, K, c=c, dtype=dt))
     assert d(16, 8, 2048, 128, 32, 2, P.F32) == 2048
     assert d(16, 8, 2048, 128, 32, 2, P.BF16) == 2048
     assert d(32, 32, 4096, 64, 48, 1, P.BF16) == 4096
-    assert d(4, 8, 17984, 128, 32, 1, P.F32) == 64          # N = 128: the warp-per-chunk path
-    C5 = -(-2 * sms // 16)
-    assert d(4, 4, 65536, 64, 16, 1, P.F32) == -(-65536 // C5)
+    chunks = lambda S: -(-28 * sms // (10 * S))
+    assert d(4, 8, 17984, 128, 32, 1, P.F32) == -(-17984 // chunks(32))
+    assert d(4, 4, 65536, 64, 16, 1, P.F32) == -(-65536 // chunks(16))
     assert d(1, 2, 300, 128, 32, 2, P.F32) == 64
