@@ -315,6 +315,15 @@ __device__ __forceinline__ void lds_sv_pred(uint32_t addr, int q, int m, float& 
 #define PDSSM_SEQ_PRED 0   // measured slower (config 2 fwd 0.185 -> 0.27 ms): the zero-slot reads stay
 #endif
 
+// packed fp32x2 add (sm_100a FADD2): the complex gather tree and the bias add in half the instructions
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+    float2 r;
+    asm("{.reg .b64 a, b, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\tadd.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;}"
+        : "=f"(r.x), "=f"(r.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return r;
+}
+
 template <typename T>
 __device__ __forceinline__ void st_stream(T* p, float v, uint64_t pol) {
     if constexpr (std::is_same<T, float>::value) {
@@ -557,7 +566,12 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
         k1 = kb[t + 2];
         // pairwise sum of the 8 slots (sources past the in-degree read the zero slot)
         auto sum8 = [&](const SV (&x)[CAP], float& sr, float& si) {
-            if constexpr (GCAP == 6) {
+            if constexpr (NC == 2) {   // packed: same pairwise order, FADD2
+                float2 t = add2(add2(x[0], x[1]), add2(x[2], x[3]));
+                t = add2(t, GCAP == 6 ? add2(x[4], x[5]) : add2(add2(x[4], x[5]), add2(x[6], x[7])));
+                sr = t.x;
+                si = t.y;
+            } else if constexpr (GCAP == 6) {
                 sr = ((fused::re_of<NC>(x[0]) + fused::re_of<NC>(x[1])) + (fused::re_of<NC>(x[2]) + fused::re_of<NC>(x[3]))) +
                      (fused::re_of<NC>(x[4]) + fused::re_of<NC>(x[5]));
                 si = ((fused::im_of<NC>(x[0]) + fused::im_of<NC>(x[1])) + (fused::im_of<NC>(x[2]) + fused::im_of<NC>(x[3]))) +
@@ -601,8 +615,14 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
                 }
             }
         }
-        hr = ar + bcr;
-        hi = NC == 2 ? ai + bci : 0.f;
+        if constexpr (NC == 2) {
+            const float2 hv = add2(make_float2(ar, ai), make_float2(bcr, bci));
+            hr = hv.x;
+            hi = hv.y;
+        } else {
+            hr = ar + bcr;
+            hi = 0.f;
+        }
         if constexpr (MODE != 1) {
             st_stream<T>(hout, hr, pol);
             if constexpr (NC == 2) st_stream<T>(hout + N, hi, pol);
