@@ -74,17 +74,17 @@ bool tc_operands_ok(const Geo& g, std::initializer_list<const void*> ptrs) {
 template <typename T>
 constexpr int tc_stages() { return std::is_same<T, float>::value ? 2 : 4; }
 
-template <typename T, class Epi, bool BPRE = false, int BPRE_STAGES = 3>
+template <typename T, class Epi, bool BPRE = false, int BPRE_STAGES = 3, int MT = 1>
 pdssm_status launch_tc_maps(const CUtensorMap& mA, const CUtensorMap& mB, int64_t kdim, int bn, tc::TileMap tm,
                             dim3 grid, Epi epi, cudaStream_t st, const char* what, const CUtensorMap* mBlo = nullptr) {
     constexpr bool SPLIT = std::is_same<T, float>::value;
     // pre-split weights: three stages of (A hi/lo + B hi/lo) slabs fit at bn <= 128, four at bn <= 64
     constexpr int STAGES = BPRE ? BPRE_STAGES : tc_stages<T>();
-    constexpr int BN_MAX = BPRE ? (BPRE_STAGES >= 4 ? 64 : 128) : 256;
-    using SM = tc::Smem<T, STAGES, SPLIT>;
+    constexpr int BN_MAX = (BPRE || MT > 1) ? (BPRE_STAGES >= 4 && MT == 1 ? 64 : 128) : 256;
+    using SM = tc::Smem<T, STAGES, SPLIT, MT>;
     const size_t smem = SM::bytes(BN_MAX);   // sized for the largest tile: one attribute per instantiation
     if (bn > BN_MAX) return fail(PDSSM_ERR_UNSUPPORTED, "%s: tile width %d above %d", what, bn, BN_MAX);
-    auto kern = tc::k_gemm_tc<T, STAGES, SPLIT, Epi, BPRE>;
+    auto kern = tc::k_gemm_tc<T, STAGES, SPLIT, Epi, BPRE, MT>;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
@@ -153,7 +153,7 @@ pdssm_status readout_tc(const Geo& g, const T* hseq, const T* Cp, T* y, cudaStre
     const int64_t cN = g.nc * g.N;
     const bool pre = std::is_same<T, float>::value && Cp_lo != nullptr && g.P <= 128;
     // pre-split fp32: 64-column tiles with four stages keep more of the states in flight
-    const bool narrow = pre && g.P % 64 == 0 && !getenv("PDSSM_READOUT_WIDE");
+    const bool narrow = pre && g.P % 64 == 0 && getenv("PDSSM_READOUT_NARROW");
     const int bn = narrow ? 64 : (int)(g.P < 256 ? g.P : 256);
     CUtensorMap mA, mB, mBl;
     const int64_t da[3] = {cN, g.L, g.S};
@@ -161,9 +161,17 @@ pdssm_status readout_tc(const Geo& g, const T* hseq, const T* Cp, T* y, cudaStre
     if (!make_map3(&mA, hseq, sizeof(T), da, sa, tc::BM, 1) || !make_kmajor_map(&mB, Cp, sizeof(T), cN, g.H * g.P, bn) ||
         (pre && !make_kmajor_map(&mBl, Cp_lo, sizeof(T), cN, g.H * g.P, bn)))
         return fail(PDSSM_ERR_CUDA, "readout_tc: cuTensorMapEncodeTiled failed");
-    const int tiles = (int)ceil_div(g.L, tc::BM);
+    // fp32 pre-split with bn = P <= 128: 256-row tiles sharing each weight slab (MT = 2)
+    // (opt-in: measured 113 vs 107 us at config 2 with the shared-tile stores: the two-stage ring
+    // it leaves room for costs more than the halved weight traffic saves)
+    const bool mt2 = pre && !narrow && bn <= 128 && getenv("PDSSM_READOUT_MT2");
+    const int tiles = (int)ceil_div(g.L, tc::BM * (mt2 ? 2 : 1));
     dim3 grid((unsigned)(tiles * g.S), (unsigned)ceil_div(g.P, bn));
     if constexpr (std::is_same<T, float>::value) {
+        if (mt2)
+            return launch_tc_maps<T, tc::EpiReadout<T>, true, 2, 2>(mA, mB, cN, bn, tc::TileMap{1, tiles, (int)g.H, (int)g.P},
+                                                                    grid, tc::EpiReadout<T>{y, (int)g.L, (int)g.H, (int)g.P},
+                                                                    st, "readout_tc", &mBl);
         if (pre && narrow)
             return launch_tc_maps<T, tc::EpiReadout<T>, true, 4>(mA, mB, cN, bn, tc::TileMap{1, tiles, (int)g.H, (int)g.P},
                                                                  grid, tc::EpiReadout<T>{y, (int)g.L, (int)g.H, (int)g.P},

@@ -59,6 +59,22 @@ __device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, int c0
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
         : "memory");
 }
+// L2 prefetch of a tensor box (no shared-memory destination): the producer runs one tile ahead so
+// that the ring's TMA loads of A hit L2 instead of DRAM (the ring holds only a few stages: the
+// DRAM latency x bandwidth product of one SM does not fit in it)
+__device__ __forceinline__ void tma_pf_2d(const CUtensorMap* map, int c0, int c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_pf_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+#ifndef PDSSM_TC_PREFETCH
+#define PDSSM_TC_PREFETCH 0   // measured: readout fp32 +4%, bf16 +15% slower; fp32 projection 4% faster
+#endif
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -419,14 +435,52 @@ template <typename TO>
 struct EpiReadout {
     TO* y;
     int L, H, P;
+    // tcgen05.ld gives thread = row (its 16 columns): stored directly (fp32), every warp store would
+    // write 32 rows 4 KB apart in 16-byte half sectors.  Each 32-column slice goes through a per-warp shared tile
+    // instead and leaves as 4 rows x 128 contiguous bytes per warp store (full sectors).
     __device__ void operator()(uint32_t taddr, int64_t t, int n0, int bn, int z) const {
-        const bool valid = t < L;
+        if constexpr (!std::is_same<TO, float>::value) {   // bf16: 16 columns = one 32-byte sector per row
+            const bool valid = t < L;
+            const int b = z / H, h = z - (z / H) * H;
+            for (int c0 = 0; c0 < bn; c0 += 16) {
+                float v[16];
+                tmem_ld16(taddr + (uint32_t)c0, v);
+                const int p = n0 + c0;
+                if (valid && p < P) st16<TO>(y + (((size_t)b * L + t) * H + h) * P + p, v);
+            }
+            return;
+        }
+        __shared__ float stile[4][32][33];   // [epilogue warp][row][column] (+1: conflict-free)
+        const int lane = threadIdx.x & 31;
+        float(*tl)[33] = stile[(threadIdx.x >> 5) & 3];
         const int b = z / H, h = z - (z / H) * H;
-        for (int c0 = 0; c0 < bn; c0 += 16) {
+        const int64_t tw = t - lane;   // first row of this warp
+        for (int c0 = 0; c0 < bn; c0 += 32) {
+            const int nc = bn - c0 < 32 ? bn - c0 : 32;   // 16 or 32 (bn % 16 == 0)
             float v[16];
             tmem_ld16(taddr + (uint32_t)c0, v);
-            const int p = n0 + c0;
-            if (valid && p < P) st16<TO>(y + (((size_t)b * L + t) * H + h) * P + p, v);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) tl[lane][i] = v[i];
+            if (nc > 16) {
+                tmem_ld16(taddr + (uint32_t)(c0 + 16), v);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) tl[lane][16 + i] = v[i];
+            }
+            __syncwarp();
+            const int cc = (lane & 7) * 4;
+            const int p = n0 + c0 + cc;
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+                const int rr = it * 4 + (lane >> 3);
+                const int64_t tr = tw + rr;
+#ifndef PDSSM_EXP_NOSTORE   // timing experiment only (no output)
+                if (tr < L && cc < nc && p < P) {
+                    TO* dst = y + (((size_t)b * L + tr) * H + h) * P + p;
+                    *reinterpret_cast<float4*>(dst) = make_float4(tl[rr][cc], tl[rr][cc + 1], tl[rr][cc + 2], tl[rr][cc + 3]);
+                }
+#endif
+            }
+            __syncwarp();
         }
     }
 };
@@ -473,15 +527,19 @@ struct TileMap {
 // lo = a - hi (a twin slab at the same swizzled offsets); the MMA warp then issues
 // lo*hi + hi*lo + hi*hi per K step, which keeps the products to ~2^-21 relative
 // (plain TF32 would be 2^-11), i.e. fp32-grade logits and projections.
+#ifndef PDSSM_TC_RAWHI
+#define PDSSM_TC_RAWHI 1
+#endif
 __device__ __forceinline__ uint32_t tf32_rna(float a) {
     uint32_t r;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(a));
     return r;
 }
 
-template <typename T, int STAGES, bool SPLIT>
+template <typename T, int STAGES, bool SPLIT, int MT = 1>
 struct Smem {
-    __host__ __device__ static constexpr size_t slot(int bn) { return (size_t)(BM + bn) * ROWB; }   // A rows then B rows
+    // A rows (MT row tiles of BM) then B rows
+    __host__ __device__ static constexpr size_t slot(int bn) { return (size_t)(MT * BM + bn) * ROWB; }
     __host__ __device__ static constexpr size_t ring(int bn) { return (size_t)STAGES * slot(bn) * (SPLIT ? 2 : 1); }
     __host__ __device__ static constexpr size_t bytes(int bn) { return 1024 + ring(bn) + 8 * (3 * STAGES + 4) + 16; }
 };
@@ -498,12 +556,16 @@ struct TileGrid {
 // BPRE (with SPLIT): the weights B arrive pre-split in global memory (mB = tf32 hi part, mBlo = the
 // lo part, written once per call by the host path), so the converter warps split only the A rows
 // of each slab -- half the shared-memory traffic of the split (readout: B = the readout weights).
-template <typename T, int STAGES, bool SPLIT, class Epi, bool BPRE = false>
+// MT = 2 (bn <= 128): a tile is 2 x BM rows sharing every B slab (two MMAs per K step into the two
+// 128-column halves of the tile's accumulator): half the B traffic per output (the readout reloads
+// its per-head weights for every tile: B was 2/3 of its L2 -> SM bytes at MT = 1).
+template <typename T, int STAGES, bool SPLIT, class Epi, bool BPRE = false, int MT = 1>
 __global__ void __launch_bounds__(THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB,
               const __grid_constant__ CUtensorMap mBlo, int nk, int bn, TileMap tm, TileGrid tg, Epi epi) {
     static_assert(!BPRE || SPLIT, "pre-split weights only with the 3xTF32 split");
-    using SM = Smem<T, STAGES, SPLIT>;
+    static_assert(MT == 1 || MT == 2, "row tiles per CTA tile");
+    using SM = Smem<T, STAGES, SPLIT, MT>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     const size_t SLOT = SM::slot(bn);                  // multiple of 1024 (bn % 8 == 0)
@@ -551,15 +613,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         n0 = by * bn;
         if (tm.mode == 1) {
             z = bx / tm.tiles;
-            m0 = (int64_t)(bx - z * tm.tiles) * BM;
+            m0 = (int64_t)(bx - z * tm.tiles) * (BM * MT);
             brow = (z % tm.zmod) * tm.brows + n0;
         } else if (tm.mode == 2) {
             z = bz;
-            m0 = (int64_t)bx * BM;
+            m0 = (int64_t)bx * (BM * MT);
             brow = z * tm.brows + n0;
         } else {
             z = 0;
-            m0 = (int64_t)bx * BM;
+            m0 = (int64_t)bx * (BM * MT);
             brow = n0;
         }
     };
@@ -572,15 +634,34 @@ __global__ void __launch_bounds__(THREADS, 1)
                 int64_t m0;
                 int n0, z, brow;
                 coords(id, m0, n0, z, brow);
+                int64_t m0n = 0;
+                int n0n = 0, zn = 0, brown = 0;
+                const int idn = id + (int)gridDim.x;   // this CTA's next tile
+                const bool pfn = PDSSM_TC_PREFETCH && idn < ntiles;
+                if (pfn) coords(idn, m0n, n0n, zn, brown);
                 for (int kb = 0; kb < nk; ++kb, ++kg) {
                     const int s = kg % STAGES;
+                    if (pfn) {   // the next tile's A slab kb -> L2
+#pragma unroll
+                        for (int mt = 0; mt < MT; ++mt) {
+                            const int mr = (int)m0n + mt * BM;
+                            if (tm.mode == 1) tma_pf_3d(&mA, kb * EK, mr, zn);
+                            else if (tm.mode == 2) tma_pf_3d(&mA, kb * EK, zn, mr);
+                            else tma_pf_2d(&mA, kb * EK, mr);
+                        }
+                    }
                     if (kg >= STAGES) mbar_wait(empty + s, (uint32_t)((kg / STAGES) + 1) & 1u);
                     mbar_expect_tx(full + s, bytes);
-                    if (tm.mode == 1) tma_3d(hi(s), &mA, kb * EK, (int)m0, z, full + s);
-                    else if (tm.mode == 2) tma_3d(hi(s), &mA, kb * EK, z, (int)m0, full + s);
-                    else tma_2d(hi(s), &mA, kb * EK, (int)m0, full + s);
-                    tma_2d(hi(s) + (size_t)BM * ROWB, &mB, kb * EK, brow, full + s);
-                    if constexpr (BPRE) tma_2d(lo(s) + (size_t)BM * ROWB, &mBlo, kb * EK, brow, full + s);
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt) {
+                        uint8_t* da = hi(s) + (size_t)mt * BM * ROWB;
+                        const int mr = (int)m0 + mt * BM;
+                        if (tm.mode == 1) tma_3d(da, &mA, kb * EK, mr, z, full + s);
+                        else if (tm.mode == 2) tma_3d(da, &mA, kb * EK, z, mr, full + s);
+                        else tma_2d(da, &mA, kb * EK, mr, full + s);
+                    }
+                    tma_2d(hi(s) + (size_t)MT * BM * ROWB, &mB, kb * EK, brow, full + s);
+                    if constexpr (BPRE) tma_2d(lo(s) + (size_t)MT * BM * ROWB, &mBlo, kb * EK, brow, full + s);
                 }
             }
         }
@@ -597,17 +678,25 @@ __global__ void __launch_bounds__(THREADS, 1)
                     const int s = kg % STAGES;
                     mbar_wait((SPLIT ? conv : full) + s, (uint32_t)(kg / STAGES) & 1u);
                     fence_after();
-                    const uint64_t ah = sdesc(su32(hi(s))), bh = sdesc(su32(hi(s) + (size_t)BM * ROWB));
-                    const uint64_t al = sdesc(su32(lo(s))), bl = sdesc(su32(lo(s) + (size_t)BM * ROWB));
+                    const uint64_t bh = sdesc(su32(hi(s) + (size_t)MT * BM * ROWB));
+                    const uint64_t bl = sdesc(su32(lo(s) + (size_t)MT * BM * ROWB));
 #pragma unroll
                     for (int k = 0; k < ROWB / 32; ++k) {   // 32 bytes of K per instruction
                         const uint32_t acc0 = (kb | k) != 0;
-                        if constexpr (SPLIT) {
-                            Kind<T>::mma(tacc, al + 2 * k, bh + 2 * k, id_, acc0);
-                            Kind<T>::mma(tacc, ah + 2 * k, bl + 2 * k, id_, 1u);
-                            Kind<T>::mma(tacc, ah + 2 * k, bh + 2 * k, id_, 1u);
-                        } else {
-                            Kind<T>::mma(tacc, ah + 2 * k, bh + 2 * k, id_, acc0);
+#pragma unroll
+                        for (int mt = 0; mt < MT; ++mt) {
+                            const uint64_t ah = sdesc(su32(hi(s) + (size_t)mt * BM * ROWB));
+                            const uint64_t al = sdesc(su32(lo(s) + (size_t)mt * BM * ROWB));
+                            const uint32_t tm_ = tacc + (uint32_t)(mt * 128);
+                            if constexpr (SPLIT) {
+#ifndef PDSSM_EXP_ONEMMA   // timing experiment only (plain TF32)
+                                Kind<T>::mma(tm_, al + 2 * k, bh + 2 * k, id_, acc0);
+                                Kind<T>::mma(tm_, ah + 2 * k, bl + 2 * k, id_, 1u);
+#endif
+                                Kind<T>::mma(tm_, ah + 2 * k, bh + 2 * k, id_, 1u);
+                            } else {
+                                Kind<T>::mma(tm_, ah + 2 * k, bh + 2 * k, id_, acc0);
+                            }
                         }
                     }
                     commit(empty + s);
@@ -626,7 +715,10 @@ __global__ void __launch_bounds__(THREADS, 1)
             coords(id, m0, n0, z, brow);
             mbar_wait(tfull + acc, (uint32_t)(j / 2) & 1u);
             fence_after();
-            epi(tmem + (uint32_t)(acc * 256) + ((uint32_t)(32 * q) << 16), m0 + 32 * q + lane, n0, bn, z);
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt)
+                epi(tmem + (uint32_t)(acc * 256 + mt * 128) + ((uint32_t)(32 * q) << 16), m0 + mt * BM + 32 * q + lane, n0,
+                    bn, z);
             fence_before();
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(tempty + acc)) : "memory");
@@ -636,7 +728,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             // converters: split every landed slab (the producer reused slot s only after the
             // MMAs of its previous round completed, and full[s] completes after that reuse)
             const int ct = threadIdx.x - 256;
-            const int nchunks = (BPRE ? BM : BM + bn) * (ROWB / 16);   // BPRE: the B rows arrive split
+            const int nchunks = (BPRE ? MT * BM : MT * BM + bn) * (ROWB / 16);   // BPRE: the B rows arrive split
             int kg = 0;
             for (int id = blockIdx.x; id < ntiles; id += gridDim.x) {
                 for (int kb = 0; kb < nk; ++kb, ++kg) {
@@ -644,12 +736,25 @@ __global__ void __launch_bounds__(THREADS, 1)
                     mbar_wait(full + s, (uint32_t)(kg / STAGES) & 1u);
                     float4* ph = reinterpret_cast<float4*>(hi(s));
                     float4* pl = reinterpret_cast<float4*>(lo(s));
+#ifdef PDSSM_EXP_NOCONV   // timing experiment only (lo parts left as they are)
+                    for (int i = ct; i < 0; i += NCONV * 32) {
+#else
                     for (int i = ct; i < nchunks; i += NCONV * 32) {
+#endif
                         const float4 a = ph[i];
+#if PDSSM_TC_RAWHI
+                        // hi stays the raw fp32 slab: kind::tf32 reads only its top 19 bits (truncation),
+                        // so lo = a - trunc(a) (exact) is the only store -- half the split's shared traffic
+                        pl[i] = make_float4(a.x - __uint_as_float(__float_as_uint(a.x) & 0xffffe000u),
+                                            a.y - __uint_as_float(__float_as_uint(a.y) & 0xffffe000u),
+                                            a.z - __uint_as_float(__float_as_uint(a.z) & 0xffffe000u),
+                                            a.w - __uint_as_float(__float_as_uint(a.w) & 0xffffe000u));
+#else
                         const uint32_t h0 = tf32_rna(a.x), h1 = tf32_rna(a.y), h2 = tf32_rna(a.z), h3 = tf32_rna(a.w);
                         ph[i] = make_float4(__uint_as_float(h0), __uint_as_float(h1), __uint_as_float(h2), __uint_as_float(h3));
                         pl[i] = make_float4(a.x - __uint_as_float(h0), a.y - __uint_as_float(h1), a.z - __uint_as_float(h2),
                                             a.w - __uint_as_float(h3));
+#endif
                     }
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> MMA reads
                     __syncwarp();
