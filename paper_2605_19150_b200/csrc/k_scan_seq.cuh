@@ -917,11 +917,19 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq(SeqArgs a) {
             }
             km1 = t >= 2 ? kb[t - 2] : 0;
         }
+        // (real scans, NC = 1: the imaginary terms are spelled out away -- x * 0 does not fold in IEEE
+        // arithmetic, so the complex expressions would cost ~6 instructions per step for nothing)
         const float pr = fused::re_of<NC>(lpv), pm = fused::im_of<NC>(lpv);
-        lr = ecr + Dcr * pr + Dci * pm;                   // lambda_{t-1} = e_{t-1} + conj(D_t) lp
-        li = NC == 2 ? eci + Dcr * pm - Dci * pr : 0.f;
+        if constexpr (NC == 2) {
+            lr = ecr + Dcr * pr + Dci * pm;               // lambda_{t-1} = e_{t-1} + conj(D_t) lp
+            li = eci + Dcr * pm - Dci * pr;
+        } else {
+            lr = ecr + Dcr * pr;
+            li = 0.f;
+        }
         if constexpr (EMIT) {
-            const float ddr = hcr * pr + hci * pm, ddi = hcr * pm - hci * pr;   // dD_t = conj(h_{t-1}) lp
+            const float ddr = NC == 2 ? hcr * pr + hci * pm : hcr * pr;   // dD_t = conj(h_{t-1}) lp
+            const float ddi = NC == 2 ? hcr * pm - hci * pr : 0.f;
             if constexpr (PD) {
                 ddf[0] = ddr;
                 if constexpr (NC == 2) ddf[N] = ddi;
@@ -931,8 +939,12 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq(SeqArgs a) {
                 if constexpr (NC == 2) st_stream<T>(ddp + N, ddi, pol);
                 ddp -= row;
             }
-            const float qr = Dcr * hcr - Dci * hci, qi = Dcr * hci + Dci * hcr;
-            gs[(size_t)(v & 31) * (N + 1) + j] = pr * qr + pm * qi;   // this thread's term of g_t
+            if constexpr (NC == 2) {
+                const float qr = Dcr * hcr - Dci * hci, qi = Dcr * hci + Dci * hcr;
+                gs[(size_t)(v & 31) * (N + 1) + j] = pr * qr + pm * qi;   // this thread's term of g_t
+            } else {
+                gs[(size_t)(v & 31) * (N + 1) + j] = pr * (Dcr * hcr);
+            }
         }
     };
     for (int g = 0; g < ngroups; ++g) {
