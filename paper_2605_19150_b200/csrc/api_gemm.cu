@@ -74,17 +74,17 @@ bool tc_operands_ok(const Geo& g, std::initializer_list<const void*> ptrs) {
 template <typename T>
 constexpr int tc_stages() { return std::is_same<T, float>::value ? 2 : 4; }
 
-template <typename T, class Epi, bool BPRE = false, int BPRE_STAGES = 3, int MT = 1>
+template <typename T, class Epi, bool BPRE = false, int BPRE_STAGES = 3, int MT = 1, bool ATM = false>
 pdssm_status launch_tc_maps(const CUtensorMap& mA, const CUtensorMap& mB, int64_t kdim, int bn, tc::TileMap tm,
                             dim3 grid, Epi epi, cudaStream_t st, const char* what, const CUtensorMap* mBlo = nullptr) {
     constexpr bool SPLIT = std::is_same<T, float>::value;
     // pre-split weights: three stages of (A hi/lo + B hi/lo) slabs fit at bn <= 128, four at bn <= 64
     constexpr int STAGES = BPRE ? BPRE_STAGES : tc_stages<T>();
-    constexpr int BN_MAX = (BPRE || MT > 1) ? (BPRE_STAGES >= 4 && MT == 1 ? 64 : 128) : 256;
-    using SM = tc::Smem<T, STAGES, SPLIT, MT>;
+    constexpr int BN_MAX = (BPRE || MT > 1) ? (BPRE_STAGES >= 4 && MT == 1 && !ATM ? 64 : 128) : 256;
+    using SM = tc::Smem<T, STAGES, SPLIT, MT, ATM>;
     const size_t smem = SM::bytes(BN_MAX);   // sized for the largest tile: one attribute per instantiation
     if (bn > BN_MAX) return fail(PDSSM_ERR_UNSUPPORTED, "%s: tile width %d above %d", what, bn, BN_MAX);
-    auto kern = tc::k_gemm_tc<T, STAGES, SPLIT, Epi, BPRE, MT>;
+    auto kern = tc::k_gemm_tc<T, STAGES, SPLIT, Epi, BPRE, MT, ATM>;
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
     std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); });
@@ -167,7 +167,14 @@ pdssm_status readout_tc(const Geo& g, const T* hseq, const T* Cp, T* y, cudaStre
     const bool mt2 = pre && !narrow && bn <= 128 && getenv("PDSSM_READOUT_MT2");
     const int tiles = (int)ceil_div(g.L, tc::BM * (mt2 ? 2 : 1));
     dim3 grid((unsigned)(tiles * g.S), (unsigned)ceil_div(g.P, bn));
+    // fp32 pre-split, bn <= 128: A (the states) from tensor memory (PDSSM_READOUT_ATM=0: from shared memory)
+    const char* atm_env = getenv("PDSSM_READOUT_ATM");
+    const bool atm = pre && !narrow && !mt2 && bn <= 128 && !(atm_env && atm_env[0] == '0');
     if constexpr (std::is_same<T, float>::value) {
+        if (atm)
+            return launch_tc_maps<T, tc::EpiReadout<T>, true, 4, 1, true>(mA, mB, cN, bn, tc::TileMap{1, tiles, (int)g.H, (int)g.P},
+                                                                          grid, tc::EpiReadout<T>{y, (int)g.L, (int)g.H, (int)g.P},
+                                                                          st, "readout_tc", &mBl);
         if (mt2)
             return launch_tc_maps<T, tc::EpiReadout<T>, true, 2, 2>(mA, mB, cN, bn, tc::TileMap{1, tiles, (int)g.H, (int)g.P},
                                                                     grid, tc::EpiReadout<T>{y, (int)g.L, (int)g.H, (int)g.P},

@@ -119,6 +119,24 @@ struct Kind<float> {
     }
 };
 
+// D (+)= A B with A from tensor memory (tf32, K-major rows = TMEM lanes), B from shared memory
+__device__ __forceinline__ void mma_ta(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t id, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(b), "r"(id), "r"(acc)
+        : "memory");
+}
+// 16 consecutive 32-bit columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+        "%16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+
 __device__ __forceinline__ void commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
                  : "memory");
@@ -536,11 +554,11 @@ __device__ __forceinline__ uint32_t tf32_rna(float a) {
     return r;
 }
 
-template <typename T, int STAGES, bool SPLIT, int MT = 1>
+template <typename T, int STAGES, bool SPLIT, int MT = 1, bool ATM = false>
 struct Smem {
-    // A rows (MT row tiles of BM) then B rows
-    __host__ __device__ static constexpr size_t slot(int bn) { return (size_t)(MT * BM + bn) * ROWB; }
-    __host__ __device__ static constexpr size_t ring(int bn) { return (size_t)STAGES * slot(bn) * (SPLIT ? 2 : 1); }
+    // A rows (MT row tiles of BM) then B rows (ATM: then the B lo rows; the A lo parts live in TMEM)
+    __host__ __device__ static constexpr size_t slot(int bn) { return (size_t)(MT * BM + bn * (ATM ? 2 : 1)) * ROWB; }
+    __host__ __device__ static constexpr size_t ring(int bn) { return (size_t)STAGES * slot(bn) * (SPLIT && !ATM ? 2 : 1); }
     __host__ __device__ static constexpr size_t bytes(int bn) { return 1024 + ring(bn) + 8 * (3 * STAGES + 4) + 16; }
 };
 
@@ -559,13 +577,21 @@ struct TileGrid {
 // MT = 2 (bn <= 128): a tile is 2 x BM rows sharing every B slab (two MMAs per K step into the two
 // 128-column halves of the tile's accumulator): half the B traffic per output (the readout reloads
 // its per-head weights for every tile: B was 2/3 of its L2 -> SM bytes at MT = 1).
-template <typename T, int STAGES, bool SPLIT, class Epi, bool BPRE = false, int MT = 1>
+// ATM (with SPLIT, BPRE, MT = 1, bn <= 128): the A operand is read from TENSOR memory.  The tf32
+// MMAs at N = 128 read 8 KB of shared operands per 64-cycle instruction -- the whole shared-memory
+// bandwidth, three times per K step with the 3xTF32 split; with A (raw hi and lo, written by the
+// converter warps with tcgen05.st straight from the landed slab) in TMEM, only B is read from shared
+// memory.  TMEM: accumulators 2 x 128 columns, then STAGES x (32 hi + 32 lo) A columns.
+template <typename T, int STAGES, bool SPLIT, class Epi, bool BPRE = false, int MT = 1, bool ATM = false>
 __global__ void __launch_bounds__(THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB,
               const __grid_constant__ CUtensorMap mBlo, int nk, int bn, TileMap tm, TileGrid tg, Epi epi) {
     static_assert(!BPRE || SPLIT, "pre-split weights only with the 3xTF32 split");
     static_assert(MT == 1 || MT == 2, "row tiles per CTA tile");
-    using SM = Smem<T, STAGES, SPLIT, MT>;
+    static_assert(!ATM || (SPLIT && BPRE && MT == 1 && 256 + STAGES * 64 <= 512), "A in TMEM: readout shape");
+    constexpr uint32_t ACCS = ATM ? 128 : 256;   // accumulator stride (columns)
+    constexpr uint32_t ACOL = 256;               // ATM: first A column
+    using SM = Smem<T, STAGES, SPLIT, MT, ATM>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     const size_t SLOT = SM::slot(bn);                  // multiple of 1024 (bn % 8 == 0)
@@ -628,7 +654,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     constexpr int EK = ROWB / (int)sizeof(T);   // elements of K per slab row
     if (warp == 0) {
         if (lane == 0) {
-            const uint32_t bytes = (uint32_t)(SLOT + (BPRE ? (size_t)bn * ROWB : 0));
+            const uint32_t bytes = (uint32_t)(SLOT + (BPRE && !ATM ? (size_t)bn * ROWB : 0));
             int kg = 0;
             for (int id = blockIdx.x; id < ntiles; id += gridDim.x) {
                 int64_t m0;
@@ -661,7 +687,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                         else tma_2d(da, &mA, kb * EK, mr, full + s);
                     }
                     tma_2d(hi(s) + (size_t)MT * BM * ROWB, &mB, kb * EK, brow, full + s);
-                    if constexpr (BPRE) tma_2d(lo(s) + (size_t)MT * BM * ROWB, &mBlo, kb * EK, brow, full + s);
+                    if constexpr (ATM) tma_2d(hi(s) + (size_t)(BM + bn) * ROWB, &mBlo, kb * EK, brow, full + s);
+                    else if constexpr (BPRE) tma_2d(lo(s) + (size_t)MT * BM * ROWB, &mBlo, kb * EK, brow, full + s);
                 }
             }
         }
@@ -673,13 +700,25 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const int acc = j & 1;
                 if (j >= 2) mbar_wait(tempty + acc, (uint32_t)((j / 2) - 1) & 1u);   // epilogue drained it
                 fence_after();
-                const uint32_t tacc = tmem + (uint32_t)(acc * 256);
+                const uint32_t tacc = tmem + (uint32_t)acc * ACCS;
                 for (int kb = 0; kb < nk; ++kb, ++kg) {
                     const int s = kg % STAGES;
                     mbar_wait((SPLIT ? conv : full) + s, (uint32_t)(kg / STAGES) & 1u);
                     fence_after();
                     const uint64_t bh = sdesc(su32(hi(s) + (size_t)MT * BM * ROWB));
-                    const uint64_t bl = sdesc(su32(lo(s) + (size_t)MT * BM * ROWB));
+                    const uint64_t bl = sdesc(su32(ATM ? hi(s) + (size_t)(BM + bn) * ROWB : lo(s) + (size_t)MT * BM * ROWB));
+                    if constexpr (ATM) {
+                        const uint32_t ah = tmem + ACOL + (uint32_t)s * 64, al = ah + 32;
+#pragma unroll
+                        for (int k = 0; k < ROWB / 32; ++k) {   // 8 tf32 columns of A per instruction
+                            const uint32_t acc0 = (kb | k) != 0;
+                            mma_ta(tacc, al + 8 * k, bh + 2 * k, id_, acc0);
+                            mma_ta(tacc, ah + 8 * k, bl + 2 * k, id_, 1u);
+                            mma_ta(tacc, ah + 8 * k, bh + 2 * k, id_, 1u);
+                        }
+                        commit(empty + s);
+                        continue;
+                    }
 #pragma unroll
                     for (int k = 0; k < ROWB / 32; ++k) {   // 32 bytes of K per instruction
                         const uint32_t acc0 = (kb | k) != 0;
@@ -717,14 +756,49 @@ __global__ void __launch_bounds__(THREADS, 1)
             fence_after();
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt)
-                epi(tmem + (uint32_t)(acc * 256 + mt * 128) + ((uint32_t)(32 * q) << 16), m0 + mt * BM + 32 * q + lane, n0,
-                    bn, z);
+                epi(tmem + (uint32_t)acc * ACCS + (uint32_t)(mt * 128) + ((uint32_t)(32 * q) << 16), m0 + mt * BM + 32 * q + lane,
+                    n0, bn, z);
             fence_before();
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(tempty + acc)) : "memory");
         }
     } else if (warp >= 8) {
-        if constexpr (SPLIT) {
+        if constexpr (ATM) {
+            // converters -> TMEM: warp 8 + q and 12 + q serve the tile rows 32q..32q+31 (their TMEM lane
+            // quarter), K elements 0..15 and 16..31 of each landed slab; raw fp32 = hi (the MMA
+            // truncates to tf32), lo = a - trunc(a).  The A columns of stage s are rewritten only after
+            // full[s] completed again, i.e. after the MMAs that read them committed (empty[s]).
+            const int q = warp & 3, hk = (warp - 8) >> 2;
+            const int m = 32 * q + lane;   // this thread's tile row
+            int kg = 0;
+            for (int id = blockIdx.x; id < ntiles; id += gridDim.x) {
+                for (int kb = 0; kb < nk; ++kb, ++kg) {
+                    const int s = kg % STAGES;
+                    mbar_wait(full + s, (uint32_t)(kg / STAGES) & 1u);
+                    const uint8_t* rowp = hi(s) + (size_t)m * ROWB;
+                    uint32_t rh[16], rl[16];
+#pragma unroll
+                    for (int cc = 0; cc < 4; ++cc) {   // 16-byte chunk 4 hk + cc of the SWIZZLE_128B row
+                        const int c = 4 * hk + cc;
+                        const float4 a = *reinterpret_cast<const float4*>(rowp + ((c ^ (m & 7)) << 4));
+                        const float av[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const uint32_t bits = __float_as_uint(av[u]);
+                            rh[4 * cc + u] = bits;
+                            rl[4 * cc + u] = __float_as_uint(av[u] - __uint_as_float(bits & 0xffffe000u));
+                        }
+                    }
+                    const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + ACOL + (uint32_t)s * 64 + (uint32_t)(16 * hk);
+                    tmem_st16(ta, rh);
+                    tmem_st16(ta + 32, rl);
+                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                    fence_before();
+                    __syncwarp();
+                    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(conv + s)) : "memory");
+                }
+            }
+        } else if constexpr (SPLIT) {
             // converters: split every landed slab (the producer reused slot s only after the
             // MMAs of its previous round completed, and full[s] completes after that reuse)
             const int ct = threadIdx.x - 256;
