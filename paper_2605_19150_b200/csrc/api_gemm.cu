@@ -93,7 +93,22 @@ pdssm_status launch_tc_maps(const CUtensorMap& mA, const CUtensorMap& mB, int64_
     const tc::TileGrid tg{(int)grid.x, (int)grid.y, (int)grid.z};
     const int ntiles = tg.gx * tg.gy * tg.gz;
     const int nctas = ntiles < num_sms_dev() ? ntiles : num_sms_dev();   // persistent
-    kern<<<nctas, tc::THREADS, SM::bytes(bn), st>>>(mA, mB, mBlo ? *mBlo : mB, nk, bn, tm, tg, epi);
+    // programmatic dependent launch: the prologue (barriers, TMEM allocation, tensormap prefetch)
+    // overlaps the tail of the previous launch (the readout's weight split triggers it at entry);
+    // the TMA producer's griddepcontrol.wait orders every global access of the kernel after it
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)nctas);
+    cfg.blockDim = dim3(tc::THREADS);
+    cfg.dynamicSmemBytes = SM::bytes(bn);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const CUtensorMap mBl = mBlo ? *mBlo : mB;
+    cudaError_t le = cudaLaunchKernelEx(&cfg, kern, mA, mB, mBl, (int)nk, bn, tm, tg, epi);
+    if (le != cudaSuccess) return fail(PDSSM_ERR_CUDA, "%s launch: %s", what, cudaGetErrorString(le));
     return cuda_check(what);
 }
 
@@ -116,6 +131,7 @@ pdssm_status launch_tc(const Geo& g, const void* A, int64_t rows_a, const void* 
 template <typename T>
 __global__ void k_readout_weights(const float* __restrict__ C, T* __restrict__ Cp, T* __restrict__ CT, int H, int nc,
                                   int P, int N, float* __restrict__ Cp_lo = nullptr) {
+    asm volatile("griddepcontrol.launch_dependents;");   // the GEMM after it may start its prologue
     const int64_t total = (int64_t)H * nc * P * N;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int n = (int)(i % N);

@@ -654,6 +654,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     constexpr int EK = ROWB / (int)sizeof(T);   // elements of K per slab row
     if (warp == 0) {
         if (lane == 0) {
+            // (programmatic dependent launch) everything this kernel reads or writes in global memory
+            // is ordered after the producer's first load, hence after the previous launch completed
+            asm volatile("griddepcontrol.wait;" ::: "memory");
             const uint32_t bytes = (uint32_t)(SLOT + (BPRE && !ATM ? (size_t)bn * ROWB : 0));
             int kg = 0;
             for (int id = blockIdx.x; id < ntiles; id += gridDim.x) {

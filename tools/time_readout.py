@@ -38,3 +38,15 @@ err = float((got - ref).abs().max() / ref.abs().max())
 byt = h.numel() * h.element_size() + y.numel() * y.element_size()
 print(f"readout {dt} {us:.1f} us  {byt / us / 1e3:.0f} GB/s  rel_err {err:.2e}  variant={os.environ.get('PDSSM_LIB_VARIANT', '')} "
       f"wide={os.environ.get('PDSSM_READOUT_WIDE', '')}")
+# per-kernel device durations (torch profiler, CUPTI): the GEMM alone vs the per-call weight split
+try:
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for _ in range(5):
+            P.readout(h, Cw, out=y, ws=ws)
+        torch.cuda.synchronize()
+    for ev in prof.key_averages():
+        if ev.device_type.name == "CUDA" or "pdssm" in ev.key:
+            print(f"  {ev.key[:90]:90s} {ev.device_time_total / max(ev.count, 1):8.1f} us x{ev.count}")
+except Exception as e:   # profiler unavailable: the wall-clock number above stands
+    print("profiler:", e)
