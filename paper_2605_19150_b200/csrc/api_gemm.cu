@@ -412,9 +412,16 @@ pdssm_status layer_gemm(const Geo& g, const void* x, const void* S, const uint16
                             lt.n_sel, lt.n_prj};
         dim3 grid((unsigned)ceil_div(M, tc::BM), (unsigned)(n_tot / lt.bn));
         *done = true;
-        if constexpr (F32)
+        if constexpr (F32) {
+            // A (the token rows) from tensor memory (bn = 128): the MMAs read only the weights from shared
+            // memory (PDSSM_LAYER_ATM=0: the shared-memory split)
+            const char* e = getenv("PDSSM_LAYER_ATM");
+            if (lt.bn <= 128 && !(e && e[0] == '0'))
+                return launch_tc_maps<T, tc::EpiLayer<T>, true, 4, 1, true>(mA, mB, g.d_in, lt.bn, tc::TileMap{0, 1, 1, 0}, grid,
+                                                                            epi, st, "layer_gemm", &mBl);
             return launch_tc_maps<T, tc::EpiLayer<T>, true>(mA, mB, g.d_in, lt.bn, tc::TileMap{0, 1, 1, 0}, grid, epi, st,
                                                             "layer_gemm", &mBl);
+        }
         else
             return launch_tc_maps<T>(mA, mB, g.d_in, lt.bn, tc::TileMap{0, 1, 1, 0}, grid, epi, st, "layer_gemm");
     });
