@@ -84,13 +84,14 @@ def test_project_validation(P):
 @pytest.mark.parametrize("shape", [(2, 2, 300, 2, 64, 32), (1, 3, 129, 1, 32, 16), (2, 1, 70, 2, 16, 5),
                                    (1, 8, 256, 2, 128, 128), (2, 2, 700, 2, 128, 128), (1, 2, 384, 1, 128, 96)])
 @pytest.mark.parametrize("bf16", [False, True])
-@pytest.mark.parametrize("variant", ["", "PDSSM_READOUT_MT2", "PDSSM_READOUT_NARROW"])
+@pytest.mark.parametrize("variant", ["", "PDSSM_READOUT_MT2", "PDSSM_READOUT_NARROW", "PDSSM_READOUT_ATM=0"])
 def test_readout_standalone(P, path, shape, bf16, variant, monkeypatch):
     """a8 readout y_t = Re(C_h h_t) (Eq. 1) on given states, against oracle.readout."""
-    if variant:   # the opt-in tilings of the fp32 tensor-core readout (MT = 2 row tiles, 64-column tiles)
+    if variant:   # the other tilings of the fp32 tensor-core readout (MT = 2 row tiles, 64-column tiles, A in smem)
         if bf16:
             pytest.skip("fp32 pre-split variants")
-        monkeypatch.setenv(variant, "1")
+        name, _, val = variant.partition("=")
+        monkeypatch.setenv(name, val or "1")
     B, H, L, c, N, Pp = shape
     rng = np.random.default_rng(L + N)
     h = rng.standard_normal((B, H, L, c, N)).astype(np.float32)

@@ -299,11 +299,14 @@ def test_soft_select_parity(P, N, K, bf16):
     assert got.min() >= 0 and got.max() < N
 
 
-@pytest.mark.parametrize("c,N,bf16", [(2, 128, False), (1, 64, False), (2, 64, True)])
-def test_layer_fwd_gen_parity(P, c, N, bf16):
+@pytest.mark.parametrize("c,N,bf16,atm", [(2, 128, False, "1"), (1, 64, False, "1"), (2, 64, True, "1"),
+                                          (2, 128, False, "0")])
+def test_layer_fwd_gen_parity(P, c, N, bf16, atm, monkeypatch):
     """NEXT-2: selector + projection + D_t generator as one fused tcgen05 GEMM (pdssm_layer_fwd_gen),
     then the scan and the readout, against the oracle chain select -> project_b -> diag_generator ->
-    scan_forward -> readout (R30).  Integer-valued x, S: the selections are exact (R18)."""
+    scan_forward -> readout (R30).  Integer-valued x, S: the selections are exact (R18).
+    atm "0": the fp32 fused GEMM with the token rows in shared memory instead of tensor memory."""
+    monkeypatch.setenv("PDSSM_LAYER_ATM", atm)
     B, H, L, K, d_in, Pp = 2, 2, 150, 8, 64, 32
     x = synth.tokens_x(B, L, d_in, seed=N + 1, integer=True)
     S = synth.selector(H, K, d_in, seed=N + 1, integer=True)
