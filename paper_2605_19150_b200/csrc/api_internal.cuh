@@ -266,7 +266,9 @@ inline int seq_ring(const Geo& g, bool bwd, bool agg, size_t esz_e, int spc = 1,
     if (Lk <= 0) Lk = g.L;
     const int ngroups = (int)ceil_div(Lk, G);
     const int64_t ctas = ctas_in > 0 ? ctas_in : g.S / spc;
-    const int64_t want = std::min<int64_t>(std::max<int64_t>(ceil_div(ctas, num_sms_dev()), 1), kSeqMaxPerSm);
+    int cap = kSeqMaxPerSm;   // PDSSM_SEQ_MAX_PER_SM: tuning experiments only
+    if (const char* e = getenv("PDSSM_SEQ_MAX_PER_SM")) cap = std::max(1, std::min(8, atoi(e)));
+    const int64_t want = std::min<int64_t>(std::max<int64_t>(ceil_div(ctas, num_sms_dev()), 1), cap);
     // the largest ring at the wanted occupancy; if even two slots do not fit there, fewer CTAs per SM
     // (down to one): occupancy degrades, applicability does not depend on the batch size
     for (int64_t per_sm = want; per_sm >= 1; --per_sm) {
