@@ -175,7 +175,7 @@ inline size_t ws_bytes_g(const Geo& g, int op) {
             return 2 * seq_act_bytes(g) + layer_w_bytes(g) + (sel > fwd ? sel : fwd);
         }
         case PDSSM_OP_SEGMENT: {
-            size_t fwd = plan_bytes(g) + chunk_state_bytes_g(g);
+            size_t fwd = plan_bytes(g) + chunk_state_bytes_g(g) + seq_plan_bytes(g);
             size_t bwd = 2 * cs_f_bytes(g) + (g.P > 0 ? seq_f_bytes(g) + readout_w_bytes(g) : 0);
             return fwd > bwd ? fwd : bwd;
         }
@@ -303,6 +303,23 @@ inline bool seqc_applicable(const Geo& g, std::initializer_list<const void*> ptr
            seq_ring(g, true, false, g.act, 1, g.tau, ctas, G) >= 2;
 }
 
+// the chunked single-CTA Phase A (k_fwd_seq MODE 1) for the sequence-parallel segment summary: chunks of
+// >= 128 steps (shorter ones keep the generic per-chunk kernel), 16-byte aligned rows, a ring that fits
+inline bool seqc_phaseA_ok(const Geo& g, std::initializer_list<const void*> ptrs) {
+    if (env_path_is("generic") || g.tau < 128 || !seq_shape_ok(g.N, g.K, g.tau, g.nc, g.act)) return false;
+    for (const void* p : ptrs)
+        if (misaligned(p, 16)) return false;
+    return seq_ring(g, false, true, g.act, 1, g.tau, g.S * g.C, seqc_group(g.N)) >= 2;
+}
+
+// its backward counterpart (k_bwd_seq MODE 1, beta'_c), adjoint rows of esz_e bytes
+inline bool seqc_phaseA_bwd_ok(const Geo& g, size_t esz_e, std::initializer_list<const void*> ptrs) {
+    if (env_path_is("generic") || g.tau < 128 || !seq_shape_ok(g.N, g.K, g.tau, g.nc, g.act)) return false;
+    for (const void* p : ptrs)
+        if (misaligned(p, 16)) return false;
+    return seq_ring(g, true, false, esz_e, 1, g.tau, g.S * g.C, seqc_group(g.N)) >= 2;
+}
+
 inline bool seq_applicable(const Geo& g, std::initializer_list<const void*> ptrs) {
     if (g.C != 1 || env_path_is("fused") || env_path_is("generic")) return false;
     if (!seq_shape_ok(g.N, g.K, g.L, g.nc, g.act)) return false;
@@ -325,8 +342,9 @@ inline pdssm_status seq_set_smem(const void* f, size_t bytes) {
 pdssm_status fwd_seq(const Geo& g, seq::SeqArgs& sa, uint8_t* rec, uint8_t* wm, uint8_t* ovf, cudaStream_t st);
 pdssm_status bwd_seq_run(const Geo& g, seq::SeqArgs& sa, bool e_f32, cudaStream_t st);
 // chunked single-CTA path (MODE 1 / phase B / MODE 2)
-pdssm_status fwd_seqc(const Geo& g, seq::SeqArgs& sa, uint8_t* rec, uint8_t* wm, uint8_t* ovf, cudaStream_t st);
-pdssm_status bwd_seqc_run(const Geo& g, seq::SeqArgs& sa, bool e_f32, cudaStream_t st);
+pdssm_status fwd_seqc(const Geo& g, seq::SeqArgs& sa, uint8_t* rec, uint8_t* wm, uint8_t* ovf, cudaStream_t st,
+                      bool phaseA_only = false);
+pdssm_status bwd_seqc_run(const Geo& g, seq::SeqArgs& sa, bool e_f32, cudaStream_t st, bool phaseA_only = false);
 // api_seq_bwd.cu: recompute-mode backward, one CTA per sequence (k_scan_rc.cuh)
 bool bwd_seq_rc_applicable(const Geo& g, std::initializer_list<const void*> ptrs);
 pdssm_status bwd_seq_rc_run(const Geo& g, seq::RcArgs& ra, bool e_f32, uint8_t* rec, uint8_t* wm, uint8_t* ovf,

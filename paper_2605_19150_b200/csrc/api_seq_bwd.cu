@@ -102,7 +102,7 @@ pdssm_status bwd_seq_rc_run(const Geo& g, seq::RcArgs& ra, bool e_f32, uint8_t* 
 // chunked single-CTA path: Phase A' (MODE 1: beta'_c) -> Phase B' (mu chain through the forward
 // aggregates: k_bwd_phaseB) -> Phase C' (MODE 2: replay from e + mu_c, emitting the gradients)
 template <typename TE>
-pdssm_status bwd_seqc(const Geo& g, seq::SeqArgs& sa, cudaStream_t st) {
+pdssm_status bwd_seqc(const Geo& g, seq::SeqArgs& sa, cudaStream_t st, bool phaseA_only) {
     const int64_t ctas = g.S * g.C;
     sa.G = seqc_group(g.N);
     sa.spc = 1;
@@ -128,7 +128,7 @@ pdssm_status bwd_seqc(const Geo& g, seq::SeqArgs& sa, cudaStream_t st) {
                 pdssm_status rr = seq_set_smem((const void*)kA, ly.bytes);
                 if (rr) return rr;
                 kA<<<(unsigned)ctas, (unsigned)g.N + 32, ly.bytes, st>>>(sa);
-                if ((rr = cuda_check("bwd_seqc_A"))) return rr;
+                if ((rr = cuda_check("bwd_seqc_A")) || phaseA_only) return rr;   // (sequence-parallel summary)
                 k_bwd_phaseB<NC><<<(unsigned)g.S, thr, (size_t)NC * g.N * 4, st>>>(sa.cs, sa.betap, sa.lam_in, sa.mu,
                                                                                      nullptr, (int)g.N, g.C);
                 if ((rr = cuda_check("bwd_seqc_B"))) return rr;
@@ -140,8 +140,8 @@ pdssm_status bwd_seqc(const Geo& g, seq::SeqArgs& sa, cudaStream_t st) {
     });
 }
 
-pdssm_status bwd_seqc_run(const Geo& g, seq::SeqArgs& sa, bool e_f32, cudaStream_t st) {
-    return e_f32 ? bwd_seqc<float>(g, sa, st) : bwd_seqc<void>(g, sa, st);
+pdssm_status bwd_seqc_run(const Geo& g, seq::SeqArgs& sa, bool e_f32, cudaStream_t st, bool phaseA_only) {
+    return e_f32 ? bwd_seqc<float>(g, sa, st, phaseA_only) : bwd_seqc<void>(g, sa, st, phaseA_only);
 }
 
 }  // namespace api

@@ -76,7 +76,8 @@ pdssm_status fwd_seq(const Geo& g, seq::SeqArgs& sa, uint8_t* rec, uint8_t* wm, 
 
 // chunked single-CTA path: Phase A (MODE 1, every chunk's aggregate) -> Phase B (carries and, under
 // EXPORT_MAPS, the exclusive prefix maps: k_fwd_phaseB) -> Phase C (MODE 2, replay storing h)
-pdssm_status fwd_seqc(const Geo& g, seq::SeqArgs& sa, uint8_t* rec, uint8_t* wm, uint8_t* ovf, cudaStream_t st) {
+pdssm_status fwd_seqc(const Geo& g, seq::SeqArgs& sa, uint8_t* rec, uint8_t* wm, uint8_t* ovf, cudaStream_t st,
+                      bool phaseA_only) {
     seq::k_build_seq_plan<<<(unsigned)(g.H * g.K), (unsigned)g.N, (size_t)g.N * 2, st>>>(
         sa.dict_idx, rec, wm, ovf, const_cast<uint16_t*>(sa.pstart), const_cast<uint16_t*>(sa.psrc), (int)g.N, g.flags);
     pdssm_status r = cuda_check("build_seq_plan");
@@ -109,7 +110,7 @@ pdssm_status fwd_seqc(const Geo& g, seq::SeqArgs& sa, uint8_t* rec, uint8_t* wm,
                           : g.N == 64 ? seq::k_fwd_seq<T, NC, PD, false, false, 64, 1, kSeqcG64, false, 2>
                                       : seq::k_fwd_seq<T, NC, PD, false, false, 0, 1, kSeqcG128, false, 2>;
                 pdssm_status rr = launch(kA, true, "fwd_seqc_A");
-                if (rr) return rr;
+                if (rr || phaseA_only) return rr;   // (the sequence-parallel summary needs the aggregates only)
                 k_fwd_phaseB<NC><<<(unsigned)g.S, thr, (size_t)NC * g.N * 4 + (size_t)g.N * 2 + 16, st>>>(
                     sa.cs, sa.h0, sa.maps, nullptr, (int)g.N, g.C);
                 if ((rr = cuda_check("fwd_seqc_B"))) return rr;

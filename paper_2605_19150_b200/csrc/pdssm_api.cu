@@ -478,15 +478,40 @@ pdssm_status pdssm_segment_summary(const uint8_t* kstar, const uint16_t* dict_id
     uint16_t* pstart = bump.take<uint16_t>((size_t)g.H * g.K * (g.N + 1) * 2);
     uint16_t* psrc = bump.take<uint16_t>((size_t)g.H * g.K * g.N * 2);
     void* csmem = bump.take<char>(chunk_state_bytes_g(g));
-    ChunkStateView cs = cs_view(g, csmem);
-    if ((r = launch_plan(g, dict_idx, pstart, psrc, st))) return r;
-    if ((r = fwd_three_phase(g, kstar, dict_idx, pstart, psrc, diag, bias, nullptr, cs, nullptr, nullptr, false, st)))
-        return r;
+    uint8_t* srec = bump.take<uint8_t>(seq_rec_bytes(g));
+    uint8_t* swm = bump.take<uint8_t>(seq_wm_bytes(g));
+    uint8_t* sovf = bump.take<uint8_t>(seq_ovf_bytes(g));
+    // The summary is the fold of chunk aggregates, whatever the chunking (Alg. 1's composition is
+    // associative): chunks shorter than 128 steps are merged to 128 here so that the
+    // chunked single-CTA kernel takes them (fewer chunks: the caller's chunk_state-sized workspace fits)
+    Geo gs = g;
+    if (gs.tau < 128 && gs.L > gs.tau) {
+        gs.tau = (int)std::min<int64_t>(128, gs.L);
+        gs.C = (int)ceil_div(gs.L, gs.tau);
+    }
+    if (!seqc_phaseA_ok(gs, {g.diag_mode == PDSSM_DIAG_PER_STEP ? diag : nullptr, bias})) gs = g;
+    ChunkStateView cs = cs_view(gs, csmem);
+    if (seqc_phaseA_ok(gs, {g.diag_mode == PDSSM_DIAG_PER_STEP ? diag : nullptr, bias})) {
+        // the chunk aggregates by the chunked single-CTA kernel (Phase A only; its plan launch also
+        // writes the CSR lists): one read of the segment at the single-chunk kernels' step rate
+        seq::SeqArgs sa{};
+        sa.kstar = kstar; sa.dict_idx = dict_idx; sa.rec = srec; sa.wm = swm; sa.ovf = sovf; sa.pstart = pstart;
+        sa.psrc = psrc;
+        sa.diag = g.diag_mode == PDSSM_DIAG_PER_STEP ? diag : nullptr;
+        sa.diag_dict = g.diag_mode == PDSSM_DIAG_PER_DICT ? static_cast<const float*>(diag) : nullptr;
+        sa.bias = bias; sa.h0 = nullptr; sa.cs = cs; sa.maps = nullptr; sa.out0 = nullptr;
+        sa.H = (int)g.H; sa.L = (int)g.L; sa.N = (int)g.N; sa.K = (int)g.K; sa.flags = g.flags;
+        if ((r = fwd_seqc(gs, sa, srec, swm, sovf, st, true))) return r;
+    } else {
+        if ((r = launch_plan(g, dict_idx, pstart, psrc, st))) return r;
+        if ((r = fwd_three_phase(g, kstar, dict_idx, pstart, psrc, diag, bias, nullptr, cs, nullptr, nullptr, false, st)))
+            return r;
+    }
     SummaryView sv{static_cast<char*>(summary_out), summary_block_bytes(g), npad8(g.N)};
     return with_nc(g.nc, [&](auto ncv) {
         constexpr int NC = decltype(ncv)::value;
         k_fold_aggregates<NC><<<(unsigned)g.S, threads_for(g.N), (size_t)NC * g.N * 4 + g.N * 2 + 16, st>>>(
-            cs, sv, (int)g.N, g.C);
+            cs, sv, (int)g.N, gs.C);
         return cuda_check("fold_aggregates");
     });
 }
@@ -546,9 +571,19 @@ pdssm_status pdssm_segment_summary_bwd(const uint8_t* kstar, const uint16_t* dic
                     const TE* e = nullptr;
                     if (std::is_same<TE, float>::value && dy_opt) e = reinterpret_cast<const TE*>(ebuf);
                     else if (dh_opt) e = reinterpret_cast<const TE*>(dh_opt);
-                    k_bwd_phaseA<T, TE, NC, PD><<<items, thr, (size_t)2 * NC * g.N * 4, st>>>(
-                        kstar, dict_idx, dg, dd, e, betap, (int)g.H, (int)g.L, (int)g.N, (int)g.K, g.tau, g.C);
-                    pdssm_status rr = cuda_check("bwd_phaseA");
+                    pdssm_status rr;
+                    if (seqc_phaseA_bwd_ok(g, sizeof(TE), {dg, e})) {
+                        // beta'_c of every chunk by the chunked single-CTA kernel (Phase A' only)
+                        seq::SeqArgs sa{};
+                        sa.kstar = kstar; sa.dict_idx = dict_idx; sa.diag = dg; sa.diag_dict = dd; sa.bias = e;
+                        sa.cs = cs; sa.betap = betap; sa.mu = mu;
+                        sa.H = (int)g.H; sa.L = (int)g.L; sa.N = (int)g.N; sa.K = (int)g.K; sa.flags = g.flags;
+                        rr = bwd_seqc_run(g, sa, std::is_same<TE, float>::value && !std::is_same<T, float>::value, st, true);
+                    } else {
+                        k_bwd_phaseA<T, TE, NC, PD><<<items, thr, (size_t)2 * NC * g.N * 4, st>>>(
+                            kstar, dict_idx, dg, dd, e, betap, (int)g.H, (int)g.L, (int)g.N, (int)g.K, g.tau, g.C);
+                        rr = cuda_check("bwd_phaseA");
+                    }
                     if (rr) return rr;
                     k_bwd_phaseB<NC><<<(unsigned)g.S, thr, (size_t)NC * g.N * 4, st>>>(cs, betap, nullptr, mu,
                                                                                          beta_out, (int)g.N, g.C);

@@ -26,9 +26,12 @@ def path(request, monkeypatch):
     return request.param
 
 
-@pytest.mark.parametrize("G,c", [(2, 2), (4, 1), (3, 2)])
-def test_sp_virtual_ranks(P, G, c, path):
-    B, H, L, N, K, tau = 2, 2, 301, 32, 8, 32
+# (N, tau, L): short chunks (generic per-chunk summaries) and chunks of >= 128 steps at N = 64 / 128,
+# whose summaries take the chunked single-CTA Phase A / A' kernels (pdssm_segment_summary(_bwd))
+@pytest.mark.parametrize("G,c,N,tau,L", [(2, 2, 32, 32, 301), (4, 1, 32, 32, 301), (3, 2, 32, 32, 301),
+                                         (3, 1, 64, 128, 1000), (2, 2, 128, 256, 1100), (4, 1, 128, 128, 900)])
+def test_sp_virtual_ranks(P, G, c, N, tau, L, path):
+    B, H, K = 2, 2, 8
     inp = synth.scan_inputs(B, H, L, N, K, c, seed=40 + G, h0=True, dh=True)
     dev = {k: torch.from_numpy(v).cuda() for k, v in inp.items()}
     di = dev["dict_idx"].to(torch.int16)
