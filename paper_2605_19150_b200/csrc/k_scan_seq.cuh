@@ -341,6 +341,12 @@ __device__ __forceinline__ void st_stream(T* p, float v, uint64_t pol) {
 // forward: h_{t-1} is stored at step t right after the gather loads are issued (off the chain)
 // instead of right after it is computed
 constexpr bool SEQ_DEFER_STORE = PDSSM_SEQ_DEFER_STORE != 0;
+#ifndef PDSSM_SEQ_EARLY_ADDR
+#define PDSSM_SEQ_EARLY_ADDR 0
+#endif
+// forward (no maps, no tiers): the gather addresses of step t+1 are computed during step t, from a
+// record loaded a step earlier, instead of between h_t and the store of v_{t+1} (on the chain)
+constexpr bool SEQ_EARLY_ADDR = PDSSM_SEQ_EARLY_ADDR != 0;
 constexpr int SEQ_G = 16;    // backward: steps per ring slot (one TMA group)
 constexpr int SEQ_GF = 32;   // forward: steps per ring slot
 
@@ -488,6 +494,26 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
     rc = rec[(size_t)k * N + il];
     m = wm[k * NW + w];
     load_ops(sb, k);
+    // (on by default at N = 64 only: measured config 5 forward 0.469 -> 0.447 ms, config 2 (N = 128)
+    // 0.175 -> 0.181 ms)
+    constexpr bool EARLY = (SEQ_EARLY_ADDR || NN == 64) && !AGG && !TIER;
+    uint32_t gan[CAP];   // EARLY: this step's gather addresses (computed during the previous step)
+    uint2 rcn = rc;      // EARLY: the record of the next step
+    auto addr8 = [&](uint2 rc_, char* vb_, uint32_t (&a_)[CAP]) {
+        uint32_t lo[4], hi4[4];
+        const uint32_t vb_s = fused::smem_u32(vb_);
+        gather_addr4(rc_.x, vb_s, SVB, lo);
+        gather_addr4(rc_.y, vb_s, SVB, hi4);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            a_[q] = lo[q];
+            a_[4 + q] = hi4[q];
+        }
+    };
+    if constexpr (EARLY) {
+        addr8(rc, xbc, gan);              // step 0 (parity 0)
+        rcn = rec[(size_t)k1 * N + il];   // step 1
+    }
     auto step = [&](const int r, const int g, const int t, auto ovfv) {
         constexpr bool OVF = decltype(ovfv)::value;
         char* vbc = xbc + (t & 1) * XB;
@@ -496,7 +522,10 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
 #pragma unroll
         for (int q = 0; q < CAP; ++q) off[q] = __byte_perm(q < 4 ? rc.x : rc.y, 0u, 0x4440u + (uint32_t)(q & 3)) * SVB;
         uint32_t ga[CAP];   // shared addresses of this step's gather, computed before the barrier
-        {
+        if constexpr (EARLY) {
+#pragma unroll
+            for (int q = 0; q < CAP; ++q) ga[q] = gan[q];
+        } else {
             uint32_t lo[4], hi4[4] = {0u, 0u, 0u, 0u};
             const uint32_t vb_s = fused::smem_u32(vbc);
             gather_addr4(rc.x, vb_s, SVB, lo);
@@ -561,7 +590,7 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
         // operands of step t+1 (consumed a step later)
         if (r < G - 1) {
             k = k1;
-            rc = rec[(size_t)k * N + il];
+            if constexpr (!EARLY) rc = rec[(size_t)k * N + il];
             m = wm[k * NW + w];
             load_ops(sb + (r + 1) * ROWB, k);
         } else if (g + 1 < ngroups) {
@@ -572,11 +601,16 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
             sb = ring + (size_t)slot * Ly.slot + SUBOFF;
             fused::mbar_wait(bars + slot, ph);
             k = k1;
-            rc = rec[(size_t)k * N + il];
+            if constexpr (!EARLY) rc = rec[(size_t)k * N + il];
             m = wm[k * NW + w];
             load_ops(sb, k);
         }
+        if constexpr (EARLY) {   // addresses of step t+1 from its record (loaded a step ago); record of t+2
+            addr8(rcn, xbc + ((t + 1) & 1) * XB, gan);
+            rc = rcn;
+        }
         k1 = kb[t + 2];
+        if constexpr (EARLY) rcn = rec[(size_t)k1 * N + il];
         // pairwise sum of the 8 slots (sources past the in-degree read the zero slot)
         auto sum8 = [&](const SV (&x)[CAP], float& sr, float& si) {
             if constexpr (NC == 2) {   // packed: same pairwise order, FADD2
