@@ -341,6 +341,10 @@ __device__ __forceinline__ void st_stream(T* p, float v, uint64_t pol) {
 // forward: h_{t-1} is stored at step t right after the gather loads are issued (off the chain)
 // instead of right after it is computed
 constexpr bool SEQ_DEFER_STORE = PDSSM_SEQ_DEFER_STORE != 0;
+#ifndef PDSSM_SEQ_BWD_EARLY_STS
+#define PDSSM_SEQ_BWD_EARLY_STS 0
+#endif
+constexpr bool SEQ_BWD_EARLY_STS = PDSSM_SEQ_BWD_EARLY_STS != 0;
 #ifndef PDSSM_SEQ_EARLY_ADDR
 #define PDSSM_SEQ_EARLY_ADDR 0
 #endif
@@ -766,6 +770,9 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq(SeqArgs a) {
     constexpr int SVB = (int)sizeof(SV);
     constexpr bool CHUNK = MODE != 0;
     constexpr bool EMIT = MODE != 1;   // db, dD, g stored (and h rows read)
+    // early exchange store of lambda (below): on for the whole-sequence kernel (config 2 bf16 backward
+    // 0.191 -> 0.182 ms, config 4 0.668 -> 0.629 ms), off in the chunk modes (config 5 measured slower)
+    constexpr bool BES = SEQ_BWD_EARLY_STS || MODE == 0;
     static_assert(!CHUNK || SPC == 1, "chunk modes: one sequence per CTA");
     extern __shared__ __align__(128) uint8_t smem[];
     const int C = CHUNK ? a.C : 1;
@@ -901,16 +908,22 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq(SeqArgs a) {
         load_row(sb, L - 1 - t_lo0, L - 1, kb[L - 1]);
     }
     int km1 = L > 1 ? kb[L - 2] : 0;   // k* of step t-1
+    // BWD_EARLY_STS: lambda_{t-1} goes to its exchange row as soon as it is computed (step t, after
+    // that step's barrier: every thread is done reading that buffer, last read at step t+1), and
+    // db_{t-1} = lambda_{t-1} is stored at step t-1 while its gather load is in flight -- the stores of
+    // db / dD no longer sit between lambda_{t-1} and its exchange store
+    if constexpr (BES)   // lambda_{L-1}
+        *reinterpret_cast<SV*>(xbc + ((L - 1) & 1) * (N * SVB) + j * SVB) = fused::mk<NC>(lr, li);
     auto step = [&](const int rr, const int g, const int t, const int t_lo, const bool inner) {
         // inner: full group with t_lo > 0 -> rows of step t-1 are compile-time, t-1 > 0
         const int v = L - 1 - t;
-        if constexpr (EMIT) {
+        if constexpr (EMIT && !BES) {
             st_stream<T>(dbp, lr, pol);                       // db_t = lambda_t
             if constexpr (NC == 2) st_stream<T>(dbp + N, li, pol);
             dbp -= row;
         }
         char* lbc = xbc + (t & 1) * (N * SVB);
-        *reinterpret_cast<SV*>(lbc + j * SVB) = fused::mk<NC>(lr, li);
+        if constexpr (!BES) *reinterpret_cast<SV*>(lbc + j * SVB) = fused::mk<NC>(lr, li);
         const float Dcr = Dr, Dci = Di, ecr = er, eci = ei, hcr = hr, hci = hi;
         uint32_t la;   // shared address of lambda_t[P_t[j]], computed before the barrier
         asm volatile("mad.lo.u32 %0, %1, %2, %3;" : "=r"(la) : "r"(p), "r"(SVB), "r"(fused::smem_u32(lbc)));
@@ -920,6 +933,11 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq(SeqArgs a) {
             float re, im;
             lds_sv<NC>(la, re, im);
             lpv = fused::mk<NC>(re, im);
+        }
+        if constexpr (EMIT && BES) {   // db_t = lambda_t, off the chain
+            st_stream<T>(dbp, lr, pol);
+            if constexpr (NC == 2) st_stream<T>(dbp + N, li, pol);
+            dbp -= row;
         }
         if (rr == 0 && jt == 0 && g >= 1) {   // every compute thread is done with the previous group's slot
             mbar_arrive(bars + R + (slot == 0 ? R - 1 : slot - 1));
@@ -978,6 +996,8 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_bwd_seq(SeqArgs a) {
             lr = ecr + Dcr * pr;
             li = 0.f;
         }
+        if constexpr (BES)
+            if (t > 0) *reinterpret_cast<SV*>(xbc + ((t - 1) & 1) * (N * SVB) + j * SVB) = fused::mk<NC>(lr, li);
         if constexpr (EMIT) {
             const float ddr = NC == 2 ? hcr * pr + hci * pm : hcr * pr;   // dD_t = conj(h_{t-1}) lp
             const float ddi = NC == 2 ? hcr * pm - hci * pr : 0.f;
