@@ -1,6 +1,6 @@
 #!/bin/bash
 mkdir -p gpurun_out
-PDSSM_READOUT_WIDE=1 timeout 600 ncu --set full --clock-control none --import-source on -k "regex:k_gemm_tc" -s 3 -c 1 \
+timeout 600 ncu --set full --clock-control none --import-source on -k "regex:k_gemm_tc" -s 3 -c 1 \
   -o gpurun_out/rd_full python tools/time_readout.py f32 > /dev/null 2>&1
 echo "ncu $?"
 python tools/ncu_summary.py gpurun_out/rd_full.ncu-rep k_gemm_tc > gpurun_out/rd_summary.txt 2>&1
