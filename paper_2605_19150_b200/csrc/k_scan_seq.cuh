@@ -352,7 +352,10 @@ constexpr bool SEQ_BWD_EARLY_STS = PDSSM_SEQ_BWD_EARLY_STS != 0;
 // record loaded a step earlier, instead of between h_t and the store of v_{t+1} (on the chain)
 constexpr bool SEQ_EARLY_ADDR = PDSSM_SEQ_EARLY_ADDR != 0;
 constexpr int SEQ_G = 16;    // backward: steps per ring slot (one TMA group)
-constexpr int SEQ_GF = 32;   // forward: steps per ring slot
+#ifndef PDSSM_SEQ_GF
+#define PDSSM_SEQ_GF 32
+#endif
+constexpr int SEQ_GF = PDSSM_SEQ_GF;   // forward: steps per ring slot
 
 // ============================================================================ forward
 // Step t (r = t mod 8 is compile-time inside a full group, so ring rows, the exchange
