@@ -345,6 +345,10 @@ constexpr bool SEQ_DEFER_STORE = PDSSM_SEQ_DEFER_STORE != 0;
 #define PDSSM_SEQ_BWD_EARLY_STS 0
 #endif
 constexpr bool SEQ_BWD_EARLY_STS = PDSSM_SEQ_BWD_EARLY_STS != 0;
+#ifndef PDSSM_SEQ_SKEW
+#define PDSSM_SEQ_SKEW 1   // measured: config 2 forward 0.175 -> 0.172 ms (fp32), 0.188 -> 0.179 ms (bf16)
+#endif
+constexpr bool SEQ_SKEW = PDSSM_SEQ_SKEW != 0;
 #ifndef PDSSM_SEQ_EARLY_ADDR
 #define PDSSM_SEQ_EARLY_ADDR 0
 #endif
@@ -638,8 +642,33 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
             }
         };
         float ar, ai, cr = 0.f, ci = 0.f;
+        // SKEW (8 slots, no maps): the later-arriving slots enter last and b_t early --
+        // (((v0+v1)+(v2+v3)) + (v4+v5)) + b, then + (v6+v7): two adds after the last gather load instead
+        // of four (a fixed order too; not the balanced tree of the other variants)
+        // (complex only: real scans measured slower with it -- config 4 0.641 -> 0.707 ms, config 5 +1%)
+        constexpr bool SKEW = SEQ_SKEW && NC == 2 && GCAP == 8 && !AGG;
+        bool with_b = false;
 #if !defined(FWD_EXP_SLOTS)
-        if (tier4) {
+        if constexpr (SKEW) {
+            if (!tier4) {
+                if constexpr (NC == 2) {
+                    float2 t = add2(add2(add2(v[0], v[1]), add2(v[2], v[3])), add2(v[4], v[5]));
+                    t = add2(add2(t, make_float2(bcr, bci)), add2(v[6], v[7]));
+                    ar = t.x;
+                    ai = t.y;
+                } else {
+                    const float t = (((fused::re_of<NC>(v[0]) + fused::re_of<NC>(v[1])) +
+                                      (fused::re_of<NC>(v[2]) + fused::re_of<NC>(v[3]))) +
+                                     (fused::re_of<NC>(v[4]) + fused::re_of<NC>(v[5]))) + bcr;
+                    ar = t + (fused::re_of<NC>(v[6]) + fused::re_of<NC>(v[7]));
+                    ai = 0.f;
+                }
+                with_b = true;
+            } else {
+                ar = (fused::re_of<NC>(v[0]) + fused::re_of<NC>(v[1])) + (fused::re_of<NC>(v[2]) + fused::re_of<NC>(v[3]));
+                ai = (fused::im_of<NC>(v[0]) + fused::im_of<NC>(v[1])) + (fused::im_of<NC>(v[2]) + fused::im_of<NC>(v[3]));
+            }
+        } else if (tier4) {
             ar = (fused::re_of<NC>(v[0]) + fused::re_of<NC>(v[1])) + (fused::re_of<NC>(v[2]) + fused::re_of<NC>(v[3]));
             ai = (fused::im_of<NC>(v[0]) + fused::im_of<NC>(v[1])) + (fused::im_of<NC>(v[2]) + fused::im_of<NC>(v[3]));
         } else {
@@ -655,6 +684,7 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
         }
         if (OVF && mc == WM_OVF) {   // preimage longer than CAP: CSR plan (rare, warp-uniform)
             ar = ai = cr = ci = 0.f;
+            with_b = false;
             const SV* vb = reinterpret_cast<const SV*>(vbc);
             const SV* vb2 = reinterpret_cast<const SV*>(vbc2);
             const size_t e = (size_t)h * K + kc;
@@ -670,11 +700,11 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
             }
         }
         if constexpr (NC == 2) {
-            const float2 hv = add2(make_float2(ar, ai), make_float2(bcr, bci));
+            const float2 hv = with_b ? make_float2(ar, ai) : add2(make_float2(ar, ai), make_float2(bcr, bci));
             hr = hv.x;
             hi = hv.y;
         } else {
-            hr = ar + bcr;
+            hr = with_b ? ar : ar + bcr;
             hi = 0.f;
         }
         if constexpr (MODE != 1 && !SEQ_DEFER_STORE) {
