@@ -651,18 +651,10 @@ __global__ void __launch_bounds__(MAXN + 32, 1) k_fwd_seq(SeqArgs a) {
 #if !defined(FWD_EXP_SLOTS)
         if constexpr (SKEW) {
             if (!tier4) {
-                if constexpr (NC == 2) {
-                    float2 t = add2(add2(add2(v[0], v[1]), add2(v[2], v[3])), add2(v[4], v[5]));
-                    t = add2(add2(t, make_float2(bcr, bci)), add2(v[6], v[7]));
-                    ar = t.x;
-                    ai = t.y;
-                } else {
-                    const float t = (((fused::re_of<NC>(v[0]) + fused::re_of<NC>(v[1])) +
-                                      (fused::re_of<NC>(v[2]) + fused::re_of<NC>(v[3]))) +
-                                     (fused::re_of<NC>(v[4]) + fused::re_of<NC>(v[5]))) + bcr;
-                    ar = t + (fused::re_of<NC>(v[6]) + fused::re_of<NC>(v[7]));
-                    ai = 0.f;
-                }
+                float2 t = add2(add2(add2(v[0], v[1]), add2(v[2], v[3])), add2(v[4], v[5]));
+                t = add2(add2(t, make_float2(bcr, bci)), add2(v[6], v[7]));
+                ar = t.x;
+                ai = t.y;
                 with_b = true;
             } else {
                 ar = (fused::re_of<NC>(v[0]) + fused::re_of<NC>(v[1])) + (fused::re_of<NC>(v[2]) + fused::re_of<NC>(v[3]));
