@@ -59,7 +59,10 @@ def test_mixer_function_surrogate_gradients(blk):
 
 def test_parity_training_reduces_loss(blk):
     from paper_2605_19150_b200 import train_fsa
-    r = train_fsa.train_task("parity", steps=300, batch=64, max_len=16, seed=0)
+    # lr 5e-4: the recipe of DESIGN.md §13 (the parity sweep, profiles/r02_train_parity_sweep.jsonl: at the
+    # paper's 2e-3 a short run can stay near chance depending on the last bits of the arithmetic;
+    # tools/probe_train.py: 5e-4 reaches < 1e-3 in 300 steps for seeds 0-2)
+    r = train_fsa.train_task("parity", steps=300, batch=64, max_len=16, seed=0, lr=5e-4)
     assert np.isfinite(r["final_train_loss"])
     assert r["final_train_loss"] < 0.6          # chance level is ln 2 = 0.693
     assert set(r["val_acc_by_len"]) == set(train_fsa.EVAL_LENGTHS)
